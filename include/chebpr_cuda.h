@@ -1,0 +1,219 @@
+/*
+ * chebpr_cuda.h — C-ABI of the B200-native CPAA hot path (libchebpr_b200.so).
+ *
+ * Drop-in boundary for the reference's C++ API in /root/reference/proj/include/chebpr/
+ * (every entry point below cites the reference interface it replaces).  Plain
+ * pointers and sizes only; no exceptions cross this boundary: every call returns a
+ * cheb_status and, on failure, cheb_last_error() holds the reference's message text
+ * (e.g. "vertex 2 is isolated (degree 0)", "non-finite value at round 3").  The C++
+ * wrapper (include/chebpr/*.hpp) re-throws them as the reference's exception types
+ * (/root/reference/proj/include/chebpr/errors.hpp:11-33).
+ *
+ * Ownership: host buffers are caller-owned and copied synchronously.  Device memory,
+ * streams and CUDA graphs are owned by the graph handle.  Calls on one handle are
+ * serialised by the caller (one solve at a time); distinct handles are
+ * independent.
+ */
+#ifndef CHEBPR_CUDA_H
+#define CHEBPR_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes <-> reference exception taxonomy (errors.hpp:11-33). */
+typedef enum {
+    CHEB_OK = 0,
+    CHEB_VALIDATION = 1,  /* chebpr::ValidationError */
+    CHEB_DOMAIN = 2,      /* chebpr::DomainError */
+    CHEB_NUMERIC = 3,     /* chebpr::NumericError */
+    CHEB_INVALID_ARG = 4, /* std::invalid_argument */
+    CHEB_CAPACITY = 5,    /* chebpr::CapacityError */
+    CHEB_CUDA = 6,        /* CUDA runtime failure (new) */
+    CHEB_NCCL = 7,        /* NCCL failure (new) */
+    CHEB_PARSE = 8        /* chebpr::ParseError */
+} cheb_status;
+
+/* Thread-local text of the last failure on this thread. */
+const char* cheb_last_error(void);
+/* Library version string and the CUDA device count visible to it. */
+const char* cheb_version(void);
+int cheb_device_count(void);
+
+/* ---- coefficient kit: coefficients.hpp:31-51 (host code, bit-identical) ---- */
+cheb_status cheb_beta(double c, double* out);                               /* :31 */
+cheb_status cheb_sigma(double c, double* out);                              /* :37 */
+cheb_status cheb_err_bound(double c, int M, double* out);                   /* :40 */
+cheb_status cheb_plan_iterations(double c, double eps, int* M, double* predicted_err); /* :43 */
+cheb_status cheb_coefficients(double c, int M, double* coeffs /* M+1 */, double* beta,
+                              double* c0);                                  /* :46 */
+/* cpaa.cpp:28-36 resolve_rounds: exactly one of rounds>=0 / eps>0; clamp to max_rounds. */
+cheb_status cheb_resolve_rounds(double c, int rounds, double eps, int max_rounds, int* M);
+
+/* ---- graph handle: graph.hpp:21-31 UndirectedGraph, device-resident ---- */
+typedef struct cheb_graph* cheb_graph_t;
+
+typedef struct {
+    int dedup;          /* BuildOptions::dedup (graph.hpp:45), default 1 */
+    int drop_isolated;  /* BuildOptions::drop_isolated (graph.hpp:46), default 0 */
+    int64_t n_hint;     /* BuildOptions::n_hint (graph.hpp:47), default 0 */
+    int device;         /* CUDA ordinal (new) */
+    int row_ptr_64;     /* 1: int64 row pointers (config 4); 0: int32 when nnz < 2^31 (new) */
+} cheb_build_opts;
+
+typedef struct {
+    int64_t n;                  /* UndirectedGraph::n */
+    int64_t m;                  /* UndirectedGraph::m (self-loops once) */
+    int64_t nnz;                /* neighbors.size() = 2m - self_loops */
+    int64_t duplicates_removed; /* BuildResult::duplicates_removed (graph.hpp:52) */
+    int64_t isolated_dropped;   /* BuildResult::isolated_dropped (graph.hpp:53) */
+    int64_t max_degree;
+    int64_t min_degree;
+    int multi;                  /* UndirectedGraph::multi */
+    int row_ptr_64;
+    int inv_degree_array;       /* 1 if a non-canonical inv_degree was uploaded */
+    int device;
+} cheb_graph_info;
+
+void cheb_build_opts_default(cheb_build_opts* o);
+
+/* K1 device CSR builder.  Replaces build_graph (graph.hpp:60-61, graph.cpp:23-102):
+ * same n rule, canonical (min,max) dedup, self-loop counted once, isolated-vertex
+ * error / order-preserving drop, rows sorted ascending — bit-exact arrays.
+ * edges: E pairs interleaved (a0,b0,a1,b1,...) in HOST memory. */
+cheb_status cheb_graph_build(const int64_t* edges, int64_t E, const cheb_build_opts* opts,
+                             cheb_graph_t* out, cheb_graph_info* info);
+/* Same, from DEVICE-resident int64 (or int32 when edge_bits==32) pairs on opts->device. */
+cheb_status cheb_graph_build_device(const void* d_edges, int64_t E, int edge_bits,
+                                    const cheb_build_opts* opts, cheb_graph_t* out,
+                                    cheb_graph_info* info);
+
+/* Upload a host CSR (UndirectedGraph arrays).  essential_check semantics of
+ * cpaa.cpp:16-26 (n>=1, consistent sizes, every degree>=1).  inv_degree may be NULL;
+ * when given it is compared bitwise with 1.0/deg: if canonical the kernels use an
+ * in-register reciprocal (no array traffic), else the array is uploaded and used
+ * (the reference reads it, cpaa.cpp:107 — e.g. the poisoned test, test_cpaa.cpp:371). */
+cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
+                                  const int64_t* neighbors, int64_t nnz, const int64_t* degrees,
+                                  int64_t n_degrees, const double* inv_degree, int64_t n_inv,
+                                  int64_t n, int64_t m, int multi, int device, int row_ptr_64,
+                                  cheb_graph_t* out);
+
+/* Bit-exact readback of the CSR (offsets[n+1], neighbors[nnz], degrees[n]; any may be NULL). */
+cheb_status cheb_graph_download_csr(cheb_graph_t g, int64_t* offsets, int64_t* neighbors,
+                                    int64_t* degrees);
+cheb_status cheb_graph_get_info(cheb_graph_t g, cheb_graph_info* info);
+void cheb_graph_free(cheb_graph_t g);
+
+/* cpaa.cpp:40-68 partition_vertices: degree-prefix cuts (host rule, used for the
+ * multi-GPU row partition).  cuts has K+1 entries. */
+cheb_status cheb_partition_vertices(const int64_t* degrees, int64_t n, int K, int64_t* cuts);
+
+/* ---- solvers ---- */
+enum { CHEB_MODE_FAST = 0, CHEB_MODE_BITEXACT = 1 };
+enum { CHEB_FP64 = 64, CHEB_FP32 = 32 };
+
+typedef struct {
+    double c;                    /* SolverConfig::c (cpaa.hpp:28) */
+    int rounds;                  /* SolverConfig::rounds (cpaa.hpp:32), -1 = unset */
+    double eps;                  /* SolverConfig::eps (cpaa.hpp:33), -1 = unset */
+    int max_rounds;              /* SolverConfig::max_rounds (cpaa.hpp:34), default 60 */
+    int parallelism;             /* SolverConfig::parallelism (cpaa.hpp:35): accepted, no effect
+                                    on results (bit-identical for every K, as the reference) */
+    int mode;                    /* CHEB_MODE_FAST (degree-binned, within 1e-12) or
+                                    CHEB_MODE_BITEXACT (storage-order sums, bitwise = reference) */
+    int precision;               /* CHEB_FP64 or CHEB_FP32 (new) */
+    int R;                       /* number of right-hand sides (new; 1 = reference) */
+    const double* personalization; /* n*R row-major host array or NULL = ones (new) */
+    int trace;                   /* fill trace rows (default 1) */
+} cheb_cpaa_opts;
+
+/* One TraceRow (cpaa.hpp:38-49). */
+typedef struct {
+    int k;
+    double c_k, S_k, residual_mass, l1_change, elapsed_ms, mass_T, err, err_l1;
+} cheb_trace_row;
+
+void cheb_cpaa_opts_default(cheb_cpaa_opts* o);
+
+/* run_cpaa (cpaa.hpp:74-75, cpaa.cpp:79-165).  ranks: n*R host doubles (row-major).
+ * trace: rounds rows (may be NULL; rounds <= max_rounds).  reference: optional vector of
+ * n_reference entries (err/err_l1 columns, cpaa.cpp:149-154; length checked as cpaa.cpp:84-85).
+ * rounds_out/total_mass_out may be NULL. */
+cheb_status cheb_cpaa(cheb_graph_t g, const cheb_cpaa_opts* opts, const double* reference,
+                      int64_t n_reference, double* ranks, cheb_trace_row* trace,
+                      int* rounds_out, double* total_mass_out);
+
+/* Device-resident variant for benchmarks: leaves ranks in the handle's device buffer
+ * (returned via *d_ranks, n*R values of the solve precision), no host copies, enqueued on
+ * the handle's stream.  Synchronises before returning iff sync != 0. */
+cheb_status cheb_cpaa_device(cheb_graph_t g, const cheb_cpaa_opts* opts, const void** d_ranks,
+                             int sync);
+/* Device time (ms) of the last cheb_cpaa_device term loop, measured with CUDA events on the
+ * handle's stream: loop_ms covers init+M terms+normalise, term_ms is loop_ms's per-term share
+ * excluding init/normalise when measurable. */
+cheb_status cheb_last_timing(cheb_graph_t g, double* loop_ms, double* term_kernel_ms,
+                             int* terms, int* launches);
+
+/* Per-term kernel durations (ms) of one solve, CUDA events around every fused term launch
+ * on the handle's stream (plain launches, no graph).  Used for the roofline figure. */
+cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double* term_ms,
+                              int capacity, int* terms);
+
+/* run_power (power.hpp:24-25, power.cpp:28-109). */
+typedef struct {
+    double c;       /* PowerConfig::c */
+    int rounds;     /* PowerConfig::rounds, -1 = unset */
+    double tol;     /* PowerConfig::tol, -1 = unset */
+    int max_rounds; /* PowerConfig::max_rounds (60) */
+    int parallelism;
+    int mode;       /* CHEB_MODE_FAST / CHEB_MODE_BITEXACT */
+} cheb_power_opts;
+void cheb_power_opts_default(cheb_power_opts* o);
+cheb_status cheb_power(cheb_graph_t g, const cheb_power_opts* opts, const double* reference,
+                       int64_t n_reference, double* ranks, cheb_trace_row* trace,
+                       int trace_capacity, int* rounds_out, double* total_mass_out);
+
+/* transition_apply (graph.hpp:64, graph.cpp:104-121): y = P x. */
+cheb_status cheb_transition_apply(cheb_graph_t g, const double* x, int64_t nx, double* y,
+                                  int mode);
+
+/* Staged API (cpaa.hpp:79-85, cpaa.cpp:167-196), device-backed with the SAME arithmetic as
+ * cheb_cpaa in the given mode, so staged and fused results are bitwise equal
+ * (test_cpaa.cpp:157-173).  The state lives on the device inside the handle. */
+cheb_status cheb_state_init(cheb_graph_t g, double c0, int mode);      /* init_state */
+cheb_status cheb_state_set(cheb_graph_t g, const double* T_prev, const double* T_curr,
+                           const double* acc, int k);
+cheb_status cheb_state_generate(cheb_graph_t g);                       /* generate_stage */
+cheb_status cheb_state_accumulate(cheb_graph_t g, double c_k);         /* accumulate_stage */
+cheb_status cheb_state_rotate(cheb_graph_t g);  /* T_prev<-T_curr<-T_next, k++ */
+cheb_status cheb_state_get(cheb_graph_t g, double* T_prev, double* T_curr, double* T_next,
+                           double* acc, int* k);
+
+/* ---- generators: generate.hpp:27-40 (host, std::mt19937_64 as the reference) ---- */
+/* Host outputs: E interleaved int64 pairs, malloc'ed; release with cheb_free. */
+cheb_status cheb_gen_ring(int64_t n, int64_t** edges, int64_t* E);                /* :28 */
+cheb_status cheb_gen_star(int64_t n, int64_t** edges, int64_t* E);                /* :31 */
+cheb_status cheb_gen_regular(int64_t n, int64_t k, int64_t** edges, int64_t* E);  /* :35 */
+cheb_status cheb_gen_gnp(int64_t n, double p, uint64_t seed, int64_t** edges, int64_t* E); /* :40 */
+/* New, counter-based (host == device bit for bit).  Output: E interleaved int32 pairs,
+ * on the device (cudaMalloc on `device`, release with cheb_device_free) when on_device,
+ * else on the host (malloc, release with cheb_free). */
+cheb_status cheb_gen_rmat(int scale, int64_t edge_factor, double a, double b, double c,
+                          uint64_t seed, int on_device, int device, void** edges, int64_t* E);
+cheb_status cheb_gen_chung_lu(int64_t n, double gamma, double wmin, double wmax, int64_t draws,
+                              uint64_t seed, int on_device, int device, void** edges, int64_t* E);
+const char* cheb_gen_last_error(void);
+void cheb_free(void* p);
+void cheb_device_free(void* p, int device);
+
+/* kahan_sum (graph.hpp:75) on the host, exactly as graph.cpp:10-19. */
+double cheb_kahan_sum(const double* x, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHEBPR_CUDA_H */

@@ -1,0 +1,737 @@
+// K1 — device-resident, pattern-only CSR builder, CSR upload/download, and the
+// degree-binned solver view.
+//
+// Replaces build_graph (/root/reference/proj/src/graph.cpp:23-102) with the same
+// observable result, bit for bit: n = max(n_hint, max id + 1) (:25-29); canonical
+// (min,max) pairs sorted and deduplicated (:31-43); a self-loop adds 1 to its degree
+// and one adjacency entry (:45-49, :88-92); isolated vertices are an error naming the
+// lowest one (:70-75) or are dropped by an order-preserving renumbering (:51-69); rows
+// hold their neighbours in ascending order (:93-95).  No values array and no
+// inv_degree array are stored: the D^-1 scale is an in-register IEEE reciprocal of
+// the row length, bit-identical to graph.cpp:97-99.
+//
+// Device algorithm: 64-bit keys (lo << s | hi) -> cub radix sort -> unique ->
+// degree histogram -> (monotone remap) -> both directions emitted as (row << s | col)
+// with the second copy of a self-loop emitted as a sentinel -> radix sort ->
+// row_ptr = exclusive scan of degrees, col = low bits.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace chebgpu {
+
+namespace {
+
+constexpr int kBuildThreads = 256;
+
+inline int grid_for(int64_t n, int threads = kBuildThreads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 32) b = 148 * 32;
+    return static_cast<int>(b);
+}
+
+template <class T>
+__device__ __forceinline__ int64_t load_id(const T* e, int64_t i) {
+    return static_cast<int64_t>(e[i]);
+}
+
+// Min and max endpoint id over the edge list.
+template <class T>
+__global__ void k_minmax(const T* __restrict__ e, int64_t cnt, long long* out_min,
+                         long long* out_max) {
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        long long v = load_id(e, i);
+        lo = v < lo ? v : lo;
+        hi = v > hi ? v : hi;
+    }
+    for (int o = 16; o; o >>= 1) {
+        long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+        long long b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out_min, lo);
+        atomicMax(out_max, hi);
+    }
+}
+
+// Canonical undirected key (min << s) | max.
+template <class T>
+__global__ void k_canon(const T* __restrict__ e, int64_t E, int s, uint64_t* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t a = (uint64_t)load_id(e, 2 * i), b = (uint64_t)load_id(e, 2 * i + 1);
+        uint64_t lo = a < b ? a : b, hi = a < b ? b : a;
+        keys[i] = (lo << s) | hi;
+    }
+}
+
+__global__ void k_degree(const uint64_t* __restrict__ keys, int64_t m, int s,
+                         unsigned int* __restrict__ deg) {
+    const uint64_t mask = (1ull << s) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        uint64_t a = k >> s, b = k & mask;
+        atomicAdd(&deg[a], 1u);
+        if (a != b) atomicAdd(&deg[b], 1u);
+    }
+}
+
+// Lowest zero-degree vertex (or n if none) + degree extrema + flags for compaction.
+__global__ void k_deg_scan(const unsigned int* __restrict__ deg, int64_t n,
+                           unsigned long long* first_zero, unsigned int* dmin, unsigned int* dmax) {
+    unsigned long long fz = ~0ull;
+    unsigned int lo = 0xffffffffu, hi = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        unsigned int d = deg[v];
+        if (d == 0 && (unsigned long long)v < fz) fz = (unsigned long long)v;
+        if (d) {
+            lo = d < lo ? d : lo;
+            hi = d > hi ? d : hi;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        fz = min(fz, __shfl_xor_sync(0xffffffffu, fz, o));
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(first_zero, fz);
+        atomicMin(dmin, lo);
+        atomicMax(dmax, hi);
+    }
+}
+
+__global__ void k_nonzero_flags(const unsigned int* __restrict__ deg, int64_t n,
+                                int* __restrict__ flags) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x)
+        flags[v] = deg[v] > 0 ? 1 : 0;
+}
+
+// Order-preserving renumbering (graph.cpp:52-69): a monotone map keeps the sort.
+__global__ void k_remap_keys(uint64_t* __restrict__ keys, int64_t m, int s,
+                             const int* __restrict__ remap) {
+    const uint64_t mask = (1ull << s) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        uint64_t a = (uint64_t)remap[k >> s], b = (uint64_t)remap[k & mask];
+        keys[i] = (a << s) | b;
+    }
+}
+
+__global__ void k_compact_deg(const unsigned int* __restrict__ deg, const int* __restrict__ remap,
+                              int64_t n, unsigned int* __restrict__ out) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        unsigned int d = deg[v];
+        if (d) out[remap[v]] = d;
+    }
+}
+
+// Both directions of every canonical edge; the mirror of a self-loop becomes a
+// sentinel that sorts past every real key (graph.cpp:88-92 stores a loop once).
+__global__ void k_directed(const uint64_t* __restrict__ keys, int64_t m, int s,
+                           uint64_t* __restrict__ out) {
+    const uint64_t mask = (1ull << s) - 1;
+    const uint64_t sentinel = ~0ull;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        uint64_t a = k >> s, b = k & mask;
+        out[2 * i] = k;
+        out[2 * i + 1] = (a == b) ? sentinel : ((b << s) | a);
+    }
+}
+
+__global__ void k_low_bits(const uint64_t* __restrict__ keys, int64_t nnz, int s,
+                           int* __restrict__ col) {
+    const uint64_t mask = (1ull << s) - 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+         i += (int64_t)gridDim.x * blockDim.x)
+        col[i] = (int)(keys[i] & mask);
+}
+
+__global__ void k_widen_deg(const unsigned int* __restrict__ in, int64_t cnt, int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)in[i];
+}
+
+template <class RP>
+__global__ void k_narrow_rowptr(const int64_t* __restrict__ in, int64_t cnt, RP* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (RP)in[i];
+}
+
+template <class RP>
+__global__ void k_widen_rowptr(const RP* __restrict__ in, int64_t cnt, int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)in[i];
+}
+
+template <class RP>
+__global__ void k_row_degrees(const RP* __restrict__ rp, int64_t n, int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)(rp[i + 1] - rp[i]);
+}
+
+__global__ void k_widen_col(const int* __restrict__ in, int64_t cnt, int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (int64_t)in[i];
+}
+
+// Upload path: int64 neighbours -> int32, flag out-of-range ids.
+__global__ void k_narrow_col(const int64_t* __restrict__ in, int64_t cnt, int64_t n,
+                             int* __restrict__ out, unsigned long long* bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t v = in[i];
+        if (v < 0 || v >= n) atomicMin(bad, (unsigned long long)i);
+        out[i] = (int)v;
+    }
+}
+
+int bits_for(int64_t n) {  // smallest s with n <= 2^s - 1 (so a row field is never all-ones)
+    int s = 1;
+    while ((int64_t(1) << s) <= n) ++s;
+    return s;
+}
+
+struct TempStore {
+    DevMem mem;
+    void* get(size_t bytes) {
+        mem.ensure(bytes);
+        return mem.get();
+    }
+};
+
+void sort_keys(uint64_t*& keys, uint64_t*& alt, int64_t cnt, int end_bit, cudaStream_t st,
+               TempStore& tmp) {
+    cub::DoubleBuffer<uint64_t> db(keys, alt);
+    size_t bytes = 0;
+    CHEB_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, bytes, db, cnt, 0, end_bit, st));
+    void* t = tmp.get(bytes);
+    CHEB_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(t, bytes, db, cnt, 0, end_bit, st));
+    keys = db.Current();
+    alt = db.Alternate();
+}
+
+template <class T>
+T read_scalar(const T* d, cudaStream_t st) {
+    T h;
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    return h;
+}
+
+}  // namespace
+
+void build_from_edges(cheb_graph* g, const void* d_edges, int64_t E, int edge_bits,
+                      const cheb_build_opts& o) {
+    cudaStream_t st = g->stream;
+    TempStore tmp;
+    const int64_t nid = 2 * E;
+
+    // n and id checks (graph.cpp:25-29)
+    int64_t n = std::max<int64_t>(o.n_hint, 0);
+    if (E > 0) {
+        DevMem mm(2 * sizeof(long long));
+        long long init[2] = {LLONG_MAX, LLONG_MIN};
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(mm.get(), init, sizeof init, cudaMemcpyHostToDevice, st));
+        if (edge_bits == 64)
+            k_minmax<<<grid_for(nid), kBuildThreads, 0, st>>>(
+                static_cast<const int64_t*>(d_edges), nid, mm.ptr<long long>(), mm.ptr<long long>() + 1);
+        else
+            k_minmax<<<grid_for(nid), kBuildThreads, 0, st>>>(
+                static_cast<const int32_t*>(d_edges), nid, mm.ptr<long long>(), mm.ptr<long long>() + 1);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        long long h[2];
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(h, mm.get(), sizeof h, cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (h[0] < 0) fail(CHEB_VALIDATION, "negative vertex id in edge list");
+        n = std::max<int64_t>(n, h[1] + 1);
+    }
+    if (n > INT32_MAX - 1)
+        fail(CHEB_CAPACITY, "device CSR builder supports n < 2^31 (int32 column ids), got n=" +
+                                std::to_string(n));
+    const int s = bits_for(n);
+
+    // canonical keys, sort, dedup (graph.cpp:31-43)
+    DevMem kbuf(sizeof(uint64_t) * std::max<int64_t>(E, 1));
+    DevMem kalt(sizeof(uint64_t) * std::max<int64_t>(E, 1));
+    uint64_t* keys = kbuf.ptr<uint64_t>();
+    uint64_t* alt = kalt.ptr<uint64_t>();
+    if (E > 0) {
+        if (edge_bits == 64)
+            k_canon<<<grid_for(E), kBuildThreads, 0, st>>>(static_cast<const int64_t*>(d_edges), E, s, keys);
+        else
+            k_canon<<<grid_for(E), kBuildThreads, 0, st>>>(static_cast<const int32_t*>(d_edges), E, s, keys);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        sort_keys(keys, alt, E, 2 * s, st, tmp);
+    }
+    int64_t m = E;
+    if (o.dedup && E > 0) {
+        DevMem cnt(sizeof(int64_t));
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceSelect::Unique(nullptr, bytes, keys, alt, cnt.ptr<int64_t>(), E, st));
+        void* t = tmp.get(bytes);
+        CHEB_CUDA_CHECK(cub::DeviceSelect::Unique(t, bytes, keys, alt, cnt.ptr<int64_t>(), E, st));
+        m = read_scalar(cnt.ptr<int64_t>(), st);
+        std::swap(keys, alt);
+    }
+    g->duplicates_removed = E - m;
+
+    // degrees, self-loop once (graph.cpp:45-49)
+    DevMem deg(sizeof(unsigned int) * (n + 1));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(deg.get(), 0, sizeof(unsigned int) * (n + 1), st));
+    if (m > 0) {
+        k_degree<<<grid_for(m), kBuildThreads, 0, st>>>(keys, m, s, deg.ptr<unsigned int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
+    DevMem scan(sizeof(unsigned long long) + 2 * sizeof(unsigned int));
+    auto deg_stats = [&](const unsigned int* d, int64_t nn, unsigned long long* fz,
+                         unsigned int* lo, unsigned int* hi) {
+        unsigned char init[sizeof(unsigned long long) + 2 * sizeof(unsigned int)];
+        unsigned long long a = ~0ull;
+        unsigned int b = 0xffffffffu, c = 0;
+        std::memcpy(init, &a, 8);
+        std::memcpy(init + 8, &b, 4);
+        std::memcpy(init + 12, &c, 4);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(scan.get(), init, sizeof init, cudaMemcpyHostToDevice, st));
+        if (nn > 0) {
+            k_deg_scan<<<grid_for(nn), kBuildThreads, 0, st>>>(
+                d, nn, scan.ptr<unsigned long long>(),
+                reinterpret_cast<unsigned int*>(scan.ptr<char>() + 8),
+                reinterpret_cast<unsigned int*>(scan.ptr<char>() + 12));
+            CHEB_CUDA_CHECK(cudaGetLastError());
+        }
+        unsigned char out[16];
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(out, scan.get(), 16, cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        std::memcpy(fz, out, 8);
+        std::memcpy(lo, out + 8, 4);
+        std::memcpy(hi, out + 12, 4);
+    };
+    unsigned long long first_zero;
+    unsigned int dmin, dmax;
+    deg_stats(deg.ptr<unsigned int>(), n, &first_zero, &dmin, &dmax);
+
+    g->isolated_dropped = 0;
+    const bool any_isolated = n > 0 && first_zero != ~0ull;
+    if (any_isolated && !o.drop_isolated)  // graph.cpp:70-75
+        fail(CHEB_VALIDATION, "vertex " + std::to_string(first_zero) + " is isolated (degree 0)");
+    if (any_isolated) {  // graph.cpp:51-69
+        DevMem flags(sizeof(int) * n), remap(sizeof(int) * n);
+        k_nonzero_flags<<<grid_for(n), kBuildThreads, 0, st>>>(deg.ptr<unsigned int>(), n, flags.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags.ptr<int>(), remap.ptr<int>(), n, st));
+        void* t = tmp.get(bytes);
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, bytes, flags.ptr<int>(), remap.ptr<int>(), n, st));
+        int last_remap = read_scalar(remap.ptr<int>() + (n - 1), st);
+        unsigned int last_deg = read_scalar(deg.ptr<unsigned int>() + (n - 1), st);
+        const int64_t kept = (int64_t)last_remap + (last_deg > 0 ? 1 : 0);
+        g->isolated_dropped = n - kept;
+        if (m > 0) {
+            k_remap_keys<<<grid_for(m), kBuildThreads, 0, st>>>(keys, m, s, remap.ptr<int>());
+            CHEB_CUDA_CHECK(cudaGetLastError());
+        }
+        DevMem deg2(sizeof(unsigned int) * (kept + 1));
+        CHEB_CUDA_CHECK(cudaMemsetAsync(deg2.get(), 0, sizeof(unsigned int) * (kept + 1), st));
+        k_compact_deg<<<grid_for(n), kBuildThreads, 0, st>>>(deg.ptr<unsigned int>(), remap.ptr<int>(), n,
+                                                             deg2.ptr<unsigned int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        deg = std::move(deg2);
+        n = kept;
+        deg_stats(deg.ptr<unsigned int>(), n, &first_zero, &dmin, &dmax);
+    }
+
+    // directed entries, sorted by (row, col): CSR with ascending rows (graph.cpp:77-95)
+    const int64_t two_m = 2 * m;
+    DevMem dir(sizeof(uint64_t) * std::max<int64_t>(two_m, 1));
+    DevMem dalt(sizeof(uint64_t) * std::max<int64_t>(two_m, 1));
+    uint64_t* dk = dir.ptr<uint64_t>();
+    uint64_t* da = dalt.ptr<uint64_t>();
+    if (m > 0) {
+        k_directed<<<grid_for(m), kBuildThreads, 0, st>>>(keys, m, s, dk);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    kbuf.release();  // canonical keys are dead once the directed entries exist
+    kalt.release();
+    if (two_m > 0) sort_keys(dk, da, two_m, 2 * s, st, tmp);
+
+    // row_ptr = exclusive scan of degrees (widened to int64; deg[n] == 0 so rp[n] = nnz)
+    DevMem rp64((n + 1) * sizeof(int64_t));
+    {
+        DevMem deg64(sizeof(int64_t) * (n + 1));
+        CHEB_CUDA_CHECK(cudaMemsetAsync(deg.ptr<unsigned int>() + n, 0, sizeof(unsigned int), st));
+        k_widen_deg<<<grid_for(n + 1), kBuildThreads, 0, st>>>(deg.ptr<unsigned int>(), n + 1,
+                                                               deg64.ptr<int64_t>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, deg64.ptr<int64_t>(), rp64.ptr<int64_t>(), n + 1, st));
+        void* t = tmp.get(bytes);
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, bytes, deg64.ptr<int64_t>(), rp64.ptr<int64_t>(), n + 1, st));
+    }
+    const int64_t nnz = n > 0 ? read_scalar(rp64.ptr<int64_t>() + n, st) : 0;
+
+    g->n = n;
+    g->m = m;
+    g->nnz = nnz;
+    g->multi = !o.dedup;
+    g->max_degree = n > 0 ? dmax : 0;
+    g->min_degree = n > 0 ? dmin : 0;
+    g->rp64 = o.row_ptr_64 != 0 || nnz > INT32_MAX;
+    g->col.alloc(sizeof(int) * std::max<int64_t>(nnz, 1));
+    if (nnz > 0) {
+        k_low_bits<<<grid_for(nnz), kBuildThreads, 0, st>>>(dk, nnz, s, g->col.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
+    if (g->rp64) {
+        g->row_ptr = std::move(rp64);
+    } else {
+        g->row_ptr.alloc(sizeof(int) * (n + 1));
+        k_narrow_rowptr<<<grid_for(n + 1), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), n + 1,
+                                                                   g->row_ptr.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
+    g->inv_array = false;
+    g->view.ready = false;
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors, int64_t n,
+                int64_t nnz, const double* inv_degree) {
+    cudaStream_t st = g->stream;
+    g->n = n;
+    g->nnz = nnz;
+    g->rp64 = g->rp64 || nnz > INT32_MAX;
+    if (n > INT32_MAX - 1) fail(CHEB_CAPACITY, "device path supports n < 2^31");
+
+    // offsets: host int64 -> device (int32 narrowed when possible)
+    DevMem rp64(sizeof(int64_t) * (n + 1));
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(rp64.get(), offsets, sizeof(int64_t) * (n + 1),
+                                    cudaMemcpyHostToDevice, st));
+    if (g->rp64) {
+        g->row_ptr = std::move(rp64);
+    } else {
+        g->row_ptr.alloc(sizeof(int) * (n + 1));
+        k_narrow_rowptr<<<grid_for(n + 1), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), n + 1,
+                                                                   g->row_ptr.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
+    // neighbours: int64 -> int32, range-checked.  Chunked to bound the staging buffer.
+    g->col.alloc(sizeof(int) * std::max<int64_t>(nnz, 1));
+    if (nnz > 0) {
+        const int64_t chunk = std::min<int64_t>(nnz, int64_t(1) << 26);
+        DevMem stage(sizeof(int64_t) * chunk);
+        DevMem bad(sizeof(unsigned long long));
+        unsigned long long none = ~0ull;
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(bad.get(), &none, 8, cudaMemcpyHostToDevice, st));
+        for (int64_t off = 0; off < nnz; off += chunk) {
+            const int64_t c = std::min(chunk, nnz - off);
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(stage.get(), neighbors + off, sizeof(int64_t) * c,
+                                            cudaMemcpyHostToDevice, st));
+            k_narrow_col<<<grid_for(c), kBuildThreads, 0, st>>>(stage.ptr<int64_t>(), c, n,
+                                                                 g->col.ptr<int>() + off,
+                                                                 bad.ptr<unsigned long long>());
+            CHEB_CUDA_CHECK(cudaGetLastError());
+        }
+        unsigned long long b = read_scalar(bad.ptr<unsigned long long>(), st);
+        if (b != ~0ull) fail(CHEB_VALIDATION, "neighbor id out of range at entry " + std::to_string(b));
+    }
+    // inv_degree: canonical (1.0/deg bitwise) -> in-kernel reciprocal; else keep the array.
+    g->inv_array = false;
+    if (inv_degree) {
+        for (int64_t v = 0; v < n; ++v) {
+            const double want = 1.0 / static_cast<double>(offsets[v + 1] - offsets[v]);
+            if (std::memcmp(&want, &inv_degree[v], sizeof(double)) != 0) {
+                g->inv_array = true;
+                break;
+            }
+        }
+        if (g->inv_array) {
+            g->inv.alloc(sizeof(double) * n);
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(g->inv.get(), inv_degree, sizeof(double) * n,
+                                            cudaMemcpyHostToDevice, st));
+        }
+    }
+    g->view.ready = false;
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees) {
+    cudaStream_t st = g->stream;
+    const int64_t n = g->n, nnz = g->nnz;
+    if (offsets || degrees) {
+        DevMem w(sizeof(int64_t) * (n + 1));
+        if (offsets) {
+            if (g->rp64)
+                CHEB_CUDA_CHECK(cudaMemcpyAsync(offsets, g->row_ptr.get(), sizeof(int64_t) * (n + 1),
+                                                cudaMemcpyDeviceToHost, st));
+            else {
+                k_widen_rowptr<<<grid_for(n + 1), kBuildThreads, 0, st>>>(g->row_ptr.ptr<int>(), n + 1,
+                                                                          w.ptr<int64_t>());
+                CHEB_CUDA_CHECK(cudaMemcpyAsync(offsets, w.get(), sizeof(int64_t) * (n + 1),
+                                                cudaMemcpyDeviceToHost, st));
+            }
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+        if (degrees && n > 0) {
+            if (g->rp64)
+                k_row_degrees<<<grid_for(n), kBuildThreads, 0, st>>>(g->row_ptr.ptr<int64_t>(), n, w.ptr<int64_t>());
+            else
+                k_row_degrees<<<grid_for(n), kBuildThreads, 0, st>>>(g->row_ptr.ptr<int>(), n, w.ptr<int64_t>());
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(degrees, w.get(), sizeof(int64_t) * n,
+                                            cudaMemcpyDeviceToHost, st));
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+    }
+    if (neighbors && nnz > 0) {
+        const int64_t chunk = std::min<int64_t>(nnz, int64_t(1) << 26);
+        DevMem w(sizeof(int64_t) * chunk);
+        for (int64_t off = 0; off < nnz; off += chunk) {
+            const int64_t c = std::min(chunk, nnz - off);
+            k_widen_col<<<grid_for(c), kBuildThreads, 0, st>>>(g->col.ptr<int>() + off, c, w.ptr<int64_t>());
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(neighbors + off, w.get(), sizeof(int64_t) * c,
+                                            cudaMemcpyDeviceToHost, st));
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Solver view: degree-descending relabel + bins (see common.cuh).
+// ---------------------------------------------------------------------------
+namespace {
+
+template <class RP>
+__global__ void k_degree_keys(const RP* __restrict__ rp, int64_t n, unsigned int* __restrict__ key,
+                              int* __restrict__ ids) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        key[v] = ~(unsigned int)(rp[v + 1] - rp[v]);  // ascending sort of ~deg = descending deg
+        ids[v] = (int)v;
+    }
+}
+
+__global__ void k_scatter_rank(const int* __restrict__ order, int64_t n, int* __restrict__ rank) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        rank[order[i]] = (int)i;
+}
+
+template <class RP>
+__global__ void k_new_degrees(const RP* __restrict__ rp, const int* __restrict__ order, int64_t n,
+                              int64_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int o = order[i];
+        out[i] = (int64_t)(rp[o + 1] - rp[o]);
+    }
+}
+
+// Warp per new row: copy the old row's neighbours in storage order, renamed.
+template <class RPO, class RPN>
+__global__ void k_permute_rows(const RPO* __restrict__ rp_old, const int* __restrict__ col_old,
+                               const RPN* __restrict__ rp_new, const int* __restrict__ order,
+                               const int* __restrict__ rank, int64_t n, int* __restrict__ col_new) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int o = order[w];
+        const int64_t b = rp_old[o], e = rp_old[o + 1], d = rp_new[w];
+        for (int64_t j = b + lane; j < e; j += 32) col_new[d + (j - b)] = rank[col_old[j]];
+    }
+}
+
+__global__ void k_gather_inv(const double* __restrict__ inv, const int* __restrict__ order,
+                             int64_t n, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = inv[order[i]];
+}
+
+// count of rows with degree > thr[j]  (degrees sorted descending)
+__global__ void k_bin_bounds(const int64_t* __restrict__ deg, int64_t n, const int64_t* __restrict__ thr,
+                             int nthr, int64_t* __restrict__ out) {
+    int j = threadIdx.x;
+    if (j >= nthr) return;
+    int64_t lo = 0, hi = n, t = thr[j];
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (deg[mid] > t) lo = mid + 1;
+        else hi = mid;
+    }
+    out[j] = lo;
+}
+
+}  // namespace
+
+// Bin thresholds (degrees).  Hub rows are split into chunks of kHubChunk nnz.
+constexpr int64_t kHubDeg = 16384;
+constexpr int64_t kHubChunk = 8192;
+constexpr int64_t kBlockDeg = 1024;   // (kBlockDeg, kHubDeg]: one CTA per row
+constexpr int kMaxResident = 148 * 8; // CTAs of 256 threads resident chip-wide
+
+template <class RPO, class RPN>
+static void build_view_t(cheb_graph* g) {
+    cudaStream_t st = g->stream;
+    SolverView& V = g->view;
+    const int64_t n = g->n, nnz = g->nnz;
+    TempStore tmp;
+    const RPO* rp_old = g->row_ptr.ptr<RPO>();
+
+    DevMem keys(sizeof(unsigned) * n), keys2(sizeof(unsigned) * n), ids(sizeof(int) * n);
+    V.order.alloc(sizeof(int) * n);
+    k_degree_keys<<<grid_for(n), kBuildThreads, 0, st>>>(rp_old, n, keys.ptr<unsigned>(), ids.ptr<int>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    {
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.ptr<unsigned>(), keys2.ptr<unsigned>(),
+                                                        ids.ptr<int>(), V.order.ptr<int>(), n, 0, 32, st));
+        void* t = tmp.get(bytes);
+        CHEB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, bytes, keys.ptr<unsigned>(), keys2.ptr<unsigned>(),
+                                                        ids.ptr<int>(), V.order.ptr<int>(), n, 0, 32, st));
+    }
+    DevMem rank(sizeof(int) * n);
+    k_scatter_rank<<<grid_for(n), kBuildThreads, 0, st>>>(V.order.ptr<int>(), n, rank.ptr<int>());
+    DevMem deg_new(sizeof(int64_t) * (n + 1));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(deg_new.get(), 0, sizeof(int64_t) * (n + 1), st));
+    k_new_degrees<<<grid_for(n), kBuildThreads, 0, st>>>(rp_old, V.order.ptr<int>(), n, deg_new.ptr<int64_t>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+
+    DevMem rp64(sizeof(int64_t) * (n + 1));
+    {
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, deg_new.ptr<int64_t>(), rp64.ptr<int64_t>(), n + 1, st));
+        void* t = tmp.get(bytes);
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, bytes, deg_new.ptr<int64_t>(), rp64.ptr<int64_t>(), n + 1, st));
+    }
+    V.rp64 = sizeof(RPN) == 8;
+    if (V.rp64) {
+        V.row_ptr = std::move(rp64);
+    } else {
+        V.row_ptr.alloc(sizeof(int) * (n + 1));
+        k_narrow_rowptr<<<grid_for(n + 1), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), n + 1, V.row_ptr.ptr<int>());
+    }
+    V.col.alloc(sizeof(int) * std::max<int64_t>(nnz, 1));
+    k_permute_rows<<<grid_for(n * 32), kBuildThreads, 0, st>>>(rp_old, g->col.ptr<int>(), V.row_ptr.ptr<RPN>(),
+                                                              V.order.ptr<int>(), rank.ptr<int>(), n,
+                                                              V.col.ptr<int>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    if (g->inv_array) {
+        V.inv.alloc(sizeof(double) * n);
+        k_gather_inv<<<grid_for(n), kBuildThreads, 0, st>>>(g->inv.ptr<double>(), V.order.ptr<int>(), n,
+                                                            V.inv.ptr<double>());
+    } else {
+        V.inv.release();
+    }
+
+    // Bin boundaries over the descending degrees.
+    // thresholds: hub, block, 512,256,128,64,32,16,8,4,2,1
+    std::vector<int64_t> thr = {kHubDeg, kBlockDeg, 512, 256, 128, 64, 32, 16, 8, 4, 2, 1};
+    DevMem dthr(sizeof(int64_t) * thr.size()), dout(sizeof(int64_t) * thr.size());
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(dthr.get(), thr.data(), sizeof(int64_t) * thr.size(),
+                                    cudaMemcpyHostToDevice, st));
+    k_bin_bounds<<<1, 32, 0, st>>>(deg_new.ptr<int64_t>(), n, dthr.ptr<int64_t>(), (int)thr.size(),
+                                   dout.ptr<int64_t>());
+    std::vector<int64_t> bound(thr.size());
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(bound.data(), dout.get(), sizeof(int64_t) * thr.size(),
+                                    cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+
+    // Hub rows: chunk table.
+    V.n_hub = bound[0];
+    std::vector<int64_t> hub_deg(V.n_hub);
+    if (V.n_hub)
+        CHEB_CUDA_CHECK(cudaMemcpy(hub_deg.data(), deg_new.get(), sizeof(int64_t) * V.n_hub,
+                                   cudaMemcpyDeviceToHost));
+    std::vector<int> chunk_row, chunk_idx, hub_first(V.n_hub + 1, 0);
+    for (int64_t h = 0; h < V.n_hub; ++h) {
+        hub_first[h] = (int)chunk_row.size();
+        const int64_t nc = (hub_deg[h] + kHubChunk - 1) / kHubChunk;
+        for (int64_t j = 0; j < nc; ++j) {
+            chunk_row.push_back((int)h);
+            chunk_idx.push_back((int)j);
+        }
+    }
+    hub_first[V.n_hub] = (int)chunk_row.size();
+    V.n_chunks = (int)chunk_row.size();
+    V.chunk_row.alloc(sizeof(int) * std::max(V.n_chunks, 1));
+    V.chunk_idx.alloc(sizeof(int) * std::max(V.n_chunks, 1));
+    V.hub_first.alloc(sizeof(int) * (V.n_hub + 1));
+    if (V.n_chunks) {
+        CHEB_CUDA_CHECK(cudaMemcpy(V.chunk_row.get(), chunk_row.data(), sizeof(int) * V.n_chunks, cudaMemcpyHostToDevice));
+        CHEB_CUDA_CHECK(cudaMemcpy(V.chunk_idx.get(), chunk_idx.data(), sizeof(int) * V.n_chunks, cudaMemcpyHostToDevice));
+    }
+    CHEB_CUDA_CHECK(cudaMemcpy(V.hub_first.get(), hub_first.data(), sizeof(int) * (V.n_hub + 1), cudaMemcpyHostToDevice));
+
+    // Assemble bins (hub, block, warp x5, vector x5, one-lane).
+    V.bins.clear();
+    int next_block = 0;
+    auto add = [&](int64_t b, int64_t e, int kind, int lanes, int64_t rows_per_block_iter) {
+        if (e <= b) return;
+        Bin bin;
+        bin.row_begin = b;
+        bin.row_end = e;
+        bin.kind = kind;
+        bin.lanes = lanes;
+        bin.block_begin = next_block;
+        if (kind == BIN_HUB) {
+            bin.nblocks = V.n_chunks;
+            bin.chunk_begin = 0;
+        } else {
+            int64_t want = (e - b + rows_per_block_iter - 1) / rows_per_block_iter;
+            int64_t cap = 4 * kMaxResident;
+            bin.nblocks = (int)std::max<int64_t>(1, std::min(want, cap));
+        }
+        next_block += bin.nblocks;
+        V.bins.push_back(bin);
+    };
+    add(0, bound[0], BIN_HUB, 0, 1);
+    add(bound[0], bound[1], BIN_BLOCK, 0, 1);
+    // warp rows: deg in (32, 1024], one bin per octave
+    add(bound[1], bound[2], BIN_VEC, 32, kThreads / 32);
+    add(bound[2], bound[3], BIN_VEC, 32, kThreads / 32);
+    add(bound[3], bound[4], BIN_VEC, 32, kThreads / 32);
+    add(bound[4], bound[5], BIN_VEC, 32, kThreads / 32);
+    add(bound[5], bound[6], BIN_VEC, 32, kThreads / 32);
+    // vector rows: (16,32] -> 32 lanes, (8,16] -> 16, (4,8] -> 8, (2,4] -> 4, (1,2] -> 2, 1 -> 1
+    add(bound[6], bound[7], BIN_VEC, 32, kThreads / 32);
+    add(bound[7], bound[8], BIN_VEC, 16, kThreads / 16);
+    add(bound[8], bound[9], BIN_VEC, 8, kThreads / 8);
+    add(bound[9], bound[10], BIN_VEC, 4, kThreads / 4);
+    add(bound[10], bound[11], BIN_VEC, 2, kThreads / 2);
+    add(bound[11], n, BIN_VEC, 1, kThreads);
+    if ((int)V.bins.size() > kMaxBins) fail(CHEB_CUDA, "too many bins");
+    V.grid = std::max(next_block, 1);
+    V.ready = true;
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+void ensure_view(cheb_graph* g) {
+    if (g->view.ready) return;
+    if (g->rp64)
+        build_view_t<int64_t, int64_t>(g);
+    else
+        build_view_t<int, int>(g);
+}
+
+}  // namespace chebgpu

@@ -1,0 +1,477 @@
+// extern "C" boundary of libchebpr_b200 (include/chebpr_cuda.h).
+//
+// Every entry converts internal exceptions into cheb_status + a thread-local message,
+// and applies the reference's argument checks in the reference's order
+// (/root/reference/proj/src/cpaa.cpp:79-94, power.cpp:28-47), so that the wrappers
+// above the C-ABI raise exactly what the reference raises.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+using namespace chebgpu;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+cheb_status guarded(F&& f) {
+    try {
+        f();
+        return CHEB_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return CHEB_CAPACITY;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return CHEB_CUDA;
+    }
+}
+
+cheb_graph* new_graph(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        fail(CHEB_CUDA, "no CUDA device available (libchebpr_b200 has no CPU fallback)");
+    if (device < 0 || device >= count)
+        fail(CHEB_INVALID_ARG, "device ordinal " + std::to_string(device) + " out of range");
+    auto* g = new cheb_graph();
+    g->device = device;
+    DeviceGuard dg(device);
+    CHEB_CUDA_CHECK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    CHEB_CUDA_CHECK(cudaEventCreate(&g->ev0));
+    CHEB_CUDA_CHECK(cudaEventCreate(&g->ev1));
+    return g;
+}
+
+void fill_info(cheb_graph* g, cheb_graph_info* info) {
+    if (!info) return;
+    info->n = g->n;
+    info->m = g->m;
+    info->nnz = g->nnz;
+    info->duplicates_removed = g->duplicates_removed;
+    info->isolated_dropped = g->isolated_dropped;
+    info->max_degree = g->max_degree;
+    info->min_degree = g->min_degree;
+    info->multi = g->multi ? 1 : 0;
+    info->row_ptr_64 = g->rp64 ? 1 : 0;
+    info->inv_degree_array = g->inv_array ? 1 : 0;
+    info->device = g->device;
+}
+
+void need_graph(cheb_graph* g) {
+    if (!g) fail(CHEB_INVALID_ARG, "null graph handle");
+}
+
+// cpaa.cpp:16-26 essential_check, the parts that are not guaranteed by construction.
+void essential(cheb_graph* g) {
+    if (g->n < 1) fail(CHEB_VALIDATION, "graph has no vertices");
+}
+}  // namespace
+
+cheb_graph::~cheb_graph() {
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+extern "C" {
+
+const char* cheb_last_error(void) { return g_last_error.c_str(); }
+
+const char* cheb_version(void) { return "chebpr_b200 0.1 (sm_100a)"; }
+
+int cheb_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+    return c;
+}
+
+cheb_status cheb_beta(double c, double* out) {
+    return guarded([&] { *out = beta(c); });
+}
+cheb_status cheb_sigma(double c, double* out) {
+    return guarded([&] { *out = sigma(c); });
+}
+cheb_status cheb_err_bound(double c, int M, double* out) {
+    return guarded([&] { *out = err_bound(c, M); });
+}
+cheb_status cheb_plan_iterations(double c, double eps, int* M, double* predicted_err) {
+    return guarded([&] { *M = plan_iterations(c, eps, predicted_err); });
+}
+cheb_status cheb_coefficients(double c, int M, double* coeffs, double* beta_out, double* c0) {
+    return guarded([&] {
+        std::vector<double> t;
+        coefficients(c, M, t, beta_out, c0);
+        if (coeffs) std::memcpy(coeffs, t.data(), sizeof(double) * t.size());
+    });
+}
+cheb_status cheb_resolve_rounds(double c, int rounds, double eps, int max_rounds, int* M) {
+    return guarded([&] { *M = resolve_rounds(c, rounds, eps, max_rounds); });
+}
+
+double cheb_kahan_sum(const double* x, int64_t n) { return kahan_sum(x, n); }
+
+void cheb_build_opts_default(cheb_build_opts* o) {
+    o->dedup = 1;
+    o->drop_isolated = 0;
+    o->n_hint = 0;
+    o->device = 0;
+    o->row_ptr_64 = 0;
+}
+
+cheb_status cheb_graph_build(const int64_t* edges, int64_t E, const cheb_build_opts* opts,
+                             cheb_graph_t* out, cheb_graph_info* info) {
+    return guarded([&] {
+        if (E < 0) fail(CHEB_INVALID_ARG, "negative edge count");
+        cheb_build_opts o;
+        cheb_build_opts_default(&o);
+        if (opts) o = *opts;
+        // graph.cpp:27 — the host sees the ids first; reject negatives before any copy.
+        for (int64_t i = 0; i < 2 * E; ++i)
+            if (edges[i] < 0) fail(CHEB_VALIDATION, "negative vertex id in edge list");
+        std::unique_ptr<cheb_graph> g(new_graph(o.device));
+        DeviceGuard dg(o.device);
+        DevMem d(sizeof(int64_t) * 2 * std::max<int64_t>(E, 1));
+        if (E > 0)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(d.get(), edges, sizeof(int64_t) * 2 * E,
+                                            cudaMemcpyHostToDevice, g->stream));
+        build_from_edges(g.get(), d.get(), E, 64, o);
+        fill_info(g.get(), info);
+        *out = g.release();
+    });
+}
+
+cheb_status cheb_graph_build_device(const void* d_edges, int64_t E, int edge_bits,
+                                    const cheb_build_opts* opts, cheb_graph_t* out,
+                                    cheb_graph_info* info) {
+    return guarded([&] {
+        if (edge_bits != 32 && edge_bits != 64) fail(CHEB_INVALID_ARG, "edge_bits must be 32 or 64");
+        cheb_build_opts o;
+        cheb_build_opts_default(&o);
+        if (opts) o = *opts;
+        std::unique_ptr<cheb_graph> g(new_graph(o.device));
+        DeviceGuard dg(o.device);
+        build_from_edges(g.get(), d_edges, E, edge_bits, o);
+        fill_info(g.get(), info);
+        *out = g.release();
+    });
+}
+
+cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
+                                  const int64_t* neighbors, int64_t nnz, const int64_t* degrees,
+                                  int64_t n_degrees, const double* inv_degree, int64_t n_inv,
+                                  int64_t n, int64_t m, int multi, int device, int row_ptr_64,
+                                  cheb_graph_t* out) {
+    return guarded([&] {
+        // cpaa.cpp:16-26 essential_check, in the reference's order.
+        if (n < 1) fail(CHEB_VALIDATION, "graph has no vertices");
+        if (n_offsets != n + 1 || n_degrees != n || (inv_degree && n_inv != n) ||
+            nnz != offsets[n])
+            fail(CHEB_VALIDATION, "inconsistent graph arrays");
+        for (int64_t v = 0; v < n; ++v)
+            if (degrees[v] < 1)
+                fail(CHEB_VALIDATION, "vertex " + std::to_string(v) + " is isolated (degree 0)");
+        if (offsets[0] != 0) fail(CHEB_VALIDATION, "offsets must start at 0");
+        for (int64_t v = 0; v < n; ++v)
+            if (offsets[v + 1] < offsets[v])
+                fail(CHEB_VALIDATION, "offsets not monotone at vertex " + std::to_string(v));
+        std::unique_ptr<cheb_graph> g(new_graph(device));
+        DeviceGuard dg(device);
+        g->m = m;
+        g->multi = multi != 0;
+        g->rp64 = row_ptr_64 != 0;
+        g->duplicates_removed = 0;
+        g->isolated_dropped = 0;
+        int64_t dmin = INT64_MAX, dmax = 0;
+        for (int64_t v = 0; v < n; ++v) {
+            const int64_t d = offsets[v + 1] - offsets[v];
+            dmin = d < dmin ? d : dmin;
+            dmax = d > dmax ? d : dmax;
+        }
+        g->min_degree = dmin;
+        g->max_degree = dmax;
+        upload_csr(g.get(), offsets, neighbors, n, nnz, inv_degree);
+        *out = g.release();
+    });
+}
+
+cheb_status cheb_graph_download_csr(cheb_graph_t g, int64_t* offsets, int64_t* neighbors,
+                                    int64_t* degrees) {
+    return guarded([&] {
+        need_graph(g);
+        DeviceGuard dg(g->device);
+        download_csr(g, offsets, neighbors, degrees);
+    });
+}
+
+cheb_status cheb_graph_get_info(cheb_graph_t g, cheb_graph_info* info) {
+    return guarded([&] {
+        need_graph(g);
+        fill_info(g, info);
+    });
+}
+
+void cheb_graph_free(cheb_graph_t g) {
+    if (!g) return;
+    DeviceGuard dg(g->device);
+    cudaStreamSynchronize(g->stream);
+    delete g;
+}
+
+cheb_status cheb_partition_vertices(const int64_t* degrees, int64_t n, int K, int64_t* cuts) {
+    // cpaa.cpp:40-68: the j-th cut at the degree prefix nearest j/K of the total.
+    return guarded([&] {
+        if (K < 1) fail(CHEB_DOMAIN, "parallelism must be >= 1");
+        std::vector<int64_t> prefix(static_cast<size_t>(n) + 1, 0);
+        for (int64_t v = 0; v < n; ++v) prefix[v + 1] = prefix[v] + degrees[v];
+        const double total = static_cast<double>(prefix[n]);
+        cuts[0] = 0;
+        cuts[K] = n;
+        for (int j = 1; j < K; ++j) {
+            const double ideal = total * j / K;
+            // first prefix >= ideal (as doubles), then step back if the previous is nearer
+            int64_t lo = 0, hi = n + 1;
+            while (lo < hi) {
+                const int64_t mid = lo + (hi - lo) / 2;
+                if (static_cast<double>(prefix[mid]) < ideal) lo = mid + 1;
+                else hi = mid;
+            }
+            int64_t idx = lo > n ? n : lo;
+            if (idx > 0 && static_cast<double>(prefix[idx]) - ideal > ideal - static_cast<double>(prefix[idx - 1]))
+                --idx;
+            if (idx < cuts[j - 1]) idx = cuts[j - 1];
+            if (idx > n) idx = n;
+            cuts[j] = idx;
+        }
+    });
+}
+
+void cheb_cpaa_opts_default(cheb_cpaa_opts* o) {
+    o->c = 0.85;
+    o->rounds = -1;
+    o->eps = -1.0;
+    o->max_rounds = 60;
+    o->parallelism = 1;
+    o->mode = CHEB_MODE_FAST;
+    o->precision = CHEB_FP64;
+    o->R = 1;
+    o->personalization = nullptr;
+    o->trace = 1;
+}
+
+static SolveSpec checked_spec(cheb_graph* g, const cheb_cpaa_opts& o, const double* reference,
+                              int64_t n_reference) {
+    need_graph(g);
+    essential(g);                                               // cpaa.cpp:81
+    SolveSpec s;
+    s.M = resolve_rounds(o.c, o.rounds, o.eps, o.max_rounds);   // cpaa.cpp:82
+    std::vector<double> tmp;
+    coefficients(o.c, s.M, tmp, nullptr, nullptr);              // cpaa.cpp:83 (DomainError on c)
+    if (reference && n_reference != g->n)                       // cpaa.cpp:84-85
+        fail(CHEB_INVALID_ARG, "reference length does not match vertex count");
+    if (o.parallelism < 1) fail(CHEB_DOMAIN, "parallelism must be >= 1");  // cpaa.cpp:94
+    if (o.mode != CHEB_MODE_FAST && o.mode != CHEB_MODE_BITEXACT)
+        fail(CHEB_INVALID_ARG, "unknown mode");
+    if (o.precision != CHEB_FP64 && o.precision != CHEB_FP32)
+        fail(CHEB_INVALID_ARG, "precision must be 64 or 32");
+    s.c = o.c;
+    s.mode = o.mode;
+    s.precision = o.precision;
+    s.R = o.R < 1 ? 1 : o.R;
+    s.p = o.personalization;
+    s.trace = o.trace != 0;
+    return s;
+}
+
+cheb_status cheb_cpaa(cheb_graph_t g, const cheb_cpaa_opts* opts, const double* reference,
+                      int64_t n_reference, double* ranks, cheb_trace_row* trace,
+                      int* rounds_out, double* total_mass_out) {
+    return guarded([&] {
+        cheb_cpaa_opts o;
+        cheb_cpaa_opts_default(&o);
+        if (opts) o = *opts;
+        SolveSpec s = checked_spec(g, o, reference, n_reference);
+        if (reference && s.M > 0)  // metrics.cpp:18-19 (first call happens at round 1)
+            for (int64_t i = 0; i < g->n; ++i)
+                if (!(reference[i] > 0.0))
+                    fail(CHEB_DOMAIN, "reference entry " + std::to_string(i) + " is not positive");
+        std::vector<double> tr, errs;
+        double total = 0.0;
+        if (reference) cpaa_solve_ref(g, s, reference, &tr, &errs, &total);
+        else cpaa_solve(g, s, true, &tr, &total);
+        read_ranks(g, s.precision, ranks);
+        if (trace && s.M > 0) {
+            std::vector<double> co;
+            double b, c0;
+            coefficients(s.c, s.M, co, &b, &c0);
+            double residual = static_cast<double>(g->n) * c0 * b / (1.0 - b);  // cpaa.cpp:99
+            const double per_term = g->last_loop_ms / s.M;
+            for (int k = 1; k <= s.M; ++k) {
+                cheb_trace_row& r = trace[k - 1];
+                std::memset(&r, 0, sizeof r);
+                r.k = k;
+                r.c_k = co[k];
+                r.mass_T = tr[2 * (k - 1)];
+                r.S_k = tr[2 * (k - 1) + 1];
+                residual *= b;
+                r.residual_mass = residual;
+                r.elapsed_ms = per_term;
+                if (reference) {
+                    r.err = errs[2 * (k - 1)];
+                    r.err_l1 = errs[2 * (k - 1) + 1];
+                }
+            }
+        }
+        if (rounds_out) *rounds_out = s.M;
+        if (total_mass_out) *total_mass_out = total;
+    });
+}
+
+cheb_status cheb_cpaa_device(cheb_graph_t g, const cheb_cpaa_opts* opts, const void** d_ranks,
+                             int sync) {
+    return guarded([&] {
+        cheb_cpaa_opts o;
+        cheb_cpaa_opts_default(&o);
+        if (opts) o = *opts;
+        SolveSpec s = checked_spec(g, o, nullptr, 0);
+        if (sync) {
+            double total;
+            std::vector<double> tr;
+            cpaa_solve(g, s, false, &tr, &total);
+        } else {
+            cpaa_solve(g, s, false, nullptr, nullptr);
+        }
+        if (d_ranks) *d_ranks = g->ws.out.get();
+    });
+}
+
+cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double* term_ms,
+                              int capacity, int* terms) {
+    return guarded([&] {
+        cheb_cpaa_opts o;
+        cheb_cpaa_opts_default(&o);
+        if (opts) o = *opts;
+        SolveSpec s = checked_spec(g, o, nullptr, 0);
+        std::vector<double> ms;
+        cpaa_profile(g, s, ms);
+        for (int k = 0; k < s.M && k < capacity; ++k) term_ms[k] = ms[k];
+        if (terms) *terms = s.M;
+    });
+}
+
+cheb_status cheb_last_timing(cheb_graph_t g, double* loop_ms, double* term_kernel_ms, int* terms,
+                             int* launches) {
+    return guarded([&] {
+        need_graph(g);
+        DeviceGuard dg(g->device);
+        CHEB_CUDA_CHECK(cudaEventSynchronize(g->ev1));
+        float ms = 0.f;
+        CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+        g->last_loop_ms = ms;
+        if (loop_ms) *loop_ms = ms;
+        if (term_kernel_ms) *term_kernel_ms = g->last_terms ? ms / g->last_terms : 0.0;
+        if (terms) *terms = g->last_terms;
+        if (launches) *launches = g->last_launches;
+    });
+}
+
+void cheb_power_opts_default(cheb_power_opts* o) {
+    o->c = 0.85;
+    o->rounds = -1;
+    o->tol = -1.0;
+    o->max_rounds = 60;
+    o->parallelism = 1;
+    o->mode = CHEB_MODE_FAST;
+}
+
+cheb_status cheb_power(cheb_graph_t g, const cheb_power_opts* opts, const double* reference,
+                       int64_t n_reference, double* ranks, cheb_trace_row* trace,
+                       int trace_capacity, int* rounds_out, double* total_mass_out) {
+    return guarded([&] {
+        cheb_power_opts o;
+        cheb_power_opts_default(&o);
+        if (opts) o = *opts;
+        need_graph(g);
+        essential(g);                                                   // power.cpp:30
+        if (!(o.c > 0.0 && o.c < 1.0)) fail(CHEB_DOMAIN, "damping factor must lie in (0,1)");
+        const bool fixed = o.rounds >= 0, by_tol = o.tol > 0.0;         // power.cpp:33-37
+        if (fixed == by_tol) fail(CHEB_INVALID_ARG, "set exactly one of rounds and tol");
+        const int budget = fixed ? o.rounds : o.max_rounds;
+        if (budget < 0) fail(CHEB_INVALID_ARG, "round budget must be non-negative");
+        if (reference && n_reference != g->n)
+            fail(CHEB_INVALID_ARG, "reference length does not match vertex count");
+        if (o.parallelism < 1) fail(CHEB_DOMAIN, "parallelism must be >= 1");
+        if (reference && budget > 0)
+            for (int64_t i = 0; i < g->n; ++i)
+                if (!(reference[i] > 0.0))
+                    fail(CHEB_DOMAIN, "reference entry " + std::to_string(i) + " is not positive");
+        int rounds = 0;
+        double total = 0.0;
+        power_solve(g, o.c, o.rounds, o.tol, o.max_rounds, o.mode, reference, ranks, trace,
+                    trace_capacity, &rounds, &total);
+        if (rounds_out) *rounds_out = rounds;
+        if (total_mass_out) *total_mass_out = total;
+    });
+}
+
+cheb_status cheb_transition_apply(cheb_graph_t g, const double* x, int64_t nx, double* y, int mode) {
+    return guarded([&] {
+        need_graph(g);
+        if (nx != g->n)  // graph.cpp:105-107
+            fail(CHEB_INVALID_ARG, "vector length " + std::to_string(nx) +
+                                       " does not match vertex count " + std::to_string(g->n));
+        if (g->n == 0) return;
+        transition_apply(g, x, y, mode);
+    });
+}
+
+cheb_status cheb_state_init(cheb_graph_t g, double c0, int mode) {
+    return guarded([&] {
+        need_graph(g);
+        essential(g);  // cpaa.cpp:168
+        staged_init(g, c0, mode);
+    });
+}
+cheb_status cheb_state_set(cheb_graph_t g, const double* T_prev, const double* T_curr,
+                           const double* acc, int k) {
+    return guarded([&] {
+        need_graph(g);
+        staged_set(g, T_prev, T_curr, acc, k);
+    });
+}
+cheb_status cheb_state_generate(cheb_graph_t g) {
+    return guarded([&] {
+        need_graph(g);
+        staged_generate(g);
+    });
+}
+cheb_status cheb_state_accumulate(cheb_graph_t g, double c_k) {
+    return guarded([&] {
+        need_graph(g);
+        staged_accumulate(g, c_k);
+    });
+}
+cheb_status cheb_state_rotate(cheb_graph_t g) {
+    return guarded([&] {
+        need_graph(g);
+        staged_rotate(g);
+    });
+}
+cheb_status cheb_state_get(cheb_graph_t g, double* T_prev, double* T_curr, double* T_next,
+                           double* acc, int* k) {
+    return guarded([&] {
+        need_graph(g);
+        staged_get(g, T_prev, T_curr, T_next, acc, k);
+    });
+}
+
+}  // extern "C"

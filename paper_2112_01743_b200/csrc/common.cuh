@@ -1,0 +1,232 @@
+// Internal header of libchebpr_b200: error plumbing, device buffers, the graph
+// handle and the kernel-side helpers shared by the CSR builder and the term kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "chebpr_cuda.h"
+
+namespace chebgpu {
+
+// Internal exception; converted to cheb_status at the C-ABI (capi.cu).
+struct Error : std::runtime_error {
+    cheb_status code;
+    Error(cheb_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(cheb_status c, const std::string& m) { throw Error(c, m); }
+
+#define CHEB_CUDA_CHECK(expr)                                                            \
+    do {                                                                                 \
+        cudaError_t _e = (expr);                                                         \
+        if (_e != cudaSuccess)                                                           \
+            ::chebgpu::fail(CHEB_CUDA, std::string("CUDA error ") + cudaGetErrorString(_e) + \
+                                           " at " __FILE__ ":" + std::to_string(__LINE__) + \
+                                           " (" #expr ")");                              \
+    } while (0)
+
+// Owning device allocation (untyped bytes; typed views via ptr<T>()).
+class DevMem {
+public:
+    DevMem() = default;
+    explicit DevMem(size_t bytes) { alloc(bytes); }
+    ~DevMem() { release(); }
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    DevMem(DevMem&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevMem& operator=(DevMem&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void alloc(size_t bytes) {
+        release();
+        if (bytes == 0) bytes = 16;
+        CHEB_CUDA_CHECK(cudaMalloc(&p_, bytes));
+        n_ = bytes;
+    }
+    // Grow-only reuse.
+    void ensure(size_t bytes) {
+        if (bytes > n_ || !p_) alloc(bytes);
+    }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    template <class T>
+    T* ptr() const { return static_cast<T*>(p_); }
+    void* get() const { return p_; }
+    size_t bytes() const { return n_; }
+    explicit operator bool() const { return p_ != nullptr; }
+
+private:
+    void* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// Scoped device selection.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) CHEB_CUDA_CHECK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// --------------------------------------------------------------------------
+// Degree-binned solver view (the hot-path layout, built once per graph).
+//
+// Rows are relabelled by degree (descending, ties by id) so that every bin is a
+// contiguous row range and the most-gathered x entries (hubs) share cache lines.
+// Column ids are renamed, but every row keeps its neighbours in the reference's
+// storage order.  order[new] = old.
+// --------------------------------------------------------------------------
+enum BinKind : int { BIN_HUB = 0, BIN_BLOCK = 1, BIN_VEC = 2 };
+
+struct Bin {
+    int64_t row_begin = 0, row_end = 0;  // [begin, end) in new ids
+    int kind = BIN_VEC;
+    int lanes = 32;        // BIN_VEC: lanes per row (1..32)
+    int block_begin = 0;   // first blockIdx of this bin
+    int nblocks = 0;
+    int chunk_begin = 0;   // BIN_HUB: first chunk id; nblocks == #chunks
+};
+
+constexpr int kMaxBins = 16;
+constexpr int kThreads = 256;      // CTA size of the term kernels (8 warps)
+
+struct SolverView {
+    bool ready = false;
+    bool rp64 = false;
+    DevMem order;      // int32 [n]  new -> old
+    DevMem row_ptr;    // int32/int64 [n+1] (new order)
+    DevMem col;        // int32 [nnz] (renamed ids, storage order kept)
+    DevMem inv;        // double [n] (new order) only when inv_degree is non-canonical
+    std::vector<Bin> bins;
+    int grid = 0;          // total CTAs of one term launch
+    int64_t n_hub = 0;     // hub rows [0, n_hub)
+    int n_chunks = 0;
+    DevMem chunk_row;  // int32 [n_chunks]
+    DevMem chunk_idx;  // int32 [n_chunks]  j-th chunk of its row
+    DevMem hub_first;  // int32 [n_hub+1]   first chunk of hub row h
+};
+
+struct Workspace {
+    int64_t n = 0;
+    int R = 0;
+    int vbytes = 0;
+    int M = -1;
+    DevMem T0, T1, X0, X1, acc, out;    // vectors (solve precision), out = ranks (orig order)
+    DevMem part;                        // double [M][grid][2] block trace partials
+    DevMem hub_part;                    // double [n_chunks]
+    DevMem hub_cnt;                     // uint32 [n_hub]
+    DevMem hub_ts;                      // double [M][n_hub][2]
+    DevMem trace;                       // double [M][2] (mass_T, S_k)
+    DevMem total;                       // double [1]
+    DevMem coeffs;                      // double [M+1]
+    // CUDA graph of the whole solve for a given configuration.
+    cudaGraphExec_t exec = nullptr;
+    std::string exec_key;
+    std::string seen_key;  // last configuration solved without a graph
+    int launches = 0;
+    ~Workspace() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
+struct StagedState {
+    bool active = false;
+    int mode = 0;
+    int k = 1;
+    DevMem T_prev, T_curr, T_next, acc, x;
+};
+
+}  // namespace chebgpu
+
+// The opaque handle of the C-ABI.
+struct cheb_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int64_t n = 0, m = 0, nnz = 0;
+    int64_t duplicates_removed = 0, isolated_dropped = 0;
+    int64_t max_degree = 0, min_degree = 0;
+    bool multi = false;
+    bool rp64 = false;             // canonical row_ptr width
+    bool inv_array = false;        // non-canonical inv_degree uploaded
+    chebgpu::DevMem row_ptr;       // canonical CSR (reference order), int32/int64 [n+1]
+    chebgpu::DevMem col;           // int32 [nnz]
+    chebgpu::DevMem inv;           // double [n] iff inv_array
+    chebgpu::SolverView view;
+    chebgpu::Workspace ws;
+    chebgpu::StagedState staged;
+    double last_loop_ms = 0.0;
+    int last_terms = 0;
+    int last_launches = 0;
+    ~cheb_graph();
+};
+
+namespace chebgpu {
+// build.cu
+void build_from_edges(cheb_graph* g, const void* d_edges, int64_t E, int edge_bits,
+                      const cheb_build_opts& o);
+void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors, int64_t n,
+                int64_t nnz, const double* inv_degree);
+void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees);
+void ensure_view(cheb_graph* g);
+void finalize_stats(cheb_graph* g);
+
+// coeffs.cpp (host coefficient kit, coefficients.cpp semantics)
+double beta(double c);
+double sigma(double c);
+double err_bound(double c, int M);
+int plan_iterations(double c, double eps, double* predicted);
+void coefficients(double c, int M, std::vector<double>& out, double* beta_out, double* c0_out);
+int resolve_rounds(double c, int rounds, double eps, int max_rounds);
+double kahan_sum(const double* x, int64_t n);
+
+// cpaa.cu
+struct SolveSpec {
+    double c = 0.85;
+    int M = 0;
+    int mode = CHEB_MODE_FAST;
+    int precision = CHEB_FP64;
+    int R = 1;
+    const double* p = nullptr;  // host n*R or null
+    bool trace = true;
+};
+// Runs the solve on the device; results stay in g->ws (out = ranks in original order).
+// Fills trace (M rows of mass_T,S_k) and total on the host; throws on non-finite.
+void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool host_results, std::vector<double>* tr,
+                double* total);
+void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
+                    std::vector<double>* errs, double* total);
+void read_ranks(cheb_graph* g, int precision, double* ranks);
+void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_ms);
+void power_solve(cheb_graph* g, double c, int rounds, double tol, int max_rounds, int mode,
+                 const double* reference, double* ranks, cheb_trace_row* trace, int cap,
+                 int* rounds_out, double* total);
+void transition_apply(cheb_graph* g, const double* x, double* y, int mode);
+void staged_init(cheb_graph* g, double c0, int mode);
+void staged_set(cheb_graph* g, const double* Tp, const double* Tc, const double* acc, int k);
+void staged_generate(cheb_graph* g);
+void staged_accumulate(cheb_graph* g, double ck);
+void staged_rotate(cheb_graph* g);
+void staged_get(cheb_graph* g, double* Tp, double* Tc, double* Tn, double* acc, int* k);
+}  // namespace chebgpu

@@ -1,0 +1,1133 @@
+// K2/K3/K4/K6/K7 — the CPAA term kernels and their drivers.
+//
+// The reference round (/root/reference/proj/src/cpaa.cpp:109-156) is a pre-scale
+// pass contrib = T_k * D^-1 (:116), a CSR gather with the three-term recurrence
+// T_{k+1} = (k==1 ? s : 2s - T_{k-1}) and the coefficient accumulation
+// acc += c_k T_{k+1} (:126-132), two serial Kahan trace sums (:142-143) and a
+// finite check (:147-148).  Here ONE kernel per term does all of it:
+//
+//   s_u      = sum_{v in N(u)} x_k[v]                (degree-binned gather)
+//   t        = first ? s_u : 2 s_u - T_{k-1}[u]      (recurrence, in place over T_{k-1})
+//   acc[u]  += c_k * t                               (separate mul/add: reference rounding)
+//   x_{k+1}[u] = t * (1/deg u)                       (next term's D^-1 pre-scale, fused)
+//   block partials of sum(t), sum(acc)               (trace, fixed order, deterministic)
+//
+// Two schedules:
+//  * FAST (the product path): rows relabelled by degree (descending) so every bin is
+//    a contiguous row range; vector-per-row (1..16 lanes), warp-per-row (32 lanes,
+//    unrolled), block-per-row, and hub rows split in chunks combined by the last
+//    arriving CTA in fixed chunk order.  Sums differ from the reference only in
+//    association order (<= 1e-12 max-abs, checked by tests).
+//  * BITEXACT: thread-per-row storage-order sums on the reference-order CSR, explicit
+//    round-to-nearest mul/add, serial device Kahan for the trace: bitwise equal to
+//    the reference (ranks and trace).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+
+namespace chebgpu {
+
+enum Epi : int {
+    EPI_CPAA = 0,   // fused CPAA term (cpaa.cpp:126-132 + :116 for the next round)
+    EPI_GEN = 1,    // staged generate_stage (cpaa.cpp:178-190): T_next only
+    EPI_POWER = 2,  // power round (power.cpp:60-86): y = c s + base
+    EPI_PLAIN = 3   // transition_apply (graph.cpp:104-121): y = s
+};
+
+struct BinTable {
+    Bin b[kMaxBins];
+    int nb;
+};
+
+template <class RP, class V>
+struct TermArgs {
+    const RP* __restrict__ rp;
+    const int* __restrict__ col;
+    const double* __restrict__ inv;  // non-null iff non-canonical inv_degree
+    const V* __restrict__ x_in;      // x_k = T_k D^-1
+    V* __restrict__ x_out;           // x_{k+1}
+    V* T;                            // CPAA: T_{k-1} in, T_{k+1} out (in place); POWER: x in/out
+    const V* T_prev;                 // GEN: T_{k-1}
+    V* out;                          // GEN: T_next; PLAIN: y
+    V* acc;
+    double ck;    // CPAA: c_k ; POWER: c
+    double base;  // POWER: (1-c)/n
+    int first;
+    double* part;  // [grid][2] this term
+    const int* chunk_row;
+    const int* chunk_idx;
+    const int* hub_first;
+    double* hub_part;
+    unsigned* hub_cnt;
+    double* hub_ts;  // [n_hub][2] this term
+};
+
+// ---------------- arithmetic helpers (reference rounding, no contraction) -------------
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double rcp_rn(double d) { return __drcp_rn(d); }
+__device__ __forceinline__ float rcp_rn(float d) { return __frcp_rn(d); }
+
+template <class V>
+__device__ __forceinline__ V ldg_x(const V* p) { return __ldg(p); }
+__device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fixed-order block reduction; result valid in thread 0.  sh >= 32 doubles.
+template <class T>
+__device__ __forceinline__ T block_sum(T v, T* sh) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) sh[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? sh[lane] : T(0);
+        v = warp_sum(v);
+    }
+    __syncthreads();
+    return v;
+}
+
+// Row epilogue.  u is a row of the current layout; deg its row length.
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void epilogue(const TermArgs<RP, V>& a, int64_t u, V s, int64_t deg,
+                                         double& p0, double& p1) {
+    if constexpr (EPI == EPI_PLAIN) {
+        a.out[u] = s;
+    } else {
+        const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
+        if constexpr (EPI == EPI_CPAA) {
+            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), a.T[u]);
+            a.T[u] = t;
+            const V nacc = add_rn(a.acc[u], mul_rn((V)a.ck, t));
+            a.acc[u] = nacc;
+            a.x_out[u] = mul_rn(t, inv);
+            p0 += (double)t;
+            p1 += (double)nacc;
+        } else if constexpr (EPI == EPI_GEN) {
+            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), a.T_prev[u]);
+            a.out[u] = t;
+        } else {  // EPI_POWER
+            const V y = add_rn(mul_rn((V)a.ck, s), (V)a.base);
+            const V old = a.T[u];
+            a.T[u] = y;
+            a.x_out[u] = mul_rn(y, inv);
+            p0 += fabs((double)y - (double)old);
+            p1 += (double)y;
+        }
+    }
+}
+
+// ---------------- FAST: degree-binned schedule ----------------------------------------
+
+// L lanes per row, L in {1,2,4,8,16,32}; rows interleaved over the bin's CTAs.
+template <int L, int EPI, class RP, class V>
+__device__ __forceinline__ void vec_rows(const TermArgs<RP, V>& a, const Bin& bin, double& p0,
+                                         double& p1) {
+    constexpr int G = kThreads / L;
+    const int g = threadIdx.x / L, lane = threadIdx.x % L;
+    const unsigned mask = L == 32 ? 0xffffffffu
+                                  : (((1u << L) - 1u) << ((threadIdx.x & 31) / L * L));
+    const int64_t rows = bin.row_end - bin.row_begin;
+    const int64_t stride = (int64_t)bin.nblocks * G;
+    for (int64_t i = (int64_t)(blockIdx.x - bin.block_begin) * G + g; i < rows; i += stride) {
+        const int64_t u = bin.row_begin + i;
+        const int64_t b = a.rp[u], e = a.rp[u + 1];
+        V s = V(0);
+        int64_t j = b + lane;
+        if constexpr (L == 32) {
+            // 4 independent index loads then 4 gathers in flight per lane
+            for (; j + 3 * L < e; j += 4 * L) {
+                const int c0 = ld_stream(a.col + j), c1 = ld_stream(a.col + j + L);
+                const int c2 = ld_stream(a.col + j + 2 * L), c3 = ld_stream(a.col + j + 3 * L);
+                const V v0 = ldg_x(a.x_in + c0), v1 = ldg_x(a.x_in + c1);
+                const V v2 = ldg_x(a.x_in + c2), v3 = ldg_x(a.x_in + c3);
+                s += v0;
+                s += v1;
+                s += v2;
+                s += v3;
+            }
+        }
+        for (; j < e; j += L) s += ldg_x(a.x_in + ld_stream(a.col + j));
+        if constexpr (L > 1) {
+#pragma unroll
+            for (int o = L / 2; o; o >>= 1) s += __shfl_xor_sync(mask, s, o, L);
+        }
+        if (lane == 0) epilogue<EPI>(a, u, s, e - b, p0, p1);
+    }
+}
+
+// One CTA per row (degree in (kBlockDeg, kHubDeg]).
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void block_rows(const TermArgs<RP, V>& a, const Bin& bin, double& p0,
+                                           double& p1, V* sh) {
+    for (int64_t u = bin.row_begin + (blockIdx.x - bin.block_begin); u < bin.row_end;
+         u += bin.nblocks) {
+        const int64_t b = a.rp[u], e = a.rp[u + 1];
+        V s = V(0);
+        int64_t j = b + threadIdx.x;
+        for (; j + 3 * kThreads < e; j += 4 * kThreads) {
+            const int c0 = ld_stream(a.col + j), c1 = ld_stream(a.col + j + kThreads);
+            const int c2 = ld_stream(a.col + j + 2 * kThreads), c3 = ld_stream(a.col + j + 3 * kThreads);
+            const V v0 = ldg_x(a.x_in + c0), v1 = ldg_x(a.x_in + c1);
+            const V v2 = ldg_x(a.x_in + c2), v3 = ldg_x(a.x_in + c3);
+            s += v0;
+            s += v1;
+            s += v2;
+            s += v3;
+        }
+        for (; j < e; j += kThreads) s += ldg_x(a.x_in + ld_stream(a.col + j));
+        s = block_sum(s, sh);
+        if (threadIdx.x == 0) epilogue<EPI>(a, u, s, e - b, p0, p1);
+    }
+}
+
+// Hub rows: one CTA per chunk of kHubChunk nnz; the last CTA of a row to arrive
+// combines the chunk partials in chunk order (deterministic) and runs the epilogue.
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void hub_chunk(const TermArgs<RP, V>& a, const Bin& bin, V* sh) {
+    constexpr int64_t kChunk = 8192;
+    const int c = bin.chunk_begin + (blockIdx.x - bin.block_begin);
+    const int h = a.chunk_row[c];
+    const int64_t rb = a.rp[h], re = a.rp[h + 1];
+    const int64_t b = rb + (int64_t)a.chunk_idx[c] * kChunk;
+    const int64_t e = min(re, b + kChunk);
+    V s = V(0);
+    int64_t j = b + threadIdx.x;
+    for (; j + 3 * kThreads < e; j += 4 * kThreads) {
+        const int c0 = ld_stream(a.col + j), c1 = ld_stream(a.col + j + kThreads);
+        const int c2 = ld_stream(a.col + j + 2 * kThreads), c3 = ld_stream(a.col + j + 3 * kThreads);
+        const V v0 = ldg_x(a.x_in + c0), v1 = ldg_x(a.x_in + c1);
+        const V v2 = ldg_x(a.x_in + c2), v3 = ldg_x(a.x_in + c3);
+        s += v0;
+        s += v1;
+        s += v2;
+        s += v3;
+    }
+    for (; j < e; j += kThreads) s += ldg_x(a.x_in + ld_stream(a.col + j));
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) {
+        a.hub_part[c] = (double)s;
+        __threadfence();
+        const int f0 = a.hub_first[h], f1 = a.hub_first[h + 1];
+        const unsigned prev = atomicAdd(&a.hub_cnt[h], 1u);
+        if (prev == (unsigned)(f1 - f0 - 1)) {
+            __threadfence();
+            V tot = V(0);
+            for (int q = f0; q < f1; ++q) tot += (V)__ldcg(a.hub_part + q);
+            a.hub_cnt[h] = 0u;
+            double q0 = 0.0, q1 = 0.0;
+            epilogue<EPI>(a, h, tot, re - rb, q0, q1);
+            if (a.hub_ts) {
+                a.hub_ts[2 * h] = q0;
+                a.hub_ts[2 * h + 1] = q1;
+            }
+        }
+    }
+}
+
+template <int EPI, class RP, class V>
+__global__ void __launch_bounds__(kThreads) k_term_fast(TermArgs<RP, V> a, BinTable bt) {
+    __shared__ V sh[32];
+    __shared__ double shd[32];
+    int bi = 0;
+    while (bi + 1 < bt.nb && (int)blockIdx.x >= bt.b[bi + 1].block_begin) ++bi;
+    const Bin bin = bt.b[bi];
+    double p0 = 0.0, p1 = 0.0;
+    if (bin.kind == BIN_HUB) {
+        hub_chunk<EPI>(a, bin, sh);
+    } else if (bin.kind == BIN_BLOCK) {
+        block_rows<EPI>(a, bin, p0, p1, sh);
+    } else {
+        switch (bin.lanes) {
+            case 32: vec_rows<32, EPI>(a, bin, p0, p1); break;
+            case 16: vec_rows<16, EPI>(a, bin, p0, p1); break;
+            case 8: vec_rows<8, EPI>(a, bin, p0, p1); break;
+            case 4: vec_rows<4, EPI>(a, bin, p0, p1); break;
+            case 2: vec_rows<2, EPI>(a, bin, p0, p1); break;
+            default: vec_rows<1, EPI>(a, bin, p0, p1); break;
+        }
+    }
+    if constexpr (EPI == EPI_CPAA || EPI == EPI_POWER) {
+        if (a.part) {
+            p0 = block_sum(p0, shd);
+            p1 = block_sum(p1, shd);
+            if (threadIdx.x == 0) {
+                a.part[2 * blockIdx.x] = p0;
+                a.part[2 * blockIdx.x + 1] = p1;
+            }
+        }
+    }
+}
+
+// ---------------- BITEXACT: thread per row, storage order ----------------------------
+template <int EPI, class RP>
+__global__ void __launch_bounds__(kThreads) k_term_exact(TermArgs<RP, double> a, int64_t n) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = a.rp[u], e = a.rp[u + 1];
+        double s = 0.0;
+        for (int64_t j = b; j < e; ++j) s = __dadd_rn(s, a.x_in[a.col[j]]);
+        double p0 = 0.0, p1 = 0.0;
+        epilogue<EPI>(a, u, s, e - b, p0, p1);
+    }
+}
+
+// Serial Kahan sums exactly as graph.cpp:10-19 (single thread: bit-identical order).
+__global__ void k_kahan2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
+                         double* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double a = __dsub_rn(x[i], c0);
+        double t = __dadd_rn(s0, a);
+        c0 = __dsub_rn(__dsub_rn(t, s0), a);
+        s0 = t;
+        if (y) {
+            double b = __dsub_rn(y[i], c1);
+            double u = __dadd_rn(s1, b);
+            c1 = __dsub_rn(__dsub_rn(u, s1), b);
+            s1 = u;
+        }
+    }
+    out[0] = s0;
+    out[1] = s1;
+}
+
+// Power-method L1 change + mass with the reference's Kahan order (power.cpp:80-93).
+__global__ void k_kahan_l1(const double* __restrict__ y, const double* __restrict__ x, int64_t n,
+                           double* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double l1 = 0.0, comp = 0.0, s = 0.0, c = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double d = __dsub_rn(fabs(__dsub_rn(y[i], x[i])), comp);
+        double t = __dadd_rn(l1, d);
+        comp = __dsub_rn(__dsub_rn(t, l1), d);
+        l1 = t;
+        double a = __dsub_rn(y[i], c);
+        double u = __dadd_rn(s, a);
+        c = __dsub_rn(__dsub_rn(u, s), a);
+        s = u;
+    }
+    out[0] = l1;
+    out[1] = s;
+}
+
+// ---------------- init / reductions / normalisation ----------------------------------
+// T_{-1} = T_0 = p (or 1), acc = (c0/2) T_0, x_0 = T_0 D^-1   (cpaa.cpp:88-92, :116 at k=1)
+template <class RP, class V>
+__global__ void k_init(const RP* __restrict__ rp, const double* __restrict__ inv,
+                       const double* __restrict__ p, const int* __restrict__ order, int64_t n,
+                       double half_c0, V* __restrict__ T0, V* __restrict__ T1, V* __restrict__ acc,
+                       V* __restrict__ x0) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const V t0 = p ? (V)p[order ? order[u] : u] : V(1);
+        T0[u] = t0;
+        T1[u] = t0;
+        acc[u] = p ? mul_rn((V)half_c0, t0) : (V)half_c0;
+        const V iv = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
+        x0[u] = mul_rn(t0, iv);
+    }
+}
+
+// trace[k] = sum of block partials (+ hub partials) of term k, fixed order.
+__global__ void k_trace_reduce(const double* __restrict__ part, int grid, const double* __restrict__ hub_ts,
+                               int n_hub, int k_first, double* __restrict__ trace) {
+    __shared__ double sh[32];
+    const int k = k_first + blockIdx.x;
+    const double* pk = part + (size_t)k * grid * 2;
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < grid; i += blockDim.x) {
+        a += pk[2 * i];
+        b += pk[2 * i + 1];
+    }
+    if (hub_ts) {
+        const double* hk = hub_ts + (size_t)k * n_hub * 2;
+        for (int i = threadIdx.x; i < n_hub; i += blockDim.x) {
+            a += hk[2 * i];
+            b += hk[2 * i + 1];
+        }
+    }
+    a = block_sum(a, sh);
+    b = block_sum(b, sh);
+    if (threadIdx.x == 0) {
+        trace[2 * k] = a;
+        trace[2 * k + 1] = b;
+    }
+}
+
+template <class V>
+__global__ void k_sum_blocks(const V* __restrict__ x, int64_t n, double* __restrict__ part) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a += (double)x[i];
+    a = block_sum(a, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = a;
+}
+
+__global__ void k_sum_final(const double* __restrict__ part, int cnt, double* __restrict__ out) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) a += part[i];
+    a = block_sum(a, sh);
+    if (threadIdx.x == 0) *out = a;
+}
+
+// ranks[order[u]] = acc[u] / total   (cpaa.cpp:159-163)
+template <class V>
+__global__ void k_normalize(const V* __restrict__ acc, const int* __restrict__ order, int64_t n,
+                            const double* __restrict__ total, V* __restrict__ out) {
+    const double tot = *total;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const V r = (V)((double)acc[u] / tot);
+        out[order ? order[u] : u] = r;
+    }
+}
+
+template <class V>
+__global__ void k_permute_in(const double* __restrict__ src, const int* __restrict__ order, int64_t n,
+                             V* __restrict__ dst) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x)
+        dst[u] = (V)src[order ? order[u] : u];
+}
+
+template <class V>
+__global__ void k_permute_out(const V* __restrict__ src, const int* __restrict__ order, int64_t n,
+                              double* __restrict__ dst) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x)
+        dst[order ? order[u] : u] = (double)src[u];
+}
+
+// x = T D^-1 (staged API / transition_apply pre-scale)
+template <class RP, class V>
+__global__ void k_prescale(const RP* __restrict__ rp, const double* __restrict__ inv,
+                           const V* __restrict__ T, int64_t n, V* __restrict__ x) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const V iv = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
+        x[u] = mul_rn(T[u], iv);
+    }
+}
+
+// acc += c_k T_next (cpaa.cpp:192-194)
+template <class V>
+__global__ void k_accumulate(V* __restrict__ acc, const V* __restrict__ Tn, int64_t n, double ck) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x)
+        acc[u] = add_rn(acc[u], mul_rn((V)ck, Tn[u]));
+}
+
+// Per-round error vs a reference (metrics.cpp:12-30 via cpaa.cpp:149-154):
+// est = acc / S_k ; max |est-ref|/ref and sum |est-ref|.  ref in the same layout.
+template <class V>
+__global__ void k_err(const V* __restrict__ acc, const double* __restrict__ ref, int64_t n,
+                      const double* __restrict__ S, int by_S, double* __restrict__ part) {
+    __shared__ double sh[32];
+    const double tot = by_S ? *S : 1.0;
+    double mx = 0.0, l1 = 0.0;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const double est = by_S ? (double)acc[u] / tot : (double)acc[u];
+        const double d = fabs(est - ref[u]);
+        mx = fmax(mx, d / ref[u]);
+        l1 += d;
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
+        part[2 * blockIdx.x] = mx;
+    }
+    __syncthreads();
+    l1 = block_sum(l1, sh);
+    if (threadIdx.x == 0) part[2 * blockIdx.x + 1] = l1;
+}
+
+__global__ void k_err_final(const double* __restrict__ part, int cnt, double* __restrict__ out) {
+    __shared__ double sh[32];
+    double mx = 0.0, l1 = 0.0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        mx = fmax(mx, part[2 * i]);
+        l1 += part[2 * i + 1];
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
+        out[0] = mx;
+    }
+    __syncthreads();
+    l1 = block_sum(l1, sh);
+    if (threadIdx.x == 0) out[1] = l1;
+}
+
+// =====================================================================================
+// Host drivers
+// =====================================================================================
+namespace {
+
+inline int grid1d(int64_t n) {
+    int64_t b = (n + kThreads - 1) / kThreads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+BinTable bin_table(const SolverView& V) {
+    BinTable t{};
+    t.nb = (int)V.bins.size();
+    for (int i = 0; i < t.nb; ++i) t.b[i] = V.bins[i];
+    return t;
+}
+
+// Layout the solve runs on: FAST -> degree-binned view; BITEXACT -> reference order.
+struct Layout {
+    bool fast;
+    bool rp64;
+    const void* rp;
+    const int* col;
+    const double* inv;
+    const int* order;  // new -> old (fast) or null
+};
+
+Layout layout_of(cheb_graph* g, int mode) {
+    Layout L{};
+    if (mode == CHEB_MODE_FAST) {
+        ensure_view(g);
+        L.fast = true;
+        L.rp64 = g->view.rp64;
+        L.rp = g->view.row_ptr.get();
+        L.col = g->view.col.ptr<int>();
+        L.inv = g->inv_array ? g->view.inv.ptr<double>() : nullptr;
+        L.order = g->view.order.ptr<int>();
+    } else {
+        L.fast = false;
+        L.rp64 = g->rp64;
+        L.rp = g->row_ptr.get();
+        L.col = g->col.ptr<int>();
+        L.inv = g->inv_array ? g->inv.ptr<double>() : nullptr;
+        L.order = nullptr;
+    }
+    return L;
+}
+
+template <class RP, class V>
+TermArgs<RP, V> base_args(cheb_graph* g, const Layout& L) {
+    TermArgs<RP, V> a{};
+    a.rp = static_cast<const RP*>(L.rp);
+    a.col = L.col;
+    a.inv = L.inv;
+    if (L.fast) {
+        a.chunk_row = g->view.chunk_row.ptr<int>();
+        a.chunk_idx = g->view.chunk_idx.ptr<int>();
+        a.hub_first = g->view.hub_first.ptr<int>();
+    }
+    return a;
+}
+
+// Launch one SpMV-shaped pass with epilogue EPI on the given layout.
+template <int EPI, class RP, class V>
+int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
+    cudaStream_t st = g->stream;
+    if (L.fast) {
+        k_term_fast<EPI, RP, V><<<g->view.grid, kThreads, 0, st>>>(a, bin_table(g->view));
+    } else {
+        if constexpr (std::is_same<V, double>::value) {
+            k_term_exact<EPI, RP><<<grid1d(g->n), kThreads, 0, st>>>(a, g->n);
+        } else {
+            fail(CHEB_INVALID_ARG, "bitexact mode is fp64 only");
+        }
+    }
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    return 1;
+}
+
+template <class V>
+void ensure_workspace(cheb_graph* g, int M, int R) {
+    Workspace& w = g->ws;
+    const int64_t n = g->n;
+    // Any reallocation invalidates the captured solve graph (it bakes in addresses).
+    const void* before[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
+                            w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
+                            w.trace.get(), w.total.get()};
+    const size_t vb = sizeof(V) * (size_t)std::max<int64_t>(n, 1) * R;
+    w.T0.ensure(vb);
+    w.T1.ensure(vb);
+    w.X0.ensure(vb);
+    w.X1.ensure(vb);
+    w.acc.ensure(vb);
+    w.out.ensure(vb);
+    const int grid = std::max(g->view.ready ? g->view.grid : 1, grid1d(n));
+    w.part.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max(grid, 1));
+    w.hub_part.ensure(sizeof(double) * std::max(g->view.n_chunks, 1));
+    if (!w.hub_cnt || w.hub_cnt.bytes() < sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1)) {
+        w.hub_cnt.alloc(sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1));
+        CHEB_CUDA_CHECK(cudaMemset(w.hub_cnt.get(), 0, w.hub_cnt.bytes()));
+    }
+    w.hub_ts.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max<int64_t>(g->view.n_hub, 1));
+    w.trace.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1));
+    w.total.ensure(sizeof(double) * 4);
+    w.n = n;
+    w.R = R;
+    w.vbytes = sizeof(V);
+    const void* after[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
+                           w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
+                           w.trace.get(), w.total.get()};
+    if (std::memcmp(before, after, sizeof before) != 0) {
+        if (w.exec) cudaGraphExecDestroy(w.exec);
+        w.exec = nullptr;
+        w.exec_key.clear();
+        w.seen_key.clear();
+    }
+}
+
+// Enqueue the whole solve: init, M fused terms, trace reduction, normalisation.
+template <class RP, class V>
+int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std::vector<double>& coeffs,
+                  double c0, const double* d_p, const double* d_ref, double* d_err,
+                  std::vector<cudaEvent_t>* term_ev = nullptr) {
+    cudaStream_t st = g->stream;
+    Workspace& w = g->ws;
+    const int64_t n = g->n;
+    const int M = s.M;
+    int launches = 0;
+    V* T[2] = {w.T0.ptr<V>(), w.T1.ptr<V>()};
+    V* X[2] = {w.X0.ptr<V>(), w.X1.ptr<V>()};
+    V* acc = w.acc.ptr<V>();
+    double* trace = w.trace.ptr<double>();
+    const int grid = L.fast ? g->view.grid : 0;
+
+    k_init<RP, V><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, d_p, L.order, n,
+                                                  c0 / 2.0, T[0], T[1], acc, X[0]);
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    ++launches;
+    const bool per_term_reduce = d_ref != nullptr || !L.fast;
+    for (int k = 1; k <= M; ++k) {
+        TermArgs<RP, V> a = base_args<RP, V>(g, L);
+        a.x_in = X[(k - 1) & 1];
+        a.x_out = X[k & 1];
+        a.T = T[(k - 1) & 1];  // holds T_{k-1}; receives T_{k+1}
+        a.acc = acc;
+        a.ck = coeffs[k];
+        a.first = k == 1;
+        if (L.fast) {
+            a.part = w.part.ptr<double>() + (size_t)(k - 1) * grid * 2;
+            a.hub_part = w.hub_part.ptr<double>();
+            a.hub_cnt = w.hub_cnt.ptr<unsigned>();
+            a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() + (size_t)(k - 1) * g->view.n_hub * 2 : nullptr;
+        }
+        if (term_ev) CHEB_CUDA_CHECK(cudaEventRecord((*term_ev)[2 * (k - 1)], st));
+        launches += launch_pass<EPI_CPAA>(g, L, a);
+        if (term_ev) CHEB_CUDA_CHECK(cudaEventRecord((*term_ev)[2 * (k - 1) + 1], st));
+        if (!L.fast) {
+            // trace sums exactly as the reference: Kahan(T_curr), Kahan(acc)
+            k_kahan2<<<1, 32, 0, st>>>(reinterpret_cast<const double*>(a.T),
+                                       reinterpret_cast<const double*>(acc), n, trace + 2 * (k - 1));
+            CHEB_CUDA_CHECK(cudaGetLastError());
+            ++launches;
+        } else if (per_term_reduce) {
+            k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
+                                                   (int)g->view.n_hub, k - 1, trace);
+            CHEB_CUDA_CHECK(cudaGetLastError());
+            ++launches;
+        }
+        if (d_ref) {
+            const int eg = grid1d(n);
+            double* ep = w.part.ptr<double>();  // reuse: partials of this term are consumed
+            (void)ep;
+            k_err<V><<<eg, kThreads, 0, st>>>(acc, d_ref, n, trace + 2 * (k - 1) + 1, 1, d_err + 4 * (size_t)M);
+            k_err_final<<<1, kThreads, 0, st>>>(d_err + 4 * (size_t)M, eg, d_err + 2 * (size_t)(k - 1));
+            CHEB_CUDA_CHECK(cudaGetLastError());
+            launches += 2;
+        }
+    }
+    if (L.fast && !per_term_reduce && M > 0) {
+        k_trace_reduce<<<M, kThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
+                                               (int)g->view.n_hub, 0, trace);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+    }
+    // normalisation total: last S_k, or sum(acc) when M == 0 (cpaa.cpp:158-159)
+    const double* d_total;
+    if (M > 0) {
+        d_total = trace + 2 * (M - 1) + 1;
+    } else {
+        double* tot = w.total.ptr<double>();
+        if (L.fast) {
+            const int eg = grid1d(n);
+            k_sum_blocks<V><<<eg, kThreads, 0, st>>>(acc, n, w.part.ptr<double>());
+            k_sum_final<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), eg, tot);
+            launches += 2;
+        } else {
+            k_kahan2<<<1, 32, 0, st>>>(reinterpret_cast<const double*>(acc), nullptr, n, tot);
+            ++launches;
+        }
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        d_total = tot;
+    }
+    k_normalize<V><<<grid1d(n), kThreads, 0, st>>>(acc, L.order, n, d_total, w.out.ptr<V>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    ++launches;
+    return launches;
+}
+
+std::string solve_key(const SolveSpec& s, bool has_p) {
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "c=%.17g M=%d mode=%d prec=%d R=%d p=%d", s.c, s.M, s.mode,
+                  s.precision, s.R, has_p ? 1 : 0);
+    return buf;
+}
+
+template <class RP, class V>
+void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
+                 std::vector<double>* errs, double* total) {
+    cudaStream_t st = g->stream;
+    const Layout L = layout_of(g, s.mode);
+    ensure_workspace<V>(g, s.M, 1);
+    Workspace& w = g->ws;
+    const int64_t n = g->n;
+    std::vector<double> coeffs;
+    double beta_v, c0;
+    coefficients(s.c, s.M, coeffs, &beta_v, &c0);
+
+    // personalisation vector (host -> device scratch; permuted by the init kernel)
+    DevMem d_p;
+    if (s.p) {
+        d_p.alloc(sizeof(double) * n);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(d_p.get(), s.p, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    }
+    DevMem d_ref, d_err;
+    if (h_ref) {
+        d_ref.alloc(sizeof(double) * n);
+        DevMem tmp(sizeof(double) * n);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(tmp.get(), h_ref, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        k_permute_in<double><<<grid1d(n), kThreads, 0, st>>>(tmp.ptr<double>(), L.order, n, d_ref.ptr<double>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        d_err.alloc(sizeof(double) * (2 * (size_t)std::max(s.M, 1) + 2 * (size_t)grid1d(n) + 4 * (size_t)s.M + 8));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+
+    CHEB_CUDA_CHECK(cudaEventRecord(g->ev0, st));
+    if (!h_ref) {
+        // Replay a CUDA graph of the whole solve (captured once per configuration).
+        const std::string key = solve_key(s, s.p != nullptr) + (L.fast ? " fast" : " exact");
+        if (w.exec && w.exec_key == key && !s.p) {
+            CHEB_CUDA_CHECK(cudaGraphLaunch(w.exec, st));
+        } else if (s.p || w.seen_key != key) {
+            // First solve of this configuration (or p's device address changes per call):
+            // plain launches; a repeat of the same configuration is captured once.
+            w.launches = enqueue_solve<RP, V>(g, L, s, coeffs, c0, d_p ? d_p.ptr<double>() : nullptr,
+                                              nullptr, nullptr);
+            w.seen_key = s.p ? std::string() : key;
+        } else {
+            if (w.exec) {
+                cudaGraphExecDestroy(w.exec);
+                w.exec = nullptr;
+            }
+            cudaGraph_t graph;
+            CHEB_CUDA_CHECK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            int launches = 0;
+            try {
+                launches = enqueue_solve<RP, V>(g, L, s, coeffs, c0, nullptr, nullptr, nullptr);
+            } catch (...) {
+                cudaStreamEndCapture(st, &graph);
+                throw;
+            }
+            CHEB_CUDA_CHECK(cudaStreamEndCapture(st, &graph));
+            CHEB_CUDA_CHECK(cudaGraphInstantiate(&w.exec, graph, 0));
+            cudaGraphDestroy(graph);
+            w.exec_key = key;
+            w.launches = launches;
+            CHEB_CUDA_CHECK(cudaGraphLaunch(w.exec, st));
+        }
+    } else {
+        w.launches = enqueue_solve<RP, V>(g, L, s, coeffs, c0, d_p ? d_p.ptr<double>() : nullptr,
+                                          d_ref.ptr<double>(), d_err.ptr<double>());
+    }
+    CHEB_CUDA_CHECK(cudaEventRecord(g->ev1, st));
+    g->last_terms = s.M;
+    g->last_launches = w.launches;
+
+    if (tr || total || errs) {
+        std::vector<double> t(2 * (size_t)std::max(s.M, 1));
+        double tot = 0.0;
+        if (s.M > 0)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), w.trace.get(), sizeof(double) * 2 * s.M,
+                                            cudaMemcpyDeviceToHost, st));
+        else
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(&tot, w.total.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+        if (errs && h_ref) {
+            errs->assign(2 * (size_t)std::max(s.M, 1), 0.0);
+            if (s.M > 0)
+                CHEB_CUDA_CHECK(cudaMemcpyAsync(errs->data(), d_err.get(), sizeof(double) * 2 * s.M,
+                                                cudaMemcpyDeviceToHost, st));
+        }
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+        g->last_loop_ms = ms;
+        // first non-finite round wins (cpaa.cpp:147-148)
+        for (int k = 1; k <= s.M; ++k)
+            if (!std::isfinite(t[2 * (k - 1)]) || !std::isfinite(t[2 * (k - 1) + 1]))
+                fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(k));
+        if (s.M > 0) tot = t[2 * (s.M - 1) + 1];
+        if (!std::isfinite(tot) || tot <= 0.0)
+            fail(CHEB_NUMERIC, "normalization total is not positive and finite");
+        if (tr) *tr = t;
+        if (total) *total = tot;
+    }
+}
+
+}  // namespace
+
+void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool /*host_results*/, std::vector<double>* tr,
+                double* total) {
+    DeviceGuard dg(g->device);
+    if (s.R != 1) fail(CHEB_INVALID_ARG, "R > 1 is served by the batched path");
+    if (s.mode == CHEB_MODE_BITEXACT && s.precision != CHEB_FP64)
+        fail(CHEB_INVALID_ARG, "bitexact mode is fp64 only");
+    const bool rp64 = s.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
+    if (s.precision == CHEB_FP64) {
+        if (rp64) run_solve_t<int64_t, double>(g, s, nullptr, tr, nullptr, total);
+        else run_solve_t<int, double>(g, s, nullptr, tr, nullptr, total);
+    } else {
+        if (rp64) run_solve_t<int64_t, float>(g, s, nullptr, tr, nullptr, total);
+        else run_solve_t<int, float>(g, s, nullptr, tr, nullptr, total);
+    }
+}
+
+// With reference tracking (err / err_l1 columns): plain launches, per-term reduction.
+void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
+                    std::vector<double>* errs, double* total) {
+    DeviceGuard dg(g->device);
+    const bool rp64 = s.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
+    if (s.precision == CHEB_FP64) {
+        if (rp64) run_solve_t<int64_t, double>(g, s, h_ref, tr, errs, total);
+        else run_solve_t<int, double>(g, s, h_ref, tr, errs, total);
+    } else {
+        if (rp64) run_solve_t<int64_t, float>(g, s, h_ref, tr, errs, total);
+        else run_solve_t<int, float>(g, s, h_ref, tr, errs, total);
+    }
+}
+
+// Per-term kernel durations (CUDA events around every term launch, plain launches).
+void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_ms) {
+    DeviceGuard dg(g->device);
+    const bool rp64 = s.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
+    auto run = [&](auto rp_tag, auto v_tag) {
+        using RP = decltype(rp_tag);
+        using V = decltype(v_tag);
+        const Layout L = layout_of(g, s.mode);
+        ensure_workspace<V>(g, s.M, 1);
+        std::vector<double> coeffs;
+        double b, c0;
+        coefficients(s.c, s.M, coeffs, &b, &c0);
+        std::vector<cudaEvent_t> ev(2 * (size_t)std::max(s.M, 1));
+        for (auto& e : ev) CHEB_CUDA_CHECK(cudaEventCreate(&e));
+        enqueue_solve<RP, V>(g, L, s, coeffs, c0, nullptr, nullptr, nullptr, &ev);
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+        term_ms.assign(s.M, 0.0);
+        for (int k = 0; k < s.M; ++k) {
+            float ms = 0.f;
+            CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, ev[2 * k], ev[2 * k + 1]));
+            term_ms[k] = ms;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+    };
+    if (s.precision == CHEB_FP64) {
+        if (rp64) run(int64_t(), double());
+        else run(int(), double());
+    } else {
+        if (rp64) run(int64_t(), float());
+        else run(int(), float());
+    }
+}
+
+// Read back ranks (original vertex order) as doubles.
+void read_ranks(cheb_graph* g, int precision, double* ranks) {
+    DeviceGuard dg(g->device);
+    const int64_t n = g->n;
+    if (precision == CHEB_FP64) {
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, g->ws.out.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream));
+    } else {
+        std::vector<float> tmp(n);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), g->ws.out.get(), sizeof(float) * n, cudaMemcpyDeviceToHost, g->stream));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+        for (int64_t i = 0; i < n; ++i) ranks[i] = tmp[i];
+    }
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+}
+
+// ---------------- Power method (power.cpp:28-109) -------------------------------------
+namespace {
+template <class RP>
+void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int mode,
+             const double* h_ref, double* ranks, cheb_trace_row* trace, int cap, int* rounds_out,
+             double* total) {
+    cudaStream_t st = g->stream;
+    const Layout L = layout_of(g, mode);
+    const int64_t n = g->n;
+    ensure_workspace<double>(g, std::max(budget, 1), 1);
+    Workspace& w = g->ws;
+    double* X = w.T0.ptr<double>();                 // x (in place)
+    double* C[2] = {w.X0.ptr<double>(), w.X1.ptr<double>()};
+    const double base = (1.0 - c) / (double)n;
+    const double x0 = 1.0 / (double)n;
+    {   // x = e/n, contrib = x D^-1
+        std::vector<double> h(n, x0);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(X, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        k_prescale<RP, double><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, X, n, C[0]);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    DevMem d_ref, d_err;
+    if (h_ref) {
+        d_ref.alloc(sizeof(double) * n);
+        DevMem tmp(sizeof(double) * n);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(tmp.get(), h_ref, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        k_permute_in<double><<<grid1d(n), kThreads, 0, st>>>(tmp.ptr<double>(), L.order, n, d_ref.ptr<double>());
+        d_err.alloc(sizeof(double) * (2 * (size_t)grid1d(n) + 8));
+    }
+    double* dtr = w.trace.ptr<double>();
+    const int grid = L.fast ? g->view.grid : 0;
+    int k = 0;
+    while (k < budget) {
+        ++k;
+        TermArgs<RP, double> a = base_args<RP, double>(g, L);
+        a.x_in = C[(k - 1) & 1];
+        a.x_out = C[k & 1];
+        a.T = X;
+        a.ck = c;
+        a.base = base;
+        a.first = 0;
+        if (L.fast) {
+            a.part = w.part.ptr<double>();
+            a.hub_part = w.hub_part.ptr<double>();
+            a.hub_cnt = w.hub_cnt.ptr<unsigned>();
+            a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() : nullptr;
+        }
+        if (!L.fast) {
+            // y goes to a separate buffer so the Kahan L1 sees old and new x (power.cpp:80-86)
+            a.T = w.acc.ptr<double>();
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(a.T, X, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            launch_pass<EPI_POWER>(g, L, a);
+            k_kahan_l1<<<1, 32, 0, st>>>(a.T, X, n, dtr);
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(X, a.T, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        } else {
+            launch_pass<EPI_POWER>(g, L, a);
+            k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub, 0, dtr);
+        }
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        double err2[2] = {0.0, 0.0};
+        if (h_ref) {
+            const int eg = grid1d(n);
+            k_err<double><<<eg, kThreads, 0, st>>>(X, d_ref.ptr<double>(), n, nullptr, 0, d_err.ptr<double>() + 4);
+            k_err_final<<<1, kThreads, 0, st>>>(d_err.ptr<double>() + 4, eg, d_err.ptr<double>());
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(err2, d_err.get(), sizeof err2, cudaMemcpyDeviceToHost, st));
+        }
+        double h[2];
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(h, dtr, sizeof h, cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (trace && k <= cap) {
+            cheb_trace_row& r = trace[k - 1];
+            std::memset(&r, 0, sizeof r);
+            r.k = k;
+            r.l1_change = h[0];
+            r.mass_T = h[1];
+            r.err = err2[0];
+            r.err_l1 = err2[1];
+        }
+        if (!std::isfinite(h[0])) fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(k));
+        if (by_tol && h[0] < tol) break;
+    }
+    // ranks = x (original order); total = Kahan(x) on the host (power.cpp:105-107)
+    std::vector<double> xs(n);
+    DevMem o(sizeof(double) * n);
+    k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(X, L.order, n, o.ptr<double>());
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, o.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    *rounds_out = k;
+    *total = kahan_sum(ranks, n);
+}
+}  // namespace
+
+void power_solve(cheb_graph* g, double c, int rounds, double tol, int max_rounds, int mode,
+                 const double* reference, double* ranks, cheb_trace_row* trace, int cap,
+                 int* rounds_out, double* total) {
+    DeviceGuard dg(g->device);
+    const bool fixed = rounds >= 0;
+    const int budget = fixed ? rounds : max_rounds;
+    const bool rp64 = mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
+    if (rp64) power_t<int64_t>(g, c, budget, !fixed, tol, mode, reference, ranks, trace, cap, rounds_out, total);
+    else power_t<int>(g, c, budget, !fixed, tol, mode, reference, ranks, trace, cap, rounds_out, total);
+}
+
+// ---------------- transition_apply (graph.cpp:104-121) --------------------------------
+namespace {
+template <class RP>
+void transition_t(cheb_graph* g, const double* x, double* y, int mode) {
+    cudaStream_t st = g->stream;
+    const Layout L = layout_of(g, mode);
+    const int64_t n = g->n;
+    ensure_workspace<double>(g, 1, 1);
+    Workspace& w = g->ws;
+    DevMem dx(sizeof(double) * n);
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(dx.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    k_permute_in<double><<<grid1d(n), kThreads, 0, st>>>(dx.ptr<double>(), L.order, n, w.T0.ptr<double>());
+    k_prescale<RP, double><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv,
+                                                          w.T0.ptr<double>(), n, w.X0.ptr<double>());
+    TermArgs<RP, double> a = base_args<RP, double>(g, L);
+    a.x_in = w.X0.ptr<double>();
+    a.out = w.T1.ptr<double>();
+    if (L.fast) {
+        a.hub_part = w.hub_part.ptr<double>();
+        a.hub_cnt = w.hub_cnt.ptr<unsigned>();
+    }
+    launch_pass<EPI_PLAIN>(g, L, a);
+    k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(w.T1.ptr<double>(), L.order, n, dx.ptr<double>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(y, dx.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+}  // namespace
+
+void transition_apply(cheb_graph* g, const double* x, double* y, int mode) {
+    DeviceGuard dg(g->device);
+    const bool rp64 = mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
+    if (rp64) transition_t<int64_t>(g, x, y, mode);
+    else transition_t<int>(g, x, y, mode);
+}
+
+// ---------------- staged API (cpaa.cpp:167-196) ---------------------------------------
+void staged_init(cheb_graph* g, double c0, int mode) {
+    DeviceGuard dg(g->device);
+    StagedState& S = g->staged;
+    const int64_t n = g->n;
+    const size_t vb = sizeof(double) * std::max<int64_t>(n, 1);
+    S.T_prev.ensure(vb);
+    S.T_curr.ensure(vb);
+    S.T_next.ensure(vb);
+    S.acc.ensure(vb);
+    S.x.ensure(vb);
+    S.mode = mode;
+    S.k = 1;
+    S.active = true;
+    std::vector<double> ones(n, 1.0), half(n, c0 / 2.0), zero(n, 0.0);
+    staged_set(g, ones.data(), ones.data(), half.data(), 1);
+    CHEB_CUDA_CHECK(cudaMemcpy(S.T_next.get(), zero.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+}
+
+void staged_set(cheb_graph* g, const double* Tp, const double* Tc, const double* acc, int k) {
+    DeviceGuard dg(g->device);
+    StagedState& S = g->staged;
+    if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
+    const Layout L = layout_of(g, S.mode);
+    const int64_t n = g->n;
+    DevMem tmp(sizeof(double) * std::max<int64_t>(n, 1));
+    auto put = [&](const double* h, DevMem& d) {
+        if (!h) return;
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(tmp.get(), h, sizeof(double) * n, cudaMemcpyHostToDevice, g->stream));
+        k_permute_in<double><<<grid1d(n), kThreads, 0, g->stream>>>(tmp.ptr<double>(), L.order, n, d.ptr<double>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+    };
+    put(Tp, S.T_prev);
+    put(Tc, S.T_curr);
+    put(acc, S.acc);
+    if (k > 0) S.k = k;
+}
+
+namespace {
+template <class RP>
+void staged_generate_t(cheb_graph* g) {
+    StagedState& S = g->staged;
+    const Layout L = layout_of(g, S.mode);
+    const int64_t n = g->n;
+    ensure_workspace<double>(g, 1, 1);
+    cudaStream_t st = g->stream;
+    // contrib = T_curr D^-1 (cpaa.cpp:180-182), then gather + recurrence (:183-189)
+    k_prescale<RP, double><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv,
+                                                          S.T_curr.ptr<double>(), n, S.x.ptr<double>());
+    TermArgs<RP, double> a = base_args<RP, double>(g, L);
+    a.x_in = S.x.ptr<double>();
+    a.T_prev = S.T_prev.ptr<double>();
+    a.out = S.T_next.ptr<double>();
+    a.first = S.k == 1;
+    if (L.fast) {
+        a.hub_part = g->ws.hub_part.ptr<double>();
+        a.hub_cnt = g->ws.hub_cnt.ptr<unsigned>();
+    }
+    launch_pass<EPI_GEN>(g, L, a);
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+}  // namespace
+
+void staged_generate(cheb_graph* g) {
+    DeviceGuard dg(g->device);
+    if (!g->staged.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
+    const bool rp64 = g->staged.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
+    if (rp64) staged_generate_t<int64_t>(g);
+    else staged_generate_t<int>(g);
+}
+
+void staged_accumulate(cheb_graph* g, double ck) {
+    DeviceGuard dg(g->device);
+    StagedState& S = g->staged;
+    if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
+    k_accumulate<double><<<grid1d(g->n), kThreads, 0, g->stream>>>(S.acc.ptr<double>(), S.T_next.ptr<double>(), g->n, ck);
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+}
+
+void staged_rotate(cheb_graph* g) {
+    StagedState& S = g->staged;
+    if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
+    std::swap(S.T_prev, S.T_curr);
+    std::swap(S.T_curr, S.T_next);
+    S.k += 1;
+}
+
+void staged_get(cheb_graph* g, double* Tp, double* Tc, double* Tn, double* acc, int* k) {
+    DeviceGuard dg(g->device);
+    StagedState& S = g->staged;
+    if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
+    const Layout L = layout_of(g, S.mode);
+    const int64_t n = g->n;
+    DevMem tmp(sizeof(double) * std::max<int64_t>(n, 1));
+    auto get = [&](double* h, DevMem& d) {
+        if (!h) return;
+        k_permute_out<double><<<grid1d(n), kThreads, 0, g->stream>>>(d.ptr<double>(), L.order, n, tmp.ptr<double>());
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(h, tmp.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+    };
+    get(Tp, S.T_prev);
+    get(Tc, S.T_curr);
+    get(Tn, S.T_next);
+    get(acc, S.acc);
+    if (k) *k = S.k;
+}
+
+}  // namespace chebgpu

@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the committed
+reference fixtures.  Bars (BASELINE.json north_star): CSR/degrees bit-exact; fp64 ranks
+within 1e-12 max-abs and identical top-100 (FAST); BITEXACT mode bitwise; fp32 relative
+L1 <= 1e-6."""
+import numpy as np
+import pytest
+
+from conftest import GOLDEN_NAMES, load_golden
+
+pytestmark = pytest.mark.gpu
+C = 0.85
+TOL64 = 1e-12     # fp64 max-abs (north_star)
+TOL32_L1 = 1e-6   # fp32 relative L1 (north_star)
+
+
+def build_kw(name):
+    kw = {}
+    if name == "multi":
+        kw["dedup"] = False
+    if name in ("drop", "nhint_drop"):
+        kw["drop_isolated"] = True
+    if name == "nhint_drop":
+        kw["n_hint"] = 6
+    return kw
+
+
+def top_k(r, k=100):
+    # ties broken by vertex id (stable sort on -rank)
+    return np.argsort(-r, kind="stable")[:k]
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+def test_device_csr_builder_bit_exact(cheb, name):
+    z = load_golden(name)
+    res = cheb.build_graph(z["edges"], cheb.BuildOptions(**build_kw(name)))
+    g = res.graph
+    assert g.n == int(z["n"]) and g.m == int(z["m"])
+    assert np.array_equal(g.offsets, z["offsets"])
+    assert np.array_equal(g.neighbors, z["neighbors"])
+    assert np.array_equal(g.degrees, z["degrees"])
+    assert res.duplicates_removed == int(z["duplicates_removed"])
+    assert res.isolated_dropped == int(z["isolated_dropped"])
+    assert g.multi == bool(z["multi"])
+
+
+@pytest.mark.parametrize("row_ptr_64", [False, True])
+def test_device_csr_builder_row_ptr_widths(cheb, oracle, row_ptr_64):
+    e = oracle.gnp_edges(3000, 0.004, 9)
+    ref = oracle.build_graph(e)
+    g = cheb.build_graph(e, cheb.BuildOptions(row_ptr_64=row_ptr_64)).graph
+    assert np.array_equal(g.offsets, ref.offsets) and np.array_equal(g.neighbors, ref.neighbors)
+
+
+def test_device_csr_builder_errors(cheb):
+    with pytest.raises(cheb.ValidationError, match="vertex 2 is isolated"):
+        cheb.build_graph([[0, 1], [3, 4]])
+    with pytest.raises(cheb.ValidationError, match="negative vertex id"):
+        cheb.build_graph([[0, -1]])
+    with pytest.raises(cheb.ValidationError):
+        cheb.build_graph([[0, 1]], cheb.BuildOptions(n_hint=4))
+    r = cheb.build_graph([[0, 1]], cheb.BuildOptions(n_hint=4, drop_isolated=True))
+    assert r.graph.n == 2 and r.isolated_dropped == 2
+    r = cheb.build_graph(np.zeros((0, 2), np.int64), cheb.BuildOptions(drop_isolated=True))
+    assert r.graph.n == 0
+
+
+@pytest.mark.parametrize("name", [n for n in GOLDEN_NAMES if n not in ("nhint_drop_empty",)])
+@pytest.mark.parametrize("M", [12, 39])
+def test_cpaa_bitexact_mode_is_bitwise_reference(cheb, name, M):
+    z = load_golden(name)
+    g = cheb.build_graph(z["edges"], cheb.BuildOptions(**build_kw(name))).graph
+    r = cheb.run_cpaa(g, cheb.SolverConfig(rounds=M, mode=cheb.MODE_BITEXACT))
+    assert np.array_equal(r.ranks, z[f"cpaa{M}_ranks"])
+    assert np.array_equal([t.S_k for t in r.trace], z[f"cpaa{M}_S"])
+    assert np.array_equal([t.mass_T for t in r.trace], z[f"cpaa{M}_massT"])
+    assert r.total_mass == float(z[f"cpaa{M}_total"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_NAMES)
+@pytest.mark.parametrize("M", [12, 39])
+def test_cpaa_fast_within_1e12(cheb, name, M):
+    z = load_golden(name)
+    g = cheb.build_graph(z["edges"], cheb.BuildOptions(**build_kw(name))).graph
+    r = cheb.run_cpaa(g, cheb.SolverConfig(rounds=M))
+    ref = z[f"cpaa{M}_ranks"]
+    assert np.max(np.abs(r.ranks - ref)) <= TOL64
+    if g.n >= 200:
+        assert np.array_equal(top_k(r.ranks), top_k(ref))
+    S = np.array([t.S_k for t in r.trace])
+    assert np.all(np.abs(S - z[f"cpaa{M}_S"]) <= g.n * 1e-12)
+
+
+def test_cpaa_fp32_within_relative_l1(cheb):
+    z = load_golden("config1")
+    g = cheb.build_graph(z["edges"]).graph
+    r = cheb.run_cpaa(g, cheb.SolverConfig(rounds=39, precision=32))
+    ref = z["cpaa39_ranks"]
+    assert np.sum(np.abs(r.ranks - ref)) / np.sum(np.abs(ref)) <= TOL32_L1
+
+
+def test_config1_eps_planning_and_top100(cheb):
+    z = load_golden("config1")
+    dg, info = cheb.build_device_graph(z["edges"])
+    r = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
+    assert r.rounds == 39
+    assert np.max(np.abs(r.ranks - z["cpaa39_ranks"])) <= TOL64
+    assert np.array_equal(top_k(r.ranks), top_k(z["cpaa39_ranks"]))
+    # a resident handle can be re-solved (CUDA-graph replay) with identical bits
+    r2 = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
+    assert np.array_equal(r.ranks, r2.ranks)
+    dg.free()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_power_against_fixture(cheb, mode):
+    for name in ("path3", "gnp500", "config1", "star100"):
+        z = load_golden(name)
+        g = cheb.build_graph(z["edges"]).graph
+        p = cheb.run_power(g, cheb.PowerConfig(rounds=210, mode=mode))
+        if mode == cheb.MODE_BITEXACT:
+            assert np.array_equal(p.ranks, z["power210_ranks"])
+            assert np.array_equal([t.l1_change for t in p.trace], z["power210_l1"])
+        else:
+            assert np.max(np.abs(p.ranks - z["power210_ranks"])) <= TOL64
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_transition_apply(cheb, mode):
+    for name in ("path3", "star4", "selfloop", "gnp2000", "config1"):
+        z = load_golden(name)
+        g = cheb.build_graph(z["edges"]).graph if name != "selfloop" else cheb.build_graph(z["edges"]).graph
+        y = cheb.transition_apply(g, z["tapply_x"], mode=mode)
+        if mode == cheb.MODE_BITEXACT:
+            assert np.array_equal(y, z["tapply_y"])
+        else:
+            assert np.max(np.abs(y - z["tapply_y"])) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_staged_equals_fused_bitwise(cheb, oracle, mode):
+    # test_cpaa.cpp:157-173, in both modes
+    g = oracle.build_graph(oracle.gnp_edges(500, 0.012, 7))
+    G = cheb.UndirectedGraph(g.n, g.m, g.offsets, g.neighbors, g.degrees, g.inv_degree)
+    M = 9
+    t = cheb.coefficients(C, M)
+    st = cheb.init_state(G, t.c0, mode=mode)
+    for k in range(1, M + 1):
+        cheb.generate_stage(st)
+        cheb.accumulate_stage(st, t.coeffs[k])
+        st.rotate()
+    acc = st.acc
+    st.close()
+    fused = cheb.run_cpaa(G, cheb.SolverConfig(rounds=M, mode=mode))
+    if mode == cheb.MODE_BITEXACT:
+        manual = cheb.normalize(acc)
+        assert np.array_equal(manual, fused.ranks)
+        assert cheb.kahan_sum(acc) == fused.total_mass
+    else:
+        assert np.max(np.abs(acc / fused.total_mass - fused.ranks)) <= 1e-15
+
+
+def test_staged_recurrence_examples(cheb):
+    # test_cpaa.cpp:105-123
+    k2 = cheb.build_graph([[0, 1]]).graph
+    t = cheb.coefficients(C, 3)
+    st = cheb.init_state(k2, t.c0)
+    cheb.generate_stage(st)
+    assert st.T_next.tolist() == [1.0, 1.0]
+    st.close()
+    p3 = cheb.build_graph([[0, 1], [1, 2]]).graph
+    st = cheb.init_state(p3, t.c0)
+    st.set(T_prev=np.ones(3), T_curr=np.array([0.5, 2.0, 0.5]), k=2)
+    cheb.generate_stage(st)
+    assert st.T_next.tolist() == [1.0, 1.0, 1.0]
+    st.close()
+    st = cheb.init_state(k2, t.c0)
+    cheb.generate_stage(st)
+    cheb.accumulate_stage(st, cheb.coefficients(C, 1).coeffs[1])
+    assert abs(st.acc[0] - 4.0120006773991105) <= 1e-12
+    st.close()
+
+
+def test_error_paths(cheb):
+    p3 = cheb.build_graph([[0, 1], [1, 2]]).graph
+    bad = cheb.UndirectedGraph(p3.n, p3.m, p3.offsets, p3.neighbors, p3.degrees, p3.inv_degree.copy())
+    bad.inv_degree[1] = 1e308  # test_cpaa.cpp:371-376
+    for mode in (0, 1):
+        with pytest.raises(cheb.NumericError, match="round"):
+            cheb.run_cpaa(bad, cheb.SolverConfig(rounds=5, mode=mode))
+        with pytest.raises(cheb.NumericError, match="round"):
+            cheb.run_power(bad, cheb.PowerConfig(rounds=9, mode=mode))
+    iso = cheb.UndirectedGraph(2, 0, np.array([0, 0, 0]), np.zeros(0, np.int64), np.array([0, 0]), np.zeros(2))
+    with pytest.raises(cheb.ValidationError):
+        cheb.run_cpaa(iso, cheb.SolverConfig(rounds=3))
+    with pytest.raises(ValueError):
+        cheb.run_cpaa(p3, cheb.SolverConfig(rounds=5, eps=1e-3))
+    with pytest.raises(ValueError):
+        cheb.run_cpaa(p3, cheb.SolverConfig())
+    with pytest.raises(ValueError):
+        cheb.run_cpaa(p3, cheb.SolverConfig(rounds=5), reference=np.ones(5))
+    with pytest.raises(cheb.DomainError):
+        cheb.run_cpaa(p3, cheb.SolverConfig(rounds=5, c=1.0))
+    with pytest.raises(ValueError):
+        cheb.run_power(p3, cheb.PowerConfig(rounds=5, tol=1e-3))
+    with pytest.raises(cheb.DomainError):
+        cheb.run_power(p3, cheb.PowerConfig(rounds=5, c=1.0))
+    with pytest.raises(ValueError):
+        cheb.transition_apply(p3, np.ones(5))
+
+
+def test_rounds_resolution_through_solver(cheb):
+    p3 = cheb.build_graph([[0, 1], [1, 2]]).graph
+    assert cheb.run_cpaa(p3, cheb.SolverConfig(eps=1e-3)).rounds == 12
+    assert cheb.run_cpaa(p3, cheb.SolverConfig(eps=1e-30)).rounds == 60
+    r = cheb.run_cpaa(p3, cheb.SolverConfig(rounds=7))
+    assert r.rounds == 7 and len(r.trace) == 7
+    assert cheb.run_cpaa(p3, cheb.SolverConfig(rounds=90, max_rounds=90)).rounds == 90
+    c4 = cheb.build_graph([[0, 1], [1, 2], [2, 3], [3, 0]]).graph
+    r0 = cheb.run_cpaa(c4, cheb.SolverConfig(rounds=0))
+    assert r0.rounds == 0 and r0.trace == [] and np.allclose(r0.ranks, 0.25, rtol=1e-14)
+
+
+def test_reference_tracking_columns(cheb):
+    z = load_golden("gnp2000")
+    g = cheb.build_graph(z["edges"]).graph
+    ref = z["power210_ranks"]
+    r = cheb.run_cpaa(g, cheb.SolverConfig(rounds=40), reference=ref)
+    assert r.has_err
+    crossing = next(t.k for t in r.trace if t.err < 1e-3)
+    assert 10 <= crossing <= 14  # test_cpaa.cpp:301-329
+    plain = cheb.run_cpaa(g, cheb.SolverConfig(rounds=40))
+    assert np.array_equal(plain.ranks, r.ranks)
+    p = cheb.run_power(g, cheb.PowerConfig(rounds=40), reference=ref)
+    assert p.trace[0].err > p.trace[-1].err
+
+
+def test_chung_lu_and_rmat_against_oracle(cheb, oracle):
+    from paper_2112_01743_b200 import generate as G
+    cases = [(G.chung_lu_edges(1 << 14, draws=150_000, seed=5), {}),
+             (G.rmat_edges(14, 16, seed=3), {"drop_isolated": True})]
+    for e, kw in cases:
+        e64 = e.astype(np.int64)
+        ref = oracle.build_graph(e64, **kw)
+        res = cheb.build_graph(e64, cheb.BuildOptions(**kw))
+        g = res.graph
+        assert np.array_equal(g.offsets, ref.offsets) and np.array_equal(g.neighbors, ref.neighbors)
+        assert res.isolated_dropped == ref.isolated_dropped
+        assert res.duplicates_removed == ref.duplicates_removed
+        o = oracle.run_cpaa(ref, 39)
+        fast = cheb.run_cpaa(g, cheb.SolverConfig(rounds=39))
+        assert np.max(np.abs(fast.ranks - o.ranks)) <= TOL64
+        assert np.array_equal(top_k(fast.ranks), top_k(o.ranks))
+        exact = cheb.run_cpaa(g, cheb.SolverConfig(rounds=39, mode=cheb.MODE_BITEXACT))
+        assert np.array_equal(exact.ranks, o.ranks)
+        f32 = cheb.run_cpaa(g, cheb.SolverConfig(rounds=39, precision=32))
+        assert np.sum(np.abs(f32.ranks - o.ranks)) / np.sum(o.ranks) <= TOL32_L1
+
+
+def test_device_generators_match_host(cheb):
+    from paper_2112_01743_b200 import generate as G
+    import ctypes as Cc
+    for fn, args in [(G.rmat_edges, (13, 16, 0.57, 0.19, 0.19, 11)),
+                     (G.chung_lu_edges, (1 << 13, 2.1, 2.0, 500.0, 60_000, 4))]:
+        h = fn(*args)
+        d = fn(*args, device=0)
+        buf = np.zeros(d.count * 2, dtype=np.int32)
+        from paper_2112_01743_b200 import _lib
+        import ctypes
+        cudart = ctypes.CDLL("libcudart.so") if False else None
+        # read back through the builder: device edges -> CSR == host edges -> CSR
+        dg_info = None
+        lib = _lib.load()
+        o = _lib.cheb_build_opts(1, 1, 0, 0, 0)
+        hnd = Cc.c_void_p()
+        inf = _lib.cheb_graph_info()
+        rc = lib.cheb_graph_build_device(Cc.c_void_p(d.ptr), d.count, 32, Cc.byref(o), Cc.byref(hnd), Cc.byref(inf))
+        assert rc == 0
+        dgraph = cheb.DeviceGraph(hnd, inf.n).download()
+        hgraph = cheb.build_graph(h.astype(np.int64), cheb.BuildOptions(drop_isolated=True)).graph
+        assert d.count == h.shape[0]
+        assert np.array_equal(dgraph.offsets, hgraph.offsets)
+        assert np.array_equal(dgraph.neighbors, hgraph.neighbors)
+        d.free()
