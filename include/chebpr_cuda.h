@@ -163,6 +163,11 @@ cheb_status cheb_last_timing(cheb_graph_t g, double* loop_ms, double* term_kerne
 cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double* term_ms,
                               int capacity, int* terms);
 
+/* Experiment knobs for kernel studies (not for production use): "hot" caps the shared-memory
+ * hot-prefix size in vertices (-1 = full capacity); "nogather" = 1 replaces x gathers by
+ * constants (timing of everything but the gather; results are wrong). */
+cheb_status cheb_set_tuning(const char* key, int value);
+
 /* run_power (power.hpp:24-25, power.cpp:28-109). */
 typedef struct {
     double c;       /* PowerConfig::c */

@@ -568,27 +568,70 @@ __global__ void k_gather_inv(const double* __restrict__ inv, const int* __restri
         out[i] = inv[order[i]];
 }
 
-// count of rows with degree > thr[j]  (degrees sorted descending)
-__global__ void k_bin_bounds(const int64_t* __restrict__ deg, int64_t n, const int64_t* __restrict__ thr,
-                             int nthr, int64_t* __restrict__ out) {
-    int j = threadIdx.x;
-    if (j >= nthr) return;
-    int64_t lo = 0, hi = n, t = thr[j];
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (deg[mid] > t) lo = mid + 1;
-        else hi = mid;
-    }
-    out[j] = lo;
-}
-
 }  // namespace
 
-// Bin thresholds (degrees).  Hub rows are split into chunks of kHubChunk nnz.
-constexpr int64_t kHubDeg = 16384;
-constexpr int64_t kHubChunk = 8192;
-constexpr int64_t kBlockDeg = 1024;   // (kBlockDeg, kHubDeg]: one CTA per row
-constexpr int kMaxResident = 148 * 8; // CTAs of 256 threads resident chip-wide
+// Greedy tiling of the degree-sorted rows (runs of equal degree, descending).
+static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
+                                    const std::vector<int64_t>& run_cnt, int64_t n, int64_t nnz,
+                                    int64_t* n_hub, int* n_chunk_tiles, std::vector<int>& hub_first) {
+    std::vector<Tile> tiles;
+    int64_t row = 0, z = 0;
+    int64_t cur_rows = 0, cur_nnz = 0, cur_row0 = 0, cur_z0 = 0, cur_dmax = 0;
+    *n_hub = 0;
+    *n_chunk_tiles = 0;
+    auto lanes_log2 = [](int64_t dmax, int64_t rows) {
+        // as many lanes per row as the 32 lanes allow, but no more than the degree needs
+        int lg = 0;
+        while (lg < 5 && (rows << (lg + 1)) <= 32 && (int64_t(1) << (lg + 1)) <= dmax * 2) ++lg;
+        return lg;
+    };
+    auto close = [&] {
+        if (cur_rows == 0) return;
+        tiles.push_back(Tile{cur_z0, (int32_t)cur_row0, (int32_t)lanes_log2(cur_dmax, cur_rows)});
+        cur_rows = cur_nnz = 0;
+    };
+    for (size_t r = 0; r < run_deg.size(); ++r) {
+        const int64_t d = run_deg[r];
+        int64_t c = run_cnt[r];
+        if (d > kWarpNnz) {
+            close();
+            for (int64_t i = 0; i < c; ++i) {
+                const int64_t nch = (d + kWarpNnz - 1) / kWarpNnz;
+                hub_first.push_back((int)tiles.size());
+                for (int64_t j = 0; j < nch; ++j) tiles.push_back(Tile{z + j * kWarpNnz, (int32_t)row, kTileChunk});
+                *n_chunk_tiles += (int)nch;
+                ++row;
+                z += d;
+            }
+            *n_hub += c;
+            continue;
+        }
+        while (c > 0) {
+            if (cur_rows == 0) {
+                cur_row0 = row;
+                cur_z0 = z;
+                cur_dmax = d;
+            }
+            const int64_t room_rows = kWarpRows - cur_rows;
+            const int64_t room_nnz = d > 0 ? (kWarpNnz - cur_nnz) / d : INT64_MAX;
+            const int64_t k = std::min(c, std::min(room_rows, room_nnz));
+            if (k == 0) {
+                close();
+                continue;
+            }
+            cur_rows += k;
+            cur_nnz += k * d;
+            row += k;
+            z += k * d;
+            c -= k;
+            if (cur_rows == kWarpRows || kWarpNnz - cur_nnz < d) close();
+        }
+    }
+    close();
+    if (row != n || z != nnz) fail(CHEB_CUDA, "tiling does not cover the graph");
+    tiles.push_back(Tile{nnz, (int32_t)n, 0});  // sentinel
+    return tiles;
+}
 
 template <class RPO, class RPN>
 static void build_view_t(cheb_graph* g) {
@@ -631,7 +674,7 @@ static void build_view_t(cheb_graph* g) {
         V.row_ptr.alloc(sizeof(int) * (n + 1));
         k_narrow_rowptr<<<grid_for(n + 1), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), n + 1, V.row_ptr.ptr<int>());
     }
-    V.col.alloc(sizeof(int) * std::max<int64_t>(nnz, 1));
+    V.col.alloc(sizeof(int) * std::max<int64_t>(nnz, 1) + 64);  // TMA reads round up to 16 B
     k_permute_rows<<<grid_for(n * 32), kBuildThreads, 0, st>>>(rp_old, g->col.ptr<int>(), V.row_ptr.ptr<RPN>(),
                                                               V.order.ptr<int>(), rank.ptr<int>(), n,
                                                               V.col.ptr<int>());
@@ -644,84 +687,37 @@ static void build_view_t(cheb_graph* g) {
         V.inv.release();
     }
 
-    // Bin boundaries over the descending degrees.
-    // thresholds: hub, block, 512,256,128,64,32,16,8,4,2,1
-    std::vector<int64_t> thr = {kHubDeg, kBlockDeg, 512, 256, 128, 64, 32, 16, 8, 4, 2, 1};
-    DevMem dthr(sizeof(int64_t) * thr.size()), dout(sizeof(int64_t) * thr.size());
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(dthr.get(), thr.data(), sizeof(int64_t) * thr.size(),
-                                    cudaMemcpyHostToDevice, st));
-    k_bin_bounds<<<1, 32, 0, st>>>(deg_new.ptr<int64_t>(), n, dthr.ptr<int64_t>(), (int)thr.size(),
-                                   dout.ptr<int64_t>());
-    std::vector<int64_t> bound(thr.size());
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(bound.data(), dout.get(), sizeof(int64_t) * thr.size(),
-                                    cudaMemcpyDeviceToHost, st));
-    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-
-    // Hub rows: chunk table.
-    V.n_hub = bound[0];
-    std::vector<int64_t> hub_deg(V.n_hub);
-    if (V.n_hub)
-        CHEB_CUDA_CHECK(cudaMemcpy(hub_deg.data(), deg_new.get(), sizeof(int64_t) * V.n_hub,
-                                   cudaMemcpyDeviceToHost));
-    std::vector<int> chunk_row, chunk_idx, hub_first(V.n_hub + 1, 0);
-    for (int64_t h = 0; h < V.n_hub; ++h) {
-        hub_first[h] = (int)chunk_row.size();
-        const int64_t nc = (hub_deg[h] + kHubChunk - 1) / kHubChunk;
-        for (int64_t j = 0; j < nc; ++j) {
-            chunk_row.push_back((int)h);
-            chunk_idx.push_back((int)j);
-        }
+    // Runs of equal degree (descending) -> greedy tiles on the host.
+    std::vector<int64_t> run_deg, run_cnt;
+    if (n > 0) {
+        DevMem uniq(sizeof(int64_t) * n), cnts(sizeof(int64_t) * n), nruns(sizeof(int64_t));
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, deg_new.ptr<int64_t>(), uniq.ptr<int64_t>(),
+                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), n, st));
+        void* t = tmp.get(bytes);
+        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(t, bytes, deg_new.ptr<int64_t>(), uniq.ptr<int64_t>(),
+                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), n, st));
+        const int64_t R = read_scalar(nruns.ptr<int64_t>(), st);
+        run_deg.resize(R);
+        run_cnt.resize(R);
+        CHEB_CUDA_CHECK(cudaMemcpy(run_deg.data(), uniq.get(), sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
+        CHEB_CUDA_CHECK(cudaMemcpy(run_cnt.data(), cnts.get(), sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
     }
-    hub_first[V.n_hub] = (int)chunk_row.size();
-    V.n_chunks = (int)chunk_row.size();
-    V.chunk_row.alloc(sizeof(int) * std::max(V.n_chunks, 1));
-    V.chunk_idx.alloc(sizeof(int) * std::max(V.n_chunks, 1));
-    V.hub_first.alloc(sizeof(int) * (V.n_hub + 1));
-    if (V.n_chunks) {
-        CHEB_CUDA_CHECK(cudaMemcpy(V.chunk_row.get(), chunk_row.data(), sizeof(int) * V.n_chunks, cudaMemcpyHostToDevice));
-        CHEB_CUDA_CHECK(cudaMemcpy(V.chunk_idx.get(), chunk_idx.data(), sizeof(int) * V.n_chunks, cudaMemcpyHostToDevice));
+    std::vector<int> hub_first;
+    const std::vector<Tile> tiles = make_tiles(run_deg, run_cnt, n, nnz, &V.n_hub, &V.n_chunk_tiles, hub_first);
+    hub_first.push_back(V.n_chunk_tiles);
+    V.hub_first.alloc(sizeof(int) * hub_first.size());
+    CHEB_CUDA_CHECK(cudaMemcpy(V.hub_first.get(), hub_first.data(), sizeof(int) * hub_first.size(),
+                               cudaMemcpyHostToDevice));
+    V.n_tiles = (int)tiles.size() - 1;
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        V.grid = std::max(1, std::min(sms, (V.n_tiles + kWarps - 1) / kWarps));
     }
-    CHEB_CUDA_CHECK(cudaMemcpy(V.hub_first.get(), hub_first.data(), sizeof(int) * (V.n_hub + 1), cudaMemcpyHostToDevice));
-
-    // Assemble bins (hub, block, warp x5, vector x5, one-lane).
-    V.bins.clear();
-    int next_block = 0;
-    auto add = [&](int64_t b, int64_t e, int kind, int lanes, int64_t rows_per_block_iter) {
-        if (e <= b) return;
-        Bin bin;
-        bin.row_begin = b;
-        bin.row_end = e;
-        bin.kind = kind;
-        bin.lanes = lanes;
-        bin.block_begin = next_block;
-        if (kind == BIN_HUB) {
-            bin.nblocks = V.n_chunks;
-            bin.chunk_begin = 0;
-        } else {
-            int64_t want = (e - b + rows_per_block_iter - 1) / rows_per_block_iter;
-            int64_t cap = 4 * kMaxResident;
-            bin.nblocks = (int)std::max<int64_t>(1, std::min(want, cap));
-        }
-        next_block += bin.nblocks;
-        V.bins.push_back(bin);
-    };
-    add(0, bound[0], BIN_HUB, 0, 1);
-    add(bound[0], bound[1], BIN_BLOCK, 0, 1);
-    // warp rows: deg in (32, 1024], one bin per octave
-    add(bound[1], bound[2], BIN_VEC, 32, kThreads / 32);
-    add(bound[2], bound[3], BIN_VEC, 32, kThreads / 32);
-    add(bound[3], bound[4], BIN_VEC, 32, kThreads / 32);
-    add(bound[4], bound[5], BIN_VEC, 32, kThreads / 32);
-    add(bound[5], bound[6], BIN_VEC, 32, kThreads / 32);
-    // vector rows: (16,32] -> 32 lanes, (8,16] -> 16, (4,8] -> 8, (2,4] -> 4, (1,2] -> 2, 1 -> 1
-    add(bound[6], bound[7], BIN_VEC, 32, kThreads / 32);
-    add(bound[7], bound[8], BIN_VEC, 16, kThreads / 16);
-    add(bound[8], bound[9], BIN_VEC, 8, kThreads / 8);
-    add(bound[9], bound[10], BIN_VEC, 4, kThreads / 4);
-    add(bound[10], bound[11], BIN_VEC, 2, kThreads / 2);
-    add(bound[11], n, BIN_VEC, 1, kThreads);
-    if ((int)V.bins.size() > kMaxBins) fail(CHEB_CUDA, "too many bins");
-    V.grid = std::max(next_block, 1);
+    V.tiles.alloc(sizeof(Tile) * tiles.size());
+    CHEB_CUDA_CHECK(cudaMemcpy(V.tiles.get(), tiles.data(), sizeof(Tile) * tiles.size(), cudaMemcpyHostToDevice));
     V.ready = true;
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
 }

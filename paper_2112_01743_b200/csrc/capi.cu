@@ -368,6 +368,15 @@ cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double
     });
 }
 
+cheb_status cheb_set_tuning(const char* key, int value) {
+    return guarded([&] {
+        const std::string k = key ? key : "";
+        if (k == "hot") tuning().hot = value;
+        else if (k == "nogather") tuning().nogather = value;
+        else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
+    });
+}
+
 cheb_status cheb_last_timing(cheb_graph_t g, double* loop_ms, double* term_kernel_ms, int* terms,
                              int* launches) {
     return guarded([&] {

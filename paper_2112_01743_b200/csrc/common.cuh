@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -97,19 +98,21 @@ struct DeviceGuard {
 // Column ids are renamed, but every row keeps its neighbours in the reference's
 // storage order.  order[new] = old.
 // --------------------------------------------------------------------------
-enum BinKind : int { BIN_HUB = 0, BIN_BLOCK = 1, BIN_VEC = 2 };
-
-struct Bin {
-    int64_t row_begin = 0, row_end = 0;  // [begin, end) in new ids
-    int kind = BIN_VEC;
-    int lanes = 32;        // BIN_VEC: lanes per row (1..32)
-    int block_begin = 0;   // first blockIdx of this bin
-    int nblocks = 0;
-    int chunk_begin = 0;   // BIN_HUB: first chunk id; nblocks == #chunks
+// Warp tiles of the degree-sorted view.  meta: low 4 bits = log2(lanes per row) for
+// pack tiles; kTileChunk marks a 256-nnz chunk of a row with degree > kWarpNnz (row_begin = the
+// row).  tiles[n_tiles] is a sentinel {nnz, n}.
+struct Tile {
+    int64_t nnz_begin;
+    int32_t row_begin;
+    int32_t meta;
 };
-
-constexpr int kMaxBins = 16;
-constexpr int kThreads = 256;      // CTA size of the term kernels (8 warps)
+constexpr int kThreads = 256;        // CTA size of the auxiliary kernels
+constexpr int kWarps = 32;           // warps per CTA of the term kernel (1 CTA / SM)
+constexpr int kWarpNnz = 248;        // nnz per tile: with <= 7 alignment slots, 8 per lane
+constexpr int kWarpRows = 32;        // rows per pack tile (one per lane)
+constexpr int kColBuf = 264;         // ints per TMA column buffer (256 + alignment slack)
+constexpr int kHotBytes = 128 * 1024;  // shared-memory copy of the hot x prefix
+constexpr int kTileChunk = 0x10;
 
 struct SolverView {
     bool ready = false;
@@ -118,13 +121,12 @@ struct SolverView {
     DevMem row_ptr;    // int32/int64 [n+1] (new order)
     DevMem col;        // int32 [nnz] (renamed ids, storage order kept)
     DevMem inv;        // double [n] (new order) only when inv_degree is non-canonical
-    std::vector<Bin> bins;
-    int grid = 0;          // total CTAs of one term launch
-    int64_t n_hub = 0;     // hub rows [0, n_hub)
-    int n_chunks = 0;
-    DevMem chunk_row;  // int32 [n_chunks]
-    DevMem chunk_idx;  // int32 [n_chunks]  j-th chunk of its row
-    DevMem hub_first;  // int32 [n_hub+1]   first chunk of hub row h
+    DevMem tiles;      // Tile [n_tiles + 1]
+    int n_tiles = 0;
+    int grid = 0;          // CTAs of one term launch (persistent: one per SM)
+    int64_t n_hub = 0;     // rows [0, n_hub) with degree > kWarpNnz (chunk tiles)
+    int n_chunk_tiles = 0;
+    DevMem hub_first;      // int32 [n_hub + 1]: first chunk tile of each hub row
 };
 
 struct Workspace {
@@ -134,7 +136,7 @@ struct Workspace {
     int M = -1;
     DevMem T0, T1, X0, X1, acc, out;    // vectors (solve precision), out = ranks (orig order)
     DevMem part;                        // double [M][grid][2] block trace partials
-    DevMem hub_part;                    // double [n_chunks]
+    DevMem hub_part;                    // double [grid] chunk partials
     DevMem hub_cnt;                     // uint32 [n_hub]
     DevMem hub_ts;                      // double [M][n_hub][2]
     DevMem trace;                       // double [M][2] (mass_T, S_k)
@@ -183,6 +185,20 @@ struct cheb_graph {
 };
 
 namespace chebgpu {
+// Experiment knobs (cheb_set_tuning); defaults = the product configuration.
+struct Tuning {
+    int hot = -1;       // cap on the shared-memory hot prefix (vertices); -1 = capacity
+    int nogather = 0;   // 1: skip the x gathers (timing experiments only; wrong results)
+};
+inline Tuning& tuning() {
+    static Tuning t = [] {
+        Tuning x;
+        if (const char* e = std::getenv("CHEB_TUNE_HOT")) x.hot = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_NOGATHER")) x.nogather = std::atoi(e);
+        return x;
+    }();
+    return t;
+}
 // build.cu
 void build_from_edges(cheb_graph* g, const void* d_edges, int64_t E, int edge_bits,
                       const cheb_build_opts& o);

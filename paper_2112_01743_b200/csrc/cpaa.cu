@@ -39,11 +39,6 @@ enum Epi : int {
     EPI_PLAIN = 3   // transition_apply (graph.cpp:104-121): y = s
 };
 
-struct BinTable {
-    Bin b[kMaxBins];
-    int nb;
-};
-
 template <class RP, class V>
 struct TermArgs {
     const RP* __restrict__ rp;
@@ -59,12 +54,10 @@ struct TermArgs {
     double base;  // POWER: (1-c)/n
     int first;
     double* part;  // [grid][2] this term
-    const int* chunk_row;
-    const int* chunk_idx;
-    const int* hub_first;
-    double* hub_part;
+    double* hub_part;  // [n_tiles] chunk partials
     unsigned* hub_cnt;
     double* hub_ts;  // [n_hub][2] this term
+    int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
 };
 
 // ---------------- arithmetic helpers (reference rounding, no contraction) -------------
@@ -135,143 +128,376 @@ __device__ __forceinline__ void epilogue(const TermArgs<RP, V>& a, int64_t u, V 
     }
 }
 
-// ---------------- FAST: degree-binned schedule ----------------------------------------
+// ---------------- FAST: persistent warp-tiled schedule ---------------------------------
+//
+// The view's rows are sorted by degree (descending) and cut into WARP tiles (build.cu):
+//  * pack tiles: <= 32 consecutive whole rows with <= kWarpNnz (256) nnz;
+//  * chunk tiles: a slice of <= kWarpNnz (256) nnz of a row with degree > kWarpNnz;
+//    a row with several chunks is finished by the last chunk to arrive, which combines
+//    the chunk partials in chunk order (deterministic).
+// One CTA of 32 warps per SM; each warp walks tiles blockIdx*32+warp, +gridDim*32, ...
+// (static, deterministic) with no CTA barrier inside the term: per tile a lane issues
+// its 8 column-id loads, the row end pointer, T_{k-1} and acc at once, then 8 gathers.
+// Gathers of the hottest vertices (ids < H: the degree-sorted hub prefix, ~50% of all
+// gathers on power-law graphs) hit a shared-memory copy of x_k[0..H) refreshed at the
+// start of every term; the rest go through L1/L2.  Measured on B200
+// (tools/micro_gather.cu): random LDS.64 876 G/s vs random LDG over an L2-resident
+// table 256 G/s — the gather, not HBM, bounds this path.
 
-// L lanes per row, L in {1,2,4,8,16,32}; rows interleaved over the bin's CTAs.
-template <int L, int EPI, class RP, class V>
-__device__ __forceinline__ void vec_rows(const TermArgs<RP, V>& a, const Bin& bin, double& p0,
-                                         double& p1) {
-    constexpr int G = kThreads / L;
-    const int g = threadIdx.x / L, lane = threadIdx.x % L;
-    const unsigned mask = L == 32 ? 0xffffffffu
-                                  : (((1u << L) - 1u) << ((threadIdx.x & 31) / L * L));
-    const int64_t rows = bin.row_end - bin.row_begin;
-    const int64_t stride = (int64_t)bin.nblocks * G;
-    for (int64_t i = (int64_t)(blockIdx.x - bin.block_begin) * G + g; i < rows; i += stride) {
-        const int64_t u = bin.row_begin + i;
-        const int64_t b = a.rp[u], e = a.rp[u + 1];
-        V s = V(0);
-        int64_t j = b + lane;
-        if constexpr (L == 32) {
-            // 4 independent index loads then 4 gathers in flight per lane
-            for (; j + 3 * L < e; j += 4 * L) {
-                const int c0 = ld_stream(a.col + j), c1 = ld_stream(a.col + j + L);
-                const int c2 = ld_stream(a.col + j + 2 * L), c3 = ld_stream(a.col + j + 3 * L);
-                const V v0 = ldg_x(a.x_in + c0), v1 = ldg_x(a.x_in + c1);
-                const V v2 = ldg_x(a.x_in + c2), v3 = ldg_x(a.x_in + c3);
-                s += v0;
-                s += v1;
-                s += v2;
-                s += v3;
-            }
-        }
-        for (; j < e; j += L) s += ldg_x(a.x_in + ld_stream(a.col + j));
-        if constexpr (L > 1) {
+// Gather x[c[q]] for the lane's 8 column ids: cold ids (>= H) as predicated global loads
+// issued back to back, hot ids as predicated shared loads; c < 0 = no element (0).
+template <class V, int U>
+__device__ __forceinline__ void gather8(const V* __restrict__ x, const V* hot, int H, const int (&c)[U],
+                                        V (&v)[U]) {
 #pragma unroll
-            for (int o = L / 2; o; o >>= 1) s += __shfl_xor_sync(mask, s, o, L);
+    for (int q = 0; q < U; ++q) {
+        v[q] = V(0);
+        if (c[q] >= H) v[q] = ldg_x(x + c[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+        if ((unsigned)c[q] < (unsigned)H) v[q] = hot[c[q]];
+}
+
+// TMA bulk copy global -> shared (cp.async.bulk), completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* mbar) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(gsrc), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, unsigned count) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, unsigned bytes) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile(
+        "{\n"
+        ".reg .pred done;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        "@!done bra WAIT_%=;\n"
+        "}\n" :: "r"(bar), "r"(parity) : "memory");
+}
+
+// Row epilogue with the row's operands already loaded (prev = T_{k-1} / old x).
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, V s, int64_t deg,
+                                           V prev, V accv, double& p0, double& p1) {
+    if constexpr (EPI == EPI_PLAIN) {
+        a.out[u] = s;
+    } else {
+        const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
+        if constexpr (EPI == EPI_CPAA) {
+            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
+            a.T[u] = t;
+            const V nacc = add_rn(accv, mul_rn((V)a.ck, t));
+            a.acc[u] = nacc;
+            a.x_out[u] = mul_rn(t, inv);
+            p0 += (double)t;
+            p1 += (double)nacc;
+        } else if constexpr (EPI == EPI_GEN) {
+            a.out[u] = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
+        } else {  // EPI_POWER
+            const V y = add_rn(mul_rn((V)a.ck, s), (V)a.base);
+            a.T[u] = y;
+            a.x_out[u] = mul_rn(y, inv);
+            p0 += fabs((double)y - (double)prev);
+            p1 += (double)y;
         }
-        if (lane == 0) epilogue<EPI>(a, u, s, e - b, p0, p1);
     }
 }
 
-// One CTA per row (degree in (kBlockDeg, kHubDeg]).
 template <int EPI, class RP, class V>
-__device__ __forceinline__ void block_rows(const TermArgs<RP, V>& a, const Bin& bin, double& p0,
-                                           double& p1, V* sh) {
-    for (int64_t u = bin.row_begin + (blockIdx.x - bin.block_begin); u < bin.row_end;
-         u += bin.nblocks) {
-        const int64_t b = a.rp[u], e = a.rp[u + 1];
-        V s = V(0);
-        int64_t j = b + threadIdx.x;
-        for (; j + 3 * kThreads < e; j += 4 * kThreads) {
-            const int c0 = ld_stream(a.col + j), c1 = ld_stream(a.col + j + kThreads);
-            const int c2 = ld_stream(a.col + j + 2 * kThreads), c3 = ld_stream(a.col + j + 3 * kThreads);
-            const V v0 = ldg_x(a.x_in + c0), v1 = ldg_x(a.x_in + c1);
-            const V v2 = ldg_x(a.x_in + c2), v3 = ldg_x(a.x_in + c3);
-            s += v0;
-            s += v1;
-            s += v2;
-            s += v3;
-        }
-        for (; j < e; j += kThreads) s += ldg_x(a.x_in + ld_stream(a.col + j));
-        s = block_sum(s, sh);
-        if (threadIdx.x == 0) epilogue<EPI>(a, u, s, e - b, p0, p1);
+__device__ __forceinline__ const V* prev_src(const TermArgs<RP, V>& a) {
+    if constexpr (EPI == EPI_GEN) return a.T_prev;
+    else return a.T;
+}
+
+template <class V>
+__device__ __forceinline__ V warp_sum_v(V v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <class V>
+constexpr int hot_capacity() { return (kHotBytes / (int)sizeof(V)); }
+
+// Per-warp shared scratch of the term kernel.
+template <class V>
+struct alignas(16) WarpScratch {
+    int colb[2][kColBuf];   // TMA landing buffers for the column ids of the next tiles
+    int wend[33];           // tile-local row end positions (+1 guard)
+    int tailr[32];          // row continued past each lane (-1 none)
+    V wsum[32];             // row sums
+    V tailv[32];            // open partial of each lane
+    uint64_t mbar[2];
+};
+
+template <class V>
+constexpr size_t warp_smem_bytes() {
+    return (size_t)kHotBytes + (size_t)kWarps * sizeof(WarpScratch<V>) + 2 * 32 * sizeof(double);
+}
+
+// Tile in registers.
+struct TileR {
+    int64_t z0;
+    int r0, rows, cnt, meta;
+};
+
+__device__ __forceinline__ TileR load_tile(const Tile* __restrict__ tiles, int t, int ntiles) {
+    TileR r{0, 0, 0, 0, 0};
+    if (t < ntiles) {
+        const Tile a = tiles[t], b = tiles[t + 1];
+        r.z0 = a.nnz_begin;
+        r.r0 = a.row_begin;
+        r.meta = a.meta;
+        r.cnt = (int)(b.nnz_begin - a.nnz_begin);
+        r.rows = (a.meta & kTileChunk) ? 1 : (b.row_begin - a.row_begin);
+    }
+    return r;
+}
+
+// Lane 0: bulk-copy the tile's column ids from the 8-aligned position a0 = z0 & ~7 (so
+// lane l's 8 positions a0+8l.. are two 16-byte shared loads) into buf.
+__device__ __forceinline__ void issue_cols(const int* __restrict__ col, const TileR& t, int* buf,
+                                           uint64_t* mbar) {
+    const int64_t a0 = t.z0 & ~int64_t(7);
+    const unsigned bytes = (unsigned)(((t.z0 - a0) + t.cnt + 3) & ~3) * 4u;
+    mbar_expect_tx(mbar, bytes);
+    bulk_g2s(buf, col + a0, bytes, mbar);
+}
+
+// Streaming operands of a pack tile (row ends, T_{k-1}, acc): one row per lane.
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR& t, int& end, V& pv,
+                                          V& av) {
+    const int lane = threadIdx.x & 31;
+    end = 0;
+    pv = V(0);
+    av = V(0);
+    if (t.meta & kTileChunk) return;
+    if (lane < t.rows) {
+        end = (int)(a.rp[t.r0 + lane + 1] - t.z0);
+        if constexpr (EPI != EPI_PLAIN) pv = prev_src<EPI>(a)[t.r0 + lane];
+        if constexpr (EPI == EPI_CPAA) av = a.acc[t.r0 + lane];
     }
 }
 
-// Hub rows: one CTA per chunk of kHubChunk nnz; the last CTA of a row to arrive
-// combines the chunk partials in chunk order (deterministic) and runs the epilogue.
 template <int EPI, class RP, class V>
-__device__ __forceinline__ void hub_chunk(const TermArgs<RP, V>& a, const Bin& bin, V* sh) {
-    constexpr int64_t kChunk = 8192;
-    const int c = bin.chunk_begin + (blockIdx.x - bin.block_begin);
-    const int h = a.chunk_row[c];
-    const int64_t rb = a.rp[h], re = a.rp[h + 1];
-    const int64_t b = rb + (int64_t)a.chunk_idx[c] * kChunk;
-    const int64_t e = min(re, b + kChunk);
-    V s = V(0);
-    int64_t j = b + threadIdx.x;
-    for (; j + 3 * kThreads < e; j += 4 * kThreads) {
-        const int c0 = ld_stream(a.col + j), c1 = ld_stream(a.col + j + kThreads);
-        const int c2 = ld_stream(a.col + j + 2 * kThreads), c3 = ld_stream(a.col + j + 3 * kThreads);
-        const V v0 = ldg_x(a.x_in + c0), v1 = ldg_x(a.x_in + c1);
-        const V v2 = ldg_x(a.x_in + c2), v3 = ldg_x(a.x_in + c3);
-        s += v0;
-        s += v1;
-        s += v2;
-        s += v3;
-    }
-    for (; j < e; j += kThreads) s += ldg_x(a.x_in + ld_stream(a.col + j));
-    s = block_sum(s, sh);
+__global__ void __launch_bounds__(kWarps * 32, 1)
+k_term_warp(TermArgs<RP, V> a, const Tile* __restrict__ tiles, int ntiles, int H) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    V* hot = reinterpret_cast<V*>(smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpScratch<V>& ws = reinterpret_cast<WarpScratch<V>*>(smem + kHotBytes)[warp];
+    double* red = reinterpret_cast<double*>(smem + kHotBytes + kWarps * sizeof(WarpScratch<V>));
+    __shared__ __align__(8) uint64_t mbar_hot;
+    constexpr bool kPrev = EPI != EPI_PLAIN;
+    constexpr bool kAcc = EPI == EPI_CPAA;
+    constexpr int U = 8;  // positions per lane
+
+    // hot prefix x_k[0..H) -> shared memory (TMA bulk copies; sub-16-byte tail by loads)
+    const unsigned hot_bytes = (unsigned)(H * sizeof(V)) & ~15u;
     if (threadIdx.x == 0) {
-        a.hub_part[c] = (double)s;
-        __threadfence();
-        const int f0 = a.hub_first[h], f1 = a.hub_first[h + 1];
-        const unsigned prev = atomicAdd(&a.hub_cnt[h], 1u);
-        if (prev == (unsigned)(f1 - f0 - 1)) {
-            __threadfence();
-            V tot = V(0);
-            for (int q = f0; q < f1; ++q) tot += (V)__ldcg(a.hub_part + q);
-            a.hub_cnt[h] = 0u;
-            double q0 = 0.0, q1 = 0.0;
-            epilogue<EPI>(a, h, tot, re - rb, q0, q1);
-            if (a.hub_ts) {
-                a.hub_ts[2 * h] = q0;
-                a.hub_ts[2 * h + 1] = q1;
+        mbar_init(&mbar_hot, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (lane == 0) {
+        mbar_init(&ws.mbar[0], 1);
+        mbar_init(&ws.mbar[1], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&mbar_hot, hot_bytes);
+        constexpr unsigned kPiece = 32768;
+        for (unsigned off = 0; off < hot_bytes; off += kPiece)
+            bulk_g2s(smem + off, reinterpret_cast<const unsigned char*>(a.x_in) + off,
+                     min(kPiece, hot_bytes - off), &mbar_hot);
+    }
+    for (int i = hot_bytes / sizeof(V) + threadIdx.x; i < H; i += blockDim.x) hot[i] = ldg_x(a.x_in + i);
+
+    // software pipeline over this warp's tiles: columns of tile i+1 arrive by TMA and its
+    // row operands by registers while tile i gathers.
+    const int stride = gridDim.x * kWarps;
+    int t = blockIdx.x * kWarps + warp;
+    TileR cur = load_tile(tiles, t, ntiles);
+    TileR nxt = load_tile(tiles, t + stride, ntiles);
+    if (lane == 0 && t < ntiles) issue_cols(a.col, cur, ws.colb[0], &ws.mbar[0]);
+    int end, nend;
+    V pv, av, npv, nav;
+    load_rows<EPI>(a, cur, end, pv, av);
+    unsigned phase = 0;  // bit b = parity of buffer b
+    double p0 = 0.0, p1 = 0.0;
+    mbar_wait(&mbar_hot, 0);
+    __syncthreads();
+
+    for (int i = 0; t < ntiles; t += stride, ++i) {
+        const int b = i & 1;
+        const bool has_next = t + stride < ntiles;
+        if (lane == 0 && has_next) issue_cols(a.col, nxt, ws.colb[b ^ 1], &ws.mbar[b ^ 1]);
+        load_rows<EPI>(a, nxt, nend, npv, nav);
+        const TileR nn = load_tile(tiles, t + 2 * stride, ntiles);
+
+        mbar_wait(&ws.mbar[b], (phase >> b) & 1u);
+        phase ^= 1u << b;
+        // lane owns tile-local positions P = 8*lane + q - off, q < 8 (contiguous)
+        const int off = (int)(cur.z0 & 7);
+        const int P0 = 8 * lane - off;
+        int c[U];
+        {
+            const int4 lo = *reinterpret_cast<const int4*>(&ws.colb[b][8 * lane]);
+            const int4 hi = *reinterpret_cast<const int4*>(&ws.colb[b][8 * lane + 4]);
+            const int cc[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+            for (int q = 0; q < U; ++q) c[q] = (P0 + q >= 0 && P0 + q < cur.cnt) ? cc[q] : -1;
+        }
+        V v[U];
+        if (a.tune_nogather) {
+#pragma unroll
+            for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
+        } else {
+            gather8(a.x_in, hot, H, c, v);
+        }
+
+        if (cur.meta & kTileChunk) {
+            // slice of a row with degree > kWarpNnz: partial only; the row is completed by
+            // k_hub_finalize after this kernel (kernel boundary orders it; no fences)
+            V s = V(0);
+#pragma unroll
+            for (int q = 0; q < U; ++q) s += v[q];
+            s = warp_sum_v(s);
+            if (lane == 0) a.hub_part[t] = (double)s;
+        } else {
+            // rows of the tile: wend[i] = tile-local end of row i (one row per lane)
+            const int rows = cur.rows;
+            if (lane < rows) {
+                ws.wend[lane] = end;
+                ws.wsum[lane] = V(0);
+            }
+            __syncwarp();
+            // merge-path walk over the lane's contiguous positions
+            const int pf = max(P0, 0), pl = min(P0 + U, cur.cnt);  // [pf, pl) valid
+            int r = 0;
+            if (pf < pl) {
+                // first row whose end is past pf (rows <= 32: binary search in smem)
+                int lo = 0, hi = rows - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (ws.wend[mid] > pf) hi = mid;
+                    else lo = mid + 1;
+                }
+                r = lo;
+            }
+            int rstart = r ? ws.wend[r - 1] : 0;
+            int rend = ws.wend[r < rows ? r : rows - 1];
+            V run = V(0);
+            V head = V(0);
+            int head_row = -1;  // row whose start lies before pf and ends in this lane
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int P = P0 + q;
+                if (P >= pf && P < pl) {
+                    while (P >= rend) {
+                        if (rstart < pf) {
+                            head = run;
+                            head_row = r;
+                        } else {
+                            ws.wsum[r] = run;
+                        }
+                        ++r;
+                        run = V(0);
+                        rstart = rend;
+                        rend = ws.wend[r];
+                    }
+                    run += v[q];
+                }
+            }
+            int tail_row = -1;
+            if (pf < pl) {
+                if (rend == pl) {  // the open row ends exactly at the lane's last position
+                    if (rstart < pf) {
+                        head = run;
+                        head_row = r;
+                    } else {
+                        ws.wsum[r] = run;
+                    }
+                } else {
+                    tail_row = r;  // continues into the next lane(s)
+                }
+            }
+            ws.tailv[lane] = run;
+            ws.tailr[lane] = tail_row;
+            __syncwarp();
+            if (head_row >= 0) {  // add the carries of the preceding lanes, nearest first
+                V tot = head;
+                for (int j = lane - 1; j >= 0 && ws.tailr[j] == head_row; --j) tot += ws.tailv[j];
+                ws.wsum[head_row] = tot;
+            }
+            __syncwarp();
+            if (lane < rows) {
+                const int b0 = lane ? ws.wend[lane - 1] : 0;
+                epilogue_v<EPI>(a, (int64_t)cur.r0 + lane, ws.wsum[lane], (int64_t)(end - b0), pv, av, p0, p1);
             }
         }
-    }
-}
-
-template <int EPI, class RP, class V>
-__global__ void __launch_bounds__(kThreads) k_term_fast(TermArgs<RP, V> a, BinTable bt) {
-    __shared__ V sh[32];
-    __shared__ double shd[32];
-    int bi = 0;
-    while (bi + 1 < bt.nb && (int)blockIdx.x >= bt.b[bi + 1].block_begin) ++bi;
-    const Bin bin = bt.b[bi];
-    double p0 = 0.0, p1 = 0.0;
-    if (bin.kind == BIN_HUB) {
-        hub_chunk<EPI>(a, bin, sh);
-    } else if (bin.kind == BIN_BLOCK) {
-        block_rows<EPI>(a, bin, p0, p1, sh);
-    } else {
-        switch (bin.lanes) {
-            case 32: vec_rows<32, EPI>(a, bin, p0, p1); break;
-            case 16: vec_rows<16, EPI>(a, bin, p0, p1); break;
-            case 8: vec_rows<8, EPI>(a, bin, p0, p1); break;
-            case 4: vec_rows<4, EPI>(a, bin, p0, p1); break;
-            case 2: vec_rows<2, EPI>(a, bin, p0, p1); break;
-            default: vec_rows<1, EPI>(a, bin, p0, p1); break;
-        }
+        __syncwarp();
+        cur = nxt;
+        nxt = nn;
+        end = nend;
+        pv = npv;
+        av = nav;
     }
     if constexpr (EPI == EPI_CPAA || EPI == EPI_POWER) {
         if (a.part) {
-            p0 = block_sum(p0, shd);
-            p1 = block_sum(p1, shd);
-            if (threadIdx.x == 0) {
-                a.part[2 * blockIdx.x] = p0;
-                a.part[2 * blockIdx.x + 1] = p1;
+            p0 = warp_sum_v(p0);
+            p1 = warp_sum_v(p1);
+            if (lane == 0) {
+                red[warp] = p0;
+                red[32 + warp] = p1;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                double q0 = lane < kWarps ? red[lane] : 0.0;
+                double q1 = lane < kWarps ? red[32 + lane] : 0.0;
+                q0 = warp_sum_v(q0);
+                q1 = warp_sum_v(q1);
+                if (lane == 0) {
+                    a.part[2 * blockIdx.x] = q0;
+                    a.part[2 * blockIdx.x + 1] = q1;
+                }
+            }
+        }
+    }
+}
+
+// Hub rows (degree > kWarpNnz, rows [0, n_hub) of the view): one warp per row sums the
+// row's chunk partials in chunk order and runs the fused epilogue.  Chunk tiles of row h
+// are the consecutive tiles [hub_first[h], hub_first[h+1]).
+template <int EPI, class RP, class V>
+__global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const int* __restrict__ hub_first,
+                                                      int64_t n_hub) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < n_hub;
+         h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int f0 = hub_first[h], f1 = hub_first[h + 1];
+        V tot = V(0);
+        for (int q = f0 + lane; q < f1; q += 32) tot += (V)a.hub_part[q];
+        tot = warp_sum_v(tot);
+        if (lane == 0) {
+            const int64_t deg = a.rp[h + 1] - a.rp[h];
+            double q0 = 0.0, q1 = 0.0;
+            const V hp = EPI != EPI_PLAIN ? prev_src<EPI>(a)[h] : V(0);
+            const V ha = EPI == EPI_CPAA ? a.acc[h] : V(0);
+            epilogue_v<EPI>(a, h, tot, deg, hp, ha, q0, q1);
+            if (a.hub_ts) {
+                a.hub_ts[2 * h] = q0;
+                a.hub_ts[2 * h + 1] = q1;
             }
         }
     }
@@ -496,13 +722,6 @@ inline int grid1d(int64_t n) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
 }
 
-BinTable bin_table(const SolverView& V) {
-    BinTable t{};
-    t.nb = (int)V.bins.size();
-    for (int i = 0; i < t.nb; ++i) t.b[i] = V.bins[i];
-    return t;
-}
-
 // Layout the solve runs on: FAST -> degree-binned view; BITEXACT -> reference order.
 struct Layout {
     bool fast;
@@ -540,11 +759,6 @@ TermArgs<RP, V> base_args(cheb_graph* g, const Layout& L) {
     a.rp = static_cast<const RP*>(L.rp);
     a.col = L.col;
     a.inv = L.inv;
-    if (L.fast) {
-        a.chunk_row = g->view.chunk_row.ptr<int>();
-        a.chunk_idx = g->view.chunk_idx.ptr<int>();
-        a.hub_first = g->view.hub_first.ptr<int>();
-    }
     return a;
 }
 
@@ -553,7 +767,26 @@ template <int EPI, class RP, class V>
 int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
     cudaStream_t st = g->stream;
     if (L.fast) {
-        k_term_fast<EPI, RP, V><<<g->view.grid, kThreads, 0, st>>>(a, bin_table(g->view));
+        static bool attr_set = false;  // per template instance
+        constexpr size_t smem = warp_smem_bytes<V>();
+        if (!attr_set) {
+            CHEB_CUDA_CHECK(cudaFuncSetAttribute(k_term_warp<EPI, RP, V>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set = true;
+        }
+        int H = (int)std::min<int64_t>(g->n, hot_capacity<V>());
+        if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);
+        TermArgs<RP, V> ab = a;
+        ab.tune_nogather = tuning().nogather;
+        k_term_warp<EPI, RP, V><<<g->view.grid, kWarps * 32, smem, st>>>(ab, g->view.tiles.ptr<Tile>(),
+                                                                          g->view.n_tiles, H);
+        if (g->view.n_hub > 0) {
+            CHEB_CUDA_CHECK(cudaGetLastError());
+            const int hb = (int)std::min<int64_t>((g->view.n_hub * 32 + 255) / 256, 148 * 16);
+            k_hub_finalize<EPI, RP, V><<<hb, 256, 0, st>>>(a, g->view.hub_first.ptr<int>(), g->view.n_hub);
+            CHEB_CUDA_CHECK(cudaGetLastError());
+            return 2;
+        }
     } else {
         if constexpr (std::is_same<V, double>::value) {
             k_term_exact<EPI, RP><<<grid1d(g->n), kThreads, 0, st>>>(a, g->n);
@@ -582,7 +815,7 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     w.out.ensure(vb);
     const int grid = std::max(g->view.ready ? g->view.grid : 1, grid1d(n));
     w.part.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max(grid, 1));
-    w.hub_part.ensure(sizeof(double) * std::max(g->view.n_chunks, 1));
+    w.hub_part.ensure(sizeof(double) * std::max(g->view.n_tiles, 1));
     if (!w.hub_cnt || w.hub_cnt.bytes() < sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1)) {
         w.hub_cnt.alloc(sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1));
         CHEB_CUDA_CHECK(cudaMemset(w.hub_cnt.get(), 0, w.hub_cnt.bytes()));
