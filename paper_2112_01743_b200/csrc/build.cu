@@ -580,9 +580,10 @@ static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
     *n_hub = 0;
     *n_chunk_tiles = 0;
     auto lanes_log2 = [](int64_t dmax, int64_t rows) {
-        // as many lanes per row as the 32 lanes allow, but no more than the degree needs
+        // lanes per row: as many as 32 lanes allow for the tile's rows, but no more than
+        // ~dmax/4 (each lane then walks >= 4 nnz; rows of a tile have similar degree)
         int lg = 0;
-        while (lg < 5 && (rows << (lg + 1)) <= 32 && (int64_t(1) << (lg + 1)) <= dmax * 2) ++lg;
+        while (lg < 5 && (rows << (lg + 1)) <= 32 && (int64_t(4) << (lg + 1)) <= dmax + 3) ++lg;
         return lg;
     };
     auto close = [&] {

@@ -233,10 +233,6 @@ constexpr int hot_capacity() { return (kHotBytes / (int)sizeof(V)); }
 template <class V>
 struct alignas(16) WarpScratch {
     int colb[2][kColBuf];   // TMA landing buffers for the column ids of the next tiles
-    int wend[33];           // tile-local row end positions (+1 guard)
-    int tailr[32];          // row continued past each lane (-1 none)
-    V wsum[32];             // row sums
-    V tailv[32];            // open partial of each lane
     uint64_t mbar[2];
 };
 
@@ -274,19 +270,24 @@ __device__ __forceinline__ void issue_cols(const int* __restrict__ col, const Ti
     bulk_g2s(buf, col + a0, bytes, mbar);
 }
 
-// Streaming operands of a pack tile (row ends, T_{k-1}, acc): one row per lane.
+// Streaming operands of a pack tile for the lane that leads row g's lane group
+// (L = 1 << lg lanes per row): tile-local row start/end, T_{k-1}, acc.
 template <int EPI, class RP, class V>
-__device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR& t, int& end, V& pv,
-                                          V& av) {
+__device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR& t, int& rs, int& re,
+                                          V& pv, V& av) {
     const int lane = threadIdx.x & 31;
-    end = 0;
+    rs = 0;
+    re = 0;
     pv = V(0);
     av = V(0);
     if (t.meta & kTileChunk) return;
-    if (lane < t.rows) {
-        end = (int)(a.rp[t.r0 + lane + 1] - t.z0);
-        if constexpr (EPI != EPI_PLAIN) pv = prev_src<EPI>(a)[t.r0 + lane];
-        if constexpr (EPI == EPI_CPAA) av = a.acc[t.r0 + lane];
+    const int lg = t.meta & 0xf;
+    const int g = lane >> lg;
+    if ((lane & ((1 << lg) - 1)) == 0 && g < t.rows) {
+        rs = (int)(a.rp[t.r0 + g] - t.z0);
+        re = (int)(a.rp[t.r0 + g + 1] - t.z0);
+        if constexpr (EPI != EPI_PLAIN) pv = prev_src<EPI>(a)[t.r0 + g];
+        if constexpr (EPI == EPI_CPAA) av = a.acc[t.r0 + g];
     }
 }
 
@@ -330,9 +331,9 @@ k_term_warp(TermArgs<RP, V> a, const Tile* __restrict__ tiles, int ntiles, int H
     TileR cur = load_tile(tiles, t, ntiles);
     TileR nxt = load_tile(tiles, t + stride, ntiles);
     if (lane == 0 && t < ntiles) issue_cols(a.col, cur, ws.colb[0], &ws.mbar[0]);
-    int end, nend;
+    int rs, re, nrs, nre;
     V pv, av, npv, nav;
-    load_rows<EPI>(a, cur, end, pv, av);
+    load_rows<EPI>(a, cur, rs, re, pv, av);
     unsigned phase = 0;  // bit b = parity of buffer b
     double p0 = 0.0, p1 = 0.0;
     mbar_wait(&mbar_hot, 0);
@@ -342,114 +343,72 @@ k_term_warp(TermArgs<RP, V> a, const Tile* __restrict__ tiles, int ntiles, int H
         const int b = i & 1;
         const bool has_next = t + stride < ntiles;
         if (lane == 0 && has_next) issue_cols(a.col, nxt, ws.colb[b ^ 1], &ws.mbar[b ^ 1]);
-        load_rows<EPI>(a, nxt, nend, npv, nav);
+        load_rows<EPI>(a, nxt, nrs, nre, npv, nav);
         const TileR nn = load_tile(tiles, t + 2 * stride, ntiles);
 
         mbar_wait(&ws.mbar[b], (phase >> b) & 1u);
         phase ^= 1u << b;
-        // lane owns tile-local positions P = 8*lane + q - off, q < 8 (contiguous)
-        const int off = (int)(cur.z0 & 7);
-        const int P0 = 8 * lane - off;
-        int c[U];
-        {
-            const int4 lo = *reinterpret_cast<const int4*>(&ws.colb[b][8 * lane]);
-            const int4 hi = *reinterpret_cast<const int4*>(&ws.colb[b][8 * lane + 4]);
-            const int cc[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-#pragma unroll
-            for (int q = 0; q < U; ++q) c[q] = (P0 + q >= 0 && P0 + q < cur.cnt) ? cc[q] : -1;
-        }
-        V v[U];
-        if (a.tune_nogather) {
-#pragma unroll
-            for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
-        } else {
-            gather8(a.x_in, hot, H, c, v);
-        }
+        const int* cb = ws.colb[b] + (int)(cur.z0 & 7);  // tile-local position p at cb[p]
 
         if (cur.meta & kTileChunk) {
-            // slice of a row with degree > kWarpNnz: partial only; the row is completed by
-            // k_hub_finalize after this kernel (kernel boundary orders it; no fences)
-            V s = V(0);
-#pragma unroll
-            for (int q = 0; q < U; ++q) s += v[q];
-            s = warp_sum_v(s);
-            if (lane == 0) a.hub_part[t] = (double)s;
-        } else {
-            // rows of the tile: wend[i] = tile-local end of row i (one row per lane)
-            const int rows = cur.rows;
-            if (lane < rows) {
-                ws.wend[lane] = end;
-                ws.wsum[lane] = V(0);
-            }
-            __syncwarp();
-            // merge-path walk over the lane's contiguous positions
-            const int pf = max(P0, 0), pl = min(P0 + U, cur.cnt);  // [pf, pl) valid
-            int r = 0;
-            if (pf < pl) {
-                // first row whose end is past pf (rows <= 32: binary search in smem)
-                int lo = 0, hi = rows - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi) >> 1;
-                    if (ws.wend[mid] > pf) hi = mid;
-                    else lo = mid + 1;
-                }
-                r = lo;
-            }
-            int rstart = r ? ws.wend[r - 1] : 0;
-            int rend = ws.wend[r < rows ? r : rows - 1];
-            V run = V(0);
-            V head = V(0);
-            int head_row = -1;  // row whose start lies before pf and ends in this lane
+            // slice of a row with degree > kWarpNnz: lane owns positions lane + 32 q; the
+            // partial completes in k_hub_finalize after this kernel (no fences)
+            int c[U];
 #pragma unroll
             for (int q = 0; q < U; ++q) {
-                const int P = P0 + q;
-                if (P >= pf && P < pl) {
-                    while (P >= rend) {
-                        if (rstart < pf) {
-                            head = run;
-                            head_row = r;
-                        } else {
-                            ws.wsum[r] = run;
-                        }
-                        ++r;
-                        run = V(0);
-                        rstart = rend;
-                        rend = ws.wend[r];
-                    }
-                    run += v[q];
-                }
+                const int p = lane + 32 * q;
+                c[q] = p < cur.cnt ? cb[p] : -1;
             }
-            int tail_row = -1;
-            if (pf < pl) {
-                if (rend == pl) {  // the open row ends exactly at the lane's last position
-                    if (rstart < pf) {
-                        head = run;
-                        head_row = r;
-                    } else {
-                        ws.wsum[r] = run;
-                    }
+            V v[U];
+            if (a.tune_nogather) {
+#pragma unroll
+                for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
+            } else {
+                gather8(a.x_in, hot, H, c, v);
+            }
+            V sum = V(0);
+#pragma unroll
+            for (int q = 0; q < U; ++q) sum += v[q];
+            sum = warp_sum_v(sum);
+            if (lane == 0) a.hub_part[t] = (double)sum;
+        } else {
+            // rows of similar degree (degree-sorted view): L lanes per row, row g owned by
+            // lanes [g L, g L + L); its leader prefetched start/end/T_{k-1}/acc
+            const int lg = cur.meta & 0xf;
+            const int L = 1 << lg;
+            const int li = lane & (L - 1), g = lane >> lg;
+            int rb = rs, rend = re;
+            if (lg) {
+                const int leader = lane & ~(L - 1);
+                rb = __shfl_sync(0xffffffffu, rs, leader);
+                rend = __shfl_sync(0xffffffffu, re, leader);
+            }
+            V sum = V(0);
+            for (int j = rb + li; j < rend; j += 4 * L) {
+                int c[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) c[q] = j + q * L < rend ? cb[j + q * L] : -1;
+                V v[4];
+                if (a.tune_nogather) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
                 } else {
-                    tail_row = r;  // continues into the next lane(s)
+                    gather8(a.x_in, hot, H, c, v);
                 }
+                sum += v[0];
+                sum += v[1];
+                sum += v[2];
+                sum += v[3];
             }
-            ws.tailv[lane] = run;
-            ws.tailr[lane] = tail_row;
-            __syncwarp();
-            if (head_row >= 0) {  // add the carries of the preceding lanes, nearest first
-                V tot = head;
-                for (int j = lane - 1; j >= 0 && ws.tailr[j] == head_row; --j) tot += ws.tailv[j];
-                ws.wsum[head_row] = tot;
-            }
-            __syncwarp();
-            if (lane < rows) {
-                const int b0 = lane ? ws.wend[lane - 1] : 0;
-                epilogue_v<EPI>(a, (int64_t)cur.r0 + lane, ws.wsum[lane], (int64_t)(end - b0), pv, av, p0, p1);
-            }
+            for (int o = L >> 1; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (li == 0 && g < cur.rows)
+                epilogue_v<EPI>(a, (int64_t)cur.r0 + g, sum, (int64_t)(rend - rb), pv, av, p0, p1);
         }
         __syncwarp();
         cur = nxt;
         nxt = nn;
-        end = nend;
+        rs = nrs;
+        re = nre;
         pv = npv;
         av = nav;
     }
