@@ -717,6 +717,25 @@ static void build_view_t(cheb_graph* g) {
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         V.grid = std::max(1, std::min(sms, (V.n_tiles + kWarps - 1) / kWarps));
     }
+    {   // per-warp programs (warp-major), padded to whole descriptor blocks
+        const int S = V.grid * kWarps;
+        const int per = (V.n_tiles + S - 1) / S;
+        V.prog_len = std::max(kDescBlock, (per + kDescBlock - 1) / kDescBlock * kDescBlock);
+        std::vector<WTile> prog((size_t)S * V.prog_len, WTile{0, 0, 0, 0, 0});
+        for (int t = 0; t < V.n_tiles; ++t) {
+            const Tile& a = tiles[t];
+            const Tile& b = tiles[t + 1];
+            WTile w;
+            w.nnz_begin = a.nnz_begin;
+            w.row_begin = a.row_begin;
+            w.cnt = (uint16_t)(b.nnz_begin - a.nnz_begin);
+            w.rows = (uint8_t)((a.meta & kTileChunk) ? 1 : (b.row_begin - a.row_begin));
+            w.meta = (uint8_t)a.meta;
+            prog[(size_t)(t % S) * V.prog_len + t / S] = w;
+        }
+        V.prog.alloc(sizeof(WTile) * prog.size());
+        CHEB_CUDA_CHECK(cudaMemcpy(V.prog.get(), prog.data(), sizeof(WTile) * prog.size(), cudaMemcpyHostToDevice));
+    }
     V.tiles.alloc(sizeof(Tile) * tiles.size());
     CHEB_CUDA_CHECK(cudaMemcpy(V.tiles.get(), tiles.data(), sizeof(Tile) * tiles.size(), cudaMemcpyHostToDevice));
     V.ready = true;

@@ -106,6 +106,17 @@ struct Tile {
     int32_t row_begin;
     int32_t meta;
 };
+// A tile as stored in a warp's program (warp-major copy of the tiles the warp visits:
+// tile t = w + i * (grid * kWarps) is entry i of warp w).
+struct WTile {
+    int64_t nnz_begin;
+    int32_t row_begin;
+    uint16_t cnt;
+    uint8_t rows;
+    uint8_t meta;
+};
+static_assert(sizeof(WTile) == 16, "WTile is 16 bytes");
+constexpr int kDescBlock = 8;        // descriptors per TMA refill of a warp's program ring
 constexpr int kThreads = 256;        // CTA size of the auxiliary kernels
 constexpr int kWarps = 32;           // warps per CTA of the term kernel (1 CTA / SM)
 constexpr int kWarpNnz = 248;        // nnz per tile: with <= 7 alignment slots, 8 per lane
@@ -122,6 +133,8 @@ struct SolverView {
     DevMem col;        // int32 [nnz] (renamed ids, storage order kept)
     DevMem inv;        // double [n] (new order) only when inv_degree is non-canonical
     DevMem tiles;      // Tile [n_tiles + 1]
+    DevMem prog;       // WTile [grid * kWarps][prog_len]: per-warp tile programs
+    int prog_len = 0;  // entries per warp (multiple of kDescBlock)
     int n_tiles = 0;
     int grid = 0;          // CTAs of one term launch (persistent: one per SM)
     int64_t n_hub = 0;     // rows [0, n_hub) with degree > kWarpNnz (chunk tiles)

@@ -232,8 +232,10 @@ constexpr int hot_capacity() { return (kHotBytes / (int)sizeof(V)); }
 // Per-warp shared scratch of the term kernel.
 template <class V>
 struct alignas(16) WarpScratch {
-    int colb[2][kColBuf];   // TMA landing buffers for the column ids of the next tiles
-    uint64_t mbar[2];
+    int colb[2][kColBuf];   // TMA landing buffers: column ids of the current / next tile
+    WTile desc[2][kDescBlock];  // TMA ring of this warp's tile program
+    uint64_t colm[2];       // mbarriers of colb
+    uint64_t descm[2];      // mbarriers of desc
 };
 
 template <class V>
@@ -247,21 +249,17 @@ struct TileR {
     int r0, rows, cnt, meta;
 };
 
-__device__ __forceinline__ TileR load_tile(const Tile* __restrict__ tiles, int t, int ntiles) {
-    TileR r{0, 0, 0, 0, 0};
-    if (t < ntiles) {
-        const Tile a = tiles[t], b = tiles[t + 1];
-        r.z0 = a.nnz_begin;
-        r.r0 = a.row_begin;
-        r.meta = a.meta;
-        r.cnt = (int)(b.nnz_begin - a.nnz_begin);
-        r.rows = (a.meta & kTileChunk) ? 1 : (b.row_begin - a.row_begin);
-    }
+__device__ __forceinline__ TileR tile_of(const WTile& d) {
+    TileR r;
+    r.z0 = d.nnz_begin;
+    r.r0 = d.row_begin;
+    r.cnt = d.cnt;
+    r.rows = d.rows;
+    r.meta = d.meta;
     return r;
 }
 
-// Lane 0: bulk-copy the tile's column ids from the 8-aligned position a0 = z0 & ~7 (so
-// lane l's 8 positions a0+8l.. are two 16-byte shared loads) into buf.
+// Lane 0: bulk-copy the tile's column ids from the 8-aligned position a0 = z0 & ~7 into buf.
 __device__ __forceinline__ void issue_cols(const int* __restrict__ col, const TileR& t, int* buf,
                                            uint64_t* mbar) {
     const int64_t a0 = t.z0 & ~int64_t(7);
@@ -270,50 +268,145 @@ __device__ __forceinline__ void issue_cols(const int* __restrict__ col, const Ti
     bulk_g2s(buf, col + a0, bytes, mbar);
 }
 
-// Streaming operands of a pack tile for the lane that leads row g's lane group
-// (L = 1 << lg lanes per row): tile-local row start/end, T_{k-1}, acc.
+// Row operands of a pack tile for the lane leading row g's lane group (L = 1 << lg lanes
+// per row): tile-local row start/end, T_{k-1}, acc.
+template <class V>
+struct RowOps {
+    int rs, re;
+    V pv, av;
+};
+
 template <int EPI, class RP, class V>
-__device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR& t, int& rs, int& re,
-                                          V& pv, V& av) {
+__device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR& t, RowOps<V>& o) {
     const int lane = threadIdx.x & 31;
-    rs = 0;
-    re = 0;
-    pv = V(0);
-    av = V(0);
+    o.rs = 0;
+    o.re = 0;
+    o.pv = V(0);
+    o.av = V(0);
     if (t.meta & kTileChunk) return;
     const int lg = t.meta & 0xf;
     const int g = lane >> lg;
     if ((lane & ((1 << lg) - 1)) == 0 && g < t.rows) {
-        rs = (int)(a.rp[t.r0 + g] - t.z0);
-        re = (int)(a.rp[t.r0 + g + 1] - t.z0);
-        if constexpr (EPI != EPI_PLAIN) pv = prev_src<EPI>(a)[t.r0 + g];
-        if constexpr (EPI == EPI_CPAA) av = a.acc[t.r0 + g];
+        o.rs = (int)(a.rp[t.r0 + g] - t.z0);
+        o.re = (int)(a.rp[t.r0 + g + 1] - t.z0);
+        if constexpr (EPI != EPI_PLAIN) o.pv = prev_src<EPI>(a)[t.r0 + g];
+        if constexpr (EPI == EPI_CPAA) o.av = a.acc[t.r0 + g];
+    }
+}
+
+// Lane 0: bulk-copy descriptor block blk of this warp's program into ring slot blk & 1.
+__device__ __forceinline__ void issue_desc(const WTile* my, int blk, WarpScratch<double>* unused,
+                                           WTile* slot, uint64_t* mbar) {
+    (void)unused;
+    mbar_expect_tx(mbar, kDescBlock * sizeof(WTile));
+    bulk_g2s(slot, my + (size_t)blk * kDescBlock, kDescBlock * sizeof(WTile), mbar);
+}
+
+// One tile of the warp's program.  cur: this tile's row operands (loaded one tile ago);
+// nxt receives the next tile's.  No register prefetched here is copied at the end.
+template <int EPI, class RP, class V, class WS>
+__device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, const V* hot, int H, WS& ws,
+                                          const WTile* my, int w, int S, int nt, int i,
+                                          const RowOps<V>& cur, RowOps<V>& nxt, double& p0, double& p1) {
+    const int lane = threadIdx.x & 31;
+    constexpr int U = 8;
+    const TileR d = tile_of(ws.desc[(i / kDescBlock) & 1][i % kDescBlock]);
+    if (i + 1 < nt) {
+        const int j = i + 1;
+        if (j % kDescBlock == 0) mbar_wait(&ws.descm[(j / kDescBlock) & 1], ((j / kDescBlock) >> 1) & 1);
+        const TileR dn = tile_of(ws.desc[(j / kDescBlock) & 1][j % kDescBlock]);
+        if (lane == 0) issue_cols(a.col, dn, ws.colb[j & 1], &ws.colm[j & 1]);
+        load_rows<EPI>(a, dn, nxt);
+    }
+    const int t = w + i * S;  // tile id (slot of a hub-row partial)
+    mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
+    const int* cb = ws.colb[i & 1] + (int)(d.z0 & 7);  // tile-local position p at cb[p]
+
+    if (d.meta & kTileChunk) {
+        // slice of a row with degree > kWarpNnz: partial only; completed by k_hub_finalize
+        int c[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int pp = lane + 32 * q;
+            c[q] = pp < d.cnt ? cb[pp] : -1;
+        }
+        V v[U];
+        if (a.tune_nogather) {
+#pragma unroll
+            for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
+        } else {
+            gather8(a.x_in, hot, H, c, v);
+        }
+        V sum = V(0);
+#pragma unroll
+        for (int q = 0; q < U; ++q) sum += v[q];
+        sum = warp_sum_v(sum);
+        if (lane == 0) a.hub_part[t] = (double)sum;
+    } else {
+        // rows of similar degree: L lanes per row, row g owned by lanes [g L, g L + L)
+        const int lg = d.meta & 0xf;
+        const int L = 1 << lg;
+        const int li = lane & (L - 1), g = lane >> lg;
+        int rb = cur.rs, rend = cur.re;
+        if (lg) {
+            const int leader = lane & ~(L - 1);
+            rb = __shfl_sync(0xffffffffu, rb, leader);
+            rend = __shfl_sync(0xffffffffu, rend, leader);
+        }
+        V sum = V(0);
+        for (int jj = rb + li; jj < rend; jj += 4 * L) {
+            int c[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
+            V v[4];
+            if (a.tune_nogather) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
+            } else {
+                gather8(a.x_in, hot, H, c, v);
+            }
+            sum += v[0];
+            sum += v[1];
+            sum += v[2];
+            sum += v[3];
+        }
+        for (int o = L >> 1; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (li == 0 && g < d.rows)
+            epilogue_v<EPI>(a, (int64_t)d.r0 + g, sum, (int64_t)(rend - rb), cur.pv, cur.av, p0, p1);
+    }
+    __syncwarp();
+    // descriptor block of tile i fully consumed: refill its slot two blocks ahead
+    if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
+        const int blk = i / kDescBlock + 2;
+        if (blk * kDescBlock < nt) issue_desc(my, blk, nullptr, ws.desc[blk & 1], &ws.descm[blk & 1]);
     }
 }
 
 template <int EPI, class RP, class V>
 __global__ void __launch_bounds__(kWarps * 32, 1)
-k_term_warp(TermArgs<RP, V> a, const Tile* __restrict__ tiles, int ntiles, int H) {
+k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles, int H) {
     extern __shared__ __align__(16) unsigned char smem[];
     V* hot = reinterpret_cast<V*>(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpScratch<V>& ws = reinterpret_cast<WarpScratch<V>*>(smem + kHotBytes)[warp];
     double* red = reinterpret_cast<double*>(smem + kHotBytes + kWarps * sizeof(WarpScratch<V>));
     __shared__ __align__(8) uint64_t mbar_hot;
-    constexpr bool kPrev = EPI != EPI_PLAIN;
-    constexpr bool kAcc = EPI == EPI_CPAA;
-    constexpr int U = 8;  // positions per lane
+
+    const int S = gridDim.x * kWarps;
+    const int w = blockIdx.x * kWarps + warp;
+    const int nt = w < ntiles ? (ntiles - w + S - 1) / S : 0;
+    const WTile* my = prog + (size_t)w * P;
 
     // hot prefix x_k[0..H) -> shared memory (TMA bulk copies; sub-16-byte tail by loads)
     const unsigned hot_bytes = (unsigned)(H * sizeof(V)) & ~15u;
-    if (threadIdx.x == 0) {
-        mbar_init(&mbar_hot, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    if (threadIdx.x == 0) mbar_init(&mbar_hot, 1);
     if (lane == 0) {
-        mbar_init(&ws.mbar[0], 1);
-        mbar_init(&ws.mbar[1], 1);
+        mbar_init(&ws.colm[0], 1);
+        mbar_init(&ws.colm[1], 1);
+        mbar_init(&ws.descm[0], 1);
+        mbar_init(&ws.descm[1], 1);
     }
+    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     if (threadIdx.x == 0) {
         mbar_expect_tx(&mbar_hot, hot_bytes);
@@ -322,95 +415,27 @@ k_term_warp(TermArgs<RP, V> a, const Tile* __restrict__ tiles, int ntiles, int H
             bulk_g2s(smem + off, reinterpret_cast<const unsigned char*>(a.x_in) + off,
                      min(kPiece, hot_bytes - off), &mbar_hot);
     }
+    if (lane == 0) {
+        if (nt > 0) issue_desc(my, 0, nullptr, ws.desc[0], &ws.descm[0]);
+        if (nt > kDescBlock) issue_desc(my, 1, nullptr, ws.desc[1], &ws.descm[1]);
+    }
     for (int i = hot_bytes / sizeof(V) + threadIdx.x; i < H; i += blockDim.x) hot[i] = ldg_x(a.x_in + i);
 
-    // software pipeline over this warp's tiles: columns of tile i+1 arrive by TMA and its
-    // row operands by registers while tile i gathers.
-    const int stride = gridDim.x * kWarps;
-    int t = blockIdx.x * kWarps + warp;
-    TileR cur = load_tile(tiles, t, ntiles);
-    TileR nxt = load_tile(tiles, t + stride, ntiles);
-    if (lane == 0 && t < ntiles) issue_cols(a.col, cur, ws.colb[0], &ws.mbar[0]);
-    int rs, re, nrs, nre;
-    V pv, av, npv, nav;
-    load_rows<EPI>(a, cur, rs, re, pv, av);
-    unsigned phase = 0;  // bit b = parity of buffer b
+    RowOps<V> A, B;
+    if (nt > 0) {
+        mbar_wait(&ws.descm[0], 0);
+        const TileR d0 = tile_of(ws.desc[0][0]);
+        if (lane == 0) issue_cols(a.col, d0, ws.colb[0], &ws.colm[0]);
+        load_rows<EPI>(a, d0, A);
+    }
     double p0 = 0.0, p1 = 0.0;
     mbar_wait(&mbar_hot, 0);
     __syncthreads();
 
-    for (int i = 0; t < ntiles; t += stride, ++i) {
-        const int b = i & 1;
-        const bool has_next = t + stride < ntiles;
-        if (lane == 0 && has_next) issue_cols(a.col, nxt, ws.colb[b ^ 1], &ws.mbar[b ^ 1]);
-        load_rows<EPI>(a, nxt, nrs, nre, npv, nav);
-        const TileR nn = load_tile(tiles, t + 2 * stride, ntiles);
-
-        mbar_wait(&ws.mbar[b], (phase >> b) & 1u);
-        phase ^= 1u << b;
-        const int* cb = ws.colb[b] + (int)(cur.z0 & 7);  // tile-local position p at cb[p]
-
-        if (cur.meta & kTileChunk) {
-            // slice of a row with degree > kWarpNnz: lane owns positions lane + 32 q; the
-            // partial completes in k_hub_finalize after this kernel (no fences)
-            int c[U];
-#pragma unroll
-            for (int q = 0; q < U; ++q) {
-                const int p = lane + 32 * q;
-                c[q] = p < cur.cnt ? cb[p] : -1;
-            }
-            V v[U];
-            if (a.tune_nogather) {
-#pragma unroll
-                for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
-            } else {
-                gather8(a.x_in, hot, H, c, v);
-            }
-            V sum = V(0);
-#pragma unroll
-            for (int q = 0; q < U; ++q) sum += v[q];
-            sum = warp_sum_v(sum);
-            if (lane == 0) a.hub_part[t] = (double)sum;
-        } else {
-            // rows of similar degree (degree-sorted view): L lanes per row, row g owned by
-            // lanes [g L, g L + L); its leader prefetched start/end/T_{k-1}/acc
-            const int lg = cur.meta & 0xf;
-            const int L = 1 << lg;
-            const int li = lane & (L - 1), g = lane >> lg;
-            int rb = rs, rend = re;
-            if (lg) {
-                const int leader = lane & ~(L - 1);
-                rb = __shfl_sync(0xffffffffu, rs, leader);
-                rend = __shfl_sync(0xffffffffu, re, leader);
-            }
-            V sum = V(0);
-            for (int j = rb + li; j < rend; j += 4 * L) {
-                int c[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) c[q] = j + q * L < rend ? cb[j + q * L] : -1;
-                V v[4];
-                if (a.tune_nogather) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
-                } else {
-                    gather8(a.x_in, hot, H, c, v);
-                }
-                sum += v[0];
-                sum += v[1];
-                sum += v[2];
-                sum += v[3];
-            }
-            for (int o = L >> 1; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            if (li == 0 && g < cur.rows)
-                epilogue_v<EPI>(a, (int64_t)cur.r0 + g, sum, (int64_t)(rend - rb), pv, av, p0, p1);
-        }
-        __syncwarp();
-        cur = nxt;
-        nxt = nn;
-        rs = nrs;
-        re = nre;
-        pv = npv;
-        av = nav;
+    for (int i = 0; i < nt; i += 2) {
+        term_step<EPI>(a, hot, H, ws, my, w, S, nt, i, A, B, p0, p1);
+        if (i + 1 >= nt) break;
+        term_step<EPI>(a, hot, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
     }
     if constexpr (EPI == EPI_CPAA || EPI == EPI_POWER) {
         if (a.part) {
@@ -737,8 +762,8 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);
         TermArgs<RP, V> ab = a;
         ab.tune_nogather = tuning().nogather;
-        k_term_warp<EPI, RP, V><<<g->view.grid, kWarps * 32, smem, st>>>(ab, g->view.tiles.ptr<Tile>(),
-                                                                          g->view.n_tiles, H);
+        k_term_warp<EPI, RP, V><<<g->view.grid, kWarps * 32, smem, st>>>(
+            ab, g->view.prog.ptr<WTile>(), g->view.prog_len, g->view.n_tiles, H);
         if (g->view.n_hub > 0) {
             CHEB_CUDA_CHECK(cudaGetLastError());
             const int hb = (int)std::min<int64_t>((g->view.n_hub * 32 + 255) / 256, 148 * 16);
