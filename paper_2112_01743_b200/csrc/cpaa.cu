@@ -144,10 +144,22 @@ __device__ __forceinline__ void epilogue(const TermArgs<RP, V>& a, int64_t u, V 
 // (tools/micro_gather.cu): random LDS.64 876 G/s vs random LDG over an L2-resident
 // table 256 G/s — the gather, not HBM, bounds this path.
 
-// Gather x[c[q]] for the lane's 8 column ids: cold ids (>= H) as predicated global loads
-// issued back to back, hot ids as predicated shared loads; c < 0 = no element (0).
+__device__ __forceinline__ double lds_v(unsigned addr, double) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float lds_v(unsigned addr, float) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+// Gather x[c[q]] for a lane's column ids: cold ids (>= H) as predicated global loads
+// issued back to back, hot ids from the shared-memory copy at 32-bit address hot_s;
+// c < 0 = no element (0).
 template <class V, int U>
-__device__ __forceinline__ void gather8(const V* __restrict__ x, const V* hot, int H, const int (&c)[U],
+__device__ __forceinline__ void gather8(const V* __restrict__ x, unsigned hot_s, int H, const int (&c)[U],
                                         V (&v)[U]) {
 #pragma unroll
     for (int q = 0; q < U; ++q) {
@@ -156,7 +168,7 @@ __device__ __forceinline__ void gather8(const V* __restrict__ x, const V* hot, i
     }
 #pragma unroll
     for (int q = 0; q < U; ++q)
-        if ((unsigned)c[q] < (unsigned)H) v[q] = hot[c[q]];
+        if ((unsigned)c[q] < (unsigned)H) v[q] = lds_v(hot_s + (unsigned)c[q] * (unsigned)sizeof(V), V(0));
 }
 
 // TMA bulk copy global -> shared (cp.async.bulk), completion on an mbarrier.
@@ -302,10 +314,15 @@ __device__ __forceinline__ void issue_desc(const WTile* my, int blk, WarpScratch
     bulk_g2s(slot, my + (size_t)blk * kDescBlock, kDescBlock * sizeof(WTile), mbar);
 }
 
+#ifndef CHEB_PACK_UNROLL
+#define CHEB_PACK_UNROLL 4
+#endif
+constexpr int kPackUnroll = CHEB_PACK_UNROLL;  // gathers in flight per lane in pack tiles
+
 // One tile of the warp's program.  cur: this tile's row operands (loaded one tile ago);
 // nxt receives the next tile's.  No register prefetched here is copied at the end.
 template <int EPI, class RP, class V, class WS>
-__device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, const V* hot, int H, WS& ws,
+__device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot_s, int H, WS& ws,
                                           const WTile* my, int w, int S, int nt, int i,
                                           const RowOps<V>& cur, RowOps<V>& nxt, double& p0, double& p1) {
     const int lane = threadIdx.x & 31;
@@ -335,7 +352,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, const V* hot
 #pragma unroll
             for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
         } else {
-            gather8(a.x_in, hot, H, c, v);
+            gather8(a.x_in, hot_s, H, c, v);
         }
         V sum = V(0);
 #pragma unroll
@@ -354,21 +371,19 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, const V* hot
             rend = __shfl_sync(0xffffffffu, rend, leader);
         }
         V sum = V(0);
-        for (int jj = rb + li; jj < rend; jj += 4 * L) {
-            int c[4];
+        for (int jj = rb + li; jj < rend; jj += kPackUnroll * L) {
+            int c[kPackUnroll];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
-            V v[4];
+            for (int q = 0; q < kPackUnroll; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
+            V v[kPackUnroll];
             if (a.tune_nogather) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
+                for (int q = 0; q < kPackUnroll; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
             } else {
-                gather8(a.x_in, hot, H, c, v);
+                gather8(a.x_in, hot_s, H, c, v);
             }
-            sum += v[0];
-            sum += v[1];
-            sum += v[2];
-            sum += v[3];
+#pragma unroll
+            for (int q = 0; q < kPackUnroll; ++q) sum += v[q];
         }
         for (int o = L >> 1; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         if (li == 0 && g < d.rows)
@@ -387,6 +402,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles, int H) {
     extern __shared__ __align__(16) unsigned char smem[];
     V* hot = reinterpret_cast<V*>(smem);
+    const unsigned hot_s = (unsigned)__cvta_generic_to_shared(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpScratch<V>& ws = reinterpret_cast<WarpScratch<V>*>(smem + kHotBytes)[warp];
     double* red = reinterpret_cast<double*>(smem + kHotBytes + kWarps * sizeof(WarpScratch<V>));
@@ -433,9 +449,9 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
     __syncthreads();
 
     for (int i = 0; i < nt; i += 2) {
-        term_step<EPI>(a, hot, H, ws, my, w, S, nt, i, A, B, p0, p1);
+        term_step<EPI>(a, hot_s, H, ws, my, w, S, nt, i, A, B, p0, p1);
         if (i + 1 >= nt) break;
-        term_step<EPI>(a, hot, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
+        term_step<EPI>(a, hot_s, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
     }
     if constexpr (EPI == EPI_CPAA || EPI == EPI_POWER) {
         if (a.part) {
