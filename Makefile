@@ -7,9 +7,9 @@ NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-ffp-contract=off
 SRC_DIR   := paper_2112_01743_b200/csrc
 LIB_DIR   := paper_2112_01743_b200/lib
 OBJ_DIR   := build/obj
-SRCS      := $(SRC_DIR)/build.cu $(SRC_DIR)/cpaa.cu $(SRC_DIR)/capi.cu $(SRC_DIR)/generate.cu $(SRC_DIR)/coeffs.cpp
+SRCS      := $(SRC_DIR)/build.cu $(SRC_DIR)/cpaa.cu $(SRC_DIR)/capi.cu $(SRC_DIR)/generate.cu $(SRC_DIR)/spmm.cu $(SRC_DIR)/coeffs.cpp
 OBJS      := $(patsubst $(SRC_DIR)/%,$(OBJ_DIR)/%.o,$(SRCS))
-HDRS      := $(SRC_DIR)/common.cuh include/chebpr_cuda.h
+HDRS      := $(SRC_DIR)/common.cuh $(SRC_DIR)/device.cuh include/chebpr_cuda.h
 
 all: $(LIB_DIR)/libchebpr_b200.so oracle
 

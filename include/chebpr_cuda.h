@@ -158,6 +158,15 @@ cheb_status cheb_cpaa_device(cheb_graph_t g, const cheb_cpaa_opts* opts, const v
 cheb_status cheb_last_timing(cheb_graph_t g, double* loop_ms, double* term_kernel_ms,
                              int* terms, int* launches);
 
+/* Batched personalised CPAA (K5, config 5): R right-hand sides in one SpMM-shaped pass per
+ * term.  Column r starts from T_0 = e_{seeds[r]} (seeds: R vertex ids) or from the dense
+ * opts->personalization (n x R row-major) or from ones.  ranks: n x R row-major host doubles
+ * (column r normalised by totals[r]); trace rows carry sums over all R columns.  FAST only. */
+cheb_status cheb_cpaa_batch(cheb_graph_t g, const cheb_cpaa_opts* opts, const int64_t* seeds,
+                            double* ranks, double* totals, cheb_trace_row* trace, int* rounds_out);
+cheb_status cheb_cpaa_batch_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, const int64_t* seeds,
+                                    double* term_ms, int capacity, int* terms);
+
 /* Per-term kernel durations (ms) of one solve, CUDA events around every fused term launch
  * on the handle's stream (plain launches, no graph).  Used for the roofline figure. */
 cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double* term_ms,

@@ -9,7 +9,7 @@ from .api import (  # noqa: F401
     DeviceGraph, DomainError, Error, GraphStats, IterationState, MODE_BITEXACT, MODE_FAST,
     NumericError, PageRankResult, ParseError, PowerConfig, SolverConfig, TraceRow,
     UndirectedGraph, ValidationError, VertexRange, accumulate_stage, beta, build_device_graph,
-    build_graph, coefficients, device_count, err_bound, generate_stage, init_state, kahan_sum,
+    build_graph, coefficients, run_cpaa_batch, BatchResult, device_count, err_bound, generate_stage, init_state, kahan_sum,
     normalize, partition_vertices, plan_iterations, reference_pagerank, run_cpaa, run_power,
     sigma, transition_apply, upload, validate,
 )

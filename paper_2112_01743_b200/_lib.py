@@ -80,6 +80,10 @@ _SIGS = {
                                    C.POINTER(C.c_void_p), C.c_int]),
     "cheb_last_timing": (C.c_int, [C.c_void_p, F64P, F64P, IP, IP]),
     "cheb_set_tuning": (C.c_int, [C.c_char_p, C.c_int]),
+    "cheb_cpaa_batch": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), I64P, F64P, F64P,
+                                  C.POINTER(cheb_trace_row), IP]),
+    "cheb_cpaa_batch_profile": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), I64P, F64P, C.c_int,
+                                          IP]),
     "cheb_cpaa_profile": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), F64P, C.c_int, IP]),
     "cheb_power_opts_default": (None, [C.POINTER(cheb_power_opts)]),
     "cheb_power": (C.c_int, [C.c_void_p, C.POINTER(cheb_power_opts), F64P, C.c_int64, F64P,

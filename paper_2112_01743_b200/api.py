@@ -478,6 +478,45 @@ def run_cpaa(g, cfg: Optional[SolverConfig] = None, reference=None) -> PageRankR
             dg.free()
 
 
+@dataclass
+class BatchResult:
+    ranks: np.ndarray        # n x R, column r normalised
+    totals: np.ndarray       # R normalisation totals
+    trace: list              # per term, sums over all R columns
+    rounds: int = 0
+
+
+def run_cpaa_batch(g, cfg: Optional[SolverConfig] = None, seeds=None, personalization=None) -> BatchResult:
+    """Batched personalised CPAA (K5, config 5): one SpMM-shaped pass per term over R
+    right-hand sides.  ``seeds`` (R vertex ids) gives one-hot columns; ``personalization``
+    an explicit n x R block; neither = R=cfg-defined ones columns is not meaningful, so one
+    of them is required."""
+    cfg = cfg or SolverConfig()
+    n = g.n
+    if n < 1:
+        raise ValidationError("graph has no vertices")
+    sd = None if seeds is None else _i64(seeds)
+    pp = None if personalization is None else _f64(personalization)
+    if sd is None and pp is None:
+        raise ValueError("give seeds or personalization")
+    R = int(sd.size if sd is not None else pp.reshape(n, -1).shape[1])
+    dg, owned = _as_device(g, cfg.device)
+    try:
+        o = _cpaa_opts(cfg, pp)
+        o.R = R
+        cap = max(cfg.max_rounds, cfg.rounds, 1) + 1
+        tr = (L.cheb_trace_row * cap)()
+        ranks = np.zeros(n * R)
+        totals = np.zeros(R)
+        rounds = C.c_int()
+        _check(_lib().cheb_cpaa_batch(dg.handle, C.byref(o), _pi(sd), _pd(ranks), _pd(totals), tr,
+                                      C.byref(rounds)))
+        return BatchResult(ranks.reshape(n, R), totals, _trace_rows(tr, rounds.value), rounds.value)
+    finally:
+        if owned:
+            dg.free()
+
+
 class IterationState:
     """cpaa.hpp:79-82 — staged state, device-backed (same arithmetic as run_cpaa)."""
 

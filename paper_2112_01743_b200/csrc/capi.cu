@@ -368,6 +368,77 @@ cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double
     });
 }
 
+static BatchSpec batch_spec(cheb_graph* g, const cheb_cpaa_opts& o, const int64_t* seeds) {
+    need_graph(g);
+    essential(g);
+    BatchSpec b;
+    b.M = resolve_rounds(o.c, o.rounds, o.eps, o.max_rounds);
+    std::vector<double> tmp;
+    coefficients(o.c, b.M, tmp, nullptr, nullptr);
+    if (o.parallelism < 1) fail(CHEB_DOMAIN, "parallelism must be >= 1");
+    if (o.mode != CHEB_MODE_FAST) fail(CHEB_INVALID_ARG, "the batched path runs the FAST schedule only");
+    if (o.precision != CHEB_FP64 && o.precision != CHEB_FP32)
+        fail(CHEB_INVALID_ARG, "precision must be 64 or 32");
+    if (o.R < 1) fail(CHEB_INVALID_ARG, "R must be >= 1");
+    if (seeds && o.personalization) fail(CHEB_INVALID_ARG, "give seeds or a dense personalization, not both");
+    if (seeds)
+        for (int r = 0; r < o.R; ++r)
+            if (seeds[r] < 0 || seeds[r] >= g->n)
+                fail(CHEB_VALIDATION, "seed vertex " + std::to_string(seeds[r]) + " out of range");
+    b.c = o.c;
+    b.precision = o.precision;
+    b.R = o.R;
+    b.p = o.personalization;
+    b.seeds = seeds;
+    return b;
+}
+
+cheb_status cheb_cpaa_batch(cheb_graph_t g, const cheb_cpaa_opts* opts, const int64_t* seeds,
+                            double* ranks, double* totals, cheb_trace_row* trace, int* rounds_out) {
+    return guarded([&] {
+        cheb_cpaa_opts o;
+        cheb_cpaa_opts_default(&o);
+        if (opts) o = *opts;
+        BatchSpec b = batch_spec(g, o, seeds);
+        std::vector<double> tr, tot;
+        cpaa_batch_solve(g, b, tr, tot, nullptr);
+        if (ranks) read_batch_ranks(g, ranks, b.R);
+        if (totals) std::memcpy(totals, tot.data(), sizeof(double) * b.R);
+        if (trace && b.M > 0) {
+            std::vector<double> co;
+            double be, c0;
+            coefficients(b.c, b.M, co, &be, &c0);
+            double residual = static_cast<double>(g->n) * b.R * c0 * be / (1.0 - be);
+            for (int k = 1; k <= b.M; ++k) {
+                cheb_trace_row& r = trace[k - 1];
+                std::memset(&r, 0, sizeof r);
+                r.k = k;
+                r.c_k = co[k];
+                r.mass_T = tr[2 * (k - 1)];
+                r.S_k = tr[2 * (k - 1) + 1];
+                residual *= be;
+                r.residual_mass = residual;
+                r.elapsed_ms = g->last_loop_ms / b.M;
+            }
+        }
+        if (rounds_out) *rounds_out = b.M;
+    });
+}
+
+cheb_status cheb_cpaa_batch_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, const int64_t* seeds,
+                                    double* term_ms, int capacity, int* terms) {
+    return guarded([&] {
+        cheb_cpaa_opts o;
+        cheb_cpaa_opts_default(&o);
+        if (opts) o = *opts;
+        BatchSpec b = batch_spec(g, o, seeds);
+        std::vector<double> tr, tot, ms;
+        cpaa_batch_solve(g, b, tr, tot, &ms);
+        for (int k = 0; k < b.M && k < capacity; ++k) term_ms[k] = ms[k];
+        if (terms) *terms = b.M;
+    });
+}
+
 cheb_status cheb_set_tuning(const char* key, int value) {
     return guarded([&] {
         const std::string k = key ? key : "";

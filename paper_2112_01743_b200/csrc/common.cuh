@@ -165,6 +165,10 @@ struct Workspace {
     }
 };
 
+struct BatchWorkspace {
+    DevMem T0, T1, X0, X1, acc, out, part, hub_part, hub_ts, trace, colpart, totals;
+};
+
 struct StagedState {
     bool active = false;
     int mode = 0;
@@ -191,6 +195,7 @@ struct cheb_graph {
     chebgpu::SolverView view;
     chebgpu::Workspace ws;
     chebgpu::StagedState staged;
+    chebgpu::BatchWorkspace bws;
     double last_loop_ms = 0.0;
     int last_terms = 0;
     int last_launches = 0;
@@ -244,6 +249,17 @@ struct SolveSpec {
 // Fills trace (M rows of mass_T,S_k) and total on the host; throws on non-finite.
 void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool host_results, std::vector<double>* tr,
                 double* total);
+struct BatchSpec {
+    double c = 0.85;
+    int M = 0;
+    int precision = CHEB_FP64;
+    int R = 1;
+    const double* p = nullptr;      // host n x R row-major, or null
+    const int64_t* seeds = nullptr;  // host R vertex ids (one-hot columns), or null
+};
+void cpaa_batch_solve(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace,
+                      std::vector<double>& totals, std::vector<double>* term_ms);
+void read_batch_ranks(cheb_graph* g, double* ranks, int R);
 void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
                     std::vector<double>* errs, double* total);
 void read_ranks(cheb_graph* g, int precision, double* ranks);
