@@ -43,7 +43,30 @@ CONFIGS = {
                desc="R-MAT scale 22, ef 16, (0.57,0.19,0.19,0.05), relabelled, isolated dropped"),
     "c4": dict(kind="rmat", scale=25, ef=16, seed=4, drop=True, rp64=True,
                desc="R-MAT scale 25, ef 16, int64 row pointers, isolated dropped"),
+    "c5": dict(kind="chung_lu", n=1 << 22, gamma=2.1, wmin=2.0, wmax=50_000.0,
+               draws=41_943_040, seed=5, drop=False, R=64,
+               desc="Chung-Lu n=2^22, ~40M undirected edges, 64 one-hot seeds (degree >= 5), SpMM R=64"),
 }
+
+
+def c5_seeds(dg, R: int, seed: int = 5):
+    """64 seed vertices drawn uniformly (without replacement) from vertices of degree >= 5,
+    with a fixed counter-based draw (splitmix64), so both arms use the same seeds."""
+    deg = np.diff(dg.download().offsets)
+    cand = np.nonzero(deg >= 5)[0]
+    out, used, i = [], set(), 0
+    M64 = (1 << 64) - 1
+    while len(out) < R:
+        z = (seed * 0x9E3779B97F4A7C15 + i * 0xBF58476D1CE4E5B9) & M64
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+        z ^= z >> 31
+        v = int(cand[z % len(cand)])
+        i += 1
+        if v not in used:
+            used.add(v)
+            out.append(v)
+    return np.array(out, dtype=np.int64)
 
 
 def log(*a):
@@ -89,10 +112,14 @@ class Dist:
 # clocks sampling during the timed region
 # ----------------------------------------------------------------------------------------
 class Clocks:
+    """nvidia-smi sampler (5 ms period) started before the timed region; summary() keeps the
+    samples whose arrival time falls inside [mark_start, mark_end] (+ one period of slack)."""
+
     def __init__(self, device: int):
         self.device = device
         self.proc = None
-        self.lines = []
+        self.samples = []  # (host time, line)
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -101,17 +128,27 @@ class Clocks:
                  "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "5"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 3.0
+            while not self.samples and time.time() < deadline:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.samples.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+        time.sleep(0.02)
 
     def __exit__(self, *a):
         if self.proc:
@@ -124,7 +161,10 @@ class Clocks:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lo = (self.t0 or 0) - 0.006
+        hi = (self.t1 or time.time()) + 0.006
+        window = [ln for t, ln in self.samples if lo <= t <= hi]
+        for ln in window:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -139,7 +179,7 @@ class Clocks:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "period_ms": 5}
 
 
 # ----------------------------------------------------------------------------------------
@@ -261,6 +301,135 @@ def run_reference_arm(args):
 # ----------------------------------------------------------------------------------------
 # GPU arm
 # ----------------------------------------------------------------------------------------
+class Solver:
+    """One step = one CPAA solve to eps 1e-10 on the resident graph (scalar K2 path, or the
+    batched K5 path when the config has R right-hand sides)."""
+
+    def __init__(self, dg, info, cfg, precision):
+        import paper_2112_01743_b200 as cheb
+        from paper_2112_01743_b200 import _lib as L
+        self.cheb, self.L, self.lib = cheb, L, L.load()
+        self.dg, self.info, self.cfg = dg, info, cfg
+        self.R = int(cfg.get("R", 1))
+        self.M = cheb.plan_iterations(DAMPING, EPS).M
+        o = L.cheb_cpaa_opts()
+        self.lib.cheb_cpaa_opts_default(C.byref(o))
+        o.eps, o.c, o.precision, o.R = EPS, DAMPING, precision, self.R
+        self.opts = o
+        self.seeds = c5_seeds(dg, self.R) if self.R > 1 else None
+        self.d_ranks = C.c_void_p()
+
+    def _seed_ptr(self):
+        return None if self.seeds is None else self.seeds.ctypes.data_as(self.L.I64P)
+
+    def solve(self, handle=None):
+        h = handle or self.dg.handle
+        if self.R > 1:
+            self.cheb.api._check(self.lib.cheb_cpaa_batch(h, C.byref(self.opts), self._seed_ptr(),
+                                                          None, None, None, None))
+        else:
+            self.cheb.api._check(self.lib.cheb_cpaa_device(h, C.byref(self.opts), C.byref(self.d_ranks), 0))
+
+    def last_ms(self):
+        lm, tm, terms, launches = C.c_double(), C.c_double(), C.c_int(), C.c_int()
+        self.cheb.api._check(self.lib.cheb_last_timing(self.dg.handle, C.byref(lm), C.byref(tm),
+                                                       C.byref(terms), C.byref(launches)))
+        return lm.value, launches.value
+
+    def term_ms(self):
+        cap = 64
+        ms = (C.c_double * cap)()
+        terms = C.c_int()
+        if self.R > 1:
+            self.cheb.api._check(self.lib.cheb_cpaa_batch_profile(self.dg.handle, C.byref(self.opts),
+                                                                  self._seed_ptr(), ms, cap, C.byref(terms)))
+        else:
+            self.cheb.api._check(self.lib.cheb_cpaa_profile(self.dg.handle, C.byref(self.opts), ms, cap,
+                                                            C.byref(terms)))
+        return [ms[i] for i in range(terms.value)]
+
+    def e2e(self, device, steps, flush, dist):
+        """Through the reference-facing C-ABI with host buffers: pinned int64 CSR upload,
+        solve, ranks (and trace) read back to host memory, every step."""
+        import torch
+        L, lib = self.L, self.lib
+        host = self.dg.download()
+        n, R = host.n, self.R
+        off = torch.from_numpy(host.offsets).pin_memory().numpy()
+        nb = torch.from_numpy(host.neighbors).pin_memory().numpy()
+        deg, inv = host.degrees, host.inv_degree
+        ranks = torch.empty(n * R, dtype=torch.float64).pin_memory().numpy()
+        tr = (L.cheb_trace_row * 64)()
+        rounds, tot = C.c_int(), C.c_double()
+        totals = np.zeros(R)
+
+        def step():
+            h = C.c_void_p()
+            self.cheb.api._check(lib.cheb_graph_upload_csr(
+                off.ctypes.data_as(L.I64P), off.size, nb.ctypes.data_as(L.I64P), nb.size,
+                deg.ctypes.data_as(L.I64P), deg.size, inv.ctypes.data_as(L.F64P), inv.size,
+                n, int(host.m), 0, device, int(self.info["row_ptr_64"]), C.byref(h)))
+            if R > 1:
+                self.cheb.api._check(lib.cheb_cpaa_batch(h, C.byref(self.opts), self._seed_ptr(),
+                                                         ranks.ctypes.data_as(L.F64P),
+                                                         totals.ctypes.data_as(L.F64P), tr, C.byref(rounds)))
+            else:
+                self.cheb.api._check(lib.cheb_cpaa(h, C.byref(self.opts), None, 0, ranks.ctypes.data_as(L.F64P),
+                                                   tr, C.byref(rounds), C.byref(tot)))
+            lib.cheb_graph_free(h)
+
+        step()
+        dist.barrier()
+        times = []
+        for _ in range(max(1, min(steps, 5))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            step()
+            times.append(time.perf_counter() - t)
+        e2e_s = dist.max(statistics.mean(times))
+        units = self.info["nnz"] * self.R * self.M
+        return {"value": round(dist.world * units / e2e_s / 1e9, 4), "unit": "GTEPS",
+                "h2d_bytes_per_step": int(off.nbytes + nb.nbytes),
+                "d2h_bytes_per_step": int(ranks.nbytes + 2 * self.M * 8),
+                "ms_per_step": round(e2e_s * 1e3, 3),
+                "path": "cheb_graph_upload_csr(pinned int64 CSR) + " +
+                        ("cheb_cpaa_batch" if R > 1 else "cheb_cpaa") + "(host ranks) + cheb_graph_free"}
+
+
+def cpu_baseline_line(solver, cfg, args):
+    """The reference compiled unmodified (oracle/_ref) on the same CSR, all host threads; for
+    the batched config the reference has no personalisation, so one column of the restated
+    oracle loop (T_0 = e_seed) is timed single-threaded and labelled 'port'."""
+    try:
+        host = solver.dg.download()
+        if solver.R > 1:
+            from oracle import Oracle, CSR
+            o = Oracle()
+            g = CSR(host.n, host.m, host.offsets, host.neighbors, host.degrees, host.inv_degree)
+            p = np.zeros(host.n)
+            p[solver.seeds[0]] = 1.0
+            t = time.perf_counter()
+            o.run_cpaa(g, solver.M, p=p)
+            dt = time.perf_counter() - t
+            return {"value": round(host.neighbors.size * solver.M / dt / 1e9, 6), "unit": "GTEPS",
+                    "cores": 1, "kind": "port",
+                    "sample": f"restated oracle loop (oracle/cpaa_oracle.c), 1 of {solver.R} one-hot columns "
+                              f"(M={solver.M}), wall {dt * 1e3:.0f} ms; the reference has no personalisation"}
+        e = np.stack([np.repeat(np.arange(host.n), np.diff(host.offsets)), host.neighbors], 1)
+        e = e[e[:, 0] <= e[:, 1]]
+        threads = os.cpu_count() or 1
+        r = cpu_reference_run(dict(cfg, drop=False), 1, 0, threads, host_edges=e)
+        cms = statistics.mean(r["wall_ms"])
+        return {"value": round(r["nnz"] * r["M"] / (cms * 1e-3) / 1e9, 6), "unit": "GTEPS",
+                "cores": threads, "kind": "reference",
+                "sample": f"one full run_cpaa (M={r['M']}) on the same {args.config} CSR "
+                          f"({r['nnz']} entries), K={threads} threads, wall {cms:.0f} ms"}
+    except Exception as ex:  # noqa: BLE001
+        return {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
+                "sample": f"failed: {type(ex).__name__}: {ex}"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -280,135 +449,66 @@ def main():
         return run_reference_arm(args)
 
     import torch
-    import paper_2112_01743_b200 as cheb
-    from paper_2112_01743_b200 import _lib as L
 
     dist = Dist(args.gpus)
     device = dist.local
     torch.cuda.set_device(device)
     cfg = CONFIGS[args.config]
-    lib = L.load()
 
     t0 = time.perf_counter()
     dg, info = build_device(cfg, device)
     build_s = time.perf_counter() - t0
     n, nnz = info["n"], info["nnz"]
-    M = cheb.plan_iterations(DAMPING, EPS).M
-    opts = L.cheb_cpaa_opts()
-    lib.cheb_cpaa_opts_default(C.byref(opts))
-    opts.eps = EPS
-    opts.c = DAMPING
-    opts.precision = args.precision
-    d_ranks = C.c_void_p()
-
-    def solve():
-        cheb.api._check(lib.cheb_cpaa_device(dg.handle, C.byref(opts), C.byref(d_ranks), 0))
-
-    def step_ms():
-        lm, tm, terms, launches = C.c_double(), C.c_double(), C.c_int(), C.c_int()
-        cheb.api._check(lib.cheb_last_timing(dg.handle, C.byref(lm), C.byref(tm), C.byref(terms),
-                                             C.byref(launches)))
-        return lm.value, launches.value
+    sv = Solver(dg, info, cfg, args.precision)
+    M, R = sv.M, sv.R
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
     for _ in range(args.warmup):
-        solve()
-        step_ms()
+        sv.solve()
+        sv.last_ms()
     if args.profile_only:
         torch.cuda.synchronize()
-        log(f"profile-only: n={n} nnz={nnz} built in {build_s:.2f}s")
+        log(f"profile-only: n={n} nnz={nnz} R={R} built in {build_s:.2f}s")
         return 0
 
-    dist.barrier()
-    torch.cuda.synchronize()
-    times, launches = [], 0
     with Clocks(device) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        times, launches = [], 0
+        clk.mark_start()
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
-            solve()
-            ms, nl = step_ms()
+            sv.solve()
+            ms, nl = sv.last_ms()
             times.append(ms)
             launches += nl
-    torch.cuda.synchronize()
-    dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark_end()
+        dist.barrier()
     total_ms = dist.max(sum(times))
     ms_step = total_ms / args.steps
-    value = dist.world * nnz * M / (ms_step * 1e-3) / 1e9
+    value = dist.world * nnz * R * M / (ms_step * 1e-3) / 1e9
 
-    # dominant kernel: the fused term kernel, per-launch CUDA-event durations
-    cap = 64
-    term_ms = (C.c_double * cap)()
-    terms = C.c_int()
+    # dominant kernel: the fused term kernel (+ its hub-row finalize), CUDA events per term
     flush.zero_()
     torch.cuda.synchronize()
-    cheb.api._check(lib.cheb_cpaa_profile(dg.handle, C.byref(opts), term_ms, cap, C.byref(terms)))
-    tms = [term_ms[i] for i in range(terms.value)]
+    tms = sv.term_ms()
     steady = tms[1:] if len(tms) > 1 else tms
     mean_term = statistics.mean(steady)
     vbytes = 8 if args.precision == 64 else 4
     rp_bytes = 8 if info["row_ptr_64"] else 4
-    B = algorithmic_bytes(n, nnz, rp_bytes, vbytes)
+    B = algorithmic_bytes(n, nnz, rp_bytes, vbytes, R)
     peak, peak_kind = peaks()
     achieved = B / (mean_term * 1e-3) / 1e9
 
-    # e2e through the reference-facing C-ABI with host buffers (pinned), every step
-    e2e = None
-    if not args.no_e2e:
-        host = dg.download()
-        off = torch.from_numpy(host.offsets).pin_memory().numpy()
-        nb = torch.from_numpy(host.neighbors).pin_memory().numpy()
-        deg = host.degrees
-        inv = host.inv_degree
-        ranks = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
-        tr = (L.cheb_trace_row * 64)()
-        rounds, tot = C.c_int(), C.c_double()
-
-        def e2e_step():
-            h = C.c_void_p()
-            cheb.api._check(lib.cheb_graph_upload_csr(
-                off.ctypes.data_as(L.I64P), off.size, nb.ctypes.data_as(L.I64P), nb.size,
-                deg.ctypes.data_as(L.I64P), deg.size, inv.ctypes.data_as(L.F64P), inv.size,
-                n, int(host.m), 0, device, int(info["row_ptr_64"]), C.byref(h)))
-            cheb.api._check(lib.cheb_cpaa(h, C.byref(opts), None, 0, ranks.ctypes.data_as(L.F64P),
-                                          tr, C.byref(rounds), C.byref(tot)))
-            lib.cheb_graph_free(h)
-
-        e2e_step()
-        dist.barrier()
-        e2e_times = []
-        for _ in range(max(1, min(args.steps, 5))):
-            flush.zero_()
-            torch.cuda.synchronize()
-            t = time.perf_counter()
-            e2e_step()
-            e2e_times.append(time.perf_counter() - t)
-        e2e_s = dist.max(statistics.mean(e2e_times))
-        e2e = {"value": round(dist.world * nnz * M / e2e_s / 1e9, 4), "unit": "GTEPS",
-               "h2d_bytes_per_step": int(off.nbytes + nb.nbytes),
-               "d2h_bytes_per_step": int(ranks.nbytes + 2 * M * 8),
-               "ms_per_step": round(e2e_s * 1e3, 3),
-               "path": "cheb_graph_upload_csr(pinned int64 CSR) + cheb_cpaa(host ranks) + free"}
-
-    # CPU baseline: the reference compiled unmodified, same graph, all host threads
+    e2e = None if args.no_e2e else sv.e2e(device, args.steps, flush, dist)
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        try:
-            host = dg.download()
-            e = np.stack([np.repeat(np.arange(host.n), np.diff(host.offsets)), host.neighbors], 1)
-            e = e[e[:, 0] <= e[:, 1]]
-            threads = os.cpu_count() or 1
-            r = cpu_reference_run(dict(cfg, drop=False), 1, 0, threads, host_edges=e)
-            cms = statistics.mean(r["wall_ms"])
-            cpu = {"value": round(r["nnz"] * r["M"] / (cms * 1e-3) / 1e9, 6), "unit": "GTEPS",
-                   "cores": threads, "kind": "reference",
-                   "sample": f"one full run_cpaa (M={r['M']}) on the same {args.config} CSR "
-                             f"({r['nnz']} entries), K={threads} threads, wall {cms:.0f} ms"}
-        except Exception as ex:  # noqa: BLE001
-            cpu = {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
-                   "sample": f"failed: {type(ex).__name__}: {ex}"}
+        cpu = cpu_baseline_line(sv, cfg, args)
 
     if dist.rank == 0:
+        kernel = "k_spmm_term + k_spmm_hub_finalize" if R > 1 else "k_term_warp<EPI_CPAA> + k_hub_finalize"
         line = {
             "metric": "cpaa_gteps_per_term",
             "value": round(value, 3),
@@ -422,16 +522,18 @@ def main():
             "vs_baseline": None,
             "dtype": "f64" if args.precision == 64 else "f32",
             "data": "synthetic",
-            "config": {"workload": args.config, "desc": cfg["desc"], "n": n, "nnz": nnz,
+            "config": {"workload": args.config, "desc": cfg["desc"], "n": n, "nnz": nnz, "R": R,
                        "edges_drawn": info["edges_drawn"], "max_degree": info["max_degree"],
                        "terms": M, "eps": EPS, "c": DAMPING,
                        "time_to_1e-10_ms": round(ms_step, 4),
+                       "gteps_definition": "nnz*R*terms/step_time (every CSR entry one traversal)",
                        "parallelism": "replicas" if dist.world > 1 else "single",
                        "l2": "flushed (512 MiB write) before every timed step",
                        "graph_build_s": round(build_s, 3)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                         "kernel": "k_term_fast<EPI_CPAA>", "bytes_per_launch": B,
+                         "kernel": kernel, "bytes_per_launch": B,
+                         "bytes_formula": "4 nnz + I_r (n+1) + 6 V R n (SURVEY.md 8d)",
                          "mean_launch_us": round(mean_term * 1e3, 3), "peak_kind": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
