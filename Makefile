@@ -23,7 +23,7 @@ $(OBJ_DIR)/%.cpp.o: $(SRC_DIR)/%.cpp $(HDRS)
 
 $(LIB_DIR)/libchebpr_b200.so: $(OBJS)
 	@mkdir -p $(LIB_DIR)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lnccl
 
 oracle:
 	$(MAKE) -C oracle

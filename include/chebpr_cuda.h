@@ -112,6 +112,28 @@ void cheb_graph_free(cheb_graph_t g);
  * multi-GPU row partition).  cuts has K+1 entries. */
 cheb_status cheb_partition_vertices(const int64_t* degrees, int64_t n, int K, int64_t* cuts);
 
+/* Multi-GPU row partition plan (host only): the view's degree-descending relabel
+ * (order[new] = old, ties by id), the reference cut rule (cpaa.cpp:40-68) applied to the
+ * relabelled degree sequence -> cuts[G+1] over new ids, and the exchange slot size
+ * max_rows = the largest slice.  Padded x position of new id u on rank r:
+ * r * max_rows + (u - cuts[r]). */
+cheb_status cheb_partition_plan(const int64_t* degrees, int64_t n, int G, int64_t* order,
+                                int64_t* cuts, int64_t* max_rows);
+
+/* Multi-GPU (one process per GPU): an NCCL communicator shared by G ranks.  Attaching
+ * it to a graph handle (every rank holds the same graph) partitions the solver view per
+ * cheb_partition_plan: cheb_cpaa then becomes a collective over the G ranks — each rank
+ * runs the fused term kernel on its rows and all-gathers x_{k+1} (ncclAllGather, equal
+ * padded slots) before the next term; trace sums are combined in rank order and every
+ * rank receives the full ranks vector.  FAST schedule only. */
+typedef struct cheb_comm* cheb_comm_t;
+cheb_status cheb_nccl_unique_id(void* out, int out_bytes); /* 128-byte ncclUniqueId */
+cheb_status cheb_comm_create(const void* unique_id, int nranks, int rank, int device, cheb_comm_t* out);
+void cheb_comm_destroy(cheb_comm_t c);
+cheb_status cheb_graph_attach_comm(cheb_graph_t g, cheb_comm_t comm);
+cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, int64_t* nnz_local,
+                                      int64_t* max_rows);
+
 /* ---- solvers ---- */
 enum { CHEB_MODE_FAST = 0, CHEB_MODE_BITEXACT = 1 };
 enum { CHEB_FP64 = 64, CHEB_FP32 = 32 };

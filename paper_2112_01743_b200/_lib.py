@@ -73,6 +73,7 @@ _SIGS = {
     "cheb_graph_get_info": (C.c_int, [C.c_void_p, C.POINTER(cheb_graph_info)]),
     "cheb_graph_free": (None, [C.c_void_p]),
     "cheb_partition_vertices": (C.c_int, [I64P, C.c_int64, C.c_int, I64P]),
+    "cheb_partition_plan": (C.c_int, [I64P, C.c_int64, C.c_int, I64P, I64P, I64P]),
     "cheb_cpaa_opts_default": (None, [C.POINTER(cheb_cpaa_opts)]),
     "cheb_cpaa": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), F64P, C.c_int64, F64P,
                             C.POINTER(cheb_trace_row), IP, F64P]),
@@ -80,6 +81,11 @@ _SIGS = {
                                    C.POINTER(C.c_void_p), C.c_int]),
     "cheb_last_timing": (C.c_int, [C.c_void_p, F64P, F64P, IP, IP]),
     "cheb_set_tuning": (C.c_int, [C.c_char_p, C.c_int]),
+    "cheb_nccl_unique_id": (C.c_int, [C.c_void_p, C.c_int]),
+    "cheb_comm_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "cheb_comm_destroy": (None, [C.c_void_p]),
+    "cheb_graph_attach_comm": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "cheb_graph_partition_info": (C.c_int, [C.c_void_p, I64P, I64P, I64P, I64P]),
     "cheb_cpaa_batch": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), I64P, F64P, F64P,
                                   C.POINTER(cheb_trace_row), IP]),
     "cheb_cpaa_batch_profile": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), I64P, F64P, C.c_int,

@@ -561,6 +561,24 @@ __global__ void k_permute_rows(const RPO* __restrict__ rp_old, const int* __rest
     }
 }
 
+// padded exchange position of every old id: new id u on rank r -> r*max_rows + (u - cuts[r])
+__global__ void k_posmap(const int* __restrict__ rank_of_old, int64_t n, const int64_t* __restrict__ cuts, int G,
+                         int64_t max_rows, int* __restrict__ pos) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = rank_of_old[v];
+        int r = 0;
+        while (r + 1 < G && u >= cuts[r + 1]) ++r;
+        pos[v] = (int)(r * max_rows + (u - cuts[r]));
+    }
+}
+
+__global__ void k_copy_i32(const int* __restrict__ in, int64_t n, int* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i];
+}
+
 __global__ void k_gather_inv(const double* __restrict__ inv, const int* __restrict__ order,
                              int64_t n, double* __restrict__ out) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -638,7 +656,7 @@ template <class RPO, class RPN>
 static void build_view_t(cheb_graph* g) {
     cudaStream_t st = g->stream;
     SolverView& V = g->view;
-    const int64_t n = g->n, nnz = g->nnz;
+    const int64_t n = g->n;
     TempStore tmp;
     const RPO* rp_old = g->row_ptr.ptr<RPO>();
 
@@ -661,43 +679,94 @@ static void build_view_t(cheb_graph* g) {
     k_new_degrees<<<grid_for(n), kBuildThreads, 0, st>>>(rp_old, V.order.ptr<int>(), n, deg_new.ptr<int64_t>());
     CHEB_CUDA_CHECK(cudaGetLastError());
 
-    DevMem rp64(sizeof(int64_t) * (n + 1));
-    {
-        size_t bytes = 0;
-        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, deg_new.ptr<int64_t>(), rp64.ptr<int64_t>(), n + 1, st));
-        void* t = tmp.get(bytes);
-        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, bytes, deg_new.ptr<int64_t>(), rp64.ptr<int64_t>(), n + 1, st));
+    // Row partition over G ranks: the reference cut rule on the relabelled
+    // degrees; this rank keeps sorted rows [lo, hi) and renames columns to padded slots.
+    Partition& P = g->part;
+    DevMem posmap;
+    const int* colmap = rank.ptr<int>();
+    if (P.G > 1) {
+        std::vector<int64_t> dh(n);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(dh.data(), deg_new.get(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        P.cuts.assign(P.G + 1, 0);
+        partition_cuts(dh.data(), n, P.G, P.cuts.data());
+        P.max_rows = 0;
+        for (int r = 0; r < P.G; ++r) P.max_rows = std::max(P.max_rows, P.cuts[r + 1] - P.cuts[r]);
+        if (P.G * P.max_rows > INT32_MAX) fail(CHEB_CAPACITY, "padded exchange layout exceeds int32 ids");
+        DevMem dcuts(sizeof(int64_t) * (P.G + 1));
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(dcuts.get(), P.cuts.data(), sizeof(int64_t) * (P.G + 1), cudaMemcpyHostToDevice, st));
+        posmap.alloc(sizeof(int) * n);
+        k_posmap<<<grid_for(n), kBuildThreads, 0, st>>>(rank.ptr<int>(), n, dcuts.ptr<int64_t>(), P.G, P.max_rows,
+                                                        posmap.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        colmap = posmap.ptr<int>();
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    } else {
+        P.cuts = {0, n};
+        P.max_rows = n;
     }
+    const int64_t lo = P.cuts[P.rank], hi = P.cuts[P.rank + 1], nl = hi - lo;
+    V.lo = lo;
+    V.n_local = nl;
+    V.x_len = (int64_t)P.G * P.max_rows;
+    V.x_off = (int64_t)P.rank * P.max_rows;
+
+    DevMem rp64(sizeof(int64_t) * (nl + 1));
+    {
+        // deg_new[hi] may be a real degree: scan nl+1 entries of a copy with a zero tail
+        DevMem dl(sizeof(int64_t) * (nl + 1));
+        CHEB_CUDA_CHECK(cudaMemsetAsync(dl.get(), 0, sizeof(int64_t) * (nl + 1), st));
+        if (nl > 0)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(dl.get(), deg_new.ptr<int64_t>() + lo, sizeof(int64_t) * nl,
+                                            cudaMemcpyDeviceToDevice, st));
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, dl.ptr<int64_t>(), rp64.ptr<int64_t>(), nl + 1, st));
+        void* t = tmp.get(bytes);
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, bytes, dl.ptr<int64_t>(), rp64.ptr<int64_t>(), nl + 1, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    const int64_t nnz_l = nl > 0 ? read_scalar(rp64.ptr<int64_t>() + nl, st) : 0;
+    V.nnz_local = nnz_l;
     V.rp64 = sizeof(RPN) == 8;
     if (V.rp64) {
         V.row_ptr = std::move(rp64);
     } else {
-        V.row_ptr.alloc(sizeof(int) * (n + 1));
-        k_narrow_rowptr<<<grid_for(n + 1), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), n + 1, V.row_ptr.ptr<int>());
+        V.row_ptr.alloc(sizeof(int) * (nl + 1));
+        k_narrow_rowptr<<<grid_for(nl + 1), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), nl + 1, V.row_ptr.ptr<int>());
     }
-    V.col.alloc(sizeof(int) * std::max<int64_t>(nnz, 1) + 64);  // TMA reads round up to 16 B
-    k_permute_rows<<<grid_for(n * 32), kBuildThreads, 0, st>>>(rp_old, g->col.ptr<int>(), V.row_ptr.ptr<RPN>(),
-                                                              V.order.ptr<int>(), rank.ptr<int>(), n,
-                                                              V.col.ptr<int>());
-    CHEB_CUDA_CHECK(cudaGetLastError());
+    V.col.alloc(sizeof(int) * std::max<int64_t>(nnz_l, 1) + 64);  // TMA reads round up to 16 B
+    if (nl > 0) {
+        k_permute_rows<<<grid_for(nl * 32), kBuildThreads, 0, st>>>(rp_old, g->col.ptr<int>(), V.row_ptr.ptr<RPN>(),
+                                                                   V.order.ptr<int>() + lo, colmap, nl,
+                                                                   V.col.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
     if (g->inv_array) {
-        V.inv.alloc(sizeof(double) * n);
-        k_gather_inv<<<grid_for(n), kBuildThreads, 0, st>>>(g->inv.ptr<double>(), V.order.ptr<int>(), n,
-                                                            V.inv.ptr<double>());
+        V.inv.alloc(sizeof(double) * std::max<int64_t>(nl, 1));
+        if (nl > 0)
+            k_gather_inv<<<grid_for(nl), kBuildThreads, 0, st>>>(g->inv.ptr<double>(), V.order.ptr<int>() + lo, nl,
+                                                                 V.inv.ptr<double>());
     } else {
         V.inv.release();
+    }
+    if (P.G > 1 || P.comm) {  // keep the global order (final un-permute), local order for row ids
+        V.order_full = std::move(V.order);
+        V.order.alloc(sizeof(int) * std::max<int64_t>(nl, 1));
+        if (nl > 0)
+            k_copy_i32<<<grid_for(nl), kBuildThreads, 0, st>>>(V.order_full.ptr<int>() + lo, nl, V.order.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
     }
 
     // Runs of equal degree (descending) -> greedy tiles on the host.
     std::vector<int64_t> run_deg, run_cnt;
-    if (n > 0) {
-        DevMem uniq(sizeof(int64_t) * n), cnts(sizeof(int64_t) * n), nruns(sizeof(int64_t));
+    if (nl > 0) {
+        DevMem uniq(sizeof(int64_t) * nl), cnts(sizeof(int64_t) * nl), nruns(sizeof(int64_t));
         size_t bytes = 0;
-        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, deg_new.ptr<int64_t>(), uniq.ptr<int64_t>(),
-                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), n, st));
+        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, deg_new.ptr<int64_t>() + lo, uniq.ptr<int64_t>(),
+                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), nl, st));
         void* t = tmp.get(bytes);
-        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(t, bytes, deg_new.ptr<int64_t>(), uniq.ptr<int64_t>(),
-                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), n, st));
+        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(t, bytes, deg_new.ptr<int64_t>() + lo, uniq.ptr<int64_t>(),
+                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), nl, st));
         const int64_t R = read_scalar(nruns.ptr<int64_t>(), st);
         run_deg.resize(R);
         run_cnt.resize(R);
@@ -705,7 +774,7 @@ static void build_view_t(cheb_graph* g) {
         CHEB_CUDA_CHECK(cudaMemcpy(run_cnt.data(), cnts.get(), sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
     }
     std::vector<int> hub_first;
-    const std::vector<Tile> tiles = make_tiles(run_deg, run_cnt, n, nnz, &V.n_hub, &V.n_chunk_tiles, hub_first);
+    const std::vector<Tile> tiles = make_tiles(run_deg, run_cnt, nl, nnz_l, &V.n_hub, &V.n_chunk_tiles, hub_first);
     hub_first.push_back(V.n_chunk_tiles);
     V.hub_first.alloc(sizeof(int) * hub_first.size());
     CHEB_CUDA_CHECK(cudaMemcpy(V.hub_first.get(), hub_first.data(), sizeof(int) * hub_first.size(),

@@ -4,14 +4,22 @@
 // and applies the reference's argument checks in the reference's order
 // (/root/reference/proj/src/cpaa.cpp:79-94, power.cpp:28-47), so that the wrappers
 // above the C-ABI raise exactly what the reference raises.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#include <nccl.h>
+
 #include "common.cuh"
 
 using namespace chebgpu;
+
+struct cheb_comm {
+    ncclComm_t nccl = nullptr;
+    int nranks = 1, rank = 0, device = 0;
+};
 
 namespace {
 thread_local std::string g_last_error;
@@ -65,6 +73,10 @@ void fill_info(cheb_graph* g, cheb_graph_info* info) {
 
 void need_graph(cheb_graph* g) {
     if (!g) fail(CHEB_INVALID_ARG, "null graph handle");
+}
+
+void single_gpu_only(cheb_graph* g) {
+    if (g->part.G > 1) fail(CHEB_INVALID_ARG, "operation not available on a partitioned (multi-GPU) handle");
 }
 
 // cpaa.cpp:16-26 essential_check, the parts that are not guaranteed by construction.
@@ -228,30 +240,24 @@ void cheb_graph_free(cheb_graph_t g) {
 }
 
 cheb_status cheb_partition_vertices(const int64_t* degrees, int64_t n, int K, int64_t* cuts) {
-    // cpaa.cpp:40-68: the j-th cut at the degree prefix nearest j/K of the total.
+    return guarded([&] { partition_cuts(degrees, n, K, cuts); });
+}
+
+cheb_status cheb_partition_plan(const int64_t* degrees, int64_t n, int G, int64_t* order,
+                                int64_t* cuts, int64_t* max_rows) {
+    // degree-descending relabel (ties by id; the view's order) + the reference cut rule on
+    // the relabelled degrees; slot size = the largest slice.
     return guarded([&] {
-        if (K < 1) fail(CHEB_DOMAIN, "parallelism must be >= 1");
-        std::vector<int64_t> prefix(static_cast<size_t>(n) + 1, 0);
-        for (int64_t v = 0; v < n; ++v) prefix[v + 1] = prefix[v] + degrees[v];
-        const double total = static_cast<double>(prefix[n]);
-        cuts[0] = 0;
-        cuts[K] = n;
-        for (int j = 1; j < K; ++j) {
-            const double ideal = total * j / K;
-            // first prefix >= ideal (as doubles), then step back if the previous is nearer
-            int64_t lo = 0, hi = n + 1;
-            while (lo < hi) {
-                const int64_t mid = lo + (hi - lo) / 2;
-                if (static_cast<double>(prefix[mid]) < ideal) lo = mid + 1;
-                else hi = mid;
-            }
-            int64_t idx = lo > n ? n : lo;
-            if (idx > 0 && static_cast<double>(prefix[idx]) - ideal > ideal - static_cast<double>(prefix[idx - 1]))
-                --idx;
-            if (idx < cuts[j - 1]) idx = cuts[j - 1];
-            if (idx > n) idx = n;
-            cuts[j] = idx;
-        }
+        if (G < 1) fail(CHEB_DOMAIN, "parallelism must be >= 1");
+        std::vector<int64_t> ids(n), dsorted(n);
+        for (int64_t v = 0; v < n; ++v) ids[v] = v;
+        std::stable_sort(ids.begin(), ids.end(), [&](int64_t a, int64_t b) { return degrees[a] > degrees[b]; });
+        for (int64_t i = 0; i < n; ++i) dsorted[i] = degrees[ids[i]];
+        partition_cuts(dsorted.data(), n, G, cuts);
+        int64_t mr = 0;
+        for (int r = 0; r < G; ++r) mr = std::max(mr, cuts[r + 1] - cuts[r]);
+        if (order) std::memcpy(order, ids.data(), sizeof(int64_t) * n);
+        if (max_rows) *max_rows = mr;
     });
 }
 
@@ -370,6 +376,7 @@ cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double
 
 static BatchSpec batch_spec(cheb_graph* g, const cheb_cpaa_opts& o, const int64_t* seeds) {
     need_graph(g);
+    single_gpu_only(g);
     essential(g);
     BatchSpec b;
     b.M = resolve_rounds(o.c, o.rounds, o.eps, o.max_rounds);
@@ -439,6 +446,73 @@ cheb_status cheb_cpaa_batch_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, 
     });
 }
 
+cheb_status cheb_nccl_unique_id(void* out, int out_bytes) {
+    return guarded([&] {
+        if (out_bytes < (int)sizeof(ncclUniqueId)) fail(CHEB_INVALID_ARG, "unique id buffer too small");
+        ncclUniqueId id;
+        const ncclResult_t r = ncclGetUniqueId(&id);
+        if (r != ncclSuccess) fail(CHEB_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+        std::memcpy(out, &id, sizeof id);
+    });
+}
+
+cheb_status cheb_comm_create(const void* unique_id, int nranks, int rank, int device, cheb_comm_t* out) {
+    return guarded([&] {
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(CHEB_INVALID_ARG, "bad rank / nranks");
+        DeviceGuard dg(device);
+        auto* c = new cheb_comm();
+        c->nranks = nranks;
+        c->rank = rank;
+        c->device = device;
+        ncclUniqueId id;
+        std::memcpy(&id, unique_id, sizeof id);
+        const ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+        if (r != ncclSuccess) {
+            delete c;
+            fail(CHEB_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+        *out = c;
+    });
+}
+
+void cheb_comm_destroy(cheb_comm_t c) {
+    if (!c) return;
+    DeviceGuard dg(c->device);
+    if (c->nccl) ncclCommDestroy(c->nccl);
+    delete c;
+}
+
+cheb_status cheb_graph_attach_comm(cheb_graph_t g, cheb_comm_t comm) {
+    return guarded([&] {
+        need_graph(g);
+        if (!comm) fail(CHEB_INVALID_ARG, "null communicator");
+        if (comm->device != g->device) fail(CHEB_INVALID_ARG, "communicator and graph live on different devices");
+        g->part.G = comm->nranks;
+        g->part.rank = comm->rank;
+        g->part.comm = comm->nccl;
+        g->view.ready = false;  // rebuild the solver view as this rank's slice
+        if (g->ws.exec) {
+            cudaGraphExecDestroy(g->ws.exec);
+            g->ws.exec = nullptr;
+        }
+        g->ws.exec_key.clear();
+        g->ws.seen_key.clear();
+    });
+}
+
+cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, int64_t* nnz_local,
+                                      int64_t* max_rows) {
+    return guarded([&] {
+        need_graph(g);
+        DeviceGuard dg(g->device);
+        ensure_view(g);
+        if (lo) *lo = g->part.cuts[g->part.rank];
+        if (hi) *hi = g->part.cuts[g->part.rank + 1];
+        if (nnz_local) *nnz_local = g->view.nnz_local;
+        if (max_rows) *max_rows = g->part.max_rows;
+    });
+}
+
 cheb_status cheb_set_tuning(const char* key, int value) {
     return guarded([&] {
         const std::string k = key ? key : "";
@@ -481,6 +555,7 @@ cheb_status cheb_power(cheb_graph_t g, const cheb_power_opts* opts, const double
         cheb_power_opts_default(&o);
         if (opts) o = *opts;
         need_graph(g);
+        single_gpu_only(g);
         essential(g);                                                   // power.cpp:30
         if (!(o.c > 0.0 && o.c < 1.0)) fail(CHEB_DOMAIN, "damping factor must lie in (0,1)");
         const bool fixed = o.rounds >= 0, by_tol = o.tol > 0.0;         // power.cpp:33-37
@@ -506,6 +581,7 @@ cheb_status cheb_power(cheb_graph_t g, const cheb_power_opts* opts, const double
 cheb_status cheb_transition_apply(cheb_graph_t g, const double* x, int64_t nx, double* y, int mode) {
     return guarded([&] {
         need_graph(g);
+        single_gpu_only(g);
         if (nx != g->n)  // graph.cpp:105-107
             fail(CHEB_INVALID_ARG, "vector length " + std::to_string(nx) +
                                        " does not match vertex count " + std::to_string(g->n));
@@ -517,6 +593,7 @@ cheb_status cheb_transition_apply(cheb_graph_t g, const double* x, int64_t nx, d
 cheb_status cheb_state_init(cheb_graph_t g, double c0, int mode) {
     return guarded([&] {
         need_graph(g);
+        single_gpu_only(g);
         essential(g);  // cpaa.cpp:168
         staged_init(g, c0, mode);
     });

@@ -4,6 +4,7 @@
 // its bits must match the reference's exactly.
 #include <cmath>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 
@@ -73,6 +74,31 @@ int resolve_rounds(double c, int rounds, double eps, int max_rounds) {
     if (max_rounds < 0) fail(CHEB_INVALID_ARG, "max_rounds must be non-negative");
     const int M = by_rounds ? rounds : plan_iterations(c, eps, nullptr);
     return M < max_rounds ? M : max_rounds;
+}
+
+void partition_cuts(const int64_t* degrees, int64_t n, int K, int64_t* cuts) {
+    // cpaa.cpp:40-68: the j-th cut at the degree prefix nearest j/K of the total.
+    if (K < 1) fail(CHEB_DOMAIN, "parallelism must be >= 1");
+    std::vector<int64_t> prefix(static_cast<size_t>(n) + 1, 0);
+    for (int64_t v = 0; v < n; ++v) prefix[v + 1] = prefix[v] + degrees[v];
+    const double total = static_cast<double>(prefix[n]);
+    cuts[0] = 0;
+    cuts[K] = n;
+    for (int j = 1; j < K; ++j) {
+        const double ideal = total * j / K;
+        int64_t lo = 0, hi = n + 1;  // first prefix >= ideal (as doubles)
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if (static_cast<double>(prefix[mid]) < ideal) lo = mid + 1;
+            else hi = mid;
+        }
+        int64_t idx = lo > n ? n : lo;
+        if (idx > 0 && static_cast<double>(prefix[idx]) - ideal > ideal - static_cast<double>(prefix[idx - 1]))
+            --idx;
+        if (idx < cuts[j - 1]) idx = cuts[j - 1];
+        if (idx > n) idx = n;
+        cuts[j] = idx;
+    }
 }
 
 double kahan_sum(const double* x, int64_t n) {  // graph.cpp:10-19, compensated serial sum

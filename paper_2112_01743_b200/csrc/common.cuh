@@ -128,7 +128,9 @@ constexpr int kTileChunk = 0x10;
 struct SolverView {
     bool ready = false;
     bool rp64 = false;
-    DevMem order;      // int32 [n]  new -> old
+    DevMem order;      // int32 [n_local]  local new row -> old id
+    DevMem order_full; // int32 [n]  global new -> old (partitioned runs only)
+    int64_t n_local = 0, nnz_local = 0, lo = 0, x_len = 0, x_off = 0;
     DevMem row_ptr;    // int32/int64 [n+1] (new order)
     DevMem col;        // int32 [nnz] (renamed ids, storage order kept)
     DevMem inv;        // double [n] (new order) only when inv_degree is non-canonical
@@ -140,6 +142,17 @@ struct SolverView {
     int64_t n_hub = 0;     // rows [0, n_hub) with degree > kWarpNnz (chunk tiles)
     int n_chunk_tiles = 0;
     DevMem hub_first;      // int32 [n_hub + 1]: first chunk tile of each hub row
+};
+
+// 1-D row partition of the degree-sorted view over G GPUs (one process per GPU).
+// Rank r owns sorted rows [cuts[r], cuts[r+1]); x is exchanged in a padded layout of
+// G slots of max_rows entries (slot r = rank r's rows), so an NCCL all-gather with equal
+// counts replicates x_{k+1} on every rank.
+struct Partition {
+    int G = 1, rank = 0;
+    std::vector<int64_t> cuts{0, 0};
+    int64_t max_rows = 0;
+    void* comm = nullptr;  // ncclComm_t (owned by the cheb_comm handle, not by the graph)
 };
 
 struct Workspace {
@@ -196,6 +209,7 @@ struct cheb_graph {
     chebgpu::Workspace ws;
     chebgpu::StagedState staged;
     chebgpu::BatchWorkspace bws;
+    chebgpu::Partition part;
     double last_loop_ms = 0.0;
     int last_terms = 0;
     int last_launches = 0;
@@ -225,6 +239,9 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
 void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees);
 void ensure_view(cheb_graph* g);
 void finalize_stats(cheb_graph* g);
+
+// host: partition_vertices rule (cpaa.cpp:40-68) over a degree sequence
+void partition_cuts(const int64_t* degrees, int64_t n, int K, int64_t* cuts);
 
 // coeffs.cpp (host coefficient kit, coefficients.cpp semantics)
 double beta(double c);

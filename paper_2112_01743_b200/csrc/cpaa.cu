@@ -28,8 +28,18 @@
 #include <cstring>
 #include <string>
 
+#include <nccl.h>
+
 #include "common.cuh"
 #include "device.cuh"
+
+#define CHEB_NCCL_CHECK(expr)                                                              \
+    do {                                                                                   \
+        ncclResult_t _r = (expr);                                                          \
+        if (_r != ncclSuccess)                                                             \
+            ::chebgpu::fail(CHEB_NCCL, std::string("NCCL error ") + ncclGetErrorString(_r) + \
+                                           " at " __FILE__ ":" + std::to_string(__LINE__)); \
+    } while (0)
 
 namespace chebgpu {
 
@@ -769,7 +779,8 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     const void* before[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
                             w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
                             w.trace.get(), w.total.get()};
-    const size_t vb = sizeof(V) * (size_t)std::max<int64_t>(n, 1) * R;
+    const int64_t vlen = std::max<int64_t>(std::max<int64_t>(n, g->view.x_len), 1);
+    const size_t vb = sizeof(V) * (size_t)vlen * R;
     w.T0.ensure(vb);
     w.T1.ensure(vb);
     w.X0.ensure(vb);
@@ -890,6 +901,154 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
     return launches;
 }
 
+// ---------------- multi-GPU: row partition + NCCL all-gather of x per term ----------
+template <class V>
+ncclDataType_t nccl_type() { return sizeof(V) == 8 ? ncclDouble : ncclFloat; }
+
+__global__ void k_sum_ranks(const double* __restrict__ all, int G, int len, double* __restrict__ out) {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < G; ++r) s += all[(size_t)r * len + i];  // rank order: deterministic
+        out[i] = s;
+    }
+}
+
+template <class V>
+__global__ void k_normalize_slot(const V* __restrict__ acc, int64_t nl, const double* __restrict__ total,
+                                 V* __restrict__ slot) {
+    const double tot = *total;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nl;
+         u += (int64_t)gridDim.x * blockDim.x)
+        slot[u] = (V)((double)acc[u] / tot);
+}
+
+template <class V>
+__global__ void k_unpermute_padded(const V* __restrict__ padded, const int64_t* __restrict__ cuts, int G,
+                                   int64_t max_rows, const int* __restrict__ order_full, V* __restrict__ out) {
+    const int64_t total = (int64_t)G * max_rows;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(p / max_rows);
+        const int64_t i = p - r * max_rows;
+        if (i < cuts[r + 1] - cuts[r]) out[order_full[cuts[r] + i]] = padded[p];
+    }
+}
+
+template <class RP, class V>
+void run_solve_dist(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, double* total,
+                    std::vector<double>* term_ms = nullptr) {
+    cudaStream_t st = g->stream;
+    Partition& P = g->part;
+    SolverView& Vw = g->view;
+    ncclComm_t comm = static_cast<ncclComm_t>(P.comm);
+    const Layout L = layout_of(g, CHEB_MODE_FAST);
+    ensure_workspace<V>(g, s.M, 1);
+    Workspace& w = g->ws;
+    const int64_t nl = Vw.n_local, mr = P.max_rows;
+    const int M = s.M, G = P.G;
+    std::vector<double> coeffs;
+    double beta_v, c0;
+    coefficients(s.c, M, coeffs, &beta_v, &c0);
+    DevMem d_p;
+    if (s.p) {
+        d_p.alloc(sizeof(double) * g->n);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(d_p.get(), s.p, sizeof(double) * g->n, cudaMemcpyHostToDevice, st));
+    }
+    DevMem trace_all(sizeof(double) * 2 * (size_t)std::max(M, 1) * G), tglob(sizeof(double) * 2 * std::max(M, 1));
+    DevMem rbuf(sizeof(V) * (size_t)std::max<int64_t>(Vw.x_len, 1)), dcuts(sizeof(int64_t) * (G + 1));
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(dcuts.get(), P.cuts.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, st));
+    V* T[2] = {w.T0.ptr<V>(), w.T1.ptr<V>()};
+    V* X[2] = {w.X0.ptr<V>(), w.X1.ptr<V>()};
+    V* acc = w.acc.ptr<V>();
+    const ncclDataType_t ty = nccl_type<V>();
+    int launches = 0;
+    std::vector<cudaEvent_t> tev;
+    if (term_ms) {
+        tev.resize(2 * (size_t)std::max(M, 1));
+        for (auto& e : tev) CHEB_CUDA_CHECK(cudaEventCreate(&e));
+    }
+
+    CHEB_CUDA_CHECK(cudaEventRecord(g->ev0, st));
+    // T_{-1} = T_0, acc, x_0 for the local rows (p indexed by old id through the local order)
+    k_init<RP, V><<<grid1d(nl), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, d_p.ptr<double>(), L.order,
+                                                   nl, c0 / 2.0, T[0], T[1], acc, X[0] + Vw.x_off);
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    ++launches;
+    CHEB_NCCL_CHECK(ncclAllGather(X[0] + Vw.x_off, X[0], (size_t)mr, ty, comm, st));
+    for (int k = 1; k <= M; ++k) {
+        TermArgs<RP, V> a = base_args<RP, V>(g, L);
+        a.x_in = X[(k - 1) & 1];
+        a.x_out = X[k & 1] + Vw.x_off;
+        a.T = T[(k - 1) & 1];
+        a.acc = acc;
+        a.ck = coeffs[k];
+        a.first = k == 1;
+        a.part = w.part.ptr<double>() + (size_t)(k - 1) * Vw.grid * 2;
+        a.hub_part = w.hub_part.ptr<double>();
+        a.hub_cnt = w.hub_cnt.ptr<unsigned>();
+        a.hub_ts = Vw.n_hub ? w.hub_ts.ptr<double>() + (size_t)(k - 1) * Vw.n_hub * 2 : nullptr;
+        if (term_ms) CHEB_CUDA_CHECK(cudaEventRecord(tev[2 * (k - 1)], st));
+        launches += launch_pass<EPI_CPAA>(g, L, a);
+        if (term_ms) CHEB_CUDA_CHECK(cudaEventRecord(tev[2 * (k - 1) + 1], st));
+        k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), Vw.grid, w.hub_ts.ptr<double>(),
+                                               (int)Vw.n_hub, k - 1, w.trace.ptr<double>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+        // x_{k+1}: every rank's slot -> every rank (in place, equal counts)
+        CHEB_NCCL_CHECK(ncclAllGather(X[k & 1] + Vw.x_off, X[k & 1], (size_t)mr, ty, comm, st));
+    }
+    const double* d_total;
+    if (M > 0) {
+        CHEB_NCCL_CHECK(ncclAllGather(w.trace.ptr<double>(), trace_all.ptr<double>(), 2 * (size_t)M, ncclDouble, comm, st));
+        k_sum_ranks<<<1, 256, 0, st>>>(trace_all.ptr<double>(), G, 2 * M, tglob.ptr<double>());
+        d_total = tglob.ptr<double>() + 2 * (M - 1) + 1;
+    } else {
+        const int eg = grid1d(nl);
+        k_sum_blocks<V><<<eg, kThreads, 0, st>>>(acc, nl, w.part.ptr<double>());
+        k_sum_final<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), eg, w.total.ptr<double>());
+        CHEB_NCCL_CHECK(ncclAllGather(w.total.ptr<double>(), trace_all.ptr<double>(), 1, ncclDouble, comm, st));
+        k_sum_ranks<<<1, 32, 0, st>>>(trace_all.ptr<double>(), G, 1, tglob.ptr<double>());
+        d_total = tglob.ptr<double>();
+    }
+    k_normalize_slot<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf.ptr<V>() + Vw.x_off);
+    CHEB_NCCL_CHECK(ncclAllGather(rbuf.ptr<V>() + Vw.x_off, rbuf.ptr<V>(), (size_t)mr, ty, comm, st));
+    k_unpermute_padded<V><<<grid1d(Vw.x_len), kThreads, 0, st>>>(rbuf.ptr<V>(), dcuts.ptr<int64_t>(), G, mr,
+                                                                Vw.order_full.ptr<int>(), w.out.ptr<V>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    launches += 4;
+    CHEB_CUDA_CHECK(cudaEventRecord(g->ev1, st));
+    g->last_terms = M;
+    g->last_launches = launches;
+    w.launches = launches;
+
+    std::vector<double> t(2 * (size_t)std::max(M, 1));
+    double tot = 0.0;
+    if (M > 0)
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), tglob.get(), sizeof(double) * 2 * M, cudaMemcpyDeviceToHost, st));
+    else
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(&tot, tglob.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+    g->last_loop_ms = ms;
+    if (term_ms) {
+        term_ms->assign(M, 0.0);
+        for (int k = 0; k < M; ++k) {
+            float tk = 0.f;
+            CHEB_CUDA_CHECK(cudaEventElapsedTime(&tk, tev[2 * k], tev[2 * k + 1]));
+            (*term_ms)[k] = tk;
+        }
+        for (auto& e : tev) cudaEventDestroy(e);
+    }
+    for (int k = 1; k <= M; ++k)
+        if (!std::isfinite(t[2 * (k - 1)]) || !std::isfinite(t[2 * (k - 1) + 1]))
+            fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(k));
+    if (M > 0) tot = t[2 * (M - 1) + 1];
+    if (!std::isfinite(tot) || tot <= 0.0) fail(CHEB_NUMERIC, "normalization total is not positive and finite");
+    if (tr) *tr = t;
+    if (total) *total = tot;
+}
+
 std::string solve_key(const SolveSpec& s, bool has_p) {
     char buf[160];
     std::snprintf(buf, sizeof buf, "c=%.17g M=%d mode=%d prec=%d R=%d p=%d", s.c, s.M, s.mode,
@@ -900,6 +1059,12 @@ std::string solve_key(const SolveSpec& s, bool has_p) {
 template <class RP, class V>
 void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
                  std::vector<double>* errs, double* total) {
+    if (g->part.comm) {
+        if (h_ref) fail(CHEB_INVALID_ARG, "reference tracking is not available on a partitioned handle");
+        if (s.mode != CHEB_MODE_FAST) fail(CHEB_INVALID_ARG, "a partitioned handle runs the FAST schedule only");
+        run_solve_dist<RP, V>(g, s, tr, total);
+        return;
+    }
     cudaStream_t st = g->stream;
     const Layout L = layout_of(g, s.mode);
     ensure_workspace<V>(g, s.M, 1);
@@ -1036,6 +1201,10 @@ void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_m
     auto run = [&](auto rp_tag, auto v_tag) {
         using RP = decltype(rp_tag);
         using V = decltype(v_tag);
+        if (g->part.comm) {
+            run_solve_dist<RP, V>(g, s, nullptr, nullptr, &term_ms);
+            return;
+        }
         const Layout L = layout_of(g, s.mode);
         ensure_workspace<V>(g, s.M, 1);
         std::vector<double> coeffs;

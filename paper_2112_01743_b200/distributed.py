@@ -1,0 +1,64 @@
+"""Multi-GPU plumbing: one process per GPU, an NCCL communicator created by the library
+(cheb_comm_create) from a unique id that rank 0 draws and torch.distributed broadcasts.
+Attaching it to a graph handle makes cheb_cpaa a collective over the ranks."""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from .api import _check, DeviceGraph
+
+
+def partition_plan(degrees, G: int):
+    """cheb_partition_plan: (order new->old, cuts[G+1] over new ids, max_rows)."""
+    deg = np.ascontiguousarray(degrees, dtype=np.int64)
+    n = deg.size
+    order = np.zeros(n, dtype=np.int64)
+    cuts = np.zeros(G + 1, dtype=np.int64)
+    mr = C.c_int64()
+    _check(L.load().cheb_partition_plan(deg.ctypes.data_as(L.I64P), n, G, order.ctypes.data_as(L.I64P),
+                                        cuts.ctypes.data_as(L.I64P), C.byref(mr)))
+    return order, cuts, int(mr.value)
+
+
+class Communicator:
+    """NCCL communicator over the ranks of a torch.distributed process group."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        lib = L.load()
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            _check(lib.cheb_nccl_unique_id(uid, 128))
+        if world > 1:
+            backend = dist.get_backend(group)
+            dev = torch.device("cuda", device) if backend == "nccl" else torch.device("cpu")
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=dev)
+            dist.broadcast(t, src=0, group=group)
+            uid = (C.c_ubyte * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        _check(lib.cheb_comm_create(uid, world, rank, device, C.byref(h)))
+        self.handle, self.rank, self.world, self.device = h, rank, world, device
+
+    def attach(self, dg: DeviceGraph):
+        _check(L.load().cheb_graph_attach_comm(dg.handle, self.handle))
+
+    def close(self):
+        if self.handle:
+            L.load().cheb_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def partition_info(dg: DeviceGraph) -> dict:
+    lo, hi, nnz, mr = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+    _check(L.load().cheb_graph_partition_info(dg.handle, C.byref(lo), C.byref(hi), C.byref(nnz), C.byref(mr)))
+    return {"lo": lo.value, "hi": hi.value, "nnz_local": nnz.value, "max_rows": mr.value}

@@ -322,3 +322,24 @@ def test_batched_dense_personalization_and_uniform_column(cheb, oracle):
     # scalar path with an explicit personalisation vector agrees too
     single = cheb.run_cpaa(g, cheb.SolverConfig(rounds=39, personalization=P[:, 1]))
     assert np.max(np.abs(single.ranks - res.ranks[:, 1])) <= TOL64
+
+
+def test_nccl_partitioned_path_single_rank(cheb):
+    """The multi-GPU code path (NCCL communicator attached, per-term all-gather, rank-ordered
+    trace combine, padded gather + un-permute) at world size 1 on one B200: identical bits
+    to the single-GPU solve.  Multi-rank correctness is covered on CPU by
+    tests/test_multigpu_cpu.py (same plan and exchange protocol)."""
+    from paper_2112_01743_b200.distributed import Communicator, partition_info
+    for name in ("config1", "gnp2000", "star100"):
+        z = load_golden(name)
+        dg, _ = cheb.build_device_graph(z["edges"])
+        plain = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+        comm = Communicator(0, 1, 0)
+        comm.attach(dg)
+        info = partition_info(dg)
+        assert (info["lo"], info["hi"]) == (0, int(z["n"]))
+        part = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+        assert np.array_equal(part.ranks, plain.ranks)
+        assert np.max(np.abs(part.ranks - z["cpaa39_ranks"])) <= TOL64
+        dg.free()
+        comm.close()
