@@ -9,9 +9,11 @@ LIB_DIR   := paper_2112_01743_b200/lib
 OBJ_DIR   := build/obj
 SRCS      := $(SRC_DIR)/build.cu $(SRC_DIR)/cpaa.cu $(SRC_DIR)/capi.cu $(SRC_DIR)/generate.cu $(SRC_DIR)/spmm.cu $(SRC_DIR)/coeffs.cpp
 OBJS      := $(patsubst $(SRC_DIR)/%,$(OBJ_DIR)/%.o,$(SRCS))
+REFTEST_SRC ?= /root/reference/proj/tests
+REFTESTS    := test_coefficients test_graph test_cpaa test_power test_metrics
 HDRS      := $(SRC_DIR)/common.cuh $(SRC_DIR)/device.cuh include/chebpr_cuda.h
 
-all: $(LIB_DIR)/libchebpr_b200.so oracle
+all: $(LIB_DIR)/libchebpr_b200.so $(LIB_DIR)/libchebpr_dropin.so oracle $(if $(wildcard $(REFTEST_SRC)/test_cpaa.cpp),reftests,)
 
 $(OBJ_DIR)/%.cu.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p $(OBJ_DIR)
@@ -25,6 +27,20 @@ $(LIB_DIR)/libchebpr_b200.so: $(OBJS)
 	@mkdir -p $(LIB_DIR)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lnccl
 
+# C++ drop-in layer (the reference's chebpr:: API over the C-ABI)
+$(LIB_DIR)/libchebpr_dropin.so: $(SRC_DIR)/dropin.cpp $(wildcard include/chebpr/*.hpp) include/chebpr_cuda.h $(LIB_DIR)/libchebpr_b200.so
+	g++ -std=c++20 -O2 -fPIC -shared -ffp-contract=off -Wall -Wextra -Iinclude -o $@ $(SRC_DIR)/dropin.cpp \
+	    -L$(LIB_DIR) -lchebpr_b200 -Wl,-rpath,'$$ORIGIN'
+
+# The reference's own doctest suites compiled UNCHANGED against the drop-in (test
+# infrastructure; sources read in place from /root/reference, binaries into build/reftests).
+reftests: $(addprefix build/reftests/,$(REFTESTS))
+
+build/reftests/%: $(REFTEST_SRC)/%.cpp $(LIB_DIR)/libchebpr_dropin.so tests/cpp/doctest.h
+	@mkdir -p build/reftests
+	g++ -std=c++20 -O2 -Iinclude -Itests/cpp -I$(REFTEST_SRC) -o $@ $< \
+	    -L$(LIB_DIR) -lchebpr_dropin -lchebpr_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIB_DIR)'
+
 oracle:
 	$(MAKE) -C oracle
 
@@ -32,4 +48,4 @@ clean:
 	rm -rf build $(LIB_DIR)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean reftests

@@ -6,7 +6,7 @@
  * pointers and sizes only; no exceptions cross this boundary: every call returns a
  * cheb_status and, on failure, cheb_last_error() holds the reference's message text
  * (e.g. "vertex 2 is isolated (degree 0)", "non-finite value at round 3").  The C++
- * wrapper (include/chebpr/*.hpp) re-throws them as the reference's exception types
+ * wrapper (include/chebpr/ headers) re-throws them as the reference's exception types
  * (/root/reference/proj/include/chebpr/errors.hpp:11-33).
  *
  * Ownership: host buffers are caller-owned and copied synchronously.  Device memory,
