@@ -85,10 +85,39 @@ void essential(cheb_graph* g) {
 }
 }  // namespace
 
+void chebgpu::retain_pool_memory() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static bool done[64] = {};
+    if (dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done[dev] = true;
+}
+
 cheb_graph::~cheb_graph() {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    {   // return every buffer to the pool on this graph's stream while it still exists
+        row_ptr.release();
+        col.release();
+        inv.release();
+        view = chebgpu::SolverView{};
+        if (ws.exec) {
+            cudaGraphExecDestroy(ws.exec);
+            ws.exec = nullptr;
+        }
+        ws.T0.release(); ws.T1.release(); ws.X0.release(); ws.X1.release(); ws.acc.release();
+        ws.out.release(); ws.part.release(); ws.hub_part.release(); ws.hub_cnt.release();
+        ws.hub_ts.release(); ws.trace.release(); ws.total.release(); ws.coeffs.release();
+        staged = chebgpu::StagedState{};
+        bws = chebgpu::BatchWorkspace{};
+    }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
@@ -151,7 +180,7 @@ cheb_status cheb_graph_build(const int64_t* edges, int64_t E, const cheb_build_o
         for (int64_t i = 0; i < 2 * E; ++i)
             if (edges[i] < 0) fail(CHEB_VALIDATION, "negative vertex id in edge list");
         std::unique_ptr<cheb_graph> g(new_graph(o.device));
-        DeviceGuard dg(o.device);
+        GraphScope gs(g.get());
         DevMem d(sizeof(int64_t) * 2 * std::max<int64_t>(E, 1));
         if (E > 0)
             CHEB_CUDA_CHECK(cudaMemcpyAsync(d.get(), edges, sizeof(int64_t) * 2 * E,
@@ -171,7 +200,7 @@ cheb_status cheb_graph_build_device(const void* d_edges, int64_t E, int edge_bit
         cheb_build_opts_default(&o);
         if (opts) o = *opts;
         std::unique_ptr<cheb_graph> g(new_graph(o.device));
-        DeviceGuard dg(o.device);
+        GraphScope gs(g.get());
         build_from_edges(g.get(), d_edges, E, edge_bits, o);
         fill_info(g.get(), info);
         *out = g.release();
@@ -193,22 +222,20 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
             if (degrees[v] < 1)
                 fail(CHEB_VALIDATION, "vertex " + std::to_string(v) + " is isolated (degree 0)");
         if (offsets[0] != 0) fail(CHEB_VALIDATION, "offsets must start at 0");
-        for (int64_t v = 0; v < n; ++v)
-            if (offsets[v + 1] < offsets[v])
-                fail(CHEB_VALIDATION, "offsets not monotone at vertex " + std::to_string(v));
+        int64_t dmin = INT64_MAX, dmax = 0;
+        for (int64_t v = 0; v < n; ++v) {  // one pass: monotone offsets + degree extrema
+            const int64_t d = offsets[v + 1] - offsets[v];
+            if (d < 0) fail(CHEB_VALIDATION, "offsets not monotone at vertex " + std::to_string(v));
+            dmin = d < dmin ? d : dmin;
+            dmax = d > dmax ? d : dmax;
+        }
         std::unique_ptr<cheb_graph> g(new_graph(device));
-        DeviceGuard dg(device);
+        GraphScope gs(g.get());
         g->m = m;
         g->multi = multi != 0;
         g->rp64 = row_ptr_64 != 0;
         g->duplicates_removed = 0;
         g->isolated_dropped = 0;
-        int64_t dmin = INT64_MAX, dmax = 0;
-        for (int64_t v = 0; v < n; ++v) {
-            const int64_t d = offsets[v + 1] - offsets[v];
-            dmin = d < dmin ? d : dmin;
-            dmax = d > dmax ? d : dmax;
-        }
         g->min_degree = dmin;
         g->max_degree = dmax;
         upload_csr(g.get(), offsets, neighbors, n, nnz, inv_degree);
@@ -220,7 +247,7 @@ cheb_status cheb_graph_download_csr(cheb_graph_t g, int64_t* offsets, int64_t* n
                                     int64_t* degrees) {
     return guarded([&] {
         need_graph(g);
-        DeviceGuard dg(g->device);
+        GraphScope gs(g);
         download_csr(g, offsets, neighbors, degrees);
     });
 }
@@ -234,7 +261,7 @@ cheb_status cheb_graph_get_info(cheb_graph_t g, cheb_graph_info* info) {
 
 void cheb_graph_free(cheb_graph_t g) {
     if (!g) return;
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     cudaStreamSynchronize(g->stream);
     delete g;
 }
@@ -504,7 +531,7 @@ cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, 
                                       int64_t* max_rows) {
     return guarded([&] {
         need_graph(g);
-        DeviceGuard dg(g->device);
+        GraphScope gs(g);
         ensure_view(g);
         if (lo) *lo = g->part.cuts[g->part.rank];
         if (hi) *hi = g->part.cuts[g->part.rank + 1];
@@ -526,7 +553,7 @@ cheb_status cheb_last_timing(cheb_graph_t g, double* loop_ms, double* term_kerne
                              int* launches) {
     return guarded([&] {
         need_graph(g);
-        DeviceGuard dg(g->device);
+        GraphScope gs(g);
         CHEB_CUDA_CHECK(cudaEventSynchronize(g->ev1));
         float ms = 0.f;
         CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));

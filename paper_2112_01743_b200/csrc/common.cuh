@@ -33,6 +33,21 @@ struct Error : std::runtime_error {
                                            " (" #expr ")");                              \
     } while (0)
 
+// Stream that device allocations of the current API call are ordered on (set by
+// AllocScope).  Allocations come from the device's stream-ordered memory pool, whose
+// release threshold is raised once per device so freed blocks are reused instead of
+// returned to the driver (cheap per-call setup for the reference's stateless API).
+inline cudaStream_t& alloc_stream() {
+    thread_local cudaStream_t s = nullptr;
+    return s;
+}
+struct AllocScope {
+    cudaStream_t prev;
+    explicit AllocScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+    ~AllocScope() { alloc_stream() = prev; }
+};
+void retain_pool_memory();  // capi.cu
+
 // Owning device allocation (untyped bytes; typed views via ptr<T>()).
 class DevMem {
 public:
@@ -41,12 +56,17 @@ public:
     ~DevMem() { release(); }
     DevMem(const DevMem&) = delete;
     DevMem& operator=(const DevMem&) = delete;
-    DevMem(DevMem&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DevMem(DevMem&& o) noexcept : p_(o.p_), n_(o.n_), st_(o.st_), async_(o.async_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
     DevMem& operator=(DevMem&& o) noexcept {
         if (this != &o) {
             release();
             p_ = o.p_;
             n_ = o.n_;
+            st_ = o.st_;
+            async_ = o.async_;
             o.p_ = nullptr;
             o.n_ = 0;
         }
@@ -55,7 +75,14 @@ public:
     void alloc(size_t bytes) {
         release();
         if (bytes == 0) bytes = 16;
-        CHEB_CUDA_CHECK(cudaMalloc(&p_, bytes));
+        st_ = alloc_stream();
+        async_ = st_ != nullptr;
+        if (async_) {
+            retain_pool_memory();
+            CHEB_CUDA_CHECK(cudaMallocAsync(&p_, bytes, st_));
+        } else {
+            CHEB_CUDA_CHECK(cudaMalloc(&p_, bytes));
+        }
         n_ = bytes;
     }
     // Grow-only reuse.
@@ -63,7 +90,10 @@ public:
         if (bytes > n_ || !p_) alloc(bytes);
     }
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_) {
+            if (async_) cudaFreeAsync(p_, st_);
+            else cudaFree(p_);
+        }
         p_ = nullptr;
         n_ = 0;
     }
@@ -76,6 +106,8 @@ public:
 private:
     void* p_ = nullptr;
     size_t n_ = 0;
+    cudaStream_t st_ = nullptr;
+    bool async_ = false;
 };
 
 // Scoped device selection.
@@ -217,6 +249,12 @@ struct cheb_graph {
 };
 
 namespace chebgpu {
+// Device + allocation-stream scope of an API call on a graph handle.
+struct GraphScope {
+    DeviceGuard dg;
+    AllocScope as;
+    explicit GraphScope(const cheb_graph* g) : dg(g->device), as(g->stream) {}
+};
 // Experiment knobs (cheb_set_tuning); defaults = the product configuration.
 struct Tuning {
     int hot = -1;       // cap on the shared-memory hot prefix (vertices); -1 = capacity

@@ -1166,7 +1166,7 @@ void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::ve
 
 void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool /*host_results*/, std::vector<double>* tr,
                 double* total) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     if (s.R != 1) fail(CHEB_INVALID_ARG, "R > 1 is served by the batched path");
     if (s.mode == CHEB_MODE_BITEXACT && s.precision != CHEB_FP64)
         fail(CHEB_INVALID_ARG, "bitexact mode is fp64 only");
@@ -1183,7 +1183,7 @@ void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool /*host_results*/, std::v
 // With reference tracking (err / err_l1 columns): plain launches, per-term reduction.
 void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
                     std::vector<double>* errs, double* total) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     const bool rp64 = s.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
     if (s.precision == CHEB_FP64) {
         if (rp64) run_solve_t<int64_t, double>(g, s, h_ref, tr, errs, total);
@@ -1196,7 +1196,7 @@ void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std:
 
 // Per-term kernel durations (CUDA events around every term launch, plain launches).
 void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_ms) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     const bool rp64 = s.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
     auto run = [&](auto rp_tag, auto v_tag) {
         using RP = decltype(rp_tag);
@@ -1233,7 +1233,7 @@ void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_m
 
 // Read back ranks (original vertex order) as doubles.
 void read_ranks(cheb_graph* g, int precision, double* ranks) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     const int64_t n = g->n;
     if (precision == CHEB_FP64) {
         CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, g->ws.out.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream));
@@ -1342,7 +1342,7 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
 void power_solve(cheb_graph* g, double c, int rounds, double tol, int max_rounds, int mode,
                  const double* reference, double* ranks, cheb_trace_row* trace, int cap,
                  int* rounds_out, double* total) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     const bool fixed = rounds >= 0;
     const int budget = fixed ? rounds : max_rounds;
     const bool rp64 = mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
@@ -1380,7 +1380,7 @@ void transition_t(cheb_graph* g, const double* x, double* y, int mode) {
 }  // namespace
 
 void transition_apply(cheb_graph* g, const double* x, double* y, int mode) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     const bool rp64 = mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
     if (rp64) transition_t<int64_t>(g, x, y, mode);
     else transition_t<int>(g, x, y, mode);
@@ -1388,7 +1388,7 @@ void transition_apply(cheb_graph* g, const double* x, double* y, int mode) {
 
 // ---------------- staged API (cpaa.cpp:167-196) ---------------------------------------
 void staged_init(cheb_graph* g, double c0, int mode) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     StagedState& S = g->staged;
     const int64_t n = g->n;
     const size_t vb = sizeof(double) * std::max<int64_t>(n, 1);
@@ -1406,7 +1406,7 @@ void staged_init(cheb_graph* g, double c0, int mode) {
 }
 
 void staged_set(cheb_graph* g, const double* Tp, const double* Tc, const double* acc, int k) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     StagedState& S = g->staged;
     if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
     const Layout L = layout_of(g, S.mode);
@@ -1451,7 +1451,7 @@ void staged_generate_t(cheb_graph* g) {
 }  // namespace
 
 void staged_generate(cheb_graph* g) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     if (!g->staged.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
     const bool rp64 = g->staged.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
     if (rp64) staged_generate_t<int64_t>(g);
@@ -1459,7 +1459,7 @@ void staged_generate(cheb_graph* g) {
 }
 
 void staged_accumulate(cheb_graph* g, double ck) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     StagedState& S = g->staged;
     if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
     k_accumulate<double><<<grid1d(g->n), kThreads, 0, g->stream>>>(S.acc.ptr<double>(), S.T_next.ptr<double>(), g->n, ck);
@@ -1476,7 +1476,7 @@ void staged_rotate(cheb_graph* g) {
 }
 
 void staged_get(cheb_graph* g, double* Tp, double* Tc, double* Tn, double* acc, int* k) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     StagedState& S = g->staged;
     if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
     const Layout L = layout_of(g, S.mode);

@@ -456,7 +456,7 @@ void batch_dispatch(cheb_graph* g, const BatchSpec& s, std::vector<double>& tr, 
 
 void cpaa_batch_solve(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace,
                       std::vector<double>& totals, std::vector<double>* term_ms) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     if (s.R < 1 || s.R > 128) fail(CHEB_INVALID_ARG, "batched solve supports 1 <= R <= 128");
     ensure_view(g);
     if (g->view.rp64) {
@@ -469,7 +469,7 @@ void cpaa_batch_solve(cheb_graph* g, const BatchSpec& s, std::vector<double>& tr
 }
 
 void read_batch_ranks(cheb_graph* g, double* ranks, int R) {
-    DeviceGuard dg(g->device);
+    GraphScope gs(g);
     CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, g->bws.out.get(), sizeof(double) * (size_t)g->n * R,
                                     cudaMemcpyDeviceToHost, g->stream));
     CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
