@@ -545,6 +545,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         const std::string k = key ? key : "";
         if (k == "hot") tuning().hot = value;
         else if (k == "nogather") tuning().nogather = value;
+        else if (k == "skip") tuning().skip = value;
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }

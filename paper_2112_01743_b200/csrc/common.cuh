@@ -154,7 +154,7 @@ constexpr int kWarps = 32;           // warps per CTA of the term kernel (1 CTA 
 constexpr int kWarpNnz = 248;        // nnz per tile: with <= 7 alignment slots, 8 per lane
 constexpr int kWarpRows = 32;        // rows per pack tile (one per lane)
 constexpr int kColBuf = 264;         // ints per TMA column buffer (256 + alignment slack)
-constexpr int kHotBytes = 128 * 1024;  // shared-memory copy of the hot x prefix
+constexpr int kHotBytes = 86 * 1024;  // shared hot x prefix; sized so hot + scratch fit the 164 KB carve-out and L1 keeps ~64 KB (tools/variant_run.sh sweep)
 constexpr int kTileChunk = 0x10;
 
 struct SolverView {
@@ -259,12 +259,14 @@ struct GraphScope {
 struct Tuning {
     int hot = -1;       // cap on the shared-memory hot prefix (vertices); -1 = capacity
     int nogather = 0;   // 1: skip the x gathers (timing experiments only; wrong results)
+    int skip = 0;       // bit 0: skip chunk tiles, bit 1: skip pack tiles (experiments only)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
         Tuning x;
         if (const char* e = std::getenv("CHEB_TUNE_HOT")) x.hot = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_NOGATHER")) x.nogather = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_SKIP")) x.skip = std::atoi(e);
         return x;
     }();
     return t;

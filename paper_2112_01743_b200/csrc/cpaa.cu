@@ -69,6 +69,7 @@ struct TermArgs {
     unsigned* hub_cnt;
     double* hub_ts;  // [n_hub][2] this term
     int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
+    int tune_skip;      // experiments only: bit 0 skip chunk tiles, bit 1 skip pack tiles
 };
 
 // Row epilogue.  u is a row of the current layout; deg its row length.
@@ -117,6 +118,30 @@ __device__ __forceinline__ void epilogue(const TermArgs<RP, V>& a, int64_t u, V 
 // (tools/micro_gather.cu): random LDS.64 876 G/s vs random LDG over an L2-resident
 // table 256 G/s — the gather, not HBM, bounds this path.
 
+// Cold x gathers: read-only path without L1 allocation (the L1 left next to the shared
+// hot prefix is tiny; a random line would only evict another).
+#ifndef CHEB_COLD_NOALLOC
+#define CHEB_COLD_NOALLOC 0
+#endif
+__device__ __forceinline__ double ldg_cold(const double* p) {
+#if CHEB_COLD_NOALLOC
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float ldg_cold(const float* p) {
+#if CHEB_COLD_NOALLOC
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 __device__ __forceinline__ double lds_v(unsigned addr, double) {
     double v;
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
@@ -137,7 +162,7 @@ __device__ __forceinline__ void gather8(const V* __restrict__ x, unsigned hot_s,
 #pragma unroll
     for (int q = 0; q < U; ++q) {
         v[q] = V(0);
-        if (c[q] >= H) v[q] = ldg_x(x + c[q]);
+        if (c[q] >= H) v[q] = ldg_cold(x + c[q]);
     }
 #pragma unroll
     for (int q = 0; q < U; ++q)
@@ -310,6 +335,14 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
     }
     const int t = w + i * S;  // tile id (slot of a hub-row partial)
     mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
+    if (a.tune_skip && ((a.tune_skip & 1) ? (d.meta & kTileChunk) : !(d.meta & kTileChunk))) {
+        __syncwarp();
+        if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
+            const int blk = i / kDescBlock + 2;
+            if (blk * kDescBlock < nt) issue_desc(my, blk, nullptr, ws.desc[blk & 1], &ws.descm[blk & 1]);
+        }
+        return;
+    }
     const int* cb = ws.colb[i & 1] + (int)(d.z0 & 7);  // tile-local position p at cb[p]
 
     if (d.meta & kTileChunk) {
@@ -751,6 +784,7 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);
         TermArgs<RP, V> ab = a;
         ab.tune_nogather = tuning().nogather;
+        ab.tune_skip = tuning().skip;
         k_term_warp<EPI, RP, V><<<g->view.grid, kWarps * 32, smem, st>>>(
             ab, g->view.prog.ptr<WTile>(), g->view.prog_len, g->view.n_tiles, H);
         if (g->view.n_hub > 0) {

@@ -42,3 +42,7 @@ run("default")
 run("hot=0 (all L2 gathers)", hot=0)
 run("hot=4096", hot=4096)
 run("no gathers", nogather=1)
+run("chunk tiles only", skip=2)
+run("pack tiles only", skip=1)
+run("chunk only, no gathers", skip=2, nogather=1)
+run("pack only, no gathers", skip=1, nogather=1)
