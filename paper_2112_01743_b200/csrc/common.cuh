@@ -48,6 +48,11 @@ struct AllocScope {
 };
 void retain_pool_memory();  // capi.cu
 
+// L2 persistence for the gathered vector: an access-policy window over the first `bytes` of
+// `base` (the degree-sorted hot prefix of x), sized to the device's persisting-L2 limit.
+// Returns false when the device offers no persisting L2.
+bool l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* w);
+
 // Owning device allocation (untyped bytes; typed views via ptr<T>()).
 class DevMem {
 public:
@@ -260,6 +265,7 @@ struct Tuning {
     int hot = -1;       // cap on the shared-memory hot prefix (vertices); -1 = capacity
     int nogather = 0;   // 1: skip the x gathers (timing experiments only; wrong results)
     int skip = 0;       // bit 0: skip chunk tiles, bit 1: skip pack tiles (experiments only)
+    int l2win = 1;      // 1: persisting-L2 window over the hot prefix of x (default on)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -267,6 +273,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_HOT")) x.hot = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_NOGATHER")) x.nogather = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_SKIP")) x.skip = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_L2WIN")) x.l2win = std::atoi(e);
         return x;
     }();
     return t;

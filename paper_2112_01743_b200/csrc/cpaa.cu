@@ -785,8 +785,23 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         TermArgs<RP, V> ab = a;
         ab.tune_nogather = tuning().nogather;
         ab.tune_skip = tuning().skip;
-        k_term_warp<EPI, RP, V><<<g->view.grid, kWarps * 32, smem, st>>>(
-            ab, g->view.prog.ptr<WTile>(), g->view.prog_len, g->view.n_tiles, H);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(g->view.grid);
+        cfg.blockDim = dim3(kWarps * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        cfg.attrs = attr;
+        cfg.numAttrs = 0;
+        // keep the hot (degree-sorted) prefix of x_k resident in L2 across the term
+        if (tuning().l2win &&
+            l2_window(a.x_in, (size_t)std::max<int64_t>(g->view.x_len, 1) * sizeof(V),
+                      &attr[0].val.accessPolicyWindow)) {
+            attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+            cfg.numAttrs = 1;
+        }
+        CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V>, ab, (const WTile*)g->view.prog.ptr<WTile>(),
+                                           g->view.prog_len, g->view.n_tiles, H));
         if (g->view.n_hub > 0) {
             CHEB_CUDA_CHECK(cudaGetLastError());
             const int hb = (int)std::min<int64_t>((g->view.n_hub * 32 + 255) / 256, 148 * 16);

@@ -391,7 +391,21 @@ void batch_run(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace, st
         a.hub_part = w.hub_part.ptr<double>();
         a.hub_ts = Vw.n_hub ? w.hub_ts.ptr<double>() : nullptr;
         if (term_ms) CHEB_CUDA_CHECK(cudaEventRecord(ev[2 * (k - 1)], st));
-        k_spmm_term<RP, V, VPL><<<grid, 256, 0, st>>>(a, Vw.tiles.ptr<Tile>(), Vw.n_tiles);
+        {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(256);
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            cfg.attrs = attr;
+            cfg.numAttrs = 0;
+            if (tuning().l2win > 1 && l2_window(a.x_in, elems * sizeof(V), &attr[0].val.accessPolicyWindow)) {
+                attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+                cfg.numAttrs = 1;
+            }
+            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_spmm_term<RP, V, VPL>, a, (const Tile*)Vw.tiles.ptr<Tile>(),
+                                               Vw.n_tiles));
+        }
         CHEB_CUDA_CHECK(cudaGetLastError());
         ++launches;
         if (Vw.n_hub) {

@@ -343,3 +343,22 @@ def test_nccl_partitioned_path_single_rank(cheb):
         assert np.max(np.abs(part.ranks - z["cpaa39_ranks"])) <= TOL64
         dg.free()
         comm.close()
+
+
+def test_int64_row_pointer_solves(cheb):
+    """Config 4 uses int64 row pointers: the same solves on an rp64 handle."""
+    for name in ("gnp2000", "star100", "config1"):
+        z = load_golden(name)
+        dg, info = cheb.build_device_graph(z["edges"], cheb.BuildOptions(row_ptr_64=True))
+        assert info["row_ptr_64"] == 1
+        g = dg.download()
+        assert np.array_equal(g.offsets, z["offsets"]) and np.array_equal(g.neighbors, z["neighbors"])
+        fast = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+        assert np.max(np.abs(fast.ranks - z["cpaa39_ranks"])) <= TOL64
+        exact = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39, mode=cheb.MODE_BITEXACT))
+        assert np.array_equal(exact.ranks, z["cpaa39_ranks"])
+        p = cheb.run_power(dg, cheb.PowerConfig(rounds=210))
+        assert np.max(np.abs(p.ranks - z["power210_ranks"])) <= TOL64
+        b = cheb.run_cpaa_batch(dg, cheb.SolverConfig(rounds=39), personalization=np.ones((g.n, 2)))
+        assert np.max(np.abs(b.ranks[:, 1] - z["cpaa39_ranks"])) <= TOL64
+        dg.free()

@@ -35,12 +35,13 @@ def run(label, **kv):
     t = min(res)
     print(f"{label:28s} {t*1e3:8.1f} us/term  {B/(t*1e-3)/1e9:7.1f} GB/s  {info['nnz']/(t*1e-3)/1e9:7.1f} GTEPS")
     for k in kv:
-        lib.cheb_set_tuning(k.encode(), -1 if k == "hot" else 0)
+        lib.cheb_set_tuning(k.encode(), {"hot": -1, "l2win": 1}.get(k, 0))
 
 
 run("default")
 run("hot=0 (all L2 gathers)", hot=0)
 run("hot=4096", hot=4096)
+run("no L2 window", l2win=0)
 run("no gathers", nogather=1)
 run("chunk tiles only", skip=2)
 run("pack tiles only", skip=1)
