@@ -86,6 +86,11 @@ struct VecIO<float, 4> {
     }
 };
 
+#ifndef CHEB_SPMM_UNROLL
+#define CHEB_SPMM_UNROLL 8
+#endif
+constexpr int kSpmmUnroll = CHEB_SPMM_UNROLL;
+
 // Sum over CSR entries [b, e) of the gathered R-vectors (lane's VPL columns), 4 entries
 // (4 column ids then 4 row gathers) in flight per lane.
 template <class RP, class V, int VPL>
@@ -95,22 +100,18 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
     for (int k = 0; k < VPL; ++k) s[k] = V(0);
     const int off = lane * VPL;
     int64_t j = b;
-    for (; j + 3 < e; j += 4) {
-        const int c0 = __ldg(a.col + j), c1 = __ldg(a.col + j + 1);
-        const int c2 = __ldg(a.col + j + 2), c3 = __ldg(a.col + j + 3);
-        V v0[VPL], v1[VPL], v2[VPL], v3[VPL];
-        if (live) {
-            VecIO<V, VPL>::ld(a.x_in + (int64_t)c0 * a.Rs + off, v0);
-            VecIO<V, VPL>::ld(a.x_in + (int64_t)c1 * a.Rs + off, v1);
-            VecIO<V, VPL>::ld(a.x_in + (int64_t)c2 * a.Rs + off, v2);
-            VecIO<V, VPL>::ld(a.x_in + (int64_t)c3 * a.Rs + off, v3);
+    for (; j + kSpmmUnroll - 1 < e; j += kSpmmUnroll) {
+        int c[kSpmmUnroll];
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) {
-                s[k] += v0[k];
-                s[k] += v1[k];
-                s[k] += v2[k];
-                s[k] += v3[k];
-            }
+        for (int q = 0; q < kSpmmUnroll; ++q) c[q] = __ldg(a.col + j + q);
+        if (live) {
+            V v[kSpmmUnroll][VPL];
+#pragma unroll
+            for (int q = 0; q < kSpmmUnroll; ++q) VecIO<V, VPL>::ld(a.x_in + (int64_t)c[q] * a.Rs + off, v[q]);
+#pragma unroll
+            for (int q = 0; q < kSpmmUnroll; ++q)
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) s[k] += v[q][k];
         }
     }
     for (; j < e; ++j) {
