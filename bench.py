@@ -357,7 +357,8 @@ class Solver:
         n, R = host.n, self.R
         off = torch.from_numpy(host.offsets).pin_memory().numpy()
         nb = torch.from_numpy(host.neighbors).pin_memory().numpy()
-        deg, inv = host.degrees, host.inv_degree
+        deg = host.degrees  # read on the host only (essential checks)
+        inv = torch.from_numpy(host.inv_degree).pin_memory().numpy()
         ranks = torch.empty(n * R, dtype=torch.float64).pin_memory().numpy()
         tr = (L.cheb_trace_row * 64)()
         rounds, tot = C.c_int(), C.c_double()
@@ -392,10 +393,10 @@ class Solver:
         e2e_s = dist.max(statistics.mean(times))
         units = self.info["nnz"] * self.R * self.M
         return {"value": round(units / e2e_s / 1e9, 4), "unit": "GTEPS",
-                "h2d_bytes_per_step": int(off.nbytes + nb.nbytes),
+                "h2d_bytes_per_step": int(off.nbytes + nb.nbytes + inv.nbytes),
                 "d2h_bytes_per_step": int(ranks.nbytes + 2 * self.M * 8),
                 "ms_per_step": round(e2e_s * 1e3, 3),
-                "path": "cheb_graph_upload_csr(pinned int64 CSR) + " +
+                "path": "cheb_graph_upload_csr(pinned int64 CSR + inv_degree) + " +
                         ("cheb_cpaa_batch" if R > 1 else "cheb_cpaa") + "(host ranks) + cheb_graph_free"}
 
 

@@ -17,6 +17,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <chrono>
+#include <mutex>
 #include <cstring>
 
 #include "common.cuh"
@@ -196,13 +198,24 @@ __global__ void k_widen_col(const int* __restrict__ in, int64_t cnt, int64_t* __
 }
 
 // Upload path: int64 neighbours -> int32, flag out-of-range ids.
-__global__ void k_narrow_col(const int64_t* __restrict__ in, int64_t cnt, int64_t n,
+__global__ void k_narrow_col(const int64_t* __restrict__ in, int64_t cnt, int64_t n, int64_t base,
                              int* __restrict__ out, unsigned long long* bad) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
          i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t v = in[i];
-        if (v < 0 || v >= n) atomicMin(bad, (unsigned long long)i);
-        out[i] = (int)v;
+        const int64_t v = in[i];
+        const bool ok = v >= 0 && v < n;
+        if (!ok) atomicMin(bad, (unsigned long long)(base + i));
+        out[i] = ok ? (int)v : 0;  // never an out-of-range id on the device
+    }
+}
+
+// inv_degree canonical iff every entry is 1.0/deg bitwise (IEEE division, as the host's).
+__global__ void k_inv_check(const int64_t* __restrict__ rp, const double* __restrict__ inv, int64_t n,
+                            int* __restrict__ differs) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const double want = __ddiv_rn(1.0, (double)(rp[v + 1] - rp[v]));
+        if (__double_as_longlong(want) != __double_as_longlong(inv[v])) *differs = 1;
     }
 }
 
@@ -416,64 +429,131 @@ void build_from_edges(cheb_graph* g, const void* d_edges, int64_t E, int edge_bi
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
+template <class RPO, class RPN>
+static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<void()>& before_col);
+
+static bool dbg_on() {
+    static const bool on = getenv("CHEB_DEBUG_UPLOAD") != nullptr;
+    return on;
+}
+static std::chrono::steady_clock::time_point& dbg_t0() {
+    static std::chrono::steady_clock::time_point t;
+    return t;
+}
+static void dbg_mark(const char* what) {
+    if (!dbg_on()) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[upload] %-24s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - dbg_t0()).count());
+}
+
 void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors, int64_t n,
-                int64_t nnz, const double* inv_degree) {
+                int64_t nnz, const double* inv_degree, const std::function<void()>& host_checks) {
     cudaStream_t st = g->stream;
+    const bool dbg = dbg_on();
+    dbg_t0() = std::chrono::steady_clock::now();
+    auto mark = dbg_mark;
     g->n = n;
     g->nnz = nnz;
     g->rp64 = g->rp64 || nnz > INT32_MAX;
     if (n > INT32_MAX - 1) fail(CHEB_CAPACITY, "device path supports n < 2^31");
 
-    // offsets: host int64 -> device (int32 narrowed when possible)
+    // 1. offsets: host int64 -> device (int32 narrowed when possible)
     DevMem rp64(sizeof(int64_t) * (n + 1));
     CHEB_CUDA_CHECK(cudaMemcpyAsync(rp64.get(), offsets, sizeof(int64_t) * (n + 1),
                                     cudaMemcpyHostToDevice, st));
-    if (g->rp64) {
-        g->row_ptr = std::move(rp64);
-    } else {
+    if (!g->rp64) {
         g->row_ptr.alloc(sizeof(int) * (n + 1));
         k_narrow_rowptr<<<grid_for(n + 1), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), n + 1,
                                                                    g->row_ptr.ptr<int>());
         CHEB_CUDA_CHECK(cudaGetLastError());
     }
-    // neighbours: int64 -> int32, range-checked.  Chunked to bound the staging buffer.
-    g->col.alloc(sizeof(int) * std::max<int64_t>(nnz, 1));
-    if (nnz > 0) {
-        const int64_t chunk = std::min<int64_t>(nnz, int64_t(1) << 26);
-        DevMem stage(sizeof(int64_t) * chunk);
-        DevMem bad(sizeof(unsigned long long));
-        unsigned long long none = ~0ull;
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(bad.get(), &none, 8, cudaMemcpyHostToDevice, st));
-        for (int64_t off = 0; off < nnz; off += chunk) {
-            const int64_t c = std::min(chunk, nnz - off);
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(stage.get(), neighbors + off, sizeof(int64_t) * c,
-                                            cudaMemcpyHostToDevice, st));
-            k_narrow_col<<<grid_for(c), kBuildThreads, 0, st>>>(stage.ptr<int64_t>(), c, n,
-                                                                 g->col.ptr<int>() + off,
-                                                                 bad.ptr<unsigned long long>());
-            CHEB_CUDA_CHECK(cudaGetLastError());
-        }
-        unsigned long long b = read_scalar(bad.ptr<unsigned long long>(), st);
-        if (b != ~0ull) fail(CHEB_VALIDATION, "neighbor id out of range at entry " + std::to_string(b));
-    }
-    // inv_degree: canonical (1.0/deg bitwise) -> in-kernel reciprocal; else keep the array.
+    // 2. inv_degree: checked on the device; kept only when not canonical (graph.cpp:97-100)
+    DevMem flags(sizeof(unsigned long long) + sizeof(int));
+    auto* bad = flags.ptr<unsigned long long>();
+    auto* inv_differs = reinterpret_cast<int*>(flags.ptr<char>() + sizeof(unsigned long long));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(inv_differs, 0, sizeof(int), st));
     g->inv_array = false;
     if (inv_degree) {
-        for (int64_t v = 0; v < n; ++v) {
-            const double want = 1.0 / static_cast<double>(offsets[v + 1] - offsets[v]);
-            if (std::memcmp(&want, &inv_degree[v], sizeof(double)) != 0) {
-                g->inv_array = true;
-                break;
-            }
+        g->inv.alloc(sizeof(double) * n);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(g->inv.get(), inv_degree, sizeof(double) * n,
+                                        cudaMemcpyHostToDevice, st));
+        k_inv_check<<<grid_for(n), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), g->inv.ptr<double>(), n,
+                                                          inv_differs);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
+    cudaEvent_t ev_rp = nullptr, ev_col = nullptr, ev_view = nullptr;
+    struct Events {
+        cudaEvent_t* e[3];
+        ~Events() {
+            for (auto* p : e)
+                if (*p) cudaEventDestroy(*p);
         }
-        if (g->inv_array) {
-            g->inv.alloc(sizeof(double) * n);
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(g->inv.get(), inv_degree, sizeof(double) * n,
+    } evs{{&ev_rp, &ev_col, &ev_view}};
+    for (auto* p : evs.e) CHEB_CUDA_CHECK(cudaEventCreateWithFlags(p, cudaEventDisableTiming));
+    CHEB_CUDA_CHECK(cudaEventRecord(ev_rp, st));
+
+    // 3. neighbours: int64 -> int32, range-checked.  Chunked to bound the staging buffer.
+    g->col.alloc(sizeof(int) * std::max<int64_t>(nnz, 1));
+    if (nnz > 0) {
+        const int64_t chunk = std::min<int64_t>(nnz, int64_t(1) << 25);
+        DevMem stage[2] = {DevMem(sizeof(int64_t) * chunk), DevMem(sizeof(int64_t) * chunk)};
+        int i = 0;
+        for (int64_t off = 0; off < nnz; off += chunk, i ^= 1) {
+            const int64_t c = std::min(chunk, nnz - off);
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(stage[i].get(), neighbors + off, sizeof(int64_t) * c,
                                             cudaMemcpyHostToDevice, st));
+            k_narrow_col<<<grid_for(c), kBuildThreads, 0, st>>>(stage[i].ptr<int64_t>(), c, n, off,
+                                                                 g->col.ptr<int>() + off, bad);
+            CHEB_CUDA_CHECK(cudaGetLastError());
         }
     }
-    g->view.ready = false;
+    CHEB_CUDA_CHECK(cudaEventRecord(ev_col, st));
+    mark("enqueued copies");
+
+    // 4. the reference's host-side checks, while the copies are in flight
+    if (host_checks) host_checks();
+    mark("host checks");
+
+    if (g->rp64) g->row_ptr = std::move(rp64);  // the view reads the canonical row_ptr
+
+    // 5. solver view (single-GPU layout) on the auxiliary stream: the degree-only half
+    //    overlaps the neighbour copy; the column permute waits for it.
+    if (g->part.G == 1 && !g->part.comm && n > 0) {
+        if (!g->aux) CHEB_CUDA_CHECK(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
+        CHEB_CUDA_CHECK(cudaStreamWaitEvent(g->aux, ev_rp, 0));
+        {
+            AllocScope as(g->aux);
+            g->view = SolverView{};
+            auto wait_col = [&] { CHEB_CUDA_CHECK(cudaStreamWaitEvent(g->aux, ev_col, 0)); };
+            if (g->rp64)
+                build_view_t<int64_t, int64_t>(g, g->aux, wait_col);
+            else
+                build_view_t<int, int>(g, g->aux, wait_col);
+        }
+        mark("view enqueued");
+        if (dbg) { cudaEventSynchronize(ev_col); mark("neighbours landed"); cudaStreamSynchronize(g->aux); mark("view done"); }
+        CHEB_CUDA_CHECK(cudaEventRecord(ev_view, g->aux));
+        CHEB_CUDA_CHECK(cudaStreamWaitEvent(st, ev_view, 0));
+        g->view.set_stream(st);
+    }
+    rp64.release();  // (int32 graphs) stream-ordered after the narrowing and the inv check
+
+    // 6. device-side verdicts
+    unsigned char out[sizeof(unsigned long long) + sizeof(int)];
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(out, flags.get(), sizeof out, cudaMemcpyDeviceToHost, st));
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    unsigned long long b;
+    int differs;
+    std::memcpy(&b, out, sizeof b);
+    std::memcpy(&differs, out + sizeof b, sizeof differs);
+    mark("synced");
+    if (b != ~0ull) fail(CHEB_VALIDATION, "neighbor id out of range at entry " + std::to_string(b));
+    g->inv_array = inv_degree && differs;
+    if (g->inv_array && g->view.ready) {  // the view gathers inv in its row order
+        g->view.ready = false;
+    }
+    if (!g->inv_array) g->inv.release();
 }
 
 void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees) {
@@ -588,6 +668,36 @@ __global__ void k_gather_inv(const double* __restrict__ inv, const int* __restri
 
 }  // namespace
 
+// Pinned staging for the view's small host<->device transfers.  Pageable copies are staged
+// by the driver behind whatever the copy engine is doing — during an upload that is the
+// neighbour array — so the view build would wait for it.  Grow-only slots, process-wide,
+// held under a lock for one build (every build ends with a stream synchronize).
+struct PinnedArena {
+    std::mutex mu;
+    void* p[5] = {};
+    size_t n[5] = {};
+    void* get(int slot, size_t bytes) {
+        if (bytes > n[slot]) {
+            if (p[slot]) CHEB_CUDA_CHECK(cudaFreeHost(p[slot]));
+            p[slot] = nullptr;
+            n[slot] = 0;
+            const size_t want = std::max<size_t>(bytes + bytes / 4, 1 << 16);
+            CHEB_CUDA_CHECK(cudaHostAlloc(&p[slot], want, cudaHostAllocPortable));
+            n[slot] = want;
+        }
+        return p[slot];
+    }
+};
+PinnedArena& pinned_arena() {
+    static PinnedArena* a = new PinnedArena();  // never destroyed: outlives every handle
+    return *a;
+}
+void h2d_staged(void* dst, const void* src, size_t bytes, int slot, cudaStream_t st) {
+    void* h = pinned_arena().get(slot, bytes);
+    std::memcpy(h, src, bytes);
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, st));
+}
+
 // Greedy tiling of the degree-sorted rows (runs of equal degree, descending).
 static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
                                     const std::vector<int64_t>& run_cnt, int64_t n, int64_t nnz,
@@ -653,8 +763,7 @@ static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
 }
 
 template <class RPO, class RPN>
-static void build_view_t(cheb_graph* g) {
-    cudaStream_t st = g->stream;
+static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<void()>& before_col) {
     SolverView& V = g->view;
     const int64_t n = g->n;
     TempStore tmp;
@@ -672,6 +781,7 @@ static void build_view_t(cheb_graph* g) {
         CHEB_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(t, bytes, keys.ptr<unsigned>(), keys2.ptr<unsigned>(),
                                                         ids.ptr<int>(), V.order.ptr<int>(), n, 0, 32, st));
     }
+    dbg_mark("  view: sort enqueued");
     DevMem rank(sizeof(int) * n);
     k_scatter_rank<<<grid_for(n), kBuildThreads, 0, st>>>(V.order.ptr<int>(), n, rank.ptr<int>());
     DevMem deg_new(sizeof(int64_t) * (n + 1));
@@ -725,7 +835,9 @@ static void build_view_t(cheb_graph* g) {
         CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, bytes, dl.ptr<int64_t>(), rp64.ptr<int64_t>(), nl + 1, st));
         CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     }
+    dbg_mark("  view: scan synced");
     const int64_t nnz_l = nl > 0 ? read_scalar(rp64.ptr<int64_t>() + nl, st) : 0;
+    dbg_mark("  view: nnz read");
     V.nnz_local = nnz_l;
     V.rp64 = sizeof(RPN) == 8;
     if (V.rp64) {
@@ -734,7 +846,67 @@ static void build_view_t(cheb_graph* g) {
         V.row_ptr.alloc(sizeof(int) * (nl + 1));
         k_narrow_rowptr<<<grid_for(nl + 1), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), nl + 1, V.row_ptr.ptr<int>());
     }
+    // Runs of equal degree (descending) -> greedy tiles on the host
+    // (degree-only: overlaps the neighbour upload when built from upload_csr).
+    std::lock_guard<std::mutex> staging_lock(pinned_arena().mu);
+    std::vector<int64_t> run_deg, run_cnt;
+    std::vector<int> hub_first;
+    if (nl > 0) {
+        DevMem uniq(sizeof(int64_t) * nl), cnts(sizeof(int64_t) * nl), nruns(sizeof(int64_t));
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, deg_new.ptr<int64_t>() + lo, uniq.ptr<int64_t>(),
+                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), nl, st));
+        void* t = tmp.get(bytes);
+        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(t, bytes, deg_new.ptr<int64_t>() + lo, uniq.ptr<int64_t>(),
+                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), nl, st));
+        const int64_t R = read_scalar(nruns.ptr<int64_t>(), st);
+        run_deg.resize(R);
+        run_cnt.resize(R);
+        auto* hd = static_cast<int64_t*>(pinned_arena().get(3, sizeof(int64_t) * R));
+        auto* hc = static_cast<int64_t*>(pinned_arena().get(4, sizeof(int64_t) * R));
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(hd, uniq.get(), sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(hc, cnts.get(), sizeof(int64_t) * R, cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        std::memcpy(run_deg.data(), hd, sizeof(int64_t) * R);
+        std::memcpy(run_cnt.data(), hc, sizeof(int64_t) * R);
+    }
+    dbg_mark("  view: runs read");
+    const std::vector<Tile> tiles = make_tiles(run_deg, run_cnt, nl, nnz_l, &V.n_hub, &V.n_chunk_tiles, hub_first);
+    hub_first.push_back(V.n_chunk_tiles);
+    V.hub_first.alloc(sizeof(int) * hub_first.size());
+    h2d_staged(V.hub_first.get(), hub_first.data(), sizeof(int) * hub_first.size(), 0, st);
+    V.n_tiles = (int)tiles.size() - 1;
+    {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        V.grid = std::max(1, std::min(sms, (V.n_tiles + kWarps - 1) / kWarps));
+    }
+    {   // per-warp programs (warp-major), padded to whole descriptor blocks
+        const int S = V.grid * kWarps;
+        const int per = (V.n_tiles + S - 1) / S;
+        V.prog_len = std::max(kDescBlock, (per + kDescBlock - 1) / kDescBlock * kDescBlock);
+        const size_t np = (size_t)S * V.prog_len;
+        auto* prog = static_cast<WTile*>(pinned_arena().get(1, sizeof(WTile) * np));  // built in place
+        std::memset(prog, 0, sizeof(WTile) * np);
+        for (int t = 0; t < V.n_tiles; ++t) {
+            const Tile& a = tiles[t];
+            const Tile& b = tiles[t + 1];
+            WTile w;
+            w.nnz_begin = a.nnz_begin;
+            w.row_begin = a.row_begin;
+            w.cnt = (uint16_t)(b.nnz_begin - a.nnz_begin);
+            w.rows = (uint8_t)((a.meta & kTileChunk) ? 1 : (b.row_begin - a.row_begin));
+            w.meta = (uint8_t)a.meta;
+            prog[(size_t)(t % S) * V.prog_len + t / S] = w;
+        }
+        V.prog.alloc(sizeof(WTile) * np);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(V.prog.get(), prog, sizeof(WTile) * np, cudaMemcpyHostToDevice, st));
+    }
+    V.tiles.alloc(sizeof(Tile) * tiles.size());
+    h2d_staged(V.tiles.get(), tiles.data(), sizeof(Tile) * tiles.size(), 2, st);
     V.col.alloc(sizeof(int) * std::max<int64_t>(nnz_l, 1) + 64);  // TMA reads round up to 16 B
+    if (before_col) before_col();
     if (nl > 0) {
         k_permute_rows<<<grid_for(nl * 32), kBuildThreads, 0, st>>>(rp_old, g->col.ptr<int>(), V.row_ptr.ptr<RPN>(),
                                                                    V.order.ptr<int>() + lo, colmap, nl,
@@ -757,66 +929,18 @@ static void build_view_t(cheb_graph* g) {
         CHEB_CUDA_CHECK(cudaGetLastError());
     }
 
-    // Runs of equal degree (descending) -> greedy tiles on the host.
-    std::vector<int64_t> run_deg, run_cnt;
-    if (nl > 0) {
-        DevMem uniq(sizeof(int64_t) * nl), cnts(sizeof(int64_t) * nl), nruns(sizeof(int64_t));
-        size_t bytes = 0;
-        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, deg_new.ptr<int64_t>() + lo, uniq.ptr<int64_t>(),
-                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), nl, st));
-        void* t = tmp.get(bytes);
-        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(t, bytes, deg_new.ptr<int64_t>() + lo, uniq.ptr<int64_t>(),
-                                                           cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), nl, st));
-        const int64_t R = read_scalar(nruns.ptr<int64_t>(), st);
-        run_deg.resize(R);
-        run_cnt.resize(R);
-        CHEB_CUDA_CHECK(cudaMemcpy(run_deg.data(), uniq.get(), sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
-        CHEB_CUDA_CHECK(cudaMemcpy(run_cnt.data(), cnts.get(), sizeof(int64_t) * R, cudaMemcpyDeviceToHost));
-    }
-    std::vector<int> hub_first;
-    const std::vector<Tile> tiles = make_tiles(run_deg, run_cnt, nl, nnz_l, &V.n_hub, &V.n_chunk_tiles, hub_first);
-    hub_first.push_back(V.n_chunk_tiles);
-    V.hub_first.alloc(sizeof(int) * hub_first.size());
-    CHEB_CUDA_CHECK(cudaMemcpy(V.hub_first.get(), hub_first.data(), sizeof(int) * hub_first.size(),
-                               cudaMemcpyHostToDevice));
-    V.n_tiles = (int)tiles.size() - 1;
-    {
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        V.grid = std::max(1, std::min(sms, (V.n_tiles + kWarps - 1) / kWarps));
-    }
-    {   // per-warp programs (warp-major), padded to whole descriptor blocks
-        const int S = V.grid * kWarps;
-        const int per = (V.n_tiles + S - 1) / S;
-        V.prog_len = std::max(kDescBlock, (per + kDescBlock - 1) / kDescBlock * kDescBlock);
-        std::vector<WTile> prog((size_t)S * V.prog_len, WTile{0, 0, 0, 0, 0});
-        for (int t = 0; t < V.n_tiles; ++t) {
-            const Tile& a = tiles[t];
-            const Tile& b = tiles[t + 1];
-            WTile w;
-            w.nnz_begin = a.nnz_begin;
-            w.row_begin = a.row_begin;
-            w.cnt = (uint16_t)(b.nnz_begin - a.nnz_begin);
-            w.rows = (uint8_t)((a.meta & kTileChunk) ? 1 : (b.row_begin - a.row_begin));
-            w.meta = (uint8_t)a.meta;
-            prog[(size_t)(t % S) * V.prog_len + t / S] = w;
-        }
-        V.prog.alloc(sizeof(WTile) * prog.size());
-        CHEB_CUDA_CHECK(cudaMemcpy(V.prog.get(), prog.data(), sizeof(WTile) * prog.size(), cudaMemcpyHostToDevice));
-    }
-    V.tiles.alloc(sizeof(Tile) * tiles.size());
-    CHEB_CUDA_CHECK(cudaMemcpy(V.tiles.get(), tiles.data(), sizeof(Tile) * tiles.size(), cudaMemcpyHostToDevice));
+    dbg_mark("  view: tiles staged");
     V.ready = true;
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    dbg_mark("  view: synced");
 }
 
 void ensure_view(cheb_graph* g) {
     if (g->view.ready) return;
     if (g->rp64)
-        build_view_t<int64_t, int64_t>(g);
+        build_view_t<int64_t, int64_t>(g, g->stream, nullptr);
     else
-        build_view_t<int, int>(g);
+        build_view_t<int, int>(g, g->stream, nullptr);
 }
 
 }  // namespace chebgpu

@@ -135,6 +135,7 @@ cheb_graph::~cheb_graph() {
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    if (aux) cudaStreamSynchronize(aux);
     if (stream) cudaStreamSynchronize(stream);
     {   // return every buffer to the pool on this graph's stream while it still exists
         row_ptr.release();
@@ -154,6 +155,7 @@ cheb_graph::~cheb_graph() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (stream) cudaStreamDestroy(stream);
+    if (aux) cudaStreamDestroy(aux);
     if (prev >= 0) cudaSetDevice(prev);
 }
 
@@ -251,17 +253,6 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
         if (n_offsets != n + 1 || n_degrees != n || (inv_degree && n_inv != n) ||
             nnz != offsets[n])
             fail(CHEB_VALIDATION, "inconsistent graph arrays");
-        for (int64_t v = 0; v < n; ++v)
-            if (degrees[v] < 1)
-                fail(CHEB_VALIDATION, "vertex " + std::to_string(v) + " is isolated (degree 0)");
-        if (offsets[0] != 0) fail(CHEB_VALIDATION, "offsets must start at 0");
-        int64_t dmin = INT64_MAX, dmax = 0;
-        for (int64_t v = 0; v < n; ++v) {  // one pass: monotone offsets + degree extrema
-            const int64_t d = offsets[v + 1] - offsets[v];
-            if (d < 0) fail(CHEB_VALIDATION, "offsets not monotone at vertex " + std::to_string(v));
-            dmin = d < dmin ? d : dmin;
-            dmax = d > dmax ? d : dmax;
-        }
         std::unique_ptr<cheb_graph> g(new_graph(device));
         GraphScope gs(g.get());
         g->m = m;
@@ -269,9 +260,23 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
         g->rp64 = row_ptr_64 != 0;
         g->duplicates_removed = 0;
         g->isolated_dropped = 0;
-        g->min_degree = dmin;
-        g->max_degree = dmax;
-        upload_csr(g.get(), offsets, neighbors, n, nnz, inv_degree);
+        // the remaining checks are O(n) host loops: they run while the CSR copies are in flight
+        auto host_checks = [&] {
+            for (int64_t v = 0; v < n; ++v)
+                if (degrees[v] < 1)
+                    fail(CHEB_VALIDATION, "vertex " + std::to_string(v) + " is isolated (degree 0)");
+            if (offsets[0] != 0) fail(CHEB_VALIDATION, "offsets must start at 0");
+            int64_t dmin = INT64_MAX, dmax = 0;
+            for (int64_t v = 0; v < n; ++v) {  // one pass: monotone offsets + degree extrema
+                const int64_t d = offsets[v + 1] - offsets[v];
+                if (d < 0) fail(CHEB_VALIDATION, "offsets not monotone at vertex " + std::to_string(v));
+                dmin = d < dmin ? d : dmin;
+                dmax = d > dmax ? d : dmax;
+            }
+            g->min_degree = dmin;
+            g->max_degree = dmax;
+        };
+        upload_csr(g.get(), offsets, neighbors, n, nnz, inv_degree, host_checks);
         *out = g.release();
     });
 }

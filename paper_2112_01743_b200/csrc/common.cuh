@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -102,6 +103,11 @@ public:
         p_ = nullptr;
         n_ = 0;
     }
+    // Return the block to the pool on `s` from now on (a buffer built on an auxiliary
+    // stream and joined into the owner's stream).
+    void set_stream(cudaStream_t s) {
+        if (async_) st_ = s;
+    }
     template <class T>
     T* ptr() const { return static_cast<T*>(p_); }
     void* get() const { return p_; }
@@ -179,6 +185,9 @@ struct SolverView {
     int64_t n_hub = 0;     // rows [0, n_hub) with degree > kWarpNnz (chunk tiles)
     int n_chunk_tiles = 0;
     DevMem hub_first;      // int32 [n_hub + 1]: first chunk tile of each hub row
+    void set_stream(cudaStream_t s) {
+        for (DevMem* d : {&order, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first}) d->set_stream(s);
+    }
 };
 
 // 1-D row partition of the degree-sorted view over G GPUs (one process per GPU).
@@ -232,6 +241,7 @@ struct StagedState {
 struct cheb_graph {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux = nullptr;    // solver-view build overlapped with the CSR upload
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int64_t n = 0, m = 0, nnz = 0;
     int64_t duplicates_removed = 0, isolated_dropped = 0;
@@ -281,8 +291,11 @@ inline Tuning& tuning() {
 // build.cu
 void build_from_edges(cheb_graph* g, const void* d_edges, int64_t E, int edge_bits,
                       const cheb_build_opts& o);
+// Upload of a host CSR: the H2D copies are enqueued first, `host_checks` (the reference's
+// host-side validation) runs while they are in flight, and the solver view is built on an
+// auxiliary stream as soon as the offsets have landed, overlapping the neighbour copy.
 void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors, int64_t n,
-                int64_t nnz, const double* inv_degree);
+                int64_t nnz, const double* inv_degree, const std::function<void()>& host_checks);
 void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees);
 void ensure_view(cheb_graph* g);
 void finalize_stats(cheb_graph* g);
