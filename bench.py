@@ -400,6 +400,19 @@ class Solver:
                         ("cheb_cpaa_batch" if R > 1 else "cheb_cpaa") + "(host ranks) + cheb_graph_free"}
 
 
+def measured_traffic(config, precision, world):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    (profiles/traffic.json), or None when this workload has not been captured."""
+    if world != 1:
+        return None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"{config}/f{precision}", {}).get("bytes")
+    except (OSError, ValueError):
+        return None
+
+
 def cpu_baseline_line(solver, cfg, args):
     """The reference compiled unmodified (oracle/_ref) on the same CSR, all host threads; for
     the batched config the reference has no personalisation, so one column of the restated
@@ -542,7 +555,9 @@ def main():
                        "l2": "flushed (512 MiB write) before every timed step",
                        "graph_build_s": round(build_s, 3)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": measured_traffic(args.config, args.precision, dist.world),
+                         "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
                          "kernel": kernel, "bytes_per_launch": B,
                          "bytes_formula": "4 nnz + I_r (n+1) + 6 V R n (SURVEY.md 8d)",
                          "mean_launch_us": round(mean_term * 1e3, 3), "peak_kind": peak_kind},

@@ -20,6 +20,11 @@ KEYS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "achieved_occupancy_pct"),
     ("smsp__thread_inst_executed_per_inst_executed.ratio", "avg_active_threads_per_warp_inst"),
     ("sm__inst_executed.avg.per_cycle_active", "ipc"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1_wavefronts_shared"),
+    ("memory_l1_wavefronts_shared_ideal", "l1_wavefronts_shared_ideal"),
+    ("l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum", "l1_wavefronts_global_ld"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "l1_requests_global_ld"),
+    ("smsp__inst_executed.sum", "warp_instructions"),
     ("launch__registers_per_thread", "registers"),
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
