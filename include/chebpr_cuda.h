@@ -108,6 +108,42 @@ cheb_status cheb_graph_download_csr(cheb_graph_t g, int64_t* offsets, int64_t* n
 cheb_status cheb_graph_get_info(cheb_graph_t g, cheb_graph_info* info);
 void cheb_graph_free(cheb_graph_t g);
 
+/* ---- graph ingest (graph_io.hpp / graph_io.cpp:50-174), parsed on the device ---- */
+typedef struct {
+    int dedup;          /* LoadOptions::dedup (graph_io.hpp:25), default 1 */
+    int drop_isolated;  /* LoadOptions::drop_isolated (graph_io.hpp:26), default 0 */
+    int symmetrize;     /* LoadOptions::symmetrize (graph_io.hpp:27), default 0 */
+    int device;         /* CUDA ordinal (new) */
+    int row_ptr_64;     /* as cheb_build_opts (new) */
+} cheb_load_opts;
+
+typedef struct {        /* GraphStats (graph.hpp:33-42) + ingest facts */
+    int64_t n, m;
+    double avg_degree;  /* m / n */
+    int64_t min_degree, max_degree, self_loops, duplicates_removed, isolated_dropped;
+    int64_t lines;      /* text lines consumed */
+    int weights_ignored; /* Matrix Market real field: the reference warns once (graph_io.cpp:134-138) */
+} cheb_graph_stats;
+
+void cheb_load_opts_default(cheb_load_opts* o);
+/* load_edge_list (graph_io.cpp:50-70) / load_matrix_market (72-174): the file is streamed
+ * to the device through a pinned ring, split into lines and parsed by GPU threads, then
+ * built by K1 (build_graph + the validate stats of finish(), graph_io.cpp:31-46).  Errors:
+ * CHEB_PARSE / CHEB_VALIDATION with the reference's message text naming the first failing
+ * line.  The caller prints the reference's warnings (isolated_dropped > 0,
+ * weights_ignored). */
+cheb_status cheb_graph_load_edge_list(const char* path, const cheb_load_opts* opts, cheb_graph_t* out,
+                                      cheb_graph_stats* stats);
+cheb_status cheb_graph_load_matrix_market(const char* path, const cheb_load_opts* opts, cheb_graph_t* out,
+                                          cheb_graph_stats* stats);
+/* Same from an in-memory text (format 0 = edge list, 1 = Matrix Market); `name` stands in
+ * for the path in messages. */
+cheb_status cheb_graph_parse_text(const char* text, int64_t bytes, int format, const char* name,
+                                  const cheb_load_opts* opts, cheb_graph_t* out, cheb_graph_stats* stats);
+/* validate (graph.cpp:123-186) statistics of a device graph built by K1 (whose invariants
+ * hold by construction): n, m, avg/min/max degree, self loops, builder counts. */
+cheb_status cheb_graph_validate_stats(cheb_graph_t g, cheb_graph_stats* stats);
+
 /* cpaa.cpp:40-68 partition_vertices: degree-prefix cuts (host rule, used for the
  * multi-GPU row partition).  cuts has K+1 entries. */
 cheb_status cheb_partition_vertices(const int64_t* degrees, int64_t n, int K, int64_t* cuts);

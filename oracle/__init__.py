@@ -214,6 +214,8 @@ class Reference:
         L.ref_plan_iterations.argtypes = [C.c_double, C.c_double, C.POINTER(C.c_int), F64P]
         L.ref_err_bound.argtypes = [C.c_double, C.c_int, F64P]
         L.ref_partition_vertices.argtypes = [C.c_void_p, C.c_int, I64P]
+        L.ref_load.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p), I64P,
+                               C.POINTER(C.c_double)]
         L.ref_kahan_sum.restype = C.c_double
         L.ref_kahan_sum.argtypes = [F64P, C.c_int64]
 
@@ -254,6 +256,20 @@ class Reference:
                                            _p(g.degrees, I64P), g.degrees.size, _p(g.inv_degree),
                                            g.inv_degree.size, int(g.multi))
         return RefGraph(self, C.c_void_p(h), g.n, g.m, g.neighbors.size, 0, 0, multi=g.multi)
+
+    def load(self, path, fmt="edges", dedup=True, drop_isolated=False, symmetrize=False):
+        """The reference's own load_edge_list / load_matrix_market (graph_io.cpp:50-174).
+        Returns (RefGraph, stats dict); raises OracleError(code, message) like the C++."""
+        h = C.c_void_p()
+        st = np.zeros(8, dtype=np.int64)
+        avg = C.c_double()
+        self._check(self.lib.ref_load(os.fsencode(path), 0 if fmt == "edges" else 1, int(dedup),
+                                      int(drop_isolated), int(symmetrize), C.byref(h), _p(st, I64P),
+                                      C.byref(avg)))
+        stats = dict(n=int(st[0]), m=int(st[1]), min_degree=int(st[2]), max_degree=int(st[3]),
+                     self_loops=int(st[4]), duplicates_removed=int(st[5]), isolated_dropped=int(st[6]),
+                     avg_degree=avg.value)
+        return RefGraph(self, h, int(st[0]), int(st[1]), int(st[7]), int(st[5]), int(st[6]), multi=not dedup), stats
 
     def coefficients(self, c, M):
         out = np.zeros(M + 1)

@@ -18,6 +18,7 @@
 #include "chebpr/errors.hpp"
 #include "chebpr/generate.hpp"
 #include "chebpr/graph.hpp"
+#include "chebpr/graph_io.hpp"
 #include "chebpr/metrics.hpp"
 #include "chebpr/power.hpp"
 
@@ -145,6 +146,29 @@ void* ref_graph_from_arrays(int64_t n, int64_t m, const int64_t* offsets, int64_
     g->inv_degree.assign(inv_degree, inv_degree + n_inv);
     g->multi = multi != 0;
     return g;
+}
+
+// load_edge_list / load_matrix_market (graph_io.cpp:50-174) through the reference itself.
+// stats: n, m, min_degree, max_degree, self_loops, duplicates_removed, isolated_dropped, nnz.
+int ref_load(const char* path, int format, int dedup, int drop_isolated, int symmetrize, void** handle,
+             int64_t* stats, double* avg_degree) {
+    return guard([&] {
+        LoadOptions o;
+        o.dedup = dedup != 0;
+        o.drop_isolated = drop_isolated != 0;
+        o.symmetrize = symmetrize != 0;
+        LoadedGraph lg = format == 0 ? load_edge_list(path, o) : load_matrix_market(path, o);
+        stats[0] = lg.stats.n;
+        stats[1] = lg.stats.m;
+        stats[2] = lg.stats.min_degree;
+        stats[3] = lg.stats.max_degree;
+        stats[4] = lg.stats.self_loops;
+        stats[5] = lg.stats.duplicates_removed;
+        stats[6] = lg.stats.isolated_dropped;
+        stats[7] = static_cast<int64_t>(lg.graph.neighbors.size());
+        *avg_degree = lg.stats.avg_degree;
+        *handle = new UndirectedGraph(std::move(lg.graph));
+    });
 }
 
 void ref_graph_free(void* h) { delete static_cast<UndirectedGraph*>(h); }

@@ -11,7 +11,8 @@ from .api import (  # noqa: F401
     UndirectedGraph, ValidationError, VertexRange, accumulate_stage, beta, build_device_graph,
     build_graph, coefficients, run_cpaa_batch, BatchResult, device_count, err_bound, generate_stage, init_state, kahan_sum,
     normalize, partition_vertices, plan_iterations, reference_pagerank, run_cpaa, run_power,
-    sigma, transition_apply, upload, validate,
+    sigma, transition_apply, upload, validate, LoadOptions, LoadedGraph, load_edge_list,
+    load_matrix_market, load_device_graph, parse_text,
 )
 
 __version__ = "0.1.0"

@@ -43,6 +43,18 @@ class cheb_trace_row(C.Structure):
                 ("err_l1", C.c_double)]
 
 
+class cheb_load_opts(C.Structure):
+    _fields_ = [("dedup", C.c_int), ("drop_isolated", C.c_int), ("symmetrize", C.c_int),
+                ("device", C.c_int), ("row_ptr_64", C.c_int)]
+
+
+class cheb_graph_stats(C.Structure):
+    _fields_ = [("n", C.c_int64), ("m", C.c_int64), ("avg_degree", C.c_double),
+                ("min_degree", C.c_int64), ("max_degree", C.c_int64), ("self_loops", C.c_int64),
+                ("duplicates_removed", C.c_int64), ("isolated_dropped", C.c_int64),
+                ("lines", C.c_int64), ("weights_ignored", C.c_int)]
+
+
 class cheb_power_opts(C.Structure):
     _fields_ = [("c", C.c_double), ("rounds", C.c_int), ("tol", C.c_double),
                 ("max_rounds", C.c_int), ("parallelism", C.c_int), ("mode", C.c_int)]
@@ -70,6 +82,14 @@ _SIGS = {
                                         F64P, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
                                         C.c_int, C.POINTER(C.c_void_p)]),
     "cheb_graph_download_csr": (C.c_int, [C.c_void_p, I64P, I64P, I64P]),
+    "cheb_load_opts_default": (None, [C.POINTER(cheb_load_opts)]),
+    "cheb_graph_load_edge_list": (C.c_int, [C.c_char_p, C.POINTER(cheb_load_opts), C.POINTER(C.c_void_p),
+                                            C.POINTER(cheb_graph_stats)]),
+    "cheb_graph_load_matrix_market": (C.c_int, [C.c_char_p, C.POINTER(cheb_load_opts), C.POINTER(C.c_void_p),
+                                                C.POINTER(cheb_graph_stats)]),
+    "cheb_graph_parse_text": (C.c_int, [C.c_char_p, C.c_int64, C.c_int, C.c_char_p, C.POINTER(cheb_load_opts),
+                                        C.POINTER(C.c_void_p), C.POINTER(cheb_graph_stats)]),
+    "cheb_graph_validate_stats": (C.c_int, [C.c_void_p, C.POINTER(cheb_graph_stats)]),
     "cheb_graph_get_info": (C.c_int, [C.c_void_p, C.POINTER(cheb_graph_info)]),
     "cheb_graph_free": (None, [C.c_void_p]),
     "cheb_partition_vertices": (C.c_int, [I64P, C.c_int64, C.c_int, I64P]),

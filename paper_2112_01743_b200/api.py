@@ -9,6 +9,8 @@ the only path.  Additive options (``mode``, ``precision``, ``device``,
 from __future__ import annotations
 
 import ctypes as C
+import os
+import sys
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -258,6 +260,85 @@ def build_device_graph(edges, opts: Optional[BuildOptions] = None):
     inf = L.cheb_graph_info()
     _check(_lib().cheb_graph_build(_pi(e), e.shape[0], C.byref(o), C.byref(h), C.byref(inf)))
     return DeviceGraph(h, inf.n), {k: getattr(inf, k) for k, _ in L.cheb_graph_info._fields_}
+
+
+@dataclass
+class LoadOptions:
+    """graph_io.hpp:24-28 (+ device placement)."""
+    dedup: bool = True
+    drop_isolated: bool = False
+    symmetrize: bool = False
+    device: int = 0          # new
+    row_ptr_64: bool = False  # new
+
+
+@dataclass
+class LoadedGraph:
+    """graph_io.hpp:30-33: the host CSR and its validated stats."""
+    graph: UndirectedGraph
+    stats: GraphStats
+    device_graph: Optional["DeviceGraph"] = None  # new: the resident device CSR
+    lines: int = 0                                # new: text lines consumed
+
+
+def _load_opts(opts: Optional[LoadOptions]) -> "L.cheb_load_opts":
+    opts = opts or LoadOptions()
+    return L.cheb_load_opts(int(opts.dedup), int(opts.drop_isolated), int(opts.symmetrize),
+                            int(opts.device), int(opts.row_ptr_64))
+
+
+def _finish_load(rc: int, h: C.c_void_p, st, path: str, keep_device: bool) -> LoadedGraph:
+    _check(rc)
+    if st.weights_ignored:  # graph_io.cpp:134-138
+        print(f"warning: {path}: real weights ignored, using pattern only", file=sys.stderr)
+    if st.isolated_dropped > 0:  # graph_io.cpp:38-40
+        print(f"warning: dropped {st.isolated_dropped} isolated vertices", file=sys.stderr)
+    dg = DeviceGraph(h, st.n)
+    stats = GraphStats(st.n, st.m, st.avg_degree, st.min_degree, st.max_degree, st.self_loops,
+                       st.duplicates_removed, st.isolated_dropped)
+    res = LoadedGraph(dg.download(), stats, None, st.lines)
+    if keep_device:
+        res.device_graph = dg
+    else:
+        dg.free()
+    return res
+
+
+def load_edge_list(path: str, opts: Optional[LoadOptions] = None, keep_device: bool = False) -> LoadedGraph:
+    """graph_io.hpp:35 — the file is parsed on the GPU (line split + from_chars-exact ints)
+    and built by K1; errors name the first failing line like graph_io.cpp:62-64."""
+    h, st = C.c_void_p(), L.cheb_graph_stats()
+    o = _load_opts(opts)
+    rc = _lib().cheb_graph_load_edge_list(os.fsencode(path), C.byref(o), C.byref(h), C.byref(st))
+    return _finish_load(rc, h, st, path, keep_device)
+
+
+def load_matrix_market(path: str, opts: Optional[LoadOptions] = None, keep_device: bool = False) -> LoadedGraph:
+    """graph_io.hpp:36 — header on the host, entries parsed and mirror-checked on the GPU."""
+    h, st = C.c_void_p(), L.cheb_graph_stats()
+    o = _load_opts(opts)
+    rc = _lib().cheb_graph_load_matrix_market(os.fsencode(path), C.byref(o), C.byref(h), C.byref(st))
+    return _finish_load(rc, h, st, path, keep_device)
+
+
+def load_device_graph(path: str, fmt: str = "edges", opts: Optional[LoadOptions] = None):
+    """Load straight to a resident device handle (no host CSR): (DeviceGraph, GraphStats)."""
+    h, st = C.c_void_p(), L.cheb_graph_stats()
+    o = _load_opts(opts)
+    fn = _lib().cheb_graph_load_edge_list if fmt == "edges" else _lib().cheb_graph_load_matrix_market
+    _check(fn(os.fsencode(path), C.byref(o), C.byref(h), C.byref(st)))
+    return DeviceGraph(h, st.n), GraphStats(st.n, st.m, st.avg_degree, st.min_degree, st.max_degree,
+                                            st.self_loops, st.duplicates_removed, st.isolated_dropped)
+
+
+def parse_text(text: bytes, fmt: str = "edges", name: str = "<memory>",
+               opts: Optional[LoadOptions] = None, keep_device: bool = False) -> LoadedGraph:
+    """In-memory variant of the loaders (`name` stands in for the path in messages)."""
+    h, st = C.c_void_p(), L.cheb_graph_stats()
+    o = _load_opts(opts)
+    rc = _lib().cheb_graph_parse_text(text, len(text), 0 if fmt == "edges" else 1, name.encode(),
+                                      C.byref(o), C.byref(h), C.byref(st))
+    return _finish_load(rc, h, st, name, keep_device)
 
 
 def upload(g: UndirectedGraph, device: int = 0, row_ptr_64: bool = False) -> DeviceGraph:

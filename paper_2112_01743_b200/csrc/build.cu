@@ -277,6 +277,9 @@ void build_from_edges(cheb_graph* g, const void* d_edges, int64_t E, int edge_bi
         CHEB_CUDA_CHECK(cudaMemcpyAsync(h, mm.get(), sizeof h, cudaMemcpyDeviceToHost, st));
         CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
         if (h[0] < 0) fail(CHEB_VALIDATION, "negative vertex id in edge list");
+        if (h[1] >= INT32_MAX - 1)  // before max id + 1 can overflow (graph.cpp:25-29)
+            fail(CHEB_CAPACITY, "device CSR builder supports n < 2^31 (int32 column ids), got max id " +
+                                    std::to_string(h[1]));
         n = std::max<int64_t>(n, h[1] + 1);
     }
     if (n > INT32_MAX - 1)

@@ -281,6 +281,76 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
     });
 }
 
+void cheb_load_opts_default(cheb_load_opts* o) {
+    o->dedup = 1;
+    o->drop_isolated = 0;
+    o->symmetrize = 0;
+    o->device = 0;
+    o->row_ptr_64 = 0;
+}
+
+namespace {
+void stats_of(cheb_graph* g, cheb_graph_stats* s) {  // graph.cpp:123-186 validate's numbers
+    s->n = g->n;
+    s->m = g->m;
+    s->avg_degree = g->n > 0 ? static_cast<double>(g->m) / static_cast<double>(g->n) : 0.0;
+    s->min_degree = g->n > 0 ? g->min_degree : 0;
+    s->max_degree = g->n > 0 ? g->max_degree : 0;
+    s->self_loops = count_self_loops(g);
+    s->duplicates_removed = g->duplicates_removed;
+    s->isolated_dropped = g->isolated_dropped;
+}
+
+cheb_status load_common(const char* path, const char* text, int64_t bytes, int format,
+                        const cheb_load_opts* opts, cheb_graph_t* out, cheb_graph_stats* stats) {
+    return guarded([&] {
+        if (!path) fail(CHEB_INVALID_ARG, "null path");
+        cheb_load_opts o;
+        cheb_load_opts_default(&o);
+        if (opts) o = *opts;
+        std::unique_ptr<cheb_graph> g(new_graph(o.device));
+        GraphScope gs(g.get());
+        int64_t lines = 0;
+        int wi = 0;
+        load_graph_text(g.get(), path, text, bytes, format, o, &lines, &wi);
+        if (stats) {
+            stats_of(g.get(), stats);
+            stats->lines = lines;
+            stats->weights_ignored = wi;
+        }
+        *out = g.release();
+    });
+}
+}  // namespace
+
+cheb_status cheb_graph_load_edge_list(const char* path, const cheb_load_opts* opts, cheb_graph_t* out,
+                                      cheb_graph_stats* stats) {
+    return load_common(path, nullptr, 0, 0, opts, out, stats);
+}
+
+cheb_status cheb_graph_load_matrix_market(const char* path, const cheb_load_opts* opts, cheb_graph_t* out,
+                                          cheb_graph_stats* stats) {
+    return load_common(path, nullptr, 0, 1, opts, out, stats);
+}
+
+cheb_status cheb_graph_parse_text(const char* text, int64_t bytes, int format, const char* name,
+                                  const cheb_load_opts* opts, cheb_graph_t* out, cheb_graph_stats* stats) {
+    if (!text && bytes > 0) return guarded([] { fail(CHEB_INVALID_ARG, "null text"); });
+    static const char empty = 0;
+    return load_common(name ? name : "<memory>", text ? text : &empty, bytes, format, opts, out, stats);
+}
+
+cheb_status cheb_graph_validate_stats(cheb_graph_t g, cheb_graph_stats* stats) {
+    return guarded([&] {
+        need_graph(g);
+        GraphScope gs(g);
+        if (!stats) fail(CHEB_INVALID_ARG, "null stats");
+        stats_of(g, stats);
+        stats->lines = 0;
+        stats->weights_ignored = 0;
+    });
+}
+
 cheb_status cheb_graph_download_csr(cheb_graph_t g, int64_t* offsets, int64_t* neighbors,
                                     int64_t* degrees) {
     return guarded([&] {

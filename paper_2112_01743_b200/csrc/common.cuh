@@ -299,6 +299,10 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
 void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees);
 void ensure_view(cheb_graph* g);
 void finalize_stats(cheb_graph* g);
+// ingest.cu
+void load_graph_text(cheb_graph* g, const std::string& path, const char* mem, int64_t mem_bytes, int format,
+                     const cheb_load_opts& o, int64_t* lines, int* weights_ignored);
+int64_t count_self_loops(cheb_graph* g);
 
 // host: partition_vertices rule (cpaa.cpp:40-68) over a degree sequence
 void partition_cuts(const int64_t* degrees, int64_t n, int K, int64_t* cuts);

@@ -178,6 +178,32 @@ CoefficientTable coefficients_quadrature(double c, int M, double tol) {
 }
 
 // ---------------------------------------------------------------- graph.hpp
+namespace {
+// Host copy of a device graph (graph.hpp:21-31 arrays); frees the handle.
+UndirectedGraph host_graph(cheb_graph_t h) {
+    cheb_graph_info info;
+    cheb_status s = cheb_graph_get_info(h, &info);
+    if (s != CHEB_OK) {
+        cheb_graph_free(h);
+        check(s);
+    }
+    UndirectedGraph g;
+    g.n = info.n;
+    g.m = info.m;
+    g.multi = info.multi != 0;
+    g.offsets.resize(static_cast<size_t>(info.n) + 1);
+    g.neighbors.resize(static_cast<size_t>(info.nnz));
+    g.degrees.resize(static_cast<size_t>(info.n));
+    s = cheb_graph_download_csr(h, g.offsets.data(), g.neighbors.data(), g.degrees.data());
+    cheb_graph_free(h);
+    check(s);
+    if (info.n == 0) g.offsets.assign(1, 0);
+    g.inv_degree.resize(static_cast<size_t>(info.n));
+    for (size_t v = 0; v < g.degrees.size(); ++v) g.inv_degree[v] = 1.0 / static_cast<double>(g.degrees[v]);
+    return g;
+}
+}  // namespace
+
 BuildResult build_graph(const std::vector<std::pair<int64_t, int64_t>>& edges, const BuildOptions& opts) {
     std::vector<int64_t> flat(2 * edges.size() + 2);
     for (size_t i = 0; i < edges.size(); ++i) {
@@ -194,19 +220,7 @@ BuildResult build_graph(const std::vector<std::pair<int64_t, int64_t>>& edges, c
     cheb_graph_info info;
     check(cheb_graph_build(flat.data(), (int64_t)edges.size(), &o, &h, &info));
     BuildResult r;
-    UndirectedGraph& g = r.graph;
-    g.n = info.n;
-    g.m = info.m;
-    g.multi = info.multi != 0;
-    g.offsets.resize(static_cast<size_t>(info.n) + 1);
-    g.neighbors.resize(static_cast<size_t>(info.nnz));
-    g.degrees.resize(static_cast<size_t>(info.n));
-    const cheb_status s = cheb_graph_download_csr(h, g.offsets.data(), g.neighbors.data(), g.degrees.data());
-    cheb_graph_free(h);
-    check(s);
-    if (info.n == 0) g.offsets.assign(1, 0);
-    g.inv_degree.resize(static_cast<size_t>(info.n));
-    for (size_t v = 0; v < g.degrees.size(); ++v) g.inv_degree[v] = 1.0 / static_cast<double>(g.degrees[v]);
+    r.graph = host_graph(h);
     r.duplicates_removed = info.duplicates_removed;
     r.isolated_dropped = info.isolated_dropped;
     return r;
@@ -573,131 +587,43 @@ void write_edge_list(const std::string& path, const EdgeList& edges, const std::
 }
 
 // ---------------------------------------------------------------- graph_io.hpp
+// The files are parsed on the GPU (csrc/ingest.cu, cheb_graph_load_*) and built by K1;
+// finish()'s warnings (graph_io.cpp:38-40, 134-138) are printed here.
 namespace {
-const char* skip_blanks(const char* p, const char* e) {
-    while (p < e && (*p == ' ' || *p == '\t' || *p == '\r')) ++p;
-    return p;
-}
-bool read_int(const char*& p, const char* e, int64_t& v) {
-    p = skip_blanks(p, e);
-    const auto r = std::from_chars(p, e, v);
-    if (r.ec != std::errc{} || r.ptr == p) return false;
-    p = r.ptr;
-    return true;
-}
-bool only_blanks(const char* p, const char* e) { return skip_blanks(p, e) == e; }
-
-LoadedGraph finish_load(const EdgeList& edges, const LoadOptions& opts, int64_t n_hint) {
-    BuildOptions b;
-    b.dedup = opts.dedup;
-    b.drop_isolated = opts.drop_isolated;
-    b.n_hint = n_hint;
-    BuildResult r = build_graph(edges, b);
-    if (r.isolated_dropped > 0)
-        std::fprintf(stderr, "warning: dropped %lld isolated vertices\n", (long long)r.isolated_dropped);
+LoadedGraph load_on_device(const std::string& path, const LoadOptions& opts, bool matrix_market) {
+    cheb_load_opts o;
+    cheb_load_opts_default(&o);
+    o.dedup = opts.dedup ? 1 : 0;
+    o.drop_isolated = opts.drop_isolated ? 1 : 0;
+    o.symmetrize = opts.symmetrize ? 1 : 0;
+    cheb_graph_t h = nullptr;
+    cheb_graph_stats st;
+    check(matrix_market ? cheb_graph_load_matrix_market(path.c_str(), &o, &h, &st)
+                        : cheb_graph_load_edge_list(path.c_str(), &o, &h, &st));
+    if (st.weights_ignored)
+        std::fprintf(stderr, "warning: %s: real weights ignored, using pattern only\n", path.c_str());
+    if (st.isolated_dropped > 0)
+        std::fprintf(stderr, "warning: dropped %lld isolated vertices\n", (long long)st.isolated_dropped);
     LoadedGraph lg;
-    lg.stats = validate(r.graph, r.duplicates_removed, r.isolated_dropped);
-    lg.graph = std::move(r.graph);
+    lg.graph = host_graph(h);
+    lg.stats.n = st.n;
+    lg.stats.m = st.m;
+    lg.stats.avg_degree = st.avg_degree;
+    lg.stats.min_degree = st.min_degree;
+    lg.stats.max_degree = st.max_degree;
+    lg.stats.self_loops = st.self_loops;
+    lg.stats.duplicates_removed = st.duplicates_removed;
+    lg.stats.isolated_dropped = st.isolated_dropped;
     return lg;
 }
 }  // namespace
 
 LoadedGraph load_edge_list(const std::string& path, const LoadOptions& opts) {
-    std::ifstream in(path);
-    if (!in) throw ParseError("cannot open " + path);
-    EdgeList edges;
-    std::string line;
-    for (int64_t ln = 1; std::getline(in, line); ++ln) {
-        const char* p = skip_blanks(line.data(), line.data() + line.size());
-        const char* e = line.data() + line.size();
-        if (p == e || *p == '#') continue;
-        int64_t a, b;
-        if (!read_int(p, e, a) || !read_int(p, e, b) || !only_blanks(p, e) || a < 0 || b < 0)
-            throw ParseError(path + ":" + std::to_string(ln) + ": expected two non-negative vertex ids");
-        edges.emplace_back(a, b);
-    }
-    return finish_load(edges, opts, 0);
+    return load_on_device(path, opts, false);
 }
 
 LoadedGraph load_matrix_market(const std::string& path, const LoadOptions& opts) {
-    std::ifstream in(path);
-    if (!in) throw ParseError("cannot open " + path);
-    std::string line;
-    if (!std::getline(in, line)) throw ParseError(path + ": empty file");
-    std::istringstream hdr(line);
-    std::string banner, object, format, field, symmetry;
-    hdr >> banner >> object >> format >> field >> symmetry;
-    auto lower = [](std::string s) {
-        for (auto& ch : s) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
-        return s;
-    };
-    object = lower(object);
-    format = lower(format);
-    field = lower(field);
-    symmetry = lower(symmetry);
-    if (banner != "%%MatrixMarket" || object != "matrix") throw ParseError(path + ": not a Matrix Market matrix file");
-    if (format != "coordinate") throw ParseError(path + ": unsupported format '" + format + "' (coordinate only)");
-    if (field != "pattern" && field != "real")
-        throw ParseError(path + ": unsupported field '" + field + "' (pattern or real only)");
-    if (symmetry != "symmetric" && symmetry != "general")
-        throw ParseError(path + ": unsupported symmetry '" + symmetry + "' (symmetric or general only)");
-    const bool weighted = field == "real", sym = symmetry == "symmetric";
-    int64_t ln = 1, rows = 0, cols = 0, cnt = 0;
-    for (;;) {
-        if (!std::getline(in, line)) throw ParseError(path + ": missing size line");
-        ++ln;
-        const char* p = skip_blanks(line.data(), line.data() + line.size());
-        const char* e = line.data() + line.size();
-        if (p == e || *p == '%') continue;
-        if (!read_int(p, e, rows) || !read_int(p, e, cols) || !read_int(p, e, cnt) || !only_blanks(p, e))
-            throw ParseError(path + ":" + std::to_string(ln) + ": malformed size line");
-        break;
-    }
-    if (rows != cols)
-        throw ValidationError(path + ": adjacency matrix must be square, got " + std::to_string(rows) + "x" +
-                              std::to_string(cols));
-    EdgeList ent;
-    bool warned = false;
-    for (int64_t k = 0; k < cnt; ++k) {
-        if (!std::getline(in, line))
-            throw ParseError(path + ": expected " + std::to_string(cnt) + " entries, got " + std::to_string(k));
-        ++ln;
-        const char* p = line.data();
-        const char* e = line.data() + line.size();
-        int64_t i, j;
-        const std::string where = path + ":" + std::to_string(ln);
-        if (!read_int(p, e, i) || !read_int(p, e, j)) throw ParseError(where + ": malformed entry");
-        if (weighted) {
-            p = skip_blanks(p, e);
-            if (p == e) throw ParseError(where + ": missing weight");
-            double w;
-            const auto r = std::from_chars(p, e, w);
-            if (r.ec != std::errc{}) throw ParseError(where + ": malformed weight");
-            p = r.ptr;
-            if (!warned) {
-                std::fprintf(stderr, "warning: %s: real weights ignored, using pattern only\n", path.c_str());
-                warned = true;
-            }
-        }
-        if (!only_blanks(p, e)) throw ParseError(where + ": trailing characters");
-        if (i < 1 || i > rows || j < 1 || j > cols) throw ParseError(where + ": index out of range");
-        ent.emplace_back(i - 1, j - 1);
-    }
-    EdgeList edges;
-    if (sym || opts.symmetrize) {
-        edges = std::move(ent);
-    } else {
-        EdgeList sorted = ent;
-        std::sort(sorted.begin(), sorted.end());
-        for (const auto& [i, j] : ent)
-            if (i != j && !std::binary_search(sorted.begin(), sorted.end(), std::make_pair(j, i)))
-                throw ValidationError(path + ": general matrix is not symmetric: entry (" + std::to_string(i + 1) +
-                                      "," + std::to_string(j + 1) + ") has no (" + std::to_string(j + 1) + "," +
-                                      std::to_string(i + 1) + ") counterpart (use symmetrize to force)");
-        for (const auto& [i, j] : ent)
-            if (i >= j) edges.emplace_back(i, j);
-    }
-    return finish_load(edges, opts, rows);
+    return load_on_device(path, opts, true);
 }
 
 }  // namespace chebpr

@@ -1,0 +1,706 @@
+// Graph ingest on the device: edge-list and Matrix Market text parsed by the GPU and fed
+// straight into the K1 builder.
+//
+// Replaces the reference loaders /root/reference/proj/src/graph_io.cpp:50-174 with the same
+// line semantics:
+//   * lines are split at '\n' exactly as std::getline does (a final line without '\n'
+//     counts, a trailing '\n' does not open an empty line), numbered from 1;
+//   * blanks are ' ', '\t', '\r' (graph_io.cpp:18-21); integers follow std::from_chars for
+//     int64 (optional '-', decimal digits, out-of-range = failure; graph_io.cpp:23-29);
+//   * edge list: blank and '#' lines skipped, anything else must be two non-negative ids
+//     and nothing but blanks (graph_io.cpp:56-66);
+//   * Matrix Market: banner / size line parsed on the host (graph_io.cpp:75-111), then
+//     exactly `nnz` entry lines on the device with the reference's per-line check order
+//     (malformed entry, missing weight, malformed weight, trailing characters, index out of
+//     range; graph_io.cpp:116-144), the general-matrix mirror check (153-165) as a device
+//     sort + binary search, and one orientation kept (166-168);
+//   * errors name the FIRST failing line (a device atomicMin over line numbers), with the
+//     reference's message text.
+// Real weights are only syntax-checked (their values are ignored by the reference).  The
+// device decides every weight whose value is certainly finite and normal-range; tokens that
+// could overflow/underflow or spell inf/nan are re-checked on the host with std::from_chars
+// itself, so the verdict is the reference's exactly.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include <algorithm>
+#include <cctype>
+#include <charconv>
+#include <cstring>
+#include <fstream>
+#include <mutex>
+#include <sstream>
+
+#include "common.cuh"
+
+namespace chebgpu {
+namespace {
+
+constexpr int kIngestThreads = 256;
+
+inline int blocks_for(int64_t n) {
+    int64_t b = (n + kIngestThreads - 1) / kIngestThreads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 64));
+}
+
+// ---------------------------------------------------------------------------------------
+// Host restatement of one line (used for the header and for uncertain weight lines).
+const char* skip_blanks(const char* p, const char* e) {
+    while (p < e && (*p == ' ' || *p == '\t' || *p == '\r')) ++p;
+    return p;
+}
+bool read_int(const char*& p, const char* e, int64_t& v) {
+    p = skip_blanks(p, e);
+    const auto r = std::from_chars(p, e, v);
+    if (r.ec != std::errc{} || r.ptr == p) return false;
+    p = r.ptr;
+    return true;
+}
+bool only_blanks(const char* p, const char* e) { return skip_blanks(p, e) == e; }
+
+enum EntryCode : int {
+    kOk = 0,
+    kMalformedEntry = 1,
+    kMissingWeight = 2,
+    kMalformedWeight = 3,
+    kTrailing = 4,
+    kOutOfRange = 5,
+    kEdgeBad = 6,  // edge list: "expected two non-negative vertex ids"
+};
+
+// Matrix Market entry line, graph_io.cpp:121-143 order.
+int mm_entry_host(const char* p, const char* e, bool weighted, int64_t rows, int64_t cols) {
+    int64_t i, j;
+    if (!read_int(p, e, i) || !read_int(p, e, j)) return kMalformedEntry;
+    if (weighted) {
+        p = skip_blanks(p, e);
+        if (p == e) return kMissingWeight;
+        double w;
+        const auto r = std::from_chars(p, e, w);
+        if (r.ec != std::errc{}) return kMalformedWeight;
+        p = r.ptr;
+    }
+    if (!only_blanks(p, e)) return kTrailing;
+    if (i < 1 || i > rows || j < 1 || j > cols) return kOutOfRange;
+    return kOk;
+}
+
+std::string entry_message(const std::string& where, int code) {
+    switch (code) {
+        case kMalformedEntry: return where + ": malformed entry";
+        case kMissingWeight: return where + ": missing weight";
+        case kMalformedWeight: return where + ": malformed weight";
+        case kTrailing: return where + ": trailing characters";
+        case kOutOfRange: return where + ": index out of range";
+        default: return where + ": expected two non-negative vertex ids";
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Device line parsing.
+__device__ __forceinline__ bool is_blank(unsigned char c) { return c == ' ' || c == '\t' || c == '\r'; }
+__device__ __forceinline__ bool is_digit(unsigned char c) { return c >= '0' && c <= '9'; }
+
+__device__ __forceinline__ int64_t d_skip(const unsigned char* t, int64_t p, int64_t e) {
+    while (p < e && is_blank(t[p])) ++p;
+    return p;
+}
+
+// std::from_chars(int64) after skipping blanks: optional '-', >= 1 digit, in range.
+__device__ bool d_read_int(const unsigned char* t, int64_t& p, int64_t e, long long& out) {
+    int64_t q = d_skip(t, p, e);
+    bool neg = false;
+    if (q < e && t[q] == '-') {
+        neg = true;
+        ++q;
+    }
+    const int64_t d0 = q;
+    unsigned long long v = 0;
+    bool ovf = false;
+    while (q < e && is_digit(t[q])) {
+        const unsigned dig = t[q] - '0';
+        if (v > (~0ull - dig) / 10) ovf = true;
+        else v = v * 10 + dig;
+        ++q;
+    }
+    if (q == d0) return false;
+    if (ovf || v > (neg ? 9223372036854775808ull : 9223372036854775807ull)) return false;
+    out = neg ? (long long)(0ull - v) : (long long)v;
+    p = q;
+    return true;
+}
+
+// std::from_chars(double, general) prefix at p (blanks already skipped, p < e).
+// Returns 1 = certainly valid (end of token in *q), 0 = certainly invalid (invalid_argument),
+// 2 = decided on the host (inf/nan spellings; values that could leave the normal range).
+__device__ int d_scan_double(const unsigned char* t, int64_t p, int64_t e, int64_t* q_out) {
+    int64_t q = p;
+    if (t[q] == '-') ++q;
+    if (q < e) {
+        const unsigned char c = t[q] | 0x20;
+        if (c == 'i' || c == 'n') return 2;
+    }
+    int64_t intd = 0, fracd = 0, lead0 = 0;
+    bool nonzero = false;
+    while (q < e && is_digit(t[q])) {
+        if (!nonzero && t[q] == '0') ++lead0;
+        else nonzero = true;
+        ++intd;
+        ++q;
+    }
+    if (q < e && t[q] == '.') {
+        ++q;
+        while (q < e && is_digit(t[q])) {
+            nonzero = nonzero || t[q] != '0';
+            ++fracd;
+            ++q;
+        }
+    }
+    if (intd + fracd == 0) return 0;  // no digits: "-", ".", "-.", "x"
+    long long ex = 0;
+    bool big_exp = false;
+    if (q < e && (t[q] | 0x20) == 'e') {
+        int64_t r = q + 1;
+        bool eneg = false;
+        if (r < e && (t[r] == '-' || t[r] == '+')) {
+            eneg = t[r] == '-';
+            ++r;
+        }
+        if (r < e && is_digit(t[r])) {
+            while (r < e && is_digit(t[r])) {
+                if (ex < 100000) ex = ex * 10 + (t[r] - '0');
+                else big_exp = true;
+                ++r;
+            }
+            if (eneg) ex = -ex;
+            q = r;
+        }  // else: exponent not consumed (general format rolls back to the 'e')
+    }
+    *q_out = q;
+    if (!nonzero) return big_exp || ex > 100000 || ex < -100000 ? 2 : 1;  // zero is exact
+    // magnitude is within [1e(-fracd-lead0-1+ex), 1e(intd+ex)]: certain iff well inside
+    // the normal double range.
+    const long long hi = intd + ex, lo = ex - fracd - 1;
+    if (big_exp || intd + fracd > 400 || hi > 300 || lo < -300) return 2;
+    return 1;
+}
+
+struct LineArgs {
+    const unsigned char* text;
+    const int64_t* nl;  // newline positions
+    int64_t n_nl, bytes, n_lines;
+    int64_t line0;      // line number of line 0 minus 1
+    // Matrix Market
+    int64_t rows, cols;
+    int weighted;
+};
+
+__device__ __forceinline__ void line_span(const LineArgs& a, int64_t i, int64_t& b, int64_t& e) {
+    b = i == 0 ? 0 : a.nl[i - 1] + 1;
+    e = i < a.n_nl ? a.nl[i] : a.bytes;
+}
+
+// Edge list lines (graph_io.cpp:56-66).  pairs[i] = (a,b) and keep[i] = 1 for an edge line.
+__global__ void k_parse_edge_lines(LineArgs a, long long* __restrict__ pairs, unsigned char* __restrict__ keep,
+                                   unsigned long long* __restrict__ first_err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_lines;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b, e;
+        line_span(a, i, b, e);
+        int64_t p = d_skip(a.text, b, e);
+        unsigned char k = 0;
+        if (p < e && a.text[p] != '#') {
+            long long x = 0, y = 0;
+            const bool ok = d_read_int(a.text, p, e, x) && d_read_int(a.text, p, e, y) &&
+                            d_skip(a.text, p, e) == e && x >= 0 && y >= 0;
+            if (ok) {
+                pairs[2 * i] = x;
+                pairs[2 * i + 1] = y;
+                k = 1;
+            } else {
+                atomicMin(first_err, (unsigned long long)(a.line0 + i + 1) * 8 + kEdgeBad);
+            }
+        }
+        keep[i] = k;
+    }
+}
+
+// Matrix Market entry lines (graph_io.cpp:116-144).  pairs[i] = (i-1, j-1); flag[i]:
+// 1 = decided valid, 2 = host re-check needed.
+__global__ void k_parse_mm_lines(LineArgs a, long long* __restrict__ pairs, unsigned char* __restrict__ flag,
+                                 unsigned long long* __restrict__ first_err,
+                                 unsigned long long* __restrict__ n_uncertain) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n_lines;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b, e;
+        line_span(a, i, b, e);
+        int64_t p = b;
+        long long r = 0, c = 0;
+        int code = kOk;
+        unsigned char f = 1;
+        if (!d_read_int(a.text, p, e, r) || !d_read_int(a.text, p, e, c)) {
+            code = kMalformedEntry;
+        } else {
+            if (a.weighted) {
+                p = d_skip(a.text, p, e);
+                if (p == e) {
+                    code = kMissingWeight;
+                } else {
+                    int64_t q = p;
+                    const int v = d_scan_double(a.text, p, e, &q);
+                    if (v == 0) code = kMalformedWeight;
+                    else if (v == 2) f = 2;
+                    else p = q;
+                }
+            }
+            if (code == kOk && f == 1) {
+                if (d_skip(a.text, p, e) != e) code = kTrailing;
+                else if (r < 1 || r > a.rows || c < 1 || c > a.cols) code = kOutOfRange;
+            }
+        }
+        if (code != kOk) {
+            atomicMin(first_err, (unsigned long long)(a.line0 + i + 1) * 8 + code);
+            f = 0;
+        } else {
+            pairs[2 * i] = r - 1;
+            pairs[2 * i + 1] = c - 1;
+            if (f == 2) atomicAdd(n_uncertain, 1ull);
+        }
+        flag[i] = f;
+    }
+}
+
+// General matrices: mirror lookup of every off-diagonal entry (graph_io.cpp:153-165).
+__global__ void k_mm_keys(const long long* __restrict__ pairs, int64_t n, unsigned long long rows,
+                          unsigned long long* __restrict__ keys) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        keys[i] = (unsigned long long)pairs[2 * i] * rows + (unsigned long long)pairs[2 * i + 1];
+}
+
+__global__ void k_mm_mirror(const long long* __restrict__ pairs, int64_t n, unsigned long long rows,
+                            const unsigned long long* __restrict__ sorted, unsigned long long* __restrict__ first_missing,
+                            unsigned char* __restrict__ keep) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long i = pairs[2 * k], j = pairs[2 * k + 1];
+        keep[k] = i >= j;
+        if (i == j) continue;
+        const unsigned long long want = j * rows + i;
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if (sorted[mid] < want) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo == n || sorted[lo] != want) atomicMin(first_missing, (unsigned long long)k);
+    }
+}
+
+struct IsNewline {
+    __device__ __forceinline__ long long operator()(unsigned char c) const { return c == '\n'; }
+};
+struct NewlineAt {
+    const unsigned char* t;
+    __device__ __forceinline__ bool operator()(long long i) const { return t[i] == '\n'; }
+};
+struct IsUncertain {
+    __device__ __forceinline__ bool operator()(unsigned char f) const { return f == 2; }
+};
+
+struct Pair {
+    long long a, b;
+};
+
+template <class T>
+T fetch(const T* d, cudaStream_t st) {
+    T h;
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    return h;
+}
+
+constexpr int64_t kCubChunk = int64_t(1) << 30;  // cub item counts stay in int
+
+// Newline positions of text[0, bytes), ascending: count per chunk, then select.
+DevMem newline_positions(const unsigned char* text, int64_t bytes, int64_t* count, cudaStream_t st) {
+    DevMem cnt(sizeof(long long)), tmp;
+    std::vector<int64_t> counts;
+    int64_t total = 0;
+    for (int64_t off = 0; off < bytes; off += kCubChunk) {
+        const int len = (int)std::min(kCubChunk, bytes - off);
+        thrust::transform_iterator<IsNewline, const unsigned char*, long long> it(text + off, IsNewline{});
+        size_t tb = 0;
+        CHEB_CUDA_CHECK(cub::DeviceReduce::Sum(nullptr, tb, it, cnt.ptr<long long>(), len, st));
+        tmp.ensure(tb + 16);
+        CHEB_CUDA_CHECK(cub::DeviceReduce::Sum(tmp.get(), tb, it, cnt.ptr<long long>(), len, st));
+        counts.push_back(fetch(cnt.ptr<long long>(), st));
+        total += counts.back();
+    }
+    DevMem out(sizeof(long long) * (size_t)std::max<int64_t>(total, 1));
+    int64_t at = 0;
+    for (size_t k = 0; (int64_t)k * kCubChunk < bytes; ++k) {
+        const int64_t off = (int64_t)k * kCubChunk;
+        const int len = (int)std::min(kCubChunk, bytes - off);
+        if (counts[k] > 0) {
+            thrust::counting_iterator<long long> it(off);
+            size_t tb = 0;
+            CHEB_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tb, it, out.ptr<long long>() + at, cnt.ptr<long long>(),
+                                                  len, NewlineAt{text}, st));
+            tmp.ensure(tb + 16);
+            CHEB_CUDA_CHECK(cub::DeviceSelect::If(tmp.get(), tb, it, out.ptr<long long>() + at, cnt.ptr<long long>(),
+                                                  len, NewlineAt{text}, st));
+        }
+        at += counts[k];
+    }
+    *count = total;
+    return out;
+}
+
+// Compact pairs[i] with keep[i] != 0 (order kept) into a fresh (a,b) int64 array.
+DevMem compact_pairs(const long long* pairs, const unsigned char* keep, int64_t n, int64_t* E, cudaStream_t st) {
+    DevMem out(sizeof(Pair) * (size_t)std::max<int64_t>(n, 1));
+    DevMem cnt(sizeof(long long)), tmp;
+    int64_t at = 0;
+    for (int64_t off = 0; off < n; off += kCubChunk) {
+        const int len = (int)std::min(kCubChunk, n - off);
+        const Pair* in = reinterpret_cast<const Pair*>(pairs) + off;
+        size_t tb = 0;
+        CHEB_CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, tb, in, keep + off, out.ptr<Pair>() + at,
+                                                   cnt.ptr<long long>(), len, st));
+        tmp.ensure(tb + 16);
+        CHEB_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp.get(), tb, in, keep + off, out.ptr<Pair>() + at,
+                                                   cnt.ptr<long long>(), len, st));
+        at += fetch(cnt.ptr<long long>(), st);
+    }
+    *E = at;
+    return out;
+}
+
+// Indices i < n with flag[i] == 2 (ascending).
+std::vector<long long> uncertain_lines(const unsigned char* flag, int64_t n, int64_t expect, cudaStream_t st) {
+    DevMem idx(sizeof(long long) * (size_t)std::max<int64_t>(expect, 1)), cnt(sizeof(long long)), tmp;
+    int64_t at = 0;
+    for (int64_t off = 0; off < n; off += kCubChunk) {
+        const int len = (int)std::min(kCubChunk, n - off);
+        thrust::counting_iterator<long long> it(off);
+        thrust::transform_iterator<IsUncertain, const unsigned char*, bool> f(flag + off, IsUncertain{});
+        size_t tb = 0;
+        CHEB_CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, tb, it, f, idx.ptr<long long>() + at, cnt.ptr<long long>(),
+                                                   len, st));
+        tmp.ensure(tb + 16);
+        CHEB_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp.get(), tb, it, f, idx.ptr<long long>() + at,
+                                                   cnt.ptr<long long>(), len, st));
+        at += fetch(cnt.ptr<long long>(), st);
+    }
+    std::vector<long long> out((size_t)at);
+    if (at > 0) {
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(out.data(), idx.get(), sizeof(long long) * (size_t)at, cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    return out;
+}
+
+// A region of text on the device (zero padded) with its newline index.
+struct DeviceText {
+    DevMem text;
+    int64_t bytes = 0;
+    DevMem nl;
+    int64_t n_nl = 0;
+    int64_t n_lines = 0;
+};
+
+void index_lines(DeviceText& t, cudaStream_t st) {
+    t.nl = newline_positions(t.text.ptr<unsigned char>(), t.bytes, &t.n_nl, st);
+    unsigned char last = '\n';
+    if (t.bytes > 0) last = fetch(t.text.ptr<unsigned char>() + t.bytes - 1, st);
+    t.n_lines = t.n_nl + (t.bytes > 0 && last != '\n' ? 1 : 0);
+}
+
+std::string line_text(const DeviceText& t, int64_t i, cudaStream_t st) {
+    long long b = 0, e = t.bytes;
+    if (i > 0) b = fetch(t.nl.ptr<long long>() + i - 1, st) + 1;
+    if (i < t.n_nl) e = fetch(t.nl.ptr<long long>() + i, st);
+    std::string s((size_t)(e - b), '\0');
+    if (e > b) {
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(&s[0], t.text.ptr<char>() + b, (size_t)(e - b), cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    return s;
+}
+
+// Pinned staging ring for file uploads (process-wide; file reads overlap the H2D copies).
+struct FileRing {
+    std::mutex mu;
+    static constexpr size_t kChunk = size_t(32) << 20;
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t done[2] = {nullptr, nullptr};
+};
+FileRing& file_ring() {
+    static FileRing* r = new FileRing();  // never destroyed: outlives every handle
+    return *r;
+}
+
+// Text source: a file (streamed through the pinned ring) or a host buffer.
+struct Source {
+    const std::string& path;
+    std::ifstream* in;     // file source
+    const char* mem;       // memory source
+    int64_t size;          // total bytes
+    int64_t pos = 0;       // host read cursor (header parsing)
+    bool getline(std::string& line) {
+        if (pos >= size) return false;
+        line.clear();
+        if (in) {
+            in->clear();
+            in->seekg(pos);
+            if (!std::getline(*in, line)) return false;
+            pos += (int64_t)line.size() + 1;  // past '\n' (or past EOF for a last unterminated line)
+        } else {
+            const char* b = mem + pos;
+            const char* nl = static_cast<const char*>(std::memchr(b, '\n', (size_t)(size - pos)));
+            const int64_t len = nl ? nl - b : size - pos;
+            line.assign(b, (size_t)len);
+            pos += len + 1;
+        }
+        if (pos > size) pos = size;
+        return true;
+    }
+    void upload(int64_t offset, DeviceText& t, cudaStream_t st) {
+        const int64_t bytes = size - offset;
+        t.bytes = bytes;
+        t.text.alloc((size_t)bytes + 16);
+        CHEB_CUDA_CHECK(cudaMemsetAsync(t.text.ptr<char>() + bytes, 0, 16, st));
+        if (bytes > 0 && !in) {
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(t.text.get(), mem + offset, (size_t)bytes, cudaMemcpyHostToDevice, st));
+        } else if (bytes > 0) {
+            FileRing& R = file_ring();
+            std::lock_guard<std::mutex> lk(R.mu);
+            for (int k = 0; k < 2; ++k) {
+                if (!R.buf[k]) CHEB_CUDA_CHECK(cudaHostAlloc(&R.buf[k], FileRing::kChunk, cudaHostAllocPortable));
+                if (!R.done[k]) CHEB_CUDA_CHECK(cudaEventCreateWithFlags(&R.done[k], cudaEventDisableTiming));
+            }
+            in->clear();
+            in->seekg(offset);
+            int k = 0;
+            for (int64_t off = 0; off < bytes; off += (int64_t)FileRing::kChunk, k ^= 1) {
+                const int64_t len = std::min<int64_t>((int64_t)FileRing::kChunk, bytes - off);
+                CHEB_CUDA_CHECK(cudaEventSynchronize(R.done[k]));  // this buffer's previous copy is done
+                in->read(static_cast<char*>(R.buf[k]), len);
+                if (in->gcount() != len) fail(CHEB_PARSE, "read failed for " + path);
+                CHEB_CUDA_CHECK(cudaMemcpyAsync(t.text.ptr<char>() + off, R.buf[k], (size_t)len,
+                                                cudaMemcpyHostToDevice, st));
+                CHEB_CUDA_CHECK(cudaEventRecord(R.done[k], st));
+            }
+        }
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+};
+
+// ---------------------------------------------------------------------------------------
+// Matrix Market header (graph_io.cpp:75-111).
+struct MMHeader {
+    bool weighted = false, symmetric = false;
+    int64_t rows = 0, cols = 0, cnt = 0;
+    int64_t lines = 0;  // lines consumed (banner .. size line)
+};
+
+MMHeader parse_mm_header(Source& src) {
+    const std::string& path = src.path;
+    MMHeader h;
+    std::string line;
+    if (!src.getline(line)) fail(CHEB_PARSE, path + ": empty file");
+    h.lines = 1;
+    std::istringstream hdr(line);
+    std::string banner, object, format, field, symmetry;
+    hdr >> banner >> object >> format >> field >> symmetry;
+    for (auto* s : {&object, &format, &field, &symmetry})
+        for (auto& ch : *s) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+    if (banner != "%%MatrixMarket" || object != "matrix") fail(CHEB_PARSE, path + ": not a Matrix Market matrix file");
+    if (format != "coordinate")
+        fail(CHEB_PARSE, path + ": unsupported format '" + format + "' (coordinate only)");
+    if (field != "pattern" && field != "real")
+        fail(CHEB_PARSE, path + ": unsupported field '" + field + "' (pattern or real only)");
+    if (symmetry != "symmetric" && symmetry != "general")
+        fail(CHEB_PARSE, path + ": unsupported symmetry '" + symmetry + "' (symmetric or general only)");
+    h.weighted = field == "real";
+    h.symmetric = symmetry == "symmetric";
+    for (;;) {
+        if (!src.getline(line)) fail(CHEB_PARSE, path + ": missing size line");
+        ++h.lines;
+        const char* p = skip_blanks(line.data(), line.data() + line.size());
+        const char* e = line.data() + line.size();
+        if (p == e || *p == '%') continue;
+        if (!read_int(p, e, h.rows) || !read_int(p, e, h.cols) || !read_int(p, e, h.cnt) || !only_blanks(p, e))
+            fail(CHEB_PARSE, path + ":" + std::to_string(h.lines) + ": malformed size line");
+        break;
+    }
+    if (h.rows != h.cols)
+        fail(CHEB_VALIDATION, path + ": adjacency matrix must be square, got " + std::to_string(h.rows) + "x" +
+                                  std::to_string(h.cols));
+    return h;
+}
+
+// Parsed edges (device int64 pairs) ready for build_from_edges.
+struct ParsedText {
+    DevMem edges;
+    int64_t E = 0;
+    int64_t n_hint = 0;
+    int64_t lines = 0;
+    bool weights_ignored = false;
+};
+
+void parse_edge_list(Source& src, cudaStream_t st, ParsedText& out) {
+    DeviceText t;
+    src.upload(0, t, st);
+    index_lines(t, st);
+    out.lines = t.n_lines;
+    if (t.n_lines == 0) return;
+    DevMem pairs(sizeof(long long) * 2 * (size_t)t.n_lines), keep((size_t)t.n_lines), err(sizeof(unsigned long long));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(err.get(), 0xff, sizeof(unsigned long long), st));
+    LineArgs a{t.text.ptr<unsigned char>(), t.nl.ptr<int64_t>(), t.n_nl, t.bytes, t.n_lines, 0, 0, 0, 0};
+    k_parse_edge_lines<<<blocks_for(t.n_lines), kIngestThreads, 0, st>>>(a, pairs.ptr<long long>(),
+                                                                         keep.ptr<unsigned char>(),
+                                                                         err.ptr<unsigned long long>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    const unsigned long long e = fetch(err.ptr<unsigned long long>(), st);
+    if (e != ~0ull) fail(CHEB_PARSE, entry_message(src.path + ":" + std::to_string(e / 8), (int)(e % 8)));
+    t.text.release();
+    t.nl.release();
+    out.edges = compact_pairs(pairs.ptr<long long>(), keep.ptr<unsigned char>(), t.n_lines, &out.E, st);
+}
+
+void parse_matrix_market(Source& src, bool symmetrize, cudaStream_t st, ParsedText& out) {
+    const std::string& path = src.path;
+    const MMHeader h = parse_mm_header(src);
+    DeviceText t;
+    src.upload(src.pos, t, st);
+    index_lines(t, st);
+    out.n_hint = h.rows;
+    const int64_t need = std::max<int64_t>(h.cnt, 0);
+    const int64_t L = std::min(need, t.n_lines);
+    out.lines = h.lines + L;
+    out.weights_ignored = h.weighted && L > 0;
+    const size_t Lc = (size_t)std::max<int64_t>(L, 1);
+    DevMem pairs(sizeof(long long) * 2 * Lc), flag(Lc), err(2 * sizeof(unsigned long long));
+    auto* first_err = err.ptr<unsigned long long>();
+    CHEB_CUDA_CHECK(cudaMemsetAsync(first_err, 0xff, sizeof(unsigned long long), st));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(first_err + 1, 0, sizeof(unsigned long long), st));
+    if (L > 0) {
+        LineArgs a{t.text.ptr<unsigned char>(), t.nl.ptr<int64_t>(), t.n_nl, t.bytes, L, h.lines,
+                   h.rows, h.cols, h.weighted ? 1 : 0};
+        k_parse_mm_lines<<<blocks_for(L), kIngestThreads, 0, st>>>(a, pairs.ptr<long long>(), flag.ptr<unsigned char>(),
+                                                                   first_err, first_err + 1);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
+    unsigned long long res[2];
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(res, err.get(), sizeof res, cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    const int64_t dev_err_line = res[0] == ~0ull ? INT64_MAX : (int64_t)(res[0] / 8);
+    if (res[1] > 0) {  // host verdicts for uncertain weights, in line order, up to the first device error
+        for (long long i : uncertain_lines(flag.ptr<unsigned char>(), L, (int64_t)res[1], st)) {
+            const int64_t lineno = h.lines + i + 1;
+            if (lineno >= dev_err_line) break;
+            const std::string s = line_text(t, i, st);
+            const int code = mm_entry_host(s.data(), s.data() + s.size(), h.weighted, h.rows, h.cols);
+            if (code != kOk) fail(CHEB_PARSE, entry_message(path + ":" + std::to_string(lineno), code));
+        }
+    }
+    if (dev_err_line != INT64_MAX)
+        fail(CHEB_PARSE, entry_message(path + ":" + std::to_string(dev_err_line), (int)(res[0] % 8)));
+    if (t.n_lines < need)
+        fail(CHEB_PARSE, path + ": expected " + std::to_string(h.cnt) + " entries, got " + std::to_string(t.n_lines));
+    t.text.release();
+    t.nl.release();
+    DevMem keep(Lc);
+    if (h.symmetric || symmetrize) {
+        CHEB_CUDA_CHECK(cudaMemsetAsync(keep.get(), 1, Lc, st));
+    } else if (L > 0) {
+        // general: every off-diagonal (i,j) needs a (j,i) (graph_io.cpp:153-165); keep i >= j
+        if (h.rows > INT32_MAX) fail(CHEB_CAPACITY, "device loader supports n < 2^31");
+        const unsigned long long R = (unsigned long long)h.rows;
+        DevMem keys(sizeof(unsigned long long) * Lc), alt(sizeof(unsigned long long) * Lc),
+            miss(sizeof(unsigned long long));
+        CHEB_CUDA_CHECK(cudaMemsetAsync(miss.get(), 0xff, sizeof(unsigned long long), st));
+        k_mm_keys<<<blocks_for(L), kIngestThreads, 0, st>>>(pairs.ptr<long long>(), L, R, keys.ptr<unsigned long long>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        int end_bit = 1;
+        while (end_bit < 64 && ((R * R - 1) >> end_bit) != 0) ++end_bit;
+        cub::DoubleBuffer<unsigned long long> db(keys.ptr<unsigned long long>(), alt.ptr<unsigned long long>());
+        size_t tb = 0;
+        CHEB_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, L, 0, end_bit, st));
+        DevMem tmp(tb + 16);
+        CHEB_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(tmp.get(), tb, db, L, 0, end_bit, st));
+        k_mm_mirror<<<blocks_for(L), kIngestThreads, 0, st>>>(pairs.ptr<long long>(), L, R, db.Current(),
+                                                              miss.ptr<unsigned long long>(), keep.ptr<unsigned char>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        const unsigned long long k = fetch(miss.ptr<unsigned long long>(), st);
+        if (k != ~0ull) {
+            const long long i = fetch(pairs.ptr<long long>() + 2 * k, st) + 1;
+            const long long j = fetch(pairs.ptr<long long>() + 2 * k + 1, st) + 1;
+            fail(CHEB_VALIDATION, path + ": general matrix is not symmetric: entry (" + std::to_string(i) + "," +
+                                      std::to_string(j) + ") has no (" + std::to_string(j) + "," + std::to_string(i) +
+                                      ") counterpart (use symmetrize to force)");
+        }
+    }
+    out.edges = compact_pairs(pairs.ptr<long long>(), keep.ptr<unsigned char>(), L, &out.E, st);
+}
+
+template <class RP>
+__global__ void k_self_loops(const RP* __restrict__ rp, const int* __restrict__ col, int64_t n,
+                             unsigned long long* __restrict__ count) {
+    unsigned long long c = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t z = rp[v]; z < rp[v + 1]; ++z) c += col[z] == v;
+    c = __reduce_add_sync(0xffffffffu, (unsigned)c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
+}
+
+}  // namespace
+
+// Self-loop count of a built graph (validate's st.self_loops, graph.cpp:151).
+int64_t count_self_loops(cheb_graph* g) {
+    cudaStream_t st = g->stream;
+    if (g->n == 0) return 0;
+    DevMem c(sizeof(unsigned long long));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(c.get(), 0, sizeof(unsigned long long), st));
+    if (g->rp64)
+        k_self_loops<<<blocks_for(g->n), kIngestThreads, 0, st>>>(g->row_ptr.ptr<int64_t>(), g->col.ptr<int>(), g->n,
+                                                                  c.ptr<unsigned long long>());
+    else
+        k_self_loops<<<blocks_for(g->n), kIngestThreads, 0, st>>>(g->row_ptr.ptr<int>(), g->col.ptr<int>(), g->n,
+                                                                  c.ptr<unsigned long long>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    return (int64_t)fetch(c.ptr<unsigned long long>(), st);
+}
+
+// Parse a graph file (path) or an in-memory text (mem != nullptr; path names it in
+// messages) on the device and build it with K1.  format 0 = edge list, 1 = Matrix Market.
+void load_graph_text(cheb_graph* g, const std::string& path, const char* mem, int64_t mem_bytes, int format,
+                     const cheb_load_opts& o, int64_t* lines, int* weights_ignored) {
+    std::ifstream in;
+    int64_t size = mem_bytes;
+    if (!mem) {
+        in.open(path, std::ios::binary);
+        if (!in) fail(CHEB_PARSE, "cannot open " + path);
+        in.seekg(0, std::ios::end);
+        size = (int64_t)in.tellg();
+        in.seekg(0);
+    }
+    Source src{path, mem ? nullptr : &in, mem, size};
+    ParsedText pt;
+    if (format == 0) parse_edge_list(src, g->stream, pt);
+    else if (format == 1) parse_matrix_market(src, o.symmetrize != 0, g->stream, pt);
+    else fail(CHEB_INVALID_ARG, "unknown graph format " + std::to_string(format));
+    cheb_build_opts b;
+    cheb_build_opts_default(&b);
+    b.dedup = o.dedup;
+    b.drop_isolated = o.drop_isolated;
+    b.n_hint = pt.n_hint;
+    b.device = o.device;
+    b.row_ptr_64 = o.row_ptr_64;
+    build_from_edges(g, pt.edges.get(), pt.E, 64, b);
+    if (lines) *lines = pt.lines;
+    if (weights_ignored) *weights_ignored = pt.weights_ignored ? 1 : 0;
+}
+
+}  // namespace chebgpu

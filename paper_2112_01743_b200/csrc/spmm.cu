@@ -90,26 +90,31 @@ struct VecIO<float, 4> {
 #define CHEB_SPMM_UNROLL 8
 #endif
 constexpr int kSpmmUnroll = CHEB_SPMM_UNROLL;
+// neighbour R-vectors in flight per lane: 8 for narrow lanes (C5: VPL = 2), 4 when a lane
+// carries 4 values (register budget)
+template <int VPL>
+__host__ __device__ constexpr int spmm_unroll() { return VPL >= 4 && kSpmmUnroll > 4 ? 4 : kSpmmUnroll; }
 
-// Sum over CSR entries [b, e) of the gathered R-vectors (lane's VPL columns), 4 entries
-// (4 column ids then 4 row gathers) in flight per lane.
+// Sum over CSR entries [b, e) of the gathered R-vectors (lane's VPL columns), U entries
+// (U column ids then U row gathers) in flight per lane.
 template <class RP, class V, int VPL>
 __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b, int64_t e, int lane,
                                            bool live, V (&s)[VPL]) {
 #pragma unroll
     for (int k = 0; k < VPL; ++k) s[k] = V(0);
     const int off = lane * VPL;
+    constexpr int U = spmm_unroll<VPL>();
     int64_t j = b;
-    for (; j + kSpmmUnroll - 1 < e; j += kSpmmUnroll) {
-        int c[kSpmmUnroll];
+    for (; j + U - 1 < e; j += U) {
+        int c[U];
 #pragma unroll
-        for (int q = 0; q < kSpmmUnroll; ++q) c[q] = __ldg(a.col + j + q);
+        for (int q = 0; q < U; ++q) c[q] = __ldg(a.col + j + q);
         if (live) {
-            V v[kSpmmUnroll][VPL];
+            V v[U][VPL];
 #pragma unroll
-            for (int q = 0; q < kSpmmUnroll; ++q) VecIO<V, VPL>::ld(a.x_in + (int64_t)c[q] * a.Rs + off, v[q]);
+            for (int q = 0; q < U; ++q) VecIO<V, VPL>::ld(a.x_in + (int64_t)c[q] * a.Rs + off, v[q]);
 #pragma unroll
-            for (int q = 0; q < kSpmmUnroll; ++q)
+            for (int q = 0; q < U; ++q)
 #pragma unroll
                 for (int k = 0; k < VPL; ++k) s[k] += v[q][k];
         }

@@ -62,6 +62,10 @@ def test_device_csr_builder_errors(cheb):
     assert r.graph.n == 2 and r.isolated_dropped == 2
     r = cheb.build_graph(np.zeros((0, 2), np.int64), cheb.BuildOptions(drop_isolated=True))
     assert r.graph.n == 0
+    with pytest.raises(cheb.CapacityError):  # max id + 1 would overflow int64 (graph.cpp:25-29)
+        cheb.build_graph([[0, 2**63 - 1]])
+    with pytest.raises(cheb.CapacityError):
+        cheb.build_graph([[0, 2**31]])
 
 
 @pytest.mark.parametrize("name", [n for n in GOLDEN_NAMES if n not in ("nhint_drop_empty",)])
