@@ -161,11 +161,17 @@ struct WTile {
 static_assert(sizeof(WTile) == 16, "WTile is 16 bytes");
 constexpr int kDescBlock = 8;        // descriptors per TMA refill of a warp's program ring
 constexpr int kThreads = 256;        // CTA size of the auxiliary kernels
-constexpr int kWarps = 32;           // warps per CTA of the term kernel (1 CTA / SM)
+#ifndef CHEB_WARPS
+#define CHEB_WARPS 32
+#endif
+constexpr int kWarps = CHEB_WARPS;   // warps per CTA of the term kernel (1 CTA / SM)
 constexpr int kWarpNnz = 248;        // nnz per tile: with <= 7 alignment slots, 8 per lane
 constexpr int kWarpRows = 32;        // rows per pack tile (one per lane)
 constexpr int kColBuf = 264;         // ints per TMA column buffer (256 + alignment slack)
-constexpr int kHotBytes = 86 * 1024;  // shared hot x prefix; sized so hot + scratch fit the 164 KB carve-out and L1 keeps ~64 KB (tools/variant_run.sh sweep)
+#ifndef CHEB_HOT_KB
+#define CHEB_HOT_KB 86
+#endif
+constexpr int kHotBytes = CHEB_HOT_KB * 1024;  // shared hot x prefix; sized so hot + scratch fit the 164 KB carve-out and L1 keeps ~64 KB (tools/variant_run.sh sweep)
 constexpr int kTileChunk = 0x10;
 
 struct SolverView {
@@ -276,6 +282,7 @@ struct Tuning {
     int nogather = 0;   // 1: skip the x gathers (timing experiments only; wrong results)
     int skip = 0;       // bit 0: skip chunk tiles, bit 1: skip pack tiles (experiments only)
     int l2win = 1;      // 1: persisting-L2 window over the hot prefix of x (default on)
+    int pdl = 1;        // 1: programmatic dependent launch along the term chain (default on)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -284,6 +291,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_NOGATHER")) x.nogather = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_SKIP")) x.skip = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_L2WIN")) x.l2win = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_PDL")) x.pdl = std::atoi(e);
         return x;
     }();
     return t;

@@ -169,6 +169,12 @@ __device__ __forceinline__ void gather8(const V* __restrict__ x, unsigned hot_s,
         if ((unsigned)c[q] < (unsigned)H) v[q] = lds_v(hot_s + (unsigned)c[q] * (unsigned)sizeof(V), V(0));
 }
 
+// Programmatic dependent launch: let the next kernel of the stream launch now (its CTAs
+// take SMs as this grid drains), and wait for the previous kernel's completion + memory
+// flush before reading anything it wrote.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // TMA bulk copy global -> shared (cp.async.bulk), completion on an mbarrier.
 __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* mbar) {
     const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -430,16 +436,18 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
     }
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
+    pdl_trigger();
+    if (lane == 0) {  // this warp's tile program is static: fetch it before the dependency wait
+        if (nt > 0) issue_desc(my, 0, nullptr, ws.desc[0], &ws.descm[0]);
+        if (nt > kDescBlock) issue_desc(my, 1, nullptr, ws.desc[1], &ws.descm[1]);
+    }
+    pdl_wait();  // x_k, T, acc come from the previous kernels of the stream
     if (threadIdx.x == 0) {
         mbar_expect_tx(&mbar_hot, hot_bytes);
         constexpr unsigned kPiece = 32768;
         for (unsigned off = 0; off < hot_bytes; off += kPiece)
             bulk_g2s(smem + off, reinterpret_cast<const unsigned char*>(a.x_in) + off,
                      min(kPiece, hot_bytes - off), &mbar_hot);
-    }
-    if (lane == 0) {
-        if (nt > 0) issue_desc(my, 0, nullptr, ws.desc[0], &ws.descm[0]);
-        if (nt > kDescBlock) issue_desc(my, 1, nullptr, ws.desc[1], &ws.descm[1]);
     }
     for (int i = hot_bytes / sizeof(V) + threadIdx.x; i < H; i += blockDim.x) hot[i] = ldg_x(a.x_in + i);
 
@@ -489,6 +497,8 @@ template <int EPI, class RP, class V>
 __global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const int* __restrict__ hub_first,
                                                       int64_t n_hub) {
     const int lane = threadIdx.x & 31;
+    pdl_trigger();
+    pdl_wait();  // the term kernel's hub partials
     for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < n_hub;
          h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int f0 = hub_first[h], f1 = hub_first[h + 1];
@@ -790,23 +800,35 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         cfg.blockDim = dim3(kWarps * 32);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         cfg.attrs = attr;
         cfg.numAttrs = 0;
         // keep the hot (degree-sorted) prefix of x_k resident in L2 across the term
         if (tuning().l2win &&
             l2_window(a.x_in, (size_t)std::max<int64_t>(g->view.x_len, 1) * sizeof(V),
-                      &attr[0].val.accessPolicyWindow)) {
-            attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-            cfg.numAttrs = 1;
+                      &attr[cfg.numAttrs].val.accessPolicyWindow)) {
+            attr[cfg.numAttrs++].id = cudaLaunchAttributeAccessPolicyWindow;
+        }
+        if (tuning().pdl) {  // overlap this launch + prologue with the previous kernel's tail
+            attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
         }
         CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V>, ab, (const WTile*)g->view.prog.ptr<WTile>(),
                                            g->view.prog_len, g->view.n_tiles, H));
         if (g->view.n_hub > 0) {
             CHEB_CUDA_CHECK(cudaGetLastError());
             const int hb = (int)std::min<int64_t>((g->view.n_hub * 32 + 255) / 256, 148 * 16);
-            k_hub_finalize<EPI, RP, V><<<hb, 256, 0, st>>>(a, g->view.hub_first.ptr<int>(), g->view.n_hub);
-            CHEB_CUDA_CHECK(cudaGetLastError());
+            cudaLaunchConfig_t hc = {};
+            hc.gridDim = dim3(hb);
+            hc.blockDim = dim3(256);
+            hc.stream = st;
+            cudaLaunchAttribute hattr[1];
+            hattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            hattr[0].val.programmaticStreamSerializationAllowed = 1;
+            hc.attrs = hattr;
+            hc.numAttrs = tuning().pdl ? 1 : 0;
+            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&hc, k_hub_finalize<EPI, RP, V>, a,
+                                               (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub));
             return 2;
         }
     } else {

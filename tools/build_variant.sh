@@ -8,10 +8,11 @@ cd "$(dirname "$0")/.."
 make -s paper_2112_01743_b200/lib/libchebpr_b200.so
 mkdir -p build/variants/obj/$name
 NVFLAGS="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC,-ffp-contract=off --expt-extended-lambda -Iinclude"
-for f in cpaa spmm; do
-  nvcc $NVFLAGS $flags -c paper_2112_01743_b200/csrc/$f.cu -o build/variants/obj/$name/$f.o
+for f in cpaa spmm build capi; do
+  nvcc $NVFLAGS $flags -c paper_2112_01743_b200/csrc/$f.cu -o build/variants/obj/$name/$f.o &
 done
-objs="build/obj/build.cu.o build/obj/capi.cu.o build/obj/generate.cu.o build/obj/ingest.cu.o build/obj/coeffs.cpp.o"
+wait
+objs="build/obj/generate.cu.o build/obj/ingest.cu.o build/obj/coeffs.cpp.o"
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/$name.so $objs \
-     build/variants/obj/$name/cpaa.o build/variants/obj/$name/spmm.o -lcudart -lnccl
+     build/variants/obj/$name/*.o -lcudart -lnccl
 echo "built build/variants/$name.so"

@@ -35,7 +35,7 @@ def run(label, **kv):
     t = min(res)
     print(f"{label:28s} {t*1e3:8.1f} us/term  {B/(t*1e-3)/1e9:7.1f} GB/s  {info['nnz']/(t*1e-3)/1e9:7.1f} GTEPS")
     for k in kv:
-        lib.cheb_set_tuning(k.encode(), {"hot": -1, "l2win": 1}.get(k, 0))
+        lib.cheb_set_tuning(k.encode(), {"hot": -1, "l2win": 1, "pdl": 1}.get(k, 0))
 
 
 run("default")
@@ -47,3 +47,4 @@ run("chunk tiles only", skip=2)
 run("pack tiles only", skip=1)
 run("chunk only, no gathers", skip=2, nogather=1)
 run("pack only, no gathers", skip=1, nogather=1)
+run("no PDL", pdl=0)
