@@ -130,16 +130,101 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
     }
 }
 
+// Streaming (evict-first) access to the T / acc blocks: each is touched once per term and
+// re-read only a term or two later (GBs of traffic in between), so keeping them out of L2
+// leaves room for the gathered x rows.  x_out (the next term's gather source) keeps the
+// normal policy.
+#ifndef CHEB_SPMM_HINTS
+#define CHEB_SPMM_HINTS 1
+#endif
+template <class V, int VPL>
+struct StreamIO {  // VPL values at p (aligned to VPL * sizeof(V))
+    static __device__ __forceinline__ void ld(const V* p, V (&o)[VPL]) {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) o[k] = CHEB_SPMM_HINTS ? __ldcs(p + k) : p[k];
+    }
+    static __device__ __forceinline__ void st(V* p, const V (&v)[VPL], bool stream) {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            if (CHEB_SPMM_HINTS && stream) __stcs(p + k, v[k]);
+            else p[k] = v[k];
+        }
+    }
+};
+template <>
+struct StreamIO<double, 2> {
+    static __device__ __forceinline__ void ld(const double* p, double (&o)[2]) {
+        const double2 v = CHEB_SPMM_HINTS ? __ldcs(reinterpret_cast<const double2*>(p))
+                                          : *reinterpret_cast<const double2*>(p);
+        o[0] = v.x;
+        o[1] = v.y;
+    }
+    static __device__ __forceinline__ void st(double* p, const double (&v)[2], bool stream) {
+        const double2 w = make_double2(v[0], v[1]);
+        if (CHEB_SPMM_HINTS && stream) __stcs(reinterpret_cast<double2*>(p), w);
+        else *reinterpret_cast<double2*>(p) = w;
+    }
+};
+template <>
+struct StreamIO<float, 2> {
+    static __device__ __forceinline__ void ld(const float* p, float (&o)[2]) {
+        const float2 v = CHEB_SPMM_HINTS ? __ldcs(reinterpret_cast<const float2*>(p))
+                                         : *reinterpret_cast<const float2*>(p);
+        o[0] = v.x;
+        o[1] = v.y;
+    }
+    static __device__ __forceinline__ void st(float* p, const float (&v)[2], bool stream) {
+        const float2 w = make_float2(v[0], v[1]);
+        if (CHEB_SPMM_HINTS && stream) __stcs(reinterpret_cast<float2*>(p), w);
+        else *reinterpret_cast<float2*>(p) = w;
+    }
+};
+template <>
+struct StreamIO<float, 4> {
+    static __device__ __forceinline__ void ld(const float* p, float (&o)[4]) {
+        const float4 v = CHEB_SPMM_HINTS ? __ldcs(reinterpret_cast<const float4*>(p))
+                                         : *reinterpret_cast<const float4*>(p);
+        o[0] = v.x;
+        o[1] = v.y;
+        o[2] = v.z;
+        o[3] = v.w;
+    }
+    static __device__ __forceinline__ void st(float* p, const float (&v)[4], bool stream) {
+        const float4 w = make_float4(v[0], v[1], v[2], v[3]);
+        if (CHEB_SPMM_HINTS && stream) __stcs(reinterpret_cast<float4*>(p), w);
+        else *reinterpret_cast<float4*>(p) = w;
+    }
+};
+
 // Fused recurrence epilogue for (row u, the lane's columns).
 template <class RP, class V, int VPL>
 __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_t u, int64_t deg, int lane,
                                                const V (&s)[VPL], double& p0, double& p1) {
     const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
+    const int c0 = lane * VPL;
+    const int64_t i0 = u * a.Rs + c0;
+    if (c0 + VPL <= a.R) {  // all of the lane's columns live: vector I/O
+        V tp[VPL], ac[VPL], t[VPL], na[VPL], xo[VPL];
+        if (!a.first) StreamIO<V, VPL>::ld(a.T + i0, tp);
+        StreamIO<V, VPL>::ld(a.acc + i0, ac);
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            t[k] = a.first ? s[k] : sub_rn(mul_rn(V(2), s[k]), tp[k]);
+            na[k] = add_rn(ac[k], mul_rn((V)a.ck, t[k]));
+            xo[k] = mul_rn(t[k], inv);
+            p0 += (double)t[k];
+            p1 += (double)na[k];
+        }
+        StreamIO<V, VPL>::st(a.T + i0, t, true);
+        StreamIO<V, VPL>::st(a.acc + i0, na, true);
+        StreamIO<V, VPL>::st(a.x_out + i0, xo, false);
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < VPL; ++k) {
-        const int c = lane * VPL + k;
+        const int c = c0 + k;
         if (c >= a.R) continue;
-        const int64_t i = u * a.Rs + c;
+        const int64_t i = i0 + k;
         const V t = a.first ? s[k] : sub_rn(mul_rn(V(2), s[k]), a.T[i]);
         a.T[i] = t;
         const V nacc = add_rn(a.acc[i], mul_rn((V)a.ck, t));
