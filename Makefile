@@ -12,6 +12,10 @@ OBJS      := $(patsubst $(SRC_DIR)/%,$(OBJ_DIR)/%.o,$(SRCS))
 REFTEST_SRC ?= /root/reference/proj/tests
 REFTESTS    := test_coefficients test_graph test_cpaa test_power test_metrics
 HDRS      := $(SRC_DIR)/common.cuh $(SRC_DIR)/device.cuh include/chebpr_cuda.h
+# NCCL: the copy torch ships (nvidia-nccl wheel), so that this library and torch resolve
+# libnccl.so.2 to the same build whichever is loaded first; the system one otherwise.
+NCCL_LIB  := $(shell python -c "import nvidia.nccl, os; print(os.path.join(list(nvidia.nccl.__path__)[0], 'lib'))" 2>/dev/null)
+LDNCCL    := $(if $(NCCL_LIB),-L$(NCCL_LIB) -l:libnccl.so.2 -Xlinker -rpath -Xlinker $(NCCL_LIB),-lnccl)
 
 all: $(LIB_DIR)/libchebpr_b200.so $(LIB_DIR)/libchebpr_dropin.so oracle $(if $(wildcard $(REFTEST_SRC)/test_cpaa.cpp),reftests,)
 
@@ -25,7 +29,7 @@ $(OBJ_DIR)/%.cpp.o: $(SRC_DIR)/%.cpp $(HDRS)
 
 $(LIB_DIR)/libchebpr_b200.so: $(OBJS)
 	@mkdir -p $(LIB_DIR)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart -lnccl
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart $(LDNCCL)
 
 # C++ drop-in layer (the reference's chebpr:: API over the C-ABI)
 $(LIB_DIR)/libchebpr_dropin.so: $(SRC_DIR)/dropin.cpp $(wildcard include/chebpr/*.hpp) include/chebpr_cuda.h $(LIB_DIR)/libchebpr_b200.so
@@ -48,4 +52,7 @@ clean:
 	rm -rf build $(LIB_DIR)
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle clean reftests
+print-ldnccl:
+	@echo $(LDNCCL)
+
+.PHONY: all oracle clean reftests print-ldnccl

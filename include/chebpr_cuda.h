@@ -285,6 +285,26 @@ void cheb_device_free(void* p, int device);
 /* kahan_sum (graph.hpp:75) on the host, exactly as graph.cpp:10-19. */
 double cheb_kahan_sum(const double* x, int64_t n);
 
+/* ---- fused push exchange: x_{k+1} stored by the term kernels straight
+ * into every rank's buffer (NVLink peer memory), a release/acquire flag barrier per term;
+ * replaces the NCCL all-gather of cheb_graph_attach_comm. ---- */
+typedef struct cheb_group* cheb_group_t;
+/* One process drives G partition ranks (graphs[r] = rank r; the same graph on every handle,
+ * on one device or several peer-accessible devices). */
+cheb_status cheb_group_create(cheb_graph_t* graphs, int G, cheb_group_t* out);
+/* cheb_cpaa over the whole group: ranks (full vector, vertex order), trace, rounds, total
+ * as cheb_cpaa.  FAST mode, no reference tracking. */
+cheb_status cheb_group_cpaa(cheb_group_t grp, const cheb_cpaa_opts* opts, double* ranks,
+                            cheb_trace_row* trace, int* rounds, double* total);
+void cheb_group_destroy(cheb_group_t grp); /* detaches the graphs (they become single-GPU) */
+/* One process per GPU: make g rank `rank` of G and write its exchange-buffer IPC handles
+ * (CHEB_PEER_EXPORT_BYTES) to out; gather every rank's bytes (rank order) and pass them to
+ * cheb_peer_import; cheb_cpaa on g then runs the partitioned solve with the push exchange. */
+#define CHEB_PEER_EXPORT_BYTES 384
+cheb_status cheb_peer_export(cheb_graph_t g, int G, int rank, void* out, size_t cap);
+cheb_status cheb_peer_import(cheb_graph_t g, const void* all, size_t bytes_per_rank);
+cheb_status cheb_peer_detach(cheb_graph_t g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,7 +12,7 @@ from .api import (  # noqa: F401
     build_graph, coefficients, run_cpaa_batch, BatchResult, device_count, err_bound, generate_stage, init_state, kahan_sum,
     normalize, partition_vertices, plan_iterations, reference_pagerank, run_cpaa, run_power,
     sigma, transition_apply, upload, validate, LoadOptions, LoadedGraph, load_edge_list,
-    load_matrix_market, load_device_graph, parse_text,
+    load_matrix_market, load_device_graph, parse_text, PartitionGroup,
 )
 
 __version__ = "0.1.0"

@@ -61,6 +61,8 @@ class cheb_power_opts(C.Structure):
 
 
 # name -> (restype, argtypes)
+PEER_EXPORT_BYTES = 384  # CHEB_PEER_EXPORT_BYTES
+
 _SIGS = {
     "cheb_last_error": (C.c_char_p, []),
     "cheb_version": (C.c_char_p, []),
@@ -105,6 +107,13 @@ _SIGS = {
     "cheb_comm_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "cheb_comm_destroy": (None, [C.c_void_p]),
     "cheb_graph_attach_comm": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "cheb_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p)]),
+    "cheb_group_cpaa": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), F64P, C.POINTER(cheb_trace_row), IP,
+                                  F64P]),
+    "cheb_group_destroy": (None, [C.c_void_p]),
+    "cheb_peer_export": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),
+    "cheb_peer_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
+    "cheb_peer_detach": (C.c_int, [C.c_void_p]),
     "cheb_graph_partition_info": (C.c_int, [C.c_void_p, I64P, I64P, I64P, I64P]),
     "cheb_cpaa_batch": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), I64P, F64P, F64P,
                                   C.POINTER(cheb_trace_row), IP]),

@@ -537,6 +537,10 @@ def run_cpaa(g, cfg: Optional[SolverConfig] = None, reference=None) -> PageRankR
     ``g`` is a host UndirectedGraph (uploaded for this call, like the stateless
     reference API) or a resident DeviceGraph.
     """
+    if isinstance(g, PartitionGroup):
+        if reference is not None:
+            raise ValueError("reference tracking is not available on a partitioned handle")
+        return g.run_cpaa(cfg)
     cfg = cfg or SolverConfig()
     n = g.n
     if n < 1:
@@ -557,6 +561,40 @@ def run_cpaa(g, cfg: Optional[SolverConfig] = None, reference=None) -> PageRankR
     finally:
         if owned:
             dg.free()
+
+
+class PartitionGroup:
+    """G row-partition ranks of one graph driven by this process (the fused push exchange,
+    DESIGN.md §6): ``graphs[r]`` becomes rank r.  ``run_cpaa(group, cfg)`` solves over all
+    ranks; on one GPU the ranks run in lockstep, on several they push x over peer memory."""
+
+    def __init__(self, graphs: Sequence["DeviceGraph"]):
+        self.graphs = list(graphs)
+        arr = (C.c_void_p * len(self.graphs))(*[g.handle for g in self.graphs])
+        self._h = C.c_void_p()
+        _check(_lib().cheb_group_create(arr, len(self.graphs), C.byref(self._h)))
+        self.n = self.graphs[0].n
+
+    def run_cpaa(self, cfg: Optional[SolverConfig] = None) -> PageRankResult:
+        cfg = cfg or SolverConfig()
+        o = _cpaa_opts(cfg, None)
+        cap = max(cfg.max_rounds, cfg.rounds, 1) + 1
+        tr = (L.cheb_trace_row * cap)()
+        ranks = np.zeros(self.n)
+        rounds, total = C.c_int(), C.c_double()
+        _check(_lib().cheb_group_cpaa(self._h, C.byref(o), _pd(ranks), tr, C.byref(rounds), C.byref(total)))
+        return PageRankResult(ranks, _trace_rows(tr, rounds.value), rounds.value, False, total.value)
+
+    def close(self):
+        if self._h:
+            _lib().cheb_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 @dataclass

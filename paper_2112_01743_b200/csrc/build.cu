@@ -522,7 +522,7 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
 
     // 5. solver view (single-GPU layout) on the auxiliary stream: the degree-only half
     //    overlaps the neighbour copy; the column permute waits for it.
-    if (g->part.G == 1 && !g->part.comm && n > 0) {
+    if (g->part.G == 1 && !g->part.comm && !g->peer && n > 0) {
         if (!g->aux) CHEB_CUDA_CHECK(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
         CHEB_CUDA_CHECK(cudaStreamWaitEvent(g->aux, ev_rp, 0));
         {
@@ -924,7 +924,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     } else {
         V.inv.release();
     }
-    if (P.G > 1 || P.comm) {  // keep the global order (final un-permute), local order for row ids
+    if (P.G > 1 || P.comm || g->peer) {  // keep the global order (final un-permute), local order for row ids
         V.order_full = std::move(V.order);
         V.order.alloc(sizeof(int) * std::max<int64_t>(nl, 1));
         if (nl > 0)

@@ -137,6 +137,11 @@ cheb_graph::~cheb_graph() {
     cudaSetDevice(device);
     if (aux) cudaStreamSynchronize(aux);
     if (stream) cudaStreamSynchronize(stream);
+    if (peer) {
+        peer->release();
+        delete peer;
+        peer = nullptr;
+    }
     {   // return every buffer to the pool on this graph's stream while it still exists
         row_ptr.release();
         col.release();
@@ -409,6 +414,32 @@ void cheb_cpaa_opts_default(cheb_cpaa_opts* o) {
     o->trace = 1;
 }
 
+// cheb_trace_row of a finished solve (cpaa.cpp:99,139-145 columns).
+static void fill_trace(cheb_graph* g, const SolveSpec& s, const std::vector<double>& tr,
+                       const std::vector<double>* errs, cheb_trace_row* trace) {
+    if (!trace || s.M <= 0) return;
+    std::vector<double> co;
+    double b, c0;
+    coefficients(s.c, s.M, co, &b, &c0);
+    double residual = static_cast<double>(g->n) * c0 * b / (1.0 - b);  // cpaa.cpp:99
+    const double per_term = g->last_loop_ms / s.M;
+    for (int k = 1; k <= s.M; ++k) {
+        cheb_trace_row& r = trace[k - 1];
+        std::memset(&r, 0, sizeof r);
+        r.k = k;
+        r.c_k = co[k];
+        r.mass_T = tr[2 * (k - 1)];
+        r.S_k = tr[2 * (k - 1) + 1];
+        residual *= b;
+        r.residual_mass = residual;
+        r.elapsed_ms = per_term;
+        if (errs) {
+            r.err = (*errs)[2 * (k - 1)];
+            r.err_l1 = (*errs)[2 * (k - 1) + 1];
+        }
+    }
+}
+
 static SolveSpec checked_spec(cheb_graph* g, const cheb_cpaa_opts& o, const double* reference,
                               int64_t n_reference) {
     need_graph(g);
@@ -450,28 +481,7 @@ cheb_status cheb_cpaa(cheb_graph_t g, const cheb_cpaa_opts* opts, const double* 
         if (reference) cpaa_solve_ref(g, s, reference, &tr, &errs, &total);
         else cpaa_solve(g, s, true, &tr, &total);
         read_ranks(g, s.precision, ranks);
-        if (trace && s.M > 0) {
-            std::vector<double> co;
-            double b, c0;
-            coefficients(s.c, s.M, co, &b, &c0);
-            double residual = static_cast<double>(g->n) * c0 * b / (1.0 - b);  // cpaa.cpp:99
-            const double per_term = g->last_loop_ms / s.M;
-            for (int k = 1; k <= s.M; ++k) {
-                cheb_trace_row& r = trace[k - 1];
-                std::memset(&r, 0, sizeof r);
-                r.k = k;
-                r.c_k = co[k];
-                r.mass_T = tr[2 * (k - 1)];
-                r.S_k = tr[2 * (k - 1) + 1];
-                residual *= b;
-                r.residual_mass = residual;
-                r.elapsed_ms = per_term;
-                if (reference) {
-                    r.err = errs[2 * (k - 1)];
-                    r.err_l1 = errs[2 * (k - 1) + 1];
-                }
-            }
-        }
+        fill_trace(g, s, tr, reference ? &errs : nullptr, trace);
         if (rounds_out) *rounds_out = s.M;
         if (total_mass_out) *total_mass_out = total;
     });
@@ -632,6 +642,220 @@ cheb_status cheb_graph_attach_comm(cheb_graph_t g, cheb_comm_t comm) {
         }
         g->ws.exec_key.clear();
         g->ws.seen_key.clear();
+    });
+}
+
+// ---------------- fused push exchange ---------------------------------------------------
+void chebgpu::PeerGroup::release() {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    opened.clear();
+    for (void* p : {X[0], X[1], trace_all, rbuf, static_cast<void*>(flags)})
+        if (p) cudaFree(p);
+    X[0] = X[1] = trace_all = rbuf = nullptr;
+    flags = nullptr;
+    table.release();
+    if (signalled) cudaEventDestroy(signalled);
+    signalled = nullptr;
+}
+
+struct cheb_group {
+    std::vector<cheb_graph*> graphs;
+};
+
+namespace {
+void drop_peer(cheb_graph* g) {
+    if (!g->peer) return;
+    DeviceGuard dg(g->device);
+    cudaStreamSynchronize(g->stream);
+    g->peer->release();
+    delete g->peer;
+    g->peer = nullptr;
+}
+
+void reset_partition(cheb_graph* g, int G, int rank) {
+    g->part.G = G;
+    g->part.rank = rank;
+    g->part.comm = nullptr;
+    g->view.ready = false;
+    if (g->ws.exec) {
+        cudaGraphExecDestroy(g->ws.exec);
+        g->ws.exec = nullptr;
+    }
+    g->ws.exec_key.clear();
+    g->ws.seen_key.clear();
+}
+
+// Make g rank `rank` of G with its own exchange buffers (view rebuilt as this rank's slice).
+void make_peer(cheb_graph* g, int G, int rank, bool lockstep) {
+    if (G < 1 || rank < 0 || rank >= G) fail(CHEB_INVALID_ARG, "bad group size / rank");
+    essential(g);
+    GraphScope gs(g);
+    drop_peer(g);
+    reset_partition(g, G, rank);
+    g->peer = new PeerGroup();
+    PeerGroup& pg = *g->peer;
+    pg.G = G;
+    pg.rank = rank;
+    pg.lockstep = lockstep;
+    ensure_view(g);
+    pg.x_len = std::max<int64_t>(g->view.x_len, 1);
+    const size_t xb = sizeof(double) * (size_t)pg.x_len;
+    CHEB_CUDA_CHECK(cudaMalloc(&pg.X[0], xb));
+    CHEB_CUDA_CHECK(cudaMalloc(&pg.X[1], xb));
+    CHEB_CUDA_CHECK(cudaMalloc(&pg.rbuf, xb));
+    CHEB_CUDA_CHECK(cudaMalloc(&pg.trace_all, sizeof(double) * 2 * (size_t)kMaxPushTerms * G));
+    CHEB_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&pg.flags), sizeof(unsigned long long) * G));
+    CHEB_CUDA_CHECK(cudaMemset(pg.flags, 0, sizeof(unsigned long long) * G));
+    if (lockstep) CHEB_CUDA_CHECK(cudaEventCreateWithFlags(&pg.signalled, cudaEventDisableTiming));
+    pg.pX0.assign(G, nullptr);
+    pg.pX1.assign(G, nullptr);
+    pg.ptrace.assign(G, nullptr);
+    pg.prbuf.assign(G, nullptr);
+    pg.pflags.assign(G, nullptr);
+    pg.pX0[rank] = pg.X[0];
+    pg.pX1[rank] = pg.X[1];
+    pg.ptrace[rank] = pg.trace_all;
+    pg.prbuf[rank] = pg.rbuf;
+    pg.pflags[rank] = pg.flags;
+}
+
+void upload_table(cheb_graph* g) {
+    PeerGroup& pg = *g->peer;
+    std::vector<void*> t;
+    for (auto* v : {&pg.pX0, &pg.pX1, &pg.ptrace, &pg.prbuf, &pg.pflags}) t.insert(t.end(), v->begin(), v->end());
+    GraphScope gs(g);
+    pg.table.alloc(sizeof(void*) * t.size());
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(pg.table.get(), t.data(), sizeof(void*) * t.size(), cudaMemcpyHostToDevice, g->stream));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+    CHEB_CUDA_CHECK(cudaDeviceSynchronize());  // buffers and flags zeroed before any peer uses them
+}
+}  // namespace
+
+cheb_status cheb_group_create(cheb_graph_t* graphs, int G, cheb_group_t* out) {
+    return guarded([&] {
+        if (!graphs || G < 1 || !out) fail(CHEB_INVALID_ARG, "bad group arguments");
+        for (int r = 0; r < G; ++r) {
+            need_graph(graphs[r]);
+            for (int q = 0; q < r; ++q)
+                if (graphs[q] == graphs[r]) fail(CHEB_INVALID_ARG, "a handle appears twice in the group");
+            if (graphs[r]->n != graphs[0]->n || graphs[r]->nnz != graphs[0]->nnz || graphs[r]->m != graphs[0]->m)
+                fail(CHEB_INVALID_ARG, "group members must hold the same graph");
+        }
+        for (int r = 0; r < G; ++r)  // peer access between distinct devices
+            for (int q = 0; q < G; ++q) {
+                const int a = graphs[r]->device, b = graphs[q]->device;
+                if (a == b) continue;
+                int ok = 0;
+                CHEB_CUDA_CHECK(cudaDeviceCanAccessPeer(&ok, a, b));
+                if (!ok) fail(CHEB_CUDA, "devices " + std::to_string(a) + " and " + std::to_string(b) +
+                                             " have no peer access");
+                DeviceGuard dg(a);
+                const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CHEB_CUDA_CHECK(e);
+                cudaGetLastError();
+            }
+        for (int r = 0; r < G; ++r) make_peer(graphs[r], G, r, true);
+        for (int r = 0; r < G; ++r) {
+            PeerGroup& pg = *graphs[r]->peer;
+            for (int q = 0; q < G; ++q) {
+                const PeerGroup& o = *graphs[q]->peer;
+                pg.pX0[q] = o.X[0];
+                pg.pX1[q] = o.X[1];
+                pg.ptrace[q] = o.trace_all;
+                pg.prbuf[q] = o.rbuf;
+                pg.pflags[q] = o.flags;
+            }
+            upload_table(graphs[r]);
+        }
+        auto* grp = new cheb_group();
+        grp->graphs.assign(graphs, graphs + G);
+        *out = grp;
+    });
+}
+
+cheb_status cheb_group_cpaa(cheb_group_t grp, const cheb_cpaa_opts* opts, double* ranks, cheb_trace_row* trace,
+                            int* rounds, double* total) {
+    return guarded([&] {
+        if (!grp || grp->graphs.empty()) fail(CHEB_INVALID_ARG, "null group");
+        cheb_graph* g0 = grp->graphs[0];
+        cheb_cpaa_opts o;
+        cheb_cpaa_opts_default(&o);
+        if (opts) o = *opts;
+        SolveSpec s = checked_spec(g0, o, nullptr, 0);
+        std::vector<double> tr;
+        double tot = 0.0;
+        group_solve(grp->graphs, s, &tr, &tot);
+        read_ranks(g0, s.precision, ranks);
+        fill_trace(g0, s, tr, nullptr, trace);
+        if (rounds) *rounds = s.M;
+        if (total) *total = tot;
+    });
+}
+
+void cheb_group_destroy(cheb_group_t grp) {
+    if (!grp) return;
+    for (cheb_graph* g : grp->graphs) {
+        drop_peer(g);
+        reset_partition(g, 1, 0);
+    }
+    delete grp;
+}
+
+cheb_status cheb_peer_export(cheb_graph_t g, int G, int rank, void* out, size_t cap) {
+    return guarded([&] {
+        need_graph(g);
+        if (!out || cap < CHEB_PEER_EXPORT_BYTES) fail(CHEB_INVALID_ARG, "export buffer too small");
+        make_peer(g, G, rank, false);
+        PeerGroup& pg = *g->peer;
+        std::memset(out, 0, CHEB_PEER_EXPORT_BYTES);
+        auto* b = static_cast<unsigned char*>(out);
+        int i = 0;
+        for (void* p : {pg.X[0], pg.X[1], pg.trace_all, pg.rbuf, static_cast<void*>(pg.flags)}) {
+            cudaIpcMemHandle_t h;
+            CHEB_CUDA_CHECK(cudaIpcGetMemHandle(&h, p));
+            std::memcpy(b + 64 * i++, &h, sizeof h);
+        }
+        const int64_t meta[2] = {pg.x_len, (int64_t)rank};
+        std::memcpy(b + 320, meta, sizeof meta);
+    });
+}
+
+cheb_status cheb_peer_import(cheb_graph_t g, const void* all, size_t bytes_per_rank) {
+    return guarded([&] {
+        need_graph(g);
+        if (!g->peer || g->peer->lockstep) fail(CHEB_INVALID_ARG, "cheb_peer_export first");
+        if (!all || bytes_per_rank < CHEB_PEER_EXPORT_BYTES) fail(CHEB_INVALID_ARG, "bad import buffer");
+        PeerGroup& pg = *g->peer;
+        GraphScope gs(g);
+        const auto* b = static_cast<const unsigned char*>(all);
+        for (int q = 0; q < pg.G; ++q) {
+            const unsigned char* e = b + bytes_per_rank * q;
+            int64_t meta[2];
+            std::memcpy(meta, e + 320, sizeof meta);
+            if (meta[1] != q || meta[0] != pg.x_len) fail(CHEB_INVALID_ARG, "peer exports out of order or mismatched");
+            if (q == pg.rank) continue;
+            void* ptr[5];
+            for (int i = 0; i < 5; ++i) {
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, e + 64 * i, sizeof h);
+                CHEB_CUDA_CHECK(cudaIpcOpenMemHandle(&ptr[i], h, cudaIpcMemLazyEnablePeerAccess));
+                pg.opened.push_back(ptr[i]);
+            }
+            pg.pX0[q] = ptr[0];
+            pg.pX1[q] = ptr[1];
+            pg.ptrace[q] = ptr[2];
+            pg.prbuf[q] = ptr[3];
+            pg.pflags[q] = ptr[4];
+        }
+        upload_table(g);
+    });
+}
+
+cheb_status cheb_peer_detach(cheb_graph_t g) {
+    return guarded([&] {
+        need_graph(g);
+        drop_peer(g);
+        reset_partition(g, 1, 0);
     });
 }
 

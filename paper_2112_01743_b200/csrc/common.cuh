@@ -207,6 +207,29 @@ struct Partition {
     void* comm = nullptr;  // ncclComm_t (owned by the cheb_comm handle, not by the graph)
 };
 
+// Fused push exchange of a row partition: every rank owns IPC-exportable
+// exchange buffers and holds pointers to every peer's copies (IPC-opened or, when one
+// process drives all ranks, plain/peer pointers).  The term epilogue stores x_{k+1} into
+// all G buffers; a release/acquire flag barrier separates terms.
+constexpr int kMaxPushTerms = 1024;  // trace slots per rank in the exchange buffer
+struct PeerGroup {
+    int G = 1, rank = 0;
+    bool lockstep = false;  // all ranks driven by one host thread (cheb_group_*)
+    int64_t x_len = 0;
+    // this rank's own buffers (cudaMalloc: IPC-exportable)
+    void* X[2] = {nullptr, nullptr};       // padded x_k, x_len * 8 bytes each
+    void* trace_all = nullptr;             // [G][2 * kMaxPushTerms] doubles
+    void* rbuf = nullptr;                  // padded ranks, x_len * 8 bytes
+    unsigned long long* flags = nullptr;   // [G] barrier epochs written by the peers
+    // every rank's buffers as seen from this device ([rank] = own)
+    std::vector<void*> pX0, pX1, ptrace, prbuf, pflags;
+    std::vector<void*> opened;             // IPC-opened peer pointers (closed on release)
+    DevMem table;                          // device copies: X0[G] X1[G] trace[G] rbuf[G] flags[G]
+    unsigned long long epoch = 0;          // barriers passed (identical on every rank)
+    cudaEvent_t signalled = nullptr;       // lockstep: this rank's last signal
+    void release();
+};
+
 struct Workspace {
     int64_t n = 0;
     int R = 0;
@@ -263,6 +286,7 @@ struct cheb_graph {
     chebgpu::StagedState staged;
     chebgpu::BatchWorkspace bws;
     chebgpu::Partition part;
+    chebgpu::PeerGroup* peer = nullptr;  // fused push exchange (instead of part.comm)
     double last_loop_ms = 0.0;
     int last_terms = 0;
     int last_launches = 0;
@@ -352,6 +376,7 @@ void read_batch_ranks(cheb_graph* g, double* ranks, int R);
 void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
                     std::vector<double>* errs, double* total);
 void read_ranks(cheb_graph* g, int precision, double* ranks);
+void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr, double* total);
 void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_ms);
 void power_solve(cheb_graph* g, double c, int rounds, double tol, int max_rounds, int mode,
                  const double* reference, double* ranks, cheb_trace_row* trace, int cap,

@@ -70,6 +70,11 @@ struct TermArgs {
     double* hub_ts;  // [n_hub][2] this term
     int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
     int tune_skip;      // experiments only: bit 0 skip chunk tiles, bit 1 skip pack tiles
+    // fused push exchange (partitioned runs): x_{k+1}[u] is stored at push[r][push_off + u]
+    // for every rank r (peer memory over NVLink) instead of x_out[u]
+    V* const* push;
+    int push_n;
+    int64_t push_off;
 };
 
 // Row epilogue.  u is a row of the current layout; deg its row length.
@@ -214,7 +219,12 @@ __device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, 
             a.T[u] = t;
             const V nacc = add_rn(accv, mul_rn((V)a.ck, t));
             a.acc[u] = nacc;
-            a.x_out[u] = mul_rn(t, inv);
+            const V xn = mul_rn(t, inv);
+            if (a.push) {  // fused exchange: straight into every rank's copy of x_{k+1}
+                for (int r = 0; r < a.push_n; ++r) a.push[r][a.push_off + u] = xn;
+            } else {
+                a.x_out[u] = xn;
+            }
             p0 += (double)t;
             p1 += (double)nacc;
         } else if constexpr (EPI == EPI_GEN) {
@@ -976,14 +986,6 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
 template <class V>
 ncclDataType_t nccl_type() { return sizeof(V) == 8 ? ncclDouble : ncclFloat; }
 
-__global__ void k_sum_ranks(const double* __restrict__ all, int G, int len, double* __restrict__ out) {
-    for (int i = threadIdx.x; i < len; i += blockDim.x) {
-        double s = 0.0;
-        for (int r = 0; r < G; ++r) s += all[(size_t)r * len + i];  // rank order: deterministic
-        out[i] = s;
-    }
-}
-
 template <class V>
 __global__ void k_normalize_slot(const V* __restrict__ acc, int64_t nl, const double* __restrict__ total,
                                  V* __restrict__ slot) {
@@ -1005,51 +1007,163 @@ __global__ void k_unpermute_padded(const V* __restrict__ padded, const int64_t* 
     }
 }
 
-template <class RP, class V>
-void run_solve_dist(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, double* total,
-                    std::vector<double>* term_ms = nullptr) {
-    cudaStream_t st = g->stream;
-    Partition& P = g->part;
-    SolverView& Vw = g->view;
-    ncclComm_t comm = static_cast<ncclComm_t>(P.comm);
-    const Layout L = layout_of(g, CHEB_MODE_FAST);
-    ensure_workspace<V>(g, s.M, 1);
-    Workspace& w = g->ws;
-    const int64_t nl = Vw.n_local, mr = P.max_rows;
-    const int M = s.M, G = P.G;
-    std::vector<double> coeffs;
-    double beta_v, c0;
-    coefficients(s.c, M, coeffs, &beta_v, &c0);
-    DevMem d_p;
-    if (s.p) {
-        d_p.alloc(sizeof(double) * g->n);
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(d_p.get(), s.p, sizeof(double) * g->n, cudaMemcpyHostToDevice, st));
+// ---------------- fused push exchange: barrier and copy kernels ------------------------
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// This rank reached `epoch`: publish it in slot [rank] of every rank's flag array.  The
+// system-scope fence orders every earlier store of this stream (the term's pushes) before it.
+__global__ void k_peer_signal(unsigned long long* const* flags, int G, int rank, unsigned long long epoch) {
+    const int r = threadIdx.x;
+    if (r < G) {
+        __threadfence_system();
+        st_release_sys(flags[r] + rank, epoch);
     }
-    DevMem trace_all(sizeof(double) * 2 * (size_t)std::max(M, 1) * G), tglob(sizeof(double) * 2 * std::max(M, 1));
-    DevMem rbuf(sizeof(V) * (size_t)std::max<int64_t>(Vw.x_len, 1)), dcuts(sizeof(int64_t) * (G + 1));
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(dcuts.get(), P.cuts.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, st));
-    V* T[2] = {w.T0.ptr<V>(), w.T1.ptr<V>()};
-    V* X[2] = {w.X0.ptr<V>(), w.X1.ptr<V>()};
-    V* acc = w.acc.ptr<V>();
-    const ncclDataType_t ty = nccl_type<V>();
+}
+
+// Wait until every rank published `epoch` into this rank's flags (acquire: their pushes are
+// visible to every later kernel of this stream).
+__global__ void k_peer_wait(const unsigned long long* flags, int G, unsigned long long epoch) {
+    const int r = threadIdx.x;
+    if (r < G)
+        while (ld_acquire_sys(flags + r) < epoch) __nanosleep(100);
+    __syncthreads();
+}
+
+// dst[r][off + i] = src[i] for every rank r (trace partials, x_0 slot).
+template <class T>
+__global__ void k_push_copy(const T* __restrict__ src, int64_t n, T* const* dst, int G, int64_t off) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = src[i];
+        for (int r = 0; r < G; ++r) dst[r][off + i] = v;
+    }
+}
+
+// ranks of the local rows, normalised, pushed into every rank's padded result buffer
+template <class V>
+__global__ void k_normalize_push(const V* __restrict__ acc, int64_t nl, const double* __restrict__ total,
+                                 V* const* dst, int G, int64_t off) {
+    const double tot = *total;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nl; u += (int64_t)gridDim.x * blockDim.x) {
+        const V v = (V)((double)acc[u] / tot);
+        for (int r = 0; r < G; ++r) dst[r][off + u] = v;
+    }
+}
+
+// out[i] = sum over ranks r (in rank order: deterministic) of all[r * stride + i]
+__global__ void k_sum_ranks_strided(const double* __restrict__ all, int G, int len, int64_t stride,
+                                    double* __restrict__ out) {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) {
+        double s = 0.0;
+        for (int r = 0; r < G; ++r) s += all[(size_t)r * stride + i];
+        out[i] = s;
+    }
+}
+
+// One partitioned solve on one rank, in phases, so that a single process can also drive
+// every rank of a group in lockstep.  Exchange: NCCL all-gathers (part.comm) or the fused
+// push (g->peer): pushes inside the kernels + a flag barrier between phases.
+template <class RP, class V>
+struct DistSolve {
+    cheb_graph* g;
+    SolveSpec s;
+    Layout L;
+    PeerGroup* pg;  // null: NCCL
+    std::vector<double> coeffs;
+    double c0 = 0.0, beta_v = 0.0;
+    DevMem d_p, trace_all, tglob, rbuf, dcuts;
+    V* T[2];
+    V* X[2];
+    V* acc;
     int launches = 0;
-    std::vector<cudaEvent_t> tev;
-    if (term_ms) {
-        tev.resize(2 * (size_t)std::max(M, 1));
-        for (auto& e : tev) CHEB_CUDA_CHECK(cudaEventCreate(&e));
+    int64_t nl = 0, mr = 0, stride = 0;
+    int M = 0, G = 1;
+    std::vector<cudaEvent_t>* tev = nullptr;
+    const double* d_total = nullptr;
+
+    DistSolve(cheb_graph* g_, const SolveSpec& s_, std::vector<cudaEvent_t>* ev) : g(g_), s(s_), tev(ev) {
+        L = layout_of(g, CHEB_MODE_FAST);
+        pg = g->peer;
+        ensure_workspace<V>(g, s.M, 1);
+        Workspace& w = g->ws;
+        const SolverView& Vw = g->view;
+        const Partition& P = g->part;
+        nl = Vw.n_local;
+        mr = P.max_rows;
+        M = s.M;
+        G = P.G;
+        if (pg && M > kMaxPushTerms) fail(CHEB_CAPACITY, "push exchange supports at most 1024 terms");
+        coefficients(s.c, M, coeffs, &beta_v, &c0);
+        cudaStream_t st = g->stream;
+        if (s.p) {
+            d_p.alloc(sizeof(double) * g->n);
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(d_p.get(), s.p, sizeof(double) * g->n, cudaMemcpyHostToDevice, st));
+        }
+        tglob.alloc(sizeof(double) * 2 * std::max(M, 1));
+        dcuts.alloc(sizeof(int64_t) * (G + 1));
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(dcuts.get(), P.cuts.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, st));
+        T[0] = w.T0.ptr<V>();
+        T[1] = w.T1.ptr<V>();
+        acc = w.acc.ptr<V>();
+        if (pg) {
+            X[0] = static_cast<V*>(pg->X[0]);
+            X[1] = static_cast<V*>(pg->X[1]);
+            stride = 2 * (int64_t)kMaxPushTerms;
+        } else {
+            X[0] = w.X0.ptr<V>();
+            X[1] = w.X1.ptr<V>();
+            trace_all.alloc(sizeof(double) * 2 * (size_t)std::max(M, 1) * G);
+            rbuf.alloc(sizeof(V) * (size_t)std::max<int64_t>(Vw.x_len, 1));
+            stride = 2 * (int64_t)std::max(M, 1);
+        }
+    }
+    ncclComm_t comm() const { return static_cast<ncclComm_t>(g->part.comm); }
+    V* const* push_table(int which) const {  // device pointer table of every rank's X[which]
+        return reinterpret_cast<V* const*>(pg->table.ptr<void*>() + (size_t)which * G);
+    }
+    double* const* trace_table() const { return reinterpret_cast<double* const*>(pg->table.ptr<void*>() + 2 * (size_t)G); }
+    V* const* rbuf_table() const { return reinterpret_cast<V* const*>(pg->table.ptr<void*>() + 3 * (size_t)G); }
+    unsigned long long* const* flag_table() const {
+        return reinterpret_cast<unsigned long long* const*>(pg->table.ptr<void*>() + 4 * (size_t)G);
     }
 
-    CHEB_CUDA_CHECK(cudaEventRecord(g->ev0, st));
-    // T_{-1} = T_0, acc, x_0 for the local rows (p indexed by old id through the local order)
-    k_init<RP, V><<<grid1d(nl), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, d_p.ptr<double>(), L.order,
-                                                   nl, c0 / 2.0, T[0], T[1], acc, X[0] + Vw.x_off);
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    ++launches;
-    CHEB_NCCL_CHECK(ncclAllGather(X[0] + Vw.x_off, X[0], (size_t)mr, ty, comm, st));
-    for (int k = 1; k <= M; ++k) {
+    // phase 0: T_{-1} = T_0, acc, x_0 of the local rows, then x_0 to every rank
+    void begin() {
+        cudaStream_t st = g->stream;
+        const SolverView& Vw = g->view;
+        CHEB_CUDA_CHECK(cudaEventRecord(g->ev0, st));
+        k_init<RP, V><<<grid1d(nl), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, d_p.ptr<double>(), L.order,
+                                                       nl, c0 / 2.0, T[0], T[1], acc, X[0] + Vw.x_off);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+        if (pg) {
+            k_push_copy<V><<<grid1d(nl), kThreads, 0, st>>>(X[0] + Vw.x_off, nl, push_table(0), G, Vw.x_off);
+            ++launches;
+        } else {
+            CHEB_NCCL_CHECK(ncclAllGather(X[0] + Vw.x_off, X[0], (size_t)mr, nccl_type<V>(), comm(), st));
+        }
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
+
+    // phase k: fused term k (pushes x_{k+1} to every rank) + this rank's trace partials
+    void term(int k) {
+        cudaStream_t st = g->stream;
+        const SolverView& Vw = g->view;
+        Workspace& w = g->ws;
         TermArgs<RP, V> a = base_args<RP, V>(g, L);
         a.x_in = X[(k - 1) & 1];
         a.x_out = X[k & 1] + Vw.x_off;
+        if (pg) {
+            a.push = push_table(k & 1);
+            a.push_n = G;
+            a.push_off = Vw.x_off;
+        }
         a.T = T[(k - 1) & 1];
         a.acc = acc;
         a.ck = coeffs[k];
@@ -1058,66 +1172,184 @@ void run_solve_dist(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, 
         a.hub_part = w.hub_part.ptr<double>();
         a.hub_cnt = w.hub_cnt.ptr<unsigned>();
         a.hub_ts = Vw.n_hub ? w.hub_ts.ptr<double>() + (size_t)(k - 1) * Vw.n_hub * 2 : nullptr;
-        if (term_ms) CHEB_CUDA_CHECK(cudaEventRecord(tev[2 * (k - 1)], st));
+        if (tev) CHEB_CUDA_CHECK(cudaEventRecord((*tev)[2 * (k - 1)], st));
         launches += launch_pass<EPI_CPAA>(g, L, a);
-        if (term_ms) CHEB_CUDA_CHECK(cudaEventRecord(tev[2 * (k - 1) + 1], st));
-        k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), Vw.grid, w.hub_ts.ptr<double>(),
-                                               (int)Vw.n_hub, k - 1, w.trace.ptr<double>());
+        if (tev) CHEB_CUDA_CHECK(cudaEventRecord((*tev)[2 * (k - 1) + 1], st));
+        k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), Vw.grid, w.hub_ts.ptr<double>(), (int)Vw.n_hub,
+                                               k - 1, w.trace.ptr<double>());
         CHEB_CUDA_CHECK(cudaGetLastError());
         ++launches;
-        // x_{k+1}: every rank's slot -> every rank (in place, equal counts)
-        CHEB_NCCL_CHECK(ncclAllGather(X[k & 1] + Vw.x_off, X[k & 1], (size_t)mr, ty, comm, st));
+        if (!pg) {  // x_{k+1}: every rank's slot -> every rank (in place, equal counts)
+            CHEB_NCCL_CHECK(ncclAllGather(X[k & 1] + Vw.x_off, X[k & 1], (size_t)mr, nccl_type<V>(), comm(), st));
+        }
     }
-    const double* d_total;
-    if (M > 0) {
-        CHEB_NCCL_CHECK(ncclAllGather(w.trace.ptr<double>(), trace_all.ptr<double>(), 2 * (size_t)M, ncclDouble, comm, st));
-        k_sum_ranks<<<1, 256, 0, st>>>(trace_all.ptr<double>(), G, 2 * M, tglob.ptr<double>());
-        d_total = tglob.ptr<double>() + 2 * (M - 1) + 1;
-    } else {
-        const int eg = grid1d(nl);
-        k_sum_blocks<V><<<eg, kThreads, 0, st>>>(acc, nl, w.part.ptr<double>());
-        k_sum_final<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), eg, w.total.ptr<double>());
-        CHEB_NCCL_CHECK(ncclAllGather(w.total.ptr<double>(), trace_all.ptr<double>(), 1, ncclDouble, comm, st));
-        k_sum_ranks<<<1, 32, 0, st>>>(trace_all.ptr<double>(), G, 1, tglob.ptr<double>());
-        d_total = tglob.ptr<double>();
-    }
-    k_normalize_slot<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf.ptr<V>() + Vw.x_off);
-    CHEB_NCCL_CHECK(ncclAllGather(rbuf.ptr<V>() + Vw.x_off, rbuf.ptr<V>(), (size_t)mr, ty, comm, st));
-    k_unpermute_padded<V><<<grid1d(Vw.x_len), kThreads, 0, st>>>(rbuf.ptr<V>(), dcuts.ptr<int64_t>(), G, mr,
-                                                                Vw.order_full.ptr<int>(), w.out.ptr<V>());
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    launches += 4;
-    CHEB_CUDA_CHECK(cudaEventRecord(g->ev1, st));
-    g->last_terms = M;
-    g->last_launches = launches;
-    w.launches = launches;
 
-    std::vector<double> t(2 * (size_t)std::max(M, 1));
-    double tot = 0.0;
-    if (M > 0)
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), tglob.get(), sizeof(double) * 2 * M, cudaMemcpyDeviceToHost, st));
-    else
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(&tot, tglob.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
-    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-    g->last_loop_ms = ms;
+    // phase M+1: every rank's trace (or, for M = 0, its acc total) to every rank
+    void trace_out() {
+        cudaStream_t st = g->stream;
+        Workspace& w = g->ws;
+        double* all = pg ? static_cast<double*>(pg->trace_all) : trace_all.ptr<double>();
+        (void)all;
+        if (M == 0) {
+            const int eg = grid1d(nl);
+            k_sum_blocks<V><<<eg, kThreads, 0, st>>>(acc, nl, w.part.ptr<double>());
+            k_sum_final<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), eg, w.total.ptr<double>());
+            launches += 2;
+        }
+        const double* src = M > 0 ? w.trace.ptr<double>() : w.total.ptr<double>();
+        const int len = M > 0 ? 2 * M : 1;
+        if (pg) {
+            k_push_copy<double><<<1, kThreads, 0, st>>>(src, len, trace_table(), G, (int64_t)pg->rank * stride);
+            ++launches;
+        } else {
+            CHEB_NCCL_CHECK(ncclAllGather(src, trace_all.ptr<double>(), (size_t)len, ncclDouble, comm(), st));
+        }
+        CHEB_CUDA_CHECK(cudaGetLastError());
+    }
+
+    // phase M+2: combine the traces in rank order, normalise the local rows, send them
+    void normalize() {
+        cudaStream_t st = g->stream;
+        const SolverView& Vw = g->view;
+        const double* all = pg ? static_cast<const double*>(pg->trace_all) : trace_all.ptr<double>();
+        const int len = M > 0 ? 2 * M : 1;
+        k_sum_ranks_strided<<<1, 256, 0, st>>>(all, G, len, pg ? stride : len, tglob.ptr<double>());
+        d_total = M > 0 ? tglob.ptr<double>() + 2 * (M - 1) + 1 : tglob.ptr<double>();
+        if (pg) {
+            k_normalize_push<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf_table(), G, Vw.x_off);
+        } else {
+            k_normalize_slot<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf.ptr<V>() + Vw.x_off);
+            CHEB_NCCL_CHECK(ncclAllGather(rbuf.ptr<V>() + Vw.x_off, rbuf.ptr<V>(), (size_t)mr, nccl_type<V>(), comm(), st));
+        }
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        launches += 2;
+    }
+
+    // phase M+3: padded ranks -> vertex order; read back the trace, check it
+    void finish(std::vector<double>* tr, double* total) {
+        cudaStream_t st = g->stream;
+        const SolverView& Vw = g->view;
+        Workspace& w = g->ws;
+        const V* padded = pg ? static_cast<const V*>(pg->rbuf) : rbuf.ptr<V>();
+        k_unpermute_padded<V><<<grid1d(Vw.x_len), kThreads, 0, st>>>(padded, dcuts.ptr<int64_t>(), G, mr,
+                                                                    Vw.order_full.ptr<int>(), w.out.ptr<V>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+        CHEB_CUDA_CHECK(cudaEventRecord(g->ev1, st));
+        g->last_terms = M;
+        g->last_launches = launches;
+        w.launches = launches;
+        std::vector<double> t(2 * (size_t)std::max(M, 1));
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), tglob.get(), sizeof(double) * (M > 0 ? 2 * M : 1),
+                                        cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        float ms = 0.f;
+        CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
+        g->last_loop_ms = ms;
+        for (int k = 1; k <= M; ++k)
+            if (!std::isfinite(t[2 * (k - 1)]) || !std::isfinite(t[2 * (k - 1) + 1]))
+                fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(k));
+        const double tot = M > 0 ? t[2 * (M - 1) + 1] : t[0];
+        if (!std::isfinite(tot) || tot <= 0.0) fail(CHEB_NUMERIC, "normalization total is not positive and finite");
+        if (tr) *tr = t;
+        if (total) *total = tot;
+    }
+
+    // push barrier, one rank per process: publish, then wait for every rank
+    void signal() {
+        ++pg->epoch;
+        k_peer_signal<<<1, 32, 0, g->stream>>>(flag_table(), G, pg->rank, pg->epoch);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        if (pg->lockstep) CHEB_CUDA_CHECK(cudaEventRecord(pg->signalled, g->stream));
+        ++launches;
+    }
+    void wait() {
+        k_peer_wait<<<1, 32, 0, g->stream>>>(pg->flags, G, pg->epoch);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+    }
+};
+
+template <class RP, class V>
+void run_solve_dist(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, double* total,
+                    std::vector<double>* term_ms = nullptr) {
+    std::vector<cudaEvent_t> tev;
     if (term_ms) {
-        term_ms->assign(M, 0.0);
-        for (int k = 0; k < M; ++k) {
+        tev.resize(2 * (size_t)std::max(s.M, 1));
+        for (auto& e : tev) CHEB_CUDA_CHECK(cudaEventCreate(&e));
+    }
+    DistSolve<RP, V> d(g, s, term_ms ? &tev : nullptr);
+    const bool push = d.pg != nullptr;
+    auto barrier = [&] {
+        if (push) {
+            d.signal();
+            d.wait();
+        }
+    };
+    d.begin();
+    barrier();
+    for (int k = 1; k <= s.M; ++k) {
+        d.term(k);
+        barrier();
+    }
+    d.trace_out();
+    barrier();
+    d.normalize();
+    barrier();
+    d.finish(tr, total);
+    if (term_ms) {
+        term_ms->assign(s.M, 0.0);
+        for (int k = 0; k < s.M; ++k) {
             float tk = 0.f;
             CHEB_CUDA_CHECK(cudaEventElapsedTime(&tk, tev[2 * k], tev[2 * k + 1]));
             (*term_ms)[k] = tk;
         }
         for (auto& e : tev) cudaEventDestroy(e);
     }
-    for (int k = 1; k <= M; ++k)
-        if (!std::isfinite(t[2 * (k - 1)]) || !std::isfinite(t[2 * (k - 1) + 1]))
-            fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(k));
-    if (M > 0) tot = t[2 * (M - 1) + 1];
-    if (!std::isfinite(tot) || tot <= 0.0) fail(CHEB_NUMERIC, "normalization total is not positive and finite");
-    if (tr) *tr = t;
-    if (total) *total = tot;
+}
+
+// One host thread drives every rank of a push group (one device or several): each phase is
+// enqueued on every rank's stream, then every rank signals, and each rank's wait kernel is
+// ordered (by events) after all signals — so no kernel ever spins on work that has not been
+// enqueued, and ranks sharing one GPU cannot deadlock.
+template <class RP, class V>
+void run_group_lockstep(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr,
+                        double* total) {
+    const int G = (int)gs.size();
+    std::vector<std::unique_ptr<DistSolve<RP, V>>> d;
+    for (cheb_graph* g : gs) {
+        GraphScope sc(g);
+        d.emplace_back(new DistSolve<RP, V>(g, s, nullptr));
+    }
+    auto each = [&](auto&& f) {
+        for (int r = 0; r < G; ++r) {
+            GraphScope sc(gs[r]);
+            f(*d[r]);
+        }
+    };
+    auto barrier = [&] {
+        each([](DistSolve<RP, V>& x) { x.signal(); });
+        for (int r = 0; r < G; ++r) {
+            GraphScope sc(gs[r]);
+            for (int q = 0; q < G; ++q)
+                CHEB_CUDA_CHECK(cudaStreamWaitEvent(gs[r]->stream, gs[q]->peer->signalled, 0));
+            d[r]->wait();
+        }
+    };
+    each([](DistSolve<RP, V>& x) { x.begin(); });
+    barrier();
+    for (int k = 1; k <= s.M; ++k) {
+        each([k](DistSolve<RP, V>& x) { x.term(k); });
+        barrier();
+    }
+    each([](DistSolve<RP, V>& x) { x.trace_out(); });
+    barrier();
+    each([](DistSolve<RP, V>& x) { x.normalize(); });
+    barrier();
+    for (int r = 0; r < G; ++r) {
+        GraphScope sc(gs[r]);
+        d[r]->finish(r == 0 ? tr : nullptr, r == 0 ? total : nullptr);
+    }
 }
 
 std::string solve_key(const SolveSpec& s, bool has_p) {
@@ -1130,7 +1362,7 @@ std::string solve_key(const SolveSpec& s, bool has_p) {
 template <class RP, class V>
 void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
                  std::vector<double>* errs, double* total) {
-    if (g->part.comm) {
+    if (g->part.comm || g->peer) {
         if (h_ref) fail(CHEB_INVALID_ARG, "reference tracking is not available on a partitioned handle");
         if (s.mode != CHEB_MODE_FAST) fail(CHEB_INVALID_ARG, "a partitioned handle runs the FAST schedule only");
         run_solve_dist<RP, V>(g, s, tr, total);
@@ -1251,6 +1483,27 @@ void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool /*host_results*/, std::v
     }
 }
 
+// Lockstep solve of a push group (every rank's handle driven by this thread).
+void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr, double* total) {
+    if (s.R != 1) fail(CHEB_INVALID_ARG, "R > 1 is served by the batched path");
+    if (s.mode != CHEB_MODE_FAST) fail(CHEB_INVALID_ARG, "a partitioned handle runs the FAST schedule only");
+    bool rp64 = false;
+    for (cheb_graph* g : gs) {
+        GraphScope sc(g);
+        ensure_view(g);
+        rp64 = rp64 || g->view.rp64;
+    }
+    for (cheb_graph* g : gs)
+        if (g->view.rp64 != rp64) fail(CHEB_INVALID_ARG, "group members disagree on row-pointer width");
+    if (s.precision == CHEB_FP64) {
+        if (rp64) run_group_lockstep<int64_t, double>(gs, s, tr, total);
+        else run_group_lockstep<int, double>(gs, s, tr, total);
+    } else {
+        if (rp64) run_group_lockstep<int64_t, float>(gs, s, tr, total);
+        else run_group_lockstep<int, float>(gs, s, tr, total);
+    }
+}
+
 // With reference tracking (err / err_l1 columns): plain launches, per-term reduction.
 void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
                     std::vector<double>* errs, double* total) {
@@ -1272,7 +1525,8 @@ void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_m
     auto run = [&](auto rp_tag, auto v_tag) {
         using RP = decltype(rp_tag);
         using V = decltype(v_tag);
-        if (g->part.comm) {
+        if (g->part.comm || g->peer) {
+            if (g->peer && g->peer->lockstep) fail(CHEB_INVALID_ARG, "profile a lockstep group through cheb_group_cpaa");
             run_solve_dist<RP, V>(g, s, nullptr, nullptr, &term_ms);
             return;
         }

@@ -58,6 +58,35 @@ class Communicator:
             pass
 
 
+class PeerExchange:
+    """Fused push exchange over the ranks of a torch.distributed process group (one process
+    per GPU): every rank exports its exchange buffers as CUDA IPC handles,
+    the handles are all-gathered, and each rank maps its peers' buffers.  After ``attach``
+    the term kernels store x_{k+1} straight into every peer's buffer (NVLink), with a flag
+    barrier per term instead of an NCCL all-gather."""
+
+    def __init__(self, dg: DeviceGraph, rank: int, world: int, group=None):
+        import torch.distributed as dist
+        lib = L.load()
+        mine = (C.c_ubyte * L.PEER_EXPORT_BYTES)()
+        _check(lib.cheb_peer_export(dg.handle, world, rank, mine, L.PEER_EXPORT_BYTES))
+        if world > 1:
+            allb = [None] * world
+            dist.all_gather_object(allb, bytes(mine), group=group)
+        else:
+            allb = [bytes(mine)]
+        buf = (C.c_ubyte * (L.PEER_EXPORT_BYTES * world)).from_buffer_copy(b"".join(allb))
+        _check(lib.cheb_peer_import(dg.handle, buf, L.PEER_EXPORT_BYTES))
+        if world > 1:
+            dist.barrier(group=group)  # every rank mapped every peer before any pushes
+        self.dg, self.rank, self.world = dg, rank, world
+
+    def detach(self):
+        if self.dg is not None and self.dg.handle:
+            _check(L.load().cheb_peer_detach(self.dg.handle))
+        self.dg = None
+
+
 def partition_info(dg: DeviceGraph) -> dict:
     lo, hi, nnz, mr = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
     _check(L.load().cheb_graph_partition_info(dg.handle, C.byref(lo), C.byref(hi), C.byref(nnz), C.byref(mr)))

@@ -1,0 +1,102 @@
+"""Fused push exchange of the row partition on one B200.
+
+A PartitionGroup drives G ranks of the same graph from one process: every rank's term kernel
+stores x_{k+1} straight into every rank's padded buffer, and a release/acquire flag barrier
+separates the terms.  On one GPU the ranks run in lockstep (each rank's wait kernel is
+event-ordered after every rank's signal, so no kernel spins on work not yet enqueued).  The
+kernels, buffers and barrier are the ones a one-process-per-GPU run uses over NVLink.
+Checked against the single-GPU solve and the reference's golden ranks."""
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+TOL64 = 1e-12
+
+pytestmark = pytest.mark.gpu
+
+
+def top_k(r, k=100):
+    return np.lexsort((np.arange(r.size), -r))[:k]
+
+
+def _handles(cheb, edges, G):
+    return [cheb.build_device_graph(edges)[0] for _ in range(G)]
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("name", ["config1", "gnp2000", "star100"])
+def test_push_group_matches_single_gpu_and_reference(cheb, name, G):
+    z = load_golden(name)
+    single_dg, _ = cheb.build_device_graph(z["edges"])
+    single = cheb.run_cpaa(single_dg, cheb.SolverConfig(rounds=39))
+    hs = _handles(cheb, z["edges"], G)
+    grp = cheb.PartitionGroup(hs)
+    res = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=39))
+    assert res.rounds == 39
+    assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
+    assert np.max(np.abs(res.ranks - z["cpaa39_ranks"])) <= TOL64
+    k = min(100, res.ranks.size)
+    assert np.array_equal(top_k(res.ranks, k), top_k(z["cpaa39_ranks"], k))
+    for a, b in zip(res.trace, single.trace):  # rank-ordered trace combine
+        assert a.k == b.k and a.c_k == b.c_k
+        assert abs(a.S_k - b.S_k) <= 1e-9 * abs(b.S_k)
+        assert abs(a.mass_T - b.mass_T) <= 1e-9 * max(1.0, abs(b.mass_T))
+    again = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=39))  # barrier epochs keep counting
+    assert np.array_equal(again.ranks, res.ranks)
+    grp.close()
+    # detached handles are single-GPU handles again
+    after = cheb.run_cpaa(hs[0], cheb.SolverConfig(rounds=39))
+    assert np.array_equal(after.ranks, single.ranks)
+
+
+def test_push_group_hub_rows_and_eps(cheb):
+    """A power-law graph with rows above the warp tile (hub chunks finalised by the second
+    kernel, whose epilogue pushes too), planned by eps."""
+    from paper_2112_01743_b200 import generate as Gen
+    e = Gen.chung_lu_edges(1 << 15, 2.1, 2.0, 5000.0, 200_000, 9)
+    single_dg, info = cheb.build_device_graph(e)
+    assert info["max_degree"] > 248
+    single = cheb.run_cpaa(single_dg, cheb.SolverConfig(eps=1e-10))
+    for G in (2, 4):
+        grp = cheb.PartitionGroup(_handles(cheb, e, G))
+        res = cheb.run_cpaa(grp, cheb.SolverConfig(eps=1e-10))
+        assert res.rounds == single.rounds == 39
+        assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
+        assert np.array_equal(top_k(res.ranks), top_k(single.ranks))
+        grp.close()
+
+
+def test_push_group_zero_rounds_and_fp32(cheb):
+    z = load_golden("gnp2000")
+    grp = cheb.PartitionGroup(_handles(cheb, z["edges"], 2))
+    r0 = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=0))
+    assert r0.rounds == 0 and np.allclose(r0.ranks, 1.0 / z["n"], rtol=0, atol=1e-15)
+    r32 = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=39, precision=32))
+    ref = z["cpaa39_ranks"]
+    assert np.abs(r32.ranks - ref).sum() / np.abs(ref).sum() <= 1e-6
+    grp.close()
+
+
+def test_push_group_rejects_mixed_graphs(cheb):
+    a, _ = cheb.build_device_graph(load_golden("gnp2000")["edges"])
+    b, _ = cheb.build_device_graph(load_golden("config1")["edges"])
+    with pytest.raises(ValueError, match="same graph"):
+        cheb.PartitionGroup([a, b])
+
+
+def test_peer_exchange_single_rank_ipc(cheb):
+    """The one-process-per-GPU wiring at world size 1: the exchange buffers are exported as
+    CUDA IPC handles and imported back, cheb_cpaa runs the partitioned solve with the push
+    exchange and the device flag barrier (signal + spin-wait kernels)."""
+    from paper_2112_01743_b200.distributed import PeerExchange
+    z = load_golden("config1")
+    dg, _ = cheb.build_device_graph(z["edges"])
+    plain = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+    px = PeerExchange(dg, 0, 1)
+    part = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+    assert np.max(np.abs(part.ranks - plain.ranks)) <= TOL64
+    assert np.max(np.abs(part.ranks - z["cpaa39_ranks"])) <= TOL64
+    px.detach()
+    again = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+    assert np.array_equal(again.ranks, plain.ranks)

@@ -14,5 +14,5 @@ done
 wait
 objs="build/obj/generate.cu.o build/obj/ingest.cu.o build/obj/coeffs.cpp.o"
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/$name.so $objs \
-     build/variants/obj/$name/*.o -lcudart -lnccl
+     build/variants/obj/$name/*.o -lcudart $(make -s -f Makefile print-ldnccl 2>/dev/null || echo -lnccl)
 echo "built build/variants/$name.so"
