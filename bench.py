@@ -305,18 +305,23 @@ class Solver:
     """One step = one CPAA solve to eps 1e-10 on the resident graph (scalar K2 path, or the
     batched K5 path when the config has R right-hand sides)."""
 
-    def __init__(self, dg, info, cfg, precision):
+    def __init__(self, dg, info, cfg, precision, rank=0, world=1):
         import paper_2112_01743_b200 as cheb
         from paper_2112_01743_b200 import _lib as L
         self.cheb, self.L, self.lib = cheb, L, L.load()
         self.dg, self.info, self.cfg = dg, info, cfg
         self.R = int(cfg.get("R", 1))
         self.M = cheb.plan_iterations(DAMPING, EPS).M
+        self.seeds = c5_seeds(dg, self.R) if self.R > 1 else None
+        if self.R > 1 and world > 1:
+            # batched config on N GPUs: replicas (§8(e)) — the graph on every GPU, the R
+            # right-hand sides split across the ranks, no per-term communication
+            self.seeds = np.ascontiguousarray(self.seeds[rank::world])
+            self.R = int(self.seeds.size)
         o = L.cheb_cpaa_opts()
         self.lib.cheb_cpaa_opts_default(C.byref(o))
         o.eps, o.c, o.precision, o.R = EPS, DAMPING, precision, self.R
         self.opts = o
-        self.seeds = c5_seeds(dg, self.R) if self.R > 1 else None
         self.d_ranks = C.c_void_p()
 
     def _seed_ptr(self):
@@ -456,6 +461,9 @@ def main():
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
+                    help="N>1: x_{k+1} exchange of the row partition (fused push over peer memory, "
+                         "or NCCL all-gather); the e2e leg always attaches an NCCL communicator")
     ap.add_argument("--profile-only", action="store_true",
                     help="build + a few solves, no timing output (for ncu captures)")
     args = ap.parse_args()
@@ -474,15 +482,20 @@ def main():
     t0 = time.perf_counter()
     dg, info = build_device(cfg, device)
     build_s = time.perf_counter() - t0
-    comm = None
-    if dist.world > 1:
-        # strong scaling: every rank holds the same graph; the solver view is partitioned
-        # by rows over the ranks and x_{k+1} is all-gathered over NVLink every term
-        from paper_2112_01743_b200.distributed import Communicator
-        comm = Communicator(dist.rank, dist.world, device)
-        comm.attach(dg)
+    comm = px = None
+    R_cfg = int(cfg.get("R", 1))
+    if dist.world > 1 and R_cfg == 1:
+        # strong scaling: every rank holds the same graph; the solver view is partitioned by
+        # rows over the ranks and x_{k+1} reaches every rank each term — pushed by the term
+        # kernels into the peers' buffers (default) or all-gathered by NCCL
+        from paper_2112_01743_b200.distributed import Communicator, PeerExchange
+        comm = Communicator(dist.rank, dist.world, device)  # e2e leg (fresh handles per step)
+        if args.exchange == "push":
+            px = PeerExchange(dg, dist.rank, dist.world)
+        else:
+            comm.attach(dg)
     n, nnz = info["n"], info["nnz"]
-    sv = Solver(dg, info, cfg, args.precision)
+    sv = Solver(dg, info, cfg, args.precision, dist.rank, dist.world)
     M, R = sv.M, sv.R
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
@@ -511,8 +524,9 @@ def main():
         dist.barrier()
     total_ms = dist.max(sum(times))
     ms_step = total_ms / args.steps
-    # whole-job rate: one graph per job (strong scaling over row partitions for N > 1)
-    value = nnz * R * M / (ms_step * 1e-3) / 1e9
+    # whole-job rate: one graph (and the config's R right-hand sides) per job — strong
+    # scaling over row partitions (R = 1) or over the split right-hand sides (R > 1)
+    value = nnz * R_cfg * M / (ms_step * 1e-3) / 1e9
 
     # dominant kernel: the fused term kernel (+ its hub-row finalize), CUDA events per term
     flush.zero_()
@@ -551,7 +565,8 @@ def main():
                        "terms": M, "eps": EPS, "c": DAMPING,
                        "time_to_1e-10_ms": round(ms_step, 4),
                        "gteps_definition": "nnz*R*terms/step_time (every CSR entry one traversal)",
-                       "parallelism": f"rowpart{dist.world}+nccl_allgather" if dist.world > 1 else "single",
+                       "parallelism": (f"rowpart{dist.world}+" + ("push" if px is not None else "nccl_allgather"))
+                       if dist.world > 1 else "single",
                        "l2": "flushed (512 MiB write) before every timed step",
                        "graph_build_s": round(build_s, 3)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
@@ -568,6 +583,8 @@ def main():
         }
         print(json.dumps(line))
     dg.free()
+    if px is not None:
+        px.detach()
     if comm is not None:
         comm.close()
     dist.close()
