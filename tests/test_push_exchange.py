@@ -100,3 +100,16 @@ def test_peer_exchange_single_rank_ipc(cheb):
     px.detach()
     again = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
     assert np.array_equal(again.ranks, plain.ranks)
+
+
+@pytest.mark.parametrize("name,G", [("path3", 5), ("k2", 3), ("cycle4", 4), ("star100", 8)])
+def test_push_group_more_ranks_than_work(cheb, name, G):
+    """Tiny graphs cut into more ranks than they have (or nearly have) rows: empty slices
+    push nothing but still signal every barrier."""
+    z = load_golden(name)
+    single = cheb.run_cpaa(cheb.build_device_graph(z["edges"])[0], cheb.SolverConfig(rounds=39))
+    grp = cheb.PartitionGroup(_handles(cheb, z["edges"], G))
+    res = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=39))
+    assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
+    assert np.max(np.abs(res.ranks - z["cpaa39_ranks"])) <= TOL64
+    grp.close()
