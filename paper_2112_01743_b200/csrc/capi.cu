@@ -151,9 +151,7 @@ cheb_graph::~cheb_graph() {
             cudaGraphExecDestroy(ws.exec);
             ws.exec = nullptr;
         }
-        ws.T0.release(); ws.T1.release(); ws.X0.release(); ws.X1.release(); ws.acc.release();
-        ws.out.release(); ws.part.release(); ws.hub_part.release(); ws.hub_cnt.release();
-        ws.hub_ts.release(); ws.trace.release(); ws.total.release(); ws.coeffs.release();
+        ws.release_buffers();
         staged = chebgpu::StagedState{};
         bws = chebgpu::BatchWorkspace{};
     }

@@ -243,11 +243,18 @@ struct Workspace {
     DevMem trace;                       // double [M][2] (mass_T, S_k)
     DevMem total;                       // double [1]
     DevMem coeffs;                      // double [M+1]
+    DevMem snap;                        // BITEXACT: double [M][2][n] snapshots of T_k, acc_k
     // CUDA graph of the whole solve for a given configuration.
     cudaGraphExec_t exec = nullptr;
     std::string exec_key;
     std::string seen_key;  // last configuration solved without a graph
     int launches = 0;
+    // every buffer back to the pool on its stream (the owner calls this while the stream lives)
+    void release_buffers() {
+        for (DevMem* d : {&T0, &T1, &X0, &X1, &acc, &out, &part, &hub_part, &hub_cnt, &hub_ts, &trace, &total,
+                          &coeffs, &snap})
+            d->release();
+    }
     ~Workspace() {
         if (exec) cudaGraphExecDestroy(exec);
     }

@@ -543,43 +543,97 @@ __global__ void __launch_bounds__(kThreads) k_term_exact(TermArgs<RP, double> a,
 }
 
 // Serial Kahan sums exactly as graph.cpp:10-19 (single thread: bit-identical order).
-__global__ void k_kahan2(const double* __restrict__ x, const double* __restrict__ y, int64_t n,
-                         double* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-        double a = __dsub_rn(x[i], c0);
-        double t = __dadd_rn(s0, a);
-        c0 = __dsub_rn(__dsub_rn(t, s0), a);
-        s0 = t;
-        if (y) {
-            double b = __dsub_rn(y[i], c1);
-            double u = __dadd_rn(s1, b);
-            c1 = __dsub_rn(__dsub_rn(u, s1), b);
-            s1 = u;
+// The reference's serial compensated sums, bit for bit (graph.cpp:10-19 order, one element
+// at a time).  The recurrence is inherently sequential, so one thread runs it; warps 1..7
+// stage the next chunk of both inputs into shared memory meanwhile, so the chain runs at
+// FP64 add latency instead of waiting on global loads.
+constexpr int kSerialChunk = 1024;
+
+template <int MODE>  // 0: Kahan(x) [, Kahan(y)]   1: power: Kahan|y - x|, Kahan(y) (power.cpp:80-93)
+__global__ void __launch_bounds__(256) k_serial_sums(const double* __restrict__ a, const double* __restrict__ b,
+                                                     int64_t n, double* __restrict__ out) {
+    __shared__ double sa[2][kSerialChunk], sb[2][kSerialChunk];
+    const int tid = threadIdx.x;
+    const bool two = b != nullptr;
+    auto stage = [&](int buf, int64_t base) {  // warps 1..7
+        const int64_t len = n - base < kSerialChunk ? n - base : (int64_t)kSerialChunk;
+        for (int64_t i = tid - 32; i < len; i += blockDim.x - 32) {
+            sa[buf][i] = a[base + i];
+            if (two) sb[buf][i] = b[base + i];
         }
+    };
+    if (tid >= 32 && n > 0) stage(0, 0);
+    __syncthreads();
+    double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
+    for (int64_t base = 0; base < n; base += kSerialChunk) {
+        const int cur = (int)((base / kSerialChunk) & 1);
+        if (tid >= 32 && base + kSerialChunk < n) stage(cur ^ 1, base + kSerialChunk);
+        if (tid == 0) {
+            const int len = (int)(n - base < kSerialChunk ? n - base : (int64_t)kSerialChunk);
+#pragma unroll 4
+            for (int j = 0; j < len; ++j) {
+                if constexpr (MODE == 0) {
+                    const double av = __dsub_rn(sa[cur][j], c0);
+                    const double t = __dadd_rn(s0, av);
+                    c0 = __dsub_rn(__dsub_rn(t, s0), av);
+                    s0 = t;
+                    if (two) {
+                        const double bv = __dsub_rn(sb[cur][j], c1);
+                        const double u = __dadd_rn(s1, bv);
+                        c1 = __dsub_rn(__dsub_rn(u, s1), bv);
+                        s1 = u;
+                    }
+                } else {  // a = y (new), b = x (old)
+                    const double y = sa[cur][j];
+                    const double d = __dsub_rn(fabs(__dsub_rn(y, sb[cur][j])), c0);
+                    const double t = __dadd_rn(s0, d);
+                    c0 = __dsub_rn(__dsub_rn(t, s0), d);
+                    s0 = t;
+                    const double av = __dsub_rn(y, c1);
+                    const double u = __dadd_rn(s1, av);
+                    c1 = __dsub_rn(__dsub_rn(u, s1), av);
+                    s1 = u;
+                }
+            }
+        }
+        __syncthreads();
     }
-    out[0] = s0;
-    out[1] = s1;
+    if (tid == 0) {
+        out[0] = s0;
+        out[1] = s1;
+    }
 }
 
-// Power-method L1 change + mass with the reference's Kahan order (power.cpp:80-93).
-__global__ void k_kahan_l1(const double* __restrict__ y, const double* __restrict__ x, int64_t n,
-                           double* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double l1 = 0.0, comp = 0.0, s = 0.0, c = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-        double d = __dsub_rn(fabs(__dsub_rn(y[i], x[i])), comp);
-        double t = __dadd_rn(l1, d);
-        comp = __dsub_rn(__dsub_rn(t, l1), d);
-        l1 = t;
-        double a = __dsub_rn(y[i], c);
-        double u = __dadd_rn(s, a);
+// Many independent serial Kahan sums (one per thread), each in the reference's element
+// order: the BITEXACT trace of all M terms after the loop (mass_T = Kahan(T_k),
+// S_k = Kahan(acc_k) from per-term snapshots).  Sums of different terms do not depend on
+// each other, so they run side by side; within a sum the order is the reference's.
+__global__ void k_kahan_many(const double* __restrict__ snaps, int64_t n, int count, double* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const double* __restrict__ x = snaps + (size_t)t * (size_t)n;
+    double s = 0.0, c = 0.0;
+    int64_t i = 0;
+    constexpr int U = 16;
+    for (; i + U <= n; i += U) {
+        double v[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) v[q] = __ldg(x + i + q);
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const double a = __dsub_rn(v[q], c);
+            const double u = __dadd_rn(s, a);
+            c = __dsub_rn(__dsub_rn(u, s), a);
+            s = u;
+        }
+    }
+    for (; i < n; ++i) {
+        const double a = __dsub_rn(x[i], c);
+        const double u = __dadd_rn(s, a);
         c = __dsub_rn(__dsub_rn(u, s), a);
         s = u;
     }
-    out[0] = l1;
-    out[1] = s;
+    out[t] = s;
 }
 
 // ---------------- init / reductions / normalisation ----------------------------------
@@ -892,6 +946,22 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     }
 }
 
+// BITEXACT trace snapshots (2 M n doubles) when they fit a quarter of the free memory (and
+// 8 GB); otherwise the per-term serial sums run instead.
+void ensure_snapshots(cheb_graph* g, int M) {
+    Workspace& w = g->ws;
+    const size_t need = sizeof(double) * 2 * (size_t)M * (size_t)g->n;
+    if (w.snap.bytes() >= need) return;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
+    if (need > free_b / 4 || need > (size_t(8) << 30)) return;
+    w.snap.alloc(need);
+    if (w.exec) cudaGraphExecDestroy(w.exec);  // a captured solve baked the old pointers in
+    w.exec = nullptr;
+    w.exec_key.clear();
+    w.seen_key.clear();
+}
+
 // Enqueue the whole solve: init, M fused terms, trace reduction, normalisation.
 template <class RP, class V>
 int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std::vector<double>& coeffs,
@@ -907,6 +977,10 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
     V* acc = w.acc.ptr<V>();
     double* trace = w.trace.ptr<double>();
     const int grid = L.fast ? g->view.grid : 0;
+    // BITEXACT trace: snapshots + one batched pass when they fit (else per-term serial sums)
+    // (reference tracking reads each term's S_k inside the loop: per-term sums there)
+    double* snap = (!L.fast && M > 0 && !d_ref && w.snap.bytes() >= sizeof(double) * 2 * (size_t)M * n)
+                       ? w.snap.ptr<double>() : nullptr;
 
     k_init<RP, V><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, d_p, L.order, n,
                                                   c0 / 2.0, T[0], T[1], acc, X[0]);
@@ -930,9 +1004,16 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
         if (term_ev) CHEB_CUDA_CHECK(cudaEventRecord((*term_ev)[2 * (k - 1)], st));
         launches += launch_pass<EPI_CPAA>(g, L, a);
         if (term_ev) CHEB_CUDA_CHECK(cudaEventRecord((*term_ev)[2 * (k - 1) + 1], st));
-        if (!L.fast) {
+        if (!L.fast && snap) {
+            // trace sums exactly as the reference, Kahan(T_curr) and Kahan(acc): snapshot the
+            // two vectors now, sum all terms' snapshots side by side after the loop
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(snap + (size_t)(2 * (k - 1)) * n, a.T, sizeof(double) * n,
+                                            cudaMemcpyDeviceToDevice, st));
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(snap + (size_t)(2 * (k - 1) + 1) * n, acc, sizeof(double) * n,
+                                            cudaMemcpyDeviceToDevice, st));
+        } else if (!L.fast) {
             // trace sums exactly as the reference: Kahan(T_curr), Kahan(acc)
-            k_kahan2<<<1, 32, 0, st>>>(reinterpret_cast<const double*>(a.T),
+            k_serial_sums<0><<<1, 256, 0, st>>>(reinterpret_cast<const double*>(a.T),
                                        reinterpret_cast<const double*>(acc), n, trace + 2 * (k - 1));
             CHEB_CUDA_CHECK(cudaGetLastError());
             ++launches;
@@ -952,6 +1033,11 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
             launches += 2;
         }
     }
+    if (snap) {
+        k_kahan_many<<<(2 * M + 31) / 32, 32, 0, st>>>(snap, n, 2 * M, trace);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+    }
     if (L.fast && !per_term_reduce && M > 0) {
         k_trace_reduce<<<M, kThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
                                                (int)g->view.n_hub, 0, trace);
@@ -970,7 +1056,7 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
             k_sum_final<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), eg, tot);
             launches += 2;
         } else {
-            k_kahan2<<<1, 32, 0, st>>>(reinterpret_cast<const double*>(acc), nullptr, n, tot);
+            k_serial_sums<0><<<1, 256, 0, st>>>(reinterpret_cast<const double*>(acc), nullptr, n, tot);
             ++launches;
         }
         CHEB_CUDA_CHECK(cudaGetLastError());
@@ -1373,6 +1459,7 @@ void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::ve
     ensure_workspace<V>(g, s.M, 1);
     Workspace& w = g->ws;
     const int64_t n = g->n;
+    if (!L.fast && s.M > 0) ensure_snapshots(g, s.M);
     std::vector<double> coeffs;
     double beta_v, c0;
     coefficients(s.c, s.M, coeffs, &beta_v, &c0);
@@ -1624,7 +1711,7 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
             a.T = w.acc.ptr<double>();
             CHEB_CUDA_CHECK(cudaMemcpyAsync(a.T, X, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
             launch_pass<EPI_POWER>(g, L, a);
-            k_kahan_l1<<<1, 32, 0, st>>>(a.T, X, n, dtr);
+            k_serial_sums<1><<<1, 256, 0, st>>>(a.T, X, n, dtr);
             CHEB_CUDA_CHECK(cudaMemcpyAsync(X, a.T, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         } else {
             launch_pass<EPI_POWER>(g, L, a);
