@@ -636,6 +636,60 @@ __global__ void k_kahan_many(const double* __restrict__ snaps, int64_t n, int co
     out[t] = s;
 }
 
+// Power rounds j = 1..nb of a speculative batch (snapshots S[0..nb] of x): thread 2(j-1)
+// runs the reference's Kahan L1 change |S[j] - S[j-1]|, thread 2(j-1)+1 the Kahan mass of
+// S[j] (power.cpp:80-93), each in element order.
+__global__ void k_power_many(const double* __restrict__ S, int64_t n, int nb, double* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * nb) return;
+    const int j = t / 2 + 1;
+    const double* __restrict__ y = S + (size_t)j * (size_t)n;
+    const double* __restrict__ x = S + (size_t)(j - 1) * (size_t)n;
+    double s = 0.0, c = 0.0;
+    constexpr int U = 16;  // loads of the next elements are independent of the chain
+    int64_t i = 0;
+    if (t & 1) {
+        for (; i + U <= n; i += U) {
+            double v[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) v[q] = __ldg(y + i + q);
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const double a = __dsub_rn(v[q], c);
+                const double u = __dadd_rn(s, a);
+                c = __dsub_rn(__dsub_rn(u, s), a);
+                s = u;
+            }
+        }
+        for (; i < n; ++i) {
+            const double a = __dsub_rn(__ldg(y + i), c);
+            const double u = __dadd_rn(s, a);
+            c = __dsub_rn(__dsub_rn(u, s), a);
+            s = u;
+        }
+    } else {
+        for (; i + U <= n; i += U) {
+            double d[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) d[q] = fabs(__dsub_rn(__ldg(y + i + q), __ldg(x + i + q)));
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const double e = __dsub_rn(d[q], c);
+                const double u = __dadd_rn(s, e);
+                c = __dsub_rn(__dsub_rn(u, s), e);
+                s = u;
+            }
+        }
+        for (; i < n; ++i) {
+            const double e = __dsub_rn(fabs(__dsub_rn(__ldg(y + i), __ldg(x + i))), c);
+            const double u = __dadd_rn(s, e);
+            c = __dsub_rn(__dsub_rn(u, s), e);
+            s = u;
+        }
+    }
+    out[t] = s;
+}
+
 // ---------------- init / reductions / normalisation ----------------------------------
 // T_{-1} = T_0 = p (or 1), acc = (c0/2) T_0, x_0 = T_0 D^-1   (cpaa.cpp:88-92, :116 at k=1)
 template <class RP, class V>
@@ -1691,7 +1745,83 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
     double* dtr = w.trace.ptr<double>();
     const int grid = L.fast ? g->view.grid : 0;
     int k = 0;
-    while (k < budget) {
+    // Speculative batches of rounds (no reference tracking): every round's x is snapshotted,
+    // the batch's L1 changes and masses are read back once, and the solve stops at the first
+    // round that meets tol — its x is in the snapshots, so the result is the per-round one.
+    const int B = h_ref ? 0 : (int)std::min<int64_t>(16, std::max(budget, 1));
+    DevMem snaps;
+    if (B > 0) {
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        if (sizeof(double) * (size_t)(B + 1) * (size_t)n <= free_b / 4)
+            snaps.alloc(sizeof(double) * (size_t)(B + 1) * (size_t)n);
+    }
+    if (snaps) {
+        double* S = snaps.ptr<double>();
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(S, X, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+        const double* final_x = S;
+        bool done = budget == 0;
+        while (!done) {
+            const int nb = std::min(B, budget - k);
+            for (int j = 1; j <= nb; ++j) {
+                const int kk = k + j;
+                double* Sj = S + (size_t)j * n;
+                CHEB_CUDA_CHECK(cudaMemcpyAsync(Sj, Sj - n, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+                TermArgs<RP, double> a = base_args<RP, double>(g, L);
+                a.x_in = C[(kk - 1) & 1];
+                a.x_out = C[kk & 1];
+                a.T = Sj;  // in: x_{k-1}; out: y = x_k
+                a.ck = c;
+                a.base = base;
+                a.first = 0;
+                if (L.fast) {
+                    a.part = w.part.ptr<double>();
+                    a.hub_part = w.hub_part.ptr<double>();
+                    a.hub_cnt = w.hub_cnt.ptr<unsigned>();
+                    a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() : nullptr;
+                }
+                launch_pass<EPI_POWER>(g, L, a);
+                if (L.fast)
+                    k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub,
+                                                           0, dtr + 2 * (j - 1));
+                CHEB_CUDA_CHECK(cudaGetLastError());
+            }
+            if (!L.fast) {
+                k_power_many<<<(2 * nb + 31) / 32, 32, 0, st>>>(S, n, nb, dtr);
+                CHEB_CUDA_CHECK(cudaGetLastError());
+            }
+            std::vector<double> h(2 * (size_t)nb);
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(h.data(), dtr, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, st));
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+            int stop = 0;
+            for (int j = 1; j <= nb && !stop; ++j) {
+                const int kk = k + j;
+                if (trace && kk <= cap) {
+                    cheb_trace_row& r = trace[kk - 1];
+                    std::memset(&r, 0, sizeof r);
+                    r.k = kk;
+                    r.l1_change = h[2 * (j - 1)];
+                    r.mass_T = h[2 * (j - 1) + 1];
+                }
+                if (!std::isfinite(h[2 * (j - 1)])) fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(kk));
+                if (by_tol && h[2 * (j - 1)] < tol) stop = j;
+            }
+            if (stop) {
+                k += stop;
+                final_x = S + (size_t)stop * n;
+                done = true;
+            } else {
+                k += nb;
+                final_x = S + (size_t)nb * n;
+                done = k >= budget;
+                if (!done)  // next batch starts from this batch's last x
+                    CHEB_CUDA_CHECK(cudaMemcpyAsync(S, final_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+                if (!done) final_x = S;
+            }
+        }
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(X, final_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    }
+    while (!snaps && k < budget) {
         ++k;
         TermArgs<RP, double> a = base_args<RP, double>(g, L);
         a.x_in = C[(k - 1) & 1];
