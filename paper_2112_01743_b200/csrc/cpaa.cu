@@ -1176,6 +1176,45 @@ __global__ void k_peer_wait(const unsigned long long* flags, int G, unsigned lon
     __syncthreads();
 }
 
+// Term tail of a one-process-per-GPU push run, one launch instead of three: this rank's
+// trace partials of term k (as k_trace_reduce), then the barrier (signal every rank, wait
+// for every rank).  Launched with PDL; waits for the term kernels before reading anything.
+__global__ void __launch_bounds__(256) k_term_tail(const double* __restrict__ part, int grid,
+                                                   const double* __restrict__ hub_ts, int n_hub, int k,
+                                                   double* __restrict__ trace, unsigned long long* const* flags,
+                                                   const unsigned long long* my_flags, int G, int rank,
+                                                   unsigned long long epoch) {
+    __shared__ double sh[32];
+    pdl_wait();
+    const double* pk = part + (size_t)k * grid * 2;
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < grid; i += blockDim.x) {
+        a += pk[2 * i];
+        b += pk[2 * i + 1];
+    }
+    if (hub_ts) {
+        const double* hk = hub_ts + (size_t)k * n_hub * 2;
+        for (int i = threadIdx.x; i < n_hub; i += blockDim.x) {
+            a += hk[2 * i];
+            b += hk[2 * i + 1];
+        }
+    }
+    a = block_sum(a, sh);
+    b = block_sum(b, sh);
+    if (threadIdx.x == 0) {
+        trace[2 * k] = a;
+        trace[2 * k + 1] = b;
+    }
+    const int r = threadIdx.x;
+    if (r < G) {
+        __threadfence_system();  // the term's pushes (earlier kernels of this stream) first
+        st_release_sys(flags[r] + rank, epoch);
+    }
+    if (r < G)
+        while (ld_acquire_sys(my_flags + r) < epoch) __nanosleep(100);
+    __syncthreads();
+}
+
 // dst[r][off + i] = src[i] for every rank r (trace partials, x_0 slot).
 template <class T>
 __global__ void k_push_copy(const T* __restrict__ src, int64_t n, T* const* dst, int G, int64_t off) {
@@ -1226,10 +1265,12 @@ struct DistSolve {
     int M = 0, G = 1;
     std::vector<cudaEvent_t>* tev = nullptr;
     const double* d_total = nullptr;
+    bool fused_tail = false;  // push, one process per GPU: trace reduce + barrier in one kernel
 
     DistSolve(cheb_graph* g_, const SolveSpec& s_, std::vector<cudaEvent_t>* ev) : g(g_), s(s_), tev(ev) {
         L = layout_of(g, CHEB_MODE_FAST);
         pg = g->peer;
+        fused_tail = pg && !pg->lockstep;
         ensure_workspace<V>(g, s.M, 1);
         Workspace& w = g->ws;
         const SolverView& Vw = g->view;
@@ -1315,8 +1356,25 @@ struct DistSolve {
         if (tev) CHEB_CUDA_CHECK(cudaEventRecord((*tev)[2 * (k - 1)], st));
         launches += launch_pass<EPI_CPAA>(g, L, a);
         if (tev) CHEB_CUDA_CHECK(cudaEventRecord((*tev)[2 * (k - 1) + 1], st));
-        k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), Vw.grid, w.hub_ts.ptr<double>(), (int)Vw.n_hub,
-                                               k - 1, w.trace.ptr<double>());
+        if (fused_tail) {
+            ++pg->epoch;
+            cudaLaunchConfig_t tc = {};
+            tc.gridDim = dim3(1);
+            tc.blockDim = dim3(256);
+            tc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            tc.attrs = at;
+            tc.numAttrs = tuning().pdl ? 1 : 0;
+            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&tc, k_term_tail, (const double*)w.part.ptr<double>(), Vw.grid,
+                                               (const double*)w.hub_ts.ptr<double>(), (int)Vw.n_hub, k - 1,
+                                               w.trace.ptr<double>(), flag_table(),
+                                               (const unsigned long long*)pg->flags, G, pg->rank, pg->epoch));
+        } else {
+            k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), Vw.grid, w.hub_ts.ptr<double>(),
+                                                   (int)Vw.n_hub, k - 1, w.trace.ptr<double>());
+        }
         CHEB_CUDA_CHECK(cudaGetLastError());
         ++launches;
         if (!pg) {  // x_{k+1}: every rank's slot -> every rank (in place, equal counts)
@@ -1430,7 +1488,7 @@ void run_solve_dist(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, 
     barrier();
     for (int k = 1; k <= s.M; ++k) {
         d.term(k);
-        barrier();
+        if (!d.fused_tail) barrier();  // (fused: the term's tail kernel was the barrier)
     }
     d.trace_out();
     barrier();
