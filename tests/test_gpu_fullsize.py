@@ -74,3 +74,40 @@ def test_config3_full_size(cheb):
     exact = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, mode=cheb.MODE_BITEXACT))
     assert np.max(np.abs(fast.ranks - exact.ranks)) <= 1e-12
     dg.free()
+
+
+def test_config4_full_size(cheb):
+    """1.05 B CSR entries, int64 row pointers, x larger than L2 (the L2 window path)."""
+    dg, info = _build("c4")
+    assert info["row_ptr_64"] == 1 and info["nnz"] > 1_000_000_000
+    fast = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
+    again = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
+    assert fast.rounds == 39 and np.array_equal(fast.ranks, again.ranks)   # deterministic
+    t = cheb.coefficients(C, 39)
+    n = float(info["n"])
+    partial = t.c0 / 2.0
+    for row in fast.trace:
+        partial += t.coeffs[row.k]
+        assert abs(row.S_k - n * partial) <= n * 1e-12                      # mass ledger
+    assert abs(cheb.kahan_sum(fast.ranks) - 1.0) <= 1e-12
+    p = cheb.run_power(dg, cheb.PowerConfig(rounds=210))                  # independent solver
+    assert np.sum(np.abs(p.ranks - fast.ranks)) <= 1e-9
+    dg.free()
+
+
+def test_config5_full_size(cheb):
+    """Batched R = 64 (K5): every column is a distribution, and columns equal the scalar
+    personalised solves (one-hot T_0) of their seeds."""
+    import bench
+    dg, info = _build("c5")
+    seeds = bench.c5_seeds(dg, 64)
+    res = cheb.run_cpaa_batch(dg, cheb.SolverConfig(eps=1e-10), seeds=seeds)
+    assert res.ranks.shape == (info["n"], 64)
+    sums = res.ranks.sum(axis=0)
+    assert np.max(np.abs(sums - 1.0)) <= 1e-10
+    for r in (0, 37):
+        p = np.zeros(info["n"])
+        p[seeds[r]] = 1.0
+        single = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, personalization=p))
+        assert np.max(np.abs(single.ranks - res.ranks[:, r])) <= 1e-12
+    dg.free()
