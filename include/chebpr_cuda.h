@@ -305,6 +305,11 @@ cheb_status cheb_peer_export(cheb_graph_t g, int G, int rank, void* out, size_t 
 cheb_status cheb_peer_import(cheb_graph_t g, const void* all, size_t bytes_per_rank);
 cheb_status cheb_peer_detach(cheb_graph_t g);
 
+/* Solver-view tile bins of the FAST schedule (for profiling): bin b = 0..5 pack tiles with
+ * 2^b lanes per row, bin 6 chunk tiles of rows above the warp tile; per bin the number of
+ * tiles, rows and CSR entries. */
+cheb_status cheb_graph_view_bins(cheb_graph_t g, int64_t* tiles, int64_t* rows, int64_t* nnz);
+
 #ifdef __cplusplus
 }
 #endif

@@ -879,6 +879,16 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     V.hub_first.alloc(sizeof(int) * hub_first.size());
     h2d_staged(V.hub_first.get(), hub_first.data(), sizeof(int) * hub_first.size(), 0, st);
     V.n_tiles = (int)tiles.size() - 1;
+    for (int b = 0; b < 7; ++b) V.bin_tiles[b] = V.bin_rows[b] = V.bin_nnz[b] = 0;
+    for (int t = 0; t < V.n_tiles; ++t) {
+        const Tile& a = tiles[t];
+        const Tile& b = tiles[t + 1];
+        const int bin = (a.meta & kTileChunk) ? 6 : (a.meta & 0xf);
+        ++V.bin_tiles[bin];
+        V.bin_nnz[bin] += b.nnz_begin - a.nnz_begin;
+        V.bin_rows[bin] += (a.meta & kTileChunk) ? 0 : (int64_t)(b.row_begin - a.row_begin);
+    }
+    V.bin_rows[6] = V.n_hub;
     {
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);

@@ -857,6 +857,19 @@ cheb_status cheb_peer_detach(cheb_graph_t g) {
     });
 }
 
+cheb_status cheb_graph_view_bins(cheb_graph_t g, int64_t* tiles, int64_t* rows, int64_t* nnz) {
+    return guarded([&] {
+        need_graph(g);
+        GraphScope gs(g);
+        ensure_view(g);
+        for (int b = 0; b < 7; ++b) {
+            if (tiles) tiles[b] = g->view.bin_tiles[b];
+            if (rows) rows[b] = g->view.bin_rows[b];
+            if (nnz) nnz[b] = g->view.bin_nnz[b];
+        }
+    });
+}
+
 cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, int64_t* nnz_local,
                                       int64_t* max_rows) {
     return guarded([&] {

@@ -191,6 +191,8 @@ struct SolverView {
     int64_t n_hub = 0;     // rows [0, n_hub) with degree > kWarpNnz (chunk tiles)
     int n_chunk_tiles = 0;
     DevMem hub_first;      // int32 [n_hub + 1]: first chunk tile of each hub row
+    // tile bins (host statistics): 0..5 = pack tiles with 2^b lanes per row, 6 = chunk tiles
+    int64_t bin_tiles[7] = {}, bin_rows[7] = {}, bin_nnz[7] = {};
     void set_stream(cudaStream_t s) {
         for (DevMem* d : {&order, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first}) d->set_stream(s);
     }
@@ -311,7 +313,7 @@ struct GraphScope {
 struct Tuning {
     int hot = -1;       // cap on the shared-memory hot prefix (vertices); -1 = capacity
     int nogather = 0;   // 1: skip the x gathers (timing experiments only; wrong results)
-    int skip = 0;       // bit 0: skip chunk tiles, bit 1: skip pack tiles (experiments only)
+    int skip = 0;       // 1: skip chunk tiles, 2: skip pack tiles, 16+b: only tile bin b (experiments only)
     int l2win = 1;      // 1: persisting-L2 window over the hot prefix of x (default on)
     int pdl = 1;        // 1: programmatic dependent launch along the term chain (default on)
 };

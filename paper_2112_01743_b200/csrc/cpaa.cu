@@ -69,7 +69,7 @@ struct TermArgs {
     unsigned* hub_cnt;
     double* hub_ts;  // [n_hub][2] this term
     int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
-    int tune_skip;      // experiments only: bit 0 skip chunk tiles, bit 1 skip pack tiles
+    int tune_skip;      // experiments only: 1 skip chunk tiles, 2 skip pack tiles, 16+b only bin b
     // fused push exchange (partitioned runs): x_{k+1}[u] is stored at push[r][push_off + u]
     // for every rank r (peer memory over NVLink) instead of x_out[u]
     V* const* push;
@@ -351,7 +351,9 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
     }
     const int t = w + i * S;  // tile id (slot of a hub-row partial)
     mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
-    if (a.tune_skip && ((a.tune_skip & 1) ? (d.meta & kTileChunk) : !(d.meta & kTileChunk))) {
+    if (a.tune_skip &&
+        (a.tune_skip >= 16 ? (((d.meta & kTileChunk) ? 6 : (d.meta & 0xf)) != a.tune_skip - 16)
+                           : ((a.tune_skip & 1) ? (d.meta & kTileChunk) : !(d.meta & kTileChunk)))) {
         __syncwarp();
         if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
             const int blk = i / kDescBlock + 2;
