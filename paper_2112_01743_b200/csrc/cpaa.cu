@@ -890,7 +890,7 @@ Layout layout_of(cheb_graph* g, int mode) {
 }
 
 template <class RP, class V>
-TermArgs<RP, V> base_args(cheb_graph* g, const Layout& L) {
+TermArgs<RP, V> base_args(cheb_graph* /*g*/, const Layout& L) {
     TermArgs<RP, V> a{};
     a.rp = static_cast<const RP*>(L.rp);
     a.col = L.col;
@@ -1081,8 +1081,6 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
         }
         if (d_ref) {
             const int eg = grid1d(n);
-            double* ep = w.part.ptr<double>();  // reuse: partials of this term are consumed
-            (void)ep;
             k_err<V><<<eg, kThreads, 0, st>>>(acc, d_ref, n, trace + 2 * (k - 1) + 1, 1, d_err + 4 * (size_t)M);
             k_err_final<<<1, kThreads, 0, st>>>(d_err + 4 * (size_t)M, eg, d_err + 2 * (size_t)(k - 1));
             CHEB_CUDA_CHECK(cudaGetLastError());
@@ -1388,8 +1386,6 @@ struct DistSolve {
     void trace_out() {
         cudaStream_t st = g->stream;
         Workspace& w = g->ws;
-        double* all = pg ? static_cast<double*>(pg->trace_all) : trace_all.ptr<double>();
-        (void)all;
         if (M == 0) {
             const int eg = grid1d(nl);
             k_sum_blocks<V><<<eg, kThreads, 0, st>>>(acc, nl, w.part.ptr<double>());
