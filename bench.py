@@ -406,6 +406,25 @@ class Solver:
                         ("cheb_cpaa_batch" if R > 1 else "cheb_cpaa") + "(host ranks) + cheb_graph_free"}
 
 
+def lsu_roofline(config, precision, world, mean_launch_us, sm_mhz):
+    """Second roofline for the gather-bound term kernel: L1TEX data-pipe wavefronts per
+    launch (ncu, profiles/traffic.json) over one wavefront per cycle per SM."""
+    if world != 1 or not sm_mhz:
+        return None
+    try:
+        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+            w = json.load(f).get(f"{config}/f{precision}", {}).get("lsu_wavefronts")
+    except (OSError, ValueError):
+        return None
+    if not w:
+        return None
+    peak = 148 * sm_mhz * 1e6  # wavefronts / s
+    floor_us = w / peak * 1e6
+    return {"bound": "l1tex_lsu_wavefronts", "wavefronts_per_launch": w, "peak_wavefronts_per_s": round(peak),
+            "floor_us": round(floor_us, 1), "achieved_us": round(mean_launch_us, 1),
+            "frac": round(floor_us / mean_launch_us, 4)}
+
+
 def measured_traffic(config, precision, world):
     """DRAM bytes per launch of the dominant kernel from the committed ncu capture
     (profiles/traffic.json), or None when this workload has not been captured."""
@@ -548,6 +567,7 @@ def main():
 
     if dist.rank == 0:
         kernel = "k_spmm_term + k_spmm_hub_finalize" if R > 1 else "k_term_warp<EPI_CPAA> + k_hub_finalize"
+        clk_summary = clk.summary()
         line = {
             "metric": "cpaa_gteps_per_term",
             "value": round(value, 3),
@@ -580,7 +600,9 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clk_summary,
+            "lsu_roofline": lsu_roofline(args.config, args.precision, dist.world, mean_term * 1e3,
+                                         clk_summary.get("sm_mhz")),
         }
         print(json.dumps(line))
     dg.free()
