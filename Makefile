@@ -38,7 +38,14 @@ $(LIB_DIR)/libchebpr_dropin.so: $(SRC_DIR)/dropin.cpp $(wildcard include/chebpr/
 
 # The reference's own doctest suites compiled UNCHANGED against the drop-in (test
 # infrastructure; sources read in place from /root/reference, binaries into build/reftests).
-reftests: $(addprefix build/reftests/,$(REFTESTS))
+reftests: $(addprefix build/reftests/,$(REFTESTS)) build/reftests/acceptance_main
+
+# The reference's acceptance gate (9 criteria), unchanged; criterion 7 drives the reference
+# CLI (out of scope), so its CLI path is a stand-in that always fails.
+build/reftests/acceptance_main: $(REFTEST_SRC)/acceptance_main.cpp $(LIB_DIR)/libchebpr_dropin.so tests/cpp/doctest.h
+	@mkdir -p build/reftests
+	g++ -std=c++20 -O2 -Iinclude -Itests/cpp -I$(REFTEST_SRC) '-DCHEBPR_CLI_PATH="/bin/false"' -o $@ $< \
+	    -L$(LIB_DIR) -lchebpr_dropin -lchebpr_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIB_DIR)' 
 
 build/reftests/%: $(REFTEST_SRC)/%.cpp $(LIB_DIR)/libchebpr_dropin.so tests/cpp/doctest.h
 	@mkdir -p build/reftests

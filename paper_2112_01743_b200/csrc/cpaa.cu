@@ -1812,6 +1812,20 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
         if (sizeof(double) * (size_t)(B + 1) * (size_t)n <= free_b / 4)
             snaps.alloc(sizeof(double) * (size_t)(B + 1) * (size_t)n);
     }
+    // per-round kernel time for the trace's elapsed_ms (power.cpp:92: the round's kernel)
+    std::vector<cudaEvent_t> rev(2 * (size_t)std::max(B, 1));
+    for (auto& e : rev) CHEB_CUDA_CHECK(cudaEventCreate(&e));
+    struct EvFree {
+        std::vector<cudaEvent_t>& v;
+        ~EvFree() {
+            for (auto e : v) cudaEventDestroy(e);
+        }
+    } ev_free{rev};
+    auto round_ms = [&](int j) {
+        float ms = 0.f;
+        CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, rev[2 * j], rev[2 * j + 1]));
+        return (double)ms;
+    };
     if (snaps) {
         double* S = snaps.ptr<double>();
         CHEB_CUDA_CHECK(cudaMemcpyAsync(S, X, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
@@ -1836,7 +1850,9 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
                     a.hub_cnt = w.hub_cnt.ptr<unsigned>();
                     a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() : nullptr;
                 }
+                CHEB_CUDA_CHECK(cudaEventRecord(rev[2 * (j - 1)], st));
                 launch_pass<EPI_POWER>(g, L, a);
+                CHEB_CUDA_CHECK(cudaEventRecord(rev[2 * (j - 1) + 1], st));
                 if (L.fast)
                     k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub,
                                                            0, dtr + 2 * (j - 1));
@@ -1858,6 +1874,7 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
                     r.k = kk;
                     r.l1_change = h[2 * (j - 1)];
                     r.mass_T = h[2 * (j - 1) + 1];
+                    r.elapsed_ms = round_ms(j - 1);
                 }
                 if (!std::isfinite(h[2 * (j - 1)])) fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(kk));
                 if (by_tol && h[2 * (j - 1)] < tol) stop = j;
@@ -1892,15 +1909,19 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
             a.hub_cnt = w.hub_cnt.ptr<unsigned>();
             a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() : nullptr;
         }
+        CHEB_CUDA_CHECK(cudaEventRecord(rev[0], st));
         if (!L.fast) {
             // y goes to a separate buffer so the Kahan L1 sees old and new x (power.cpp:80-86)
             a.T = w.acc.ptr<double>();
             CHEB_CUDA_CHECK(cudaMemcpyAsync(a.T, X, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+            CHEB_CUDA_CHECK(cudaEventRecord(rev[0], st));
             launch_pass<EPI_POWER>(g, L, a);
+            CHEB_CUDA_CHECK(cudaEventRecord(rev[1], st));
             k_serial_sums<1><<<1, 256, 0, st>>>(a.T, X, n, dtr);
             CHEB_CUDA_CHECK(cudaMemcpyAsync(X, a.T, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
         } else {
             launch_pass<EPI_POWER>(g, L, a);
+            CHEB_CUDA_CHECK(cudaEventRecord(rev[1], st));
             k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub, 0, dtr);
         }
         CHEB_CUDA_CHECK(cudaGetLastError());
@@ -1920,6 +1941,7 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
             r.k = k;
             r.l1_change = h[0];
             r.mass_T = h[1];
+            r.elapsed_ms = round_ms(0);
             r.err = err2[0];
             r.err_l1 = err2[1];
         }
