@@ -366,3 +366,26 @@ def test_int64_row_pointer_solves(cheb):
         b = cheb.run_cpaa_batch(dg, cheb.SolverConfig(rounds=39), personalization=np.ones((g.n, 2)))
         assert np.max(np.abs(b.ranks[:, 1] - z["cpaa39_ranks"])) <= TOL64
         dg.free()
+
+
+def test_pageable_upload_host_narrowing(cheb):
+    """Pageable (numpy) CSR arrays of >= 2^22 entries take the host-narrowing path (threads
+    narrow int64 -> int32 into a pinned ring while the DMA runs): same device CSR, same
+    solve, and the first out-of-range neighbour reported at its exact entry."""
+    from paper_2112_01743_b200 import generate as Gen
+    e = Gen.chung_lu_edges(1 << 18, 2.1, 2.0, 5000.0, 3_000_000, 21)
+    dg, info = cheb.build_device_graph(e)
+    assert info["nnz"] >= (1 << 22)
+    host = dg.download()
+    up = cheb.upload(host)
+    back = up.download()
+    assert np.array_equal(back.offsets, host.offsets) and np.array_equal(back.neighbors, host.neighbors)
+    a = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+    b = cheb.run_cpaa(up, cheb.SolverConfig(rounds=39))
+    assert np.array_equal(a.ranks, b.ranks)
+    bad = host.neighbors.copy()
+    bad[4_500_001] = host.n
+    bad[4_600_000] = -3
+    g2 = cheb.UndirectedGraph(host.n, host.m, host.offsets, bad, host.degrees, host.inv_degree, host.multi)
+    with pytest.raises(cheb.ValidationError, match="out of range at entry 4500001"):
+        cheb.upload(g2)

@@ -15,12 +15,14 @@ import paper_2112_01743_b200 as cheb  # noqa: E402
 from paper_2112_01743_b200 import _lib as L  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+pageable = len(sys.argv) > 2 and sys.argv[2] == "pageable"  # caller buffers as a C++ user holds them
 lib = L.load()
 dg, info = bench.build_device(bench.CONFIGS[cfg], 0)
 host = dg.download()
-off = torch.from_numpy(host.offsets).pin_memory().numpy()
-nb = torch.from_numpy(host.neighbors).pin_memory().numpy()
-inv = torch.from_numpy(host.inv_degree).pin_memory().numpy()
+pin = (lambda a: a.copy()) if pageable else (lambda a: torch.from_numpy(a).pin_memory().numpy())
+off = pin(host.offsets)
+nb = pin(host.neighbors)
+inv = pin(host.inv_degree)
 ranks = torch.empty(host.n, dtype=torch.float64).pin_memory().numpy()
 o = L.cheb_cpaa_opts()
 lib.cheb_cpaa_opts_default(C.byref(o))
