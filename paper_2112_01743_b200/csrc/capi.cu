@@ -517,6 +517,8 @@ cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double
     });
 }
 
+constexpr int kBatchBlock = 128;  // right-hand sides per SpMM pass (32 lanes x 4 values)
+
 static BatchSpec batch_spec(cheb_graph* g, const cheb_cpaa_opts& o, const int64_t* seeds) {
     need_graph(g);
     single_gpu_only(g);
@@ -551,8 +553,39 @@ cheb_status cheb_cpaa_batch(cheb_graph_t g, const cheb_cpaa_opts* opts, const in
         if (opts) o = *opts;
         BatchSpec b = batch_spec(g, o, seeds);
         std::vector<double> tr, tot;
-        cpaa_batch_solve(g, b, tr, tot, nullptr);
-        if (ranks) read_batch_ranks(g, ranks, b.R);
+        if (b.R <= kBatchBlock) {
+            cpaa_batch_solve(g, b, tr, tot, nullptr);
+            if (ranks) read_batch_ranks(g, ranks, b.R);
+        } else {
+            // more right-hand sides than one SpMM pass carries: column blocks of kBatchBlock,
+            // results scattered into the caller's n x R row-major block, traces summed
+            const int64_t n = g->n;
+            std::vector<double> blk, pblk;
+            tot.assign(b.R, 0.0);
+            for (int c0 = 0; c0 < b.R; c0 += kBatchBlock) {
+                const int Rc = std::min(kBatchBlock, b.R - c0);
+                BatchSpec bc = b;
+                bc.R = Rc;
+                bc.seeds = b.seeds ? b.seeds + c0 : nullptr;
+                if (b.p) {
+                    pblk.resize((size_t)n * Rc);
+                    for (int64_t v = 0; v < n; ++v)
+                        std::memcpy(&pblk[(size_t)v * Rc], b.p + (size_t)v * b.R + c0, sizeof(double) * Rc);
+                    bc.p = pblk.data();
+                }
+                std::vector<double> trc, totc;
+                cpaa_batch_solve(g, bc, trc, totc, nullptr);
+                if (tr.empty()) tr.assign(trc.size(), 0.0);
+                for (size_t i = 0; i < trc.size(); ++i) tr[i] += trc[i];
+                std::memcpy(tot.data() + c0, totc.data(), sizeof(double) * Rc);
+                if (ranks) {
+                    blk.resize((size_t)n * Rc);
+                    read_batch_ranks(g, blk.data(), Rc);
+                    for (int64_t v = 0; v < n; ++v)
+                        std::memcpy(ranks + (size_t)v * b.R + c0, &blk[(size_t)v * Rc], sizeof(double) * Rc);
+                }
+            }
+        }
         if (totals) std::memcpy(totals, tot.data(), sizeof(double) * b.R);
         if (trace && b.M > 0) {
             std::vector<double> co;
