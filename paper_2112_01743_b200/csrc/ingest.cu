@@ -24,7 +24,12 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <fcntl.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cctype>
 #include <charconv>
 #include <cstring>
@@ -429,11 +434,15 @@ std::string line_text(const DeviceText& t, int64_t i, cudaStream_t st) {
 }
 
 // Pinned staging ring for file uploads (process-wide; file reads overlap the H2D copies).
+// Pinned staging ring for file uploads (process-wide): reader threads pread chunks into
+// their own buffers and DMA each as soon as it is read, so file reads, copies and each
+// other overlap.
 struct FileRing {
+    static constexpr int kMaxThreads = 8;
+    static constexpr size_t kChunk = size_t(8) << 20;
     std::mutex mu;
-    static constexpr size_t kChunk = size_t(32) << 20;
-    void* buf[2] = {nullptr, nullptr};
-    cudaEvent_t done[2] = {nullptr, nullptr};
+    void* buf[2 * kMaxThreads] = {};
+    cudaEvent_t done[2 * kMaxThreads] = {};
 };
 FileRing& file_ring() {
     static FileRing* r = new FileRing();  // never destroyed: outlives every handle
@@ -475,22 +484,57 @@ struct Source {
         } else if (bytes > 0) {
             FileRing& R = file_ring();
             std::lock_guard<std::mutex> lk(R.mu);
-            for (int k = 0; k < 2; ++k) {
+            const int64_t chunks = (bytes + (int64_t)FileRing::kChunk - 1) / (int64_t)FileRing::kChunk;
+            const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+            const int T = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)FileRing::kMaxThreads, (int64_t)hw, chunks}));
+            for (int k = 0; k < 2 * T; ++k) {
                 if (!R.buf[k]) CHEB_CUDA_CHECK(cudaHostAlloc(&R.buf[k], FileRing::kChunk, cudaHostAllocPortable));
                 if (!R.done[k]) CHEB_CUDA_CHECK(cudaEventCreateWithFlags(&R.done[k], cudaEventDisableTiming));
             }
-            in->clear();
-            in->seekg(offset);
-            int k = 0;
-            for (int64_t off = 0; off < bytes; off += (int64_t)FileRing::kChunk, k ^= 1) {
-                const int64_t len = std::min<int64_t>((int64_t)FileRing::kChunk, bytes - off);
-                CHEB_CUDA_CHECK(cudaEventSynchronize(R.done[k]));  // this buffer's previous copy is done
-                in->read(static_cast<char*>(R.buf[k]), len);
-                if (in->gcount() != len) fail(CHEB_PARSE, "read failed for " + path);
-                CHEB_CUDA_CHECK(cudaMemcpyAsync(t.text.ptr<char>() + off, R.buf[k], (size_t)len,
-                                                cudaMemcpyHostToDevice, st));
-                CHEB_CUDA_CHECK(cudaEventRecord(R.done[k], st));
-            }
+            const int fd = ::open(path.c_str(), O_RDONLY);
+            if (fd < 0) fail(CHEB_PARSE, "cannot open " + path);
+            std::atomic<int64_t> next{0};
+            std::atomic<bool> failed{false};
+            std::vector<std::string> errs(T);
+            int dev = 0;
+            CHEB_CUDA_CHECK(cudaGetDevice(&dev));
+            char* dst = t.text.ptr<char>();
+            std::vector<std::thread> pool;
+            for (int w = 0; w < T; ++w)
+                pool.emplace_back([&, w] {
+                    try {
+                        CHEB_CUDA_CHECK(cudaSetDevice(dev));
+                        int parity = 0;
+                        for (;;) {
+                            const int64_t c = next.fetch_add(1);
+                            if (c >= chunks || failed.load()) break;
+                            const int k = 2 * w + parity;
+                            parity ^= 1;
+                            CHEB_CUDA_CHECK(cudaEventSynchronize(R.done[k]));  // its previous copy is done
+                            const int64_t off = c * (int64_t)FileRing::kChunk;
+                            const int64_t len = std::min<int64_t>((int64_t)FileRing::kChunk, bytes - off);
+                            int64_t got = 0;
+                            while (got < len) {
+                                const ssize_t r = ::pread(fd, static_cast<char*>(R.buf[k]) + got, (size_t)(len - got),
+                                                          (off_t)(offset + off + got));
+                                if (r <= 0) fail(CHEB_PARSE, "read failed for " + path);
+                                got += r;
+                            }
+                            CHEB_CUDA_CHECK(cudaMemcpyAsync(dst + off, R.buf[k], (size_t)len, cudaMemcpyHostToDevice, st));
+                            CHEB_CUDA_CHECK(cudaEventRecord(R.done[k], st));
+                        }
+                    } catch (const std::exception& e) {
+                        errs[w] = e.what();
+                        failed.store(true);
+                    }
+                });
+            for (auto& th : pool) th.join();
+            ::close(fd);
+            for (int w = 0; w < T; ++w)
+                if (!errs[w].empty()) {
+                    cudaStreamSynchronize(st);
+                    fail(errs[w].rfind("read failed", 0) == 0 ? CHEB_PARSE : CHEB_CUDA, errs[w]);
+                }
         }
         CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     }
