@@ -187,6 +187,19 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsig
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  :: "r"(dst), "l"(gsrc), "r"(bytes), "r"(bar) : "memory");
 }
+// Column ids are read once per term: an L2 evict-first policy on their TMA copies keeps the
+// per-term streams (~130 MB on C2, about the size of L2) from pushing x out of L2
+// (C2 73.2 -> 70.1 us/term; profiles/r01_gather_microbench.md).
+__device__ __forceinline__ void bulk_g2s_stream(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* mbar) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        :: "r"(dst), "l"(gsrc), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* mbar, unsigned count) {
     const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
@@ -291,7 +304,7 @@ __device__ __forceinline__ void issue_cols(const int* __restrict__ col, const Ti
     const int64_t a0 = t.z0 & ~int64_t(7);
     const unsigned bytes = (unsigned)(((t.z0 - a0) + t.cnt + 3) & ~3) * 4u;
     mbar_expect_tx(mbar, bytes);
-    bulk_g2s(buf, col + a0, bytes, mbar);
+    bulk_g2s_stream(buf, col + a0, bytes, mbar);
 }
 
 // Row operands of a pack tile for the lane leading row g's lane group (L = 1 << lg lanes
