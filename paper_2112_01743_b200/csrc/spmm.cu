@@ -36,6 +36,7 @@ struct BatchArgs {
     double* part;      // [grid][2]
     double* hub_part;  // [n_tiles][Rs]
     double* hub_ts;    // [n_hub][2]
+    int hub_rows;      // rows [0, hub_rows) of X are gathered under an L2 evict-last policy
 };
 
 template <class V, int VPL>
@@ -86,6 +87,61 @@ struct VecIO<float, 4> {
     }
 };
 
+// X-row gathers under an explicit L2 policy: the hub prefix of X (the most-gathered rows
+// after the degree relabel, ~64 MB) evict-last, every other row evict-first, so the rows
+// that are reused stay in L2 while the one-off rows and the streams pass through
+// (config 5: 296 -> 282 ms/solve).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+template <class V, int VPL>
+struct PolicyIO;
+template <>
+struct PolicyIO<double, 1> {
+    static __device__ __forceinline__ void ld(const double* p, double (&o)[1], uint64_t pol) {
+        asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(o[0]) : "l"(p), "l"(pol));
+    }
+};
+template <>
+struct PolicyIO<double, 2> {
+    static __device__ __forceinline__ void ld(const double* p, double (&o)[2], uint64_t pol) {
+        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(o[0]), "=d"(o[1]) : "l"(p), "l"(pol));
+    }
+};
+template <>
+struct PolicyIO<double, 4> {
+    static __device__ __forceinline__ void ld(const double* p, double (&o)[4], uint64_t pol) {
+        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(o[0]), "=d"(o[1]) : "l"(p), "l"(pol));
+        asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(o[2]), "=d"(o[3]) : "l"(p + 2), "l"(pol));
+    }
+};
+template <>
+struct PolicyIO<float, 1> {
+    static __device__ __forceinline__ void ld(const float* p, float (&o)[1], uint64_t pol) {
+        asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(o[0]) : "l"(p), "l"(pol));
+    }
+};
+template <>
+struct PolicyIO<float, 2> {
+    static __device__ __forceinline__ void ld(const float* p, float (&o)[2], uint64_t pol) {
+        asm("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(o[0]), "=f"(o[1]) : "l"(p), "l"(pol));
+    }
+};
+template <>
+struct PolicyIO<float, 4> {
+    static __device__ __forceinline__ void ld(const float* p, float (&o)[4], uint64_t pol) {
+        asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+            : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]) : "l"(p), "l"(pol));
+    }
+};
+
 #ifndef CHEB_SPMM_UNROLL
 #define CHEB_SPMM_UNROLL 8
 #endif
@@ -104,6 +160,7 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
     for (int k = 0; k < VPL; ++k) s[k] = V(0);
     const int off = lane * VPL;
     constexpr int U = spmm_unroll<VPL>();
+    const uint64_t p_hub = policy_evict_last(), p_cold = policy_evict_first();
     int64_t j = b;
     for (; j + U - 1 < e; j += U) {
         int c[U];
@@ -112,7 +169,8 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
         if (live) {
             V v[U][VPL];
 #pragma unroll
-            for (int q = 0; q < U; ++q) VecIO<V, VPL>::ld(a.x_in + (int64_t)c[q] * a.Rs + off, v[q]);
+            for (int q = 0; q < U; ++q)
+                PolicyIO<V, VPL>::ld(a.x_in + (int64_t)c[q] * a.Rs + off, v[q], c[q] < a.hub_rows ? p_hub : p_cold);
 #pragma unroll
             for (int q = 0; q < U; ++q)
 #pragma unroll
@@ -123,7 +181,7 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
         const int c0 = __ldg(a.col + j);
         if (live) {
             V v0[VPL];
-            VecIO<V, VPL>::ld(a.x_in + (int64_t)c0 * a.Rs + off, v0);
+            PolicyIO<V, VPL>::ld(a.x_in + (int64_t)c0 * a.Rs + off, v0, c0 < a.hub_rows ? p_hub : p_cold);
 #pragma unroll
             for (int k = 0; k < VPL; ++k) s[k] += v0[k];
         }
@@ -478,6 +536,7 @@ void batch_run(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace, st
         a.first = k == 1;
         a.R = R;
         a.Rs = Rs;
+        a.hub_rows = (int)std::min<int64_t>(g->n, (int64_t(64) << 20) / ((int64_t)Rs * (int64_t)sizeof(V)));
         a.part = w.part.ptr<double>();
         a.hub_part = w.hub_part.ptr<double>();
         a.hub_ts = Vw.n_hub ? w.hub_ts.ptr<double>() : nullptr;
