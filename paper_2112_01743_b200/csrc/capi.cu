@@ -735,8 +735,9 @@ void make_peer(cheb_graph* g, int G, int rank, bool lockstep) {
     CHEB_CUDA_CHECK(cudaMalloc(&pg.X[1], xb));
     CHEB_CUDA_CHECK(cudaMalloc(&pg.rbuf, xb));
     CHEB_CUDA_CHECK(cudaMalloc(&pg.trace_all, sizeof(double) * 2 * (size_t)kMaxPushTerms * G));
-    CHEB_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&pg.flags), sizeof(unsigned long long) * G));
-    CHEB_CUDA_CHECK(cudaMemset(pg.flags, 0, sizeof(unsigned long long) * G));
+    // G epoch slots written by the peers + one timeout flag raised by this rank's waits
+    CHEB_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&pg.flags), sizeof(unsigned long long) * (G + 1)));
+    CHEB_CUDA_CHECK(cudaMemset(pg.flags, 0, sizeof(unsigned long long) * (G + 1)));
     if (lockstep) CHEB_CUDA_CHECK(cudaEventCreateWithFlags(&pg.signalled, cudaEventDisableTiming));
     pg.pX0.assign(G, nullptr);
     pg.pX1.assign(G, nullptr);

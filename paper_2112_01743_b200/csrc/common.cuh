@@ -222,7 +222,7 @@ struct PeerGroup {
     void* X[2] = {nullptr, nullptr};       // padded x_k, x_len * 8 bytes each
     void* trace_all = nullptr;             // [G][2 * kMaxPushTerms] doubles
     void* rbuf = nullptr;                  // padded ranks, x_len * 8 bytes
-    unsigned long long* flags = nullptr;   // [G] barrier epochs written by the peers
+    unsigned long long* flags = nullptr;   // [G] barrier epochs written by the peers, [G] timeout flag
     // every rank's buffers as seen from this device ([rank] = own)
     std::vector<void*> pX0, pX1, ptrace, prbuf, pflags;
     std::vector<void*> opened;             // IPC-opened peer pointers (closed on release)

@@ -1170,6 +1170,24 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Wait for slot r of this rank's flags to reach epoch; give up after 20 s and raise the
+// group's timeout flag (slot G) instead of hanging the GPU if a peer never signals.
+__device__ __forceinline__ void wait_epoch(const unsigned long long* flags, int r, int G, unsigned long long epoch) {
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(flags + r) < epoch) {
+        __nanosleep(100);
+        if (global_ns() - t0 > 20000000000ull) {
+            atomicExch(const_cast<unsigned long long*>(flags) + G, 1ull);
+            return;
+        }
+    }
+}
+
 // This rank reached `epoch`: publish it in slot [rank] of every rank's flag array.  The
 // system-scope fence orders every earlier store of this stream (the term's pushes) before it.
 __global__ void k_peer_signal(unsigned long long* const* flags, int G, int rank, unsigned long long epoch) {
@@ -1184,8 +1202,7 @@ __global__ void k_peer_signal(unsigned long long* const* flags, int G, int rank,
 // visible to every later kernel of this stream).
 __global__ void k_peer_wait(const unsigned long long* flags, int G, unsigned long long epoch) {
     const int r = threadIdx.x;
-    if (r < G)
-        while (ld_acquire_sys(flags + r) < epoch) __nanosleep(100);
+    if (r < G) wait_epoch(flags, r, G, epoch);
     __syncthreads();
 }
 
@@ -1223,8 +1240,7 @@ __global__ void __launch_bounds__(256) k_term_tail(const double* __restrict__ pa
         __threadfence_system();  // the term's pushes (earlier kernels of this stream) first
         st_release_sys(flags[r] + rank, epoch);
     }
-    if (r < G)
-        while (ld_acquire_sys(my_flags + r) < epoch) __nanosleep(100);
+    if (r < G) wait_epoch(my_flags, r, G, epoch);
     __syncthreads();
 }
 
@@ -1451,7 +1467,11 @@ struct DistSolve {
         std::vector<double> t(2 * (size_t)std::max(M, 1));
         CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), tglob.get(), sizeof(double) * (M > 0 ? 2 * M : 1),
                                         cudaMemcpyDeviceToHost, st));
+        unsigned long long timed_out = 0;
+        if (pg)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(&timed_out, pg->flags + G, sizeof timed_out, cudaMemcpyDeviceToHost, st));
         CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (timed_out) fail(CHEB_CUDA, "push exchange barrier timed out (a peer stopped signalling)");
         float ms = 0.f;
         CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
         g->last_loop_ms = ms;

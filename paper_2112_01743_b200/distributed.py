@@ -66,20 +66,32 @@ class PeerExchange:
     barrier per term instead of an NCCL all-gather."""
 
     def __init__(self, dg: DeviceGraph, rank: int, world: int, group=None):
-        import torch.distributed as dist
         lib = L.load()
         mine = (C.c_ubyte * L.PEER_EXPORT_BYTES)()
-        _check(lib.cheb_peer_export(dg.handle, world, rank, mine, L.PEER_EXPORT_BYTES))
-        if world > 1:
-            allb = [None] * world
-            dist.all_gather_object(allb, bytes(mine), group=group)
-        else:
-            allb = [bytes(mine)]
-        buf = (C.c_ubyte * (L.PEER_EXPORT_BYTES * world)).from_buffer_copy(b"".join(allb))
-        _check(lib.cheb_peer_import(dg.handle, buf, L.PEER_EXPORT_BYTES))
-        if world > 1:
-            dist.barrier(group=group)  # every rank mapped every peer before any pushes
+        rc = lib.cheb_peer_export(dg.handle, world, rank, mine, L.PEER_EXPORT_BYTES)
+        err = None if rc == 0 else lib.cheb_last_error().decode()
+        # every rank reaches every collective, even after a local failure, so a failing rank
+        # cannot leave its peers blocked; all ranks then raise (or succeed) together
+        allb = self._all_gather(None if err else bytes(mine), world, group)
+        bad = [r for r, b in enumerate(allb) if b is None]
+        if not bad:
+            buf = (C.c_ubyte * (L.PEER_EXPORT_BYTES * world)).from_buffer_copy(b"".join(allb))
+            rc = lib.cheb_peer_import(dg.handle, buf, L.PEER_EXPORT_BYTES)
+            err = None if rc == 0 else lib.cheb_last_error().decode()
+            bad = [r for r, ok in enumerate(self._all_gather(err is None, world, group)) if not ok]
+        if bad:
+            lib.cheb_peer_detach(dg.handle)
+            raise RuntimeError(f"push exchange unavailable on ranks {bad}" + (f": {err}" if err else ""))
         self.dg, self.rank, self.world = dg, rank, world
+
+    @staticmethod
+    def _all_gather(obj, world, group):
+        if world == 1:
+            return [obj]
+        import torch.distributed as dist
+        out = [None] * world
+        dist.all_gather_object(out, obj, group=group)
+        return out
 
     def detach(self):
         if self.dg is not None and self.dg.handle:

@@ -83,3 +83,77 @@ def test_partition_plan_properties(cheb):
     dd = deg[order]
     g = CSR(deg.size, 0, np.concatenate([[0], np.cumsum(dd)]), np.zeros(int(dd.sum()), np.int64), dd, 1.0 / dd)
     assert np.array_equal(o.partition_vertices(g, 4), cuts)
+
+
+class _FakePeerLib:
+    """Stand-in for libchebpr_b200's peer entry points (the real ones need a GPU): export
+    writes the rank id into its bytes, or fails on `fail_rank`; import records what it got."""
+
+    def __init__(self, rank, fail_rank):
+        self.rank, self.fail_rank, self.imported, self.detached = rank, fail_rank, None, False
+        self._err = b""
+
+    def cheb_peer_export(self, h, world, rank, buf, cap):
+        if rank == self.fail_rank:
+            self._err = b"simulated export failure"
+            return 6
+        for i in range(cap):
+            buf[i] = rank
+        return 0
+
+    def cheb_peer_import(self, h, buf, per):
+        self.imported = bytes(buf)
+        return 0
+
+    def cheb_peer_detach(self, h):
+        self.detached = True
+        return 0
+
+    def cheb_last_error(self):
+        return self._err
+
+
+def _peer_worker(rank, world, port, fail_rank, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2112_01743_b200 import _lib as L
+        from paper_2112_01743_b200 import distributed as D
+        fake = _FakePeerLib(rank, fail_rank)
+        L.load = lambda *a, **k: fake  # noqa: E731
+
+        class _G:
+            handle = None
+        try:
+            D.PeerExchange(_G(), rank, world)
+            q.put((rank, "ok", fake.imported, fake.detached))
+        except RuntimeError as e:
+            q.put((rank, str(e), None, fake.detached))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail_rank", [-1, 1])
+def test_peer_exchange_host_protocol(fail_rank):
+    """The IPC-handle exchange of the push path over a world-size-2 gloo group: every rank
+    imports every rank's export bytes in rank order; a failure on one rank makes every
+    rank raise (none is left blocked in a collective) and detach."""
+    from paper_2112_01743_b200 import _lib as L
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, fail_rank, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    if fail_rank < 0:
+        for rank, status, imported, detached in out:
+            assert status == "ok" and not detached
+            assert imported == bytes([0]) * L.PEER_EXPORT_BYTES + bytes([1]) * L.PEER_EXPORT_BYTES
+    else:
+        for rank, status, imported, detached in out:
+            assert "unavailable on ranks [1]" in status and detached
