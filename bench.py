@@ -399,6 +399,8 @@ class Solver:
             t = time.perf_counter()
             step()
             times.append(time.perf_counter() - t)
+        if os.environ.get("CHEB_BENCH_VERBOSE"):
+            log("e2e steps (ms): " + " ".join(f"{1e3 * t:.2f}" for t in times))
         e2e_s = dist.max(statistics.mean(times))
         units = self.info["nnz"] * self.R * self.M
         return {"value": round(units / e2e_s / 1e9, 4), "unit": "GTEPS",

@@ -1787,16 +1787,22 @@ void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_m
 }
 
 // Read back ranks (original vertex order) as doubles.
+__global__ void k_widen_f32(const float* __restrict__ in, int64_t n, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (double)in[i];
+}
+
 void read_ranks(cheb_graph* g, int precision, double* ranks) {
     GraphScope gs(g);
     const int64_t n = g->n;
     if (precision == CHEB_FP64) {
         CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, g->ws.out.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream));
-    } else {
-        std::vector<float> tmp(n);
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), g->ws.out.get(), sizeof(float) * n, cudaMemcpyDeviceToHost, g->stream));
+    } else {  // fp32 ranks widened on the device, then one copy into the caller's buffer
+        DevMem wide(sizeof(double) * (size_t)std::max<int64_t>(n, 1));
+        k_widen_f32<<<grid1d(n), kThreads, 0, g->stream>>>(g->ws.out.ptr<float>(), n, wide.ptr<double>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, wide.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream));
         CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
-        for (int64_t i = 0; i < n; ++i) ranks[i] = tmp[i];
     }
     CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
 }

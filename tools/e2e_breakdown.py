@@ -15,7 +15,8 @@ import paper_2112_01743_b200 as cheb  # noqa: E402
 from paper_2112_01743_b200 import _lib as L  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-pageable = len(sys.argv) > 2 and sys.argv[2] == "pageable"  # caller buffers as a C++ user holds them
+pageable = "pageable" in sys.argv[2:]  # caller buffers as a C++ user holds them
+fp32 = "fp32" in sys.argv[2:]
 lib = L.load()
 dg, info = bench.build_device(bench.CONFIGS[cfg], 0)
 host = dg.download()
@@ -27,6 +28,8 @@ ranks = torch.empty(host.n, dtype=torch.float64).pin_memory().numpy()
 o = L.cheb_cpaa_opts()
 lib.cheb_cpaa_opts_default(C.byref(o))
 o.eps = 1e-10
+if fp32:
+    o.precision = 32
 tr = (L.cheb_trace_row * 64)()
 rounds, tot = C.c_int(), C.c_double()
 for it in range(4):
