@@ -1045,7 +1045,10 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         int dev = 0, l2 = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-        const bool sort_rows = (int64_t)V.x_len * 8 > (int64_t)l2 && nnz_l > 0 && nnz_l < INT32_MAX;
+        const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2 || g->want_sorted_rows)
+                                                 : tuning().sortrows > 0;
+        const bool sort_rows = big_x && nnz_l > 0 && nnz_l < INT32_MAX;
+        V.sorted_rows = sort_rows;
         if (sort_rows) {
             DevMem alt(sizeof(int) * (size_t)nnz_l + 64);
             cub::DoubleBuffer<int> db(V.col.ptr<int>(), alt.ptr<int>());

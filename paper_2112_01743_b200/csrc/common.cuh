@@ -191,6 +191,7 @@ struct SolverView {
     int64_t n_hub = 0;     // rows [0, n_hub) with degree > kWarpNnz (chunk tiles)
     int n_chunk_tiles = 0;
     DevMem hub_first;      // int32 [n_hub + 1]: first chunk tile of each hub row
+    bool sorted_rows = false;  // rows hold their renamed ids in ascending order
     // tile bins (host statistics): 0..5 = pack tiles with 2^b lanes per row, 6 = chunk tiles
     int64_t bin_tiles[7] = {}, bin_rows[7] = {}, bin_nnz[7] = {};
     void set_stream(cudaStream_t s) {
@@ -296,6 +297,7 @@ struct cheb_graph {
     chebgpu::BatchWorkspace bws;
     chebgpu::Partition part;
     chebgpu::PeerGroup* peer = nullptr;  // fused push exchange (instead of part.comm)
+    bool want_sorted_rows = false;       // a batched solve asked for ascending-id view rows
     double last_loop_ms = 0.0;
     int last_terms = 0;
     int last_launches = 0;
@@ -316,6 +318,7 @@ struct Tuning {
     int skip = 0;       // 1: skip chunk tiles, 2: skip pack tiles, 16+b: only tile bin b (experiments only)
     int l2win = 1;      // 1: persisting-L2 window over the hot prefix of x (default on)
     int pdl = 1;        // 1: programmatic dependent launch along the term chain (default on)
+    int sortrows = -1;  // view rows in ascending id order: -1 when x exceeds L2, 0 never, 1 always
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -325,6 +328,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_SKIP")) x.skip = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_L2WIN")) x.l2win = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_PDL")) x.pdl = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_SORTROWS")) x.sortrows = std::atoi(e);
         return x;
     }();
     return t;
