@@ -7,7 +7,7 @@ NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-ffp-contract=off
 SRC_DIR   := paper_2112_01743_b200/csrc
 LIB_DIR   := paper_2112_01743_b200/lib
 OBJ_DIR   := build/obj
-SRCS      := $(SRC_DIR)/build.cu $(SRC_DIR)/cpaa.cu $(SRC_DIR)/capi.cu $(SRC_DIR)/generate.cu $(SRC_DIR)/spmm.cu $(SRC_DIR)/ingest.cu $(SRC_DIR)/coeffs.cpp
+SRCS      := $(SRC_DIR)/build.cu $(SRC_DIR)/cpaa.cu $(SRC_DIR)/capi.cu $(SRC_DIR)/generate.cu $(SRC_DIR)/spmm.cu $(SRC_DIR)/ingest.cu $(SRC_DIR)/validate.cu $(SRC_DIR)/coeffs.cpp
 OBJS      := $(patsubst $(SRC_DIR)/%,$(OBJ_DIR)/%.o,$(SRCS))
 REFTEST_SRC ?= /root/reference/proj/tests
 REFTESTS    := test_coefficients test_graph test_cpaa test_power test_metrics

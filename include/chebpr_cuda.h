@@ -140,6 +140,14 @@ cheb_status cheb_graph_load_matrix_market(const char* path, const cheb_load_opts
  * for the path in messages. */
 cheb_status cheb_graph_parse_text(const char* text, int64_t bytes, int format, const char* name,
                                   const cheb_load_opts* opts, cheb_graph_t* out, cheb_graph_stats* stats);
+/* validate (graph.cpp:123-186) of a HOST CSR, run on the device: the reference's checks in
+ * its order (shape, then per vertex: monotone offsets, degree, isolated, neighbour range,
+ * sortedness, duplicates unless multi; entry counts; symmetry) with its messages naming the
+ * first failing vertex; on success the GraphStats. */
+cheb_status cheb_validate_csr(const int64_t* offsets, int64_t n_offsets, const int64_t* neighbors, int64_t nnz,
+                              const int64_t* degrees, int64_t n_degrees, int64_t n, int64_t m, int multi,
+                              int64_t duplicates_removed, int64_t isolated_dropped, int device,
+                              cheb_graph_stats* stats);
 /* validate (graph.cpp:123-186) statistics of a device graph built by K1 (whose invariants
  * hold by construction): n, m, avg/min/max degree, self loops, builder counts. */
 cheb_status cheb_graph_validate_stats(cheb_graph_t g, cheb_graph_stats* stats);

@@ -92,6 +92,8 @@ _SIGS = {
     "cheb_graph_parse_text": (C.c_int, [C.c_char_p, C.c_int64, C.c_int, C.c_char_p, C.POINTER(cheb_load_opts),
                                         C.POINTER(C.c_void_p), C.POINTER(cheb_graph_stats)]),
     "cheb_graph_validate_stats": (C.c_int, [C.c_void_p, C.POINTER(cheb_graph_stats)]),
+    "cheb_validate_csr": (C.c_int, [I64P, C.c_int64, I64P, C.c_int64, I64P, C.c_int64, C.c_int64, C.c_int64,
+                                    C.c_int, C.c_int64, C.c_int64, C.c_int, C.POINTER(cheb_graph_stats)]),
     "cheb_graph_get_info": (C.c_int, [C.c_void_p, C.POINTER(cheb_graph_info)]),
     "cheb_graph_free": (None, [C.c_void_p]),
     "cheb_partition_vertices": (C.c_int, [I64P, C.c_int64, C.c_int, I64P]),

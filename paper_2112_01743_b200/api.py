@@ -384,73 +384,20 @@ def kahan_sum(x) -> float:
 
 
 def validate(g: UndirectedGraph, duplicates_removed: int = 0, isolated_dropped: int = 0) -> GraphStats:
-    """graph.hpp:70-71 — structural re-check (graph.cpp:123-186), vectorised on the host."""
+    """graph.hpp:70-71 — structural re-check (graph.cpp:123-186) run on the device
+    (cheb_validate_csr): the reference's check order and messages, first violation by vertex."""
     n = int(g.n)
     if n < 0:
         raise ValidationError("negative vertex count")
-    off = np.asarray(g.offsets, dtype=np.int64)
-    deg = np.asarray(g.degrees, dtype=np.int64)
-    nb = np.asarray(g.neighbors, dtype=np.int64)
+    off, nb, deg = _i64(g.offsets), _i64(g.neighbors), _i64(g.degrees)
     if off.size != n + 1:
         raise ValidationError("offsets length is not n+1")
-    if off[0] != 0:
-        raise ValidationError("offsets must start at 0")
-    if deg.size != n:
-        raise ValidationError("degrees length is not n")
-    st = GraphStats(n=n, m=int(g.m), duplicates_removed=duplicates_removed,
-                    isolated_dropped=isolated_dropped)
-    d = np.diff(off)
-    bad = np.nonzero(d < 0)[0]
-    first_bad = {}
-    if bad.size:
-        first_bad[int(bad[0])] = f"offsets not monotone at vertex {int(bad[0])}"
-    mism = np.nonzero(d != deg)[0]
-    if mism.size:
-        first_bad.setdefault(int(mism[0]), f"degree mismatch at vertex {int(mism[0])}")
-    iso = np.nonzero(d < 1)[0]
-    if iso.size:
-        first_bad.setdefault(int(iso[0]), f"vertex {int(iso[0])} is isolated (degree 0)")
-    # per-row checks happen vertex by vertex in the reference; report the lowest vertex
-    if not first_bad and nb.size >= int(off[-1]) and n > 0:
-        rows = np.repeat(np.arange(n, dtype=np.int64), d)
-        w = nb[: int(off[-1])]
-        oor = np.nonzero((w < 0) | (w >= n))[0]
-        if oor.size:
-            first_bad[int(rows[oor[0]])] = f"neighbor id out of range at vertex {int(rows[oor[0]])}"
-        same_row = np.zeros(w.size, dtype=bool)
-        if w.size > 1:
-            same_row[1:] = rows[1:] == rows[:-1]
-            dec = np.nonzero(same_row[1:] & (w[1:] < w[:-1]))[0]
-            if dec.size:
-                v = int(rows[dec[0] + 1])
-                first_bad.setdefault(v, f"neighbor list not sorted at vertex {v}")
-            if not g.multi:
-                dup = np.nonzero(same_row[1:] & (w[1:] == w[:-1]))[0]
-                if dup.size:
-                    v = int(rows[dup[0] + 1])
-                    first_bad.setdefault(v, f"duplicate neighbor at vertex {v}")
-    if first_bad:
-        raise ValidationError(first_bad[min(first_bad)])
-    st.min_degree = int(deg.min()) if n else 0
-    st.max_degree = int(deg.max()) if n else 0
-    entries = int(d.sum())
-    if entries != nb.size:
-        raise ValidationError("neighbors length inconsistent with offsets")
-    rows = np.repeat(np.arange(n, dtype=np.int64), d)
-    st.self_loops = int(np.count_nonzero(nb == rows))
-    if entries != 2 * int(g.m) - st.self_loops:
-        raise ValidationError("edge count inconsistent with adjacency entries")
-    # symmetry: v in N(u) iff u in N(v)  (multiset compare of (u,v) and (v,u))
-    a = rows * max(n, 1) + nb
-    b = nb * max(n, 1) + rows
-    if not np.array_equal(np.sort(a), np.sort(b)):
-        bs = set(b.tolist()) if a.size < 2_000_000 else None
-        for u, v, key in zip(rows.tolist(), nb.tolist(), a.tolist()):
-            if bs is not None and key not in bs:
-                raise ValidationError(f"adjacency not symmetric: {v} in N({u}) but not conversely")
-        raise ValidationError("adjacency not symmetric")
-    st.avg_degree = float(g.m) / float(n) if n > 0 else 0.0
-    return st
+    st = L.cheb_graph_stats()
+    _check(_lib().cheb_validate_csr(_pi(off), off.size, _pi(nb), nb.size, _pi(deg), deg.size, n, int(g.m),
+                                    int(bool(g.multi)), int(duplicates_removed), int(isolated_dropped), 0,
+                                    C.byref(st)))
+    return GraphStats(st.n, st.m, st.avg_degree, st.min_degree, st.max_degree, st.self_loops,
+                      st.duplicates_removed, st.isolated_dropped)
 
 
 # ---------------------------------------------------------------------------

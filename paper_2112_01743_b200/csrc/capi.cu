@@ -343,6 +343,21 @@ cheb_status cheb_graph_parse_text(const char* text, int64_t bytes, int format, c
     return load_common(name ? name : "<memory>", text ? text : &empty, bytes, format, opts, out, stats);
 }
 
+cheb_status cheb_validate_csr(const int64_t* offsets, int64_t n_offsets, const int64_t* neighbors, int64_t nnz,
+                              const int64_t* degrees, int64_t n_degrees, int64_t n, int64_t m, int multi,
+                              int64_t duplicates_removed, int64_t isolated_dropped, int device,
+                              cheb_graph_stats* stats) {
+    return guarded([&] {
+        if (!offsets || n_offsets < 1) fail(CHEB_VALIDATION, "offsets length is not n+1");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+            fail(CHEB_CUDA, "no CUDA device available (libchebpr_b200 has no CPU fallback)");
+        cheb_graph_stats local;
+        validate_csr(offsets, n_offsets, neighbors, nnz, degrees, n_degrees, n, m, multi, duplicates_removed,
+                     isolated_dropped, device, stats ? stats : &local);
+    });
+}
+
 cheb_status cheb_graph_validate_stats(cheb_graph_t g, cheb_graph_stats* stats) {
     return guarded([&] {
         need_graph(g);

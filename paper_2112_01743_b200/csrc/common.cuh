@@ -348,6 +348,10 @@ void finalize_stats(cheb_graph* g);
 void load_graph_text(cheb_graph* g, const std::string& path, const char* mem, int64_t mem_bytes, int format,
                      const cheb_load_opts& o, int64_t* lines, int* weights_ignored);
 int64_t count_self_loops(cheb_graph* g);
+// validate.cu
+void validate_csr(const int64_t* offsets, int64_t n_off, const int64_t* neighbors, int64_t nnz,
+                  const int64_t* degrees, int64_t n_deg, int64_t n, int64_t m, int multi, int64_t dup_removed,
+                  int64_t iso_dropped, int device, cheb_graph_stats* st);
 
 // host: partition_vertices rule (cpaa.cpp:40-68) over a degree sequence
 void partition_cuts(const int64_t* degrees, int64_t n, int K, int64_t* cuts);

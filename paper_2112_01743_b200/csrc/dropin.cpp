@@ -238,50 +238,22 @@ Vector transition_apply(const UndirectedGraph& g, const Vector& x) {
 }
 
 GraphStats validate(const UndirectedGraph& g, int64_t duplicates_removed, int64_t isolated_dropped) {
-    // every structural invariant of graph.hpp, first violation by vertex
+    // graph.cpp:123-186 on the device (cheb_validate_csr): same check order and messages
     if (g.n < 0) throw ValidationError("negative vertex count");
     if (g.offsets.size() != static_cast<size_t>(g.n) + 1) throw ValidationError("offsets length is not n+1");
-    if (g.offsets[0] != 0) throw ValidationError("offsets must start at 0");
-    if (g.degrees.size() != static_cast<size_t>(g.n)) throw ValidationError("degrees length is not n");
+    cheb_graph_stats s;
+    check(cheb_validate_csr(g.offsets.data(), (int64_t)g.offsets.size(), g.neighbors.data(),
+                            (int64_t)g.neighbors.size(), g.degrees.data(), (int64_t)g.degrees.size(), g.n, g.m,
+                            g.multi ? 1 : 0, duplicates_removed, isolated_dropped, 0, &s));
     GraphStats st;
-    st.n = g.n;
-    st.m = g.m;
-    st.duplicates_removed = duplicates_removed;
-    st.isolated_dropped = isolated_dropped;
-    st.min_degree = g.n > 0 ? g.degrees[0] : 0;
-    int64_t entries = 0;
-    for (int64_t v = 0; v < g.n; ++v) {
-        const int64_t b = g.offsets[v], e = g.offsets[v + 1];
-        const std::string at = std::to_string(v);
-        if (e < b) throw ValidationError("offsets not monotone at vertex " + at);
-        const int64_t d = e - b;
-        if (d != g.degrees[v]) throw ValidationError("degree mismatch at vertex " + at);
-        if (d < 1) throw ValidationError("vertex " + at + " is isolated (degree 0)");
-        st.min_degree = std::min(st.min_degree, d);
-        st.max_degree = std::max(st.max_degree, d);
-        entries += d;
-        for (int64_t i = b; i < e; ++i) {
-            if (i >= (int64_t)g.neighbors.size())
-                throw ValidationError("neighbors length inconsistent with offsets");
-            const int64_t w = g.neighbors[i];
-            if (w < 0 || w >= g.n) throw ValidationError("neighbor id out of range at vertex " + at);
-            if (i > b) {
-                if (w < g.neighbors[i - 1]) throw ValidationError("neighbor list not sorted at vertex " + at);
-                if (!g.multi && w == g.neighbors[i - 1]) throw ValidationError("duplicate neighbor at vertex " + at);
-            }
-            if (w == v) ++st.self_loops;
-        }
-    }
-    if (entries != (int64_t)g.neighbors.size()) throw ValidationError("neighbors length inconsistent with offsets");
-    if (entries != 2 * g.m - st.self_loops) throw ValidationError("edge count inconsistent with adjacency entries");
-    for (int64_t u = 0; u < g.n; ++u)
-        for (int64_t i = g.offsets[u]; i < g.offsets[u + 1]; ++i) {
-            const int64_t v = g.neighbors[i];
-            if (!std::binary_search(g.neighbors.begin() + g.offsets[v], g.neighbors.begin() + g.offsets[v + 1], u))
-                throw ValidationError("adjacency not symmetric: " + std::to_string(v) + " in N(" +
-                                      std::to_string(u) + ") but not conversely");
-        }
-    st.avg_degree = g.n > 0 ? static_cast<double>(g.m) / static_cast<double>(g.n) : 0.0;
+    st.n = s.n;
+    st.m = s.m;
+    st.avg_degree = s.avg_degree;
+    st.min_degree = s.min_degree;
+    st.max_degree = s.max_degree;
+    st.self_loops = s.self_loops;
+    st.duplicates_removed = s.duplicates_removed;
+    st.isolated_dropped = s.isolated_dropped;
     return st;
 }
 

@@ -407,3 +407,50 @@ def test_batched_more_than_one_block(cheb):
         p[seeds[r]] = 1.0
         one = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39, personalization=p))
         assert np.max(np.abs(one.ranks - big.ranks[:, r])) <= 1e-12
+
+
+def test_device_validate_matches_reference(cheb, reference):
+    """cheb_validate_csr (graph.cpp:123-186 on the device) against the reference's own
+    validate on randomly corrupted CSRs: the same first error message, or the same stats.
+    Corruptions keep every row inside the neighbour array (the reference would read out of
+    bounds otherwise)."""
+    from oracle import CSR, OracleError
+    rng = np.random.default_rng(17)
+    checked = 0
+    for name in ("config1", "gnp500", "selfloop", "multi", "star100"):
+        z = load_golden(name)
+        multi = name == "multi"
+        base = CSR(int(z["n"]), int(z["m"]), z["offsets"].copy(), z["neighbors"].copy(), z["degrees"].copy(),
+                   1.0 / z["degrees"].astype(np.float64), 0, 0, multi)
+        for trial in range(40):
+            off, nb, deg, m = base.offsets.copy(), base.neighbors.copy(), base.degrees.copy(), base.m
+            kind = trial % 6
+            i = int(rng.integers(0, nb.size))
+            v = int(rng.integers(0, base.n))
+            if kind == 0:
+                nb[i] = int(rng.integers(-2, base.n + 2))          # range / order / duplicate / symmetry
+            elif kind == 1 and nb.size > 1:
+                j = int(rng.integers(0, nb.size))
+                nb[i], nb[j] = nb[j], nb[i]                         # order / symmetry
+            elif kind == 2:
+                deg[v] += int(rng.choice([-1, 1]))                  # degree mismatch
+            elif kind == 3:
+                m += int(rng.choice([-1, 1]))                       # edge count
+            elif kind == 4 and 0 < v < base.n:
+                off[v] = off[v + 1] + 1 if off[v + 1] + 1 <= nb.size else off[v]   # non-monotone, in bounds
+            elif kind == 5 and 0 < v < base.n:
+                off[v] = off[v - 1]                                 # empty row -> isolated / degree
+            g = CSR(base.n, m, off, nb, deg, base.inv_degree, 0, 0, multi)
+            try:
+                want = ("ok", reference.graph_from_csr(g).validate())
+            except OracleError as e:
+                want = ("error", e.msg)
+            try:
+                st = cheb.validate(cheb.UndirectedGraph(g.n, g.m, off, nb, deg, base.inv_degree, multi))
+                got = ("ok", dict(n=st.n, m=st.m, min_degree=st.min_degree, max_degree=st.max_degree,
+                                  self_loops=st.self_loops))
+            except cheb.ValidationError as e:
+                got = ("error", str(e))
+            assert got == want, (name, trial, kind, got, want)
+            checked += 1
+    assert checked == 200

@@ -131,8 +131,9 @@ def test_config_generators_deterministic():
     assert deg.min() >= 1  # isolated vertices rewired: n is kept
 
 
+@pytest.mark.gpu
 def test_validate_rejects_corruption(cheb, oracle):
-    # test_graph.cpp:135-165
+    # test_graph.cpp:135-165 (validate runs on the device: cheb_validate_csr)
     g = oracle.build_graph([[0, 1], [1, 2]])
     G = cheb.UndirectedGraph(g.n, g.m, g.offsets, g.neighbors, g.degrees, g.inv_degree)
     st = cheb.validate(G)

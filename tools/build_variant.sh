@@ -12,7 +12,7 @@ for f in cpaa spmm build capi; do
   nvcc $NVFLAGS $flags -c paper_2112_01743_b200/csrc/$f.cu -o build/variants/obj/$name/$f.o &
 done
 wait
-objs="build/obj/generate.cu.o build/obj/ingest.cu.o build/obj/coeffs.cpp.o"
+objs="build/obj/generate.cu.o build/obj/ingest.cu.o build/obj/validate.cu.o build/obj/coeffs.cpp.o"
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/$name.so $objs \
      build/variants/obj/$name/*.o -lcudart $(make -s -f Makefile print-ldnccl 2>/dev/null || echo -lnccl)
 echo "built build/variants/$name.so"
