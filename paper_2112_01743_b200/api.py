@@ -524,7 +524,8 @@ class PartitionGroup:
 
     def run_cpaa(self, cfg: Optional[SolverConfig] = None) -> PageRankResult:
         cfg = cfg or SolverConfig()
-        o = _cpaa_opts(cfg, None)
+        p = None if cfg.personalization is None else _f64(cfg.personalization)
+        o = _cpaa_opts(cfg, p)
         cap = max(cfg.max_rounds, cfg.rounds, 1) + 1
         tr = (L.cheb_trace_row * cap)()
         ranks = np.zeros(self.n)

@@ -113,3 +113,18 @@ def test_push_group_more_ranks_than_work(cheb, name, G):
     assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
     assert np.max(np.abs(res.ranks - z["cpaa39_ranks"])) <= TOL64
     grp.close()
+
+
+def test_push_group_personalised(cheb):
+    """A personalisation vector (T_0 = p) on a partitioned solve: the ranks index p by the
+    original vertex id through their slice of the view order."""
+    z = load_golden("gnp2000")
+    rng = np.random.default_rng(4)
+    p = rng.random(int(z["n"]))
+    single = cheb.run_cpaa(cheb.build_device_graph(z["edges"])[0],
+                           cheb.SolverConfig(rounds=39, personalization=p))
+    for G in (2, 3):
+        grp = cheb.PartitionGroup(_handles(cheb, z["edges"], G))
+        res = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=39, personalization=p))
+        assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
+        grp.close()
