@@ -7,11 +7,11 @@ NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-ffp-contract=off
 SRC_DIR   := paper_2112_01743_b200/csrc
 LIB_DIR   := paper_2112_01743_b200/lib
 OBJ_DIR   := build/obj
-SRCS      := $(SRC_DIR)/build.cu $(SRC_DIR)/cpaa.cu $(SRC_DIR)/capi.cu $(SRC_DIR)/generate.cu $(SRC_DIR)/spmm.cu $(SRC_DIR)/ingest.cu $(SRC_DIR)/validate.cu $(SRC_DIR)/coeffs.cpp
+SRCS      := $(SRC_DIR)/build.cu $(SRC_DIR)/cpaa.cu $(SRC_DIR)/dist.cu $(SRC_DIR)/power.cu $(SRC_DIR)/capi.cu $(SRC_DIR)/generate.cu $(SRC_DIR)/spmm.cu $(SRC_DIR)/ingest.cu $(SRC_DIR)/validate.cu $(SRC_DIR)/coeffs.cpp
 OBJS      := $(patsubst $(SRC_DIR)/%,$(OBJ_DIR)/%.o,$(SRCS))
 REFTEST_SRC ?= /root/reference/proj/tests
 REFTESTS    := test_coefficients test_graph test_cpaa test_power test_metrics
-HDRS      := $(SRC_DIR)/common.cuh $(SRC_DIR)/device.cuh include/chebpr_cuda.h
+HDRS      := $(SRC_DIR)/common.cuh $(SRC_DIR)/device.cuh $(SRC_DIR)/term.cuh include/chebpr_cuda.h
 # NCCL: the copy torch ships (nvidia-nccl wheel), so that this library and torch resolve
 # libnccl.so.2 to the same build whichever is loaded first; the system one otherwise.
 NCCL_LIB  := $(shell python -c "import nvidia.nccl, os; print(os.path.join(list(nvidia.nccl.__path__)[0], 'lib'))" 2>/dev/null)

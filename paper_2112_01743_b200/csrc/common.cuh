@@ -394,6 +394,8 @@ void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std:
                     std::vector<double>* errs, double* total);
 void read_ranks(cheb_graph* g, int precision, double* ranks);
 void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr, double* total);
+void dist_solve(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, double* total,
+                std::vector<double>* term_ms);  // dist.cu: one rank of a partitioned solve
 void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_ms);
 void power_solve(cheb_graph* g, double c, int rounds, double tol, int max_rounds, int mode,
                  const double* reference, double* ranks, cheb_trace_row* trace, int cap,

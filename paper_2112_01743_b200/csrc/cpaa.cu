@@ -1,1037 +1,12 @@
-// K2/K3/K4/K6/K7 — the CPAA term kernels and their drivers.
-//
-// The reference round (/root/reference/proj/src/cpaa.cpp:109-156) is a pre-scale
-// pass contrib = T_k * D^-1 (:116), a CSR gather with the three-term recurrence
-// T_{k+1} = (k==1 ? s : 2s - T_{k-1}) and the coefficient accumulation
-// acc += c_k T_{k+1} (:126-132), two serial Kahan trace sums (:142-143) and a
-// finite check (:147-148).  Here ONE kernel per term does all of it:
-//
-//   s_u      = sum_{v in N(u)} x_k[v]                (degree-binned gather)
-//   t        = first ? s_u : 2 s_u - T_{k-1}[u]      (recurrence, in place over T_{k-1})
-//   acc[u]  += c_k * t                               (separate mul/add: reference rounding)
-//   x_{k+1}[u] = t * (1/deg u)                       (next term's D^-1 pre-scale, fused)
-//   block partials of sum(t), sum(acc)               (trace, fixed order, deterministic)
-//
-// Two schedules:
-//  * FAST (the product path): rows relabelled by degree (descending) so every bin is
-//    a contiguous row range; vector-per-row (1..16 lanes), warp-per-row (32 lanes,
-//    unrolled), block-per-row, and hub rows split in chunks combined by the last
-//    arriving CTA in fixed chunk order.  Sums differ from the reference only in
-//    association order (<= 1e-12 max-abs, checked by tests).
-//  * BITEXACT: thread-per-row storage-order sums on the reference-order CSR, explicit
-//    round-to-nearest mul/add, serial device Kahan for the trace: bitwise equal to
-//    the reference (ranks and trace).
-#include <cub/cub.cuh>
-
-#include <algorithm>
-#include <cmath>
-#include <cstring>
-#include <string>
-
-#include <nccl.h>
-
-#include "common.cuh"
-#include "device.cuh"
-
-#define CHEB_NCCL_CHECK(expr)                                                              \
-    do {                                                                                   \
-        ncclResult_t _r = (expr);                                                          \
-        if (_r != ncclSuccess)                                                             \
-            ::chebgpu::fail(CHEB_NCCL, std::string("NCCL error ") + ncclGetErrorString(_r) + \
-                                           " at " __FILE__ ":" + std::to_string(__LINE__)); \
-    } while (0)
+// K2/K3/K4 single-GPU solve driver (run_cpaa, cpaa.cpp:79-165): init, M fused terms, trace
+// reduction and normalisation enqueued on the handle's stream and replayed as one CUDA
+// graph per configuration; reference tracking; per-term profiling; ranks read-back.
+// Partitioned handles go to dist.cu.
+#include "term.cuh"
 
 namespace chebgpu {
-
-enum Epi : int {
-    EPI_CPAA = 0,   // fused CPAA term (cpaa.cpp:126-132 + :116 for the next round)
-    EPI_GEN = 1,    // staged generate_stage (cpaa.cpp:178-190): T_next only
-    EPI_POWER = 2,  // power round (power.cpp:60-86): y = c s + base
-    EPI_PLAIN = 3   // transition_apply (graph.cpp:104-121): y = s
-};
-
-template <class RP, class V>
-struct TermArgs {
-    const RP* __restrict__ rp;
-    const int* __restrict__ col;
-    const double* __restrict__ inv;  // non-null iff non-canonical inv_degree
-    const V* __restrict__ x_in;      // x_k = T_k D^-1
-    V* __restrict__ x_out;           // x_{k+1}
-    V* T;                            // CPAA: T_{k-1} in, T_{k+1} out (in place); POWER: x in/out
-    const V* T_prev;                 // GEN: T_{k-1}
-    V* out;                          // GEN: T_next; PLAIN: y
-    V* acc;
-    double ck;    // CPAA: c_k ; POWER: c
-    double base;  // POWER: (1-c)/n
-    int first;
-    double* part;  // [grid][2] this term
-    double* hub_part;  // [n_tiles] chunk partials
-    unsigned* hub_cnt;
-    double* hub_ts;  // [n_hub][2] this term
-    int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
-    int tune_skip;      // experiments only: 1 skip chunk tiles, 2 skip pack tiles, 16+b only bin b
-    // fused push exchange (partitioned runs): x_{k+1}[u] is stored at push[r][push_off + u]
-    // for every rank r (peer memory over NVLink) instead of x_out[u]
-    V* const* push;
-    int push_n;
-    int64_t push_off;
-};
-
-// Row epilogue.  u is a row of the current layout; deg its row length.
-template <int EPI, class RP, class V>
-__device__ __forceinline__ void epilogue(const TermArgs<RP, V>& a, int64_t u, V s, int64_t deg,
-                                         double& p0, double& p1) {
-    if constexpr (EPI == EPI_PLAIN) {
-        a.out[u] = s;
-    } else {
-        const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
-        if constexpr (EPI == EPI_CPAA) {
-            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), a.T[u]);
-            a.T[u] = t;
-            const V nacc = add_rn(a.acc[u], mul_rn((V)a.ck, t));
-            a.acc[u] = nacc;
-            a.x_out[u] = mul_rn(t, inv);
-            p0 += (double)t;
-            p1 += (double)nacc;
-        } else if constexpr (EPI == EPI_GEN) {
-            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), a.T_prev[u]);
-            a.out[u] = t;
-        } else {  // EPI_POWER
-            const V y = add_rn(mul_rn((V)a.ck, s), (V)a.base);
-            const V old = a.T[u];
-            a.T[u] = y;
-            a.x_out[u] = mul_rn(y, inv);
-            p0 += fabs((double)y - (double)old);
-            p1 += (double)y;
-        }
-    }
-}
-
-// ---------------- FAST: persistent warp-tiled schedule ---------------------------------
-//
-// The view's rows are sorted by degree (descending) and cut into WARP tiles (build.cu):
-//  * pack tiles: <= 32 consecutive whole rows with <= kWarpNnz (256) nnz;
-//  * chunk tiles: a slice of <= kWarpNnz (256) nnz of a row with degree > kWarpNnz;
-//    a row with several chunks is finished by the last chunk to arrive, which combines
-//    the chunk partials in chunk order (deterministic).
-// One CTA of 32 warps per SM; each warp walks tiles blockIdx*32+warp, +gridDim*32, ...
-// (static, deterministic) with no CTA barrier inside the term: per tile a lane issues
-// its 8 column-id loads, the row end pointer, T_{k-1} and acc at once, then 8 gathers.
-// Gathers of the hottest vertices (ids < H: the degree-sorted hub prefix, ~50% of all
-// gathers on power-law graphs) hit a shared-memory copy of x_k[0..H) refreshed at the
-// start of every term; the rest go through L1/L2.  Measured on B200
-// (tools/micro_gather.cu): random LDS.64 876 G/s vs random LDG over an L2-resident
-// table 256 G/s — the gather, not HBM, bounds this path.
-
-// Cold x gathers: read-only path without L1 allocation (the L1 left next to the shared
-// hot prefix is tiny; a random line would only evict another).
-#ifndef CHEB_COLD_NOALLOC
-#define CHEB_COLD_NOALLOC 0
-#endif
-__device__ __forceinline__ double ldg_cold(const double* p) {
-#if CHEB_COLD_NOALLOC
-    double v;
-    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
-__device__ __forceinline__ float ldg_cold(const float* p) {
-#if CHEB_COLD_NOALLOC
-    float v;
-    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
-
-__device__ __forceinline__ double lds_v(unsigned addr, double) {
-    double v;
-    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ float lds_v(unsigned addr, float) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
-}
-
-// Gather x[c[q]] for a lane's column ids: cold ids (>= H) as predicated global loads
-// issued back to back, hot ids from the shared-memory copy at 32-bit address hot_s;
-// c < 0 = no element (0).
-template <class V, int U>
-__device__ __forceinline__ void gather8(const V* __restrict__ x, unsigned hot_s, int H, const int (&c)[U],
-                                        V (&v)[U]) {
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-        v[q] = V(0);
-        if (c[q] >= H) v[q] = ldg_cold(x + c[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q)
-        if ((unsigned)c[q] < (unsigned)H) v[q] = lds_v(hot_s + (unsigned)c[q] * (unsigned)sizeof(V), V(0));
-}
-
-// Programmatic dependent launch: let the next kernel of the stream launch now (its CTAs
-// take SMs as this grid drains), and wait for the previous kernel's completion + memory
-// flush before reading anything it wrote.  Both are no-ops without the launch attribute.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-// TMA bulk copy global -> shared (cp.async.bulk), completion on an mbarrier.
-__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* mbar) {
-    const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 :: "r"(dst), "l"(gsrc), "r"(bytes), "r"(bar) : "memory");
-}
-// Column ids are read once per term: an L2 evict-first policy on their TMA copies keeps the
-// per-term streams (~130 MB on C2, about the size of L2) from pushing x out of L2
-// (C2 73.2 -> 70.1 us/term; profiles/r01_gather_microbench.md).
-__device__ __forceinline__ void bulk_g2s_stream(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* mbar) {
-    const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-        :: "r"(dst), "l"(gsrc), "r"(bytes), "r"(bar), "l"(pol) : "memory");
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* mbar, unsigned count) {
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, unsigned bytes) {
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
-    asm volatile(
-        "{\n"
-        ".reg .pred done;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
-        "@!done bra WAIT_%=;\n"
-        "}\n" :: "r"(bar), "r"(parity) : "memory");
-}
-
-// Row epilogue with the row's operands already loaded (prev = T_{k-1} / old x).
-template <int EPI, class RP, class V>
-__device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, V s, int64_t deg,
-                                           V prev, V accv, double& p0, double& p1) {
-    if constexpr (EPI == EPI_PLAIN) {
-        a.out[u] = s;
-    } else {
-        const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
-        if constexpr (EPI == EPI_CPAA) {
-            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
-            a.T[u] = t;
-            const V nacc = add_rn(accv, mul_rn((V)a.ck, t));
-            a.acc[u] = nacc;
-            const V xn = mul_rn(t, inv);
-            if (a.push) {  // fused exchange: straight into every rank's copy of x_{k+1}
-                for (int r = 0; r < a.push_n; ++r) a.push[r][a.push_off + u] = xn;
-            } else {
-                a.x_out[u] = xn;
-            }
-            p0 += (double)t;
-            p1 += (double)nacc;
-        } else if constexpr (EPI == EPI_GEN) {
-            a.out[u] = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
-        } else {  // EPI_POWER
-            const V y = add_rn(mul_rn((V)a.ck, s), (V)a.base);
-            a.T[u] = y;
-            a.x_out[u] = mul_rn(y, inv);
-            p0 += fabs((double)y - (double)prev);
-            p1 += (double)y;
-        }
-    }
-}
-
-template <int EPI, class RP, class V>
-__device__ __forceinline__ const V* prev_src(const TermArgs<RP, V>& a) {
-    if constexpr (EPI == EPI_GEN) return a.T_prev;
-    else return a.T;
-}
-
-template <class V>
-__device__ __forceinline__ V warp_sum_v(V v) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-template <class V>
-constexpr int hot_capacity() { return (kHotBytes / (int)sizeof(V)); }
-
-// Per-warp shared scratch of the term kernel.
-template <class V>
-struct alignas(16) WarpScratch {
-    int colb[2][kColBuf];   // TMA landing buffers: column ids of the current / next tile
-    WTile desc[2][kDescBlock];  // TMA ring of this warp's tile program
-    uint64_t colm[2];       // mbarriers of colb
-    uint64_t descm[2];      // mbarriers of desc
-};
-
-template <class V>
-constexpr size_t warp_smem_bytes() {
-    return (size_t)kHotBytes + (size_t)kWarps * sizeof(WarpScratch<V>) + 2 * 32 * sizeof(double);
-}
-
-// Tile in registers.
-struct TileR {
-    int64_t z0;
-    int r0, rows, cnt, meta;
-};
-
-__device__ __forceinline__ TileR tile_of(const WTile& d) {
-    TileR r;
-    r.z0 = d.nnz_begin;
-    r.r0 = d.row_begin;
-    r.cnt = d.cnt;
-    r.rows = d.rows;
-    r.meta = d.meta;
-    return r;
-}
-
-// Lane 0: bulk-copy the tile's column ids from the 8-aligned position a0 = z0 & ~7 into buf.
-__device__ __forceinline__ void issue_cols(const int* __restrict__ col, const TileR& t, int* buf,
-                                           uint64_t* mbar) {
-    const int64_t a0 = t.z0 & ~int64_t(7);
-    const unsigned bytes = (unsigned)(((t.z0 - a0) + t.cnt + 3) & ~3) * 4u;
-    mbar_expect_tx(mbar, bytes);
-    bulk_g2s_stream(buf, col + a0, bytes, mbar);
-}
-
-// Row operands of a pack tile for the lane leading row g's lane group (L = 1 << lg lanes
-// per row): tile-local row start/end, T_{k-1}, acc.
-template <class V>
-struct RowOps {
-    int rs, re;
-    V pv, av;
-};
-
-template <int EPI, class RP, class V>
-__device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR& t, RowOps<V>& o) {
-    const int lane = threadIdx.x & 31;
-    o.rs = 0;
-    o.re = 0;
-    o.pv = V(0);
-    o.av = V(0);
-    if (t.meta & kTileChunk) return;
-    const int lg = t.meta & 0xf;
-    const int g = lane >> lg;
-    if ((lane & ((1 << lg) - 1)) == 0 && g < t.rows) {
-        o.rs = (int)(a.rp[t.r0 + g] - t.z0);
-        o.re = (int)(a.rp[t.r0 + g + 1] - t.z0);
-        if constexpr (EPI != EPI_PLAIN) o.pv = prev_src<EPI>(a)[t.r0 + g];
-        if constexpr (EPI == EPI_CPAA) o.av = a.acc[t.r0 + g];
-    }
-}
-
-// Lane 0: bulk-copy descriptor block blk of this warp's program into ring slot blk & 1.
-__device__ __forceinline__ void issue_desc(const WTile* my, int blk, WarpScratch<double>* unused,
-                                           WTile* slot, uint64_t* mbar) {
-    (void)unused;
-    mbar_expect_tx(mbar, kDescBlock * sizeof(WTile));
-    bulk_g2s(slot, my + (size_t)blk * kDescBlock, kDescBlock * sizeof(WTile), mbar);
-}
-
-#ifndef CHEB_PACK_UNROLL
-#define CHEB_PACK_UNROLL 4
-#endif
-constexpr int kPackUnroll = CHEB_PACK_UNROLL;  // gathers in flight per lane in pack tiles
-
-// One tile of the warp's program.  cur: this tile's row operands (loaded one tile ago);
-// nxt receives the next tile's.  No register prefetched here is copied at the end.
-template <int EPI, class RP, class V, class WS>
-__device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot_s, int H, WS& ws,
-                                          const WTile* my, int w, int S, int nt, int i,
-                                          const RowOps<V>& cur, RowOps<V>& nxt, double& p0, double& p1) {
-    const int lane = threadIdx.x & 31;
-    constexpr int U = 8;
-    const TileR d = tile_of(ws.desc[(i / kDescBlock) & 1][i % kDescBlock]);
-    if (i + 1 < nt) {
-        const int j = i + 1;
-        if (j % kDescBlock == 0) mbar_wait(&ws.descm[(j / kDescBlock) & 1], ((j / kDescBlock) >> 1) & 1);
-        const TileR dn = tile_of(ws.desc[(j / kDescBlock) & 1][j % kDescBlock]);
-        if (lane == 0) issue_cols(a.col, dn, ws.colb[j & 1], &ws.colm[j & 1]);
-        load_rows<EPI>(a, dn, nxt);
-    }
-    const int t = w + i * S;  // tile id (slot of a hub-row partial)
-    mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
-    if (a.tune_skip &&
-        (a.tune_skip >= 16 ? (((d.meta & kTileChunk) ? 6 : (d.meta & 0xf)) != a.tune_skip - 16)
-                           : ((a.tune_skip & 1) ? (d.meta & kTileChunk) : !(d.meta & kTileChunk)))) {
-        __syncwarp();
-        if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
-            const int blk = i / kDescBlock + 2;
-            if (blk * kDescBlock < nt) issue_desc(my, blk, nullptr, ws.desc[blk & 1], &ws.descm[blk & 1]);
-        }
-        return;
-    }
-    const int* cb = ws.colb[i & 1] + (int)(d.z0 & 7);  // tile-local position p at cb[p]
-
-    if (d.meta & kTileChunk) {
-        // slice of a row with degree > kWarpNnz: partial only; completed by k_hub_finalize
-        int c[U];
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-            const int pp = lane + 32 * q;
-            c[q] = pp < d.cnt ? cb[pp] : -1;
-        }
-        V v[U];
-        if (a.tune_nogather) {
-#pragma unroll
-            for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
-        } else {
-            gather8(a.x_in, hot_s, H, c, v);
-        }
-        V sum = V(0);
-#pragma unroll
-        for (int q = 0; q < U; ++q) sum += v[q];
-        sum = warp_sum_v(sum);
-        if (lane == 0) a.hub_part[t] = (double)sum;
-    } else {
-        // rows of similar degree: L lanes per row, row g owned by lanes [g L, g L + L)
-        const int lg = d.meta & 0xf;
-        const int L = 1 << lg;
-        const int li = lane & (L - 1), g = lane >> lg;
-        int rb = cur.rs, rend = cur.re;
-        if (lg) {
-            const int leader = lane & ~(L - 1);
-            rb = __shfl_sync(0xffffffffu, rb, leader);
-            rend = __shfl_sync(0xffffffffu, rend, leader);
-        }
-        V sum = V(0);
-        for (int jj = rb + li; jj < rend; jj += kPackUnroll * L) {
-            int c[kPackUnroll];
-#pragma unroll
-            for (int q = 0; q < kPackUnroll; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
-            V v[kPackUnroll];
-            if (a.tune_nogather) {
-#pragma unroll
-                for (int q = 0; q < kPackUnroll; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
-            } else {
-                gather8(a.x_in, hot_s, H, c, v);
-            }
-#pragma unroll
-            for (int q = 0; q < kPackUnroll; ++q) sum += v[q];
-        }
-        for (int o = L >> 1; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        if (li == 0 && g < d.rows)
-            epilogue_v<EPI>(a, (int64_t)d.r0 + g, sum, (int64_t)(rend - rb), cur.pv, cur.av, p0, p1);
-    }
-    __syncwarp();
-    // descriptor block of tile i fully consumed: refill its slot two blocks ahead
-    if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
-        const int blk = i / kDescBlock + 2;
-        if (blk * kDescBlock < nt) issue_desc(my, blk, nullptr, ws.desc[blk & 1], &ws.descm[blk & 1]);
-    }
-}
-
-template <int EPI, class RP, class V>
-__global__ void __launch_bounds__(kWarps * 32, 1)
-k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles, int H) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    V* hot = reinterpret_cast<V*>(smem);
-    const unsigned hot_s = (unsigned)__cvta_generic_to_shared(smem);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpScratch<V>& ws = reinterpret_cast<WarpScratch<V>*>(smem + kHotBytes)[warp];
-    double* red = reinterpret_cast<double*>(smem + kHotBytes + kWarps * sizeof(WarpScratch<V>));
-    __shared__ __align__(8) uint64_t mbar_hot;
-
-    const int S = gridDim.x * kWarps;
-    const int w = blockIdx.x * kWarps + warp;
-    const int nt = w < ntiles ? (ntiles - w + S - 1) / S : 0;
-    const WTile* my = prog + (size_t)w * P;
-
-    // hot prefix x_k[0..H) -> shared memory (TMA bulk copies; sub-16-byte tail by loads)
-    const unsigned hot_bytes = (unsigned)(H * sizeof(V)) & ~15u;
-    if (threadIdx.x == 0) mbar_init(&mbar_hot, 1);
-    if (lane == 0) {
-        mbar_init(&ws.colm[0], 1);
-        mbar_init(&ws.colm[1], 1);
-        mbar_init(&ws.descm[0], 1);
-        mbar_init(&ws.descm[1], 1);
-    }
-    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-    pdl_trigger();
-    if (lane == 0) {  // this warp's tile program is static: fetch it before the dependency wait
-        if (nt > 0) issue_desc(my, 0, nullptr, ws.desc[0], &ws.descm[0]);
-        if (nt > kDescBlock) issue_desc(my, 1, nullptr, ws.desc[1], &ws.descm[1]);
-    }
-    pdl_wait();  // x_k, T, acc come from the previous kernels of the stream
-    if (threadIdx.x == 0) {
-        mbar_expect_tx(&mbar_hot, hot_bytes);
-        constexpr unsigned kPiece = 32768;
-        for (unsigned off = 0; off < hot_bytes; off += kPiece)
-            bulk_g2s(smem + off, reinterpret_cast<const unsigned char*>(a.x_in) + off,
-                     min(kPiece, hot_bytes - off), &mbar_hot);
-    }
-    for (int i = hot_bytes / sizeof(V) + threadIdx.x; i < H; i += blockDim.x) hot[i] = ldg_x(a.x_in + i);
-
-    RowOps<V> A, B;
-    if (nt > 0) {
-        mbar_wait(&ws.descm[0], 0);
-        const TileR d0 = tile_of(ws.desc[0][0]);
-        if (lane == 0) issue_cols(a.col, d0, ws.colb[0], &ws.colm[0]);
-        load_rows<EPI>(a, d0, A);
-    }
-    double p0 = 0.0, p1 = 0.0;
-    mbar_wait(&mbar_hot, 0);
-    __syncthreads();
-
-    for (int i = 0; i < nt; i += 2) {
-        term_step<EPI>(a, hot_s, H, ws, my, w, S, nt, i, A, B, p0, p1);
-        if (i + 1 >= nt) break;
-        term_step<EPI>(a, hot_s, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
-    }
-    if constexpr (EPI == EPI_CPAA || EPI == EPI_POWER) {
-        if (a.part) {
-            p0 = warp_sum_v(p0);
-            p1 = warp_sum_v(p1);
-            if (lane == 0) {
-                red[warp] = p0;
-                red[32 + warp] = p1;
-            }
-            __syncthreads();
-            if (warp == 0) {
-                double q0 = lane < kWarps ? red[lane] : 0.0;
-                double q1 = lane < kWarps ? red[32 + lane] : 0.0;
-                q0 = warp_sum_v(q0);
-                q1 = warp_sum_v(q1);
-                if (lane == 0) {
-                    a.part[2 * blockIdx.x] = q0;
-                    a.part[2 * blockIdx.x + 1] = q1;
-                }
-            }
-        }
-    }
-}
-
-// Hub rows (degree > kWarpNnz, rows [0, n_hub) of the view): one warp per row sums the
-// row's chunk partials in chunk order and runs the fused epilogue.  Chunk tiles of row h
-// are the consecutive tiles [hub_first[h], hub_first[h+1]).
-template <int EPI, class RP, class V>
-__global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const int* __restrict__ hub_first,
-                                                      int64_t n_hub) {
-    const int lane = threadIdx.x & 31;
-    pdl_trigger();
-    pdl_wait();  // the term kernel's hub partials
-    for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < n_hub;
-         h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int f0 = hub_first[h], f1 = hub_first[h + 1];
-        V tot = V(0);
-        for (int q = f0 + lane; q < f1; q += 32) tot += (V)a.hub_part[q];
-        tot = warp_sum_v(tot);
-        if (lane == 0) {
-            const int64_t deg = a.rp[h + 1] - a.rp[h];
-            double q0 = 0.0, q1 = 0.0;
-            const V hp = EPI != EPI_PLAIN ? prev_src<EPI>(a)[h] : V(0);
-            const V ha = EPI == EPI_CPAA ? a.acc[h] : V(0);
-            epilogue_v<EPI>(a, h, tot, deg, hp, ha, q0, q1);
-            if (a.hub_ts) {
-                a.hub_ts[2 * h] = q0;
-                a.hub_ts[2 * h + 1] = q1;
-            }
-        }
-    }
-}
-
-// ---------------- BITEXACT: thread per row, storage order ----------------------------
-template <int EPI, class RP>
-__global__ void __launch_bounds__(kThreads) k_term_exact(TermArgs<RP, double> a, int64_t n) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = a.rp[u], e = a.rp[u + 1];
-        double s = 0.0;
-        for (int64_t j = b; j < e; ++j) s = __dadd_rn(s, a.x_in[a.col[j]]);
-        double p0 = 0.0, p1 = 0.0;
-        epilogue<EPI>(a, u, s, e - b, p0, p1);
-    }
-}
-
-// Serial Kahan sums exactly as graph.cpp:10-19 (single thread: bit-identical order).
-// The reference's serial compensated sums, bit for bit (graph.cpp:10-19 order, one element
-// at a time).  The recurrence is inherently sequential, so one thread runs it; warps 1..7
-// stage the next chunk of both inputs into shared memory meanwhile, so the chain runs at
-// FP64 add latency instead of waiting on global loads.
-constexpr int kSerialChunk = 1024;
-
-template <int MODE>  // 0: Kahan(x) [, Kahan(y)]   1: power: Kahan|y - x|, Kahan(y) (power.cpp:80-93)
-__global__ void __launch_bounds__(256) k_serial_sums(const double* __restrict__ a, const double* __restrict__ b,
-                                                     int64_t n, double* __restrict__ out) {
-    __shared__ double sa[2][kSerialChunk], sb[2][kSerialChunk];
-    const int tid = threadIdx.x;
-    const bool two = b != nullptr;
-    auto stage = [&](int buf, int64_t base) {  // warps 1..7
-        const int64_t len = n - base < kSerialChunk ? n - base : (int64_t)kSerialChunk;
-        for (int64_t i = tid - 32; i < len; i += blockDim.x - 32) {
-            sa[buf][i] = a[base + i];
-            if (two) sb[buf][i] = b[base + i];
-        }
-    };
-    if (tid >= 32 && n > 0) stage(0, 0);
-    __syncthreads();
-    double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
-    for (int64_t base = 0; base < n; base += kSerialChunk) {
-        const int cur = (int)((base / kSerialChunk) & 1);
-        if (tid >= 32 && base + kSerialChunk < n) stage(cur ^ 1, base + kSerialChunk);
-        if (tid == 0) {
-            const int len = (int)(n - base < kSerialChunk ? n - base : (int64_t)kSerialChunk);
-#pragma unroll 4
-            for (int j = 0; j < len; ++j) {
-                if constexpr (MODE == 0) {
-                    const double av = __dsub_rn(sa[cur][j], c0);
-                    const double t = __dadd_rn(s0, av);
-                    c0 = __dsub_rn(__dsub_rn(t, s0), av);
-                    s0 = t;
-                    if (two) {
-                        const double bv = __dsub_rn(sb[cur][j], c1);
-                        const double u = __dadd_rn(s1, bv);
-                        c1 = __dsub_rn(__dsub_rn(u, s1), bv);
-                        s1 = u;
-                    }
-                } else {  // a = y (new), b = x (old)
-                    const double y = sa[cur][j];
-                    const double d = __dsub_rn(fabs(__dsub_rn(y, sb[cur][j])), c0);
-                    const double t = __dadd_rn(s0, d);
-                    c0 = __dsub_rn(__dsub_rn(t, s0), d);
-                    s0 = t;
-                    const double av = __dsub_rn(y, c1);
-                    const double u = __dadd_rn(s1, av);
-                    c1 = __dsub_rn(__dsub_rn(u, s1), av);
-                    s1 = u;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    if (tid == 0) {
-        out[0] = s0;
-        out[1] = s1;
-    }
-}
-
-// Many independent serial Kahan sums (one per thread), each in the reference's element
-// order: the BITEXACT trace of all M terms after the loop (mass_T = Kahan(T_k),
-// S_k = Kahan(acc_k) from per-term snapshots).  Sums of different terms do not depend on
-// each other, so they run side by side; within a sum the order is the reference's.
-__global__ void k_kahan_many(const double* __restrict__ snaps, int64_t n, int count, double* __restrict__ out) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= count) return;
-    const double* __restrict__ x = snaps + (size_t)t * (size_t)n;
-    double s = 0.0, c = 0.0;
-    int64_t i = 0;
-    constexpr int U = 16;
-    for (; i + U <= n; i += U) {
-        double v[U];
-#pragma unroll
-        for (int q = 0; q < U; ++q) v[q] = __ldg(x + i + q);
-#pragma unroll
-        for (int q = 0; q < U; ++q) {
-            const double a = __dsub_rn(v[q], c);
-            const double u = __dadd_rn(s, a);
-            c = __dsub_rn(__dsub_rn(u, s), a);
-            s = u;
-        }
-    }
-    for (; i < n; ++i) {
-        const double a = __dsub_rn(x[i], c);
-        const double u = __dadd_rn(s, a);
-        c = __dsub_rn(__dsub_rn(u, s), a);
-        s = u;
-    }
-    out[t] = s;
-}
-
-// Power rounds j = 1..nb of a speculative batch (snapshots S[0..nb] of x): thread 2(j-1)
-// runs the reference's Kahan L1 change |S[j] - S[j-1]|, thread 2(j-1)+1 the Kahan mass of
-// S[j] (power.cpp:80-93), each in element order.
-__global__ void k_power_many(const double* __restrict__ S, int64_t n, int nb, double* __restrict__ out) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= 2 * nb) return;
-    const int j = t / 2 + 1;
-    const double* __restrict__ y = S + (size_t)j * (size_t)n;
-    const double* __restrict__ x = S + (size_t)(j - 1) * (size_t)n;
-    double s = 0.0, c = 0.0;
-    constexpr int U = 16;  // loads of the next elements are independent of the chain
-    int64_t i = 0;
-    if (t & 1) {
-        for (; i + U <= n; i += U) {
-            double v[U];
-#pragma unroll
-            for (int q = 0; q < U; ++q) v[q] = __ldg(y + i + q);
-#pragma unroll
-            for (int q = 0; q < U; ++q) {
-                const double a = __dsub_rn(v[q], c);
-                const double u = __dadd_rn(s, a);
-                c = __dsub_rn(__dsub_rn(u, s), a);
-                s = u;
-            }
-        }
-        for (; i < n; ++i) {
-            const double a = __dsub_rn(__ldg(y + i), c);
-            const double u = __dadd_rn(s, a);
-            c = __dsub_rn(__dsub_rn(u, s), a);
-            s = u;
-        }
-    } else {
-        for (; i + U <= n; i += U) {
-            double d[U];
-#pragma unroll
-            for (int q = 0; q < U; ++q) d[q] = fabs(__dsub_rn(__ldg(y + i + q), __ldg(x + i + q)));
-#pragma unroll
-            for (int q = 0; q < U; ++q) {
-                const double e = __dsub_rn(d[q], c);
-                const double u = __dadd_rn(s, e);
-                c = __dsub_rn(__dsub_rn(u, s), e);
-                s = u;
-            }
-        }
-        for (; i < n; ++i) {
-            const double e = __dsub_rn(fabs(__dsub_rn(__ldg(y + i), __ldg(x + i))), c);
-            const double u = __dadd_rn(s, e);
-            c = __dsub_rn(__dsub_rn(u, s), e);
-            s = u;
-        }
-    }
-    out[t] = s;
-}
-
-// ---------------- init / reductions / normalisation ----------------------------------
-// T_{-1} = T_0 = p (or 1), acc = (c0/2) T_0, x_0 = T_0 D^-1   (cpaa.cpp:88-92, :116 at k=1)
-template <class RP, class V>
-__global__ void k_init(const RP* __restrict__ rp, const double* __restrict__ inv,
-                       const double* __restrict__ p, const int* __restrict__ order, int64_t n,
-                       double half_c0, V* __restrict__ T0, V* __restrict__ T1, V* __restrict__ acc,
-                       V* __restrict__ x0) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x) {
-        const V t0 = p ? (V)p[order ? order[u] : u] : V(1);
-        T0[u] = t0;
-        T1[u] = t0;
-        acc[u] = p ? mul_rn((V)half_c0, t0) : (V)half_c0;
-        const V iv = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
-        x0[u] = mul_rn(t0, iv);
-    }
-}
-
-// trace[k] = sum of block partials (+ hub partials) of term k, fixed order.
-__global__ void k_trace_reduce(const double* __restrict__ part, int grid, const double* __restrict__ hub_ts,
-                               int n_hub, int k_first, double* __restrict__ trace) {
-    __shared__ double sh[32];
-    const int k = k_first + blockIdx.x;
-    const double* pk = part + (size_t)k * grid * 2;
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < grid; i += blockDim.x) {
-        a += pk[2 * i];
-        b += pk[2 * i + 1];
-    }
-    if (hub_ts) {
-        const double* hk = hub_ts + (size_t)k * n_hub * 2;
-        for (int i = threadIdx.x; i < n_hub; i += blockDim.x) {
-            a += hk[2 * i];
-            b += hk[2 * i + 1];
-        }
-    }
-    a = block_sum(a, sh);
-    b = block_sum(b, sh);
-    if (threadIdx.x == 0) {
-        trace[2 * k] = a;
-        trace[2 * k + 1] = b;
-    }
-}
-
-template <class V>
-__global__ void k_sum_blocks(const V* __restrict__ x, int64_t n, double* __restrict__ part) {
-    __shared__ double sh[32];
-    double a = 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        a += (double)x[i];
-    a = block_sum(a, sh);
-    if (threadIdx.x == 0) part[blockIdx.x] = a;
-}
-
-__global__ void k_sum_final(const double* __restrict__ part, int cnt, double* __restrict__ out) {
-    __shared__ double sh[32];
-    double a = 0.0;
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) a += part[i];
-    a = block_sum(a, sh);
-    if (threadIdx.x == 0) *out = a;
-}
-
-// ranks[order[u]] = acc[u] / total   (cpaa.cpp:159-163)
-template <class V>
-__global__ void k_normalize(const V* __restrict__ acc, const int* __restrict__ order, int64_t n,
-                            const double* __restrict__ total, V* __restrict__ out) {
-    const double tot = *total;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x) {
-        const V r = (V)((double)acc[u] / tot);
-        out[order ? order[u] : u] = r;
-    }
-}
-
-template <class V>
-__global__ void k_permute_in(const double* __restrict__ src, const int* __restrict__ order, int64_t n,
-                             V* __restrict__ dst) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x)
-        dst[u] = (V)src[order ? order[u] : u];
-}
-
-template <class V>
-__global__ void k_permute_out(const V* __restrict__ src, const int* __restrict__ order, int64_t n,
-                              double* __restrict__ dst) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x)
-        dst[order ? order[u] : u] = (double)src[u];
-}
-
-// x = T D^-1 (staged API / transition_apply pre-scale)
-template <class RP, class V>
-__global__ void k_prescale(const RP* __restrict__ rp, const double* __restrict__ inv,
-                           const V* __restrict__ T, int64_t n, V* __restrict__ x) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x) {
-        const V iv = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
-        x[u] = mul_rn(T[u], iv);
-    }
-}
-
-// acc += c_k T_next (cpaa.cpp:192-194)
-template <class V>
-__global__ void k_accumulate(V* __restrict__ acc, const V* __restrict__ Tn, int64_t n, double ck) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x)
-        acc[u] = add_rn(acc[u], mul_rn((V)ck, Tn[u]));
-}
-
-// Per-round error vs a reference (metrics.cpp:12-30 via cpaa.cpp:149-154):
-// est = acc / S_k ; max |est-ref|/ref and sum |est-ref|.  ref in the same layout.
-template <class V>
-__global__ void k_err(const V* __restrict__ acc, const double* __restrict__ ref, int64_t n,
-                      const double* __restrict__ S, int by_S, double* __restrict__ part) {
-    __shared__ double sh[32];
-    const double tot = by_S ? *S : 1.0;
-    double mx = 0.0, l1 = 0.0;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x) {
-        const double est = by_S ? (double)acc[u] / tot : (double)acc[u];
-        const double d = fabs(est - ref[u]);
-        mx = fmax(mx, d / ref[u]);
-        l1 += d;
-    }
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
-        part[2 * blockIdx.x] = mx;
-    }
-    __syncthreads();
-    l1 = block_sum(l1, sh);
-    if (threadIdx.x == 0) part[2 * blockIdx.x + 1] = l1;
-}
-
-__global__ void k_err_final(const double* __restrict__ part, int cnt, double* __restrict__ out) {
-    __shared__ double sh[32];
-    double mx = 0.0, l1 = 0.0;
-    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-        mx = fmax(mx, part[2 * i]);
-        l1 += part[2 * i + 1];
-    }
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
-        out[0] = mx;
-    }
-    __syncthreads();
-    l1 = block_sum(l1, sh);
-    if (threadIdx.x == 0) out[1] = l1;
-}
-
-// =====================================================================================
-// Host drivers
-// =====================================================================================
 namespace {
 
-inline int grid1d(int64_t n) {
-    int64_t b = (n + kThreads - 1) / kThreads;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
-}
-
-// Layout the solve runs on: FAST -> degree-binned view; BITEXACT -> reference order.
-struct Layout {
-    bool fast;
-    bool rp64;
-    const void* rp;
-    const int* col;
-    const double* inv;
-    const int* order;  // new -> old (fast) or null
-};
-
-Layout layout_of(cheb_graph* g, int mode) {
-    Layout L{};
-    if (mode == CHEB_MODE_FAST) {
-        ensure_view(g);
-        L.fast = true;
-        L.rp64 = g->view.rp64;
-        L.rp = g->view.row_ptr.get();
-        L.col = g->view.col.ptr<int>();
-        L.inv = g->inv_array ? g->view.inv.ptr<double>() : nullptr;
-        L.order = g->view.order.ptr<int>();
-    } else {
-        L.fast = false;
-        L.rp64 = g->rp64;
-        L.rp = g->row_ptr.get();
-        L.col = g->col.ptr<int>();
-        L.inv = g->inv_array ? g->inv.ptr<double>() : nullptr;
-        L.order = nullptr;
-    }
-    return L;
-}
-
-template <class RP, class V>
-TermArgs<RP, V> base_args(cheb_graph* /*g*/, const Layout& L) {
-    TermArgs<RP, V> a{};
-    a.rp = static_cast<const RP*>(L.rp);
-    a.col = L.col;
-    a.inv = L.inv;
-    return a;
-}
-
-// Launch one SpMV-shaped pass with epilogue EPI on the given layout.
-template <int EPI, class RP, class V>
-int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
-    cudaStream_t st = g->stream;
-    if (L.fast) {
-        static bool attr_set = false;  // per template instance
-        constexpr size_t smem = warp_smem_bytes<V>();
-        if (!attr_set) {
-            CHEB_CUDA_CHECK(cudaFuncSetAttribute(k_term_warp<EPI, RP, V>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_set = true;
-        }
-        int H = (int)std::min<int64_t>(g->n, hot_capacity<V>());
-        if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);
-        TermArgs<RP, V> ab = a;
-        ab.tune_nogather = tuning().nogather;
-        ab.tune_skip = tuning().skip;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(g->view.grid);
-        cfg.blockDim = dim3(kWarps * 32);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[2];
-        cfg.attrs = attr;
-        cfg.numAttrs = 0;
-        // keep the hot (degree-sorted) prefix of x_k resident in L2 across the term
-        if (tuning().l2win &&
-            l2_window(a.x_in, (size_t)std::max<int64_t>(g->view.x_len, 1) * sizeof(V),
-                      &attr[cfg.numAttrs].val.accessPolicyWindow)) {
-            attr[cfg.numAttrs++].id = cudaLaunchAttributeAccessPolicyWindow;
-        }
-        if (tuning().pdl) {  // overlap this launch + prologue with the previous kernel's tail
-            attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
-        }
-        CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V>, ab, (const WTile*)g->view.prog.ptr<WTile>(),
-                                           g->view.prog_len, g->view.n_tiles, H));
-        if (g->view.n_hub > 0) {
-            CHEB_CUDA_CHECK(cudaGetLastError());
-            const int hb = (int)std::min<int64_t>((g->view.n_hub * 32 + 255) / 256, 148 * 16);
-            cudaLaunchConfig_t hc = {};
-            hc.gridDim = dim3(hb);
-            hc.blockDim = dim3(256);
-            hc.stream = st;
-            cudaLaunchAttribute hattr[1];
-            hattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            hattr[0].val.programmaticStreamSerializationAllowed = 1;
-            hc.attrs = hattr;
-            hc.numAttrs = tuning().pdl ? 1 : 0;
-            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&hc, k_hub_finalize<EPI, RP, V>, a,
-                                               (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub));
-            return 2;
-        }
-    } else {
-        if constexpr (std::is_same<V, double>::value) {
-            k_term_exact<EPI, RP><<<grid1d(g->n), kThreads, 0, st>>>(a, g->n);
-        } else {
-            fail(CHEB_INVALID_ARG, "bitexact mode is fp64 only");
-        }
-    }
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    return 1;
-}
-
-template <class V>
-void ensure_workspace(cheb_graph* g, int M, int R) {
-    Workspace& w = g->ws;
-    const int64_t n = g->n;
-    // Any reallocation invalidates the captured solve graph (it bakes in addresses).
-    const void* before[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
-                            w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
-                            w.trace.get(), w.total.get()};
-    const int64_t vlen = std::max<int64_t>(std::max<int64_t>(n, g->view.x_len), 1);
-    const size_t vb = sizeof(V) * (size_t)vlen * R;
-    w.T0.ensure(vb);
-    w.T1.ensure(vb);
-    w.X0.ensure(vb);
-    w.X1.ensure(vb);
-    w.acc.ensure(vb);
-    w.out.ensure(vb);
-    const int grid = std::max(g->view.ready ? g->view.grid : 1, grid1d(n));
-    w.part.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max(grid, 1));
-    w.hub_part.ensure(sizeof(double) * std::max(g->view.n_tiles, 1));
-    if (!w.hub_cnt || w.hub_cnt.bytes() < sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1)) {
-        w.hub_cnt.alloc(sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1));
-        CHEB_CUDA_CHECK(cudaMemset(w.hub_cnt.get(), 0, w.hub_cnt.bytes()));
-    }
-    w.hub_ts.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max<int64_t>(g->view.n_hub, 1));
-    w.trace.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1));
-    w.total.ensure(sizeof(double) * 4);
-    w.n = n;
-    w.R = R;
-    w.vbytes = sizeof(V);
-    const void* after[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
-                           w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
-                           w.trace.get(), w.total.get()};
-    if (std::memcmp(before, after, sizeof before) != 0) {
-        if (w.exec) cudaGraphExecDestroy(w.exec);
-        w.exec = nullptr;
-        w.exec_key.clear();
-        w.seen_key.clear();
-    }
-}
-
-// BITEXACT trace snapshots (2 M n doubles) when they fit a quarter of the free memory (and
-// 8 GB); otherwise the per-term serial sums run instead.
-void ensure_snapshots(cheb_graph* g, int M) {
-    Workspace& w = g->ws;
-    const size_t need = sizeof(double) * 2 * (size_t)M * (size_t)g->n;
-    if (w.snap.bytes() >= need) return;
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
-    if (need > free_b / 4 || need > (size_t(8) << 30)) return;
-    w.snap.alloc(need);
-    if (w.exec) cudaGraphExecDestroy(w.exec);  // a captured solve baked the old pointers in
-    w.exec = nullptr;
-    w.exec_key.clear();
-    w.seen_key.clear();
-}
-
-// Enqueue the whole solve: init, M fused terms, trace reduction, normalisation.
 template <class RP, class V>
 int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std::vector<double>& coeffs,
                   double c0, const double* d_p, const double* d_ref, double* d_err,
@@ -1135,452 +110,6 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
     return launches;
 }
 
-// ---------------- multi-GPU: row partition + NCCL all-gather of x per term ----------
-template <class V>
-ncclDataType_t nccl_type() { return sizeof(V) == 8 ? ncclDouble : ncclFloat; }
-
-template <class V>
-__global__ void k_normalize_slot(const V* __restrict__ acc, int64_t nl, const double* __restrict__ total,
-                                 V* __restrict__ slot) {
-    const double tot = *total;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nl;
-         u += (int64_t)gridDim.x * blockDim.x)
-        slot[u] = (V)((double)acc[u] / tot);
-}
-
-template <class V>
-__global__ void k_unpermute_padded(const V* __restrict__ padded, const int64_t* __restrict__ cuts, int G,
-                                   int64_t max_rows, const int* __restrict__ order_full, V* __restrict__ out) {
-    const int64_t total = (int64_t)G * max_rows;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(p / max_rows);
-        const int64_t i = p - r * max_rows;
-        if (i < cuts[r + 1] - cuts[r]) out[order_full[cuts[r] + i]] = padded[p];
-    }
-}
-
-// ---------------- fused push exchange: barrier and copy kernels ------------------------
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-// Wait for slot r of this rank's flags to reach epoch; give up after 20 s and raise the
-// group's timeout flag (slot G) instead of hanging the GPU if a peer never signals.
-__device__ __forceinline__ void wait_epoch(const unsigned long long* flags, int r, int G, unsigned long long epoch) {
-    const unsigned long long t0 = global_ns();
-    while (ld_acquire_sys(flags + r) < epoch) {
-        __nanosleep(100);
-        if (global_ns() - t0 > 20000000000ull) {
-            atomicExch(const_cast<unsigned long long*>(flags) + G, 1ull);
-            return;
-        }
-    }
-}
-
-// This rank reached `epoch`: publish it in slot [rank] of every rank's flag array.  The
-// system-scope fence orders every earlier store of this stream (the term's pushes) before it.
-__global__ void k_peer_signal(unsigned long long* const* flags, int G, int rank, unsigned long long epoch) {
-    const int r = threadIdx.x;
-    if (r < G) {
-        __threadfence_system();
-        st_release_sys(flags[r] + rank, epoch);
-    }
-}
-
-// Wait until every rank published `epoch` into this rank's flags (acquire: their pushes are
-// visible to every later kernel of this stream).
-__global__ void k_peer_wait(const unsigned long long* flags, int G, unsigned long long epoch) {
-    const int r = threadIdx.x;
-    if (r < G) wait_epoch(flags, r, G, epoch);
-    __syncthreads();
-}
-
-// Term tail of a one-process-per-GPU push run, one launch instead of three: this rank's
-// trace partials of term k (as k_trace_reduce), then the barrier (signal every rank, wait
-// for every rank).  Launched with PDL; waits for the term kernels before reading anything.
-__global__ void __launch_bounds__(256) k_term_tail(const double* __restrict__ part, int grid,
-                                                   const double* __restrict__ hub_ts, int n_hub, int k,
-                                                   double* __restrict__ trace, unsigned long long* const* flags,
-                                                   const unsigned long long* my_flags, int G, int rank,
-                                                   unsigned long long epoch) {
-    __shared__ double sh[32];
-    pdl_wait();
-    const double* pk = part + (size_t)k * grid * 2;
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < grid; i += blockDim.x) {
-        a += pk[2 * i];
-        b += pk[2 * i + 1];
-    }
-    if (hub_ts) {
-        const double* hk = hub_ts + (size_t)k * n_hub * 2;
-        for (int i = threadIdx.x; i < n_hub; i += blockDim.x) {
-            a += hk[2 * i];
-            b += hk[2 * i + 1];
-        }
-    }
-    a = block_sum(a, sh);
-    b = block_sum(b, sh);
-    if (threadIdx.x == 0) {
-        trace[2 * k] = a;
-        trace[2 * k + 1] = b;
-    }
-    const int r = threadIdx.x;
-    if (r < G) {
-        __threadfence_system();  // the term's pushes (earlier kernels of this stream) first
-        st_release_sys(flags[r] + rank, epoch);
-    }
-    if (r < G) wait_epoch(my_flags, r, G, epoch);
-    __syncthreads();
-}
-
-// dst[r][off + i] = src[i] for every rank r (trace partials, x_0 slot).
-template <class T>
-__global__ void k_push_copy(const T* __restrict__ src, int64_t n, T* const* dst, int G, int64_t off) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const T v = src[i];
-        for (int r = 0; r < G; ++r) dst[r][off + i] = v;
-    }
-}
-
-// ranks of the local rows, normalised, pushed into every rank's padded result buffer
-template <class V>
-__global__ void k_normalize_push(const V* __restrict__ acc, int64_t nl, const double* __restrict__ total,
-                                 V* const* dst, int G, int64_t off) {
-    const double tot = *total;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nl; u += (int64_t)gridDim.x * blockDim.x) {
-        const V v = (V)((double)acc[u] / tot);
-        for (int r = 0; r < G; ++r) dst[r][off + u] = v;
-    }
-}
-
-// out[i] = sum over ranks r (in rank order: deterministic) of all[r * stride + i]
-__global__ void k_sum_ranks_strided(const double* __restrict__ all, int G, int len, int64_t stride,
-                                    double* __restrict__ out) {
-    for (int i = threadIdx.x; i < len; i += blockDim.x) {
-        double s = 0.0;
-        for (int r = 0; r < G; ++r) s += all[(size_t)r * stride + i];
-        out[i] = s;
-    }
-}
-
-// One partitioned solve on one rank, in phases, so that a single process can also drive
-// every rank of a group in lockstep.  Exchange: NCCL all-gathers (part.comm) or the fused
-// push (g->peer): pushes inside the kernels + a flag barrier between phases.
-template <class RP, class V>
-struct DistSolve {
-    cheb_graph* g;
-    SolveSpec s;
-    Layout L;
-    PeerGroup* pg;  // null: NCCL
-    std::vector<double> coeffs;
-    double c0 = 0.0, beta_v = 0.0;
-    DevMem d_p, trace_all, tglob, rbuf, dcuts;
-    V* T[2];
-    V* X[2];
-    V* acc;
-    int launches = 0;
-    int64_t nl = 0, mr = 0, stride = 0;
-    int M = 0, G = 1;
-    std::vector<cudaEvent_t>* tev = nullptr;
-    const double* d_total = nullptr;
-    bool fused_tail = false;  // push, one process per GPU: trace reduce + barrier in one kernel
-
-    DistSolve(cheb_graph* g_, const SolveSpec& s_, std::vector<cudaEvent_t>* ev) : g(g_), s(s_), tev(ev) {
-        L = layout_of(g, CHEB_MODE_FAST);
-        pg = g->peer;
-        fused_tail = pg && !pg->lockstep;
-        ensure_workspace<V>(g, s.M, 1);
-        Workspace& w = g->ws;
-        const SolverView& Vw = g->view;
-        const Partition& P = g->part;
-        nl = Vw.n_local;
-        mr = P.max_rows;
-        M = s.M;
-        G = P.G;
-        if (pg && M > kMaxPushTerms) fail(CHEB_CAPACITY, "push exchange supports at most 1024 terms");
-        coefficients(s.c, M, coeffs, &beta_v, &c0);
-        cudaStream_t st = g->stream;
-        if (s.p) {
-            d_p.alloc(sizeof(double) * g->n);
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(d_p.get(), s.p, sizeof(double) * g->n, cudaMemcpyHostToDevice, st));
-        }
-        tglob.alloc(sizeof(double) * 2 * std::max(M, 1));
-        dcuts.alloc(sizeof(int64_t) * (G + 1));
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(dcuts.get(), P.cuts.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, st));
-        T[0] = w.T0.ptr<V>();
-        T[1] = w.T1.ptr<V>();
-        acc = w.acc.ptr<V>();
-        if (pg) {
-            X[0] = static_cast<V*>(pg->X[0]);
-            X[1] = static_cast<V*>(pg->X[1]);
-            stride = 2 * (int64_t)kMaxPushTerms;
-        } else {
-            X[0] = w.X0.ptr<V>();
-            X[1] = w.X1.ptr<V>();
-            trace_all.alloc(sizeof(double) * 2 * (size_t)std::max(M, 1) * G);
-            rbuf.alloc(sizeof(V) * (size_t)std::max<int64_t>(Vw.x_len, 1));
-            stride = 2 * (int64_t)std::max(M, 1);
-        }
-    }
-    ncclComm_t comm() const { return static_cast<ncclComm_t>(g->part.comm); }
-    V* const* push_table(int which) const {  // device pointer table of every rank's X[which]
-        return reinterpret_cast<V* const*>(pg->table.ptr<void*>() + (size_t)which * G);
-    }
-    double* const* trace_table() const { return reinterpret_cast<double* const*>(pg->table.ptr<void*>() + 2 * (size_t)G); }
-    V* const* rbuf_table() const { return reinterpret_cast<V* const*>(pg->table.ptr<void*>() + 3 * (size_t)G); }
-    unsigned long long* const* flag_table() const {
-        return reinterpret_cast<unsigned long long* const*>(pg->table.ptr<void*>() + 4 * (size_t)G);
-    }
-
-    // phase 0: T_{-1} = T_0, acc, x_0 of the local rows, then x_0 to every rank
-    void begin() {
-        cudaStream_t st = g->stream;
-        const SolverView& Vw = g->view;
-        CHEB_CUDA_CHECK(cudaEventRecord(g->ev0, st));
-        k_init<RP, V><<<grid1d(nl), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, d_p.ptr<double>(), L.order,
-                                                       nl, c0 / 2.0, T[0], T[1], acc, X[0] + Vw.x_off);
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        ++launches;
-        if (pg) {
-            k_push_copy<V><<<grid1d(nl), kThreads, 0, st>>>(X[0] + Vw.x_off, nl, push_table(0), G, Vw.x_off);
-            ++launches;
-        } else {
-            CHEB_NCCL_CHECK(ncclAllGather(X[0] + Vw.x_off, X[0], (size_t)mr, nccl_type<V>(), comm(), st));
-        }
-        CHEB_CUDA_CHECK(cudaGetLastError());
-    }
-
-    // phase k: fused term k (pushes x_{k+1} to every rank) + this rank's trace partials
-    void term(int k) {
-        cudaStream_t st = g->stream;
-        const SolverView& Vw = g->view;
-        Workspace& w = g->ws;
-        TermArgs<RP, V> a = base_args<RP, V>(g, L);
-        a.x_in = X[(k - 1) & 1];
-        a.x_out = X[k & 1] + Vw.x_off;
-        if (pg) {
-            a.push = push_table(k & 1);
-            a.push_n = G;
-            a.push_off = Vw.x_off;
-        }
-        a.T = T[(k - 1) & 1];
-        a.acc = acc;
-        a.ck = coeffs[k];
-        a.first = k == 1;
-        a.part = w.part.ptr<double>() + (size_t)(k - 1) * Vw.grid * 2;
-        a.hub_part = w.hub_part.ptr<double>();
-        a.hub_cnt = w.hub_cnt.ptr<unsigned>();
-        a.hub_ts = Vw.n_hub ? w.hub_ts.ptr<double>() + (size_t)(k - 1) * Vw.n_hub * 2 : nullptr;
-        if (tev) CHEB_CUDA_CHECK(cudaEventRecord((*tev)[2 * (k - 1)], st));
-        launches += launch_pass<EPI_CPAA>(g, L, a);
-        if (tev) CHEB_CUDA_CHECK(cudaEventRecord((*tev)[2 * (k - 1) + 1], st));
-        if (fused_tail) {
-            ++pg->epoch;
-            cudaLaunchConfig_t tc = {};
-            tc.gridDim = dim3(1);
-            tc.blockDim = dim3(256);
-            tc.stream = st;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            at[0].val.programmaticStreamSerializationAllowed = 1;
-            tc.attrs = at;
-            tc.numAttrs = tuning().pdl ? 1 : 0;
-            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&tc, k_term_tail, (const double*)w.part.ptr<double>(), Vw.grid,
-                                               (const double*)w.hub_ts.ptr<double>(), (int)Vw.n_hub, k - 1,
-                                               w.trace.ptr<double>(), flag_table(),
-                                               (const unsigned long long*)pg->flags, G, pg->rank, pg->epoch));
-        } else {
-            k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), Vw.grid, w.hub_ts.ptr<double>(),
-                                                   (int)Vw.n_hub, k - 1, w.trace.ptr<double>());
-        }
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        ++launches;
-        if (!pg) {  // x_{k+1}: every rank's slot -> every rank (in place, equal counts)
-            CHEB_NCCL_CHECK(ncclAllGather(X[k & 1] + Vw.x_off, X[k & 1], (size_t)mr, nccl_type<V>(), comm(), st));
-        }
-    }
-
-    // phase M+1: every rank's trace (or, for M = 0, its acc total) to every rank
-    void trace_out() {
-        cudaStream_t st = g->stream;
-        Workspace& w = g->ws;
-        if (M == 0) {
-            const int eg = grid1d(nl);
-            k_sum_blocks<V><<<eg, kThreads, 0, st>>>(acc, nl, w.part.ptr<double>());
-            k_sum_final<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), eg, w.total.ptr<double>());
-            launches += 2;
-        }
-        const double* src = M > 0 ? w.trace.ptr<double>() : w.total.ptr<double>();
-        const int len = M > 0 ? 2 * M : 1;
-        if (pg) {
-            k_push_copy<double><<<1, kThreads, 0, st>>>(src, len, trace_table(), G, (int64_t)pg->rank * stride);
-            ++launches;
-        } else {
-            CHEB_NCCL_CHECK(ncclAllGather(src, trace_all.ptr<double>(), (size_t)len, ncclDouble, comm(), st));
-        }
-        CHEB_CUDA_CHECK(cudaGetLastError());
-    }
-
-    // phase M+2: combine the traces in rank order, normalise the local rows, send them
-    void normalize() {
-        cudaStream_t st = g->stream;
-        const SolverView& Vw = g->view;
-        const double* all = pg ? static_cast<const double*>(pg->trace_all) : trace_all.ptr<double>();
-        const int len = M > 0 ? 2 * M : 1;
-        k_sum_ranks_strided<<<1, 256, 0, st>>>(all, G, len, pg ? stride : len, tglob.ptr<double>());
-        d_total = M > 0 ? tglob.ptr<double>() + 2 * (M - 1) + 1 : tglob.ptr<double>();
-        if (pg) {
-            k_normalize_push<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf_table(), G, Vw.x_off);
-        } else {
-            k_normalize_slot<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf.ptr<V>() + Vw.x_off);
-            CHEB_NCCL_CHECK(ncclAllGather(rbuf.ptr<V>() + Vw.x_off, rbuf.ptr<V>(), (size_t)mr, nccl_type<V>(), comm(), st));
-        }
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        launches += 2;
-    }
-
-    // phase M+3: padded ranks -> vertex order; read back the trace, check it
-    void finish(std::vector<double>* tr, double* total) {
-        cudaStream_t st = g->stream;
-        const SolverView& Vw = g->view;
-        Workspace& w = g->ws;
-        const V* padded = pg ? static_cast<const V*>(pg->rbuf) : rbuf.ptr<V>();
-        k_unpermute_padded<V><<<grid1d(Vw.x_len), kThreads, 0, st>>>(padded, dcuts.ptr<int64_t>(), G, mr,
-                                                                    Vw.order_full.ptr<int>(), w.out.ptr<V>());
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        ++launches;
-        CHEB_CUDA_CHECK(cudaEventRecord(g->ev1, st));
-        g->last_terms = M;
-        g->last_launches = launches;
-        w.launches = launches;
-        std::vector<double> t(2 * (size_t)std::max(M, 1));
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), tglob.get(), sizeof(double) * (M > 0 ? 2 * M : 1),
-                                        cudaMemcpyDeviceToHost, st));
-        unsigned long long timed_out = 0;
-        if (pg)
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(&timed_out, pg->flags + G, sizeof timed_out, cudaMemcpyDeviceToHost, st));
-        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-        if (timed_out) fail(CHEB_CUDA, "push exchange barrier timed out (a peer stopped signalling)");
-        float ms = 0.f;
-        CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
-        g->last_loop_ms = ms;
-        for (int k = 1; k <= M; ++k)
-            if (!std::isfinite(t[2 * (k - 1)]) || !std::isfinite(t[2 * (k - 1) + 1]))
-                fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(k));
-        const double tot = M > 0 ? t[2 * (M - 1) + 1] : t[0];
-        if (!std::isfinite(tot) || tot <= 0.0) fail(CHEB_NUMERIC, "normalization total is not positive and finite");
-        if (tr) *tr = t;
-        if (total) *total = tot;
-    }
-
-    // push barrier, one rank per process: publish, then wait for every rank
-    void signal() {
-        ++pg->epoch;
-        k_peer_signal<<<1, 32, 0, g->stream>>>(flag_table(), G, pg->rank, pg->epoch);
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        if (pg->lockstep) CHEB_CUDA_CHECK(cudaEventRecord(pg->signalled, g->stream));
-        ++launches;
-    }
-    void wait() {
-        k_peer_wait<<<1, 32, 0, g->stream>>>(pg->flags, G, pg->epoch);
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        ++launches;
-    }
-};
-
-template <class RP, class V>
-void run_solve_dist(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, double* total,
-                    std::vector<double>* term_ms = nullptr) {
-    std::vector<cudaEvent_t> tev;
-    if (term_ms) {
-        tev.resize(2 * (size_t)std::max(s.M, 1));
-        for (auto& e : tev) CHEB_CUDA_CHECK(cudaEventCreate(&e));
-    }
-    DistSolve<RP, V> d(g, s, term_ms ? &tev : nullptr);
-    const bool push = d.pg != nullptr;
-    auto barrier = [&] {
-        if (push) {
-            d.signal();
-            d.wait();
-        }
-    };
-    d.begin();
-    barrier();
-    for (int k = 1; k <= s.M; ++k) {
-        d.term(k);
-        if (!d.fused_tail) barrier();  // (fused: the term's tail kernel was the barrier)
-    }
-    d.trace_out();
-    barrier();
-    d.normalize();
-    barrier();
-    d.finish(tr, total);
-    if (term_ms) {
-        term_ms->assign(s.M, 0.0);
-        for (int k = 0; k < s.M; ++k) {
-            float tk = 0.f;
-            CHEB_CUDA_CHECK(cudaEventElapsedTime(&tk, tev[2 * k], tev[2 * k + 1]));
-            (*term_ms)[k] = tk;
-        }
-        for (auto& e : tev) cudaEventDestroy(e);
-    }
-}
-
-// One host thread drives every rank of a push group (one device or several): each phase is
-// enqueued on every rank's stream, then every rank signals, and each rank's wait kernel is
-// ordered (by events) after all signals — so no kernel ever spins on work that has not been
-// enqueued, and ranks sharing one GPU cannot deadlock.
-template <class RP, class V>
-void run_group_lockstep(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr,
-                        double* total) {
-    const int G = (int)gs.size();
-    std::vector<std::unique_ptr<DistSolve<RP, V>>> d;
-    for (cheb_graph* g : gs) {
-        GraphScope sc(g);
-        d.emplace_back(new DistSolve<RP, V>(g, s, nullptr));
-    }
-    auto each = [&](auto&& f) {
-        for (int r = 0; r < G; ++r) {
-            GraphScope sc(gs[r]);
-            f(*d[r]);
-        }
-    };
-    auto barrier = [&] {
-        each([](DistSolve<RP, V>& x) { x.signal(); });
-        for (int r = 0; r < G; ++r) {
-            GraphScope sc(gs[r]);
-            for (int q = 0; q < G; ++q)
-                CHEB_CUDA_CHECK(cudaStreamWaitEvent(gs[r]->stream, gs[q]->peer->signalled, 0));
-            d[r]->wait();
-        }
-    };
-    each([](DistSolve<RP, V>& x) { x.begin(); });
-    barrier();
-    for (int k = 1; k <= s.M; ++k) {
-        each([k](DistSolve<RP, V>& x) { x.term(k); });
-        barrier();
-    }
-    each([](DistSolve<RP, V>& x) { x.trace_out(); });
-    barrier();
-    each([](DistSolve<RP, V>& x) { x.normalize(); });
-    barrier();
-    for (int r = 0; r < G; ++r) {
-        GraphScope sc(gs[r]);
-        d[r]->finish(r == 0 ? tr : nullptr, r == 0 ? total : nullptr);
-    }
-}
-
 std::string solve_key(const SolveSpec& s, bool has_p) {
     char buf[160];
     std::snprintf(buf, sizeof buf, "c=%.17g M=%d mode=%d prec=%d R=%d p=%d", s.c, s.M, s.mode,
@@ -1594,7 +123,7 @@ void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::ve
     if (g->part.comm || g->peer) {
         if (h_ref) fail(CHEB_INVALID_ARG, "reference tracking is not available on a partitioned handle");
         if (s.mode != CHEB_MODE_FAST) fail(CHEB_INVALID_ARG, "a partitioned handle runs the FAST schedule only");
-        run_solve_dist<RP, V>(g, s, tr, total);
+        dist_solve(g, s, tr, total, nullptr);
         return;
     }
     cudaStream_t st = g->stream;
@@ -1695,6 +224,7 @@ void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::ve
     }
 }
 
+
 }  // namespace
 
 void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool /*host_results*/, std::vector<double>* tr,
@@ -1710,27 +240,6 @@ void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool /*host_results*/, std::v
     } else {
         if (rp64) run_solve_t<int64_t, float>(g, s, nullptr, tr, nullptr, total);
         else run_solve_t<int, float>(g, s, nullptr, tr, nullptr, total);
-    }
-}
-
-// Lockstep solve of a push group (every rank's handle driven by this thread).
-void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr, double* total) {
-    if (s.R != 1) fail(CHEB_INVALID_ARG, "R > 1 is served by the batched path");
-    if (s.mode != CHEB_MODE_FAST) fail(CHEB_INVALID_ARG, "a partitioned handle runs the FAST schedule only");
-    bool rp64 = false;
-    for (cheb_graph* g : gs) {
-        GraphScope sc(g);
-        ensure_view(g);
-        rp64 = rp64 || g->view.rp64;
-    }
-    for (cheb_graph* g : gs)
-        if (g->view.rp64 != rp64) fail(CHEB_INVALID_ARG, "group members disagree on row-pointer width");
-    if (s.precision == CHEB_FP64) {
-        if (rp64) run_group_lockstep<int64_t, double>(gs, s, tr, total);
-        else run_group_lockstep<int, double>(gs, s, tr, total);
-    } else {
-        if (rp64) run_group_lockstep<int64_t, float>(gs, s, tr, total);
-        else run_group_lockstep<int, float>(gs, s, tr, total);
     }
 }
 
@@ -1757,7 +266,7 @@ void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_m
         using V = decltype(v_tag);
         if (g->part.comm || g->peer) {
             if (g->peer && g->peer->lockstep) fail(CHEB_INVALID_ARG, "profile a lockstep group through cheb_group_cpaa");
-            run_solve_dist<RP, V>(g, s, nullptr, nullptr, &term_ms);
+            dist_solve(g, s, nullptr, nullptr, &term_ms);
             return;
         }
         const Layout L = layout_of(g, s.mode);
@@ -1806,352 +315,4 @@ void read_ranks(cheb_graph* g, int precision, double* ranks) {
     }
     CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
 }
-
-// ---------------- Power method (power.cpp:28-109) -------------------------------------
-namespace {
-template <class RP>
-void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int mode,
-             const double* h_ref, double* ranks, cheb_trace_row* trace, int cap, int* rounds_out,
-             double* total) {
-    cudaStream_t st = g->stream;
-    const Layout L = layout_of(g, mode);
-    const int64_t n = g->n;
-    ensure_workspace<double>(g, std::max(budget, 1), 1);
-    Workspace& w = g->ws;
-    double* X = w.T0.ptr<double>();                 // x (in place)
-    double* C[2] = {w.X0.ptr<double>(), w.X1.ptr<double>()};
-    const double base = (1.0 - c) / (double)n;
-    const double x0 = 1.0 / (double)n;
-    {   // x = e/n, contrib = x D^-1
-        std::vector<double> h(n, x0);
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(X, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
-        k_prescale<RP, double><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, X, n, C[0]);
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-    }
-    DevMem d_ref, d_err;
-    if (h_ref) {
-        d_ref.alloc(sizeof(double) * n);
-        DevMem tmp(sizeof(double) * n);
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(tmp.get(), h_ref, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-        k_permute_in<double><<<grid1d(n), kThreads, 0, st>>>(tmp.ptr<double>(), L.order, n, d_ref.ptr<double>());
-        d_err.alloc(sizeof(double) * (2 * (size_t)grid1d(n) + 8));
-    }
-    double* dtr = w.trace.ptr<double>();
-    const int grid = L.fast ? g->view.grid : 0;
-    int k = 0;
-    // Speculative batches of rounds (no reference tracking): every round's x is snapshotted,
-    // the batch's L1 changes and masses are read back once, and the solve stops at the first
-    // round that meets tol — its x is in the snapshots, so the result is the per-round one.
-    const int B = h_ref ? 0 : (int)std::min<int64_t>(16, std::max(budget, 1));
-    DevMem snaps;
-    if (B > 0) {
-        size_t free_b = 0, total_b = 0;
-        cudaMemGetInfo(&free_b, &total_b);
-        if (sizeof(double) * (size_t)(B + 1) * (size_t)n <= free_b / 4)
-            snaps.alloc(sizeof(double) * (size_t)(B + 1) * (size_t)n);
-    }
-    // per-round kernel time for the trace's elapsed_ms (power.cpp:92: the round's kernel)
-    std::vector<cudaEvent_t> rev(2 * (size_t)std::max(B, 1));
-    for (auto& e : rev) CHEB_CUDA_CHECK(cudaEventCreate(&e));
-    struct EvFree {
-        std::vector<cudaEvent_t>& v;
-        ~EvFree() {
-            for (auto e : v) cudaEventDestroy(e);
-        }
-    } ev_free{rev};
-    auto round_ms = [&](int j) {
-        float ms = 0.f;
-        CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, rev[2 * j], rev[2 * j + 1]));
-        return (double)ms;
-    };
-    if (snaps) {
-        double* S = snaps.ptr<double>();
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(S, X, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-        const double* final_x = S;
-        bool done = budget == 0;
-        while (!done) {
-            const int nb = std::min(B, budget - k);
-            for (int j = 1; j <= nb; ++j) {
-                const int kk = k + j;
-                double* Sj = S + (size_t)j * n;
-                CHEB_CUDA_CHECK(cudaMemcpyAsync(Sj, Sj - n, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-                TermArgs<RP, double> a = base_args<RP, double>(g, L);
-                a.x_in = C[(kk - 1) & 1];
-                a.x_out = C[kk & 1];
-                a.T = Sj;  // in: x_{k-1}; out: y = x_k
-                a.ck = c;
-                a.base = base;
-                a.first = 0;
-                if (L.fast) {
-                    a.part = w.part.ptr<double>();
-                    a.hub_part = w.hub_part.ptr<double>();
-                    a.hub_cnt = w.hub_cnt.ptr<unsigned>();
-                    a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() : nullptr;
-                }
-                CHEB_CUDA_CHECK(cudaEventRecord(rev[2 * (j - 1)], st));
-                launch_pass<EPI_POWER>(g, L, a);
-                CHEB_CUDA_CHECK(cudaEventRecord(rev[2 * (j - 1) + 1], st));
-                if (L.fast)
-                    k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub,
-                                                           0, dtr + 2 * (j - 1));
-                CHEB_CUDA_CHECK(cudaGetLastError());
-            }
-            if (!L.fast) {
-                k_power_many<<<(2 * nb + 31) / 32, 32, 0, st>>>(S, n, nb, dtr);
-                CHEB_CUDA_CHECK(cudaGetLastError());
-            }
-            std::vector<double> h(2 * (size_t)nb);
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(h.data(), dtr, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, st));
-            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-            int stop = 0;
-            for (int j = 1; j <= nb && !stop; ++j) {
-                const int kk = k + j;
-                if (trace && kk <= cap) {
-                    cheb_trace_row& r = trace[kk - 1];
-                    std::memset(&r, 0, sizeof r);
-                    r.k = kk;
-                    r.l1_change = h[2 * (j - 1)];
-                    r.mass_T = h[2 * (j - 1) + 1];
-                    r.elapsed_ms = round_ms(j - 1);
-                }
-                if (!std::isfinite(h[2 * (j - 1)])) fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(kk));
-                if (by_tol && h[2 * (j - 1)] < tol) stop = j;
-            }
-            if (stop) {
-                k += stop;
-                final_x = S + (size_t)stop * n;
-                done = true;
-            } else {
-                k += nb;
-                final_x = S + (size_t)nb * n;
-                done = k >= budget;
-                if (!done)  // next batch starts from this batch's last x
-                    CHEB_CUDA_CHECK(cudaMemcpyAsync(S, final_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-                if (!done) final_x = S;
-            }
-        }
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(X, final_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-    }
-    while (!snaps && k < budget) {
-        ++k;
-        TermArgs<RP, double> a = base_args<RP, double>(g, L);
-        a.x_in = C[(k - 1) & 1];
-        a.x_out = C[k & 1];
-        a.T = X;
-        a.ck = c;
-        a.base = base;
-        a.first = 0;
-        if (L.fast) {
-            a.part = w.part.ptr<double>();
-            a.hub_part = w.hub_part.ptr<double>();
-            a.hub_cnt = w.hub_cnt.ptr<unsigned>();
-            a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() : nullptr;
-        }
-        CHEB_CUDA_CHECK(cudaEventRecord(rev[0], st));
-        if (!L.fast) {
-            // y goes to a separate buffer so the Kahan L1 sees old and new x (power.cpp:80-86)
-            a.T = w.acc.ptr<double>();
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(a.T, X, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-            CHEB_CUDA_CHECK(cudaEventRecord(rev[0], st));
-            launch_pass<EPI_POWER>(g, L, a);
-            CHEB_CUDA_CHECK(cudaEventRecord(rev[1], st));
-            k_serial_sums<1><<<1, 256, 0, st>>>(a.T, X, n, dtr);
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(X, a.T, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
-        } else {
-            launch_pass<EPI_POWER>(g, L, a);
-            CHEB_CUDA_CHECK(cudaEventRecord(rev[1], st));
-            k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub, 0, dtr);
-        }
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        double err2[2] = {0.0, 0.0};
-        if (h_ref) {
-            const int eg = grid1d(n);
-            k_err<double><<<eg, kThreads, 0, st>>>(X, d_ref.ptr<double>(), n, nullptr, 0, d_err.ptr<double>() + 4);
-            k_err_final<<<1, kThreads, 0, st>>>(d_err.ptr<double>() + 4, eg, d_err.ptr<double>());
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(err2, d_err.get(), sizeof err2, cudaMemcpyDeviceToHost, st));
-        }
-        double h[2];
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(h, dtr, sizeof h, cudaMemcpyDeviceToHost, st));
-        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-        if (trace && k <= cap) {
-            cheb_trace_row& r = trace[k - 1];
-            std::memset(&r, 0, sizeof r);
-            r.k = k;
-            r.l1_change = h[0];
-            r.mass_T = h[1];
-            r.elapsed_ms = round_ms(0);
-            r.err = err2[0];
-            r.err_l1 = err2[1];
-        }
-        if (!std::isfinite(h[0])) fail(CHEB_NUMERIC, "non-finite value at round " + std::to_string(k));
-        if (by_tol && h[0] < tol) break;
-    }
-    // ranks = x (original order); total = Kahan(x) on the host (power.cpp:105-107)
-    std::vector<double> xs(n);
-    DevMem o(sizeof(double) * n);
-    k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(X, L.order, n, o.ptr<double>());
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, o.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-    *rounds_out = k;
-    *total = kahan_sum(ranks, n);
-}
-}  // namespace
-
-void power_solve(cheb_graph* g, double c, int rounds, double tol, int max_rounds, int mode,
-                 const double* reference, double* ranks, cheb_trace_row* trace, int cap,
-                 int* rounds_out, double* total) {
-    GraphScope gs(g);
-    const bool fixed = rounds >= 0;
-    const int budget = fixed ? rounds : max_rounds;
-    const bool rp64 = mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
-    if (rp64) power_t<int64_t>(g, c, budget, !fixed, tol, mode, reference, ranks, trace, cap, rounds_out, total);
-    else power_t<int>(g, c, budget, !fixed, tol, mode, reference, ranks, trace, cap, rounds_out, total);
-}
-
-// ---------------- transition_apply (graph.cpp:104-121) --------------------------------
-namespace {
-template <class RP>
-void transition_t(cheb_graph* g, const double* x, double* y, int mode) {
-    cudaStream_t st = g->stream;
-    const Layout L = layout_of(g, mode);
-    const int64_t n = g->n;
-    ensure_workspace<double>(g, 1, 1);
-    Workspace& w = g->ws;
-    DevMem dx(sizeof(double) * n);
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(dx.get(), x, sizeof(double) * n, cudaMemcpyHostToDevice, st));
-    k_permute_in<double><<<grid1d(n), kThreads, 0, st>>>(dx.ptr<double>(), L.order, n, w.T0.ptr<double>());
-    k_prescale<RP, double><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv,
-                                                          w.T0.ptr<double>(), n, w.X0.ptr<double>());
-    TermArgs<RP, double> a = base_args<RP, double>(g, L);
-    a.x_in = w.X0.ptr<double>();
-    a.out = w.T1.ptr<double>();
-    if (L.fast) {
-        a.hub_part = w.hub_part.ptr<double>();
-        a.hub_cnt = w.hub_cnt.ptr<unsigned>();
-    }
-    launch_pass<EPI_PLAIN>(g, L, a);
-    k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(w.T1.ptr<double>(), L.order, n, dx.ptr<double>());
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(y, dx.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
-    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-}
-}  // namespace
-
-void transition_apply(cheb_graph* g, const double* x, double* y, int mode) {
-    GraphScope gs(g);
-    const bool rp64 = mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
-    if (rp64) transition_t<int64_t>(g, x, y, mode);
-    else transition_t<int>(g, x, y, mode);
-}
-
-// ---------------- staged API (cpaa.cpp:167-196) ---------------------------------------
-void staged_init(cheb_graph* g, double c0, int mode) {
-    GraphScope gs(g);
-    StagedState& S = g->staged;
-    const int64_t n = g->n;
-    const size_t vb = sizeof(double) * std::max<int64_t>(n, 1);
-    S.T_prev.ensure(vb);
-    S.T_curr.ensure(vb);
-    S.T_next.ensure(vb);
-    S.acc.ensure(vb);
-    S.x.ensure(vb);
-    S.mode = mode;
-    S.k = 1;
-    S.active = true;
-    std::vector<double> ones(n, 1.0), half(n, c0 / 2.0), zero(n, 0.0);
-    staged_set(g, ones.data(), ones.data(), half.data(), 1);
-    CHEB_CUDA_CHECK(cudaMemcpy(S.T_next.get(), zero.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
-}
-
-void staged_set(cheb_graph* g, const double* Tp, const double* Tc, const double* acc, int k) {
-    GraphScope gs(g);
-    StagedState& S = g->staged;
-    if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
-    const Layout L = layout_of(g, S.mode);
-    const int64_t n = g->n;
-    DevMem tmp(sizeof(double) * std::max<int64_t>(n, 1));
-    auto put = [&](const double* h, DevMem& d) {
-        if (!h) return;
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(tmp.get(), h, sizeof(double) * n, cudaMemcpyHostToDevice, g->stream));
-        k_permute_in<double><<<grid1d(n), kThreads, 0, g->stream>>>(tmp.ptr<double>(), L.order, n, d.ptr<double>());
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
-    };
-    put(Tp, S.T_prev);
-    put(Tc, S.T_curr);
-    put(acc, S.acc);
-    if (k > 0) S.k = k;
-}
-
-namespace {
-template <class RP>
-void staged_generate_t(cheb_graph* g) {
-    StagedState& S = g->staged;
-    const Layout L = layout_of(g, S.mode);
-    const int64_t n = g->n;
-    ensure_workspace<double>(g, 1, 1);
-    cudaStream_t st = g->stream;
-    // contrib = T_curr D^-1 (cpaa.cpp:180-182), then gather + recurrence (:183-189)
-    k_prescale<RP, double><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv,
-                                                          S.T_curr.ptr<double>(), n, S.x.ptr<double>());
-    TermArgs<RP, double> a = base_args<RP, double>(g, L);
-    a.x_in = S.x.ptr<double>();
-    a.T_prev = S.T_prev.ptr<double>();
-    a.out = S.T_next.ptr<double>();
-    a.first = S.k == 1;
-    if (L.fast) {
-        a.hub_part = g->ws.hub_part.ptr<double>();
-        a.hub_cnt = g->ws.hub_cnt.ptr<unsigned>();
-    }
-    launch_pass<EPI_GEN>(g, L, a);
-    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-}
-}  // namespace
-
-void staged_generate(cheb_graph* g) {
-    GraphScope gs(g);
-    if (!g->staged.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
-    const bool rp64 = g->staged.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
-    if (rp64) staged_generate_t<int64_t>(g);
-    else staged_generate_t<int>(g);
-}
-
-void staged_accumulate(cheb_graph* g, double ck) {
-    GraphScope gs(g);
-    StagedState& S = g->staged;
-    if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
-    k_accumulate<double><<<grid1d(g->n), kThreads, 0, g->stream>>>(S.acc.ptr<double>(), S.T_next.ptr<double>(), g->n, ck);
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
-}
-
-void staged_rotate(cheb_graph* g) {
-    StagedState& S = g->staged;
-    if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
-    std::swap(S.T_prev, S.T_curr);
-    std::swap(S.T_curr, S.T_next);
-    S.k += 1;
-}
-
-void staged_get(cheb_graph* g, double* Tp, double* Tc, double* Tn, double* acc, int* k) {
-    GraphScope gs(g);
-    StagedState& S = g->staged;
-    if (!S.active) fail(CHEB_INVALID_ARG, "staged state not initialised");
-    const Layout L = layout_of(g, S.mode);
-    const int64_t n = g->n;
-    DevMem tmp(sizeof(double) * std::max<int64_t>(n, 1));
-    auto get = [&](double* h, DevMem& d) {
-        if (!h) return;
-        k_permute_out<double><<<grid1d(n), kThreads, 0, g->stream>>>(d.ptr<double>(), L.order, n, tmp.ptr<double>());
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(h, tmp.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream));
-        CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
-    };
-    get(Tp, S.T_prev);
-    get(Tc, S.T_curr);
-    get(Tn, S.T_next);
-    get(acc, S.acc);
-    if (k) *k = S.k;
-}
-
 }  // namespace chebgpu

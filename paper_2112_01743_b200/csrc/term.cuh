@@ -1,0 +1,1042 @@
+// Device side of the CPAA path, shared by the drivers (cpaa.cu single GPU, dist.cu row
+// partition, power.cu Power / transition_apply / staged API): kernels, the launch helper
+// and the solve workspace.  Everything here has internal linkage (each driver translation
+// unit instantiates what it launches).
+//
+// The reference round (/root/reference/proj/src/cpaa.cpp:109-156) is a pre-scale pass
+// contrib = T_k * D^-1 (:116), a CSR gather with the three-term recurrence
+// T_{k+1} = (k==1 ? s : 2s - T_{k-1}) and the coefficient accumulation acc += c_k T_{k+1}
+// (:126-132), two serial Kahan trace sums (:142-143) and a finite check (:147-148).  Here one
+// term kernel does all of it:
+//
+//   s_u        = sum_{v in N(u)} x_k[v]                (warp-tiled gather)
+//   t          = first ? s_u : 2 s_u - T_{k-1}[u]      (recurrence, in place over T_{k-1})
+//   acc[u]    += c_k * t                               (separate mul/add: reference rounding)
+//   x_{k+1}[u] = t * (1/deg u)                         (next term's D^-1 pre-scale, fused)
+//   block partials of sum(t), sum(acc)                 (trace, fixed order, deterministic)
+//
+// Two schedules:
+//  * FAST (the product path, k_term_warp): rows relabelled by degree (descending); a
+//    persistent CTA of 32 warps per SM; every warp walks a static program of tiles (<= 32
+//    rows and <= 248 entries with 2^b lanes per row, or 248-entry chunks of a hub row that
+//    k_hub_finalize completes in chunk order), column ids by TMA, the hottest x entries
+//    from a shared-memory prefix.  Sums differ from the reference only in association order
+//    (<= 1e-12 max-abs, tests).
+//  * BITEXACT (k_term_exact): thread-per-row storage-order sums on the reference-order CSR,
+//    explicit round-to-nearest mul/add, the reference's serial Kahan trace sums: bitwise
+//    equal to the reference (ranks and trace).
+#pragma once
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include <nccl.h>
+
+#include "common.cuh"
+#include "device.cuh"
+
+#define CHEB_NCCL_CHECK(expr)                                                              \
+    do {                                                                                   \
+        ncclResult_t _r = (expr);                                                          \
+        if (_r != ncclSuccess)                                                             \
+            ::chebgpu::fail(CHEB_NCCL, std::string("NCCL error ") + ncclGetErrorString(_r) + \
+                                           " at " __FILE__ ":" + std::to_string(__LINE__)); \
+    } while (0)
+
+
+namespace chebgpu {
+namespace {
+
+enum Epi : int {
+    EPI_CPAA = 0,   // fused CPAA term (cpaa.cpp:126-132 + :116 for the next round)
+    EPI_GEN = 1,    // staged generate_stage (cpaa.cpp:178-190): T_next only
+    EPI_POWER = 2,  // power round (power.cpp:60-86): y = c s + base
+    EPI_PLAIN = 3   // transition_apply (graph.cpp:104-121): y = s
+};
+
+template <class RP, class V>
+struct TermArgs {
+    const RP* __restrict__ rp;
+    const int* __restrict__ col;
+    const double* __restrict__ inv;  // non-null iff non-canonical inv_degree
+    const V* __restrict__ x_in;      // x_k = T_k D^-1
+    V* __restrict__ x_out;           // x_{k+1}
+    V* T;                            // CPAA: T_{k-1} in, T_{k+1} out (in place); POWER: x in/out
+    const V* T_prev;                 // GEN: T_{k-1}
+    V* out;                          // GEN: T_next; PLAIN: y
+    V* acc;
+    double ck;    // CPAA: c_k ; POWER: c
+    double base;  // POWER: (1-c)/n
+    int first;
+    double* part;  // [grid][2] this term
+    double* hub_part;  // [n_tiles] chunk partials
+    unsigned* hub_cnt;
+    double* hub_ts;  // [n_hub][2] this term
+    int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
+    int tune_skip;      // experiments only: 1 skip chunk tiles, 2 skip pack tiles, 16+b only bin b
+    // fused push exchange (partitioned runs): x_{k+1}[u] is stored at push[r][push_off + u]
+    // for every rank r (peer memory over NVLink) instead of x_out[u]
+    V* const* push;
+    int push_n;
+    int64_t push_off;
+};
+
+// Row epilogue.  u is a row of the current layout; deg its row length.
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void epilogue(const TermArgs<RP, V>& a, int64_t u, V s, int64_t deg,
+                                         double& p0, double& p1) {
+    if constexpr (EPI == EPI_PLAIN) {
+        a.out[u] = s;
+    } else {
+        const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
+        if constexpr (EPI == EPI_CPAA) {
+            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), a.T[u]);
+            a.T[u] = t;
+            const V nacc = add_rn(a.acc[u], mul_rn((V)a.ck, t));
+            a.acc[u] = nacc;
+            a.x_out[u] = mul_rn(t, inv);
+            p0 += (double)t;
+            p1 += (double)nacc;
+        } else if constexpr (EPI == EPI_GEN) {
+            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), a.T_prev[u]);
+            a.out[u] = t;
+        } else {  // EPI_POWER
+            const V y = add_rn(mul_rn((V)a.ck, s), (V)a.base);
+            const V old = a.T[u];
+            a.T[u] = y;
+            a.x_out[u] = mul_rn(y, inv);
+            p0 += fabs((double)y - (double)old);
+            p1 += (double)y;
+        }
+    }
+}
+
+// ---------------- FAST: persistent warp-tiled schedule ---------------------------------
+//
+// The view's rows are sorted by degree (descending) and cut into WARP tiles (build.cu):
+//  * pack tiles: <= 32 consecutive whole rows with <= kWarpNnz (256) nnz;
+//  * chunk tiles: a slice of <= kWarpNnz (256) nnz of a row with degree > kWarpNnz;
+//    a row with several chunks is finished by the last chunk to arrive, which combines
+//    the chunk partials in chunk order (deterministic).
+// One CTA of 32 warps per SM; each warp walks tiles blockIdx*32+warp, +gridDim*32, ...
+// (static, deterministic) with no CTA barrier inside the term: per tile a lane issues
+// its 8 column-id loads, the row end pointer, T_{k-1} and acc at once, then 8 gathers.
+// Gathers of the hottest vertices (ids < H: the degree-sorted hub prefix, ~50% of all
+// gathers on power-law graphs) hit a shared-memory copy of x_k[0..H) refreshed at the
+// start of every term; the rest go through L1/L2.  Measured on B200
+// (tools/micro_gather.cu): random LDS.64 876 G/s vs random LDG over an L2-resident
+// table 256 G/s — the gather, not HBM, bounds this path.
+
+// Cold x gathers: read-only path without L1 allocation (the L1 left next to the shared
+// hot prefix is tiny; a random line would only evict another).
+#ifndef CHEB_COLD_NOALLOC
+#define CHEB_COLD_NOALLOC 0
+#endif
+__device__ __forceinline__ double ldg_cold(const double* p) {
+#if CHEB_COLD_NOALLOC
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float ldg_cold(const float* p) {
+#if CHEB_COLD_NOALLOC
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
+__device__ __forceinline__ double lds_v(unsigned addr, double) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float lds_v(unsigned addr, float) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+// Gather x[c[q]] for a lane's column ids: cold ids (>= H) as predicated global loads
+// issued back to back, hot ids from the shared-memory copy at 32-bit address hot_s;
+// c < 0 = no element (0).
+template <class V, int U>
+__device__ __forceinline__ void gather8(const V* __restrict__ x, unsigned hot_s, int H, const int (&c)[U],
+                                        V (&v)[U]) {
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+        v[q] = V(0);
+        if (c[q] >= H) v[q] = ldg_cold(x + c[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q)
+        if ((unsigned)c[q] < (unsigned)H) v[q] = lds_v(hot_s + (unsigned)c[q] * (unsigned)sizeof(V), V(0));
+}
+
+// Programmatic dependent launch: let the next kernel of the stream launch now (its CTAs
+// take SMs as this grid drains), and wait for the previous kernel's completion + memory
+// flush before reading anything it wrote.  Both are no-ops without the launch attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// TMA bulk copy global -> shared (cp.async.bulk), completion on an mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* mbar) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 :: "r"(dst), "l"(gsrc), "r"(bytes), "r"(bar) : "memory");
+}
+// Column ids are read once per term: an L2 evict-first policy on their TMA copies keeps the
+// per-term streams (~130 MB on C2, about the size of L2) from pushing x out of L2
+// (C2 73.2 -> 70.1 us/term; profiles/r01_gather_microbench.md).
+__device__ __forceinline__ void bulk_g2s_stream(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* mbar) {
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        :: "r"(dst), "l"(gsrc), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, unsigned count) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mbar, unsigned bytes) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+    asm volatile(
+        "{\n"
+        ".reg .pred done;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n"
+        "@!done bra WAIT_%=;\n"
+        "}\n" :: "r"(bar), "r"(parity) : "memory");
+}
+
+// Row epilogue with the row's operands already loaded (prev = T_{k-1} / old x).
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, V s, int64_t deg,
+                                           V prev, V accv, double& p0, double& p1) {
+    if constexpr (EPI == EPI_PLAIN) {
+        a.out[u] = s;
+    } else {
+        const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
+        if constexpr (EPI == EPI_CPAA) {
+            const V t = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
+            a.T[u] = t;
+            const V nacc = add_rn(accv, mul_rn((V)a.ck, t));
+            a.acc[u] = nacc;
+            const V xn = mul_rn(t, inv);
+            if (a.push) {  // fused exchange: straight into every rank's copy of x_{k+1}
+                for (int r = 0; r < a.push_n; ++r) a.push[r][a.push_off + u] = xn;
+            } else {
+                a.x_out[u] = xn;
+            }
+            p0 += (double)t;
+            p1 += (double)nacc;
+        } else if constexpr (EPI == EPI_GEN) {
+            a.out[u] = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
+        } else {  // EPI_POWER
+            const V y = add_rn(mul_rn((V)a.ck, s), (V)a.base);
+            a.T[u] = y;
+            a.x_out[u] = mul_rn(y, inv);
+            p0 += fabs((double)y - (double)prev);
+            p1 += (double)y;
+        }
+    }
+}
+
+template <int EPI, class RP, class V>
+__device__ __forceinline__ const V* prev_src(const TermArgs<RP, V>& a) {
+    if constexpr (EPI == EPI_GEN) return a.T_prev;
+    else return a.T;
+}
+
+template <class V>
+__device__ __forceinline__ V warp_sum_v(V v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <class V>
+constexpr int hot_capacity() { return (kHotBytes / (int)sizeof(V)); }
+
+// Per-warp shared scratch of the term kernel.
+template <class V>
+struct alignas(16) WarpScratch {
+    int colb[2][kColBuf];   // TMA landing buffers: column ids of the current / next tile
+    WTile desc[2][kDescBlock];  // TMA ring of this warp's tile program
+    uint64_t colm[2];       // mbarriers of colb
+    uint64_t descm[2];      // mbarriers of desc
+};
+
+template <class V>
+constexpr size_t warp_smem_bytes() {
+    return (size_t)kHotBytes + (size_t)kWarps * sizeof(WarpScratch<V>) + 2 * 32 * sizeof(double);
+}
+
+// Tile in registers.
+struct TileR {
+    int64_t z0;
+    int r0, rows, cnt, meta;
+};
+
+__device__ __forceinline__ TileR tile_of(const WTile& d) {
+    TileR r;
+    r.z0 = d.nnz_begin;
+    r.r0 = d.row_begin;
+    r.cnt = d.cnt;
+    r.rows = d.rows;
+    r.meta = d.meta;
+    return r;
+}
+
+// Lane 0: bulk-copy the tile's column ids from the 8-aligned position a0 = z0 & ~7 into buf.
+__device__ __forceinline__ void issue_cols(const int* __restrict__ col, const TileR& t, int* buf,
+                                           uint64_t* mbar) {
+    const int64_t a0 = t.z0 & ~int64_t(7);
+    const unsigned bytes = (unsigned)(((t.z0 - a0) + t.cnt + 3) & ~3) * 4u;
+    mbar_expect_tx(mbar, bytes);
+    bulk_g2s_stream(buf, col + a0, bytes, mbar);
+}
+
+// Row operands of a pack tile for the lane leading row g's lane group (L = 1 << lg lanes
+// per row): tile-local row start/end, T_{k-1}, acc.
+template <class V>
+struct RowOps {
+    int rs, re;
+    V pv, av;
+};
+
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR& t, RowOps<V>& o) {
+    const int lane = threadIdx.x & 31;
+    o.rs = 0;
+    o.re = 0;
+    o.pv = V(0);
+    o.av = V(0);
+    if (t.meta & kTileChunk) return;
+    const int lg = t.meta & 0xf;
+    const int g = lane >> lg;
+    if ((lane & ((1 << lg) - 1)) == 0 && g < t.rows) {
+        o.rs = (int)(a.rp[t.r0 + g] - t.z0);
+        o.re = (int)(a.rp[t.r0 + g + 1] - t.z0);
+        if constexpr (EPI != EPI_PLAIN) o.pv = prev_src<EPI>(a)[t.r0 + g];
+        if constexpr (EPI == EPI_CPAA) o.av = a.acc[t.r0 + g];
+    }
+}
+
+// Lane 0: bulk-copy descriptor block blk of this warp's program into ring slot blk & 1.
+__device__ __forceinline__ void issue_desc(const WTile* my, int blk, WarpScratch<double>* unused,
+                                           WTile* slot, uint64_t* mbar) {
+    (void)unused;
+    mbar_expect_tx(mbar, kDescBlock * sizeof(WTile));
+    bulk_g2s(slot, my + (size_t)blk * kDescBlock, kDescBlock * sizeof(WTile), mbar);
+}
+
+#ifndef CHEB_PACK_UNROLL
+#define CHEB_PACK_UNROLL 4
+#endif
+constexpr int kPackUnroll = CHEB_PACK_UNROLL;  // gathers in flight per lane in pack tiles
+
+// One tile of the warp's program.  cur: this tile's row operands (loaded one tile ago);
+// nxt receives the next tile's.  No register prefetched here is copied at the end.
+template <int EPI, class RP, class V, class WS>
+__device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot_s, int H, WS& ws,
+                                          const WTile* my, int w, int S, int nt, int i,
+                                          const RowOps<V>& cur, RowOps<V>& nxt, double& p0, double& p1) {
+    const int lane = threadIdx.x & 31;
+    constexpr int U = 8;
+    const TileR d = tile_of(ws.desc[(i / kDescBlock) & 1][i % kDescBlock]);
+    if (i + 1 < nt) {
+        const int j = i + 1;
+        if (j % kDescBlock == 0) mbar_wait(&ws.descm[(j / kDescBlock) & 1], ((j / kDescBlock) >> 1) & 1);
+        const TileR dn = tile_of(ws.desc[(j / kDescBlock) & 1][j % kDescBlock]);
+        if (lane == 0) issue_cols(a.col, dn, ws.colb[j & 1], &ws.colm[j & 1]);
+        load_rows<EPI>(a, dn, nxt);
+    }
+    const int t = w + i * S;  // tile id (slot of a hub-row partial)
+    mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
+    if (a.tune_skip &&
+        (a.tune_skip >= 16 ? (((d.meta & kTileChunk) ? 6 : (d.meta & 0xf)) != a.tune_skip - 16)
+                           : ((a.tune_skip & 1) ? (d.meta & kTileChunk) : !(d.meta & kTileChunk)))) {
+        __syncwarp();
+        if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
+            const int blk = i / kDescBlock + 2;
+            if (blk * kDescBlock < nt) issue_desc(my, blk, nullptr, ws.desc[blk & 1], &ws.descm[blk & 1]);
+        }
+        return;
+    }
+    const int* cb = ws.colb[i & 1] + (int)(d.z0 & 7);  // tile-local position p at cb[p]
+
+    if (d.meta & kTileChunk) {
+        // slice of a row with degree > kWarpNnz: partial only; completed by k_hub_finalize
+        int c[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const int pp = lane + 32 * q;
+            c[q] = pp < d.cnt ? cb[pp] : -1;
+        }
+        V v[U];
+        if (a.tune_nogather) {
+#pragma unroll
+            for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
+        } else {
+            gather8(a.x_in, hot_s, H, c, v);
+        }
+        V sum = V(0);
+#pragma unroll
+        for (int q = 0; q < U; ++q) sum += v[q];
+        sum = warp_sum_v(sum);
+        if (lane == 0) a.hub_part[t] = (double)sum;
+    } else {
+        // rows of similar degree: L lanes per row, row g owned by lanes [g L, g L + L)
+        const int lg = d.meta & 0xf;
+        const int L = 1 << lg;
+        const int li = lane & (L - 1), g = lane >> lg;
+        int rb = cur.rs, rend = cur.re;
+        if (lg) {
+            const int leader = lane & ~(L - 1);
+            rb = __shfl_sync(0xffffffffu, rb, leader);
+            rend = __shfl_sync(0xffffffffu, rend, leader);
+        }
+        V sum = V(0);
+        for (int jj = rb + li; jj < rend; jj += kPackUnroll * L) {
+            int c[kPackUnroll];
+#pragma unroll
+            for (int q = 0; q < kPackUnroll; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
+            V v[kPackUnroll];
+            if (a.tune_nogather) {
+#pragma unroll
+                for (int q = 0; q < kPackUnroll; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
+            } else {
+                gather8(a.x_in, hot_s, H, c, v);
+            }
+#pragma unroll
+            for (int q = 0; q < kPackUnroll; ++q) sum += v[q];
+        }
+        for (int o = L >> 1; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        if (li == 0 && g < d.rows)
+            epilogue_v<EPI>(a, (int64_t)d.r0 + g, sum, (int64_t)(rend - rb), cur.pv, cur.av, p0, p1);
+    }
+    __syncwarp();
+    // descriptor block of tile i fully consumed: refill its slot two blocks ahead
+    if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
+        const int blk = i / kDescBlock + 2;
+        if (blk * kDescBlock < nt) issue_desc(my, blk, nullptr, ws.desc[blk & 1], &ws.descm[blk & 1]);
+    }
+}
+
+template <int EPI, class RP, class V>
+__global__ void __launch_bounds__(kWarps * 32, 1)
+k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles, int H) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    V* hot = reinterpret_cast<V*>(smem);
+    const unsigned hot_s = (unsigned)__cvta_generic_to_shared(smem);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    WarpScratch<V>& ws = reinterpret_cast<WarpScratch<V>*>(smem + kHotBytes)[warp];
+    double* red = reinterpret_cast<double*>(smem + kHotBytes + kWarps * sizeof(WarpScratch<V>));
+    __shared__ __align__(8) uint64_t mbar_hot;
+
+    const int S = gridDim.x * kWarps;
+    const int w = blockIdx.x * kWarps + warp;
+    const int nt = w < ntiles ? (ntiles - w + S - 1) / S : 0;
+    const WTile* my = prog + (size_t)w * P;
+
+    // hot prefix x_k[0..H) -> shared memory (TMA bulk copies; sub-16-byte tail by loads)
+    const unsigned hot_bytes = (unsigned)(H * sizeof(V)) & ~15u;
+    if (threadIdx.x == 0) mbar_init(&mbar_hot, 1);
+    if (lane == 0) {
+        mbar_init(&ws.colm[0], 1);
+        mbar_init(&ws.colm[1], 1);
+        mbar_init(&ws.descm[0], 1);
+        mbar_init(&ws.descm[1], 1);
+    }
+    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    pdl_trigger();
+    if (lane == 0) {  // this warp's tile program is static: fetch it before the dependency wait
+        if (nt > 0) issue_desc(my, 0, nullptr, ws.desc[0], &ws.descm[0]);
+        if (nt > kDescBlock) issue_desc(my, 1, nullptr, ws.desc[1], &ws.descm[1]);
+    }
+    pdl_wait();  // x_k, T, acc come from the previous kernels of the stream
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&mbar_hot, hot_bytes);
+        constexpr unsigned kPiece = 32768;
+        for (unsigned off = 0; off < hot_bytes; off += kPiece)
+            bulk_g2s(smem + off, reinterpret_cast<const unsigned char*>(a.x_in) + off,
+                     min(kPiece, hot_bytes - off), &mbar_hot);
+    }
+    for (int i = hot_bytes / sizeof(V) + threadIdx.x; i < H; i += blockDim.x) hot[i] = ldg_x(a.x_in + i);
+
+    RowOps<V> A, B;
+    if (nt > 0) {
+        mbar_wait(&ws.descm[0], 0);
+        const TileR d0 = tile_of(ws.desc[0][0]);
+        if (lane == 0) issue_cols(a.col, d0, ws.colb[0], &ws.colm[0]);
+        load_rows<EPI>(a, d0, A);
+    }
+    double p0 = 0.0, p1 = 0.0;
+    mbar_wait(&mbar_hot, 0);
+    __syncthreads();
+
+    for (int i = 0; i < nt; i += 2) {
+        term_step<EPI>(a, hot_s, H, ws, my, w, S, nt, i, A, B, p0, p1);
+        if (i + 1 >= nt) break;
+        term_step<EPI>(a, hot_s, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
+    }
+    if constexpr (EPI == EPI_CPAA || EPI == EPI_POWER) {
+        if (a.part) {
+            p0 = warp_sum_v(p0);
+            p1 = warp_sum_v(p1);
+            if (lane == 0) {
+                red[warp] = p0;
+                red[32 + warp] = p1;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                double q0 = lane < kWarps ? red[lane] : 0.0;
+                double q1 = lane < kWarps ? red[32 + lane] : 0.0;
+                q0 = warp_sum_v(q0);
+                q1 = warp_sum_v(q1);
+                if (lane == 0) {
+                    a.part[2 * blockIdx.x] = q0;
+                    a.part[2 * blockIdx.x + 1] = q1;
+                }
+            }
+        }
+    }
+}
+
+// Hub rows (degree > kWarpNnz, rows [0, n_hub) of the view): one warp per row sums the
+// row's chunk partials in chunk order and runs the fused epilogue.  Chunk tiles of row h
+// are the consecutive tiles [hub_first[h], hub_first[h+1]).
+template <int EPI, class RP, class V>
+__global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const int* __restrict__ hub_first,
+                                                      int64_t n_hub) {
+    const int lane = threadIdx.x & 31;
+    pdl_trigger();
+    pdl_wait();  // the term kernel's hub partials
+    for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < n_hub;
+         h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int f0 = hub_first[h], f1 = hub_first[h + 1];
+        V tot = V(0);
+        for (int q = f0 + lane; q < f1; q += 32) tot += (V)a.hub_part[q];
+        tot = warp_sum_v(tot);
+        if (lane == 0) {
+            const int64_t deg = a.rp[h + 1] - a.rp[h];
+            double q0 = 0.0, q1 = 0.0;
+            const V hp = EPI != EPI_PLAIN ? prev_src<EPI>(a)[h] : V(0);
+            const V ha = EPI == EPI_CPAA ? a.acc[h] : V(0);
+            epilogue_v<EPI>(a, h, tot, deg, hp, ha, q0, q1);
+            if (a.hub_ts) {
+                a.hub_ts[2 * h] = q0;
+                a.hub_ts[2 * h + 1] = q1;
+            }
+        }
+    }
+}
+
+// ---------------- BITEXACT: thread per row, storage order ----------------------------
+template <int EPI, class RP>
+__global__ void __launch_bounds__(kThreads) k_term_exact(TermArgs<RP, double> a, int64_t n) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = a.rp[u], e = a.rp[u + 1];
+        double s = 0.0;
+        for (int64_t j = b; j < e; ++j) s = __dadd_rn(s, a.x_in[a.col[j]]);
+        double p0 = 0.0, p1 = 0.0;
+        epilogue<EPI>(a, u, s, e - b, p0, p1);
+    }
+}
+
+// Serial Kahan sums exactly as graph.cpp:10-19 (single thread: bit-identical order).
+// The reference's serial compensated sums, bit for bit (graph.cpp:10-19 order, one element
+// at a time).  The recurrence is inherently sequential, so one thread runs it; warps 1..7
+// stage the next chunk of both inputs into shared memory meanwhile, so the chain runs at
+// FP64 add latency instead of waiting on global loads.
+constexpr int kSerialChunk = 1024;
+
+template <int MODE>  // 0: Kahan(x) [, Kahan(y)]   1: power: Kahan|y - x|, Kahan(y) (power.cpp:80-93)
+__global__ void __launch_bounds__(256) k_serial_sums(const double* __restrict__ a, const double* __restrict__ b,
+                                                     int64_t n, double* __restrict__ out) {
+    __shared__ double sa[2][kSerialChunk], sb[2][kSerialChunk];
+    const int tid = threadIdx.x;
+    const bool two = b != nullptr;
+    auto stage = [&](int buf, int64_t base) {  // warps 1..7
+        const int64_t len = n - base < kSerialChunk ? n - base : (int64_t)kSerialChunk;
+        for (int64_t i = tid - 32; i < len; i += blockDim.x - 32) {
+            sa[buf][i] = a[base + i];
+            if (two) sb[buf][i] = b[base + i];
+        }
+    };
+    if (tid >= 32 && n > 0) stage(0, 0);
+    __syncthreads();
+    double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
+    for (int64_t base = 0; base < n; base += kSerialChunk) {
+        const int cur = (int)((base / kSerialChunk) & 1);
+        if (tid >= 32 && base + kSerialChunk < n) stage(cur ^ 1, base + kSerialChunk);
+        if (tid == 0) {
+            const int len = (int)(n - base < kSerialChunk ? n - base : (int64_t)kSerialChunk);
+#pragma unroll 4
+            for (int j = 0; j < len; ++j) {
+                if constexpr (MODE == 0) {
+                    const double av = __dsub_rn(sa[cur][j], c0);
+                    const double t = __dadd_rn(s0, av);
+                    c0 = __dsub_rn(__dsub_rn(t, s0), av);
+                    s0 = t;
+                    if (two) {
+                        const double bv = __dsub_rn(sb[cur][j], c1);
+                        const double u = __dadd_rn(s1, bv);
+                        c1 = __dsub_rn(__dsub_rn(u, s1), bv);
+                        s1 = u;
+                    }
+                } else {  // a = y (new), b = x (old)
+                    const double y = sa[cur][j];
+                    const double d = __dsub_rn(fabs(__dsub_rn(y, sb[cur][j])), c0);
+                    const double t = __dadd_rn(s0, d);
+                    c0 = __dsub_rn(__dsub_rn(t, s0), d);
+                    s0 = t;
+                    const double av = __dsub_rn(y, c1);
+                    const double u = __dadd_rn(s1, av);
+                    c1 = __dsub_rn(__dsub_rn(u, s1), av);
+                    s1 = u;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        out[0] = s0;
+        out[1] = s1;
+    }
+}
+
+// Many independent serial Kahan sums (one per thread), each in the reference's element
+// order: the BITEXACT trace of all M terms after the loop (mass_T = Kahan(T_k),
+// S_k = Kahan(acc_k) from per-term snapshots).  Sums of different terms do not depend on
+// each other, so they run side by side; within a sum the order is the reference's.
+__global__ void k_kahan_many(const double* __restrict__ snaps, int64_t n, int count, double* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const double* __restrict__ x = snaps + (size_t)t * (size_t)n;
+    double s = 0.0, c = 0.0;
+    int64_t i = 0;
+    constexpr int U = 16;
+    for (; i + U <= n; i += U) {
+        double v[U];
+#pragma unroll
+        for (int q = 0; q < U; ++q) v[q] = __ldg(x + i + q);
+#pragma unroll
+        for (int q = 0; q < U; ++q) {
+            const double a = __dsub_rn(v[q], c);
+            const double u = __dadd_rn(s, a);
+            c = __dsub_rn(__dsub_rn(u, s), a);
+            s = u;
+        }
+    }
+    for (; i < n; ++i) {
+        const double a = __dsub_rn(x[i], c);
+        const double u = __dadd_rn(s, a);
+        c = __dsub_rn(__dsub_rn(u, s), a);
+        s = u;
+    }
+    out[t] = s;
+}
+
+// Power rounds j = 1..nb of a speculative batch (snapshots S[0..nb] of x): thread 2(j-1)
+// runs the reference's Kahan L1 change |S[j] - S[j-1]|, thread 2(j-1)+1 the Kahan mass of
+// S[j] (power.cpp:80-93), each in element order.
+__global__ void k_power_many(const double* __restrict__ S, int64_t n, int nb, double* __restrict__ out) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * nb) return;
+    const int j = t / 2 + 1;
+    const double* __restrict__ y = S + (size_t)j * (size_t)n;
+    const double* __restrict__ x = S + (size_t)(j - 1) * (size_t)n;
+    double s = 0.0, c = 0.0;
+    constexpr int U = 16;  // loads of the next elements are independent of the chain
+    int64_t i = 0;
+    if (t & 1) {
+        for (; i + U <= n; i += U) {
+            double v[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) v[q] = __ldg(y + i + q);
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const double a = __dsub_rn(v[q], c);
+                const double u = __dadd_rn(s, a);
+                c = __dsub_rn(__dsub_rn(u, s), a);
+                s = u;
+            }
+        }
+        for (; i < n; ++i) {
+            const double a = __dsub_rn(__ldg(y + i), c);
+            const double u = __dadd_rn(s, a);
+            c = __dsub_rn(__dsub_rn(u, s), a);
+            s = u;
+        }
+    } else {
+        for (; i + U <= n; i += U) {
+            double d[U];
+#pragma unroll
+            for (int q = 0; q < U; ++q) d[q] = fabs(__dsub_rn(__ldg(y + i + q), __ldg(x + i + q)));
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const double e = __dsub_rn(d[q], c);
+                const double u = __dadd_rn(s, e);
+                c = __dsub_rn(__dsub_rn(u, s), e);
+                s = u;
+            }
+        }
+        for (; i < n; ++i) {
+            const double e = __dsub_rn(fabs(__dsub_rn(__ldg(y + i), __ldg(x + i))), c);
+            const double u = __dadd_rn(s, e);
+            c = __dsub_rn(__dsub_rn(u, s), e);
+            s = u;
+        }
+    }
+    out[t] = s;
+}
+
+// ---------------- init / reductions / normalisation ----------------------------------
+// T_{-1} = T_0 = p (or 1), acc = (c0/2) T_0, x_0 = T_0 D^-1   (cpaa.cpp:88-92, :116 at k=1)
+template <class RP, class V>
+__global__ void k_init(const RP* __restrict__ rp, const double* __restrict__ inv,
+                       const double* __restrict__ p, const int* __restrict__ order, int64_t n,
+                       double half_c0, V* __restrict__ T0, V* __restrict__ T1, V* __restrict__ acc,
+                       V* __restrict__ x0) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const V t0 = p ? (V)p[order ? order[u] : u] : V(1);
+        T0[u] = t0;
+        T1[u] = t0;
+        acc[u] = p ? mul_rn((V)half_c0, t0) : (V)half_c0;
+        const V iv = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
+        x0[u] = mul_rn(t0, iv);
+    }
+}
+
+// trace[k] = sum of block partials (+ hub partials) of term k, fixed order.
+__global__ void k_trace_reduce(const double* __restrict__ part, int grid, const double* __restrict__ hub_ts,
+                               int n_hub, int k_first, double* __restrict__ trace) {
+    __shared__ double sh[32];
+    const int k = k_first + blockIdx.x;
+    const double* pk = part + (size_t)k * grid * 2;
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < grid; i += blockDim.x) {
+        a += pk[2 * i];
+        b += pk[2 * i + 1];
+    }
+    if (hub_ts) {
+        const double* hk = hub_ts + (size_t)k * n_hub * 2;
+        for (int i = threadIdx.x; i < n_hub; i += blockDim.x) {
+            a += hk[2 * i];
+            b += hk[2 * i + 1];
+        }
+    }
+    a = block_sum(a, sh);
+    b = block_sum(b, sh);
+    if (threadIdx.x == 0) {
+        trace[2 * k] = a;
+        trace[2 * k + 1] = b;
+    }
+}
+
+template <class V>
+__global__ void k_sum_blocks(const V* __restrict__ x, int64_t n, double* __restrict__ part) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a += (double)x[i];
+    a = block_sum(a, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = a;
+}
+
+__global__ void k_sum_final(const double* __restrict__ part, int cnt, double* __restrict__ out) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) a += part[i];
+    a = block_sum(a, sh);
+    if (threadIdx.x == 0) *out = a;
+}
+
+// ranks[order[u]] = acc[u] / total   (cpaa.cpp:159-163)
+template <class V>
+__global__ void k_normalize(const V* __restrict__ acc, const int* __restrict__ order, int64_t n,
+                            const double* __restrict__ total, V* __restrict__ out) {
+    const double tot = *total;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const V r = (V)((double)acc[u] / tot);
+        out[order ? order[u] : u] = r;
+    }
+}
+
+template <class V>
+__global__ void k_permute_in(const double* __restrict__ src, const int* __restrict__ order, int64_t n,
+                             V* __restrict__ dst) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x)
+        dst[u] = (V)src[order ? order[u] : u];
+}
+
+template <class V>
+__global__ void k_permute_out(const V* __restrict__ src, const int* __restrict__ order, int64_t n,
+                              double* __restrict__ dst) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x)
+        dst[order ? order[u] : u] = (double)src[u];
+}
+
+// x = T D^-1 (staged API / transition_apply pre-scale)
+template <class RP, class V>
+__global__ void k_prescale(const RP* __restrict__ rp, const double* __restrict__ inv,
+                           const V* __restrict__ T, int64_t n, V* __restrict__ x) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const V iv = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
+        x[u] = mul_rn(T[u], iv);
+    }
+}
+
+// acc += c_k T_next (cpaa.cpp:192-194)
+template <class V>
+__global__ void k_accumulate(V* __restrict__ acc, const V* __restrict__ Tn, int64_t n, double ck) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x)
+        acc[u] = add_rn(acc[u], mul_rn((V)ck, Tn[u]));
+}
+
+// Per-round error vs a reference (metrics.cpp:12-30 via cpaa.cpp:149-154):
+// est = acc / S_k ; max |est-ref|/ref and sum |est-ref|.  ref in the same layout.
+template <class V>
+__global__ void k_err(const V* __restrict__ acc, const double* __restrict__ ref, int64_t n,
+                      const double* __restrict__ S, int by_S, double* __restrict__ part) {
+    __shared__ double sh[32];
+    const double tot = by_S ? *S : 1.0;
+    double mx = 0.0, l1 = 0.0;
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const double est = by_S ? (double)acc[u] / tot : (double)acc[u];
+        const double d = fabs(est - ref[u]);
+        mx = fmax(mx, d / ref[u]);
+        l1 += d;
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
+        part[2 * blockIdx.x] = mx;
+    }
+    __syncthreads();
+    l1 = block_sum(l1, sh);
+    if (threadIdx.x == 0) part[2 * blockIdx.x + 1] = l1;
+}
+
+__global__ void k_err_final(const double* __restrict__ part, int cnt, double* __restrict__ out) {
+    __shared__ double sh[32];
+    double mx = 0.0, l1 = 0.0;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        mx = fmax(mx, part[2 * i]);
+        l1 += part[2 * i + 1];
+    }
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, sh[w]);
+        out[0] = mx;
+    }
+    __syncthreads();
+    l1 = block_sum(l1, sh);
+    if (threadIdx.x == 0) out[1] = l1;
+}
+
+// =====================================================================================
+// Host drivers
+// =====================================================================================
+
+inline int grid1d(int64_t n) {
+    int64_t b = (n + kThreads - 1) / kThreads;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+// Layout the solve runs on: FAST -> degree-binned view; BITEXACT -> reference order.
+struct Layout {
+    bool fast;
+    bool rp64;
+    const void* rp;
+    const int* col;
+    const double* inv;
+    const int* order;  // new -> old (fast) or null
+};
+
+Layout layout_of(cheb_graph* g, int mode) {
+    Layout L{};
+    if (mode == CHEB_MODE_FAST) {
+        ensure_view(g);
+        L.fast = true;
+        L.rp64 = g->view.rp64;
+        L.rp = g->view.row_ptr.get();
+        L.col = g->view.col.ptr<int>();
+        L.inv = g->inv_array ? g->view.inv.ptr<double>() : nullptr;
+        L.order = g->view.order.ptr<int>();
+    } else {
+        L.fast = false;
+        L.rp64 = g->rp64;
+        L.rp = g->row_ptr.get();
+        L.col = g->col.ptr<int>();
+        L.inv = g->inv_array ? g->inv.ptr<double>() : nullptr;
+        L.order = nullptr;
+    }
+    return L;
+}
+
+template <class RP, class V>
+TermArgs<RP, V> base_args(cheb_graph* /*g*/, const Layout& L) {
+    TermArgs<RP, V> a{};
+    a.rp = static_cast<const RP*>(L.rp);
+    a.col = L.col;
+    a.inv = L.inv;
+    return a;
+}
+
+// Launch one SpMV-shaped pass with epilogue EPI on the given layout.
+template <int EPI, class RP, class V>
+int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
+    cudaStream_t st = g->stream;
+    if (L.fast) {
+        static bool attr_set = false;  // per template instance
+        constexpr size_t smem = warp_smem_bytes<V>();
+        if (!attr_set) {
+            CHEB_CUDA_CHECK(cudaFuncSetAttribute(k_term_warp<EPI, RP, V>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set = true;
+        }
+        int H = (int)std::min<int64_t>(g->n, hot_capacity<V>());
+        if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);
+        TermArgs<RP, V> ab = a;
+        ab.tune_nogather = tuning().nogather;
+        ab.tune_skip = tuning().skip;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(g->view.grid);
+        cfg.blockDim = dim3(kWarps * 32);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        cfg.attrs = attr;
+        cfg.numAttrs = 0;
+        // keep the hot (degree-sorted) prefix of x_k resident in L2 across the term
+        if (tuning().l2win &&
+            l2_window(a.x_in, (size_t)std::max<int64_t>(g->view.x_len, 1) * sizeof(V),
+                      &attr[cfg.numAttrs].val.accessPolicyWindow)) {
+            attr[cfg.numAttrs++].id = cudaLaunchAttributeAccessPolicyWindow;
+        }
+        if (tuning().pdl) {  // overlap this launch + prologue with the previous kernel's tail
+            attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
+        }
+        CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V>, ab, (const WTile*)g->view.prog.ptr<WTile>(),
+                                           g->view.prog_len, g->view.n_tiles, H));
+        if (g->view.n_hub > 0) {
+            CHEB_CUDA_CHECK(cudaGetLastError());
+            const int hb = (int)std::min<int64_t>((g->view.n_hub * 32 + 255) / 256, 148 * 16);
+            cudaLaunchConfig_t hc = {};
+            hc.gridDim = dim3(hb);
+            hc.blockDim = dim3(256);
+            hc.stream = st;
+            cudaLaunchAttribute hattr[1];
+            hattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            hattr[0].val.programmaticStreamSerializationAllowed = 1;
+            hc.attrs = hattr;
+            hc.numAttrs = tuning().pdl ? 1 : 0;
+            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&hc, k_hub_finalize<EPI, RP, V>, a,
+                                               (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub));
+            return 2;
+        }
+    } else {
+        if constexpr (std::is_same<V, double>::value) {
+            k_term_exact<EPI, RP><<<grid1d(g->n), kThreads, 0, st>>>(a, g->n);
+        } else {
+            fail(CHEB_INVALID_ARG, "bitexact mode is fp64 only");
+        }
+    }
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    return 1;
+}
+
+template <class V>
+void ensure_workspace(cheb_graph* g, int M, int R) {
+    Workspace& w = g->ws;
+    const int64_t n = g->n;
+    // Any reallocation invalidates the captured solve graph (it bakes in addresses).
+    const void* before[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
+                            w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
+                            w.trace.get(), w.total.get()};
+    const int64_t vlen = std::max<int64_t>(std::max<int64_t>(n, g->view.x_len), 1);
+    const size_t vb = sizeof(V) * (size_t)vlen * R;
+    w.T0.ensure(vb);
+    w.T1.ensure(vb);
+    w.X0.ensure(vb);
+    w.X1.ensure(vb);
+    w.acc.ensure(vb);
+    w.out.ensure(vb);
+    const int grid = std::max(g->view.ready ? g->view.grid : 1, grid1d(n));
+    w.part.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max(grid, 1));
+    w.hub_part.ensure(sizeof(double) * std::max(g->view.n_tiles, 1));
+    if (!w.hub_cnt || w.hub_cnt.bytes() < sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1)) {
+        w.hub_cnt.alloc(sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1));
+        CHEB_CUDA_CHECK(cudaMemset(w.hub_cnt.get(), 0, w.hub_cnt.bytes()));
+    }
+    w.hub_ts.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max<int64_t>(g->view.n_hub, 1));
+    w.trace.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1));
+    w.total.ensure(sizeof(double) * 4);
+    w.n = n;
+    w.R = R;
+    w.vbytes = sizeof(V);
+    const void* after[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
+                           w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
+                           w.trace.get(), w.total.get()};
+    if (std::memcmp(before, after, sizeof before) != 0) {
+        if (w.exec) cudaGraphExecDestroy(w.exec);
+        w.exec = nullptr;
+        w.exec_key.clear();
+        w.seen_key.clear();
+    }
+}
+
+// BITEXACT trace snapshots (2 M n doubles) when they fit a quarter of the free memory (and
+// 8 GB); otherwise the per-term serial sums run instead.
+void ensure_snapshots(cheb_graph* g, int M) {
+    Workspace& w = g->ws;
+    const size_t need = sizeof(double) * 2 * (size_t)M * (size_t)g->n;
+    if (w.snap.bytes() >= need) return;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return;
+    if (need > free_b / 4 || need > (size_t(8) << 30)) return;
+    w.snap.alloc(need);
+    if (w.exec) cudaGraphExecDestroy(w.exec);  // a captured solve baked the old pointers in
+    w.exec = nullptr;
+    w.exec_key.clear();
+    w.seen_key.clear();
+}
+
+// Enqueue the whole solve: init, M fused terms, trace reduction, normalisation.
+}  // namespace
+}  // namespace chebgpu

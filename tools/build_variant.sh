@@ -8,7 +8,7 @@ cd "$(dirname "$0")/.."
 make -s paper_2112_01743_b200/lib/libchebpr_b200.so
 mkdir -p build/variants/obj/$name
 NVFLAGS="-O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC,-ffp-contract=off --expt-extended-lambda -Iinclude"
-for f in cpaa spmm build capi; do
+for f in cpaa dist power spmm build capi; do
   nvcc $NVFLAGS $flags -c paper_2112_01743_b200/csrc/$f.cu -o build/variants/obj/$name/$f.o &
 done
 wait
