@@ -128,3 +128,14 @@ def test_push_group_personalised(cheb):
         res = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=39, personalization=p))
         assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
         grp.close()
+
+
+def test_push_group_int64_row_pointers(cheb):
+    """Partitioned solve on handles with int64 row pointers (the config-4 layout)."""
+    z = load_golden("config1")
+    single = cheb.run_cpaa(cheb.build_device_graph(z["edges"])[0], cheb.SolverConfig(rounds=39))
+    hs = [cheb.build_device_graph(z["edges"], cheb.BuildOptions(row_ptr_64=True))[0] for _ in range(2)]
+    grp = cheb.PartitionGroup(hs)
+    res = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=39))
+    assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
+    grp.close()
