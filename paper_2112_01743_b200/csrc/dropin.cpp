@@ -10,11 +10,13 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <fstream>
 #include <limits>
 #include <sstream>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "chebpr/coefficients.hpp"
@@ -205,11 +207,13 @@ UndirectedGraph host_graph(cheb_graph_t h) {
 }  // namespace
 
 BuildResult build_graph(const std::vector<std::pair<int64_t, int64_t>>& edges, const BuildOptions& opts) {
-    std::vector<int64_t> flat(2 * edges.size() + 2);
-    for (size_t i = 0; i < edges.size(); ++i) {
-        flat[2 * i] = edges[i].first;
-        flat[2 * i + 1] = edges[i].second;
-    }
+    // std::pair<int64_t, int64_t> is two adjacent int64 (standard layout, no padding): the
+    // edge vector already is the interleaved (a0, b0, a1, b1, ...) array the C-ABI takes
+    static_assert(std::is_standard_layout_v<std::pair<int64_t, int64_t>> &&
+                      sizeof(std::pair<int64_t, int64_t>) == 2 * sizeof(int64_t),
+                  "std::pair<int64_t, int64_t> must be two adjacent int64");
+    static const int64_t none[2] = {0, 0};
+    const int64_t* flat = edges.empty() ? none : &edges.front().first;
     cheb_build_opts o;
     cheb_build_opts_default(&o);
     o.dedup = opts.dedup ? 1 : 0;
@@ -218,7 +222,7 @@ BuildResult build_graph(const std::vector<std::pair<int64_t, int64_t>>& edges, c
     o.device = opts.device;
     cheb_graph_t h = nullptr;
     cheb_graph_info info;
-    check(cheb_graph_build(flat.data(), (int64_t)edges.size(), &o, &h, &info));
+    check(cheb_graph_build(flat, (int64_t)edges.size(), &o, &h, &info));
     BuildResult r;
     r.graph = host_graph(h);
     r.duplicates_removed = info.duplicates_removed;
