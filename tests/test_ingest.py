@@ -261,3 +261,17 @@ def test_loaded_graph_solves_like_built_graph(cheb, tmp_path):
     r1, r2 = cheb.run_cpaa(dg, cfg), cheb.run_cpaa(dg2, cfg)
     assert np.array_equal(r1.ranks, r2.ranks)
     assert st.n == 500 and st.self_loops == 0
+
+
+@pytest.mark.gpu
+def test_loader_errors(cheb, tmp_path):
+    with pytest.raises(cheb.ParseError, match="cannot open"):
+        cheb.load_edge_list(str(tmp_path / "missing.txt"))
+    with pytest.raises(cheb.ParseError, match="cannot open"):
+        cheb.load_matrix_market(str(tmp_path / "missing.mtx"))
+    import ctypes as C
+    from paper_2112_01743_b200 import _lib as L
+    h, st = C.c_void_p(), L.cheb_graph_stats()
+    o = L.cheb_load_opts()
+    L.load().cheb_load_opts_default(C.byref(o))
+    assert L.load().cheb_graph_parse_text(b"0 1\n", 4, 7, b"x", C.byref(o), C.byref(h), C.byref(st)) == 4  # format

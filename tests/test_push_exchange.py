@@ -139,3 +139,23 @@ def test_push_group_int64_row_pointers(cheb):
     res = cheb.run_cpaa(grp, cheb.SolverConfig(rounds=39))
     assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
     grp.close()
+
+
+def test_peer_and_group_argument_errors(cheb):
+    """The push-exchange entry points reject bad arguments with CHEB_INVALID_ARG."""
+    import ctypes as C
+    from paper_2112_01743_b200 import _lib as L
+    lib = L.load()
+    z = load_golden("k2")
+    dg, _ = cheb.build_device_graph(z["edges"])
+    out = C.c_void_p()
+    assert lib.cheb_group_create((C.c_void_p * 1)(dg.handle), 0, C.byref(out)) == 4       # G < 1
+    assert lib.cheb_group_create((C.c_void_p * 2)(dg.handle, dg.handle), 2, C.byref(out)) == 4  # duplicate
+    buf = (C.c_ubyte * 16)()
+    assert lib.cheb_peer_export(dg.handle, 2, 0, buf, 16) == 4                                # too small
+    big = (C.c_ubyte * L.PEER_EXPORT_BYTES)()
+    assert lib.cheb_peer_import(dg.handle, big, L.PEER_EXPORT_BYTES) == 4                     # no export yet
+    assert lib.cheb_peer_export(dg.handle, 2, 5, big, L.PEER_EXPORT_BYTES) == 4               # rank >= G
+    # the handle still solves as a single-GPU graph after the failed calls
+    r = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=5))
+    assert np.allclose(r.ranks, 0.5)
