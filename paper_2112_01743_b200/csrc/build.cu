@@ -743,17 +743,21 @@ __global__ void k_new_degrees(const RP* __restrict__ rp, const int* __restrict__
     }
 }
 
-// Warp per new row: copy the old row's neighbours in storage order, renamed.
-template <class RPO, class RPN>
+// Copy the old neighbours of new rows [w0, w1) in storage order, renamed.  S lanes per row
+// (S = 32: warp per row; S = 4 for the short rows, so that the ~1 M short rows of config 2
+// are not each a warp waiting on four dependent loads); S = 0: a whole CTA per row (hubs).
+template <int S, class RPO, class RPN>
 __global__ void k_permute_rows(const RPO* __restrict__ rp_old, const int* __restrict__ col_old,
                                const RPN* __restrict__ rp_new, const int* __restrict__ order,
-                               const int* __restrict__ rank, int64_t n, int* __restrict__ col_new) {
-    const int lane = threadIdx.x & 31;
-    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n;
-         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+                               const int* __restrict__ rank, int64_t w0, int64_t w1, int* __restrict__ col_new) {
+    constexpr int kPer = S == 0 ? 1 : (int)(kBuildThreads / (S == 0 ? 1 : S));  // rows per CTA
+    const int lane = S == 0 ? (int)threadIdx.x : (int)(threadIdx.x % (S == 0 ? 1 : S));
+    const int stride = S == 0 ? (int)blockDim.x : S;
+    for (int64_t w = w0 + (int64_t)blockIdx.x * kPer + (S == 0 ? 0 : threadIdx.x / (S == 0 ? 1 : S)); w < w1;
+         w += (int64_t)gridDim.x * kPer) {
         const int o = order[w];
         const int64_t b = rp_old[o], e = rp_old[o + 1], d = rp_new[w];
-        for (int64_t j = b + lane; j < e; j += 32) col_new[d + (j - b)] = rank[col_old[j]];
+        for (int64_t j = b + lane; j < e; j += stride) col_new[d + (j - b)] = rank[col_old[j]];
     }
 }
 
@@ -1034,9 +1038,23 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     V.col.alloc(sizeof(int) * std::max<int64_t>(nnz_l, 1) + 64);  // TMA reads round up to 16 B
     if (before_col) before_col();
     if (nl > 0) {
-        k_permute_rows<<<grid_for(nl * 32), kBuildThreads, 0, st>>>(rp_old, g->col.ptr<int>(), V.row_ptr.ptr<RPN>(),
-                                                                   V.order.ptr<int>() + lo, colmap, nl,
-                                                                   V.col.ptr<int>());
+        // rows are degree-descending: [0, n_huge) > 1024 entries, [n_huge, n_long) > 16
+        int64_t n_huge = 0, n_long = 0;
+        for (size_t r = 0; r < run_deg.size(); ++r) {
+            if (run_deg[r] > 1024) n_huge += run_cnt[r];
+            if (run_deg[r] > 16) n_long += run_cnt[r];
+        }
+        const int* order_l = V.order.ptr<int>() + lo;
+        const RPN* rp_l = V.row_ptr.ptr<RPN>();
+        if (n_huge > 0)
+            k_permute_rows<0><<<(int)std::min<int64_t>(n_huge, 148 * 16), kBuildThreads, 0, st>>>(
+                rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, 0, n_huge, V.col.ptr<int>());
+        if (n_long > n_huge)
+            k_permute_rows<32><<<grid_for((n_long - n_huge) * 32), kBuildThreads, 0, st>>>(
+                rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, n_huge, n_long, V.col.ptr<int>());
+        if (nl > n_long)
+            k_permute_rows<4><<<grid_for((nl - n_long) * 4), kBuildThreads, 0, st>>>(
+                rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, n_long, nl, V.col.ptr<int>());
         CHEB_CUDA_CHECK(cudaGetLastError());
         // When x does not fit L2 (config 4), ascending renamed ids within each row: a row's
         // gathers then walk x in address order (DRAM page / sector locality; C4 4.49 -> 4.03

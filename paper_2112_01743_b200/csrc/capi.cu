@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <nccl.h>
@@ -263,18 +264,45 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
         g->rp64 = row_ptr_64 != 0;
         g->duplicates_removed = 0;
         g->isolated_dropped = 0;
-        // the remaining checks are O(n) host loops: they run while the CSR copies are in flight
+        // the remaining checks are O(n) host loops: they run while the CSR copies are in
+        // flight, split over host threads (each chunk finds its first failing vertex; the
+        // lowest one is reported, in the reference's check order)
         auto host_checks = [&] {
-            for (int64_t v = 0; v < n; ++v)
-                if (degrees[v] < 1)
-                    fail(CHEB_VALIDATION, "vertex " + std::to_string(v) + " is isolated (degree 0)");
+            struct Part {
+                int64_t isolated = -1, nonmono = -1, dmin = INT64_MAX, dmax = 0;
+            };
+            const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+            const int T = n >= (int64_t(1) << 18) ? std::min(8, hw) : 1;
+            std::vector<Part> parts(T);
+            auto scan = [&](int t) {
+                Part& p = parts[t];
+                const int64_t lo = n * t / T, hi = n * (t + 1) / T;
+                for (int64_t v = lo; v < hi; ++v)
+                    if (degrees[v] < 1) {
+                        p.isolated = v;
+                        break;
+                    }
+                for (int64_t v = lo; v < hi; ++v) {  // one pass: monotone offsets + degree extrema
+                    const int64_t d = offsets[v + 1] - offsets[v];
+                    if (d < 0 && p.nonmono < 0) p.nonmono = v;
+                    p.dmin = d < p.dmin ? d : p.dmin;
+                    p.dmax = d > p.dmax ? d : p.dmax;
+                }
+            };
+            std::vector<std::thread> th;
+            for (int t = 1; t < T; ++t) th.emplace_back(scan, t);
+            scan(0);
+            for (auto& x : th) x.join();
+            for (const Part& p : parts)
+                if (p.isolated >= 0)
+                    fail(CHEB_VALIDATION, "vertex " + std::to_string(p.isolated) + " is isolated (degree 0)");
             if (offsets[0] != 0) fail(CHEB_VALIDATION, "offsets must start at 0");
             int64_t dmin = INT64_MAX, dmax = 0;
-            for (int64_t v = 0; v < n; ++v) {  // one pass: monotone offsets + degree extrema
-                const int64_t d = offsets[v + 1] - offsets[v];
-                if (d < 0) fail(CHEB_VALIDATION, "offsets not monotone at vertex " + std::to_string(v));
-                dmin = d < dmin ? d : dmin;
-                dmax = d > dmax ? d : dmax;
+            for (const Part& p : parts) {
+                if (p.nonmono >= 0)
+                    fail(CHEB_VALIDATION, "offsets not monotone at vertex " + std::to_string(p.nonmono));
+                dmin = std::min(dmin, p.dmin);
+                dmax = std::max(dmax, p.dmax);
             }
             g->min_degree = dmin;
             g->max_degree = dmax;
