@@ -631,7 +631,7 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
     // 5. solver view (single-GPU layout) on the auxiliary stream: the degree-only half
     //    overlaps the neighbour copy; the column permute waits for it.
     if (g->part.G == 1 && !g->part.comm && !g->peer && n > 0) {
-        if (!g->aux) CHEB_CUDA_CHECK(cudaStreamCreateWithFlags(&g->aux, cudaStreamNonBlocking));
+        if (!g->aux) g->aux = pooled_stream(g->device);
         CHEB_CUDA_CHECK(cudaStreamWaitEvent(g->aux, ev_rp, 0));
         {
             AllocScope as(g->aux);

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -51,7 +52,7 @@ cheb_graph* new_graph(int device) {
     auto* g = new cheb_graph();
     g->device = device;
     DeviceGuard dg(device);
-    CHEB_CUDA_CHECK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    g->stream = pooled_stream(device);
     CHEB_CUDA_CHECK(cudaEventCreate(&g->ev0));
     CHEB_CUDA_CHECK(cudaEventCreate(&g->ev1));
     return g;
@@ -85,6 +86,41 @@ void essential(cheb_graph* g) {
     if (g->n < 1) fail(CHEB_VALIDATION, "graph has no vertices");
 }
 }  // namespace
+
+namespace {
+std::mutex& stream_pool_mu() {
+    static std::mutex m;
+    return m;
+}
+std::vector<std::pair<int, cudaStream_t>>& stream_pool() {
+    static auto* v = new std::vector<std::pair<int, cudaStream_t>>();  // never destroyed (exit order)
+    return *v;
+}
+}  // namespace
+
+cudaStream_t chebgpu::pooled_stream(int device) {
+    {
+        std::lock_guard<std::mutex> lk(stream_pool_mu());
+        auto& v = stream_pool();
+        for (size_t i = 0; i < v.size(); ++i)
+            if (v[i].first == device) {
+                cudaStream_t s = v[i].second;
+                v[i] = v.back();
+                v.pop_back();
+                return s;
+            }
+    }
+    cudaStream_t s = nullptr;
+    CHEB_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+void chebgpu::release_stream(int device, cudaStream_t s) {
+    if (!s) return;
+    std::lock_guard<std::mutex> lk(stream_pool_mu());
+    if (stream_pool().size() < 64) stream_pool().emplace_back(device, s);
+    else cudaStreamDestroy(s);
+}
 
 void chebgpu::retain_pool_memory() {
     int dev = 0;
@@ -158,8 +194,8 @@ cheb_graph::~cheb_graph() {
     }
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    if (stream) cudaStreamDestroy(stream);
-    if (aux) cudaStreamDestroy(aux);
+    release_stream(device, stream);  // idle: synchronised above, buffers returned on it
+    release_stream(device, aux);
     if (prev >= 0) cudaSetDevice(prev);
 }
 

@@ -48,6 +48,10 @@ struct AllocScope {
     ~AllocScope() { alloc_stream() = prev; }
 };
 void retain_pool_memory();  // capi.cu
+// Non-blocking streams recycled across graph handles of the device (the reference API is
+// stateless, so every drop-in call makes and frees a handle): a released stream must be idle.
+cudaStream_t pooled_stream(int device);
+void release_stream(int device, cudaStream_t s);
 
 // L2 persistence for the gathered vector: an access-policy window over the first `bytes` of
 // `base` (the degree-sorted hot prefix of x), sized to the device's persisting-L2 limit.
