@@ -1065,18 +1065,21 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2 || g->want_sorted_rows)
                                                  : tuning().sortrows > 0;
-        const bool sort_rows = big_x && nnz_l > 0 && nnz_l < INT32_MAX;
-        V.sorted_rows = sort_rows;
+        const bool hubs_only = tuning().sortrows == 2 && V.n_hub > 0;
+        const bool sort_rows = (big_x || hubs_only) && nnz_l > 0 && nnz_l < INT32_MAX;
+        V.sorted_rows = sort_rows && !hubs_only;
         if (sort_rows) {
-            DevMem alt(sizeof(int) * (size_t)nnz_l + 64);
+            const int64_t segs = hubs_only ? V.n_hub : nl;
+            const RPN* offs = V.row_ptr.ptr<RPN>();
+            const int64_t items = hubs_only ? (int64_t)read_scalar(offs + segs, st) : nnz_l;
+            DevMem alt(sizeof(int) * (size_t)items + 64);
             cub::DoubleBuffer<int> db(V.col.ptr<int>(), alt.ptr<int>());
             size_t bytes = 0;
-            const RPN* offs = V.row_ptr.ptr<RPN>();
-            CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, db, (int)nnz_l, (int)nl, offs, offs + 1, st));
+            CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, db, (int)items, (int)segs, offs, offs + 1, st));
             void* t = tmp.get(bytes);
-            CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, db, (int)nnz_l, (int)nl, offs, offs + 1, st));
+            CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, db, (int)items, (int)segs, offs, offs + 1, st));
             if (db.Current() != V.col.ptr<int>())
-                CHEB_CUDA_CHECK(cudaMemcpyAsync(V.col.get(), db.Current(), sizeof(int) * nnz_l, cudaMemcpyDeviceToDevice, st));
+                CHEB_CUDA_CHECK(cudaMemcpyAsync(V.col.get(), db.Current(), sizeof(int) * items, cudaMemcpyDeviceToDevice, st));
             CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
         }
     }

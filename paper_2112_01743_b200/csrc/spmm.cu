@@ -152,12 +152,13 @@ template <int VPL>
 __host__ __device__ constexpr int spmm_unroll() { return VPL >= 4 && kSpmmUnroll > 4 ? 4 : kSpmmUnroll; }
 
 // Sum over CSR entries [b, e) of the gathered R-vectors (lane's VPL columns), U entries
-// (U column ids then U row gathers) in flight per lane.
+// (U column ids then U row gathers) in flight per lane.  Sums accumulate in fp64 whatever
+// the storage type (fp32: one rounding per row and column).
 template <class RP, class V, int VPL>
 __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b, int64_t e, int lane,
-                                           bool live, V (&s)[VPL]) {
+                                           bool live, double (&s)[VPL]) {
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) s[k] = V(0);
+    for (int k = 0; k < VPL; ++k) s[k] = 0.0;
     const int off = lane * VPL;
     constexpr int U = spmm_unroll<VPL>();
     const uint64_t p_hub = policy_evict_last(), p_cold = policy_evict_first();
@@ -171,20 +172,40 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
 #pragma unroll
             for (int q = 0; q < U; ++q)
                 PolicyIO<V, VPL>::ld(a.x_in + (int64_t)c[q] * a.Rs + off, v[q], c[q] < a.hub_rows ? p_hub : p_cold);
+            if constexpr (sizeof(V) == 8) {
 #pragma unroll
-            for (int q = 0; q < U; ++q)
+                for (int q = 0; q < U; ++q)
 #pragma unroll
-                for (int k = 0; k < VPL; ++k) s[k] += v[q][k];
+                    for (int k = 0; k < VPL; ++k) s[k] += v[q][k];
+            } else {  // fp32: the U entries in fp32, one fp32 -> fp64 conversion per U
+#pragma unroll
+                for (int k = 0; k < VPL; ++k) {
+                    V blk = v[0][k];
+#pragma unroll
+                    for (int q = 1; q < U; ++q) blk += v[q][k];
+                    s[k] += (double)blk;
+                }
+            }
         }
     }
+    V tail[VPL];  // fp32: the < U remaining entries summed in fp32, converted once
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) tail[k] = V(0);
     for (; j < e; ++j) {
         const int c0 = __ldg(a.col + j);
         if (live) {
             V v0[VPL];
             PolicyIO<V, VPL>::ld(a.x_in + (int64_t)c0 * a.Rs + off, v0, c0 < a.hub_rows ? p_hub : p_cold);
 #pragma unroll
-            for (int k = 0; k < VPL; ++k) s[k] += v0[k];
+            for (int k = 0; k < VPL; ++k) {
+                if constexpr (sizeof(V) == 8) s[k] += v0[k];
+                else tail[k] += v0[k];
+            }
         }
+    }
+    if constexpr (sizeof(V) == 4) {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) s[k] += (double)tail[k];
     }
 }
 
@@ -257,7 +278,7 @@ struct StreamIO<float, 4> {
 // Fused recurrence epilogue for (row u, the lane's columns).
 template <class RP, class V, int VPL>
 __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_t u, int64_t deg, int lane,
-                                               const V (&s)[VPL], double& p0, double& p1) {
+                                               const double (&s)[VPL], double& p0, double& p1) {
     const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
     const int c0 = lane * VPL;
     const int64_t i0 = u * a.Rs + c0;
@@ -267,7 +288,7 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_
         StreamIO<V, VPL>::ld(a.acc + i0, ac);
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
-            t[k] = a.first ? s[k] : sub_rn(mul_rn(V(2), s[k]), tp[k]);
+            t[k] = a.first ? (V)s[k] : sub_rn(mul_rn(V(2), (V)s[k]), tp[k]);
             na[k] = add_rn(ac[k], mul_rn((V)a.ck, t[k]));
             xo[k] = mul_rn(t[k], inv);
             p0 += (double)t[k];
@@ -283,7 +304,7 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_
         const int c = c0 + k;
         if (c >= a.R) continue;
         const int64_t i = i0 + k;
-        const V t = a.first ? s[k] : sub_rn(mul_rn(V(2), s[k]), a.T[i]);
+        const V t = a.first ? (V)s[k] : sub_rn(mul_rn(V(2), (V)s[k]), a.T[i]);
         a.T[i] = t;
         const V nacc = add_rn(a.acc[i], mul_rn((V)a.ck, t));
         a.acc[i] = nacc;
@@ -306,15 +327,15 @@ __global__ void __launch_bounds__(256) k_spmm_term(BatchArgs<RP, V> a, const Til
         const Tile tl = tiles[t], nx = tiles[t + 1];
         if (tl.meta & kTileChunk) {
             const int64_t z0 = tl.nnz_begin, z1 = nx.nnz_begin;
-            V s[VPL];
+            double s[VPL];
             row_gather<RP, V, VPL>(a, z0, z1, lane, live, s);
 #pragma unroll
             for (int k = 0; k < VPL; ++k)
-                if (lane * VPL + k < a.Rs) a.hub_part[(int64_t)t * a.Rs + lane * VPL + k] = (double)s[k];
+                if (lane * VPL + k < a.Rs) a.hub_part[(int64_t)t * a.Rs + lane * VPL + k] = s[k];
         } else {
             for (int64_t u = tl.row_begin; u < nx.row_begin; ++u) {
                 const int64_t b = a.rp[u], e = a.rp[u + 1];
-                V s[VPL];
+                double s[VPL];
                 row_gather<RP, V, VPL>(a, b, e, lane, live, s);
                 if (live) batch_epilogue<RP, V, VPL>(a, u, e - b, lane, s, p0, p1);
             }
@@ -347,13 +368,13 @@ __global__ void __launch_bounds__(256) k_spmm_hub_finalize(BatchArgs<RP, V> a, c
     for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < n_hub;
          h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int f0 = hub_first[h], f1 = hub_first[h + 1];
-        V s[VPL];
+        double s[VPL];
 #pragma unroll
-        for (int k = 0; k < VPL; ++k) s[k] = V(0);
+        for (int k = 0; k < VPL; ++k) s[k] = 0.0;
         if (live)
             for (int q = f0; q < f1; ++q)
 #pragma unroll
-                for (int k = 0; k < VPL; ++k) s[k] += (V)a.hub_part[(int64_t)q * a.Rs + lane * VPL + k];
+                for (int k = 0; k < VPL; ++k) s[k] += a.hub_part[(int64_t)q * a.Rs + lane * VPL + k];
         double p0 = 0.0, p1 = 0.0;
         if (live) batch_epilogue<RP, V, VPL>(a, h, a.rp[h + 1] - a.rp[h], lane, s, p0, p1);
         p0 = warp_sum_all(p0);

@@ -398,9 +398,16 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
         } else {
             gather8(a.x_in, hot_s, H, c, v);
         }
-        V sum = V(0);
+        double sum = 0.0;  // hub-row chunk sums in fp64 (fp32: a lane's U entries in fp32)
+        if constexpr (sizeof(V) == 8) {
 #pragma unroll
-        for (int q = 0; q < U; ++q) sum += v[q];
+            for (int q = 0; q < U; ++q) sum += v[q];
+        } else {
+            V blk = v[0];
+#pragma unroll
+            for (int q = 1; q < U; ++q) blk += v[q];
+            sum = (double)blk;
+        }
         sum = warp_sum_v(sum);
         if (lane == 0) a.hub_part[t] = (double)sum;
     } else {
@@ -414,6 +421,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
             rb = __shfl_sync(0xffffffffu, rb, leader);
             rend = __shfl_sync(0xffffffffu, rend, leader);
         }
+        // pack rows: <= 8 entries per lane, summed in V; hub rows (chunk tiles) use fp64
         V sum = V(0);
         for (int jj = rb + li; jj < rend; jj += kPackUnroll * L) {
             int c[kPackUnroll];
@@ -534,15 +542,15 @@ __global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const i
     for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < n_hub;
          h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         const int f0 = hub_first[h], f1 = hub_first[h + 1];
-        V tot = V(0);
-        for (int q = f0 + lane; q < f1; q += 32) tot += (V)a.hub_part[q];
+        double tot = 0.0;
+        for (int q = f0 + lane; q < f1; q += 32) tot += a.hub_part[q];
         tot = warp_sum_v(tot);
         if (lane == 0) {
             const int64_t deg = a.rp[h + 1] - a.rp[h];
             double q0 = 0.0, q1 = 0.0;
             const V hp = EPI != EPI_PLAIN ? prev_src<EPI>(a)[h] : V(0);
             const V ha = EPI == EPI_CPAA ? a.acc[h] : V(0);
-            epilogue_v<EPI>(a, h, tot, deg, hp, ha, q0, q1);
+            epilogue_v<EPI>(a, h, (V)tot, deg, hp, ha, q0, q1);
             if (a.hub_ts) {
                 a.hub_ts[2 * h] = q0;
                 a.hub_ts[2 * h + 1] = q1;

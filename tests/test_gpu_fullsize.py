@@ -110,4 +110,8 @@ def test_config5_full_size(cheb):
         p[seeds[r]] = 1.0
         single = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, personalization=p))
         assert np.max(np.abs(single.ranks - res.ranks[:, r])) <= 1e-12
+    # fp32 variant (fp32 storage, fp64 row sums): relative L1 <= 1e-6 per column
+    f32 = cheb.run_cpaa_batch(dg, cheb.SolverConfig(eps=1e-10, precision=32), seeds=seeds)
+    rel = np.sum(np.abs(f32.ranks - res.ranks), axis=0) / np.sum(np.abs(res.ranks), axis=0)
+    assert rel.max() <= 1e-6, rel.max()
     dg.free()
