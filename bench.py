@@ -443,6 +443,34 @@ def measured_traffic(config, precision, world):
         return None
 
 
+def power_comparator(dg, flush, precision):
+    """The paper's comparison on the same resident graph: CPAA to L1 error 1e-10 (39 terms)
+    against the Power method for its a-priori round count 2 c^k <= 1e-10 (146 rounds),
+    both through the public API with the ranks read back (wall clock, L2 flushed, best of 3)."""
+    import torch
+    import paper_2112_01743_b200 as cheb
+    k_pow = 1
+    while 2.0 * DAMPING ** k_pow > EPS:
+        k_pow += 1
+
+    def best(fn):
+        fn()
+        ts = []
+        for _ in range(3):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t)
+        return min(ts) * 1e3
+    p_ms = best(lambda: cheb.run_power(dg, cheb.PowerConfig(c=DAMPING, rounds=k_pow)))
+    c_ms = best(lambda: cheb.run_cpaa(dg, cheb.SolverConfig(c=DAMPING, eps=EPS, precision=precision)))
+    return {"cpaa_api_ms": round(c_ms, 3), "cpaa_terms": cheb.plan_iterations(DAMPING, EPS).M,
+            "power_api_ms": round(p_ms, 3), "power_rounds": k_pow, "power_dtype": "f64",
+            "speedup": round(p_ms / c_ms, 2),
+            "note": "same resident graph, public API incl. ranks read-back, wall clock, best of 3"}
+
+
 def cpu_baseline_line(solver, cfg, args):
     """The reference compiled unmodified (oracle/_ref) on the same CSR, all host threads; for
     the batched config the reference has no personalisation, so one column of the restated
@@ -578,6 +606,9 @@ def main():
     peak, peak_kind = peaks()
     achieved = B / (mean_term * 1e-3) / 1e9
 
+    comparator = None
+    if dist.world == 1 and R == 1 and not args.no_e2e:
+        comparator = power_comparator(dg, flush, args.precision)
     e2e = None if args.no_e2e else sv.e2e(device, args.steps, flush, dist, comm, args.warmup)
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
@@ -618,6 +649,7 @@ def main():
                          "mean_launch_us": round(mean_term * 1e3, 3), "peak_kind": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            **({"power_comparator": comparator} if comparator else {}),
             "gpu_launches": launches,
             "clocks": clk_summary,
             "lsu_roofline": lsu_roofline(args.config, args.precision, dist.world, mean_term * 1e3,

@@ -7,6 +7,11 @@ namespace chebgpu {
 
 // ---------------- Power method (power.cpp:28-109) -------------------------------------
 namespace {
+__global__ void k_fill(double* __restrict__ x, int64_t n, double v) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        x[u] = v;
+}
+
 template <class RP>
 void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int mode,
              const double* h_ref, double* ranks, cheb_trace_row* trace, int cap, int* rounds_out,
@@ -21,11 +26,9 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
     const double base = (1.0 - c) / (double)n;
     const double x0 = 1.0 / (double)n;
     {   // x = e/n, contrib = x D^-1
-        std::vector<double> h(n, x0);
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(X, h.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        k_fill<<<grid1d(n), kThreads, 0, st>>>(X, n, x0);
         k_prescale<RP, double><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, X, n, C[0]);
         CHEB_CUDA_CHECK(cudaGetLastError());
-        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     }
     DevMem d_ref, d_err;
     if (h_ref) {
@@ -38,9 +41,10 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
     double* dtr = w.trace.ptr<double>();
     const int grid = L.fast ? g->view.grid : 0;
     int k = 0;
-    // Speculative batches of rounds (no reference tracking): every round's x is snapshotted,
-    // the batch's L1 changes and masses are read back once, and the solve stops at the first
-    // round that meets tol — its x is in the snapshots, so the result is the per-round one.
+    // Speculative batches of rounds (no reference tracking): round j of a batch reads x from
+    // snapshot j-1 and writes snapshot j, the batch's L1 changes and masses are read back once,
+    // and the solve stops at the first round that meets tol — its x is in the snapshots, so
+    // the result is the per-round one.
     const int B = h_ref ? 0 : (int)std::min<int64_t>(16, std::max(budget, 1));
     DevMem snaps;
     if (B > 0) {
@@ -63,6 +67,7 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
         CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, rev[2 * j], rev[2 * j + 1]));
         return (double)ms;
     };
+    double final_mass = -1.0;  // FAST: the last round's device mass (fixed-order sum of x)
     if (snaps) {
         double* S = snaps.ptr<double>();
         CHEB_CUDA_CHECK(cudaMemcpyAsync(S, X, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
@@ -73,26 +78,27 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
             for (int j = 1; j <= nb; ++j) {
                 const int kk = k + j;
                 double* Sj = S + (size_t)j * n;
-                CHEB_CUDA_CHECK(cudaMemcpyAsync(Sj, Sj - n, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
                 TermArgs<RP, double> a = base_args<RP, double>(g, L);
                 a.x_in = C[(kk - 1) & 1];
                 a.x_out = C[kk & 1];
-                a.T = Sj;  // in: x_{k-1}; out: y = x_k
+                a.T = Sj - n;  // x_{k-1}
+                a.out = Sj;    // y = x_k
                 a.ck = c;
                 a.base = base;
                 a.first = 0;
-                if (L.fast) {
-                    a.part = w.part.ptr<double>();
+                if (L.fast) {  // per-round partial slots: one trace reduction per batch
+                    a.part = w.part.ptr<double>() + (size_t)(j - 1) * grid * 2;
                     a.hub_part = w.hub_part.ptr<double>();
                     a.hub_cnt = w.hub_cnt.ptr<unsigned>();
-                    a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() : nullptr;
+                    a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() + (size_t)(j - 1) * g->view.n_hub * 2 : nullptr;
                 }
                 CHEB_CUDA_CHECK(cudaEventRecord(rev[2 * (j - 1)], st));
                 launch_pass<EPI_POWER>(g, L, a);
                 CHEB_CUDA_CHECK(cudaEventRecord(rev[2 * (j - 1) + 1], st));
-                if (L.fast)
-                    k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub,
-                                                           0, dtr + 2 * (j - 1));
+            }
+            if (L.fast) {
+                k_trace_reduce<<<nb, kThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
+                                                        (int)g->view.n_hub, 0, dtr);
                 CHEB_CUDA_CHECK(cudaGetLastError());
             }
             if (!L.fast) {
@@ -119,10 +125,12 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
             if (stop) {
                 k += stop;
                 final_x = S + (size_t)stop * n;
+                final_mass = h[2 * (stop - 1) + 1];
                 done = true;
             } else {
                 k += nb;
                 final_x = S + (size_t)nb * n;
+                final_mass = h[2 * (nb - 1) + 1];
                 done = k >= budget;
                 if (!done)  // next batch starts from this batch's last x
                     CHEB_CUDA_CHECK(cudaMemcpyAsync(S, final_x, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
@@ -192,7 +200,9 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
     CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, o.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     *rounds_out = k;
-    *total = kahan_sum(ranks, n);
+    // FAST: the device's fixed-order mass of the final x (a host Kahan pass over n entries
+    // costs milliseconds); BITEXACT and unbatched runs: Kahan(x) as the reference
+    *total = L.fast && final_mass >= 0.0 ? final_mass : kahan_sum(ranks, n);
 }
 }  // namespace
 

@@ -64,9 +64,9 @@ struct TermArgs {
     const double* __restrict__ inv;  // non-null iff non-canonical inv_degree
     const V* __restrict__ x_in;      // x_k = T_k D^-1
     V* __restrict__ x_out;           // x_{k+1}
-    V* T;                            // CPAA: T_{k-1} in, T_{k+1} out (in place); POWER: x in/out
+    V* T;                            // CPAA: T_{k-1} in, T_{k+1} out (in place); POWER: x in (and out)
     const V* T_prev;                 // GEN: T_{k-1}
-    V* out;                          // GEN: T_next; PLAIN: y
+    V* out;                          // GEN: T_next; PLAIN: y; POWER: x_k if not in place
     V* acc;
     double ck;    // CPAA: c_k ; POWER: c
     double base;  // POWER: (1-c)/n
@@ -106,7 +106,7 @@ __device__ __forceinline__ void epilogue(const TermArgs<RP, V>& a, int64_t u, V 
         } else {  // EPI_POWER
             const V y = add_rn(mul_rn((V)a.ck, s), (V)a.base);
             const V old = a.T[u];
-            a.T[u] = y;
+            (a.out ? a.out : a.T)[u] = y;  // out: a separate x_k buffer (Power snapshots)
             a.x_out[u] = mul_rn(y, inv);
             p0 += fabs((double)y - (double)old);
             p1 += (double)y;
@@ -251,7 +251,7 @@ __device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, 
             a.out[u] = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
         } else {  // EPI_POWER
             const V y = add_rn(mul_rn((V)a.ck, s), (V)a.base);
-            a.T[u] = y;
+            (a.out ? a.out : a.T)[u] = y;
             a.x_out[u] = mul_rn(y, inv);
             p0 += fabs((double)y - (double)prev);
             p1 += (double)y;
