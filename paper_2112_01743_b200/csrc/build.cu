@@ -882,6 +882,24 @@ static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
     return tiles;
 }
 
+// Each of the first `segs` view rows' renamed ids in ascending order (cub segmented sort,
+// in place over V.col).
+template <class RPN>
+static void sort_view_rows_t(SolverView& V, int64_t segs, int64_t items, cudaStream_t st) {
+    if (segs <= 0 || items <= 0) return;
+    TempStore tmp;
+    const RPN* offs = V.row_ptr.ptr<RPN>();
+    DevMem alt(sizeof(int) * (size_t)items + 64);
+    cub::DoubleBuffer<int> db(V.col.ptr<int>(), alt.ptr<int>());
+    size_t bytes = 0;
+    CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, db, (int)items, (int)segs, offs, offs + 1, st));
+    void* t = tmp.get(bytes);
+    CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, db, (int)items, (int)segs, offs, offs + 1, st));
+    if (db.Current() != V.col.ptr<int>())
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(V.col.get(), db.Current(), sizeof(int) * items, cudaMemcpyDeviceToDevice, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
 template <class RPO, class RPN>
 static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<void()>& before_col) {
     SolverView& V = g->view;
@@ -1070,17 +1088,8 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         V.sorted_rows = sort_rows && !hubs_only;
         if (sort_rows) {
             const int64_t segs = hubs_only ? V.n_hub : nl;
-            const RPN* offs = V.row_ptr.ptr<RPN>();
-            const int64_t items = hubs_only ? (int64_t)read_scalar(offs + segs, st) : nnz_l;
-            DevMem alt(sizeof(int) * (size_t)items + 64);
-            cub::DoubleBuffer<int> db(V.col.ptr<int>(), alt.ptr<int>());
-            size_t bytes = 0;
-            CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, db, (int)items, (int)segs, offs, offs + 1, st));
-            void* t = tmp.get(bytes);
-            CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, db, (int)items, (int)segs, offs, offs + 1, st));
-            if (db.Current() != V.col.ptr<int>())
-                CHEB_CUDA_CHECK(cudaMemcpyAsync(V.col.get(), db.Current(), sizeof(int) * items, cudaMemcpyDeviceToDevice, st));
-            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+            const int64_t items = hubs_only ? (int64_t)read_scalar(V.row_ptr.ptr<RPN>() + segs, st) : nnz_l;
+            sort_view_rows_t<RPN>(V, segs, items, st);
         }
     }
     if (g->inv_array) {
@@ -1103,6 +1112,15 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     V.ready = true;
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     dbg_mark("  view: synced");
+}
+
+void sort_view_rows(cheb_graph* g) {
+    ensure_view(g);
+    SolverView& V = g->view;
+    if (V.sorted_rows || V.n_local == 0 || V.nnz_local >= INT32_MAX) return;
+    if (V.rp64) sort_view_rows_t<int64_t>(V, V.n_local, V.nnz_local, g->stream);
+    else sort_view_rows_t<int>(V, V.n_local, V.nnz_local, g->stream);
+    V.sorted_rows = true;
 }
 
 void ensure_view(cheb_graph* g) {

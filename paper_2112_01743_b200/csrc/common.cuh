@@ -347,6 +347,8 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
                 int64_t nnz, const double* inv_degree, const std::function<void()>& host_checks);
 void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees);
 void ensure_view(cheb_graph* g);
+// Ascending renamed ids within every row of the (existing) solver view, in place.
+void sort_view_rows(cheb_graph* g);
 void finalize_stats(cheb_graph* g);
 // ingest.cu
 void load_graph_text(cheb_graph* g, const std::string& path, const char* mem, int64_t mem_bytes, int format,

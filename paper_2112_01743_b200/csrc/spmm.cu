@@ -653,15 +653,14 @@ void cpaa_batch_solve(cheb_graph* g, const BatchSpec& s, std::vector<double>& tr
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         if (tuning().sortrows != 0 && !g->view.sorted_rows && x_bytes > (int64_t)l2 && !g->want_sorted_rows) {
-            g->want_sorted_rows = true;
-            g->view.ready = false;
-            if (g->ws.exec) {  // a captured scalar solve baked the old view in
+            g->want_sorted_rows = true;  // (kept for view rebuilds)
+            if (g->ws.exec) {  // a captured scalar solve baked the old row order in
                 cudaGraphExecDestroy(g->ws.exec);
                 g->ws.exec = nullptr;
             }
             g->ws.exec_key.clear();
             g->ws.seen_key.clear();
-            ensure_view(g);
+            sort_view_rows(g);  // in place: the view's rows, tiles and programs are unchanged
         }
     }
     if (g->view.rp64) {

@@ -389,6 +389,28 @@ def test_pageable_upload_host_narrowing(cheb):
     g2 = cheb.UndirectedGraph(host.n, host.m, host.offsets, bad, host.degrees, host.inv_degree, host.multi)
     with pytest.raises(cheb.ValidationError, match="out of range at entry 4500001"):
         cheb.upload(g2)
+    # host checks split over threads (n >= 2^18): the lowest failing vertex, reference order
+    def upload_with(deg=None, off=None):
+        g3 = cheb.UndirectedGraph(host.n, host.m, host.offsets if off is None else off, host.neighbors,
+                                  host.degrees if deg is None else deg, host.inv_degree, host.multi)
+        return cheb.upload(g3)
+    deg = host.degrees.copy()
+    deg[250_000] = 0
+    deg[200_001] = 0
+    with pytest.raises(cheb.ValidationError, match=r"vertex 200001 is isolated \(degree 0\)"):
+        upload_with(deg=deg)
+    deg[10] = 0
+    with pytest.raises(cheb.ValidationError, match=r"vertex 10 is isolated"):
+        upload_with(deg=deg)
+    off = host.offsets.copy()
+    off[230_000] = off[230_001] + 1
+    off[240_000] = off[240_001] + 1
+    with pytest.raises(cheb.ValidationError, match="offsets not monotone at vertex 230000"):
+        upload_with(off=off)
+    deg = host.degrees.copy()
+    deg[255_000] = 0                                   # isolated is checked before monotone
+    with pytest.raises(cheb.ValidationError, match="vertex 255000 is isolated"):
+        upload_with(deg=deg, off=off)
 
 
 def test_batched_more_than_one_block(cheb):
