@@ -456,7 +456,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1)
 k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles, int H) {
     extern __shared__ __align__(16) unsigned char smem[];
     V* hot = reinterpret_cast<V*>(smem);
-    const unsigned hot_s = (unsigned)__cvta_generic_to_shared(smem);
+    // shared-window address of the hot prefix, kept in a register: without the opaque move
+    // the compiler rematerialises it (S2R SR_CgaCtaId + MOV + LEA) before every hot gather
+    unsigned hot_s;
+    asm volatile("mov.b32 %0, %1;" : "=r"(hot_s) : "r"((unsigned)__cvta_generic_to_shared(smem)));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpScratch<V>& ws = reinterpret_cast<WarpScratch<V>*>(smem + kHotBytes)[warp];
     double* red = reinterpret_cast<double*>(smem + kHotBytes + kWarps * sizeof(WarpScratch<V>));
