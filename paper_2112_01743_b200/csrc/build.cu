@@ -211,16 +211,6 @@ __global__ void k_narrow_col(const int64_t* __restrict__ in, int64_t cnt, int64_
     }
 }
 
-// inv_degree canonical iff every entry is 1.0/deg bitwise (IEEE division, as the host's).
-__global__ void k_inv_check(const int64_t* __restrict__ rp, const double* __restrict__ inv, int64_t n,
-                            int* __restrict__ differs) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        const double want = __ddiv_rn(1.0, (double)(rp[v + 1] - rp[v]));
-        if (__double_as_longlong(want) != __double_as_longlong(inv[v])) *differs = 1;
-    }
-}
-
 int bits_for(int64_t n) {  // smallest s with n <= 2^s - 1 (so a row field is never all-ones)
     int s = 1;
     while ((int64_t(1) << s) <= n) ++s;
@@ -536,7 +526,7 @@ static void dbg_mark(const char* what) {
 }
 
 void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors, int64_t n,
-                int64_t nnz, const double* inv_degree, const std::function<void()>& host_checks) {
+                int64_t nnz, const double* inv_degree, const std::function<bool()>& host_checks) {
     cudaStream_t st = g->stream;
     const bool dbg = dbg_on();
     dbg_t0() = std::chrono::steady_clock::now();
@@ -556,21 +546,11 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
                                                                    g->row_ptr.ptr<int>());
         CHEB_CUDA_CHECK(cudaGetLastError());
     }
-    // 2. inv_degree: checked on the device; kept only when not canonical (graph.cpp:97-100)
-    DevMem flags(sizeof(unsigned long long) + sizeof(int));
+    // 2. first out-of-range neighbour entry (device verdict)
+    DevMem flags(sizeof(unsigned long long));
     auto* bad = flags.ptr<unsigned long long>();
-    auto* inv_differs = reinterpret_cast<int*>(flags.ptr<char>() + sizeof(unsigned long long));
     CHEB_CUDA_CHECK(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
-    CHEB_CUDA_CHECK(cudaMemsetAsync(inv_differs, 0, sizeof(int), st));
     g->inv_array = false;
-    if (inv_degree) {
-        g->inv.alloc(sizeof(double) * n);
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(g->inv.get(), inv_degree, sizeof(double) * n,
-                                        cudaMemcpyHostToDevice, st));
-        k_inv_check<<<grid_for(n), kBuildThreads, 0, st>>>(rp64.ptr<int64_t>(), g->inv.ptr<double>(), n,
-                                                          inv_differs);
-        CHEB_CUDA_CHECK(cudaGetLastError());
-    }
     cudaEvent_t ev_rp = nullptr, ev_col = nullptr, ev_view = nullptr;
     struct Events {
         cudaEvent_t* e[3];
@@ -613,8 +593,10 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
     if (!pageable) CHEB_CUDA_CHECK(cudaEventRecord(ev_col, st));
     mark("enqueued copies");
 
-    // 4. the reference's host-side checks, while the copies are in flight
-    if (host_checks) host_checks();
+    // 4. the reference's host-side checks, while the copies are in flight; they also tell
+    //    whether inv_degree is canonical (graph.cpp:97-99) — only a non-canonical one is
+    //    uploaded (the reference's poisoned-array semantics, cpaa.cpp:107)
+    const bool inv_canonical = host_checks ? host_checks() : inv_degree == nullptr;
     mark("host checks");
     int64_t host_bad = -1;
     bool joined = !pageable;
@@ -654,18 +636,20 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
     finish_narrowing();
     rp64.release();  // (int32 graphs) stream-ordered after the narrowing and the inv check
 
-    // 6. device-side verdicts
-    unsigned char out[sizeof(unsigned long long) + sizeof(int)];
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(out, flags.get(), sizeof out, cudaMemcpyDeviceToHost, st));
-    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    // 6. device-side verdict; a non-canonical inv_degree goes up now (the view, built
+    //    without it, is rebuilt with it on first use)
+    if (inv_degree && !inv_canonical) {
+        g->inv.alloc(sizeof(double) * n);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(g->inv.get(), inv_degree, sizeof(double) * n,
+                                        cudaMemcpyHostToDevice, st));
+    }
     unsigned long long b;
-    int differs;
-    std::memcpy(&b, out, sizeof b);
-    std::memcpy(&differs, out + sizeof b, sizeof differs);
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(&b, flags.get(), sizeof b, cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     mark("synced");
     if (host_bad >= 0 && (b == ~0ull || (unsigned long long)host_bad < b)) b = (unsigned long long)host_bad;
     if (b != ~0ull) fail(CHEB_VALIDATION, "neighbor id out of range at entry " + std::to_string(b));
-    g->inv_array = inv_degree && differs;
+    g->inv_array = inv_degree && !inv_canonical;
     if (g->inv_array && g->view.ready) {  // the view gathers inv in its row order
         g->view.ready = false;
     }

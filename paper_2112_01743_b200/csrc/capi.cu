@@ -306,6 +306,7 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
         auto host_checks = [&] {
             struct Part {
                 int64_t isolated = -1, nonmono = -1, dmin = INT64_MAX, dmax = 0;
+                bool inv_differs = false;
             };
             const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
             const int T = n >= (int64_t(1) << 18) ? std::min(8, hw) : 1;
@@ -324,6 +325,16 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
                     p.dmin = d < p.dmin ? d : p.dmin;
                     p.dmax = d > p.dmax ? d : p.dmax;
                 }
+                // inv_degree canonical iff every entry is 1.0/row length bitwise (IEEE
+                // division, as graph.cpp:97-99 stores it): then it is never uploaded
+                if (inv_degree)
+                    for (int64_t v = lo; v < hi && !p.inv_differs; ++v) {
+                        const double want = 1.0 / (double)(offsets[v + 1] - offsets[v]);
+                        uint64_t a, b;
+                        std::memcpy(&a, &want, 8);
+                        std::memcpy(&b, inv_degree + v, 8);
+                        p.inv_differs = a != b;
+                    }
             };
             std::vector<std::thread> th;
             for (int t = 1; t < T; ++t) th.emplace_back(scan, t);
@@ -342,6 +353,9 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
             }
             g->min_degree = dmin;
             g->max_degree = dmax;
+            for (const Part& p : parts)
+                if (p.inv_differs) return false;
+            return true;
         };
         upload_csr(g.get(), offsets, neighbors, n, nnz, inv_degree, host_checks);
         *out = g.release();

@@ -341,10 +341,12 @@ inline Tuning& tuning() {
 void build_from_edges(cheb_graph* g, const void* d_edges, int64_t E, int edge_bits,
                       const cheb_build_opts& o);
 // Upload of a host CSR: the H2D copies are enqueued first, `host_checks` (the reference's
-// host-side validation) runs while they are in flight, and the solver view is built on an
-// auxiliary stream as soon as the offsets have landed, overlapping the neighbour copy.
+// host-side validation; returns whether inv_degree is 1.0/row length bitwise) runs while
+// they are in flight, and the solver view is built on an auxiliary stream as soon as the
+// offsets have landed, overlapping the neighbour copy.  A canonical inv_degree is never
+// copied (the kernels take the reciprocal of the row length, bit-identical).
 void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors, int64_t n,
-                int64_t nnz, const double* inv_degree, const std::function<void()>& host_checks);
+                int64_t nnz, const double* inv_degree, const std::function<bool()>& host_checks);
 void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees);
 void ensure_view(cheb_graph* g);
 // Ascending renamed ids within every row of the (existing) solver view, in place.
