@@ -579,7 +579,9 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
         hn.start(neighbors, nnz, n, g->col.ptr<int>(), st, g->device);
     } else if (nnz > 0) {
         const int64_t chunk = std::min<int64_t>(nnz, int64_t(1) << 25);
-        DevMem stage[2] = {DevMem(sizeof(int64_t) * chunk), DevMem(sizeof(int64_t) * chunk)};
+        DevMem stage[2];
+        stage[0].alloc(sizeof(int64_t) * chunk);
+        if (chunk < nnz) stage[1].alloc(sizeof(int64_t) * chunk);
         int i = 0;
         for (int64_t off = 0; off < nnz; off += chunk, i ^= 1) {
             const int64_t c = std::min(chunk, nnz - off);
@@ -1041,6 +1043,12 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     if (before_col) before_col();
     if (nl > 0) {
         // rows are degree-descending: [0, n_huge) > 1024 entries, [n_huge, n_long) > 16
+        cudaEvent_t dbg_ev[2] = {};
+        if (dbg_on()) {
+            cudaEventCreate(&dbg_ev[0]);
+            cudaEventCreate(&dbg_ev[1]);
+            cudaEventRecord(dbg_ev[0], st);
+        }
         int64_t n_huge = 0, n_long = 0;
         for (size_t r = 0; r < run_deg.size(); ++r) {
             if (run_deg[r] > 1024) n_huge += run_cnt[r];
@@ -1058,6 +1066,15 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
             k_permute_rows<4><<<grid_for((nl - n_long) * 4), kBuildThreads, 0, st>>>(
                 rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, n_long, nl, V.col.ptr<int>());
         CHEB_CUDA_CHECK(cudaGetLastError());
+        if (dbg_ev[0]) {  // CHEB_DEBUG_UPLOAD: neighbours landed + narrowed, then permuted
+            cudaEventRecord(dbg_ev[1], st);
+            cudaEventSynchronize(dbg_ev[1]);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, dbg_ev[0], dbg_ev[1]);
+            dbg_mark(("  view: columns permuted (permute " + std::to_string(ms) + " ms)").c_str());
+            cudaEventDestroy(dbg_ev[0]);
+            cudaEventDestroy(dbg_ev[1]);
+        }
         // When x does not fit L2 (config 4), ascending renamed ids within each row: a row's
         // gathers then walk x in address order (DRAM page / sector locality; C4 4.49 -> 4.03
         // ms/term).  When x fits L2 the storage order is kept (sorting cost C2 ~1%).  The

@@ -309,32 +309,29 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
                 bool inv_differs = false;
             };
             const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-            const int T = n >= (int64_t(1) << 18) ? std::min(8, hw) : 1;
+            const int T = n >= (int64_t(1) << 18) ? std::min(16, hw) : 1;
             std::vector<Part> parts(T);
-            auto scan = [&](int t) {
-                Part& p = parts[t];
+            auto scan = [&](int t) {  // one pass over the chunk: every check's first failure
                 const int64_t lo = n * t / T, hi = n * (t + 1) / T;
-                for (int64_t v = lo; v < hi; ++v)
-                    if (degrees[v] < 1) {
-                        p.isolated = v;
-                        break;
-                    }
-                for (int64_t v = lo; v < hi; ++v) {  // one pass: monotone offsets + degree extrema
+                int64_t isolated = -1, nonmono = -1, dmin = INT64_MAX, dmax = 0;
+                bool differs = false;
+                for (int64_t v = lo; v < hi; ++v) {
+                    if (degrees[v] < 1 && isolated < 0) isolated = v;
                     const int64_t d = offsets[v + 1] - offsets[v];
-                    if (d < 0 && p.nonmono < 0) p.nonmono = v;
-                    p.dmin = d < p.dmin ? d : p.dmin;
-                    p.dmax = d > p.dmax ? d : p.dmax;
-                }
-                // inv_degree canonical iff every entry is 1.0/row length bitwise (IEEE
-                // division, as graph.cpp:97-99 stores it): then it is never uploaded
-                if (inv_degree)
-                    for (int64_t v = lo; v < hi && !p.inv_differs; ++v) {
-                        const double want = 1.0 / (double)(offsets[v + 1] - offsets[v]);
+                    if (d < 0 && nonmono < 0) nonmono = v;
+                    dmin = d < dmin ? d : dmin;
+                    dmax = d > dmax ? d : dmax;
+                    // inv_degree canonical iff every entry is 1.0/row length bitwise (IEEE
+                    // division, as graph.cpp:97-99 stores it): then it is never uploaded
+                    if (inv_degree) {
+                        const double want = 1.0 / (double)d;
                         uint64_t a, b;
                         std::memcpy(&a, &want, 8);
                         std::memcpy(&b, inv_degree + v, 8);
-                        p.inv_differs = a != b;
+                        differs |= a != b;
                     }
+                }
+                parts[t] = Part{isolated, nonmono, dmin, dmax, differs};  // locals: no false sharing
             };
             std::vector<std::thread> th;
             for (int t = 1; t < T; ++t) th.emplace_back(scan, t);
