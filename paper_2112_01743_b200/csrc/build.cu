@@ -747,6 +747,119 @@ __global__ void k_permute_rows(const RPO* __restrict__ rp_old, const int* __rest
     }
 }
 
+// Bank-aware order of hub-row chunks (FAST schedule only).  A chunk tile is read as lane l
+// of instruction q -> chunk position l + 32 q, so positions [16 w, 16 w + 16) are one
+// half-warp: one conflict group of an fp64 shared-memory gather.  Each chunk is ordered so
+// that every such window holds hot-prefix entries (ids < H) with distinct bank pairs
+// (id mod 16): the k-th entry of bank pair r goes to window k, the hot entries of a window
+// in bank-pair order, cold entries filling the remaining slots in their original order.
+// A chunk where some bank pair has more entries than there are windows keeps its order.
+// The entry set is unchanged (its partial sum is re-associated, deterministically).
+// val[q] = entry at position lane + 32 q (cnt <= 256); returns dst[q] (or -1: no entry).
+struct SchedScratch {
+    int cnt[17], msk[16], f[16];
+};
+__device__ __forceinline__ void schedule_chunk(const int (&val)[8], int cnt, int H, SchedScratch& sc,
+                                               int (&dst)[8]) {
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const int W = (cnt + 15) >> 4;
+    if (lane < 17) sc.cnt[lane] = 0;
+    __syncwarp();
+    int key[8], rk[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {  // key (bank pair 0..15, 16 = cold), stable rank within it
+        const int p = lane + 32 * q;
+        const bool live = p < cnt;
+        key[q] = live ? ((unsigned)val[q] < (unsigned)H ? (val[q] & 15) : 16) : 17;
+        const unsigned peers = __match_any_sync(0xffffffffu, key[q]);
+        rk[q] = live ? sc.cnt[key[q]] + __popc(peers & lt) : 0;
+        __syncwarp();
+        if (live && (peers & lt) == 0) sc.cnt[key[q]] += __popc(peers);  // one leader per key
+        __syncwarp();
+    }
+    // feasible iff every bank pair fits one entry per window, the last window included
+    const int c = lane < 16 ? sc.cnt[lane] : 0;
+    const int last_cap = cnt - 16 * (W - 1);
+    const int h_last = __popc(__ballot_sync(0xffffffffu, lane < 16 && c > W - 1));
+    if (!__all_sync(0xffffffffu, c <= W) || h_last > last_cap) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[q] = lane + 32 * q < cnt ? lane + 32 * q : -1;
+        return;
+    }
+    // window k: the bank pairs with more than k entries (mask; h_k of them first), then
+    // free_k cold slots; F_k = cold entries placed before window k
+    int Mk = 0;
+    for (int k = 0; k < W; ++k) {
+        const unsigned m = __ballot_sync(0xffffffffu, lane < 16 && c > k) & 0xffffu;
+        if (lane == k) Mk = (int)m;
+    }
+    const int free_k = lane < W ? (lane == W - 1 ? last_cap : 16) - __popc(Mk) : 0;
+    int F = free_k;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, F, o);
+        if (lane >= o) F += y;
+    }
+    F -= free_k;
+    if (lane < 16) {
+        sc.msk[lane] = Mk;
+        sc.f[lane] = lane < W ? F : 1 << 30;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        int d = -1;
+        if (lane + 32 * q < cnt) {
+            if (key[q] < 16) {  // hot: window rk, after the smaller bank pairs present there
+                d = 16 * rk[q] + __popc(sc.msk[rk[q]] & ((1 << key[q]) - 1));
+            } else {  // cold rank j: the last window whose first cold rank is <= j
+                int k = 0;
+#pragma unroll
+                for (int step = 8; step; step >>= 1)
+                    if (k + step < 16 && sc.f[k + step] <= rk[q]) k += step;
+                d = 16 * k + __popc(sc.msk[k]) + (rk[q] - sc.f[k]);
+            }
+        }
+        dst[q] = d;
+    }
+    __syncwarp();
+}
+
+// View columns of the hub rows (rows [0, n_hub), degree > kWarpNnz): one warp per chunk tile
+// renames the old row's slice and writes it in bank-aware order (identity when sched == 0).
+template <class RPO, class RPN>
+__global__ void k_permute_chunks(const Tile* __restrict__ tiles, int n_chunk_tiles, const RPO* __restrict__ rp_old,
+                                 const int* __restrict__ col_old, const RPN* __restrict__ rp_new,
+                                 const int* __restrict__ order, const int* __restrict__ rank, int H, int sched,
+                                 int* __restrict__ col_new) {
+    __shared__ SchedScratch scr[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_chunk_tiles;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const Tile a = tiles[t];
+        const int64_t z0 = a.nnz_begin;
+        const int cnt = (int)(tiles[t + 1].nnz_begin - z0);
+        const int h = a.row_begin;
+        const int64_t src = (int64_t)rp_old[order[h]] + (z0 - (int64_t)rp_new[h]);
+        int val[8], dst[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int p = lane + 32 * q;
+            val[q] = p < cnt ? rank[col_old[src + p]] : 0;
+        }
+        if (sched) {
+            schedule_chunk(val, cnt, H, scr[w], dst);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) dst[q] = lane + 32 * q < cnt ? lane + 32 * q : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (dst[q] >= 0) col_new[z0 + dst[q]] = val[q];
+    }
+}
+
 // padded exchange position of every old id: new id u on rank r -> r*max_rows + (u - cuts[r])
 __global__ void k_posmap(const int* __restrict__ rank_of_old, int64_t n, const int64_t* __restrict__ cuts, int G,
                          int64_t max_rows, int* __restrict__ pos) {
@@ -1042,23 +1155,32 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     V.col.alloc(sizeof(int) * std::max<int64_t>(nnz_l, 1) + 64);  // TMA reads round up to 16 B
     if (before_col) before_col();
     if (nl > 0) {
-        // rows are degree-descending: [0, n_huge) > 1024 entries, [n_huge, n_long) > 16
         cudaEvent_t dbg_ev[2] = {};
         if (dbg_on()) {
             cudaEventCreate(&dbg_ev[0]);
             cudaEventCreate(&dbg_ev[1]);
             cudaEventRecord(dbg_ev[0], st);
         }
-        int64_t n_huge = 0, n_long = 0;
+        // rows are degree-descending: hub rows [0, n_hub) by chunk tiles (in bank-aware
+        // order), then [n_hub, n_huge) > 1024 entries, [n_huge, n_long) > 16, the rest <= 16
+        int64_t n_huge = V.n_hub, n_long = V.n_hub, seen = 0;
         for (size_t r = 0; r < run_deg.size(); ++r) {
-            if (run_deg[r] > 1024) n_huge += run_cnt[r];
-            if (run_deg[r] > 16) n_long += run_cnt[r];
+            const int64_t r0 = seen, r1 = seen + run_cnt[r];
+            seen = r1;
+            if (r1 <= V.n_hub) continue;
+            const int64_t c = r1 - std::max(r0, V.n_hub);
+            if (run_deg[r] > 1024) n_huge += c;
+            if (run_deg[r] > 16) n_long += c;
         }
         const int* order_l = V.order.ptr<int>() + lo;
         const RPN* rp_l = V.row_ptr.ptr<RPN>();
-        if (n_huge > 0)
-            k_permute_rows<0><<<(int)std::min<int64_t>(n_huge, 148 * 16), kBuildThreads, 0, st>>>(
-                rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, 0, n_huge, V.col.ptr<int>());
+        if (V.n_chunk_tiles > 0)
+            k_permute_chunks<RPO, RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
+                V.tiles.ptr<Tile>(), V.n_chunk_tiles, rp_old, g->col.ptr<int>(), rp_l, order_l, colmap,
+                kHotBytes / 8, tuning().chunksched, V.col.ptr<int>());
+        if (n_huge > V.n_hub)
+            k_permute_rows<0><<<(int)std::min<int64_t>(n_huge - V.n_hub, 148 * 16), kBuildThreads, 0, st>>>(
+                rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, V.n_hub, n_huge, V.col.ptr<int>());
         if (n_long > n_huge)
             k_permute_rows<32><<<grid_for((n_long - n_huge) * 32), kBuildThreads, 0, st>>>(
                 rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, n_huge, n_long, V.col.ptr<int>());

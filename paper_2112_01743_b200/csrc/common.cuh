@@ -323,6 +323,7 @@ struct Tuning {
     int l2win = 1;      // 1: persisting-L2 window over the hot prefix of x (default on)
     int pdl = 1;        // 1: programmatic dependent launch along the term chain (default on)
     int sortrows = -1;  // view rows in ascending id order: -1 when x exceeds L2, 0 never, 1 always
+    int chunksched = 1; // hub chunks ordered for conflict-free hot gathers (k_schedule_chunks)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -333,6 +334,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_L2WIN")) x.l2win = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_PDL")) x.pdl = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_SORTROWS")) x.sortrows = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_CHUNKSCHED")) x.chunksched = std::atoi(e);
         return x;
     }();
     return t;
