@@ -93,7 +93,8 @@ cheb_status cheb_graph_build_device(const void* d_edges, int64_t E, int edge_bit
 
 /* Upload a host CSR (UndirectedGraph arrays).  essential_check semantics of
  * cpaa.cpp:16-26 (n>=1, consistent sizes, every degree>=1).  inv_degree may be NULL;
- * when given it is compared bitwise with 1.0/deg: if canonical the kernels use an
+ * when given it is compared bitwise with 1.0/deg on the host (threads, while the CSR
+ * copies are in flight): if canonical it is never copied and the kernels use an
  * in-register reciprocal (no array traffic), else the array is uploaded and used
  * (the reference reads it, cpaa.cpp:107 — e.g. the poisoned test, test_cpaa.cpp:371). */
 cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
