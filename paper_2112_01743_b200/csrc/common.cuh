@@ -245,7 +245,6 @@ struct Workspace {
     DevMem T0, T1, X0, X1, acc, out;    // vectors (solve precision), out = ranks (orig order)
     DevMem part;                        // double [M][grid][2] block trace partials
     DevMem hub_part;                    // double [grid] chunk partials
-    DevMem hub_cnt;                     // uint32 [n_hub]
     DevMem hub_ts;                      // double [M][n_hub][2]
     DevMem trace;                       // double [M][2] (mass_T, S_k)
     DevMem total;                       // double [1]
@@ -258,7 +257,7 @@ struct Workspace {
     int launches = 0;
     // every buffer back to the pool on its stream (the owner calls this while the stream lives)
     void release_buffers() {
-        for (DevMem* d : {&T0, &T1, &X0, &X1, &acc, &out, &part, &hub_part, &hub_cnt, &hub_ts, &trace, &total,
+        for (DevMem* d : {&T0, &T1, &X0, &X1, &acc, &out, &part, &hub_part, &hub_ts, &trace, &total,
                           &coeffs, &snap})
             d->release();
     }

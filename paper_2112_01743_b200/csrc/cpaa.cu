@@ -42,7 +42,6 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
         if (L.fast) {
             a.part = w.part.ptr<double>() + (size_t)(k - 1) * grid * 2;
             a.hub_part = w.hub_part.ptr<double>();
-            a.hub_cnt = w.hub_cnt.ptr<unsigned>();
             a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() + (size_t)(k - 1) * g->view.n_hub * 2 : nullptr;
         }
         if (term_ev) CHEB_CUDA_CHECK(cudaEventRecord((*term_ev)[2 * (k - 1)], st));

@@ -252,7 +252,6 @@ struct DistSolve {
         a.first = k == 1;
         a.part = w.part.ptr<double>() + (size_t)(k - 1) * Vw.grid * 2;
         a.hub_part = w.hub_part.ptr<double>();
-        a.hub_cnt = w.hub_cnt.ptr<unsigned>();
         a.hub_ts = Vw.n_hub ? w.hub_ts.ptr<double>() + (size_t)(k - 1) * Vw.n_hub * 2 : nullptr;
         if (tev) CHEB_CUDA_CHECK(cudaEventRecord((*tev)[2 * (k - 1)], st));
         launches += launch_pass<EPI_CPAA>(g, L, a);

@@ -89,7 +89,6 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
                 if (L.fast) {  // per-round partial slots: one trace reduction per batch
                     a.part = w.part.ptr<double>() + (size_t)(j - 1) * grid * 2;
                     a.hub_part = w.hub_part.ptr<double>();
-                    a.hub_cnt = w.hub_cnt.ptr<unsigned>();
                     a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() + (size_t)(j - 1) * g->view.n_hub * 2 : nullptr;
                 }
                 CHEB_CUDA_CHECK(cudaEventRecord(rev[2 * (j - 1)], st));
@@ -151,7 +150,6 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
         if (L.fast) {
             a.part = w.part.ptr<double>();
             a.hub_part = w.hub_part.ptr<double>();
-            a.hub_cnt = w.hub_cnt.ptr<unsigned>();
             a.hub_ts = g->view.n_hub ? w.hub_ts.ptr<double>() : nullptr;
         }
         CHEB_CUDA_CHECK(cudaEventRecord(rev[0], st));
@@ -236,7 +234,6 @@ void transition_t(cheb_graph* g, const double* x, double* y, int mode) {
     a.out = w.T1.ptr<double>();
     if (L.fast) {
         a.hub_part = w.hub_part.ptr<double>();
-        a.hub_cnt = w.hub_cnt.ptr<unsigned>();
     }
     launch_pass<EPI_PLAIN>(g, L, a);
     k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(w.T1.ptr<double>(), L.order, n, dx.ptr<double>());
@@ -310,7 +307,6 @@ void staged_generate_t(cheb_graph* g) {
     a.first = S.k == 1;
     if (L.fast) {
         a.hub_part = g->ws.hub_part.ptr<double>();
-        a.hub_cnt = g->ws.hub_cnt.ptr<unsigned>();
     }
     launch_pass<EPI_GEN>(g, L, a);
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));

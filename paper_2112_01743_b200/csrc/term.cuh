@@ -73,7 +73,6 @@ struct TermArgs {
     int first;
     double* part;  // [grid][2] this term
     double* hub_part;  // [n_tiles] chunk partials
-    unsigned* hub_cnt;
     double* hub_ts;  // [n_hub][2] this term
     int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
     int tune_skip;      // experiments only: 1 skip chunk tiles, 2 skip pack tiles, 16+b only bin b
@@ -1000,7 +999,7 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     const int64_t n = g->n;
     // Any reallocation invalidates the captured solve graph (it bakes in addresses).
     const void* before[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
-                            w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
+                            w.part.get(), w.hub_part.get(), w.hub_ts.get(),
                             w.trace.get(), w.total.get()};
     const int64_t vlen = std::max<int64_t>(std::max<int64_t>(n, g->view.x_len), 1);
     const size_t vb = sizeof(V) * (size_t)vlen * R;
@@ -1013,10 +1012,6 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     const int grid = std::max(g->view.ready ? g->view.grid : 1, grid1d(n));
     w.part.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max(grid, 1));
     w.hub_part.ensure(sizeof(double) * std::max(g->view.n_tiles, 1));
-    if (!w.hub_cnt || w.hub_cnt.bytes() < sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1)) {
-        w.hub_cnt.alloc(sizeof(unsigned) * (size_t)std::max<int64_t>(g->view.n_hub, 1));
-        CHEB_CUDA_CHECK(cudaMemset(w.hub_cnt.get(), 0, w.hub_cnt.bytes()));
-    }
     w.hub_ts.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max<int64_t>(g->view.n_hub, 1));
     w.trace.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1));
     w.total.ensure(sizeof(double) * 4);
@@ -1024,7 +1019,7 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     w.R = R;
     w.vbytes = sizeof(V);
     const void* after[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
-                           w.part.get(), w.hub_part.get(), w.hub_cnt.get(), w.hub_ts.get(),
+                           w.part.get(), w.hub_part.get(), w.hub_ts.get(),
                            w.trace.get(), w.total.get()};
     if (std::memcmp(before, after, sizeof before) != 0) {
         if (w.exec) cudaGraphExecDestroy(w.exec);
