@@ -1015,6 +1015,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "skip") tuning().skip = value;
         else if (k == "l2win") tuning().l2win = value;
         else if (k == "pdl") tuning().pdl = value;
+        else if (k == "chunksched") tuning().chunksched = value;  // applies to views built afterwards
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }
