@@ -321,7 +321,7 @@ struct Tuning {
     int skip = 0;       // 1: skip chunk tiles, 2: skip pack tiles, 16+b: only tile bin b (experiments only)
     int l2win = 1;      // 1: persisting-L2 window over the hot prefix of x (default on)
     int pdl = 1;        // 1: programmatic dependent launch along the term chain (default on)
-    int sortrows = -1;  // view rows in ascending id order: -1 when x exceeds L2, 0 never, 1 always
+    int sortrows = -1;  // view rows in ascending id order: -1 when x exceeds L2, 0 never, 1 always, 2 hub rows only (experiment)
     int chunksched = 1; // hub chunks ordered for conflict-free hot gathers (k_schedule_chunks)
 };
 inline Tuning& tuning() {
