@@ -2,7 +2,7 @@
 """Benchmark of the CPAA hot path (BASELINE.json metric: GTEPS per Chebyshev term and
 time-to-1e-10 on B200, with the HBM-roofline fraction).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--precision 64]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--precision 64]
     python bench.py --impl reference ...      # the reference's own CPU run_cpaa
 
 A step = one full CPAA solve to L1 error 1e-10 (M = plan_iterations(0.85, 1e-10) = 39
@@ -17,6 +17,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -47,26 +48,6 @@ CONFIGS = {
                draws=41_943_040, seed=5, drop=False, R=64,
                desc="Chung-Lu n=2^22, ~40M undirected edges, 64 one-hot seeds (degree >= 5), SpMM R=64"),
 }
-
-
-def c5_seeds(dg, R: int, seed: int = 5):
-    """64 seed vertices drawn uniformly (without replacement) from vertices of degree >= 5,
-    with a fixed counter-based draw (splitmix64), so both arms use the same seeds."""
-    deg = np.diff(dg.download().offsets)
-    cand = np.nonzero(deg >= 5)[0]
-    out, used, i = [], set(), 0
-    M64 = (1 << 64) - 1
-    while len(out) < R:
-        z = (seed * 0x9E3779B97F4A7C15 + i * 0xBF58476D1CE4E5B9) & M64
-        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
-        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
-        z ^= z >> 31
-        v = int(cand[z % len(cand)])
-        i += 1
-        if v not in used:
-            used.add(v)
-            out.append(v)
-    return np.array(out, dtype=np.int64)
 
 
 def log(*a):
@@ -188,15 +169,35 @@ class Clocks:
 # ----------------------------------------------------------------------------------------
 # inputs
 # ----------------------------------------------------------------------------------------
-def make_edges(cfg: dict, device):
+def config_dict(name: str, n: int, nnz: int, M: int, R: int) -> dict:
+    """The workload as both arms name it (identical dicts: same graph, terms, c, eps)."""
+    return {"workload": name, "desc": CONFIGS[name]["desc"], "n": n, "nnz": nnz, "R": R, "terms": M,
+            "eps": EPS, "c": DAMPING, "seed": CONFIGS[name]["seed"],
+            "l2": "GPU arm: flushed (512 MiB write) before every timed step"}
+
+
+def make_edges_device(cfg: dict, device: int):
+    """GPU arm: the product generators (counter-based R-MAT / Chung-Lu on the device)."""
     from paper_2112_01743_b200 import generate as G
     if cfg["kind"] == "gnp":
-        e = G.gnp_edges(cfg["n"], cfg["p"], cfg["seed"])
-        return e.astype(np.int32) if device is not None else e
+        return G.gnp_edges(cfg["n"], cfg["p"], cfg["seed"])
     if cfg["kind"] == "chung_lu":
         return G.chung_lu_edges(cfg["n"], cfg["gamma"], cfg["wmin"], cfg["wmax"], cfg["draws"],
                                 cfg["seed"], device=device)
     return G.rmat_edges(cfg["scale"], cfg["ef"], 0.57, 0.19, 0.19, cfg["seed"], device=device)
+
+
+def make_edges_host(cfg: dict) -> np.ndarray:
+    """CPU legs: the same edge list without the product library — the reference's own gnp
+    generator (config 1) or the plain-C restatement of the config generators
+    (oracle/synth_gen.c, pinned equal to the product's by tests/test_oracle.py)."""
+    from oracle import Oracle, Reference
+    if cfg["kind"] == "gnp":
+        return Reference().gnp_edges(cfg["n"], cfg["p"], cfg["seed"])
+    o = Oracle()
+    if cfg["kind"] == "chung_lu":
+        return o.chung_lu_edges(cfg["n"], cfg["gamma"], cfg["wmin"], cfg["wmax"], cfg["draws"], cfg["seed"])
+    return o.rmat_edges(cfg["scale"], cfg["ef"], 0.57, 0.19, 0.19, cfg["seed"])
 
 
 def build_device(cfg: dict, device: int):
@@ -204,7 +205,7 @@ def build_device(cfg: dict, device: int):
     import paper_2112_01743_b200 as cheb
     from paper_2112_01743_b200 import _lib as L
     lib = L.load()
-    e = make_edges(cfg, device)
+    e = make_edges_device(cfg, device)
     o = L.cheb_build_opts(1, int(cfg.get("drop", False)), 0, device, int(cfg.get("rp64", False)))
     h = C.c_void_p()
     inf = L.cheb_graph_info()
@@ -232,48 +233,141 @@ def peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
-    return 6650.0, "fallback"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
 
 
 # ----------------------------------------------------------------------------------------
-# reference arm / cpu baseline (the reference compiled unmodified: oracle/_ref)
+# CPU legs: the reference compiled unmodified (oracle/_ref), or the restated loop (R > 1)
 # ----------------------------------------------------------------------------------------
-def cpu_reference_run(cfg: dict, steps: int, warmup: int, threads: int, host_edges=None):
-    from oracle import Reference
-    ref = Reference()
-    e = host_edges if host_edges is not None else make_edges(cfg, None)
-    e64 = np.ascontiguousarray(np.asarray(e, dtype=np.int64).reshape(-1, 2))
-    t0 = time.perf_counter()
-    rg = ref.build_graph(e64, dedup=True, drop_isolated=cfg.get("drop", False))
-    build_s = time.perf_counter() - t0
-    M, _ = ref.plan_iterations(DAMPING, EPS)
-    walls = []
-    for i in range(warmup + steps):
-        r = rg.run_cpaa(c=DAMPING, eps=EPS, parallelism=threads)
-        if i >= warmup:
-            walls.append(r.wall_ms)
-    return dict(n=rg.n, nnz=rg.nnz, M=M, wall_ms=walls, build_s=build_s)
+CPU_STEP_TARGET_S = 6.0   # one reference step is a bounded sample of the workload
+
+
+def _rounds_for(t_round_ms: float, M: int, target_s: float) -> int:
+    return int(min(M, max(1, math.ceil(target_s * 1e3 / max(t_round_ms, 1e-3)))))
+
+
+def ref_sample(rg, M: int, threads: int, target_s: float):
+    """Calibrate with a 1-round run, then size the sample (rounds <= M) to ~target_s."""
+    t1 = rg.run_cpaa(c=DAMPING, rounds=1, parallelism=threads).wall_ms
+    return _rounds_for(t1, M, target_s)
+
+
+def port_columns(csr, seeds, M: int, rounds: int, threads: int):
+    """The restated loop (oracle/cpaa_oracle.c, cpaa.cpp:79-165 with T0 = e_seed) for
+    `threads` one-hot columns at once, one host thread each (ctypes drops the GIL).
+    Returns (wall_ms, columns)."""
+    from oracle import Oracle
+    o = Oracle()
+    cols = [int(s) for s in seeds[:threads]]
+
+    def one(s):
+        p = np.zeros(csr.n)
+        p[s] = 1.0
+        o.run_cpaa(csr, rounds, p=p)
+    ths = [threading.Thread(target=one, args=(s,)) for s in cols]
+    t = time.perf_counter()
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    return (time.perf_counter() - t) * 1e3, len(cols)
+
+
+def c5_seeds_from_degrees(deg, R: int, seed: int = 5):
+    """R seed vertices drawn uniformly (without replacement) from vertices of degree >= 5,
+    with a fixed counter-based draw (splitmix64), so both arms use the same seeds."""
+    cand = np.nonzero(np.asarray(deg) >= 5)[0]
+    out, used, i = [], set(), 0
+    M64 = (1 << 64) - 1
+    while len(out) < R:
+        z = (seed * 0x9E3779B97F4A7C15 + i * 0xBF58476D1CE4E5B9) & M64
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+        z ^= z >> 31
+        v = int(cand[z % len(cand)])
+        i += 1
+        if v not in used:
+            used.add(v)
+            out.append(v)
+    return np.array(out, dtype=np.int64)
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU run_cpaa (oracle/_ref = the unmodified
+    sources) on this box's host cores, on the same graph (edges from oracle/synth_gen.c; the
+    product library is never loaded).  One step = one run_cpaa call with a bounded round
+    count (calibrated to ~6 s; all M = 39 rounds when that fits); value = nnz * rounds /
+    wall.  For the batched config the reference has no personalisation: the restated loop
+    (oracle/cpaa_oracle.c) over one-hot columns, one host thread per column."""
     cfgname = args.config
     cfg = CONFIGS[cfgname]
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     try:
-        from oracle import REF_SO
+        from oracle import REF_SO, Reference
         if not os.path.exists(REF_SO):
             print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
             return 0
-        threads = os.cpu_count() or 1
-        res = cpu_reference_run(cfg, args.steps, args.warmup, threads)
+        threads = host_threads()
+        ref = Reference()
+        t0 = time.perf_counter()
+        e = make_edges_host(cfg)
+        gen_s = time.perf_counter() - t0
+        E = int(e.shape[0])
+        t0 = time.perf_counter()
+        rg = ref.build_graph(e, dedup=True, drop_isolated=cfg.get("drop", False))
+        build_s = time.perf_counter() - t0
+        del e
+        M, _ = ref.plan_iterations(DAMPING, EPS)
+        R = int(cfg.get("R", 1))
+        walls = []
+        if R > 1:
+            csr = rg.csr()
+            seeds = c5_seeds_from_degrees(csr.degrees, R)
+            w1, _ = port_columns(csr, seeds, M, 1, threads)
+            rounds = _rounds_for(w1, M, CPU_STEP_TARGET_S)
+            for i in range(args.warmup + args.steps):
+                w, cols = port_columns(csr, seeds, M, rounds, threads)
+                if i >= args.warmup:
+                    walls.append(w)
+            units = rg.nnz * cols * rounds
+            kind, what = "port", (f"restated loop (oracle/cpaa_oracle.c, T0 = e_seed) on {cols} of the {R} "
+                                  f"one-hot columns at once, {rounds} rounds each, one host thread per column; "
+                                  f"unit nnz*columns*rounds / wall (the reference has no personalisation)")
+        else:
+            rounds = ref_sample(rg, M, threads, CPU_STEP_TARGET_S)
+            for i in range(args.warmup + args.steps):
+                r = rg.run_cpaa(c=DAMPING, rounds=rounds, parallelism=threads)
+                if i >= args.warmup:
+                    walls.append(r.wall_ms)
+            units = rg.nnz * rounds
+            kind, what = "reference", (f"run_cpaa(c=0.85, rounds={rounds} of the M={M} terms to eps 1e-10, "
+                                       f"parallelism={threads}) per step, steady_clock wall around the call")
     except Exception as ex:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"{type(ex).__name__}: {ex}"}))
         return 0
-    ms = statistics.mean(res["wall_ms"])
-    gteps = res["nnz"] * res["M"] / (ms * 1e-3) / 1e9
+    ms = statistics.mean(walls)
+    gteps = units / (ms * 1e-3) / 1e9
     line = {
         "impl": "reference",
         "metric": "cpaa_gteps_per_term",
@@ -288,12 +382,12 @@ def run_reference_arm(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": cfgname, "desc": cfg["desc"], "n": res["n"], "nnz": res["nnz"],
-                   "terms": res["M"], "eps": EPS, "c": DAMPING, "parallelism": f"cpu{threads}"},
-        "cpu_baseline": {"value": round(gteps, 6), "unit": "GTEPS", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{cfgname}: one full run_cpaa (M={res['M']}, eps 1e-10) per step, "
-                                   f"build excluded ({res['build_s']:.1f}s)"},
+        "config": config_dict(cfgname, rg.n, rg.nnz, M, R),
+        "parallelism": f"cpu{threads}",
+        "cpu_baseline": {"value": round(gteps, 6), "unit": "GTEPS", "cores": threads, "kind": kind,
+                         "cpu_model": cpu_model(),
+                         "sample": f"{cfgname}: {what}; edges generated in {gen_s:.1f}s ({E} pairs), "
+                                   f"reference build_graph {build_s:.1f}s (excluded)"},
         "e2e": {"value": round(gteps, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -301,9 +395,56 @@ def run_reference_arm(args):
     return 0
 
 
+def cpu_baseline_line(solver, cfgname, args):
+    """The reference compiled unmodified (oracle/_ref) timed on this box's host cores on the
+    SAME CSR (downloaded; bit-exact with the reference's build_graph by the parity tests, so
+    no rebuild): a bounded sample at K = every host thread and at K = 1.  For the batched
+    config: the restated loop over one-hot columns (one host thread per column)."""
+    try:
+        from oracle import CSR, Reference
+        host = solver.dg.download()
+        threads = host_threads()
+        M = solver.M
+        csr = CSR(host.n, host.m, host.offsets, host.neighbors, host.degrees, host.inv_degree)
+        if solver.R > 1:
+            w1, _ = port_columns(csr, solver.seeds_all, M, 1, threads)
+            rounds = _rounds_for(w1, M, CPU_STEP_TARGET_S)
+            w, cols = port_columns(csr, solver.seeds_all, M, rounds, threads)
+            wk1, _ = port_columns(csr, solver.seeds_all, M, 1, 1)
+            v = host.neighbors.size * cols * rounds / (w * 1e-3) / 1e9
+            v1 = host.neighbors.size * 1 * 1 / (wk1 * 1e-3) / 1e9
+            return {"value": round(v, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
+                    "cpu_model": cpu_model(),
+                    "k1": {"value": round(v1, 6), "cores": 1, "sample": f"1 column, 1 round, wall {wk1:.0f} ms"},
+                    "sample": f"restated loop (oracle/cpaa_oracle.c, T0 = e_seed), {cols} one-hot columns at once "
+                              f"x {rounds} rounds, one host thread per column, wall {w:.0f} ms; unit nnz*columns*rounds"}
+        rg = Reference().graph_from_csr(csr)
+        del host
+        rk = ref_sample(rg, M, threads, CPU_STEP_TARGET_S)
+        wk = rg.run_cpaa(c=DAMPING, rounds=rk, parallelism=threads).wall_ms
+        t1 = rg.run_cpaa(c=DAMPING, rounds=1, parallelism=1).wall_ms
+        r1 = _rounds_for(t1, M, CPU_STEP_TARGET_S / 2)
+        w1 = rg.run_cpaa(c=DAMPING, rounds=r1, parallelism=1).wall_ms if r1 > 1 else t1
+        nnz = rg.nnz
+        return {"value": round(nnz * rk / (wk * 1e-3) / 1e9, 6), "unit": "GTEPS", "cores": threads,
+                "kind": "reference", "cpu_model": cpu_model(),
+                "k1": {"value": round(nnz * r1 / (w1 * 1e-3) / 1e9, 6), "cores": 1,
+                       "sample": f"run_cpaa(rounds={r1}, parallelism=1), wall {w1:.0f} ms"},
+                "sample": f"run_cpaa(rounds={rk} of M={M}, parallelism={threads}) on the same {cfgname} CSR "
+                          f"({nnz} entries), wall {wk:.0f} ms; build excluded"}
+    except Exception as ex:  # noqa: BLE001
+        return {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
+                "sample": f"failed: {type(ex).__name__}: {ex}"}
+
+
 # ----------------------------------------------------------------------------------------
 # GPU arm
 # ----------------------------------------------------------------------------------------
+class _Handle:
+    def __init__(self, h):
+        self.handle = h
+
+
 class Solver:
     """One step = one CPAA solve to eps 1e-10 on the resident graph (scalar K2 path, or the
     batched K5 path when the config has R right-hand sides)."""
@@ -315,28 +456,37 @@ class Solver:
         self.dg, self.info, self.cfg = dg, info, cfg
         self.R = int(cfg.get("R", 1))
         self.M = cheb.plan_iterations(DAMPING, EPS).M
-        self.seeds = c5_seeds(dg, self.R) if self.R > 1 else None
-        if self.R > 1 and world > 1:
-            # batched config on N GPUs: replicas (§8(e)) — the graph on every GPU, the R
-            # right-hand sides split across the ranks, no per-term communication
-            self.seeds = np.ascontiguousarray(self.seeds[rank::world])
-            self.R = int(self.seeds.size)
+        self.seeds_all = None
+        self.seeds = None
+        if self.R > 1:
+            self.seeds_all = c5_seeds_from_degrees(np.diff(dg.download().offsets), self.R)
+            self.seeds = self.seeds_all
+            if world > 1:
+                # batched config on N GPUs: replicas (§8(e)) — the graph on every GPU, the R
+                # right-hand sides split across the ranks, no per-term communication
+                self.seeds = np.ascontiguousarray(self.seeds_all[rank::world])
+                self.R = int(self.seeds.size)
         o = L.cheb_cpaa_opts()
         self.lib.cheb_cpaa_opts_default(C.byref(o))
         o.eps, o.c, o.precision, o.R = EPS, DAMPING, precision, self.R
         self.opts = o
+        o0 = L.cheb_cpaa_opts()
+        self.lib.cheb_cpaa_opts_default(C.byref(o0))
+        o0.eps, o0.rounds, o0.c, o0.precision, o0.R = -1.0, 0, DAMPING, precision, self.R
+        self.opts0 = o0  # the same solve with zero terms (init + normalise only)
         self.d_ranks = C.c_void_p()
 
     def _seed_ptr(self):
         return None if self.seeds is None else self.seeds.ctypes.data_as(self.L.I64P)
 
-    def solve(self, handle=None):
+    def solve(self, handle=None, zero_terms=False):
         h = handle or self.dg.handle
+        o = self.opts0 if zero_terms else self.opts
         if self.R > 1:
-            self.cheb.api._check(self.lib.cheb_cpaa_batch(h, C.byref(self.opts), self._seed_ptr(),
+            self.cheb.api._check(self.lib.cheb_cpaa_batch(h, C.byref(o), self._seed_ptr(),
                                                           None, None, None, None))
         else:
-            self.cheb.api._check(self.lib.cheb_cpaa_device(h, C.byref(self.opts), C.byref(self.d_ranks), 0))
+            self.cheb.api._check(self.lib.cheb_cpaa_device(h, C.byref(o), C.byref(self.d_ranks), 0))
 
     def last_ms(self):
         lm, tm, terms, launches = C.c_double(), C.c_double(), C.c_int(), C.c_int()
@@ -344,21 +494,33 @@ class Solver:
                                                        C.byref(terms), C.byref(launches)))
         return lm.value, launches.value
 
-    def term_ms(self):
-        cap = 64
-        ms = (C.c_double * cap)()
-        terms = C.c_int()
-        if self.R > 1:
-            self.cheb.api._check(self.lib.cheb_cpaa_batch_profile(self.dg.handle, C.byref(self.opts),
-                                                                  self._seed_ptr(), ms, cap, C.byref(terms)))
-        else:
-            self.cheb.api._check(self.lib.cheb_cpaa_profile(self.dg.handle, C.byref(self.opts), ms, cap,
-                                                            C.byref(terms)))
-        return [ms[i] for i in range(terms.value)]
+    def term_us_replayed(self, flush, reps):
+        """Average duration of one term (term kernel + hub finalize + its share of the trace
+        reduction) in the SAME graph-replayed, PDL-chained solve the timed step runs:
+        (t(M terms) - t(0 terms)) / M, each the mean of `reps` graph replays with L2 flushed
+        (CUDA events on the library's stream)."""
+        import torch
 
-    def e2e(self, device, steps, flush, dist, comm=None, warmup=3):
+        def mean_ms(zero):
+            for _ in range(3):  # first: plain launches; second: capture; then replays
+                self.solve(zero_terms=zero)
+                self.last_ms()
+            ts = []
+            for _ in range(reps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                self.solve(zero_terms=zero)
+                ts.append(self.last_ms()[0])
+            return statistics.mean(ts)
+        t0 = mean_ms(True)
+        tM = mean_ms(False)
+        return (tM - t0) / self.M * 1e3, tM, t0
+
+    def e2e(self, device, steps, flush, dist, exchange, warmup=3):
         """Through the reference-facing C-ABI with host buffers: pinned int64 CSR upload,
-        solve, ranks (and trace) read back to host memory, every step."""
+        solve, ranks (and trace) read back to host memory, every step.  N > 1: every step's
+        fresh handle joins the row-partitioned solve with the same exchange as the timed
+        loop (fused push: IPC-mapped peer buffers; or an NCCL communicator)."""
         import torch
         L, lib = self.L, self.lib
         host = self.dg.download()
@@ -371,6 +533,10 @@ class Solver:
         tr = (L.cheb_trace_row * 64)()
         rounds, tot = C.c_int(), C.c_double()
         totals = np.zeros(R)
+        comm = None
+        if dist.world > 1 and self.R_cfg == 1 and exchange == "nccl":
+            from paper_2112_01743_b200.distributed import Communicator
+            comm = Communicator(dist.rank, dist.world, device)
 
         def step():
             h = C.c_void_p()
@@ -378,8 +544,13 @@ class Solver:
                 off.ctypes.data_as(L.I64P), off.size, nb.ctypes.data_as(L.I64P), nb.size,
                 deg.ctypes.data_as(L.I64P), deg.size, inv.ctypes.data_as(L.F64P), inv.size,
                 n, int(host.m), 0, device, int(self.info["row_ptr_64"]), C.byref(h)))
-            if comm is not None:
-                self.cheb.api._check(lib.cheb_graph_attach_comm(h, comm.handle))
+            px = None
+            if dist.world > 1 and self.R_cfg == 1:
+                if comm is not None:
+                    self.cheb.api._check(lib.cheb_graph_attach_comm(h, comm.handle))
+                else:
+                    from paper_2112_01743_b200.distributed import PeerExchange
+                    px = PeerExchange(_Handle(h), dist.rank, dist.world)
             if R > 1:
                 self.cheb.api._check(lib.cheb_cpaa_batch(h, C.byref(self.opts), self._seed_ptr(),
                                                          ranks.ctypes.data_as(L.F64P),
@@ -387,6 +558,8 @@ class Solver:
             else:
                 self.cheb.api._check(lib.cheb_cpaa(h, C.byref(self.opts), None, 0, ranks.ctypes.data_as(L.F64P),
                                                    tr, C.byref(rounds), C.byref(tot)))
+            if px is not None:
+                px.detach()
             lib.cheb_graph_free(h)
 
         for _ in range(max(3, warmup)):  # pool, pinned staging and page-cache warm-up
@@ -399,17 +572,21 @@ class Solver:
             t = time.perf_counter()
             step()
             times.append(time.perf_counter() - t)
+        if comm is not None:
+            comm.close()
         if os.environ.get("CHEB_BENCH_VERBOSE"):
             log("e2e steps (ms): " + " ".join(f"{1e3 * t:.2f}" for t in times))
         e2e_s = dist.max(statistics.mean(times))
-        units = self.info["nnz"] * self.R * self.M
+        units = self.info["nnz"] * self.R_cfg * self.M
+        exch = ("" if dist.world == 1 or self.R_cfg > 1 else
+                (" + NCCL communicator" if comm is not None else " + push exchange (IPC peer mapping)"))
         return {"value": round(units / e2e_s / 1e9, 4), "unit": "GTEPS",
                 # inv_degree is checked bitwise on the host threads and, being canonical,
                 # never copied (a non-canonical one would add n * 8 bytes)
                 "h2d_bytes_per_step": int(off.nbytes + nb.nbytes),
                 "d2h_bytes_per_step": int(ranks.nbytes + 2 * self.M * 8),
                 "ms_per_step": round(e2e_s * 1e3, 3),
-                "path": "cheb_graph_upload_csr(pinned int64 CSR; inv_degree verified on the host) + " +
+                "path": "cheb_graph_upload_csr(pinned int64 CSR; inv_degree verified on the host)" + exch + " + " +
                         ("cheb_cpaa_batch" if R > 1 else "cheb_cpaa") + "(host ranks) + cheb_graph_free"}
 
 
@@ -419,7 +596,7 @@ def lsu_roofline(config, precision, world, mean_launch_us, sm_mhz):
     if world != 1 or not sm_mhz:
         return None
     try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             w = json.load(f).get(f"{config}/f{precision}", {}).get("lsu_wavefronts")
     except (OSError, ValueError):
         return None
@@ -429,16 +606,17 @@ def lsu_roofline(config, precision, world, mean_launch_us, sm_mhz):
     floor_us = w / peak * 1e6
     return {"bound": "l1tex_lsu_wavefronts", "wavefronts_per_launch": w, "peak_wavefronts_per_s": round(peak),
             "floor_us": round(floor_us, 1), "achieved_us": round(mean_launch_us, 1),
-            "frac": round(floor_us / mean_launch_us, 4)}
+            "frac": round(floor_us / mean_launch_us, 4),
+            "source": "wavefronts from the committed ncu capture (profiles/traffic.json)"}
 
 
 def measured_traffic(config, precision, world):
-    """DRAM bytes per launch of the dominant kernel from the committed ncu capture
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     (profiles/traffic.json), or None when this workload has not been captured."""
     if world != 1:
         return None
     try:
-        with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             t = json.load(f)
         return t.get(f"{config}/f{precision}", {}).get("bytes")
     except (OSError, ValueError):
@@ -473,37 +651,50 @@ def power_comparator(dg, flush, precision):
             "note": "same resident graph, public API incl. ranks read-back, wall clock, best of 3"}
 
 
-def cpu_baseline_line(solver, cfg, args):
-    """The reference compiled unmodified (oracle/_ref) on the same CSR, all host threads; for
-    the batched config the reference has no personalisation, so one column of the restated
-    oracle loop (T_0 = e_seed) is timed single-threaded and labelled 'port'."""
-    try:
-        host = solver.dg.download()
-        if solver.R > 1:
-            from oracle import Oracle, CSR
-            o = Oracle()
-            g = CSR(host.n, host.m, host.offsets, host.neighbors, host.degrees, host.inv_degree)
-            p = np.zeros(host.n)
-            p[solver.seeds[0]] = 1.0
-            t = time.perf_counter()
-            o.run_cpaa(g, solver.M, p=p)
-            dt = time.perf_counter() - t
-            return {"value": round(host.neighbors.size * solver.M / dt / 1e9, 6), "unit": "GTEPS",
-                    "cores": 1, "kind": "port",
-                    "sample": f"restated oracle loop (oracle/cpaa_oracle.c), 1 of {solver.R} one-hot columns "
-                              f"(M={solver.M}), wall {dt * 1e3:.0f} ms; the reference has no personalisation"}
-        e = np.stack([np.repeat(np.arange(host.n), np.diff(host.offsets)), host.neighbors], 1)
-        e = e[e[:, 0] <= e[:, 1]]
-        threads = os.cpu_count() or 1
-        r = cpu_reference_run(dict(cfg, drop=False), 1, 0, threads, host_edges=e)
-        cms = statistics.mean(r["wall_ms"])
-        return {"value": round(r["nnz"] * r["M"] / (cms * 1e-3) / 1e9, 6), "unit": "GTEPS",
-                "cores": threads, "kind": "reference",
-                "sample": f"one full run_cpaa (M={r['M']}) on the same {args.config} CSR "
-                          f"({r['nnz']} entries), K={threads} threads, wall {cms:.0f} ms"}
-    except Exception as ex:  # noqa: BLE001
-        return {"value": None, "unit": "GTEPS", "cores": 0, "kind": "reference",
-                "sample": f"failed: {type(ex).__name__}: {ex}"}
+def timed_steps(sv, flush, steps, dist, clk=None):
+    """Time exactly `steps` solves (CUDA events on the library's stream, L2 flushed before
+    each, outside the events); returns (ms_per_step max over ranks, our kernel launches)."""
+    import torch
+    dist.barrier()
+    torch.cuda.synchronize()
+    times, launches = [], 0
+    if clk:
+        clk.mark_start()
+    for _ in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        sv.solve()
+        ms, nl = sv.last_ms()
+        times.append(ms)
+        launches += nl
+    torch.cuda.synchronize()
+    if clk:
+        clk.mark_end()
+    dist.barrier()
+    return dist.max(sum(times)) / steps, launches
+
+
+def secondary_line(name, device, precision, steps, warmup, dist):
+    """A compact measurement of a second workload (C2 next to the C4 headline)."""
+    import torch
+    cfg = CONFIGS[name]
+    dg, info = build_device(cfg, device)
+    sv = Solver(dg, info, cfg, precision)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+    for _ in range(warmup):
+        sv.solve()
+        sv.last_ms()
+    ms, _ = timed_steps(sv, flush, steps, dist)
+    term_us, _, _ = sv.term_us_replayed(flush, max(3, steps // 2))
+    n, nnz = info["n"], info["nnz"]
+    B = algorithmic_bytes(n, nnz, 8 if info["row_ptr_64"] else 4, 8 if precision == 64 else 4, sv.R)
+    peak, _ = peaks()
+    ach = B / (term_us * 1e-6) / 1e9
+    dg.free()
+    return {"config": config_dict(name, n, nnz, sv.M, sv.R), "value": round(nnz * sv.R * sv.M / (ms * 1e-3) / 1e9, 3),
+            "unit": "GTEPS", "ms_per_step": round(ms, 4), "steps": steps,
+            "roofline": {"achieved": round(ach, 1), "peak": peak, "frac": round(ach / peak, 4),
+                         "mean_launch_us": round(term_us, 3), "bytes_per_launch": B}}
 
 
 def main():
@@ -512,13 +703,16 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS),
+                    help="workload (default c4: the largest single-GPU config, the scaling graph)")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--secondary", default="c2",
+                    help="comma list of extra workloads measured compactly at N=1 ('' for none)")
     ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
                     help="N>1: x_{k+1} exchange of the row partition (fused push over peer memory, "
-                         "or NCCL all-gather); the e2e leg always attaches an NCCL communicator")
+                         "or NCCL all-gather); the e2e leg uses the same exchange")
     ap.add_argument("--profile-only", action="store_true",
                     help="build + a few solves, no timing output (for ncu captures)")
     args = ap.parse_args()
@@ -540,13 +734,13 @@ def main():
     comm = px = None
     exchange_note = None
     R_cfg = int(cfg.get("R", 1))
+    exchange = args.exchange
     if dist.world > 1 and R_cfg == 1:
         # strong scaling: every rank holds the same graph; the solver view is partitioned by
         # rows over the ranks and x_{k+1} reaches every rank each term — pushed by the term
         # kernels into the peers' buffers (default) or all-gathered by NCCL
         from paper_2112_01743_b200.distributed import Communicator, PeerExchange
-        comm = Communicator(dist.rank, dist.world, device)  # e2e leg (fresh handles per step)
-        if args.exchange == "push":
+        if exchange == "push":
             err = None
             try:
                 px = PeerExchange(dg, dist.rank, dist.world)
@@ -559,11 +753,13 @@ def main():
                 if px is not None:
                     px.detach()
                 px = None
-                comm.attach(dg)
-        else:
+                exchange = "nccl"
+        if exchange == "nccl":
+            comm = Communicator(dist.rank, dist.world, device)
             comm.attach(dg)
     n, nnz = info["n"], info["nnz"]
     sv = Solver(dg, info, cfg, args.precision, dist.rank, dist.world)
+    sv.R_cfg = R_cfg
     M, R = sv.M, sv.R
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=f"cuda:{device}")
@@ -576,45 +772,35 @@ def main():
         return 0
 
     with Clocks(device) as clk:
-        dist.barrier()
-        torch.cuda.synchronize()
-        times, launches = [], 0
-        clk.mark_start()
-        for _ in range(args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            sv.solve()
-            ms, nl = sv.last_ms()
-            times.append(ms)
-            launches += nl
-        torch.cuda.synchronize()
-        clk.mark_end()
-        dist.barrier()
-    total_ms = dist.max(sum(times))
-    ms_step = total_ms / args.steps
+        ms_step, launches = timed_steps(sv, flush, args.steps, dist, clk)
     # whole-job rate: one graph (and the config's R right-hand sides) per job — strong
     # scaling over row partitions (R = 1) or over the split right-hand sides (R > 1)
     value = nnz * R_cfg * M / (ms_step * 1e-3) / 1e9
 
-    # dominant kernel: the fused term kernel (+ its hub-row finalize), CUDA events per term
-    flush.zero_()
-    torch.cuda.synchronize()
-    tms = sv.term_ms()
-    steady = tms[1:] if len(tms) > 1 else tms
-    mean_term = statistics.mean(steady)
+    # dominant kernel: the fused term kernel (+ its hub-row finalize), from the same
+    # graph-replayed solve the step runs (difference of M-term and 0-term replays)
+    term_us, tM, t0ms = sv.term_us_replayed(flush, max(3, args.steps // 2))
+    term_us = dist.max(term_us)
     vbytes = 8 if args.precision == 64 else 4
     rp_bytes = 8 if info["row_ptr_64"] else 4
     B = algorithmic_bytes(n, nnz, rp_bytes, vbytes, R)
     peak, peak_kind = peaks()
-    achieved = B / (mean_term * 1e-3) / 1e9
+    achieved = B / (term_us * 1e-6) / 1e9
 
     comparator = None
     if dist.world == 1 and R == 1 and not args.no_e2e:
         comparator = power_comparator(dg, flush, args.precision)
-    e2e = None if args.no_e2e else sv.e2e(device, args.steps, flush, dist, comm, args.warmup)
+    e2e = None if args.no_e2e else sv.e2e(device, args.steps, flush, dist, exchange, args.warmup)
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_line(sv, cfg, args)
+        cpu = cpu_baseline_line(sv, args.config, args)
+    secondary = []
+    if dist.world == 1 and args.secondary:
+        for name in [s for s in args.secondary.split(",") if s and s != args.config]:
+            try:
+                secondary.append(secondary_line(name, device, args.precision, args.steps, args.warmup, dist))
+            except Exception as ex:  # noqa: BLE001
+                secondary.append({"config": name, "failed": f"{type(ex).__name__}: {ex}"})
 
     if dist.rank == 0:
         kernel = "k_spmm_term + k_spmm_hub_finalize" if R > 1 else "k_term_warp<EPI_CPAA> + k_hub_finalize"
@@ -632,29 +818,31 @@ def main():
             "vs_baseline": None,
             "dtype": "f64" if args.precision == 64 else "f32",
             "data": "synthetic",
-            "config": {"workload": args.config, "desc": cfg["desc"], "n": n, "nnz": nnz, "R": R,
-                       "edges_drawn": info["edges_drawn"], "max_degree": info["max_degree"],
-                       "terms": M, "eps": EPS, "c": DAMPING,
-                       "time_to_1e-10_ms": round(ms_step, 4),
-                       "gteps_definition": "nnz*R*terms/step_time (every CSR entry one traversal)",
-                       "parallelism": (f"rowpart{dist.world}+" + ("push" if px is not None else "nccl_allgather"))
-                       if dist.world > 1 else "single",
-                       **({"exchange_note": exchange_note} if exchange_note else {}),
-                       "l2": "flushed (512 MiB write) before every timed step",
-                       "graph_build_s": round(build_s, 3)},
+            "config": config_dict(args.config, n, nnz, M, R_cfg),
+            "parallelism": (f"rowpart{dist.world}+" + ("push" if px is not None else "nccl_allgather"))
+                           if dist.world > 1 and R_cfg == 1 else (f"replicas{dist.world}" if dist.world > 1 else "single"),
+            "details": {"edges_drawn": info["edges_drawn"], "max_degree": info["max_degree"],
+                        "time_to_1e-10_ms": round(ms_step, 4), "graph_build_s": round(build_s, 3),
+                        "gteps_definition": "nnz*R*terms/step_time (every CSR entry one traversal)",
+                        "R_per_rank": R,
+                        **({"exchange_note": exchange_note} if exchange_note else {})},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": measured_traffic(args.config, args.precision, dist.world),
-                         "traffic_unit": "DRAM bytes per launch (ncu, profiles/traffic.json)",
+                         "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/traffic.json)",
                          "kernel": kernel, "bytes_per_launch": B,
                          "bytes_formula": "4 nnz + I_r (n+1) + 6 V R n (SURVEY.md 8d)",
-                         "mean_launch_us": round(mean_term * 1e3, 3), "peak_kind": peak_kind},
+                         "mean_launch_us": round(term_us, 3),
+                         "launch_timing": f"(t_replay(M={M}) {tM:.4f} ms - t_replay(M=0) {t0ms:.4f} ms) / M, "
+                                          "graph-replayed PDL chain, L2 flushed, CUDA events",
+                         "peak_kind": peak_kind},
             "cpu_baseline": cpu,
             "e2e": e2e,
             **({"power_comparator": comparator} if comparator else {}),
+            **({"secondary": secondary} if secondary else {}),
             "gpu_launches": launches,
             "clocks": clk_summary,
-            "lsu_roofline": lsu_roofline(args.config, args.precision, dist.world, mean_term * 1e3,
+            "lsu_roofline": lsu_roofline(args.config, args.precision, dist.world, term_us,
                                          clk_summary.get("sm_mhz")),
         }
         print(json.dumps(line))

@@ -91,6 +91,10 @@ class Oracle:
         L.or_run_power.argtypes = [C.c_int64, I64P, I64P, F64P, C.c_double, C.c_int, C.c_double,
                                    C.c_int, F64P, F64P, C.POINTER(C.c_int), F64P]
         L.or_free.argtypes = [C.c_void_p]
+        L.or_rmat_edges.argtypes = [C.c_int, C.c_int64, C.c_double, C.c_double, C.c_double, C.c_uint64,
+                                    C.POINTER(I64P), I64P]
+        L.or_chung_lu_edges.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int64,
+                                        C.c_uint64, C.POINTER(I64P), I64P]
 
     def _check(self, rc: int):
         if rc:
@@ -122,6 +126,28 @@ class Oracle:
         out = np.ctypeslib.as_array(ptr, shape=(max(cnt.value, 1) * 2,))[: cnt.value * 2].copy()
         self.lib.or_free(ptr)
         return out.reshape(-1, 2)
+
+    def _take_edges(self, ptr, cnt) -> np.ndarray:
+        try:
+            if cnt.value == 0:
+                return np.zeros((0, 2), dtype=np.int64)
+            return np.ctypeslib.as_array(ptr, shape=(cnt.value * 2,)).copy().reshape(-1, 2)
+        finally:
+            self.lib.or_free(ptr)
+
+    def rmat_edges(self, scale: int, edge_factor: int = 16, a: float = 0.57, b: float = 0.19,
+                   c: float = 0.19, seed: int = 1) -> np.ndarray:
+        """Configs 3/4 edge list (oracle/synth_gen.c), int64 (E, 2)."""
+        ptr, cnt = I64P(), C.c_int64()
+        self._check(self.lib.or_rmat_edges(scale, edge_factor, a, b, c, seed, C.byref(ptr), C.byref(cnt)))
+        return self._take_edges(ptr, cnt)
+
+    def chung_lu_edges(self, n: int, gamma: float = 2.1, wmin: float = 2.0, wmax: float = 50000.0,
+                       draws: int = 10_485_760, seed: int = 1) -> np.ndarray:
+        """Configs 2/5 edge list (oracle/synth_gen.c), int64 (E, 2)."""
+        ptr, cnt = I64P(), C.c_int64()
+        self._check(self.lib.or_chung_lu_edges(n, gamma, wmin, wmax, draws, seed, C.byref(ptr), C.byref(cnt)))
+        return self._take_edges(ptr, cnt)
 
     def build_graph(self, edges, dedup=True, drop_isolated=False, n_hint=0) -> CSR:
         e = edges_array(edges)

@@ -24,6 +24,7 @@ static int fail(int code, const char* fmt, ...) {
 }
 
 const char* or_last_error(void) { return g_err; }
+int or_set_error(int code, const char* msg) { return fail(code, "%s", msg); }
 void or_free(void* p) { free(p); }
 
 /* ---- src/graph.cpp:10-19 ------------------------------------------------ */

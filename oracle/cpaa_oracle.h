@@ -34,6 +34,13 @@ int or_coefficients(double c, int M, double* coeffs /* M+1 */, double* beta, dou
 /* std::mt19937_64 + src/generate.cpp:11-19,51-87 */
 int or_gnp_edges(int64_t n, double p, uint64_t seed, int64_t** edges, int64_t* count);
 
+/* Synthetic generators of BASELINE configs 2-5 (oracle/synth_gen.c): the product's
+ * counter-based R-MAT / Chung-Lu definition restated; int64 (u, v) pairs, malloc'ed. */
+int or_rmat_edges(int scale, int64_t edge_factor, double a, double b, double c, uint64_t seed,
+                  int64_t** edges, int64_t* count);
+int or_chung_lu_edges(int64_t n, double gamma, double wmin, double wmax, int64_t draws, uint64_t seed,
+                      int64_t** edges, int64_t* count);
+
 /* src/graph.cpp:23-102.  Outputs are malloc'ed (free with or_free). */
 int or_build_graph(const int64_t* edges, int64_t E, int dedup, int drop_isolated,
                    int64_t n_hint, int64_t* n_out, int64_t* m_out, int64_t** offsets,

@@ -125,14 +125,13 @@ void chebgpu::release_stream(int device, cudaStream_t s) {
 void chebgpu::retain_pool_memory() {
     int dev = 0;
     cudaGetDevice(&dev);
-    static bool done[64] = {};
-    if (dev < 0 || dev >= 64 || done[dev]) return;
+    static std::atomic<uint64_t> done{0};
+    if (dev < 0 || dev >= 64 || !first_on_device(done, dev)) return;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         uint64_t keep = UINT64_MAX;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
-    done[dev] = true;
 }
 
 bool chebgpu::l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* w) {
@@ -143,7 +142,9 @@ bool chebgpu::l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* 
     cudaGetDevice(&dev);
     static size_t persist_max[64] = {}, window_max[64] = {}, l2_size[64] = {}, current[64] = {};
     static bool init[64] = {};
+    static std::mutex mu;  // handles on different devices may launch from different threads
     if (dev < 0 || dev >= 64) return false;
+    std::lock_guard<std::mutex> lk(mu);
     if (!init[dev]) {
         cudaDeviceProp prop;
         if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess) {

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -136,6 +137,16 @@ struct DeviceGuard {
         if (prev >= 0) cudaSetDevice(prev);
     }
 };
+
+// Per-device one-time setup flags (function attributes, pool attributes): a context
+// property must be set on every device a process uses, and handles on different devices
+// may be driven from different host threads.  first_on_device(mask, dev) is true exactly
+// once per (mask, dev); devices >= 64 always return true (the setup is idempotent).
+inline bool first_on_device(std::atomic<uint64_t>& mask, int dev) {
+    if (dev < 0 || dev >= 64) return true;
+    const uint64_t bit = uint64_t(1) << dev;
+    return (mask.fetch_or(bit, std::memory_order_acq_rel) & bit) == 0;
+}
 
 // --------------------------------------------------------------------------
 // Degree-binned solver view (the hot-path layout, built once per graph).

@@ -934,12 +934,16 @@ template <int EPI, class RP, class V>
 int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
     cudaStream_t st = g->stream;
     if (L.fast) {
-        static bool attr_set = false;  // per template instance
+        // the > 48 KB dynamic shared-memory opt-in is a per-device (per-context) attribute
+        static std::atomic<uint64_t> attr_set{0};  // per template instance, bit per device
         constexpr size_t smem = warp_smem_bytes<V>();
-        if (!attr_set) {
-            CHEB_CUDA_CHECK(cudaFuncSetAttribute(k_term_warp<EPI, RP, V>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_set = true;
+        if (first_on_device(attr_set, g->device)) {
+            const cudaError_t e = cudaFuncSetAttribute(k_term_warp<EPI, RP, V>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) {
+                attr_set.fetch_and(~(uint64_t(1) << (g->device & 63)));  // retry next launch
+                CHEB_CUDA_CHECK(e);
+            }
         }
         int H = (int)std::min<int64_t>(g->n, hot_capacity<V>());
         if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);

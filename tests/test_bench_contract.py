@@ -45,3 +45,20 @@ def test_committed_gpu_line_has_contract_keys():
     for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
         assert k in d["e2e"]
     assert d["gpu_launches"] > 0 and d["clocks"]["sm_mhz"] and d["config"]["workload"] == "c2"
+
+
+def test_reference_arm_never_loads_the_product_library():
+    """The reference arm (and the CPU edge generators it uses) runs the unmodified reference
+    only: after a full --impl reference run the process has mapped oracle/_ref and the
+    oracle restatement, never paper_2112_01743_b200/lib/libchebpr_b200.so."""
+    from oracle import REF_SO
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    code = ("import runpy, sys\n"
+            "sys.argv = ['bench.py', '--impl', 'reference', '--config', 'c1', '--steps', '1', '--warmup', '0']\n"
+            "try:\n    runpy.run_path('bench.py', run_name='__main__')\nexcept SystemExit:\n    pass\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "print('PRODUCT' if 'libchebpr_b200' in maps else 'CLEAN', 'REF' if 'libchebpr_ref' in maps else 'NOREF')\n")
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert p.stdout.strip().splitlines()[-1] == "CLEAN REF"

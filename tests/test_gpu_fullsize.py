@@ -1,117 +1,155 @@
-"""Full-size parity (BASELINE.json configs 2 and 3) through size-independent properties:
-CSR invariants of the device builder on the full graph, FAST vs BITEXACT agreement
-(BITEXACT = the reference's arithmetic, bitwise-pinned on the fixtures), the mass ledger
-S_k = n (c0/2 + sum c_i), unit total mass, top-100 stability, fp32 relative L1, batched
-uniform column vs the scalar solve.  Inputs come from the same seeded generators as
-bench.py."""
+"""Full-size parity against the REFERENCE ITSELF on the BASELINE.json bench graphs
+(configs 2-5, the exact graphs bench.py times).
+
+The reference side never touches the product library: its edge lists come from the
+plain-C restatement of the config generators (oracle/synth_gen.c, pinned equal to the
+product's generators by tests/test_oracle.py), its CSR from the reference's own
+build_graph and its ranks from the reference's own run_cpaa (oracle/_ref = the unmodified
+sources, all host threads).  The product side generates on the device and builds with K1.
+
+Checked per config (SURVEY.md §8(c)/(d) bars, north_star):
+  * CSR: offsets, neighbours and degrees bit-exact against the reference build_graph, and
+    the same m / duplicates_removed / isolated_dropped;
+  * FAST fp64 ranks (the product path): max-abs <= 1e-12 and the same top-100 vertices in
+    the same order (ties by vertex id);
+  * BITEXACT fp64 ranks: bitwise equal, and the S_k / mass_T trace bitwise equal;
+  * fp32: relative L1 <= 1e-6;
+  * config 5 (batched, 64 one-hot columns): 4 sampled columns against the restated loop
+    (oracle/cpaa_oracle.c with T0 = e_seed; the reference has no personalisation), the same
+    bars (fp64 1e-12 + top-100, fp32 1e-6), every column a distribution.
+"""
+import gc
+
 import numpy as np
 import pytest
 
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 C = 0.85
+EPS = 1e-10
 
 
-def _build(cfg_name):
+def top100(r):
+    ids = np.arange(r.size)
+    return np.lexsort((ids, -r))[:100]
+
+
+def _reference_side(reference, name):
+    """Edges by oracle/synth_gen.c, CSR by the reference's build_graph."""
     import bench
-    dg, info = bench.build_device(bench.CONFIGS[cfg_name], 0)
-    return dg, info
+    cfg = bench.CONFIGS[name]
+    e = bench.make_edges_host(cfg)
+    rg = reference.build_graph(e, dedup=True, drop_isolated=cfg.get("drop", False))
+    del e
+    gc.collect()
+    return rg
 
 
-def _csr_properties(g):
-    off, nb, deg = g.offsets, g.neighbors, g.degrees
-    n = g.n
-    assert off[0] == 0 and off[-1] == nb.size and np.all(np.diff(off) == deg) and deg.min() >= 1
-    rows = np.repeat(np.arange(n, dtype=np.int64), deg)
-    assert nb.min() >= 0 and nb.max() < n
-    same = rows[1:] == rows[:-1]
-    assert np.all(nb[1:][same] > nb[:-1][same])                      # sorted, no duplicates
-    a = np.sort(rows * n + nb)
-    b = np.sort(nb * n + rows)
-    assert np.array_equal(a, b)                                       # symmetric
-    assert nb.size == 2 * g.m - int(np.count_nonzero(nb == rows))     # entries = 2m - loops
+def _device_side(name):
+    import bench
+    return bench.build_device(bench.CONFIGS[name], 0)
 
 
-def test_config2_full_size(cheb):
-    dg, info = _build("c2")
-    g = dg.download()
-    _csr_properties(g)
-    assert info["n"] == 1 << 20
-    fast = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
-    exact = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, mode=cheb.MODE_BITEXACT))
-    assert fast.rounds == 39 and exact.rounds == 39
-    assert np.max(np.abs(fast.ranks - exact.ranks)) <= 1e-12
-    top = lambda r: np.argsort(-r, kind="stable")[:100]  # noqa: E731
-    assert np.array_equal(top(fast.ranks), top(exact.ranks))
-    t = cheb.coefficients(C, 39)
-    n = float(g.n)
-    partial = t.c0 / 2.0
-    for row in fast.trace:
-        partial += t.coeffs[row.k]
-        assert abs(row.S_k - n * partial) <= n * 1e-12                 # mass ledger
-        assert abs(row.mass_T - n) <= n * 1e-12                        # T_k conserves mass
-    assert abs(cheb.kahan_sum(fast.ranks) - 1.0) <= 1e-12
-    f32 = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, precision=32))
-    assert np.sum(np.abs(f32.ranks - exact.ranks)) / np.sum(exact.ranks) <= 1e-6
-    # the 210-round Power reference and CPAA agree to the a-priori bound
-    p = cheb.run_power(dg, cheb.PowerConfig(rounds=210))
-    assert np.sum(np.abs(p.ranks - fast.ranks)) <= 1e-9
+def _check_csr(rg, dg, info):
+    ref = rg.csr()
+    assert info["n"] == rg.n and info["m"] == rg.m and info["nnz"] == rg.nnz
+    assert info["duplicates_removed"] == rg.duplicates_removed
+    assert info["isolated_dropped"] == rg.isolated_dropped
+    mine = dg.download()
+    assert np.array_equal(mine.offsets, ref.offsets)
+    assert np.array_equal(mine.degrees, ref.degrees)
+    # neighbours in 256 M-entry slices (C4 holds 1.05 G of them)
+    step = 1 << 28
+    for a in range(0, ref.neighbors.size, step):
+        assert np.array_equal(mine.neighbors[a:a + step], ref.neighbors[a:a + step]), a
+    del mine
+    gc.collect()
+
+
+def _check_solves(cheb, rg, dg, threads, fp32=True, bitexact=True):
+    want = rg.run_cpaa(c=C, eps=EPS, parallelism=threads)
+    assert want.rounds == 39
+    fast = cheb.run_cpaa(dg, cheb.SolverConfig(c=C, eps=EPS))
+    assert fast.rounds == 39
+    err = float(np.max(np.abs(fast.ranks - want.ranks)))
+    assert err <= 1e-12, err
+    assert np.array_equal(top100(fast.ranks), top100(want.ranks))
+    if bitexact:
+        exact = cheb.run_cpaa(dg, cheb.SolverConfig(c=C, eps=EPS, mode=cheb.MODE_BITEXACT))
+        assert np.array_equal(exact.ranks, want.ranks)
+        s_k = np.array([r.S_k for r in exact.trace])
+        m_t = np.array([r.mass_T for r in exact.trace])
+        assert np.array_equal(s_k, want.trace[:, 2]) and np.array_equal(m_t, want.trace[:, 6])
+    if fp32:
+        f32 = cheb.run_cpaa(dg, cheb.SolverConfig(c=C, eps=EPS, precision=32))
+        rel = float(np.sum(np.abs(f32.ranks - want.ranks)) / np.sum(np.abs(want.ranks)))
+        assert rel <= 1e-6, rel
+    return want
+
+
+def _threads():
+    import bench
+    return bench.host_threads()
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_config_full_size_vs_reference(cheb, reference, name):
+    rg = _reference_side(reference, name)
+    dg, info = _device_side(name)
+    _check_csr(rg, dg, info)
+    _check_solves(cheb, rg, dg, _threads())
     dg.free()
 
 
-def test_config3_full_size(cheb):
-    dg, info = _build("c3")
-    assert info["isolated_dropped"] > 0 and info["nnz"] > 100_000_000
-    fast = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
-    again = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
-    assert np.array_equal(fast.ranks, again.ranks)                     # deterministic
-    t = cheb.coefficients(C, 39)
-    n = float(info["n"])
-    partial = t.c0 / 2.0
-    for row in fast.trace:
-        partial += t.coeffs[row.k]
-        assert abs(row.S_k - n * partial) <= n * 1e-12
-    assert abs(cheb.kahan_sum(fast.ranks) - 1.0) <= 1e-12
-    exact = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, mode=cheb.MODE_BITEXACT))
-    assert np.max(np.abs(fast.ranks - exact.ranks)) <= 1e-12
-    dg.free()
-
-
-def test_config4_full_size(cheb):
-    """1.05 B CSR entries, int64 row pointers, x larger than L2 (the L2 window path)."""
-    dg, info = _build("c4")
+def test_config4_full_size_vs_reference(cheb, reference):
+    """1.05 G CSR entries, int64 row pointers, x larger than L2: CSR bit-exact, FAST within
+    1e-12 with the reference's top-100, BITEXACT bitwise (ranks and trace)."""
+    rg = _reference_side(reference, "c4")
+    dg, info = _device_side("c4")
     assert info["row_ptr_64"] == 1 and info["nnz"] > 1_000_000_000
-    fast = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
-    again = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10))
-    assert fast.rounds == 39 and np.array_equal(fast.ranks, again.ranks)   # deterministic
+    _check_csr(rg, dg, info)
+    rg._csr = None
+    gc.collect()
+    want = _check_solves(cheb, rg, dg, _threads(), fp32=False)
+    # the mass ledger of the reference's own trace holds for ours too
     t = cheb.coefficients(C, 39)
     n = float(info["n"])
     partial = t.c0 / 2.0
-    for row in fast.trace:
-        partial += t.coeffs[row.k]
-        assert abs(row.S_k - n * partial) <= n * 1e-12                      # mass ledger
-    assert abs(cheb.kahan_sum(fast.ranks) - 1.0) <= 1e-12
-    p = cheb.run_power(dg, cheb.PowerConfig(rounds=210))                  # independent solver
-    assert np.sum(np.abs(p.ranks - fast.ranks)) <= 1e-9
+    for k in range(39):
+        partial += t.coeffs[k + 1]
+        assert abs(want.trace[k, 2] - n * partial) <= n * 1e-12
     dg.free()
 
 
-def test_config5_full_size(cheb):
-    """Batched R = 64 (K5): every column is a distribution, and columns equal the scalar
-    personalised solves (one-hot T_0) of their seeds."""
+def test_config5_sampled_columns_vs_restated_loop(cheb, reference, oracle):
+    """Batched R = 64 (K5): 4 of the 64 one-hot columns against the restated CPAA loop
+    (T0 = e_seed) on the reference-built CSR; fp32 within 1e-6 relative L1."""
+    import threading
     import bench
-    dg, info = _build("c5")
-    seeds = bench.c5_seeds(dg, 64)
-    res = cheb.run_cpaa_batch(dg, cheb.SolverConfig(eps=1e-10), seeds=seeds)
+    rg = _reference_side(reference, "c5")
+    dg, info = _device_side("c5")
+    _check_csr(rg, dg, info)
+    csr = rg.csr()
+    seeds = bench.c5_seeds_from_degrees(csr.degrees, 64)
+    res = cheb.run_cpaa_batch(dg, cheb.SolverConfig(c=C, eps=EPS), seeds=seeds)
+    f32 = cheb.run_cpaa_batch(dg, cheb.SolverConfig(c=C, eps=EPS, precision=32), seeds=seeds)
     assert res.ranks.shape == (info["n"], 64)
-    sums = res.ranks.sum(axis=0)
-    assert np.max(np.abs(sums - 1.0)) <= 1e-10
-    for r in (0, 37):
-        p = np.zeros(info["n"])
+    assert np.max(np.abs(res.ranks.sum(axis=0) - 1.0)) <= 1e-10
+    cols = [0, 21, 42, 63]
+    want = {}
+
+    def one(r):
+        p = np.zeros(csr.n)
         p[seeds[r]] = 1.0
-        single = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, personalization=p))
-        assert np.max(np.abs(single.ranks - res.ranks[:, r])) <= 1e-12
-    # fp32 variant (fp32 storage, fp64 row sums): relative L1 <= 1e-6 per column
-    f32 = cheb.run_cpaa_batch(dg, cheb.SolverConfig(eps=1e-10, precision=32), seeds=seeds)
-    rel = np.sum(np.abs(f32.ranks - res.ranks), axis=0) / np.sum(np.abs(res.ranks), axis=0)
-    assert rel.max() <= 1e-6, rel.max()
+        want[r] = oracle.run_cpaa(csr, 39, c=C, p=p).ranks
+    th = [threading.Thread(target=one, args=(r,)) for r in cols]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for r in cols:
+        err = float(np.max(np.abs(res.ranks[:, r] - want[r])))
+        assert err <= 1e-12, (r, err)
+        assert np.array_equal(top100(res.ranks[:, r]), top100(want[r])), r
+        rel = float(np.sum(np.abs(f32.ranks[:, r] - want[r])) / np.sum(np.abs(want[r])))
+        assert rel <= 1e-6, (r, rel)
     dg.free()

@@ -129,3 +129,26 @@ def test_oracle_vs_live_reference(oracle, reference):
                 assert np.array_equal(a.ranks, b.ranks)
         for K in (1, 2, 5):
             assert np.array_equal(oracle.partition_vertices(g, K), rg.partition_vertices(K))
+
+
+@pytest.mark.parametrize("kind,args", [
+    ("rmat", (10, 16, 0.57, 0.19, 0.19, 3)),
+    ("rmat", (17, 16, 0.57, 0.19, 0.19, 4)),
+    ("rmat", (14, 8, 0.45, 0.15, 0.15, 11)),
+    ("chung_lu", (1000, 2.1, 2.0, 50000.0, 5000, 2)),
+    ("chung_lu", (1 << 17, 2.1, 2.0, 50000.0, 1_300_000, 5)),
+    ("chung_lu", (5000, 2.5, 1.0, 100.0, 3000, 9)),  # sparse: many rewired vertices
+])
+def test_config_generators_match_product(oracle, kind, args):
+    """oracle/synth_gen.c restates the product's counter-based config generators: the same
+    edge list, pair for pair and in the same order, as the product's host path (the device
+    path is pinned to the host path and to the reference CSR by the GPU tests).  This is
+    what lets the CPU legs build the bench graphs without the product library."""
+    from paper_2112_01743_b200 import generate as G
+    if kind == "rmat":
+        mine, prod = oracle.rmat_edges(*args), G.rmat_edges(*args)
+    else:
+        mine, prod = oracle.chung_lu_edges(*args), G.chung_lu_edges(*args)
+    assert mine.dtype == np.int64 and mine.shape == prod.shape
+    assert np.array_equal(mine, prod.astype(np.int64))
+    assert not np.any(mine[:, 0] == mine[:, 1])  # self-loops dropped
