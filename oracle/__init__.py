@@ -242,6 +242,9 @@ class Reference:
         L.ref_partition_vertices.argtypes = [C.c_void_p, C.c_int, I64P]
         L.ref_load.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p), I64P,
                                C.POINTER(C.c_double)]
+        L.ref_solve_to_csv.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_double, C.c_int,
+                                       C.c_char_p, C.c_char_p]
+        L.ref_write_edges.argtypes = [I64P, C.c_int64, C.c_char_p, C.c_char_p]
         L.ref_kahan_sum.restype = C.c_double
         L.ref_kahan_sum.argtypes = [F64P, C.c_int64]
 
@@ -317,6 +320,11 @@ class Reference:
         x = np.ascontiguousarray(x, dtype=np.float64)
         return self.lib.ref_kahan_sum(_p(x), x.size)
 
+    def write_edges(self, edges, path: str, comment: str):
+        """The reference's write_edge_list (generate.cpp:89-97)."""
+        e = edges_array(edges)
+        self._check(self.lib.ref_write_edges(_p(e, I64P), e.shape[0], os.fsencode(path), comment.encode()))
+
 
 @dataclass
 class RefGraph:
@@ -372,6 +380,12 @@ class RefGraph:
 
     def run_power(self, c=0.85, rounds=-1, tol=-1.0, max_rounds=60, parallelism=1, reference=None):
         return self._run(self.ref.lib.ref_run_power, c, rounds, tol, max_rounds, parallelism, reference)
+
+    def solve_to_csv(self, algo="cpaa", c=0.85, rounds=-1, eps=-1.0, max_rounds=60, ranks_path="",
+                     trace_path=""):
+        """run_cpaa / run_power, then the reference's own CSV writers (src/csv.cpp)."""
+        self.ref._check(self.ref.lib.ref_solve_to_csv(self.handle, 0 if algo == "cpaa" else 1, c, rounds, eps,
+                                                      max_rounds, os.fsencode(ranks_path), os.fsencode(trace_path)))
 
     def transition_apply(self, x):
         x = np.ascontiguousarray(x, dtype=np.float64)

@@ -15,6 +15,7 @@
 
 #include "chebpr/coefficients.hpp"
 #include "chebpr/cpaa.hpp"
+#include "chebpr/csv.hpp"
 #include "chebpr/errors.hpp"
 #include "chebpr/generate.hpp"
 #include "chebpr/graph.hpp"
@@ -306,5 +307,37 @@ int ref_partition_vertices(void* h, int K, int64_t* cuts /* K+1 */) {
 }
 
 double ref_kahan_sum(const double* x, int64_t n) { return kahan_sum(x, n); }
+
+// The reference's own CSV writers (src/csv.cpp) and edge-list writer (src/generate.cpp:89-97),
+// for byte-level parity of the CLI outputs.  algo 0 = run_cpaa, 1 = run_power.
+int ref_solve_to_csv(void* h, int algo, double c, int rounds, double eps, int max_rounds,
+                     const char* ranks_path, const char* trace_path) {
+    return guard([&] {
+        const auto& g = *static_cast<UndirectedGraph*>(h);
+        PageRankResult r;
+        if (algo == 0) {
+            SolverConfig cfg;
+            cfg.c = c;
+            cfg.rounds = rounds;
+            cfg.eps = eps;
+            cfg.max_rounds = max_rounds;
+            r = run_cpaa(g, cfg);
+            if (trace_path && *trace_path) write_cpaa_trace_csv(trace_path, r.trace, r.has_err);
+        } else {
+            PowerConfig cfg;
+            cfg.c = c;
+            cfg.rounds = rounds;
+            cfg.tol = eps;
+            cfg.max_rounds = max_rounds;
+            r = run_power(g, cfg);
+            if (trace_path && *trace_path) write_power_trace_csv(trace_path, r.trace, r.has_err);
+        }
+        if (ranks_path && *ranks_path) write_ranks_csv(ranks_path, r.ranks);
+    });
+}
+
+int ref_write_edges(const int64_t* edges, int64_t E, const char* path, const char* comment) {
+    return guard([&] { write_edge_list(path, to_edges(edges, E), comment); });
+}
 
 }  // extern "C"

@@ -70,9 +70,16 @@ struct Device {
     Device& operator=(const Device&) = delete;
 };
 
+// Mode::Auto: bit-exact up to kAutoExactNnz entries, FAST above; the environment variable
+// CHEBPR_MODE=fast|bitexact pins Auto to one schedule (so the reference's own suites can be
+// run on the FAST kernel too, tests/test_reference_suites.py).
 int resolve_mode(Mode m, const UndirectedGraph& g) {
     if (m == Mode::Fast) return CHEB_MODE_FAST;
     if (m == Mode::BitExact) return CHEB_MODE_BITEXACT;
+    if (const char* env = std::getenv("CHEBPR_MODE")) {
+        if (std::strcmp(env, "fast") == 0) return CHEB_MODE_FAST;
+        if (std::strcmp(env, "bitexact") == 0) return CHEB_MODE_BITEXACT;
+    }
     return (int64_t)g.neighbors.size() <= kAutoExactNnz ? CHEB_MODE_BITEXACT : CHEB_MODE_FAST;
 }
 

@@ -1,8 +1,11 @@
 """The reference's OWN doctest suites (/root/reference/proj/tests/test_{coefficients,graph,
-cpaa,power,metrics}.cpp), compiled unchanged against the C++ drop-in layer
-(include/chebpr/*.hpp + libchebpr_dropin.so over the C-ABI) by `make reftests` where the
-reference sources exist; the binaries travel with the repo to the GPU box.  The
-coefficient suite is host-only; the others run their solves on the B200."""
+cpaa,power,metrics,cli}.cpp), compiled unchanged against the C++ drop-in layer
+(include/chebpr/*.hpp + libchebpr_dropin.so over the C-ABI; test_cli drives our `chebpr`
+binary) by `make reftests` where the reference sources exist; the binaries travel with the
+repo to the GPU box.  The coefficient suite is host-only; the others run their solves on
+the B200 — once with the drop-in's default Mode::Auto (bit-exact schedule for small
+graphs) and once with CHEBPR_MODE=fast, so that the product kernel (k_term_warp) runs the
+reference's own assertions too."""
 import os
 import subprocess
 
@@ -13,11 +16,14 @@ from conftest import ROOT
 BIN = os.path.join(ROOT, "build", "reftests")
 
 
-def run_suite(name):
+def run_suite(name, mode=None):
     path = os.path.join(BIN, name)
     if not os.path.exists(path):
         pytest.skip(f"{path} not built (needs /root/reference at build time)")
-    p = subprocess.run([path], capture_output=True, text=True, timeout=900)
+    env = dict(os.environ)
+    if mode:
+        env["CHEBPR_MODE"] = mode
+    p = subprocess.run([path], capture_output=True, text=True, timeout=900, env=env)
     summary = p.stdout.strip().splitlines()[-1] if p.stdout.strip() else ""
     assert p.returncode == 0, f"{name} failed:\n{p.stderr[-4000:]}\n{summary}"
     assert "| 0 failed |" in summary, summary
@@ -29,9 +35,12 @@ def test_reference_coefficient_suite_host():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("suite", ["test_graph", "test_cpaa", "test_power", "test_metrics"])
-def test_reference_suite_on_b200(suite):
-    run_suite(suite)
+@pytest.mark.parametrize("mode", [None, "fast"])
+@pytest.mark.parametrize("suite", ["test_graph", "test_cpaa", "test_power", "test_metrics", "test_cli"])
+def test_reference_suite_on_b200(suite, mode):
+    summary = run_suite(suite, mode)
+    if suite == "test_cli":
+        assert "10 passed" in summary, summary
 
 
 def _strip_timings(line):
@@ -47,7 +56,9 @@ def test_reference_acceptance_gate_matches_reference():
     same PASS/FAIL verdicts and the same reported figures as the reference's own build
     (tests/golden/acceptance_reference.txt, made by tests/golden/make_acceptance_golden.sh),
     timings aside.  Criterion 5 fails for the reference too (ring / regular graphs reach the
-    uniform PageRank at round 1); criterion 7 needs the reference CLI (out of scope)."""
+    uniform PageRank at round 1).  Criterion 7 drives the CLI: the reference's golden run had
+    no CLI (CLI11 is absent here, so its tools/ cannot be built), ours drives `chebpr` and
+    must pass (ranks CSV byte-identical across K = 1, 2, 8 for cpaa and power)."""
     path = os.path.join(BIN, "acceptance_main")
     if not os.path.exists(path):
         pytest.skip(f"{path} not built (needs /root/reference at build time)")
@@ -55,4 +66,9 @@ def test_reference_acceptance_gate_matches_reference():
     ours = [_strip_timings(ln) for ln in p.stdout.splitlines() if ln.startswith("criterion")]
     want_txt = open(os.path.join(ROOT, "tests", "golden", "acceptance_reference.txt")).read()
     want = [_strip_timings(ln) for ln in want_txt.splitlines() if ln.startswith("criterion")]
-    assert len(ours) == 9 and ours == want, "\n".join(f"ours: {a}\nref:  {b}" for a, b in zip(ours, want) if a != b)
+    assert len(ours) == 9
+    c7 = ours[6]
+    assert c7.startswith("criterion 7: PASS") and "cpaa K{1,2,8} byte-identical" in c7 \
+        and "power K{1,2,8} byte-identical" in c7, c7
+    ours[6] = want[6]
+    assert ours == want, "\n".join(f"ours: {a}\nref:  {b}" for a, b in zip(ours, want) if a != b)

@@ -15,7 +15,7 @@ import paper_2112_01743_b200 as cheb  # noqa: E402
 
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 cfg = bench.CONFIGS[cfg_name]
-edges = np.asarray(bench.make_edges(cfg, None))
+edges = np.asarray(bench.make_edges_host(cfg))
 edges = edges.reshape(-1, 2).astype(np.int64)
 path = os.path.join(tempfile.mkdtemp(), f"{cfg_name}.txt")
 t = time.perf_counter()
