@@ -481,7 +481,8 @@ int main(int argc, char** argv) {
             cheb_graph_info info;
             check(cheb_graph_get_info(df.h, &info));
             const int64_t n = info.n;
-            const int mode = mode_of(run_mode, info.nnz);
+            // bit-exact sums are fp64 only: auto picks FAST for an fp32 solve
+            const int mode = run_precision == 32 && run_mode == "auto" ? CHEB_MODE_FAST : mode_of(run_mode, info.nnz);
             chebpr::Vector ranks(n);
             std::vector<cheb_trace_row> tr;
             int rounds = 0;

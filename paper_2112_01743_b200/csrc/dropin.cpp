@@ -298,7 +298,7 @@ PageRankResult run_cpaa(const UndirectedGraph& g, const SolverConfig& cfg, const
     o.eps = cfg.eps;
     o.max_rounds = cfg.max_rounds;
     o.parallelism = cfg.parallelism;
-    o.mode = resolve_mode(cfg.mode, g);
+    o.mode = cfg.precision == 32 && cfg.mode == Mode::Auto ? CHEB_MODE_FAST : resolve_mode(cfg.mode, g);  // bit-exact is fp64 only
     o.precision = cfg.precision;
     const int cap = std::max({cfg.rounds, cfg.max_rounds, 1}) + 1;
     std::vector<cheb_trace_row> tr(static_cast<size_t>(cap));
