@@ -860,6 +860,124 @@ __global__ void k_permute_chunks(const Tile* __restrict__ tiles, int n_chunk_til
     }
 }
 
+// Bank-aware entry order inside PACK tiles (rows of <= kWarpNnz entries, L = 2^lg lanes per
+// row; lane li of row g reads row offset li + s L at slot s, term.cuh term_step).  One
+// instruction (slot s) serves a half-warp's 16 lanes at once, and its hot-prefix gathers
+// (fp64 ids < H: bank pair id mod 16) conflict when two lanes hit the same bank pair.  Per
+// half-warp, entries are redistributed within each row over that half-warp's offsets of the
+// row: at every slot each lane takes, from its row's remaining entries, a hot entry on a
+// bank pair still free at that slot, else a cold entry, else any.  Rows keep their entry
+// sets (sums re-associated, deterministically).  One thread per (tile, half-warp).
+template <class RPN>
+__global__ void k_schedule_pack(const Tile* __restrict__ tiles, int t0, int t1, const RPN* __restrict__ rp, int H,
+                                int* __restrict__ col) {
+    for (int64_t job = t0 * 2 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; job < (int64_t)t1 * 2;
+         job += (int64_t)gridDim.x * blockDim.x) {
+        const int t = (int)(job >> 1), hw = (int)(job & 1);
+        const Tile a = tiles[t];
+        if (a.meta & kTileChunk) continue;
+        const int rows = tiles[t + 1].row_begin - a.row_begin;
+        const int lg = a.meta & 0xf, L = 1 << lg;
+        // rows of this half-warp and the lanes' offset classes
+        int g0, g1, cls_lo, cls_hi;
+        if (L <= 16) {
+            g0 = hw * (16 >> lg);
+            g1 = min(rows, g0 + (16 >> lg));
+            cls_lo = 0;
+            cls_hi = L;
+        } else {  // one row over both half-warps: lanes li in [16 hw, 16 hw + 16)
+            g0 = 0;
+            g1 = rows > 0 ? 1 : 0;
+            cls_lo = 16 * hw;
+            cls_hi = 16 * hw + 16;
+        }
+        if (g0 >= g1) continue;
+        int val[kWarpNnz];
+        unsigned char rowof[kWarpNnz];
+        bool used[kWarpNnz];
+        int cnt = 0;
+        int pstart[17], deg[16];
+        int64_t base[16];
+        for (int g = g0; g < g1; ++g) {
+            const int k = g - g0;
+            base[k] = (int64_t)rp[a.row_begin + g];
+            deg[k] = (int)((int64_t)rp[a.row_begin + g + 1] - base[k]);
+            pstart[k] = cnt;
+            for (int o = 0; o < deg[k]; ++o) {
+                const int li = o & (L - 1);
+                if (li < cls_lo || li >= cls_hi) continue;
+                val[cnt] = col[base[k] + o];
+                rowof[cnt] = (unsigned char)k;
+                used[cnt] = false;
+                ++cnt;
+            }
+        }
+        pstart[g1 - g0] = cnt;
+        int out[kWarpNnz];
+        for (int s = 0;; ++s) {
+            bool any = false;
+            unsigned banks = 0;
+            for (int g = g0; g < g1; ++g) {
+                const int k = g - g0;
+                for (int li = cls_lo; li < cls_hi; ++li) {
+                    const int o = li + s * L;
+                    if (o >= deg[k]) continue;
+                    any = true;
+                    int pick = -1, cold = -1, anyi = -1;
+                    for (int i = pstart[k]; i < pstart[k + 1]; ++i) {
+                        if (used[i]) continue;
+                        if (anyi < 0) anyi = i;
+                        const int v = val[i];
+                        if ((unsigned)v < (unsigned)H) {
+                            if (!(banks >> (v & 15) & 1u)) {
+                                pick = i;
+                                break;
+                            }
+                        } else if (cold < 0) {
+                            cold = i;
+                        }
+                    }
+                    if (pick < 0) pick = cold >= 0 ? cold : anyi;
+                    used[pick] = true;
+                    if ((unsigned)val[pick] < (unsigned)H) banks |= 1u << (val[pick] & 15);
+                    // slot (li, s) of row k: position among this half-warp's offsets of the row
+                    out[pick] = o;  // entry `pick` goes to row offset o
+                }
+            }
+            if (!any) break;
+        }
+        for (int i = 0; i < cnt; ++i) col[base[rowof[i]] + out[i]] = val[i];
+    }
+}
+
+// Chunk tiles of rows whose ids were sorted ascending in place (x larger than L2): the
+// same bank-aware chunk order as k_permute_chunks, applied to the sorted values (cold
+// entries keep their ascending order in the free slots, so their gathers still walk x in
+// address order).  One warp per chunk tile.
+template <class RPN>
+__global__ void k_schedule_chunks_inplace(const Tile* __restrict__ tiles, int n_chunk_tiles, int H,
+                                          int* __restrict__ col) {
+    __shared__ SchedScratch scr[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_chunk_tiles;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t z0 = tiles[t].nnz_begin;
+        const int cnt = (int)(tiles[t + 1].nnz_begin - z0);
+        int val[8], dst[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int p = lane + 32 * q;
+            val[q] = p < cnt ? col[z0 + p] : 0;
+        }
+        __syncwarp();
+        schedule_chunk(val, cnt, H, scr[w], dst);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (dst[q] >= 0) col[z0 + dst[q]] = val[q];
+        __syncwarp();
+    }
+}
+
 // padded exchange position of every old id: new id u on rank r -> r*max_rows + (u - cuts[r])
 __global__ void k_posmap(const int* __restrict__ rank_of_old, int64_t n, const int64_t* __restrict__ cuts, int G,
                          int64_t max_rows, int* __restrict__ pos) {
@@ -1213,6 +1331,17 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
             const int64_t segs = hubs_only ? V.n_hub : nl;
             const int64_t items = hubs_only ? (int64_t)read_scalar(V.row_ptr.ptr<RPN>() + segs, st) : nnz_l;
             sort_view_rows_t<RPN>(V, segs, items, st);
+            if (tuning().chunksched && V.n_chunk_tiles > 0) {  // the sort undid the chunk order
+                k_schedule_chunks_inplace<RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
+                    V.tiles.ptr<Tile>(), V.n_chunk_tiles, kHotBytes / 8, V.col.ptr<int>());
+                CHEB_CUDA_CHECK(cudaGetLastError());
+            }
+        }
+        if (tuning().packsched && V.n_tiles > V.n_chunk_tiles) {
+            const int jobs = 2 * (V.n_tiles - V.n_chunk_tiles);
+            k_schedule_pack<RPN><<<std::max(1, std::min((jobs + 127) / 128, 148 * 8)), 128, 0, st>>>(
+                V.tiles.ptr<Tile>(), V.n_chunk_tiles, V.n_tiles, V.row_ptr.ptr<RPN>(), kHotBytes / 8, V.col.ptr<int>());
+            CHEB_CUDA_CHECK(cudaGetLastError());
         }
     }
     if (g->inv_array) {

@@ -163,7 +163,8 @@ bool chebgpu::l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* 
     if (!use) return false;
     w->base_ptr = const_cast<void*>(base);
     w->num_bytes = std::min({bytes, persist_max[dev], window_max[dev]});
-    w->hitRatio = 1.0f;
+    if (tuning().l2win_mb >= 0) w->num_bytes = std::min(w->num_bytes, (size_t)tuning().l2win_mb << 20);
+    w->hitRatio = std::min(1.0f, std::max(0.0f, tuning().l2win_pct / 100.0f));
     w->hitProp = cudaAccessPropertyPersisting;
     w->missProp = cudaAccessPropertyStreaming;
     return true;
@@ -1017,6 +1018,12 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "l2win") tuning().l2win = value;
         else if (k == "pdl") tuning().pdl = value;
         else if (k == "chunksched") tuning().chunksched = value;  // applies to views built afterwards
+        else if (k == "l2win_mb") tuning().l2win_mb = value;
+        else if (k == "l2win_pct") tuning().l2win_pct = value;
+        else if (k == "streamcs") tuning().streamcs = value;
+        else if (k == "xout_hint") tuning().xout_hint = value;
+        else if (k == "xdiscard") tuning().xdiscard = value;
+        else if (k == "packsched") tuning().packsched = value;  // applies to views built afterwards
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }

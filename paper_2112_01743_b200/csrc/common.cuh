@@ -334,6 +334,14 @@ struct Tuning {
     int pdl = 1;        // 1: programmatic dependent launch along the term chain (default on)
     int sortrows = -1;  // view rows in ascending id order: -1 when x exceeds L2, 0 never, 1 always, 2 hub rows only (experiment)
     int chunksched = 1; // hub chunks ordered for conflict-free hot gathers (k_schedule_chunks)
+    int l2win_mb = -1;  // cap on the persisting window over x (MB); -1 = the device's persisting maximum
+    int l2win_pct = 100; // hitRatio of that window (percent)
+    int streamcs = 0;   // 1: per-row operands (row pointers, T, acc loads; T, acc stores) as streaming (.cs)
+    int xout_hint = -1; // x_{k+1} stores: 0 plain, 1 L2 evict_first policy, 2 .cs, 3 L2 evict_last policy;
+                        // -1: evict_last when x exceeds L2 (config 4: 4.06 -> 3.95 ms/term), else plain
+    int xdiscard = 1;   // 1: the term kernel drops the x_out buffer's (dead) lines from L2 at its start
+                        // (config 3: 384 -> 381 us/term; no write-back of dead lines)
+    int packsched = 1;  // pack-tile entries ordered for conflict-free hot gathers (k_schedule_pack)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -345,6 +353,12 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_PDL")) x.pdl = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_SORTROWS")) x.sortrows = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_CHUNKSCHED")) x.chunksched = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_L2WIN_MB")) x.l2win_mb = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_L2WIN_PCT")) x.l2win_pct = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_STREAMCS")) x.streamcs = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_XOUT_HINT")) x.xout_hint = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_XDISCARD")) x.xdiscard = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_PACKSCHED")) x.packsched = std::atoi(e);
         return x;
     }();
     return t;

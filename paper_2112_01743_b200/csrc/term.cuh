@@ -76,6 +76,9 @@ struct TermArgs {
     double* hub_ts;  // [n_hub][2] this term
     int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
     int tune_skip;      // experiments only: 1 skip chunk tiles, 2 skip pack tiles, 16+b only bin b
+    int stream_cs;      // per-row operands loaded / stored with the streaming (.cs) policy
+    int xout_hint;      // x_{k+1} store policy (tuning().xout_hint)
+    int64_t xdiscard_len;  // > 0: drop x_out[0, len) from L2 at kernel start (dead x_{k-1} lines)
     // fused push exchange (partitioned runs): x_{k+1}[u] is stored at push[r][push_off + u]
     // for every rank r (peer memory over NVLink) instead of x_out[u]
     V* const* push;
@@ -151,6 +154,37 @@ __device__ __forceinline__ float ldg_cold(const float* p) {
 #else
     return __ldg(p);
 #endif
+}
+
+template <class T>
+__device__ __forceinline__ T ld_cs(const T* p) { return __ldcs(p); }
+template <class T>
+__device__ __forceinline__ void st_cs(T* p, T v) { __stcs(p, v); }
+
+// Store with an L2 eviction-priority hint: 1 evict_first policy, 2 .cs, 3 evict_last policy.
+__device__ __forceinline__ void st_hint(double* p, double v, int h) {
+    if (h == 1 || h == 3) {
+        uint64_t pol;
+        if (h == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
+    } else if (h == 2) {
+        __stcs(p, v);
+    } else {
+        *p = v;
+    }
+}
+__device__ __forceinline__ void st_hint(float* p, float v, int h) {
+    if (h == 1 || h == 3) {
+        uint64_t pol;
+        if (h == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+        else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(v), "l"(pol) : "memory");
+    } else if (h == 2) {
+        __stcs(p, v);
+    } else {
+        *p = v;
+    }
 }
 
 __device__ __forceinline__ double lds_v(unsigned addr, double) {
@@ -235,14 +269,19 @@ __device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, 
         const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
         if constexpr (EPI == EPI_CPAA) {
             const V t = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
-            a.T[u] = t;
             const V nacc = add_rn(accv, mul_rn((V)a.ck, t));
-            a.acc[u] = nacc;
             const V xn = mul_rn(t, inv);
+            if (a.stream_cs) {
+                st_cs(a.T + u, t);
+                st_cs(a.acc + u, nacc);
+            } else {
+                a.T[u] = t;
+                a.acc[u] = nacc;
+            }
             if (a.push) {  // fused exchange: straight into every rank's copy of x_{k+1}
                 for (int r = 0; r < a.push_n; ++r) a.push[r][a.push_off + u] = xn;
             } else {
-                a.x_out[u] = xn;
+                st_hint(a.x_out + u, xn, a.xout_hint);
             }
             p0 += (double)t;
             p1 += (double)nacc;
@@ -334,10 +373,17 @@ __device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR&
     const int lg = t.meta & 0xf;
     const int g = lane >> lg;
     if ((lane & ((1 << lg) - 1)) == 0 && g < t.rows) {
-        o.rs = (int)(a.rp[t.r0 + g] - t.z0);
-        o.re = (int)(a.rp[t.r0 + g + 1] - t.z0);
-        if constexpr (EPI != EPI_PLAIN) o.pv = prev_src<EPI>(a)[t.r0 + g];
-        if constexpr (EPI == EPI_CPAA) o.av = a.acc[t.r0 + g];
+        if (a.stream_cs) {
+            o.rs = (int)(ld_cs(a.rp + t.r0 + g) - t.z0);
+            o.re = (int)(ld_cs(a.rp + t.r0 + g + 1) - t.z0);
+            if constexpr (EPI != EPI_PLAIN) o.pv = ld_cs(prev_src<EPI>(a) + t.r0 + g);
+            if constexpr (EPI == EPI_CPAA) o.av = ld_cs(a.acc + t.r0 + g);
+        } else {
+            o.rs = (int)(a.rp[t.r0 + g] - t.z0);
+            o.re = (int)(a.rp[t.r0 + g + 1] - t.z0);
+            if constexpr (EPI != EPI_PLAIN) o.pv = prev_src<EPI>(a)[t.r0 + g];
+            if constexpr (EPI == EPI_CPAA) o.av = a.acc[t.r0 + g];
+        }
     }
 }
 
@@ -486,6 +532,15 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
         if (nt > kDescBlock) issue_desc(my, 1, nullptr, ws.desc[1], &ws.descm[1]);
     }
     pdl_wait();  // x_k, T, acc come from the previous kernels of the stream
+    if (a.xdiscard_len > 0) {
+        // x_out holds x_{k-1}, dead once the previous term finished: drop its lines from L2
+        // (no write-back) so they do not hold cache space (or the persisting carve-out)
+        const int64_t lines = a.xdiscard_len * (int64_t)sizeof(V) / 128;
+        const char* base = reinterpret_cast<const char*>(a.x_out);
+        for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; l < lines;
+             l += (int64_t)gridDim.x * blockDim.x)
+            asm volatile("discard.global.L2 [%0], 128;" :: "l"(base + l * 128) : "memory");
+    }
     if (threadIdx.x == 0) {
         mbar_expect_tx(&mbar_hot, hot_bytes);
         constexpr unsigned kPiece = 32768;
@@ -950,6 +1005,15 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         TermArgs<RP, V> ab = a;
         ab.tune_nogather = tuning().nogather;
         ab.tune_skip = tuning().skip;
+        ab.stream_cs = tuning().streamcs;
+        ab.xout_hint = tuning().xout_hint;
+        if (ab.xout_hint < 0) {  // x_{k+1} lines kept in L2 for the next term when x exceeds it
+            int l2 = 0;
+            cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
+            ab.xout_hint = (int64_t)g->view.x_len * (int64_t)sizeof(V) > (int64_t)l2 ? 3 : 0;
+        }
+        // x buffers are cudaMalloc'ed (256-B aligned): whole 128-B lines of x_out only
+        ab.xdiscard_len = (EPI == EPI_CPAA && tuning().xdiscard && !a.push) ? (g->view.x_len * (int64_t)sizeof(V) / 128) * 128 / (int64_t)sizeof(V) : 0;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(g->view.grid);
         cfg.blockDim = dim3(kWarps * 32);
