@@ -609,7 +609,8 @@ cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double
     });
 }
 
-constexpr int kBatchBlock = 128;  // right-hand sides per SpMM pass (32 lanes x 4 values)
+// right-hand sides per SpMM pass (<= 128: 32 lanes x 4 values); tuning().batchblock
+static int batch_block() { return std::max(1, std::min(tuning().batchblock, 128)); }
 
 static BatchSpec batch_spec(cheb_graph* g, const cheb_cpaa_opts& o, const int64_t* seeds) {
     need_graph(g);
@@ -645,6 +646,7 @@ cheb_status cheb_cpaa_batch(cheb_graph_t g, const cheb_cpaa_opts* opts, const in
         if (opts) o = *opts;
         BatchSpec b = batch_spec(g, o, seeds);
         std::vector<double> tr, tot;
+        const int kBatchBlock = batch_block();
         if (b.R <= kBatchBlock) {
             cpaa_batch_solve(g, b, tr, tot, nullptr);
             if (ranks) read_batch_ranks(g, ranks, b.R);
@@ -659,6 +661,7 @@ cheb_status cheb_cpaa_batch(cheb_graph_t g, const cheb_cpaa_opts* opts, const in
                 BatchSpec bc = b;
                 bc.R = Rc;
                 bc.seeds = b.seeds ? b.seeds + c0 : nullptr;
+                bc.record_start = c0 == 0;
                 if (b.p) {
                     pblk.resize((size_t)n * Rc);
                     for (int64_t v = 0; v < n; ++v)
@@ -1024,6 +1027,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "xout_hint") tuning().xout_hint = value;
         else if (k == "xdiscard") tuning().xdiscard = value;
         else if (k == "packsched") tuning().packsched = value;  // applies to views built afterwards
+        else if (k == "batchblock") tuning().batchblock = std::max(1, std::min(value, 128));
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }

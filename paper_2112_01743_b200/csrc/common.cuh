@@ -342,6 +342,7 @@ struct Tuning {
     int xdiscard = 1;   // 1: the term kernel drops the x_out buffer's (dead) lines from L2 at its start
                         // (config 3: 384 -> 381 us/term; no write-back of dead lines)
     int packsched = 1;  // pack-tile entries ordered for conflict-free hot gathers (k_schedule_pack)
+    int batchblock = 128; // right-hand sides per batched pass (column blocks of one call)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -359,6 +360,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_XOUT_HINT")) x.xout_hint = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_XDISCARD")) x.xdiscard = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_PACKSCHED")) x.packsched = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_BATCHBLOCK")) x.batchblock = std::atoi(e);
         return x;
     }();
     return t;
@@ -420,6 +422,7 @@ struct BatchSpec {
     int R = 1;
     const double* p = nullptr;      // host n x R row-major, or null
     const int64_t* seeds = nullptr;  // host R vertex ids (one-hot columns), or null
+    bool record_start = true;        // false: a later column block of one call (timing spans all)
 };
 void cpaa_batch_solve(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace,
                       std::vector<double>& totals, std::vector<double>* term_ms);

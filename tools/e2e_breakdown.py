@@ -38,7 +38,7 @@ for it in range(4):
     cheb.api._check(lib.cheb_graph_upload_csr(off.ctypes.data_as(L.I64P), off.size, nb.ctypes.data_as(L.I64P),
                                               nb.size, host.degrees.ctypes.data_as(L.I64P), host.degrees.size,
                                               inv.ctypes.data_as(L.F64P), inv.size,
-                                              host.n, host.m, 0, 0, 0, C.byref(h)))
+                                              host.n, host.m, 0, 0, int(info["row_ptr_64"]), C.byref(h)))
     t1 = time.perf_counter()
     cheb.api._check(lib.cheb_cpaa(h, C.byref(o), None, 0, ranks.ctypes.data_as(L.F64P), tr, C.byref(rounds),
                                   C.byref(tot)))
