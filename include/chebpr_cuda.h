@@ -178,6 +178,10 @@ void cheb_comm_destroy(cheb_comm_t c);
 cheb_status cheb_graph_attach_comm(cheb_graph_t g, cheb_comm_t comm);
 cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, int64_t* nnz_local,
                                       int64_t* max_rows);
+/* Exchange volume of this rank's local rows per term (new; no reference counterpart): remote
+ * x_{k+1} stores of the halo-only push (a row's value goes only to the ranks owning one of
+ * its neighbours) and of replicate-to-every-rank ((G - 1) per local row). */
+cheb_status cheb_graph_exchange_info(cheb_graph_t g, int64_t* halo_stores, int64_t* all_stores);
 
 /* ---- solvers ---- */
 enum { CHEB_MODE_FAST = 0, CHEB_MODE_BITEXACT = 1 };

@@ -978,6 +978,27 @@ __global__ void k_schedule_chunks_inplace(const Tile* __restrict__ tiles, int n_
     }
 }
 
+// Halo masks of a row partition: bit r of mask[u] iff row u has a neighbour in rank r's
+// padded slot [r * max_rows, (r + 1) * max_rows) (column ids are padded positions).  Warp
+// per row; also counts the remote stores per term (halo vs replicate-to-all) in int64.
+template <class RPN>
+__global__ void k_push_mask(const RPN* __restrict__ rp, const int* __restrict__ col, int64_t nl, int64_t max_rows,
+                            int G, int rank, unsigned* __restrict__ mask, unsigned long long* __restrict__ counts) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long halo = 0;
+    for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nl;
+         u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        unsigned m = 0;
+        for (int64_t j = (int64_t)rp[u] + lane; j < (int64_t)rp[u + 1]; j += 32) m |= 1u << (int)(col[j] / max_rows);
+        for (int o = 16; o; o >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
+        if (lane == 0) {
+            mask[u] = m;
+            halo += (unsigned long long)__popc(m & ~(1u << rank));
+        }
+    }
+    if (lane == 0 && halo) atomicAdd(counts, halo);
+}
+
 // padded exchange position of every old id: new id u on rank r -> r*max_rows + (u - cuts[r])
 __global__ void k_posmap(const int* __restrict__ rank_of_old, int64_t n, const int64_t* __restrict__ cuts, int G,
                          int64_t max_rows, int* __restrict__ pos) {
@@ -1343,6 +1364,24 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
                 V.tiles.ptr<Tile>(), V.n_chunk_tiles, V.n_tiles, V.row_ptr.ptr<RPN>(), kHotBytes / 8, V.col.ptr<int>());
             CHEB_CUDA_CHECK(cudaGetLastError());
         }
+    }
+    if (P.G > 1 && nl > 0) {
+        if (P.G > 32) fail(CHEB_CAPACITY, "halo masks support at most 32 ranks");
+        V.push_mask.alloc(sizeof(unsigned) * nl);
+        DevMem cnt(sizeof(unsigned long long));
+        CHEB_CUDA_CHECK(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), st));
+        k_push_mask<RPN><<<(int)std::min<int64_t>((nl * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+            V.row_ptr.ptr<RPN>(), V.col.ptr<int>(), nl, P.max_rows, P.G, P.rank, V.push_mask.ptr<unsigned>(),
+            cnt.ptr<unsigned long long>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        unsigned long long c = 0;
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(&c, cnt.get(), sizeof c, cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        V.push_entries = (int64_t)c;
+        V.push_entries_all = nl * (int64_t)(P.G - 1);
+    } else {
+        V.push_mask.release();
+        V.push_entries = V.push_entries_all = 0;
     }
     if (g->inv_array) {
         V.inv.alloc(sizeof(double) * std::max<int64_t>(nl, 1));

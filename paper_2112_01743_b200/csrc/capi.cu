@@ -1012,6 +1012,16 @@ cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, 
     });
 }
 
+cheb_status cheb_graph_exchange_info(cheb_graph_t g, int64_t* halo_stores, int64_t* all_stores) {
+    return guarded([&] {
+        need_graph(g);
+        GraphScope gs(g);
+        ensure_view(g);
+        if (halo_stores) *halo_stores = tuning().halo ? g->view.push_entries : g->view.push_entries_all;
+        if (all_stores) *all_stores = g->view.push_entries_all;
+    });
+}
+
 cheb_status cheb_set_tuning(const char* key, int value) {
     return guarded([&] {
         const std::string k = key ? key : "";
@@ -1028,6 +1038,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "xdiscard") tuning().xdiscard = value;
         else if (k == "packsched") tuning().packsched = value;  // applies to views built afterwards
         else if (k == "batchblock") tuning().batchblock = std::max(1, std::min(value, 128));
+        else if (k == "halo") tuning().halo = value;
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }

@@ -207,10 +207,17 @@ struct SolverView {
     int n_chunk_tiles = 0;
     DevMem hub_first;      // int32 [n_hub + 1]: first chunk tile of each hub row
     bool sorted_rows = false;  // rows hold their renamed ids in ascending order
+    // Row partition (G > 1): bit r of push_mask[u] = rank r has a row with neighbour u, i.e.
+    // needs x[u] (symmetric graph: u has a neighbour owned by r).  The halo-only push stores
+    // x_{k+1}[u] only there.  push_entries = sum of popcounts over the local rows minus the
+    // rows' own-rank bits (remote stores per term).
+    DevMem push_mask;          // uint32 [n_local]
+    int64_t push_entries = 0, push_entries_all = 0;  // halo / replicate-everything remote stores
     // tile bins (host statistics): 0..5 = pack tiles with 2^b lanes per row, 6 = chunk tiles
     int64_t bin_tiles[7] = {}, bin_rows[7] = {}, bin_nnz[7] = {};
     void set_stream(cudaStream_t s) {
-        for (DevMem* d : {&order, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first}) d->set_stream(s);
+        for (DevMem* d : {&order, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first, &push_mask})
+            d->set_stream(s);
     }
 };
 
@@ -343,6 +350,7 @@ struct Tuning {
                         // (config 3: 384 -> 381 us/term; no write-back of dead lines)
     int packsched = 1;  // pack-tile entries ordered for conflict-free hot gathers (k_schedule_pack)
     int batchblock = 128; // right-hand sides per batched pass (column blocks of one call)
+    int halo = 1;       // row partition, push exchange: store x_{k+1}[u] only on the ranks that read it
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -361,6 +369,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_XDISCARD")) x.xdiscard = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_PACKSCHED")) x.packsched = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_BATCHBLOCK")) x.batchblock = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_HALO")) x.halo = std::atoi(e);
         return x;
     }();
     return t;

@@ -245,6 +245,7 @@ struct DistSolve {
             a.push = push_table(k & 1);
             a.push_n = G;
             a.push_off = Vw.x_off;
+            a.push_mask = tuning().halo ? Vw.push_mask.ptr<unsigned>() : nullptr;
         }
         a.T = T[(k - 1) & 1];
         a.acc = acc;

@@ -84,6 +84,7 @@ struct TermArgs {
     V* const* push;
     int push_n;
     int64_t push_off;
+    const unsigned* push_mask;  // halo-only push: bit r = rank r reads x[u] (null: every rank)
 };
 
 // Row epilogue.  u is a row of the current layout; deg its row length.
@@ -278,8 +279,10 @@ __device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, 
                 a.T[u] = t;
                 a.acc[u] = nacc;
             }
-            if (a.push) {  // fused exchange: straight into every rank's copy of x_{k+1}
-                for (int r = 0; r < a.push_n; ++r) a.push[r][a.push_off + u] = xn;
+            if (a.push) {  // fused exchange: straight into the copies of x_{k+1} that are read
+                const unsigned m = a.push_mask ? __ldg(a.push_mask + u) : ~0u;
+                for (int r = 0; r < a.push_n; ++r)
+                    if (m >> r & 1u) a.push[r][a.push_off + u] = xn;
             } else {
                 st_hint(a.x_out + u, xn, a.xout_hint);
             }

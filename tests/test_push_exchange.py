@@ -159,3 +159,51 @@ def test_peer_and_group_argument_errors(cheb):
     # the handle still solves as a single-GPU graph after the failed calls
     r = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=5))
     assert np.allclose(r.ranks, 0.5)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_halo_push_volume_and_bitwise_equivalence(cheb, G):
+    """Halo-only push: rank r receives x_{k+1}[u] only when one of its rows has neighbour u
+    (for a symmetric graph: u has a neighbour owned by r).  The stores skipped are exactly the
+    ones never read, so the solve is bitwise the replicate-to-all solve; the store counts per
+    rank equal a numpy recount of the masks from the partition plan."""
+    import ctypes as C
+    from paper_2112_01743_b200 import _lib as L
+    from paper_2112_01743_b200 import generate as Gen
+    from paper_2112_01743_b200.distributed import partition_plan
+    lib = L.load()
+    e = Gen.chung_lu_edges(1 << 15, 2.1, 2.0, 5000.0, 150_000, 4)
+    hs = _handles(cheb, e, G)
+    grp = cheb.PartitionGroup(hs)
+    halo = cheb.run_cpaa(grp, cheb.SolverConfig(eps=1e-10))
+    stores = []
+    for h in hs:
+        a, b = C.c_int64(), C.c_int64()
+        assert lib.cheb_graph_exchange_info(h.handle, C.byref(a), C.byref(b)) == 0
+        stores.append((a.value, b.value))
+    assert lib.cheb_set_tuning(b"halo", 0) == 0
+    try:
+        full = cheb.run_cpaa(grp, cheb.SolverConfig(eps=1e-10))
+    finally:
+        lib.cheb_set_tuning(b"halo", 1)
+    assert np.array_equal(halo.ranks, full.ranks)
+    grp.close()
+    # numpy recount: owner of each new id, masks over each local row's neighbours
+    g = hs[0].download()
+    order, cuts, mr = partition_plan(g.degrees, G)
+    new = np.empty(g.n, dtype=np.int64)
+    new[order] = np.arange(g.n)
+    rows = np.repeat(new, np.diff(g.offsets))          # new id of each entry's row
+    owner_col = np.searchsorted(cuts, new[g.neighbors], side="right") - 1
+    owner_row = np.searchsorted(cuts, rows, side="right") - 1
+    pairs = np.unique(rows * G + owner_col)            # (row, rank needing it)
+    prow = pairs // G
+    pr = pairs % G
+    prow_owner = np.searchsorted(cuts, prow, side="right") - 1
+    for r in range(G):
+        mine = prow_owner == r
+        want_halo = int(np.count_nonzero(mine & (pr != r)))
+        n_local = int(cuts[r + 1] - cuts[r])
+        assert stores[r] == (want_halo, n_local * (G - 1)), (r, stores[r], want_halo)
+    del owner_row
+    assert sum(s[0] for s in stores) < sum(s[1] for s in stores)
