@@ -1123,19 +1123,23 @@ static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
 // Each of the first `segs` view rows' renamed ids in ascending order (cub segmented sort,
 // in place over V.col).
 template <class RPN>
-static void sort_view_rows_t(SolverView& V, int64_t segs, int64_t items, cudaStream_t st) {
+static void sort_rows_of(const SolverView& V, int* col, int64_t segs, int64_t items, cudaStream_t st) {
     if (segs <= 0 || items <= 0) return;
     TempStore tmp;
     const RPN* offs = V.row_ptr.ptr<RPN>();
     DevMem alt(sizeof(int) * (size_t)items + 64);
-    cub::DoubleBuffer<int> db(V.col.ptr<int>(), alt.ptr<int>());
+    cub::DoubleBuffer<int> db(col, alt.ptr<int>());
     size_t bytes = 0;
     CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, db, (int)items, (int)segs, offs, offs + 1, st));
     void* t = tmp.get(bytes);
     CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, db, (int)items, (int)segs, offs, offs + 1, st));
-    if (db.Current() != V.col.ptr<int>())
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(V.col.get(), db.Current(), sizeof(int) * items, cudaMemcpyDeviceToDevice, st));
+    if (db.Current() != col)
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(col, db.Current(), sizeof(int) * items, cudaMemcpyDeviceToDevice, st));
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+template <class RPN>
+static void sort_view_rows_t(SolverView& V, int64_t segs, int64_t items, cudaStream_t st) {
+    sort_rows_of<RPN>(V, V.col.ptr<int>(), segs, items, st);
 }
 
 template <class RPO, class RPN>
@@ -1144,6 +1148,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     const int64_t n = g->n;
     TempStore tmp;
     const RPO* rp_old = g->row_ptr.ptr<RPO>();
+    V.col_sorted.release();  // the batched path's sorted copy follows the view
 
     DevMem keys(sizeof(unsigned) * n), keys2(sizeof(unsigned) * n), ids(sizeof(int) * n);
     V.order.alloc(sizeof(int) * n);
@@ -1343,7 +1348,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         int dev = 0, l2 = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-        const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2 || g->want_sorted_rows)
+        const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2)
                                                  : tuning().sortrows > 0;
         const bool hubs_only = tuning().sortrows == 2 && V.n_hub > 0;
         const bool sort_rows = (big_x || hubs_only) && nnz_l > 0 && nnz_l < INT32_MAX;
@@ -1352,7 +1357,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
             const int64_t segs = hubs_only ? V.n_hub : nl;
             const int64_t items = hubs_only ? (int64_t)read_scalar(V.row_ptr.ptr<RPN>() + segs, st) : nnz_l;
             sort_view_rows_t<RPN>(V, segs, items, st);
-            if (tuning().chunksched && V.n_chunk_tiles > 0) {  // the sort undid the chunk order
+            if (tuning().chunksched > 1 && V.n_chunk_tiles > 0) {  // the sort undid the chunk order
                 k_schedule_chunks_inplace<RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
                     V.tiles.ptr<Tile>(), V.n_chunk_tiles, kHotBytes / 8, V.col.ptr<int>());
                 CHEB_CUDA_CHECK(cudaGetLastError());
@@ -1405,13 +1410,20 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     dbg_mark("  view: synced");
 }
 
-void sort_view_rows(cheb_graph* g) {
+// The batched path's own ascending-id copy of the view's columns (same rows, tiles and row
+// pointers), so that a batched solve never changes the scalar FAST schedule's bits.
+const int* batch_sorted_cols(cheb_graph* g) {
     ensure_view(g);
     SolverView& V = g->view;
-    if (V.sorted_rows || V.n_local == 0 || V.nnz_local >= INT32_MAX) return;
-    if (V.rp64) sort_view_rows_t<int64_t>(V, V.n_local, V.nnz_local, g->stream);
-    else sort_view_rows_t<int>(V, V.n_local, V.nnz_local, g->stream);
-    V.sorted_rows = true;
+    if (V.sorted_rows || V.n_local == 0 || V.nnz_local >= INT32_MAX) return V.col.ptr<int>();
+    if (!V.col_sorted) {
+        V.col_sorted.alloc(sizeof(int) * (size_t)V.nnz_local + 64);
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(V.col_sorted.get(), V.col.get(), sizeof(int) * (size_t)V.nnz_local,
+                                        cudaMemcpyDeviceToDevice, g->stream));
+        if (V.rp64) sort_rows_of<int64_t>(V, V.col_sorted.ptr<int>(), V.n_local, V.nnz_local, g->stream);
+        else sort_rows_of<int>(V, V.col_sorted.ptr<int>(), V.n_local, V.nnz_local, g->stream);
+    }
+    return V.col_sorted.ptr<int>();
 }
 
 void ensure_view(cheb_graph* g) {

@@ -212,11 +212,13 @@ struct SolverView {
     // x_{k+1}[u] only there.  push_entries = sum of popcounts over the local rows minus the
     // rows' own-rank bits (remote stores per term).
     DevMem push_mask;          // uint32 [n_local]
+    DevMem col_sorted;         // batched path only: col with each row in ascending id order
     int64_t push_entries = 0, push_entries_all = 0;  // halo / replicate-everything remote stores
     // tile bins (host statistics): 0..5 = pack tiles with 2^b lanes per row, 6 = chunk tiles
     int64_t bin_tiles[7] = {}, bin_rows[7] = {}, bin_nnz[7] = {};
     void set_stream(cudaStream_t s) {
-        for (DevMem* d : {&order, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first, &push_mask})
+        for (DevMem* d : {&order, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first, &push_mask,
+                          &col_sorted})
             d->set_stream(s);
     }
 };
@@ -285,7 +287,8 @@ struct Workspace {
 };
 
 struct BatchWorkspace {
-    DevMem T0, T1, X0, X1, acc, out, part, hub_part, hub_ts, trace, colpart, totals;
+    DevMem T0, T1, X0, X1, acc, out, part, hub_part, hub_ts, trace, colpart, totals, xinv;
+    const int* col = nullptr;  // the view's columns this batched solve gathers through
 };
 
 struct StagedState {
@@ -318,7 +321,6 @@ struct cheb_graph {
     chebgpu::BatchWorkspace bws;
     chebgpu::Partition part;
     chebgpu::PeerGroup* peer = nullptr;  // fused push exchange (instead of part.comm)
-    bool want_sorted_rows = false;       // a batched solve asked for ascending-id view rows
     double last_loop_ms = 0.0;
     int last_terms = 0;
     int last_launches = 0;
@@ -340,7 +342,8 @@ struct Tuning {
     int l2win = 1;      // 1: persisting-L2 window over the hot prefix of x (default on)
     int pdl = 1;        // 1: programmatic dependent launch along the term chain (default on)
     int sortrows = -1;  // view rows in ascending id order: -1 when x exceeds L2, 0 never, 1 always, 2 hub rows only (experiment)
-    int chunksched = 1; // hub chunks ordered for conflict-free hot gathers (k_schedule_chunks)
+    int chunksched = 1; // hub chunks ordered for conflict-free hot gathers (k_permute_chunks); 2: also
+                        // re-ordered after the config-4 row sort (k_schedule_chunks_inplace: no gain, ~57 ms of view build)
     int l2win_mb = -1;  // cap on the persisting window over x (MB); -1 = the device's persisting maximum
     int l2win_pct = 100; // hitRatio of that window (percent)
     int streamcs = 0;   // 1: per-row operands (row pointers, T, acc loads; T, acc stores) as streaming (.cs)
@@ -348,7 +351,8 @@ struct Tuning {
                         // -1: evict_last when x exceeds L2 (config 4: 4.06 -> 3.95 ms/term), else plain
     int xdiscard = 1;   // 1: the term kernel drops the x_out buffer's (dead) lines from L2 at its start
                         // (config 3: 384 -> 381 us/term; no write-back of dead lines)
-    int packsched = 1;  // pack-tile entries ordered for conflict-free hot gathers (k_schedule_pack)
+    int packsched = 0;  // pack-tile entries ordered for conflict-free hot gathers (k_schedule_pack);
+                        // off: no measurable gain (C2 68.8 -> 68.5, C3 381.6 -> 380.2, C4 3953 -> 3950 us/term)
     int batchblock = 128; // right-hand sides per batched pass (column blocks of one call)
     int halo = 1;       // row partition, push exchange: store x_{k+1}[u] only on the ranks that read it
 };
@@ -386,8 +390,8 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
                 int64_t nnz, const double* inv_degree, const std::function<bool()>& host_checks);
 void download_csr(cheb_graph* g, int64_t* offsets, int64_t* neighbors, int64_t* degrees);
 void ensure_view(cheb_graph* g);
-// Ascending renamed ids within every row of the (existing) solver view, in place.
-void sort_view_rows(cheb_graph* g);
+// The batched path's ascending-id copy of the view's columns (built on first use).
+const int* batch_sorted_cols(cheb_graph* g);
 void finalize_stats(cheb_graph* g);
 // ingest.cu
 void load_graph_text(cheb_graph* g, const std::string& path, const char* mem, int64_t mem_bytes, int format,

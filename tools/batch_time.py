@@ -23,7 +23,7 @@ lib.cheb_cpaa_opts_default(C.byref(o))
 o.eps, o.precision, o.R = 1e-10, prec, 64
 sp = seeds.ctypes.data_as(L.I64P)
 ref = None
-for blk in (64, 32, 16, 8):
+for blk in (64,):
     lib.cheb_set_tuning(b"batchblock", blk)
     ts = []
     for i in range(3):
