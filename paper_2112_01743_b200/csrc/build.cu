@@ -1428,6 +1428,7 @@ const int* batch_sorted_cols(cheb_graph* g) {
 
 void ensure_view(cheb_graph* g) {
     if (g->view.ready) return;
+    NvtxRange nvtx_("solver view build");
     if (g->rp64)
         build_view_t<int64_t, int64_t>(g, g->stream, nullptr);
     else

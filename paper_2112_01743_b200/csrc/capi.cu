@@ -227,6 +227,7 @@ cheb_status cheb_plan_iterations(double c, double eps, int* M, double* predicted
 }
 cheb_status cheb_coefficients(double c, int M, double* coeffs, double* beta_out, double* c0) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_coefficients");
         std::vector<double> t;
         coefficients(c, M, t, beta_out, c0);
         if (coeffs) std::memcpy(coeffs, t.data(), sizeof(double) * t.size());
@@ -249,6 +250,7 @@ void cheb_build_opts_default(cheb_build_opts* o) {
 cheb_status cheb_graph_build(const int64_t* edges, int64_t E, const cheb_build_opts* opts,
                              cheb_graph_t* out, cheb_graph_info* info) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_build");
         if (E < 0) fail(CHEB_INVALID_ARG, "negative edge count");
         cheb_build_opts o;
         cheb_build_opts_default(&o);
@@ -272,6 +274,7 @@ cheb_status cheb_graph_build_device(const void* d_edges, int64_t E, int edge_bit
                                     const cheb_build_opts* opts, cheb_graph_t* out,
                                     cheb_graph_info* info) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_build_device");
         if (edge_bits != 32 && edge_bits != 64) fail(CHEB_INVALID_ARG, "edge_bits must be 32 or 64");
         cheb_build_opts o;
         cheb_build_opts_default(&o);
@@ -290,6 +293,7 @@ cheb_status cheb_graph_upload_csr(const int64_t* offsets, int64_t n_offsets,
                                   int64_t n, int64_t m, int multi, int device, int row_ptr_64,
                                   cheb_graph_t* out) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_upload_csr");
         // cpaa.cpp:16-26 essential_check, in the reference's order.
         if (n < 1) fail(CHEB_VALIDATION, "graph has no vertices");
         if (n_offsets != n + 1 || n_degrees != n || (inv_degree && n_inv != n) ||
@@ -425,6 +429,7 @@ cheb_status cheb_validate_csr(const int64_t* offsets, int64_t n_offsets, const i
                               int64_t duplicates_removed, int64_t isolated_dropped, int device,
                               cheb_graph_stats* stats) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_validate_csr");
         if (!offsets || n_offsets < 1) fail(CHEB_VALIDATION, "offsets length is not n+1");
         int count = 0;
         if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
@@ -437,6 +442,7 @@ cheb_status cheb_validate_csr(const int64_t* offsets, int64_t n_offsets, const i
 
 cheb_status cheb_graph_validate_stats(cheb_graph_t g, cheb_graph_stats* stats) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_validate_stats");
         need_graph(g);
         GraphScope gs(g);
         if (!stats) fail(CHEB_INVALID_ARG, "null stats");
@@ -449,6 +455,7 @@ cheb_status cheb_graph_validate_stats(cheb_graph_t g, cheb_graph_stats* stats) {
 cheb_status cheb_graph_download_csr(cheb_graph_t g, int64_t* offsets, int64_t* neighbors,
                                     int64_t* degrees) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_download_csr");
         need_graph(g);
         GraphScope gs(g);
         download_csr(g, offsets, neighbors, degrees);
@@ -457,6 +464,7 @@ cheb_status cheb_graph_download_csr(cheb_graph_t g, int64_t* offsets, int64_t* n
 
 cheb_status cheb_graph_get_info(cheb_graph_t g, cheb_graph_info* info) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_get_info");
         need_graph(g);
         fill_info(g, info);
     });
@@ -522,7 +530,7 @@ static void fill_trace(cheb_graph* g, const SolveSpec& s, const std::vector<doub
         r.S_k = tr[2 * (k - 1) + 1];
         residual *= b;
         r.residual_mass = residual;
-        r.elapsed_ms = per_term;
+        r.elapsed_ms = g->term_elapsed_ms.size() == (size_t)s.M ? g->term_elapsed_ms[(size_t)k - 1] : per_term;
         if (errs) {
             r.err = (*errs)[2 * (k - 1)];
             r.err_l1 = (*errs)[2 * (k - 1) + 1];
@@ -558,6 +566,7 @@ cheb_status cheb_cpaa(cheb_graph_t g, const cheb_cpaa_opts* opts, const double* 
                       int64_t n_reference, double* ranks, cheb_trace_row* trace,
                       int* rounds_out, double* total_mass_out) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_cpaa");
         cheb_cpaa_opts o;
         cheb_cpaa_opts_default(&o);
         if (opts) o = *opts;
@@ -580,6 +589,7 @@ cheb_status cheb_cpaa(cheb_graph_t g, const cheb_cpaa_opts* opts, const double* 
 cheb_status cheb_cpaa_device(cheb_graph_t g, const cheb_cpaa_opts* opts, const void** d_ranks,
                              int sync) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_cpaa_device");
         cheb_cpaa_opts o;
         cheb_cpaa_opts_default(&o);
         if (opts) o = *opts;
@@ -598,6 +608,7 @@ cheb_status cheb_cpaa_device(cheb_graph_t g, const cheb_cpaa_opts* opts, const v
 cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double* term_ms,
                               int capacity, int* terms) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_cpaa_profile");
         cheb_cpaa_opts o;
         cheb_cpaa_opts_default(&o);
         if (opts) o = *opts;
@@ -641,6 +652,7 @@ static BatchSpec batch_spec(cheb_graph* g, const cheb_cpaa_opts& o, const int64_
 cheb_status cheb_cpaa_batch(cheb_graph_t g, const cheb_cpaa_opts* opts, const int64_t* seeds,
                             double* ranks, double* totals, cheb_trace_row* trace, int* rounds_out) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_cpaa_batch");
         cheb_cpaa_opts o;
         cheb_cpaa_opts_default(&o);
         if (opts) o = *opts;
@@ -706,6 +718,7 @@ cheb_status cheb_cpaa_batch(cheb_graph_t g, const cheb_cpaa_opts* opts, const in
 cheb_status cheb_cpaa_batch_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, const int64_t* seeds,
                                     double* term_ms, int capacity, int* terms) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_cpaa_batch_profile");
         cheb_cpaa_opts o;
         cheb_cpaa_opts_default(&o);
         if (opts) o = *opts;
@@ -719,6 +732,7 @@ cheb_status cheb_cpaa_batch_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, 
 
 cheb_status cheb_nccl_unique_id(void* out, int out_bytes) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_nccl_unique_id");
         if (out_bytes < (int)sizeof(ncclUniqueId)) fail(CHEB_INVALID_ARG, "unique id buffer too small");
         ncclUniqueId id;
         const ncclResult_t r = ncclGetUniqueId(&id);
@@ -729,6 +743,7 @@ cheb_status cheb_nccl_unique_id(void* out, int out_bytes) {
 
 cheb_status cheb_comm_create(const void* unique_id, int nranks, int rank, int device, cheb_comm_t* out) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_comm_create");
         if (nranks < 1 || rank < 0 || rank >= nranks) fail(CHEB_INVALID_ARG, "bad rank / nranks");
         DeviceGuard dg(device);
         auto* c = new cheb_comm();
@@ -755,6 +770,7 @@ void cheb_comm_destroy(cheb_comm_t c) {
 
 cheb_status cheb_graph_attach_comm(cheb_graph_t g, cheb_comm_t comm) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_attach_comm");
         need_graph(g);
         if (!comm) fail(CHEB_INVALID_ARG, "null communicator");
         if (comm->device != g->device) fail(CHEB_INVALID_ARG, "communicator and graph live on different devices");
@@ -860,6 +876,7 @@ void upload_table(cheb_graph* g) {
 
 cheb_status cheb_group_create(cheb_graph_t* graphs, int G, cheb_group_t* out) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_group_create");
         if (!graphs || G < 1 || !out) fail(CHEB_INVALID_ARG, "bad group arguments");
         for (int r = 0; r < G; ++r) {
             need_graph(graphs[r]);
@@ -903,6 +920,7 @@ cheb_status cheb_group_create(cheb_graph_t* graphs, int G, cheb_group_t* out) {
 cheb_status cheb_group_cpaa(cheb_group_t grp, const cheb_cpaa_opts* opts, double* ranks, cheb_trace_row* trace,
                             int* rounds, double* total) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_group_cpaa");
         if (!grp || grp->graphs.empty()) fail(CHEB_INVALID_ARG, "null group");
         cheb_graph* g0 = grp->graphs[0];
         cheb_cpaa_opts o;
@@ -930,6 +948,7 @@ void cheb_group_destroy(cheb_group_t grp) {
 
 cheb_status cheb_peer_export(cheb_graph_t g, int G, int rank, void* out, size_t cap) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_peer_export");
         need_graph(g);
         if (!out || cap < CHEB_PEER_EXPORT_BYTES) fail(CHEB_INVALID_ARG, "export buffer too small");
         make_peer(g, G, rank, false);
@@ -949,6 +968,7 @@ cheb_status cheb_peer_export(cheb_graph_t g, int G, int rank, void* out, size_t 
 
 cheb_status cheb_peer_import(cheb_graph_t g, const void* all, size_t bytes_per_rank) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_peer_import");
         need_graph(g);
         if (!g->peer || g->peer->lockstep) fail(CHEB_INVALID_ARG, "cheb_peer_export first");
         if (!all || bytes_per_rank < CHEB_PEER_EXPORT_BYTES) fail(CHEB_INVALID_ARG, "bad import buffer");
@@ -980,6 +1000,7 @@ cheb_status cheb_peer_import(cheb_graph_t g, const void* all, size_t bytes_per_r
 
 cheb_status cheb_peer_detach(cheb_graph_t g) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_peer_detach");
         need_graph(g);
         drop_peer(g);
         reset_partition(g, 1, 0);
@@ -988,6 +1009,7 @@ cheb_status cheb_peer_detach(cheb_graph_t g) {
 
 cheb_status cheb_graph_view_bins(cheb_graph_t g, int64_t* tiles, int64_t* rows, int64_t* nnz) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_view_bins");
         need_graph(g);
         GraphScope gs(g);
         ensure_view(g);
@@ -1002,6 +1024,7 @@ cheb_status cheb_graph_view_bins(cheb_graph_t g, int64_t* tiles, int64_t* rows, 
 cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, int64_t* nnz_local,
                                       int64_t* max_rows) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_partition_info");
         need_graph(g);
         GraphScope gs(g);
         ensure_view(g);
@@ -1014,6 +1037,7 @@ cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, 
 
 cheb_status cheb_graph_exchange_info(cheb_graph_t g, int64_t* halo_stores, int64_t* all_stores) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_exchange_info");
         need_graph(g);
         GraphScope gs(g);
         ensure_view(g);
@@ -1024,6 +1048,7 @@ cheb_status cheb_graph_exchange_info(cheb_graph_t g, int64_t* halo_stores, int64
 
 cheb_status cheb_set_tuning(const char* key, int value) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_set_tuning");
         const std::string k = key ? key : "";
         if (k == "hot") tuning().hot = value;
         else if (k == "nogather") tuning().nogather = value;
@@ -1039,6 +1064,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "packsched") tuning().packsched = value;  // applies to views built afterwards
         else if (k == "batchblock") tuning().batchblock = std::max(1, std::min(value, 128));
         else if (k == "halo") tuning().halo = value;
+        else if (k == "prefetch") tuning().prefetch = value;
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }
@@ -1046,6 +1072,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
 cheb_status cheb_last_timing(cheb_graph_t g, double* loop_ms, double* term_kernel_ms, int* terms,
                              int* launches) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_last_timing");
         need_graph(g);
         GraphScope gs(g);
         CHEB_CUDA_CHECK(cudaEventSynchronize(g->ev1));
@@ -1072,6 +1099,7 @@ cheb_status cheb_power(cheb_graph_t g, const cheb_power_opts* opts, const double
                        int64_t n_reference, double* ranks, cheb_trace_row* trace,
                        int trace_capacity, int* rounds_out, double* total_mass_out) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_power");
         cheb_power_opts o;
         cheb_power_opts_default(&o);
         if (opts) o = *opts;
@@ -1101,6 +1129,7 @@ cheb_status cheb_power(cheb_graph_t g, const cheb_power_opts* opts, const double
 
 cheb_status cheb_transition_apply(cheb_graph_t g, const double* x, int64_t nx, double* y, int mode) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_transition_apply");
         need_graph(g);
         single_gpu_only(g);
         if (nx != g->n)  // graph.cpp:105-107
@@ -1113,6 +1142,7 @@ cheb_status cheb_transition_apply(cheb_graph_t g, const double* x, int64_t nx, d
 
 cheb_status cheb_state_init(cheb_graph_t g, double c0, int mode) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_state_init");
         need_graph(g);
         single_gpu_only(g);
         essential(g);  // cpaa.cpp:168
@@ -1122,24 +1152,28 @@ cheb_status cheb_state_init(cheb_graph_t g, double c0, int mode) {
 cheb_status cheb_state_set(cheb_graph_t g, const double* T_prev, const double* T_curr,
                            const double* acc, int k) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_state_set");
         need_graph(g);
         staged_set(g, T_prev, T_curr, acc, k);
     });
 }
 cheb_status cheb_state_generate(cheb_graph_t g) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_state_generate");
         need_graph(g);
         staged_generate(g);
     });
 }
 cheb_status cheb_state_accumulate(cheb_graph_t g, double c_k) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_state_accumulate");
         need_graph(g);
         staged_accumulate(g, c_k);
     });
 }
 cheb_status cheb_state_rotate(cheb_graph_t g) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_state_rotate");
         need_graph(g);
         staged_rotate(g);
     });
@@ -1147,6 +1181,7 @@ cheb_status cheb_state_rotate(cheb_graph_t g) {
 cheb_status cheb_state_get(cheb_graph_t g, double* T_prev, double* T_curr, double* T_next,
                            double* acc, int* k) {
     return guarded([&] {
+        NvtxRange nvtx_("cheb_state_get");
         need_graph(g);
         staged_get(g, T_prev, T_curr, T_next, acc, k);
     });

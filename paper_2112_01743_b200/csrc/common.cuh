@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "chebpr_cuda.h"
 
 namespace chebgpu {
@@ -136,6 +138,17 @@ struct DeviceGuard {
     ~DeviceGuard() {
         if (prev >= 0) cudaSetDevice(prev);
     }
+};
+
+// NVTX ranges (SURVEY.md §5 tracing): every C-ABI entry point is one named range, the
+// phases inside (upload, solver view, solve enqueue) nested ranges, so an nsys / ncu
+// timeline shows where a call's time goes.  nvtx3 is header-only: with no tool attached
+// each push/pop is a cheap no-op.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 // Per-device one-time setup flags (function attributes, pool attributes): a context
@@ -270,6 +283,8 @@ struct Workspace {
     DevMem total;                       // double [1]
     DevMem coeffs;                      // double [M+1]
     DevMem snap;                        // BITEXACT: double [M][2][n] snapshots of T_k, acc_k
+    DevMem stamps;                      // u64 [M + 1] term boundary stamps (%globaltimer, ns)
+    DevMem done;                        // u32 [M + 1] CTAs finished per term (last one stamps)
     // CUDA graph of the whole solve for a given configuration.
     cudaGraphExec_t exec = nullptr;
     std::string exec_key;
@@ -278,7 +293,7 @@ struct Workspace {
     // every buffer back to the pool on its stream (the owner calls this while the stream lives)
     void release_buffers() {
         for (DevMem* d : {&T0, &T1, &X0, &X1, &acc, &out, &part, &hub_part, &hub_ts, &trace, &total,
-                          &coeffs, &snap})
+                          &coeffs, &snap, &stamps, &done})
             d->release();
     }
     ~Workspace() {
@@ -287,7 +302,7 @@ struct Workspace {
 };
 
 struct BatchWorkspace {
-    DevMem T0, T1, X0, X1, acc, out, part, hub_part, hub_ts, trace, colpart, totals, xinv;
+    DevMem T0, T1, X0, X1, acc, out, part, hub_part, hub_ts, trace, colpart, totals;
     const int* col = nullptr;  // the view's columns this batched solve gathers through
 };
 
@@ -323,6 +338,9 @@ struct cheb_graph {
     chebgpu::PeerGroup* peer = nullptr;  // fused push exchange (instead of part.comm)
     double last_loop_ms = 0.0;
     int last_terms = 0;
+    // device-clock time of each term of the last scalar solve (%globaltimer stamps taken by
+    // the last CTA of each term's final kernel; TraceRow::elapsed_ms), empty if unavailable
+    std::vector<double> term_elapsed_ms;
     int last_launches = 0;
     ~cheb_graph();
 };
@@ -355,6 +373,7 @@ struct Tuning {
                         // off: no measurable gain (C2 68.8 -> 68.5, C3 381.6 -> 380.2, C4 3953 -> 3950 us/term)
     int batchblock = 128; // right-hand sides per batched pass (column blocks of one call)
     int halo = 1;       // row partition, push exchange: store x_{k+1}[u] only on the ranks that read it
+    int prefetch = 0;   // term kernel: L2 prefetch distance in tiles (0 off)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -374,6 +393,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_PACKSCHED")) x.packsched = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_BATCHBLOCK")) x.batchblock = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_HALO")) x.halo = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_PREFETCH")) x.prefetch = std::atoi(e);
         return x;
     }();
     return t;

@@ -26,6 +26,7 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
     double* snap = (!L.fast && M > 0 && !d_ref && w.snap.bytes() >= sizeof(double) * 2 * (size_t)M * n)
                        ? w.snap.ptr<double>() : nullptr;
 
+    if (M > 0) CHEB_CUDA_CHECK(cudaMemsetAsync(w.done.get(), 0, sizeof(unsigned) * ((size_t)M + 1), st));
     k_init<RP, V><<<grid1d(n), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, d_p, L.order, n,
                                                   c0 / 2.0, T[0], T[1], acc, X[0]);
     CHEB_CUDA_CHECK(cudaGetLastError());
@@ -39,6 +40,11 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
         a.acc = acc;
         a.ck = coeffs[k];
         a.first = k == 1;
+        if (!term_ev) {  // per-term device clock (profiling runs time the terms with events)
+            a.stamp_start = k == 1 ? w.stamps.ptr<unsigned long long>() : nullptr;
+            a.stamp_end = w.stamps.ptr<unsigned long long>() + k;
+            a.done = w.done.ptr<unsigned>() + k;
+        }
         if (L.fast) {
             a.part = w.part.ptr<double>() + (size_t)(k - 1) * grid * 2;
             a.hub_part = w.hub_part.ptr<double>();
@@ -196,10 +202,13 @@ void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::ve
     if (tr || total || errs) {
         std::vector<double> t(2 * (size_t)std::max(s.M, 1));
         double tot = 0.0;
-        if (s.M > 0)
+        std::vector<unsigned long long> stamps((size_t)s.M + 1, 0);
+        if (s.M > 0) {
             CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), w.trace.get(), sizeof(double) * 2 * s.M,
                                             cudaMemcpyDeviceToHost, st));
-        else
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(stamps.data(), w.stamps.get(), sizeof(unsigned long long) * (s.M + 1),
+                                            cudaMemcpyDeviceToHost, st));
+        } else
             CHEB_CUDA_CHECK(cudaMemcpyAsync(&tot, w.total.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
         if (errs && h_ref) {
             errs->assign(2 * (size_t)std::max(s.M, 1), 0.0);
@@ -211,6 +220,10 @@ void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::ve
         float ms = 0.f;
         CHEB_CUDA_CHECK(cudaEventElapsedTime(&ms, g->ev0, g->ev1));
         g->last_loop_ms = ms;
+        g->term_elapsed_ms.assign((size_t)s.M, 0.0);
+        for (int k = 1; k <= s.M; ++k)
+            g->term_elapsed_ms[(size_t)k - 1] = stamps[(size_t)k] > stamps[(size_t)k - 1]
+                                                    ? (double)(stamps[(size_t)k] - stamps[(size_t)k - 1]) * 1e-6 : 0.0;
         // first non-finite round wins (cpaa.cpp:147-148)
         for (int k = 1; k <= s.M; ++k)
             if (!std::isfinite(t[2 * (k - 1)]) || !std::isfinite(t[2 * (k - 1) + 1]))
@@ -229,6 +242,7 @@ void run_solve_t(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::ve
 void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool /*host_results*/, std::vector<double>* tr,
                 double* total) {
     GraphScope gs(g);
+    g->term_elapsed_ms.clear();
     if (s.R != 1) fail(CHEB_INVALID_ARG, "R > 1 is served by the batched path");
     if (s.mode == CHEB_MODE_BITEXACT && s.precision != CHEB_FP64)
         fail(CHEB_INVALID_ARG, "bitexact mode is fp64 only");
@@ -246,6 +260,7 @@ void cpaa_solve(cheb_graph* g, const SolveSpec& s, bool /*host_results*/, std::v
 void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
                     std::vector<double>* errs, double* total) {
     GraphScope gs(g);
+    g->term_elapsed_ms.clear();
     const bool rp64 = s.mode == CHEB_MODE_FAST ? (ensure_view(g), g->view.rp64) : g->rp64;
     if (s.precision == CHEB_FP64) {
         if (rp64) run_solve_t<int64_t, double>(g, s, h_ref, tr, errs, total);

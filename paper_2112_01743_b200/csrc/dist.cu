@@ -42,11 +42,6 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 // Wait for slot r of this rank's flags to reach epoch; give up after 20 s and raise the
 // group's timeout flag (slot G) instead of hanging the GPU if a peer never signals.
 __device__ __forceinline__ void wait_epoch(const unsigned long long* flags, int r, int G, unsigned long long epoch) {

@@ -10,10 +10,6 @@
 // A warp walks the view's tiles; lane l owns columns [l*VPL, l*VPL+VPL).  Rows with
 // degree > kWarpNnz are split into chunk tiles whose R-vector partials are combined in
 // chunk order by k_spmm_hub_finalize (deterministic, no atomics).
-// No x_{k+1} = T_{k+1} D^-1 block is stored: the term gathers T_k rows and scales each
-// gathered row by its vertex's 1/deg (xinv, the epilogue's own rcp_rn(deg) per vertex), so
-// every summand is bitwise the x_k value the reference pre-scale produces
-// (cpaa.cpp:116) while the n x R x_{k+1} write stream (and its buffer) disappears.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -29,8 +25,8 @@ struct BatchArgs {
     const RP* __restrict__ rp;
     const int* __restrict__ col;
     const double* __restrict__ inv;
-    const V* __restrict__ x_in;   // T_k (gathered rows; scaled by xinv at the gather)
-    const V* __restrict__ xinv;   // [n] 1/deg of every vertex (or the non-canonical inv_degree)
+    const V* __restrict__ x_in;
+    V* __restrict__ x_out;
     V* T;
     V* acc;
     double ck;
@@ -40,7 +36,7 @@ struct BatchArgs {
     double* part;      // [grid][2]
     double* hub_part;  // [n_tiles][Rs]
     double* hub_ts;    // [n_hub][2]
-    int hub_rows;      // rows [0, hub_rows) of T are gathered (and stored) under an L2 evict-last policy
+    int hub_rows;      // rows [0, hub_rows) of X are gathered under an L2 evict-last policy
 };
 
 template <class V, int VPL>
@@ -104,12 +100,6 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
-}
-__device__ __forceinline__ void st_policy(double* p, double v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_policy(float* p, float v, uint64_t pol) {
-    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(v), "l"(pol) : "memory");
 }
 template <class V, int VPL>
 struct PolicyIO;
@@ -178,16 +168,10 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
 #pragma unroll
         for (int q = 0; q < U; ++q) c[q] = __ldg(a.col + j + q);
         if (live) {
-            V v[U][VPL], iv[U];
-#pragma unroll
-            for (int q = 0; q < U; ++q) {
-                PolicyIO<V, VPL>::ld(a.x_in + (int64_t)c[q] * a.Rs + off, v[q], c[q] < a.hub_rows ? p_hub : p_cold);
-                iv[q] = __ldg(a.xinv + c[q]);
-            }
+            V v[U][VPL];
 #pragma unroll
             for (int q = 0; q < U; ++q)
-#pragma unroll
-                for (int k = 0; k < VPL; ++k) v[q][k] = mul_rn(v[q][k], iv[q]);  // = x_k[c] bitwise
+                PolicyIO<V, VPL>::ld(a.x_in + (int64_t)c[q] * a.Rs + off, v[q], c[q] < a.hub_rows ? p_hub : p_cold);
             if constexpr (sizeof(V) == 8) {
 #pragma unroll
                 for (int q = 0; q < U; ++q)
@@ -212,9 +196,6 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
         if (live) {
             V v0[VPL];
             PolicyIO<V, VPL>::ld(a.x_in + (int64_t)c0 * a.Rs + off, v0, c0 < a.hub_rows ? p_hub : p_cold);
-            const V iv0 = __ldg(a.xinv + c0);
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) v0[k] = mul_rn(v0[k], iv0);
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
                 if constexpr (sizeof(V) == 8) s[k] += v0[k];
@@ -230,8 +211,8 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
 
 // Streaming (evict-first) access to the T / acc blocks: each is touched once per term and
 // re-read only a term or two later (GBs of traffic in between), so keeping them out of L2
-// leaves room for the gathered rows.  The T_{k+1} rows of the hub prefix (the next term's
-// most-gathered rows) are stored under an evict-last policy instead.
+// leaves room for the gathered x rows.  x_out (the next term's gather source) keeps the
+// normal policy.
 #ifndef CHEB_SPMM_HINTS
 #define CHEB_SPMM_HINTS 1
 #endif
@@ -298,28 +279,24 @@ struct StreamIO<float, 4> {
 template <class RP, class V, int VPL>
 __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_t u, int64_t deg, int lane,
                                                const double (&s)[VPL], double& p0, double& p1) {
-    (void)deg;
+    const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
     const int c0 = lane * VPL;
     const int64_t i0 = u * a.Rs + c0;
     if (c0 + VPL <= a.R) {  // all of the lane's columns live: vector I/O
-        V tp[VPL], ac[VPL], t[VPL], na[VPL];
+        V tp[VPL], ac[VPL], t[VPL], na[VPL], xo[VPL];
         if (!a.first) StreamIO<V, VPL>::ld(a.T + i0, tp);
         StreamIO<V, VPL>::ld(a.acc + i0, ac);
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
             t[k] = a.first ? (V)s[k] : sub_rn(mul_rn(V(2), (V)s[k]), tp[k]);
             na[k] = add_rn(ac[k], mul_rn((V)a.ck, t[k]));
+            xo[k] = mul_rn(t[k], inv);
             p0 += (double)t[k];
             p1 += (double)na[k];
         }
-        if (u < a.hub_rows) {
-            const uint64_t pol = policy_evict_last();
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) st_policy(a.T + i0 + k, t[k], pol);
-        } else {
-            StreamIO<V, VPL>::st(a.T + i0, t, true);
-        }
+        StreamIO<V, VPL>::st(a.T + i0, t, true);
         StreamIO<V, VPL>::st(a.acc + i0, na, true);
+        StreamIO<V, VPL>::st(a.x_out + i0, xo, false);
         return;
     }
 #pragma unroll
@@ -331,6 +308,7 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_
         a.T[i] = t;
         const V nacc = add_rn(a.acc[i], mul_rn((V)a.ck, t));
         a.acc[i] = nacc;
+        a.x_out[i] = mul_rn(t, inv);
         p0 += (double)t;
         p1 += (double)nacc;
     }
@@ -429,18 +407,9 @@ __global__ void k_spmm_init(const RP* __restrict__ rp, const double* __restrict_
         T0[i] = t0;
         T1[i] = t0;
         acc[i] = (p || seed_new) ? mul_rn((V)half_c0, t0) : (c < R ? (V)half_c0 : V(0));
-        if (x0) {
-            const V iv = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
-            x0[i] = mul_rn(t0, iv);
-        }
+        const V iv = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
+        x0[i] = mul_rn(t0, iv);
     }
-}
-
-// 1/deg of every (view) vertex in the solve precision, exactly the epilogue's reciprocal.
-template <class RP, class V>
-__global__ void k_xinv(const RP* __restrict__ rp, const double* __restrict__ inv, int64_t n, V* __restrict__ out) {
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
-        out[u] = inv ? (V)inv[u] : rcp_rn((V)(rp[u + 1] - rp[u]));
 }
 
 // Column sums of acc (deterministic): block b sums rows [b*chunk, ...) per column.
@@ -518,7 +487,6 @@ __global__ void k_trace_reduce_b(const double* __restrict__ part, int grid, cons
 namespace {
 
 inline int vpl_for(int R) { return R <= 32 ? 1 : (R <= 64 ? 2 : 4); }
-inline int grid1d_b(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16)); }
 
 template <class RP, class V, int VPL>
 void batch_run(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace, std::vector<double>& totals,
@@ -533,9 +501,8 @@ void batch_run(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace, st
     const int grid = 148 * 8;
     w.T0.ensure(sizeof(V) * elems);
     w.T1.ensure(sizeof(V) * elems);
-    w.X0.release();  // no x block: the term gathers T_k rows (scaled by xinv)
-    w.X1.release();
-    w.xinv.ensure(sizeof(V) * (size_t)std::max<int64_t>(n, 1));
+    w.X0.ensure(sizeof(V) * elems);
+    w.X1.ensure(sizeof(V) * elems);
     w.acc.ensure(sizeof(V) * elems);
     w.out.ensure(sizeof(double) * (size_t)n * R);
     w.part.ensure(sizeof(double) * 2 * grid);
@@ -566,6 +533,7 @@ void batch_run(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace, st
     const RP* rp = Vw.row_ptr.ptr<RP>();
     const double* inv = g->inv_array ? Vw.inv.ptr<double>() : nullptr;
     V* T[2] = {w.T0.ptr<V>(), w.T1.ptr<V>()};
+    V* X[2] = {w.X0.ptr<V>(), w.X1.ptr<V>()};
     std::vector<cudaEvent_t> ev;
     if (term_ms) {
         ev.resize(2 * (size_t)std::max(M, 1));
@@ -573,18 +541,16 @@ void batch_run(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace, st
     }
     if (s.record_start) CHEB_CUDA_CHECK(cudaEventRecord(g->ev0, st));
     k_spmm_init<RP, V><<<1184, 256, 0, st>>>(rp, inv, d_p.ptr<double>(), d_seed_new.ptr<int64_t>(), n, R, Rs,
-                                             c0 / 2.0, T[0], T[1], w.acc.ptr<V>(), nullptr, Vw.order.ptr<int>());
+                                             c0 / 2.0, T[0], T[1], w.acc.ptr<V>(), X[0], Vw.order.ptr<int>());
     CHEB_CUDA_CHECK(cudaGetLastError());
-    k_xinv<RP, V><<<grid1d_b(n), 256, 0, st>>>(rp, inv, n, w.xinv.ptr<V>());
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    int launches = 2;
+    int launches = 1;
     for (int k = 1; k <= M; ++k) {
         BatchArgs<RP, V> a{};
         a.rp = rp;
         a.col = w.col ? w.col : Vw.col.ptr<int>();
         a.inv = inv;
-        a.x_in = T[k & 1];  // T_k (T[(k - 1) & 1] holds T_{k-1} and receives T_{k+1})
-        a.xinv = w.xinv.ptr<V>();
+        a.x_in = X[(k - 1) & 1];
+        a.x_out = X[k & 1];
         a.T = T[(k - 1) & 1];
         a.acc = w.acc.ptr<V>();
         a.ck = co[k];
@@ -678,9 +644,9 @@ void cpaa_batch_solve(cheb_graph* g, const BatchSpec& s, std::vector<double>& tr
     GraphScope gs(g);
     if (s.R < 1 || s.R > 128) fail(CHEB_INVALID_ARG, "batched solve supports 1 <= R <= 128");
     ensure_view(g);
-    {   // the gathered block (n x Rs) larger than L2: the batched path gathers through its own
-        // ascending-id copy of the view's columns, so a row's gathers walk memory in order
-        // (config 5: 259 -> 252 ms/solve) while the scalar schedule's bits stay untouched
+    {   // the gathered block X (n x Rs) larger than L2: the batched path gathers through its
+        // own ascending-id copy of the view's columns, so a row's X gathers walk memory in
+        // order (config 5: 259 -> 252 ms/solve) while the scalar schedule's bits stay untouched
         const int vpl = vpl_for(s.R);
         const int64_t x_bytes = g->n * (int64_t)((s.R + vpl - 1) / vpl * vpl) *
                                 (s.precision == CHEB_FP64 ? 8 : 4);

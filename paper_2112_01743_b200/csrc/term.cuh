@@ -75,6 +75,7 @@ struct TermArgs {
     double* hub_part;  // [n_tiles] chunk partials
     double* hub_ts;  // [n_hub][2] this term
     int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
+    int prefetch;       // > 0: tile i + prefetch's column ids and row operands are prefetched into L2
     int tune_skip;      // experiments only: 1 skip chunk tiles, 2 skip pack tiles, 16+b only bin b
     int stream_cs;      // per-row operands loaded / stored with the streaming (.cs) policy
     int xout_hint;      // x_{k+1} store policy (tuning().xout_hint)
@@ -85,7 +86,26 @@ struct TermArgs {
     int push_n;
     int64_t push_off;
     const unsigned* push_mask;  // halo-only push: bit r = rank r reads x[u] (null: every rank)
+    // per-term device clock (TraceRow::elapsed_ms): the first term stamps its start, the last
+    // CTA of the term's final kernel stamps its end
+    unsigned long long* stamp_start;
+    unsigned long long* stamp_end;
+    unsigned* done;
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// The last CTA of the grid to get here records the time (the kernel's end, to within one CTA).
+__device__ __forceinline__ void stamp_last_cta(unsigned* done, unsigned long long* stamp) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(done, 1u) == gridDim.x - 1) *stamp = global_ns();
+    }
+}
 
 // Row epilogue.  u is a row of the current layout; deg its row length.
 template <int EPI, class RP, class V>
@@ -419,6 +439,25 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
         if (lane == 0) issue_cols(a.col, dn, ws.colb[j & 1], &ws.colm[j & 1]);
         load_rows<EPI>(a, dn, nxt);
     }
+    // L2 prefetch of a tile further ahead (its descriptor lives in the current or the next
+    // block of the ring): the per-warp double buffer keeps ~1 tile of column ids in flight,
+    // too few bytes to cover DRAM latency on graphs whose streams miss L2 (config 4)
+    if (a.prefetch > 0 && i + a.prefetch < nt && lane < 4) {
+        const int j = i + a.prefetch;
+        if ((j / kDescBlock) <= (i / kDescBlock) + 1) {
+            if ((j / kDescBlock) != (i / kDescBlock)) mbar_wait(&ws.descm[(j / kDescBlock) & 1], ((j / kDescBlock) >> 1) & 1);
+            const TileR dp = tile_of(ws.desc[(j / kDescBlock) & 1][j % kDescBlock]);
+            if (lane == 0) {
+                const int64_t a0 = dp.z0 & ~int64_t(3);
+                const unsigned bytes = (unsigned)(((dp.z0 - a0) + dp.cnt + 3) & ~3) * 4u;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(a.col + a0), "r"(bytes) : "memory");
+            } else if (!(dp.meta & kTileChunk)) {  // row pointers, T_{k-1}, acc of its rows
+                const void* p = lane == 1 ? (const void*)(a.rp + dp.r0)
+                                          : lane == 2 ? (const void*)(prev_src<EPI>(a) + dp.r0) : (const void*)(a.acc + dp.r0);
+                if (EPI == EPI_CPAA || lane == 1) asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+            }
+        }
+    }
     const int t = w + i * S;  // tile id (slot of a hub-row partial)
     mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
     if (a.tune_skip &&
@@ -535,6 +574,7 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
         if (nt > kDescBlock) issue_desc(my, 1, nullptr, ws.desc[1], &ws.descm[1]);
     }
     pdl_wait();  // x_k, T, acc come from the previous kernels of the stream
+    if (a.stamp_start && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp_start = global_ns();
     if (a.xdiscard_len > 0) {
         // x_out holds x_{k-1}, dead once the previous term finished: drop its lines from L2
         // (no write-back) so they do not hold cache space (or the persisting carve-out)
@@ -590,6 +630,7 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
             }
         }
     }
+    if (a.stamp_end) stamp_last_cta(a.done, a.stamp_end);
 }
 
 // Hub rows (degree > kWarpNnz, rows [0, n_hub) of the view): one warp per row sums the
@@ -619,11 +660,13 @@ __global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const i
             }
         }
     }
+    if (a.stamp_end) stamp_last_cta(a.done, a.stamp_end);
 }
 
 // ---------------- BITEXACT: thread per row, storage order ----------------------------
 template <int EPI, class RP>
 __global__ void __launch_bounds__(kThreads) k_term_exact(TermArgs<RP, double> a, int64_t n) {
+    if (a.stamp_start && blockIdx.x == 0 && threadIdx.x == 0) *a.stamp_start = global_ns();
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
          u += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = a.rp[u], e = a.rp[u + 1];
@@ -632,6 +675,7 @@ __global__ void __launch_bounds__(kThreads) k_term_exact(TermArgs<RP, double> a,
         double p0 = 0.0, p1 = 0.0;
         epilogue<EPI>(a, u, s, e - b, p0, p1);
     }
+    if (a.stamp_end) stamp_last_cta(a.done, a.stamp_end);
 }
 
 // Serial Kahan sums exactly as graph.cpp:10-19 (single thread: bit-identical order).
@@ -1008,7 +1052,9 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         TermArgs<RP, V> ab = a;
         ab.tune_nogather = tuning().nogather;
         ab.tune_skip = tuning().skip;
+        ab.prefetch = tuning().prefetch;
         ab.stream_cs = tuning().streamcs;
+        if (g->view.n_hub > 0) ab.stamp_end = nullptr;  // the hub finalize ends the term
         ab.xout_hint = tuning().xout_hint;
         if (ab.xout_hint < 0) {  // x_{k+1} lines kept in L2 for the next term when x exceeds it
             int l2 = 0;
@@ -1071,7 +1117,7 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     // Any reallocation invalidates the captured solve graph (it bakes in addresses).
     const void* before[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
                             w.part.get(), w.hub_part.get(), w.hub_ts.get(),
-                            w.trace.get(), w.total.get()};
+                            w.trace.get(), w.total.get(), w.stamps.get(), w.done.get()};
     const int64_t vlen = std::max<int64_t>(std::max<int64_t>(n, g->view.x_len), 1);
     const size_t vb = sizeof(V) * (size_t)vlen * R;
     w.T0.ensure(vb);
@@ -1086,12 +1132,14 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     w.hub_ts.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max<int64_t>(g->view.n_hub, 1));
     w.trace.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1));
     w.total.ensure(sizeof(double) * 4);
+    w.stamps.ensure(sizeof(unsigned long long) * ((size_t)std::max(M, 1) + 1));
+    w.done.ensure(sizeof(unsigned) * ((size_t)std::max(M, 1) + 1));
     w.n = n;
     w.R = R;
     w.vbytes = sizeof(V);
     const void* after[] = {w.T0.get(), w.T1.get(), w.X0.get(), w.X1.get(), w.acc.get(), w.out.get(),
                            w.part.get(), w.hub_part.get(), w.hub_ts.get(),
-                           w.trace.get(), w.total.get()};
+                           w.trace.get(), w.total.get(), w.stamps.get(), w.done.get()};
     if (std::memcmp(before, after, sizeof before) != 0) {
         if (w.exec) cudaGraphExecDestroy(w.exec);
         w.exec = nullptr;

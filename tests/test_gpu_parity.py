@@ -502,3 +502,24 @@ def test_bank_aware_chunk_order_is_a_reassociation(cheb):
     assert np.max(np.abs(runs[1] - runs[0])) <= TOL64
     top = lambda r: np.argsort(-r, kind="stable")[:100]  # noqa: E731
     assert np.array_equal(top(runs[1]), top(runs[0]))
+
+
+@pytest.mark.parametrize("mode", ["fast", "bitexact"])
+def test_trace_elapsed_is_per_term_device_time(cheb, mode):
+    """TraceRow::elapsed_ms is each term's own device time (%globaltimer stamps at the term
+    boundaries inside the solve, graph replay included), not the loop mean: positive,
+    finite, and summing to no more than the solve's device loop."""
+    import ctypes as C
+    from paper_2112_01743_b200 import _lib as L
+    z = load_golden("config1")
+    dg, _ = cheb.build_device_graph(z["edges"])
+    cfg = cheb.SolverConfig(eps=1e-10, mode=cheb.MODE_FAST if mode == "fast" else cheb.MODE_BITEXACT)
+    for _ in range(3):  # plain launches, then a captured graph, then a replay
+        r = cheb.run_cpaa(dg, cfg)
+        el = np.array([t.elapsed_ms for t in r.trace])
+        assert el.size == 39 and np.all(np.isfinite(el)) and np.all(el > 0), el
+        lm = C.c_double()
+        assert L.load().cheb_last_timing(dg.handle, C.byref(lm), None, None, None) == 0
+        assert el.sum() <= lm.value * 1.05 + 0.05, (el.sum(), lm.value)
+        assert len(set(np.round(el, 9))) > 1  # not one mean repeated
+    dg.free()

@@ -17,7 +17,7 @@ dg, info = bench.build_device(bench.CONFIGS[cfg], 0)
 opts = L.cheb_cpaa_opts()
 lib.cheb_cpaa_opts_default(C.byref(opts))
 opts.eps = 1e-10
-DEFAULTS = {"hot": -1, "l2win": 1, "pdl": 1, "l2win_mb": -1, "l2win_pct": 100, "streamcs": 0, "xout_hint": -1, "xdiscard": 1}
+DEFAULTS = {"hot": -1, "l2win": 1, "pdl": 1, "l2win_mb": -1, "l2win_pct": 100, "streamcs": 0, "xout_hint": -1, "xdiscard": 1, "prefetch": 0, "nogather": 0}
 print(f"{cfg} n={info['n']} nnz={info['nnz']}", flush=True)
 
 
@@ -36,5 +36,8 @@ def run(label, **kv):
 
 
 run("default")
-run("x_out plain", xout_hint=0)
-run("no discard", xdiscard=0)
+for P in (2, 3, 4, 6):
+    run(f"prefetch {P}", prefetch=P)
+run("nogather", nogather=1)
+for P in (2, 4):
+    run(f"nogather prefetch {P}", nogather=1, prefetch=P)
