@@ -182,6 +182,12 @@ cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, 
  * x_{k+1} stores of the halo-only push (a row's value goes only to the ranks owning one of
  * its neighbours) and of replicate-to-every-rank ((G - 1) per local row). */
 cheb_status cheb_graph_exchange_info(cheb_graph_t g, int64_t* halo_stores, int64_t* all_stores);
+/* Solver-view introspection (new; tests and tools): sizes[5] = {n_local, nnz_local, n_hub,
+ * n_chunk_tiles, hot-prefix capacity (fp64 entries)}; row_ptr[n_local + 1] (widened), col[nnz_local]
+ * (renamed ids in storage order), order[n_local] (view row -> vertex), chunk_begin[n_chunk_tiles + 1]
+ * (first entry of every hub-row chunk tile).  Any output may be NULL. */
+cheb_status cheb_graph_view_download(cheb_graph_t g, int64_t* sizes, int64_t* row_ptr, int32_t* col,
+                                     int32_t* order, int64_t* chunk_begin);
 
 /* ---- solvers ---- */
 enum { CHEB_MODE_FAST = 0, CHEB_MODE_BITEXACT = 1 };

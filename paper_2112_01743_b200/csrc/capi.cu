@@ -1021,6 +1021,49 @@ cheb_status cheb_graph_view_bins(cheb_graph_t g, int64_t* tiles, int64_t* rows, 
     });
 }
 
+cheb_status cheb_graph_view_download(cheb_graph_t g, int64_t* sizes, int64_t* row_ptr, int32_t* col,
+                                     int32_t* order, int64_t* chunk_begin) {
+    return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_view_download");
+        need_graph(g);
+        GraphScope gs(g);
+        ensure_view(g);
+        const SolverView& V = g->view;
+        if (sizes) {
+            sizes[0] = V.n_local;
+            sizes[1] = V.nnz_local;
+            sizes[2] = V.n_hub;
+            sizes[3] = V.n_chunk_tiles;
+            sizes[4] = kHotBytes / 8;
+        }
+        cudaStream_t st = g->stream;
+        if (row_ptr) {
+            std::vector<int32_t> r32;
+            if (V.rp64) {
+                CHEB_CUDA_CHECK(cudaMemcpyAsync(row_ptr, V.row_ptr.get(), sizeof(int64_t) * (V.n_local + 1),
+                                                cudaMemcpyDeviceToHost, st));
+            } else {
+                r32.resize((size_t)V.n_local + 1);
+                CHEB_CUDA_CHECK(cudaMemcpyAsync(r32.data(), V.row_ptr.get(), sizeof(int32_t) * (V.n_local + 1),
+                                                cudaMemcpyDeviceToHost, st));
+            }
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+            for (size_t i = 0; i < r32.size(); ++i) row_ptr[i] = r32[i];
+        }
+        if (col && V.nnz_local > 0)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(col, V.col.get(), sizeof(int32_t) * V.nnz_local, cudaMemcpyDeviceToHost, st));
+        if (order && V.n_local > 0)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(order, V.order.get(), sizeof(int32_t) * V.n_local, cudaMemcpyDeviceToHost, st));
+        if (chunk_begin && V.n_chunk_tiles > 0) {
+            std::vector<Tile> t((size_t)V.n_chunk_tiles + 1);
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), V.tiles.get(), sizeof(Tile) * t.size(), cudaMemcpyDeviceToHost, st));
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+            for (size_t i = 0; i < t.size(); ++i) chunk_begin[i] = t[i].nnz_begin;
+        }
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
 cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, int64_t* nnz_local,
                                       int64_t* max_rows) {
     return guarded([&] {

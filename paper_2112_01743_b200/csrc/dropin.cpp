@@ -60,6 +60,10 @@ void check_gen(cheb_status s) {
 struct Device {
     cheb_graph_t h = nullptr;
     Device(const UndirectedGraph& g, int device) {
+        // the C-ABI reads a null inv_degree as "canonical 1/deg"; the reference's
+        // essential_check (cpaa.cpp:18-22) rejects a graph whose inv_degree is missing
+        if (g.n >= 1 && g.inv_degree.size() != static_cast<size_t>(g.n))
+            throw ValidationError("inconsistent graph arrays");
         check(cheb_graph_upload_csr(g.offsets.data(), (int64_t)g.offsets.size(), g.neighbors.data(),
                                     (int64_t)g.neighbors.size(), g.degrees.data(), (int64_t)g.degrees.size(),
                                     g.inv_degree.data(), (int64_t)g.inv_degree.size(), g.n, g.m,

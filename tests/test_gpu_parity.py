@@ -504,6 +504,62 @@ def test_bank_aware_chunk_order_is_a_reassociation(cheb):
     assert np.array_equal(top(runs[1]), top(runs[0]))
 
 
+def _view(lib, dg):
+    import ctypes as C
+    sizes = np.zeros(5, dtype=np.int64)
+    P64 = C.POINTER(C.c_int64)
+    assert lib.cheb_graph_view_download(dg.handle, sizes.ctypes.data_as(P64), None, None, None, None) == 0
+    nl, nnz, n_hub, nct, H = (int(v) for v in sizes)
+    rp = np.zeros(nl + 1, dtype=np.int64)
+    col = np.zeros(nnz, dtype=np.int32)
+    order = np.zeros(nl, dtype=np.int32)
+    cb = np.zeros(nct + 1, dtype=np.int64)
+    P32 = C.POINTER(C.c_int32)
+    assert lib.cheb_graph_view_download(dg.handle, sizes.ctypes.data_as(P64), rp.ctypes.data_as(P64),
+                                        col.ctypes.data_as(P32), order.ctypes.data_as(P32),
+                                        cb.ctypes.data_as(P64)) == 0
+    return dict(rp=rp, col=col, order=order, chunks=cb, n_hub=n_hub, H=H)
+
+
+def test_bank_aware_chunk_order_permutes_each_chunk(cheb):
+    """The bank-aware chunk schedule (k_permute_chunks) is a real per-chunk permutation: each
+    hub-row chunk holds the same multiset of ids with and without it, some chunks are
+    reordered, and where reordered each half-warp window of 16 positions reads its hot-prefix
+    ids (< H) from distinct bank pairs (id mod 16).  Rows, row pointers and the relabel are
+    identical."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    e = Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 5000.0, 600_000, 5)
+    views = {}
+    try:
+        for sched in (1, 0):
+            assert lib.cheb_set_tuning(b"chunksched", sched) == 0
+            dg, _ = cheb.build_device_graph(e)
+            views[sched] = _view(lib, dg)
+            dg.free()
+    finally:
+        lib.cheb_set_tuning(b"chunksched", 1)
+    a, b = views[1], views[0]
+    assert np.array_equal(a["rp"], b["rp"]) and np.array_equal(a["order"], b["order"])
+    assert np.array_equal(a["chunks"], b["chunks"]) and a["chunks"].size > 1
+    hub_end = int(a["rp"][a["n_hub"]])
+    assert np.array_equal(a["col"][hub_end:], b["col"][hub_end:])  # pack rows untouched
+    H = a["H"]
+    reordered = 0
+    for t in range(a["chunks"].size - 1):
+        z0, z1 = int(a["chunks"][t]), int(a["chunks"][t + 1])
+        ca, cb = a["col"][z0:z1], b["col"][z0:z1]
+        assert np.array_equal(np.sort(ca), np.sort(cb)), t
+        if not np.array_equal(ca, cb):
+            reordered += 1
+            for w0 in range(0, z1 - z0, 16):
+                win = ca[w0:w0 + 16]
+                hot = win[win < H]
+                assert np.unique(hot & 15).size == hot.size, (t, w0)
+    assert reordered > 0
+
+
 @pytest.mark.parametrize("mode", ["fast", "bitexact"])
 def test_trace_elapsed_is_per_term_device_time(cheb, mode):
     """TraceRow::elapsed_ms is each term's own device time (%globaltimer stamps at the term
