@@ -315,6 +315,10 @@ cheb_status cheb_group_create(cheb_graph_t* graphs, int G, cheb_group_t* out);
  * as cheb_cpaa.  FAST mode, no reference tracking. */
 cheb_status cheb_group_cpaa(cheb_group_t grp, const cheb_cpaa_opts* opts, double* ranks,
                             cheb_trace_row* trace, int* rounds, double* total);
+/* Per-rank balance of a lockstep group (new): the same solve with the ranks' term kernels
+ * serialised (rank r's term after rank r-1's), so each rank's mean term time (ms, CUDA events)
+ * is measured on the whole GPU; rank_term_ms[G]. */
+cheb_status cheb_group_profile(cheb_group_t grp, const cheb_cpaa_opts* opts, double* rank_term_ms, int capacity);
 void cheb_group_destroy(cheb_group_t grp); /* detaches the graphs (they become single-GPU) */
 /* One process per GPU: make g rank `rank` of G and write its exchange-buffer IPC handles
  * (CHEB_PEER_EXPORT_BYTES) to out; gather every rank's bytes (rank order) and pass them to

@@ -112,6 +112,7 @@ _SIGS = {
     "cheb_group_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p)]),
     "cheb_group_cpaa": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), F64P, C.POINTER(cheb_trace_row), IP,
                                   F64P]),
+    "cheb_group_profile": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), F64P, C.c_int]),
     "cheb_group_destroy": (None, [C.c_void_p]),
     "cheb_graph_view_bins": (C.c_int, [C.c_void_p, I64P, I64P, I64P]),
     "cheb_peer_export": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),

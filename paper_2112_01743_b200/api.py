@@ -533,6 +533,15 @@ class PartitionGroup:
         _check(_lib().cheb_group_cpaa(self._h, C.byref(o), _pd(ranks), tr, C.byref(rounds), C.byref(total)))
         return PageRankResult(ranks, _trace_rows(tr, rounds.value), rounds.value, False, total.value)
 
+    def rank_term_ms(self, cfg: Optional[SolverConfig] = None) -> np.ndarray:
+        """Mean term time of every rank's partition, the ranks' term kernels serialised so
+        each is timed on the whole GPU (cheb_group_profile): the partition's load balance."""
+        cfg = cfg or SolverConfig()
+        o = _cpaa_opts(cfg, None)
+        out = np.zeros(len(self.graphs))
+        _check(_lib().cheb_group_profile(self._h, C.byref(o), _pd(out), out.size))
+        return out
+
     def close(self):
         if self._h:
             _lib().cheb_group_destroy(self._h)

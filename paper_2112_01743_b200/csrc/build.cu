@@ -508,8 +508,21 @@ struct HostNarrow {
     }
 };
 
+// Neighbour data of an upload landing on the device in groups of old rows: group i holds old
+// rows [row_cut[i], row_cut[i + 1]) and is narrowed once ready[i] (upload stream) fires.  The
+// view permutes (and sorts) each group as it lands, overlapping the rest of the copy.
+struct ColGroups {
+    std::vector<int64_t> row_cut;
+    std::vector<cudaEvent_t> ready;
+    ~ColGroups() {
+        for (cudaEvent_t e : ready)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
 template <class RPO, class RPN>
-static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<void()>& before_col);
+static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<void()>& before_col,
+                         const ColGroups* groups = nullptr);
 
 static bool dbg_on() {
     static const bool on = getenv("CHEB_DEBUG_UPLOAD") != nullptr;
@@ -575,6 +588,20 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
         }
     }
     HostNarrow hn;
+    // Large pinned uploads land in groups of old rows (~nnz / 4 entries each), so that the view
+    // permutes and sorts each group while the next one is still being copied.
+    ColGroups groups;
+    const bool view_here = g->part.G == 1 && !g->part.comm && !g->peer && n > 0;
+    if (view_here && !pageable && nnz >= (int64_t(1) << 26)) {
+        constexpr int K = 4;
+        groups.row_cut.assign(K + 1, n);
+        groups.row_cut[0] = 0;
+        for (int i = 1; i < K; ++i)
+            groups.row_cut[i] = std::lower_bound(offsets, offsets + n + 1, nnz * i / K) - offsets;
+        for (int i = 1; i <= K; ++i) groups.row_cut[i] = std::max(groups.row_cut[i], groups.row_cut[i - 1]);
+        groups.ready.assign(K, nullptr);
+        for (auto& e : groups.ready) CHEB_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     if (pageable) {
         hn.start(neighbors, nnz, n, g->col.ptr<int>(), st, g->device);
     } else if (nnz > 0) {
@@ -583,6 +610,7 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
         stage[0].alloc(sizeof(int64_t) * chunk);
         if (chunk < nnz) stage[1].alloc(sizeof(int64_t) * chunk);
         int i = 0;
+        size_t next_group = 0;
         for (int64_t off = 0; off < nnz; off += chunk, i ^= 1) {
             const int64_t c = std::min(chunk, nnz - off);
             CHEB_CUDA_CHECK(cudaMemcpyAsync(stage[i].get(), neighbors + off, sizeof(int64_t) * c,
@@ -590,7 +618,12 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
             k_narrow_col<<<grid_for(c), kBuildThreads, 0, st>>>(stage[i].ptr<int64_t>(), c, n, off,
                                                                  g->col.ptr<int>() + off, bad);
             CHEB_CUDA_CHECK(cudaGetLastError());
+            while (next_group < groups.ready.size() && offsets[groups.row_cut[next_group + 1]] <= off + c)
+                CHEB_CUDA_CHECK(cudaEventRecord(groups.ready[next_group++], st));
         }
+        while (next_group < groups.ready.size()) CHEB_CUDA_CHECK(cudaEventRecord(groups.ready[next_group++], st));
+    } else {
+        for (auto& e : groups.ready) CHEB_CUDA_CHECK(cudaEventRecord(e, st));
     }
     if (!pageable) CHEB_CUDA_CHECK(cudaEventRecord(ev_col, st));
     mark("enqueued copies");
@@ -620,14 +653,15 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
         {
             AllocScope as(g->aux);
             g->view = SolverView{};
+            const bool grouped = !groups.ready.empty();
             auto wait_col = [&] {  // the degree-only half of the view overlapped the narrowing
                 finish_narrowing();
-                CHEB_CUDA_CHECK(cudaStreamWaitEvent(g->aux, ev_col, 0));
+                if (!grouped) CHEB_CUDA_CHECK(cudaStreamWaitEvent(g->aux, ev_col, 0));  // else per group
             };
             if (g->rp64)
-                build_view_t<int64_t, int64_t>(g, g->aux, wait_col);
+                build_view_t<int64_t, int64_t>(g, g->aux, wait_col, grouped ? &groups : nullptr);
             else
-                build_view_t<int, int>(g, g->aux, wait_col);
+                build_view_t<int, int>(g, g->aux, wait_col, grouped ? &groups : nullptr);
         }
         mark("view enqueued");
         if (dbg) { cudaEventSynchronize(ev_col); mark("neighbours landed"); cudaStreamSynchronize(g->aux); mark("view done"); }
@@ -735,13 +769,15 @@ __global__ void k_new_degrees(const RP* __restrict__ rp, const int* __restrict__
 template <int S, class RPO, class RPN>
 __global__ void k_permute_rows(const RPO* __restrict__ rp_old, const int* __restrict__ col_old,
                                const RPN* __restrict__ rp_new, const int* __restrict__ order,
-                               const int* __restrict__ rank, int64_t w0, int64_t w1, int* __restrict__ col_new) {
+                               const int* __restrict__ rank, int64_t w0, int64_t w1, int* __restrict__ col_new,
+                               int64_t oa, int64_t ob) {
     constexpr int kPer = S == 0 ? 1 : (int)(kBuildThreads / (S == 0 ? 1 : S));  // rows per CTA
     const int lane = S == 0 ? (int)threadIdx.x : (int)(threadIdx.x % (S == 0 ? 1 : S));
     const int stride = S == 0 ? (int)blockDim.x : S;
     for (int64_t w = w0 + (int64_t)blockIdx.x * kPer + (S == 0 ? 0 : threadIdx.x / (S == 0 ? 1 : S)); w < w1;
          w += (int64_t)gridDim.x * kPer) {
         const int o = order[w];
+        if (o < oa || o >= ob) continue;  // another group of old rows
         const int64_t b = rp_old[o], e = rp_old[o + 1], d = rp_new[w];
         for (int64_t j = b + lane; j < e; j += stride) col_new[d + (j - b)] = rank[col_old[j]];
     }
@@ -832,7 +868,7 @@ template <class RPO, class RPN>
 __global__ void k_permute_chunks(const Tile* __restrict__ tiles, int n_chunk_tiles, const RPO* __restrict__ rp_old,
                                  const int* __restrict__ col_old, const RPN* __restrict__ rp_new,
                                  const int* __restrict__ order, const int* __restrict__ rank, int H, int sched,
-                                 int* __restrict__ col_new) {
+                                 int* __restrict__ col_new, int64_t oa, int64_t ob) {
     __shared__ SchedScratch scr[8];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < n_chunk_tiles;
@@ -841,6 +877,7 @@ __global__ void k_permute_chunks(const Tile* __restrict__ tiles, int n_chunk_til
         const int64_t z0 = a.nnz_begin;
         const int cnt = (int)(tiles[t + 1].nnz_begin - z0);
         const int h = a.row_begin;
+        if (order[h] < oa || order[h] >= ob) continue;  // warp-uniform: another group of old rows
         const int64_t src = (int64_t)rp_old[order[h]] + (z0 - (int64_t)rp_new[h]);
         int val[8], dst[8];
 #pragma unroll
@@ -999,6 +1036,21 @@ __global__ void k_push_mask(const RPN* __restrict__ rp, const int* __restrict__ 
     if (lane == 0 && halo) atomicAdd(counts, halo);
 }
 
+// View rows whose old row lies in [oa, ob): their [begin, end) entry ranges, appended in
+// any order (each segment is sorted on its own, so the order of the list does not matter).
+template <class RPN>
+__global__ void k_group_segments(const int* __restrict__ order, const RPN* __restrict__ rp, int64_t nl, int64_t oa,
+                                 int64_t ob, int64_t* __restrict__ seg_b, int64_t* __restrict__ seg_e,
+                                 unsigned long long* __restrict__ cnt) {
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nl; w += (int64_t)gridDim.x * blockDim.x) {
+        const int o = order[w];
+        if (o < oa || o >= ob) continue;
+        const unsigned long long i = atomicAdd(cnt, 1ull);
+        seg_b[i] = (int64_t)rp[w];
+        seg_e[i] = (int64_t)rp[w + 1];
+    }
+}
+
 // padded exchange position of every old id: new id u on rank r -> r*max_rows + (u - cuts[r])
 __global__ void k_posmap(const int* __restrict__ rank_of_old, int64_t n, const int64_t* __restrict__ cuts, int G,
                          int64_t max_rows, int* __restrict__ pos) {
@@ -1143,7 +1195,8 @@ static void sort_view_rows_t(SolverView& V, int64_t segs, int64_t items, cudaStr
 }
 
 template <class RPO, class RPN>
-static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<void()>& before_col) {
+static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<void()>& before_col,
+                         const ColGroups* groups) {
     SolverView& V = g->view;
     const int64_t n = g->n;
     TempStore tmp;
@@ -1297,14 +1350,23 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     V.tiles.alloc(sizeof(Tile) * tiles.size());
     h2d_staged(V.tiles.get(), tiles.data(), sizeof(Tile) * tiles.size(), 2, st);
     V.col.alloc(sizeof(int) * std::max<int64_t>(nnz_l, 1) + 64);  // TMA reads round up to 16 B
-    if (before_col) before_col();
+    // When x does not fit L2 (config 4), ascending renamed ids within each row: a row's
+    // gathers then walk x in address order (DRAM page / sector locality; C4 4.49 -> 3.95
+    // ms/term).  When x fits L2 the storage order is kept (sorting cost C2 ~1%).  The
+    // FAST sums are re-associated either way; results stay within 1e-12.
+    int l2 = 0;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    }
+    const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2) : tuning().sortrows > 0;
+    const bool hubs_only = tuning().sortrows == 2 && V.n_hub > 0;
+    const bool sort_rows = (big_x || hubs_only) && nnz_l > 0 && nnz_l < INT32_MAX;
+    const bool sort_grouped = sort_rows && !hubs_only;  // every row, group by group into V.col
+    V.sorted_rows = sort_grouped;
     if (nl > 0) {
         cudaEvent_t dbg_ev[2] = {};
-        if (dbg_on()) {
-            cudaEventCreate(&dbg_ev[0]);
-            cudaEventCreate(&dbg_ev[1]);
-            cudaEventRecord(dbg_ev[0], st);
-        }
         // rows are degree-descending: hub rows [0, n_hub) by chunk tiles (in bank-aware
         // order), then [n_hub, n_huge) > 1024 entries, [n_huge, n_long) > 16, the rest <= 16
         int64_t n_huge = V.n_hub, n_long = V.n_hub, seen = 0;
@@ -1318,51 +1380,85 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         }
         const int* order_l = V.order.ptr<int>() + lo;
         const RPN* rp_l = V.row_ptr.ptr<RPN>();
-        if (V.n_chunk_tiles > 0)
-            k_permute_chunks<RPO, RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
-                V.tiles.ptr<Tile>(), V.n_chunk_tiles, rp_old, g->col.ptr<int>(), rp_l, order_l, colmap,
-                kHotBytes / 8, tuning().chunksched, V.col.ptr<int>());
-        if (n_huge > V.n_hub)
-            k_permute_rows<0><<<(int)std::min<int64_t>(n_huge - V.n_hub, 148 * 16), kBuildThreads, 0, st>>>(
-                rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, V.n_hub, n_huge, V.col.ptr<int>());
-        if (n_long > n_huge)
-            k_permute_rows<32><<<grid_for((n_long - n_huge) * 32), kBuildThreads, 0, st>>>(
-                rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, n_huge, n_long, V.col.ptr<int>());
-        if (nl > n_long)
-            k_permute_rows<4><<<grid_for((nl - n_long) * 4), kBuildThreads, 0, st>>>(
-                rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, n_long, nl, V.col.ptr<int>());
-        CHEB_CUDA_CHECK(cudaGetLastError());
-        if (dbg_ev[0]) {  // CHEB_DEBUG_UPLOAD: neighbours landed + narrowed, then permuted
+        DevMem perm;  // permute target when the rows are sorted afterwards (sorted into V.col)
+        if (sort_grouped) perm.alloc(sizeof(int) * (size_t)nnz_l + 64);
+        int* dst = sort_grouped ? perm.ptr<int>() : V.col.ptr<int>();
+        const int K = groups ? (int)groups->row_cut.size() - 1 : 1;
+        DevMem seg_b, seg_e, seg_n(sizeof(unsigned long long));
+        TempStore sort_tmp;
+        if (sort_grouped && K > 1) {
+            seg_b.alloc(sizeof(int64_t) * (size_t)nl);
+            seg_e.alloc(sizeof(int64_t) * (size_t)nl);
+        }
+        if (before_col) before_col();
+        if (dbg_on()) {
+            cudaEventCreate(&dbg_ev[0]);
+            cudaEventCreate(&dbg_ev[1]);
+            cudaEventRecord(dbg_ev[0], st);
+        }
+        for (int gi = 0; gi < K; ++gi) {
+            const int64_t oa = groups ? groups->row_cut[gi] : 0;
+            const int64_t ob = groups ? groups->row_cut[gi + 1] : INT64_MAX;
+            if (groups) CHEB_CUDA_CHECK(cudaStreamWaitEvent(st, groups->ready[gi], 0));
+            if (V.n_chunk_tiles > 0)
+                k_permute_chunks<RPO, RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
+                    V.tiles.ptr<Tile>(), V.n_chunk_tiles, rp_old, g->col.ptr<int>(), rp_l, order_l, colmap,
+                    kHotBytes / 8, tuning().chunksched, dst, oa, ob);
+            if (n_huge > V.n_hub)
+                k_permute_rows<0><<<(int)std::min<int64_t>(n_huge - V.n_hub, 148 * 16), kBuildThreads, 0, st>>>(
+                    rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, V.n_hub, n_huge, dst, oa, ob);
+            if (n_long > n_huge)
+                k_permute_rows<32><<<grid_for((n_long - n_huge) * 32), kBuildThreads, 0, st>>>(
+                    rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, n_huge, n_long, dst, oa, ob);
+            if (nl > n_long)
+                k_permute_rows<4><<<grid_for((nl - n_long) * 4), kBuildThreads, 0, st>>>(
+                    rp_old, g->col.ptr<int>(), rp_l, order_l, colmap, n_long, nl, dst, oa, ob);
+            CHEB_CUDA_CHECK(cudaGetLastError());
+            if (!sort_grouped) continue;
+            // this group's rows, ascending ids, from the permute target into V.col
+            size_t bytes = 0;
+            if (K == 1) {
+                CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, dst, V.col.ptr<int>(), (int)nnz_l,
+                                                                   (int)nl, rp_l, rp_l + 1, st));
+                void* t = sort_tmp.get(bytes);
+                CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, dst, V.col.ptr<int>(), (int)nnz_l,
+                                                                   (int)nl, rp_l, rp_l + 1, st));
+            } else {
+                CHEB_CUDA_CHECK(cudaMemsetAsync(seg_n.get(), 0, sizeof(unsigned long long), st));
+                k_group_segments<RPN><<<grid_for(nl), kBuildThreads, 0, st>>>(order_l, rp_l, nl, oa, ob,
+                                                                            seg_b.ptr<int64_t>(), seg_e.ptr<int64_t>(),
+                                                                            seg_n.ptr<unsigned long long>());
+                CHEB_CUDA_CHECK(cudaGetLastError());
+                const int64_t nseg = (int64_t)read_scalar(seg_n.ptr<unsigned long long>(), st);
+                if (nseg == 0) continue;
+                CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, dst, V.col.ptr<int>(), (int)nnz_l,
+                                                                   (int)nseg, seg_b.ptr<int64_t>(), seg_e.ptr<int64_t>(), st));
+                void* t = sort_tmp.get(bytes);
+                CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, dst, V.col.ptr<int>(), (int)nnz_l,
+                                                                   (int)nseg, seg_b.ptr<int64_t>(), seg_e.ptr<int64_t>(), st));
+            }
+        }
+        if (dbg_ev[0]) {  // CHEB_DEBUG_UPLOAD: neighbours landed + narrowed, then permuted (+ sorted)
             cudaEventRecord(dbg_ev[1], st);
             cudaEventSynchronize(dbg_ev[1]);
             float ms = 0.f;
             cudaEventElapsedTime(&ms, dbg_ev[0], dbg_ev[1]);
-            dbg_mark(("  view: columns permuted (permute " + std::to_string(ms) + " ms)").c_str());
+            dbg_mark(("  view: columns permuted/sorted (" + std::to_string(K) + " groups, " + std::to_string(ms) +
+                      " ms after the first)").c_str());
             cudaEventDestroy(dbg_ev[0]);
             cudaEventDestroy(dbg_ev[1]);
         }
-        // When x does not fit L2 (config 4), ascending renamed ids within each row: a row's
-        // gathers then walk x in address order (DRAM page / sector locality; C4 4.49 -> 4.03
-        // ms/term).  When x fits L2 the storage order is kept (sorting cost C2 ~1%).  The
-        // FAST sums are re-associated either way; results stay within 1e-12.
-        int dev = 0, l2 = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-        const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2)
-                                                 : tuning().sortrows > 0;
-        const bool hubs_only = tuning().sortrows == 2 && V.n_hub > 0;
-        const bool sort_rows = (big_x || hubs_only) && nnz_l > 0 && nnz_l < INT32_MAX;
-        V.sorted_rows = sort_rows && !hubs_only;
-        if (sort_rows) {
-            const int64_t segs = hubs_only ? V.n_hub : nl;
-            const int64_t items = hubs_only ? (int64_t)read_scalar(V.row_ptr.ptr<RPN>() + segs, st) : nnz_l;
+        if (sort_rows && hubs_only) {  // experiment: the hub rows only, in place
+            const int64_t segs = V.n_hub;
+            const int64_t items = (int64_t)read_scalar(V.row_ptr.ptr<RPN>() + segs, st);
             sort_view_rows_t<RPN>(V, segs, items, st);
-            if (tuning().chunksched > 1 && V.n_chunk_tiles > 0) {  // the sort undid the chunk order
-                k_schedule_chunks_inplace<RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
-                    V.tiles.ptr<Tile>(), V.n_chunk_tiles, kHotBytes / 8, V.col.ptr<int>());
-                CHEB_CUDA_CHECK(cudaGetLastError());
-            }
         }
+        if (sort_grouped && tuning().chunksched > 1 && V.n_chunk_tiles > 0) {  // the sort undid the chunk order
+            k_schedule_chunks_inplace<RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(
+                V.tiles.ptr<Tile>(), V.n_chunk_tiles, kHotBytes / 8, V.col.ptr<int>());
+            CHEB_CUDA_CHECK(cudaGetLastError());
+        }
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
         if (tuning().packsched && V.n_tiles > V.n_chunk_tiles) {
             const int jobs = 2 * (V.n_tiles - V.n_chunk_tiles);
             k_schedule_pack<RPN><<<std::max(1, std::min((jobs + 127) / 128, 148 * 8)), 128, 0, st>>>(

@@ -937,6 +937,22 @@ cheb_status cheb_group_cpaa(cheb_group_t grp, const cheb_cpaa_opts* opts, double
     });
 }
 
+cheb_status cheb_group_profile(cheb_group_t grp, const cheb_cpaa_opts* opts, double* rank_term_ms, int capacity) {
+    return guarded([&] {
+        NvtxRange nvtx_("cheb_group_profile");
+        if (!grp || grp->graphs.empty()) fail(CHEB_INVALID_ARG, "null group");
+        cheb_graph* g0 = grp->graphs[0];
+        cheb_cpaa_opts o;
+        cheb_cpaa_opts_default(&o);
+        if (opts) o = *opts;
+        SolveSpec s = checked_spec(g0, o, nullptr, 0);
+        std::vector<double> tr, ms;
+        double tot = 0.0;
+        group_solve(grp->graphs, s, &tr, &tot, &ms);
+        for (int r = 0; r < (int)ms.size() && r < capacity; ++r) rank_term_ms[r] = ms[(size_t)r];
+    });
+}
+
 void cheb_group_destroy(cheb_group_t grp) {
     if (!grp) return;
     for (cheb_graph* g : grp->graphs) {
@@ -1108,6 +1124,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "batchblock") tuning().batchblock = std::max(1, std::min(value, 128));
         else if (k == "halo") tuning().halo = value;
         else if (k == "prefetch") tuning().prefetch = value;
+        else if (k == "sortrows") tuning().sortrows = value;
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }

@@ -373,7 +373,7 @@ struct Tuning {
                         // off: no measurable gain (C2 68.8 -> 68.5, C3 381.6 -> 380.2, C4 3953 -> 3950 us/term)
     int batchblock = 128; // right-hand sides per batched pass (column blocks of one call)
     int halo = 1;       // row partition, push exchange: store x_{k+1}[u] only on the ranks that read it
-    int prefetch = 0;   // term kernel: L2 prefetch distance in tiles (0 off)
+    int prefetch = 0;   // term kernel: L2 prefetch distance in tiles (0 off); slower on C2-C4
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -463,7 +463,8 @@ void read_batch_ranks(cheb_graph* g, double* ranks, int R);
 void cpaa_solve_ref(cheb_graph* g, const SolveSpec& s, const double* h_ref, std::vector<double>* tr,
                     std::vector<double>* errs, double* total);
 void read_ranks(cheb_graph* g, int precision, double* ranks);
-void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr, double* total);
+void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr, double* total,
+                 std::vector<double>* rank_ms = nullptr);
 void dist_solve(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, double* total,
                 std::vector<double>* term_ms);  // dist.cu: one rank of a partitioned solve
 void cpaa_profile(cheb_graph* g, const SolveSpec& s, std::vector<double>& term_ms);

@@ -408,14 +408,25 @@ void run_solve_dist(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, 
 // enqueued on every rank's stream, then every rank signals, and each rank's wait kernel is
 // ordered (by events) after all signals — so no kernel ever spins on work that has not been
 // enqueued, and ranks sharing one GPU cannot deadlock.
+// rank_ms (profiling): the ranks' term kernels run one rank at a time (each rank's term waits
+// for the previous rank's term on its own stream), so that every rank's per-term time is
+// measured on the whole GPU with CUDA events — the per-rank load balance of the partition
+// as one GPU per rank would see it (the exchange stores hit local memory here).
 template <class RP, class V>
 void run_group_lockstep(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr,
-                        double* total) {
+                        double* total, std::vector<double>* rank_ms = nullptr) {
     const int G = (int)gs.size();
     std::vector<std::unique_ptr<DistSolve<RP, V>>> d;
-    for (cheb_graph* g : gs) {
-        GraphScope sc(g);
-        d.emplace_back(new DistSolve<RP, V>(g, s, nullptr));
+    std::vector<std::vector<cudaEvent_t>> tev(G);
+    std::vector<cudaEvent_t> term_done(G, nullptr);
+    for (int r = 0; r < G; ++r) {
+        GraphScope sc(gs[r]);
+        if (rank_ms) {
+            tev[r].resize(2 * (size_t)std::max(s.M, 1));
+            for (auto& e : tev[r]) CHEB_CUDA_CHECK(cudaEventCreate(&e));
+            CHEB_CUDA_CHECK(cudaEventCreateWithFlags(&term_done[r], cudaEventDisableTiming));
+        }
+        d.emplace_back(new DistSolve<RP, V>(gs[r], s, rank_ms ? &tev[r] : nullptr));
     }
     auto each = [&](auto&& f) {
         for (int r = 0; r < G; ++r) {
@@ -435,7 +446,16 @@ void run_group_lockstep(const std::vector<cheb_graph*>& gs, const SolveSpec& s, 
     each([](DistSolve<RP, V>& x) { x.begin(); });
     barrier();
     for (int k = 1; k <= s.M; ++k) {
-        each([k](DistSolve<RP, V>& x) { x.term(k); });
+        if (rank_ms) {  // serialised terms: rank r after rank r - 1
+            for (int r = 0; r < G; ++r) {
+                GraphScope sc(gs[r]);
+                if (r > 0) CHEB_CUDA_CHECK(cudaStreamWaitEvent(gs[r]->stream, term_done[r - 1], 0));
+                d[r]->term(k);
+                CHEB_CUDA_CHECK(cudaEventRecord(term_done[r], gs[r]->stream));
+            }
+        } else {
+            each([k](DistSolve<RP, V>& x) { x.term(k); });
+        }
         barrier();
     }
     each([](DistSolve<RP, V>& x) { x.trace_out(); });
@@ -445,6 +465,22 @@ void run_group_lockstep(const std::vector<cheb_graph*>& gs, const SolveSpec& s, 
     for (int r = 0; r < G; ++r) {
         GraphScope sc(gs[r]);
         d[r]->finish(r == 0 ? tr : nullptr, r == 0 ? total : nullptr);
+    }
+    if (rank_ms) {
+        rank_ms->assign(G, 0.0);
+        for (int r = 0; r < G; ++r) {
+            GraphScope sc(gs[r]);
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(gs[r]->stream));
+            double sum = 0.0;
+            for (int k = 0; k < s.M; ++k) {
+                float t = 0.f;
+                CHEB_CUDA_CHECK(cudaEventElapsedTime(&t, tev[r][2 * k], tev[r][2 * k + 1]));
+                sum += t;
+            }
+            (*rank_ms)[r] = s.M > 0 ? sum / s.M : 0.0;
+            for (auto& e : tev[r]) cudaEventDestroy(e);
+            cudaEventDestroy(term_done[r]);
+        }
     }
 }
 
@@ -465,7 +501,8 @@ void dist_solve(cheb_graph* g, const SolveSpec& s, std::vector<double>* tr, doub
 }
 
 // Lockstep solve of a push group (every rank's handle driven by this thread).
-void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr, double* total) {
+void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::vector<double>* tr, double* total,
+                 std::vector<double>* rank_ms) {
     if (s.R != 1) fail(CHEB_INVALID_ARG, "R > 1 is served by the batched path");
     if (s.mode != CHEB_MODE_FAST) fail(CHEB_INVALID_ARG, "a partitioned handle runs the FAST schedule only");
     bool rp64 = false;
@@ -477,11 +514,11 @@ void group_solve(const std::vector<cheb_graph*>& gs, const SolveSpec& s, std::ve
     for (cheb_graph* g : gs)
         if (g->view.rp64 != rp64) fail(CHEB_INVALID_ARG, "group members disagree on row-pointer width");
     if (s.precision == CHEB_FP64) {
-        if (rp64) run_group_lockstep<int64_t, double>(gs, s, tr, total);
-        else run_group_lockstep<int, double>(gs, s, tr, total);
+        if (rp64) run_group_lockstep<int64_t, double>(gs, s, tr, total, rank_ms);
+        else run_group_lockstep<int, double>(gs, s, tr, total, rank_ms);
     } else {
-        if (rp64) run_group_lockstep<int64_t, float>(gs, s, tr, total);
-        else run_group_lockstep<int, float>(gs, s, tr, total);
+        if (rp64) run_group_lockstep<int64_t, float>(gs, s, tr, total, rank_ms);
+        else run_group_lockstep<int, float>(gs, s, tr, total, rank_ms);
     }
 }
 
