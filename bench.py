@@ -787,6 +787,25 @@ def main():
     peak, peak_kind = peaks()
     achieved = B / (term_us * 1e-6) / 1e9
 
+    exchange_info = None
+    if dist.world > 1 and R_cfg == 1:
+        # exchange volume per rank per term: the halo push stores x_{k+1}[u] only on the ranks
+        # that own a neighbour of u; NCCL all-gathers every slot
+        from paper_2112_01743_b200.distributed import partition_info
+        pi = partition_info(dg)
+        vb = 8 if args.precision == 64 else 4
+        if px is not None:
+            sent = dist.max(float(pi["halo_stores"] * vb))
+        else:
+            sent = float((dist.world - 1) * pi["max_rows"] * vb)
+        exchange_info = {"scheme": "fused push, halo-only" if px is not None else "NCCL all-gather",
+                         "partition": "block-cyclic (snake order) over the degree-sorted rows",
+                         "bytes_per_rank_per_term_max": int(sent),
+                         "replicate_all_bytes_per_rank": int(pi["all_stores"] * vb),
+                         "rows_max": int(dist.max(float(pi["rows"]))), "nnz_local_max": int(dist.max(float(pi["nnz_local"]))),
+                         "nvlink_peak_gbs": 770.0,
+                         "nvlink_frac_of_term": round(sent / (term_us * 1e-6) / 770e9, 4)}
+
     comparator = None
     if dist.world == 1 and R == 1 and not args.no_e2e:
         comparator = power_comparator(dg, flush, args.precision)
@@ -839,6 +858,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             **({"power_comparator": comparator} if comparator else {}),
+            **({"exchange": exchange_info} if exchange_info else {}),
             **({"secondary": secondary} if secondary else {}),
             "gpu_launches": launches,
             "clocks": clk_summary,

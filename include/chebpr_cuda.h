@@ -176,6 +176,10 @@ cheb_status cheb_nccl_unique_id(void* out, int out_bytes); /* 128-byte ncclUniqu
 cheb_status cheb_comm_create(const void* unique_id, int nranks, int rank, int device, cheb_comm_t* out);
 void cheb_comm_destroy(cheb_comm_t c);
 cheb_status cheb_graph_attach_comm(cheb_graph_t g, cheb_comm_t comm);
+/* Rows per block of the block-cyclic (snake-order) row partition of a partitioned handle (new):
+ * block b of the degree-sorted rows, cycle c = b / G, goes to rank b mod G on even cycles and
+ * to G - 1 - (b mod G) on odd ones; x stays in the global sorted order on every rank. */
+int cheb_partition_block_rows(void);
 cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, int64_t* nnz_local,
                                       int64_t* max_rows);
 /* Exchange volume of this rank's local rows per term (new; no reference counterpart): remote

@@ -1015,18 +1015,18 @@ __global__ void k_schedule_chunks_inplace(const Tile* __restrict__ tiles, int n_
     }
 }
 
-// Halo masks of a row partition: bit r of mask[u] iff row u has a neighbour in rank r's
-// padded slot [r * max_rows, (r + 1) * max_rows) (column ids are padded positions).  Warp
-// per row; also counts the remote stores per term (halo vs replicate-to-all) in int64.
+// Halo masks of a row partition: bit r of mask[u] iff row u has a neighbour owned by rank r
+// (column ids are global sorted ids, owner = part_owner).  Warp per row; also counts the
+// remote stores per term (halo vs replicate-to-all) in int64.
 template <class RPN>
-__global__ void k_push_mask(const RPN* __restrict__ rp, const int* __restrict__ col, int64_t nl, int64_t max_rows,
+__global__ void k_push_mask(const RPN* __restrict__ rp, const int* __restrict__ col, int64_t nl,
                             int G, int rank, unsigned* __restrict__ mask, unsigned long long* __restrict__ counts) {
     const int lane = threadIdx.x & 31;
     unsigned long long halo = 0;
     for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < nl;
          u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         unsigned m = 0;
-        for (int64_t j = (int64_t)rp[u] + lane; j < (int64_t)rp[u + 1]; j += 32) m |= 1u << (int)(col[j] / max_rows);
+        for (int64_t j = (int64_t)rp[u] + lane; j < (int64_t)rp[u + 1]; j += 32) m |= 1u << part_owner(col[j], G);
         for (int o = 16; o; o >>= 1) m |= __shfl_xor_sync(0xffffffffu, m, o);
         if (lane == 0) {
             mask[u] = m;
@@ -1051,15 +1051,13 @@ __global__ void k_group_segments(const int* __restrict__ order, const RPN* __res
     }
 }
 
-// padded exchange position of every old id: new id u on rank r -> r*max_rows + (u - cuts[r])
-__global__ void k_posmap(const int* __restrict__ rank_of_old, int64_t n, const int64_t* __restrict__ cuts, int G,
-                         int64_t max_rows, int* __restrict__ pos) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t u = rank_of_old[v];
-        int r = 0;
-        while (r + 1 < G && u >= cuts[r + 1]) ++r;
-        pos[v] = (int)(r * max_rows + (u - cuts[r]));
+// This rank's rows of the block-cyclic partition: old ids and degrees of its local rows.
+__global__ void k_gather_local(const int* __restrict__ order_g, const int64_t* __restrict__ deg_g, int64_t nl,
+                               int rank, int G, int* __restrict__ order_l, int64_t* __restrict__ deg_l) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t u = part_global(i, rank, G);
+        order_l[i] = order_g[u];
+        deg_l[i] = deg_g[u];
     }
 }
 
@@ -1223,46 +1221,45 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     k_new_degrees<<<grid_for(n), kBuildThreads, 0, st>>>(rp_old, V.order.ptr<int>(), n, deg_new.ptr<int64_t>());
     CHEB_CUDA_CHECK(cudaGetLastError());
 
-    // Row partition over G ranks: the reference cut rule on the relabelled
-    // degrees; this rank keeps sorted rows [lo, hi) and renames columns to padded slots.
+    // Row partition over G ranks (block-cyclic snake order, common.cuh): this
+    // rank keeps its sorted rows (local row i = sorted row part_global(i, rank, G)); column
+    // ids stay the global sorted ids.
     Partition& P = g->part;
-    DevMem posmap;
     const int* colmap = rank.ptr<int>();
+    DevMem deg_loc;  // this rank's row degrees (G > 1)
+    const int64_t* deg_l = deg_new.ptr<int64_t>();
     if (P.G > 1) {
-        std::vector<int64_t> dh(n);
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(dh.data(), deg_new.get(), sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
-        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
-        P.cuts.assign(P.G + 1, 0);
-        partition_cuts(dh.data(), n, P.G, P.cuts.data());
-        P.max_rows = 0;
-        for (int r = 0; r < P.G; ++r) P.max_rows = std::max(P.max_rows, P.cuts[r + 1] - P.cuts[r]);
-        if (P.G * P.max_rows > INT32_MAX) fail(CHEB_CAPACITY, "padded exchange layout exceeds int32 ids");
-        DevMem dcuts(sizeof(int64_t) * (P.G + 1));
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(dcuts.get(), P.cuts.data(), sizeof(int64_t) * (P.G + 1), cudaMemcpyHostToDevice, st));
-        posmap.alloc(sizeof(int) * n);
-        k_posmap<<<grid_for(n), kBuildThreads, 0, st>>>(rank.ptr<int>(), n, dcuts.ptr<int64_t>(), P.G, P.max_rows,
-                                                        posmap.ptr<int>());
+        P.rows = part_rows(n, P.G);
+        P.max_rows = *std::max_element(P.rows.begin(), P.rows.end());
+        const int64_t nloc = P.rows[(size_t)P.rank];
+        V.order_full = std::move(V.order);
+        V.order.alloc(sizeof(int) * (size_t)std::max<int64_t>(nloc, 1));
+        deg_loc.alloc(sizeof(int64_t) * (size_t)(nloc + 1));
+        CHEB_CUDA_CHECK(cudaMemsetAsync(deg_loc.get(), 0, sizeof(int64_t) * (nloc + 1), st));
+        if (nloc > 0)
+            k_gather_local<<<grid_for(nloc), kBuildThreads, 0, st>>>(V.order_full.ptr<int>(), deg_new.ptr<int64_t>(),
+                                                                      nloc, P.rank, P.G, V.order.ptr<int>(),
+                                                                      deg_loc.ptr<int64_t>());
         CHEB_CUDA_CHECK(cudaGetLastError());
-        colmap = posmap.ptr<int>();
-        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        deg_l = deg_loc.ptr<int64_t>();
     } else {
-        P.cuts = {0, n};
+        P.rows = {n};
         P.max_rows = n;
     }
-    const int64_t lo = P.cuts[P.rank], hi = P.cuts[P.rank + 1], nl = hi - lo;
-    V.lo = lo;
+    const int64_t nl = P.rows[(size_t)P.rank];
     V.n_local = nl;
-    V.x_len = (int64_t)P.G * P.max_rows;
-    V.x_off = (int64_t)P.rank * P.max_rows;
+    V.x_len = n;
+    V.part_G = P.G;
+    V.part_r = P.rank;
+    const int64_t lo = 0;
 
     DevMem rp64(sizeof(int64_t) * (nl + 1));
     {
-        // deg_new[hi] may be a real degree: scan nl+1 entries of a copy with a zero tail
+        // scan nl+1 entries of a copy with a zero tail
         DevMem dl(sizeof(int64_t) * (nl + 1));
         CHEB_CUDA_CHECK(cudaMemsetAsync(dl.get(), 0, sizeof(int64_t) * (nl + 1), st));
         if (nl > 0)
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(dl.get(), deg_new.ptr<int64_t>() + lo, sizeof(int64_t) * nl,
-                                            cudaMemcpyDeviceToDevice, st));
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(dl.get(), deg_l, sizeof(int64_t) * nl, cudaMemcpyDeviceToDevice, st));
         size_t bytes = 0;
         CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, dl.ptr<int64_t>(), rp64.ptr<int64_t>(), nl + 1, st));
         void* t = tmp.get(bytes);
@@ -1288,10 +1285,10 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     if (nl > 0) {
         DevMem uniq(sizeof(int64_t) * nl), cnts(sizeof(int64_t) * nl), nruns(sizeof(int64_t));
         size_t bytes = 0;
-        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, deg_new.ptr<int64_t>() + lo, uniq.ptr<int64_t>(),
+        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, deg_l, uniq.ptr<int64_t>(),
                                                            cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), nl, st));
         void* t = tmp.get(bytes);
-        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(t, bytes, deg_new.ptr<int64_t>() + lo, uniq.ptr<int64_t>(),
+        CHEB_CUDA_CHECK(cub::DeviceRunLengthEncode::Encode(t, bytes, deg_l, uniq.ptr<int64_t>(),
                                                            cnts.ptr<int64_t>(), nruns.ptr<int64_t>(), nl, st));
         const int64_t R = read_scalar(nruns.ptr<int64_t>(), st);
         run_deg.resize(R);
@@ -1472,7 +1469,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         DevMem cnt(sizeof(unsigned long long));
         CHEB_CUDA_CHECK(cudaMemsetAsync(cnt.get(), 0, sizeof(unsigned long long), st));
         k_push_mask<RPN><<<(int)std::min<int64_t>((nl * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
-            V.row_ptr.ptr<RPN>(), V.col.ptr<int>(), nl, P.max_rows, P.G, P.rank, V.push_mask.ptr<unsigned>(),
+            V.row_ptr.ptr<RPN>(), V.col.ptr<int>(), nl, P.G, P.rank, V.push_mask.ptr<unsigned>(),
             cnt.ptr<unsigned long long>());
         CHEB_CUDA_CHECK(cudaGetLastError());
         unsigned long long c = 0;
@@ -1491,13 +1488,6 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
                                                                  V.inv.ptr<double>());
     } else {
         V.inv.release();
-    }
-    if (P.G > 1 || P.comm || g->peer) {  // keep the global order (final un-permute), local order for row ids
-        V.order_full = std::move(V.order);
-        V.order.alloc(sizeof(int) * std::max<int64_t>(nl, 1));
-        if (nl > 0)
-            k_copy_i32<<<grid_for(nl), kBuildThreads, 0, st>>>(V.order_full.ptr<int>() + lo, nl, V.order.ptr<int>());
-        CHEB_CUDA_CHECK(cudaGetLastError());
     }
 
     dbg_mark("  view: tiles staged");

@@ -477,6 +477,8 @@ void cheb_graph_free(cheb_graph_t g) {
     delete g;
 }
 
+int cheb_partition_block_rows(void) { return (int)kPartRows; }
+
 cheb_status cheb_partition_vertices(const int64_t* degrees, int64_t n, int K, int64_t* cuts) {
     return guarded([&] { partition_cuts(degrees, n, K, cuts); });
 }
@@ -1087,8 +1089,9 @@ cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, 
         need_graph(g);
         GraphScope gs(g);
         ensure_view(g);
-        if (lo) *lo = g->part.cuts[g->part.rank];
-        if (hi) *hi = g->part.cuts[g->part.rank + 1];
+        // block-cyclic partition: the rank owns n_local sorted rows; lo = 0, hi = n_local
+        if (lo) *lo = 0;
+        if (hi) *hi = g->view.n_local;
         if (nnz_local) *nnz_local = g->view.nnz_local;
         if (max_rows) *max_rows = g->part.max_rows;
     });

@@ -205,9 +205,10 @@ constexpr int kTileChunk = 0x10;
 struct SolverView {
     bool ready = false;
     bool rp64 = false;
-    DevMem order;      // int32 [n_local]  local new row -> old id
-    DevMem order_full; // int32 [n]  global new -> old (partitioned runs only)
-    int64_t n_local = 0, nnz_local = 0, lo = 0, x_len = 0, x_off = 0;
+    DevMem order;      // int32 [n_local]  local row -> old id
+    DevMem order_full; // int32 [n]  global sorted row -> old id (partitioned runs only)
+    int64_t n_local = 0, nnz_local = 0, x_len = 0;
+    int part_G = 1, part_r = 0;  // local row i is sorted row part_global(i, part_r, part_G)
     DevMem row_ptr;    // int32/int64 [n+1] (new order)
     DevMem col;        // int32 [nnz] (renamed ids, storage order kept)
     DevMem inv;        // double [n] (new order) only when inv_degree is non-canonical
@@ -236,16 +237,48 @@ struct SolverView {
     }
 };
 
-// 1-D row partition of the degree-sorted view over G GPUs (one process per GPU).
-// Rank r owns sorted rows [cuts[r], cuts[r+1]); x is exchanged in a padded layout of
-// G slots of max_rows entries (slot r = rank r's rows), so an NCCL all-gather with equal
-// counts replicates x_{k+1} on every rank.
+// 1-D row partition of the degree-sorted view over G GPUs (one process per GPU), block-
+// cyclic in snake order: sorted rows are cut into blocks of kPartRows; block b of cycle
+// c = b / G goes to rank j = b mod G on even cycles and to G - 1 - j on odd ones.  Every rank
+// thus holds the same mix of hub and leaf rows (nnz and row counts balanced to within a
+// block per cycle), where contiguous degree-prefix ranges (the reference's partition_vertices
+// rule, cpaa.cpp:40-68, measured round 2: tools/rank_balance.py) leave one rank with every
+// low-degree row and cap 8-GPU scaling at ~1.6x on config 4.  x keeps the global sorted
+// order on every rank (no padding): rank r's local row i is sorted row part_global(i, r, G),
+// so the view's column ids, hot prefix and L2 window are the single-GPU ones.
+constexpr int kPartLgRows = 6;
+constexpr int64_t kPartRows = int64_t(1) << kPartLgRows;
+__host__ __device__ __forceinline__ int part_owner(int64_t u, int G) {
+    const int64_t b = u >> kPartLgRows, c = b / G;
+    const int j = (int)(b - c * G);
+    return (c & 1) ? G - 1 - j : j;
+}
+__host__ __device__ __forceinline__ int64_t part_global(int64_t i, int r, int G) {
+    const int64_t c = i >> kPartLgRows;
+    const int j = (c & 1) ? G - 1 - r : r;
+    return ((c * G + j) << kPartLgRows) | (i & (kPartRows - 1));
+}
+__host__ __device__ __forceinline__ int64_t part_local(int64_t u, int G) {
+    return (((u >> kPartLgRows) / G) << kPartLgRows) | (u & (kPartRows - 1));
+}
 struct Partition {
     int G = 1, rank = 0;
-    std::vector<int64_t> cuts{0, 0};
-    int64_t max_rows = 0;
+    std::vector<int64_t> rows{0};  // rows per rank
+    int64_t max_rows = 0;          // largest rank's row count (NCCL slot size)
     void* comm = nullptr;  // ncclComm_t (owned by the cheb_comm handle, not by the graph)
 };
+// rows of an n-row view owned by each of G ranks
+inline std::vector<int64_t> part_rows(int64_t n, int G) {
+    std::vector<int64_t> rows((size_t)G, 0);
+    const int64_t nb = (n + kPartRows - 1) / kPartRows;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int64_t c = b / G;
+        const int j = (int)(b - c * G);
+        const int r = (c & 1) ? G - 1 - j : j;
+        rows[(size_t)r] += std::min<int64_t>(kPartRows, n - b * kPartRows);
+    }
+    return rows;
+}
 
 // Fused push exchange of a row partition: every rank owns IPC-exportable
 // exchange buffers and holds pointers to every peer's copies (IPC-opened or, when one

@@ -20,16 +20,20 @@ __global__ void k_normalize_slot(const V* __restrict__ acc, int64_t nl, const do
         slot[u] = (V)((double)acc[u] / tot);
 }
 
+// NCCL exchange: every rank's local values, all-gathered into G slots of max_rows, back to
+// the global sorted order (block-cyclic partition, common.cuh)
 template <class V>
-__global__ void k_unpermute_padded(const V* __restrict__ padded, const int64_t* __restrict__ cuts, int G,
-                                   int64_t max_rows, const int* __restrict__ order_full, V* __restrict__ out) {
-    const int64_t total = (int64_t)G * max_rows;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < total;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int r = (int)(p / max_rows);
-        const int64_t i = p - r * max_rows;
-        if (i < cuts[r + 1] - cuts[r]) out[order_full[cuts[r] + i]] = padded[p];
-    }
+__global__ void k_unshuffle(const V* __restrict__ slots, int64_t n, int G, int64_t max_rows, V* __restrict__ out) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        out[u] = slots[(int64_t)part_owner(u, G) * max_rows + part_local(u, G)];
+}
+
+// ranks[order[u]] = v[u] for every sorted row u (global sorted order -> vertex order)
+template <class V>
+__global__ void k_unpermute_global(const V* __restrict__ v, int64_t n, const int* __restrict__ order,
+                                   V* __restrict__ out) {
+    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+        out[order[u]] = v[u];
 }
 
 // ---------------- fused push exchange: barrier and copy kernels ------------------------
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(256) k_term_tail(const double* __restrict__ pa
     __syncthreads();
 }
 
-// dst[r][off + i] = src[i] for every rank r (trace partials, x_0 slot).
+// dst[r][off + i] = src[i] for every rank r (trace partials).
 template <class T>
 __global__ void k_push_copy(const T* __restrict__ src, int64_t n, T* const* dst, int G, int64_t off) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -120,14 +124,25 @@ __global__ void k_push_copy(const T* __restrict__ src, int64_t n, T* const* dst,
     }
 }
 
-// ranks of the local rows, normalised, pushed into every rank's padded result buffer
+// Local rows' values to every rank's global-order buffer (x_0; block-cyclic positions).
+template <class V>
+__global__ void k_push_local(const V* __restrict__ src, int64_t nl, V* const* dst, int G, int rank) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+        const V v = src[i];
+        const int64_t u = part_global(i, rank, G);
+        for (int r = 0; r < G; ++r) dst[r][u] = v;
+    }
+}
+
+// ranks of the local rows, normalised, pushed into every rank's global-order result buffer
 template <class V>
 __global__ void k_normalize_push(const V* __restrict__ acc, int64_t nl, const double* __restrict__ total,
-                                 V* const* dst, int G, int64_t off) {
+                                 V* const* dst, int G, int rank) {
     const double tot = *total;
-    for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nl; u += (int64_t)gridDim.x * blockDim.x) {
-        const V v = (V)((double)acc[u] / tot);
-        for (int r = 0; r < G; ++r) dst[r][off + u] = v;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nl; i += (int64_t)gridDim.x * blockDim.x) {
+        const V v = (V)((double)acc[i] / tot);
+        const int64_t u = part_global(i, rank, G);
+        for (int r = 0; r < G; ++r) dst[r][u] = v;
     }
 }
 
@@ -152,7 +167,7 @@ struct DistSolve {
     PeerGroup* pg;  // null: NCCL
     std::vector<double> coeffs;
     double c0 = 0.0, beta_v = 0.0;
-    DevMem d_p, trace_all, tglob, rbuf, dcuts;
+    DevMem d_p, trace_all, tglob, rbuf, slots, xloc;
     V* T[2];
     V* X[2];
     V* acc;
@@ -183,11 +198,10 @@ struct DistSolve {
             CHEB_CUDA_CHECK(cudaMemcpyAsync(d_p.get(), s.p, sizeof(double) * g->n, cudaMemcpyHostToDevice, st));
         }
         tglob.alloc(sizeof(double) * 2 * std::max(M, 1));
-        dcuts.alloc(sizeof(int64_t) * (G + 1));
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(dcuts.get(), P.cuts.data(), sizeof(int64_t) * (G + 1), cudaMemcpyHostToDevice, st));
         T[0] = w.T0.ptr<V>();
         T[1] = w.T1.ptr<V>();
         acc = w.acc.ptr<V>();
+        xloc.alloc(sizeof(V) * (size_t)std::max<int64_t>(nl, 1));
         if (pg) {
             X[0] = static_cast<V*>(pg->X[0]);
             X[1] = static_cast<V*>(pg->X[1]);
@@ -197,10 +211,21 @@ struct DistSolve {
             X[1] = w.X1.ptr<V>();
             trace_all.alloc(sizeof(double) * 2 * (size_t)std::max(M, 1) * G);
             rbuf.alloc(sizeof(V) * (size_t)std::max<int64_t>(Vw.x_len, 1));
+            slots.alloc(sizeof(V) * (size_t)std::max<int64_t>((int64_t)G * mr, 1));
             stride = 2 * (int64_t)std::max(M, 1);
         }
     }
     ncclComm_t comm() const { return static_cast<ncclComm_t>(g->part.comm); }
+    // NCCL exchange: all-gather every rank's slot (in place, equal counts), then back to the
+    // global sorted order in `dst`
+    void gather_slots(V* dst) {
+        cudaStream_t st = g->stream;
+        V* my = slots.ptr<V>() + (int64_t)g->part.rank * mr;
+        CHEB_NCCL_CHECK(ncclAllGather(my, slots.ptr<V>(), (size_t)mr, nccl_type<V>(), comm(), st));
+        k_unshuffle<V><<<grid1d(g->n), kThreads, 0, st>>>(slots.ptr<V>(), g->n, G, mr, dst);
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        ++launches;
+    }
     V* const* push_table(int which) const {  // device pointer table of every rank's X[which]
         return reinterpret_cast<V* const*>(pg->table.ptr<void*>() + (size_t)which * G);
     }
@@ -215,15 +240,17 @@ struct DistSolve {
         cudaStream_t st = g->stream;
         const SolverView& Vw = g->view;
         CHEB_CUDA_CHECK(cudaEventRecord(g->ev0, st));
+        V* x0 = pg ? xloc.ptr<V>() : slots.ptr<V>() + (int64_t)g->part.rank * mr;
         k_init<RP, V><<<grid1d(nl), kThreads, 0, st>>>(static_cast<const RP*>(L.rp), L.inv, d_p.ptr<double>(), L.order,
-                                                       nl, c0 / 2.0, T[0], T[1], acc, X[0] + Vw.x_off);
+                                                       nl, c0 / 2.0, T[0], T[1], acc, x0);
         CHEB_CUDA_CHECK(cudaGetLastError());
         ++launches;
+        (void)Vw;
         if (pg) {
-            k_push_copy<V><<<grid1d(nl), kThreads, 0, st>>>(X[0] + Vw.x_off, nl, push_table(0), G, Vw.x_off);
+            k_push_local<V><<<grid1d(nl), kThreads, 0, st>>>(x0, nl, push_table(0), G, g->part.rank);
             ++launches;
         } else {
-            CHEB_NCCL_CHECK(ncclAllGather(X[0] + Vw.x_off, X[0], (size_t)mr, nccl_type<V>(), comm(), st));
+            gather_slots(X[0]);
         }
         CHEB_CUDA_CHECK(cudaGetLastError());
     }
@@ -235,13 +262,15 @@ struct DistSolve {
         Workspace& w = g->ws;
         TermArgs<RP, V> a = base_args<RP, V>(g, L);
         a.x_in = X[(k - 1) & 1];
-        a.x_out = X[k & 1] + Vw.x_off;
         if (pg) {
+            a.x_out = X[k & 1];
+            a.part_G = G;  // local row u -> global sorted position
+            a.part_r = g->part.rank;
             a.push = push_table(k & 1);
             a.push_n = G;
-            a.push_off = Vw.x_off;
             a.push_mask = tuning().halo ? Vw.push_mask.ptr<unsigned>() : nullptr;
         }
+        if (!pg) a.x_out = slots.ptr<V>() + (int64_t)g->part.rank * mr;  // this rank's slot, local order
         a.T = T[(k - 1) & 1];
         a.acc = acc;
         a.ck = coeffs[k];
@@ -273,9 +302,7 @@ struct DistSolve {
         }
         CHEB_CUDA_CHECK(cudaGetLastError());
         ++launches;
-        if (!pg) {  // x_{k+1}: every rank's slot -> every rank (in place, equal counts)
-            CHEB_NCCL_CHECK(ncclAllGather(X[k & 1] + Vw.x_off, X[k & 1], (size_t)mr, nccl_type<V>(), comm(), st));
-        }
+        if (!pg) gather_slots(X[k & 1]);  // x_{k+1}: every rank's slot -> global order on every rank
     }
 
     // phase M+1: every rank's trace (or, for M = 0, its acc total) to every rank
@@ -308,11 +335,13 @@ struct DistSolve {
         k_sum_ranks_strided<<<1, 256, 0, st>>>(all, G, len, pg ? stride : len, tglob.ptr<double>());
         d_total = M > 0 ? tglob.ptr<double>() + 2 * (M - 1) + 1 : tglob.ptr<double>();
         if (pg) {
-            k_normalize_push<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf_table(), G, Vw.x_off);
+            k_normalize_push<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf_table(), G, g->part.rank);
         } else {
-            k_normalize_slot<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total, rbuf.ptr<V>() + Vw.x_off);
-            CHEB_NCCL_CHECK(ncclAllGather(rbuf.ptr<V>() + Vw.x_off, rbuf.ptr<V>(), (size_t)mr, nccl_type<V>(), comm(), st));
+            k_normalize_slot<V><<<grid1d(nl), kThreads, 0, st>>>(acc, nl, d_total,
+                                                                  slots.ptr<V>() + (int64_t)g->part.rank * mr);
+            gather_slots(rbuf.ptr<V>());
         }
+        (void)Vw;
         CHEB_CUDA_CHECK(cudaGetLastError());
         launches += 2;
     }
@@ -322,9 +351,9 @@ struct DistSolve {
         cudaStream_t st = g->stream;
         const SolverView& Vw = g->view;
         Workspace& w = g->ws;
-        const V* padded = pg ? static_cast<const V*>(pg->rbuf) : rbuf.ptr<V>();
-        k_unpermute_padded<V><<<grid1d(Vw.x_len), kThreads, 0, st>>>(padded, dcuts.ptr<int64_t>(), G, mr,
-                                                                    Vw.order_full.ptr<int>(), w.out.ptr<V>());
+        const V* glob = pg ? static_cast<const V*>(pg->rbuf) : rbuf.ptr<V>();
+        const int* order_g = Vw.order_full ? Vw.order_full.ptr<int>() : Vw.order.ptr<int>();  // (G = 1: same)
+        k_unpermute_global<V><<<grid1d(g->n), kThreads, 0, st>>>(glob, g->n, order_g, w.out.ptr<V>());
         CHEB_CUDA_CHECK(cudaGetLastError());
         ++launches;
         CHEB_CUDA_CHECK(cudaEventRecord(g->ev1, st));

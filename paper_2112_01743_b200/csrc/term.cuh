@@ -80,11 +80,12 @@ struct TermArgs {
     int stream_cs;      // per-row operands loaded / stored with the streaming (.cs) policy
     int xout_hint;      // x_{k+1} store policy (tuning().xout_hint)
     int64_t xdiscard_len;  // > 0: drop x_out[0, len) from L2 at kernel start (dead x_{k-1} lines)
-    // fused push exchange (partitioned runs): x_{k+1}[u] is stored at push[r][push_off + u]
+    // fused push exchange (partitioned runs): x_{k+1} of local row u is stored at
+    // push[r][part_global(u, part_r, part_G)] for the ranks r that read it
     // for every rank r (peer memory over NVLink) instead of x_out[u]
     V* const* push;
     int push_n;
-    int64_t push_off;
+    int part_G, part_r;         // G > 1: x_{k+1} of local row u goes to sorted row part_global(u, r, G)
     const unsigned* push_mask;  // halo-only push: bit r = rank r reads x[u] (null: every rank)
     // per-term device clock (TraceRow::elapsed_ms): the first term stamps its start, the last
     // CTA of the term's final kernel stamps its end
@@ -299,12 +300,13 @@ __device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, 
                 a.T[u] = t;
                 a.acc[u] = nacc;
             }
+            const int64_t pos = a.part_G > 1 ? part_global(u, a.part_r, a.part_G) : u;
             if (a.push) {  // fused exchange: straight into the copies of x_{k+1} that are read
                 const unsigned m = a.push_mask ? __ldg(a.push_mask + u) : ~0u;
                 for (int r = 0; r < a.push_n; ++r)
-                    if (m >> r & 1u) a.push[r][a.push_off + u] = xn;
+                    if (m >> r & 1u) a.push[r][pos] = xn;
             } else {
-                st_hint(a.x_out + u, xn, a.xout_hint);
+                st_hint(a.x_out + pos, xn, a.xout_hint);
             }
             p0 += (double)t;
             p1 += (double)nacc;
@@ -1062,7 +1064,8 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             ab.xout_hint = (int64_t)g->view.x_len * (int64_t)sizeof(V) > (int64_t)l2 ? 3 : 0;
         }
         // x buffers are cudaMalloc'ed (256-B aligned): whole 128-B lines of x_out only
-        ab.xdiscard_len = (EPI == EPI_CPAA && tuning().xdiscard && !a.push) ? (g->view.x_len * (int64_t)sizeof(V) / 128) * 128 / (int64_t)sizeof(V) : 0;
+        ab.xdiscard_len = (EPI == EPI_CPAA && tuning().xdiscard && !a.push && g->part.G == 1 && !g->part.comm)
+                              ? (g->view.x_len * (int64_t)sizeof(V) / 128) * 128 / (int64_t)sizeof(V) : 0;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(g->view.grid);
         cfg.blockDim = dim3(kWarps * 32);

@@ -1,6 +1,8 @@
 """Multi-GPU plumbing: one process per GPU, an NCCL communicator created by the library
-(cheb_comm_create) from a unique id that rank 0 draws and torch.distributed broadcasts.
-Attaching it to a graph handle makes cheb_cpaa a collective over the ranks."""
+(cheb_comm_create) from a unique id that rank 0 draws and torch.distributed broadcasts, or
+the fused push exchange (PeerExchange).  Attaching either to a graph handle makes cheb_cpaa a
+collective over the ranks; the rows are split block-cyclically in snake order
+over the degree-sorted relabel (cheb_partition_block_rows rows per block)."""
 from __future__ import annotations
 
 import ctypes as C
@@ -12,7 +14,9 @@ from .api import _check, DeviceGraph
 
 
 def partition_plan(degrees, G: int):
-    """cheb_partition_plan: (order new->old, cuts[G+1] over new ids, max_rows)."""
+    """cheb_partition_plan: (order new->old = the degree-descending relabel, cuts[G+1] = the
+    reference's partition_vertices rule on it, max_rows).  The device partition uses the
+    relabel with block-cyclic ownership (common.cuh part_owner), not the cuts."""
     deg = np.ascontiguousarray(degrees, dtype=np.int64)
     n = deg.size
     order = np.zeros(n, dtype=np.int64)
@@ -100,6 +104,11 @@ class PeerExchange:
 
 
 def partition_info(dg: DeviceGraph) -> dict:
+    """This rank's share of the block-cyclic row partition: rows, CSR entries, the largest
+    rank's row count, and the halo-push stores per term (vs replicate-to-all)."""
     lo, hi, nnz, mr = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
     _check(L.load().cheb_graph_partition_info(dg.handle, C.byref(lo), C.byref(hi), C.byref(nnz), C.byref(mr)))
-    return {"lo": lo.value, "hi": hi.value, "nnz_local": nnz.value, "max_rows": mr.value}
+    a, b = C.c_int64(), C.c_int64()
+    _check(L.load().cheb_graph_exchange_info(dg.handle, C.byref(a), C.byref(b)))
+    return {"rows": hi.value - lo.value, "nnz_local": nnz.value, "max_rows": mr.value,
+            "halo_stores": a.value, "all_stores": b.value}

@@ -330,7 +330,7 @@ def test_batched_dense_personalization_and_uniform_column(cheb, oracle):
 
 def test_nccl_partitioned_path_single_rank(cheb):
     """The multi-GPU code path (NCCL communicator attached, per-term all-gather, rank-ordered
-    trace combine, padded gather + un-permute) at world size 1 on one B200: identical bits
+    trace combine, slot gather + un-shuffle + un-permute) at world size 1 on one B200: identical bits
     to the single-GPU solve.  Multi-rank correctness is covered on CPU by
     tests/test_multigpu_cpu.py (same plan and exchange protocol)."""
     from paper_2112_01743_b200.distributed import Communicator, partition_info
@@ -341,7 +341,7 @@ def test_nccl_partitioned_path_single_rank(cheb):
         comm = Communicator(0, 1, 0)
         comm.attach(dg)
         info = partition_info(dg)
-        assert (info["lo"], info["hi"]) == (0, int(z["n"]))
+        assert info["rows"] == int(z["n"]) and info["max_rows"] == int(z["n"])
         part = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
         assert np.array_equal(part.ranks, plain.ranks)
         assert np.max(np.abs(part.ranks - z["cpaa39_ranks"])) <= TOL64

@@ -1,6 +1,7 @@
 """N>1 path on CPU: world_size-2 (and 3) gloo process groups run the multi-GPU CPAA
-protocol (library partition plan + padded all-gather exchange + rank-ordered trace
-combine) and must reproduce the oracle within 1e-12 with an identical top-100."""
+protocol (library relabel + block-cyclic snake partition + all-gather/un-shuffle exchange +
+rank-ordered trace combine) and must reproduce the oracle within 1e-12 with an identical
+top-100."""
 import os
 import socket
 
@@ -29,8 +30,8 @@ def _worker(rank, world, port, name, q):
         sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
         from multigpu_emul import emulate
         z = load_golden(name)
-        ranks, trace, (lo, hi, mr) = emulate(rank, world, z["offsets"], z["neighbors"])
-        q.put((rank, ranks, trace, lo, hi, mr))
+        ranks, trace, (nl, mr, counts) = emulate(rank, world, z["offsets"], z["neighbors"])
+        q.put((rank, ranks, trace, nl, mr, counts))
     finally:
         dist.destroy_process_group()
 
@@ -57,10 +58,35 @@ def test_partitioned_protocol_matches_oracle(world, name):
         assert np.all(np.abs(trace[:, 1] - z["cpaa39_S"]) <= z["n"] * 1e-12)
     if want.size >= 200:
         assert np.array_equal(np.argsort(-out[0][1], kind="stable")[:100], np.argsort(-want, kind="stable")[:100])
-    # the slices tile the sorted row range exactly
-    spans = [(lo, hi) for _, _, _, lo, hi, _ in out]
-    assert spans[0][0] == 0 and spans[-1][1] == int(z["n"])
-    assert all(spans[i][1] == spans[i + 1][0] for i in range(world - 1))
+    # the ranks' rows partition the sorted rows exactly
+    assert sum(t[3] for t in out) == int(z["n"])
+    assert [t[3] for t in out] == list(out[0][5])
+
+
+def test_block_cyclic_partition_properties():
+    """The device partition (common.cuh part_owner / part_global): snake-order blocks give
+    every rank the same mix of high- and low-degree rows — row counts and nnz balanced."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from multigpu_emul import block_rows, local_rows, part_global, part_local, part_owner
+    B = block_rows()
+    assert B >= 1 and (B & (B - 1)) == 0
+    z = load_golden("config1")
+    deg = np.sort(np.diff(z["offsets"]))[::-1]          # degree-sorted rows
+    n = deg.size
+    for G in (1, 2, 3, 4, 8):
+        u = np.arange(n)
+        own = part_owner(u, G, B)
+        for r in range(G):
+            mine = local_rows(n, r, G, B)
+            assert np.array_equal(part_global(np.arange(mine.size), r, G, B), mine)
+            assert np.array_equal(part_local(mine, G, B), np.arange(mine.size))
+        cnt = np.bincount(own, minlength=G)
+        assert cnt.max() - cnt.min() <= B
+        nnz = np.bincount(own, weights=deg, minlength=G)
+        # per cycle every rank gets one block of degree-descending rows: the rank totals differ by
+        # a telescoping sum bounded by one block of the largest rows (+ the partial last cycle)
+        assert nnz.max() - nnz.min() <= 2 * B * deg.max()
 
 
 def test_partition_plan_properties(cheb):

@@ -188,22 +188,25 @@ def test_halo_push_volume_and_bitwise_equivalence(cheb, G):
         lib.cheb_set_tuning(b"halo", 1)
     assert np.array_equal(halo.ranks, full.ranks)
     grp.close()
-    # numpy recount: owner of each new id, masks over each local row's neighbours
+    # numpy recount: owner of each sorted row (block-cyclic snake partition), masks over each
+    # local row's neighbours
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from multigpu_emul import block_rows, part_owner
+    B = block_rows()
     g = hs[0].download()
-    order, cuts, mr = partition_plan(g.degrees, G)
+    order, _, _ = partition_plan(g.degrees, G)
     new = np.empty(g.n, dtype=np.int64)
     new[order] = np.arange(g.n)
-    rows = np.repeat(new, np.diff(g.offsets))          # new id of each entry's row
-    owner_col = np.searchsorted(cuts, new[g.neighbors], side="right") - 1
-    owner_row = np.searchsorted(cuts, rows, side="right") - 1
+    rows = np.repeat(new, np.diff(g.offsets))          # sorted id of each entry's row
+    owner_col = part_owner(new[g.neighbors], G, B)
     pairs = np.unique(rows * G + owner_col)            # (row, rank needing it)
     prow = pairs // G
     pr = pairs % G
-    prow_owner = np.searchsorted(cuts, prow, side="right") - 1
+    prow_owner = part_owner(prow, G, B)
+    n_rows = np.bincount(part_owner(np.arange(g.n), G, B), minlength=G)
     for r in range(G):
         mine = prow_owner == r
         want_halo = int(np.count_nonzero(mine & (pr != r)))
-        n_local = int(cuts[r + 1] - cuts[r])
-        assert stores[r] == (want_halo, n_local * (G - 1)), (r, stores[r], want_halo)
-    del owner_row
+        assert stores[r] == (want_halo, int(n_rows[r]) * (G - 1)), (r, stores[r], want_halo)
     assert sum(s[0] for s in stores) < sum(s[1] for s in stores)
