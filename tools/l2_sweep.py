@@ -36,8 +36,6 @@ def run(label, **kv):
 
 
 run("default")
-for P in (2, 3, 4, 6):
-    run(f"prefetch {P}", prefetch=P)
-run("nogather", nogather=1)
-for P in (2, 4):
-    run(f"nogather prefetch {P}", nogather=1, prefetch=P)
+run("no discard", xdiscard=0)
+run("x_out plain", xout_hint=0)
+run("default again")
