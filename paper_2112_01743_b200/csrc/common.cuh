@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -61,6 +62,11 @@ void release_stream(int device, cudaStream_t s);
 // Returns false when the device offers no persisting L2.
 bool l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* w);
 
+inline bool alloc_debug() {
+    static const bool on = std::getenv("CHEB_DEBUG_ALLOC") != nullptr;
+    return on;
+}
+
 // Owning device allocation (untyped bytes; typed views via ptr<T>()).
 class DevMem {
 public:
@@ -90,6 +96,7 @@ public:
         if (bytes == 0) bytes = 16;
         st_ = alloc_stream();
         async_ = st_ != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         if (async_) {
             retain_pool_memory();
             CHEB_CUDA_CHECK(cudaMallocAsync(&p_, bytes, st_));
@@ -97,6 +104,11 @@ public:
             CHEB_CUDA_CHECK(cudaMalloc(&p_, bytes));
         }
         n_ = bytes;
+        if (alloc_debug()) {
+            const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            if (ms > 1.0 || bytes > (size_t(1) << 30))
+                std::fprintf(stderr, "[alloc] %s %.1f MB in %.2f ms\n", async_ ? "pool" : "cudaMalloc", bytes / 1e6, ms);
+        }
     }
     // Grow-only reuse.
     void ensure(size_t bytes) {
@@ -407,6 +419,8 @@ struct Tuning {
     int batchblock = 128; // right-hand sides per batched pass (column blocks of one call)
     int halo = 1;       // row partition, push exchange: store x_{k+1}[u] only on the ranks that read it
     int prefetch = 0;   // term kernel: L2 prefetch distance in tiles (0 off); slower on C2-C4
+    int spmm_hub_mb = 64; // batched path: MB of X rows (the hub prefix) gathered under evict-last
+    int spmm_xpol = 0;  // batched path x_{k+1} stores: 0 normal, 1 evict-last hub prefix + streaming rest
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -427,6 +441,8 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_BATCHBLOCK")) x.batchblock = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_HALO")) x.halo = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_PREFETCH")) x.prefetch = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_SPMM_HUB_MB")) x.spmm_hub_mb = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_SPMM_XPOL")) x.spmm_xpol = std::atoi(e);
         return x;
     }();
     return t;

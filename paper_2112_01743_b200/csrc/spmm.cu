@@ -37,6 +37,7 @@ struct BatchArgs {
     double* hub_part;  // [n_tiles][Rs]
     double* hub_ts;    // [n_hub][2]
     int hub_rows;      // rows [0, hub_rows) of X are gathered under an L2 evict-last policy
+    int xpol;          // x_{k+1} stores: 0 normal; 1 evict-last for the hub prefix, streaming for the rest
 };
 
 template <class V, int VPL>
@@ -95,6 +96,12 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
+}
+__device__ __forceinline__ void st_policy(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_policy(float* p, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" :: "l"(p), "f"(v), "l"(pol) : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t pol;
@@ -296,7 +303,13 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_
         }
         StreamIO<V, VPL>::st(a.T + i0, t, true);
         StreamIO<V, VPL>::st(a.acc + i0, na, true);
-        StreamIO<V, VPL>::st(a.x_out + i0, xo, false);
+        if (a.xpol == 1 && u < a.hub_rows) {  // next term's most-gathered rows stay in L2
+            const uint64_t pol = policy_evict_last();
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) st_policy(a.x_out + i0 + k, xo[k], pol);
+        } else {
+            StreamIO<V, VPL>::st(a.x_out + i0, xo, a.xpol == 1);
+        }
         return;
     }
 #pragma unroll
@@ -557,7 +570,8 @@ void batch_run(cheb_graph* g, const BatchSpec& s, std::vector<double>& trace, st
         a.first = k == 1;
         a.R = R;
         a.Rs = Rs;
-        a.hub_rows = (int)std::min<int64_t>(g->n, (int64_t(64) << 20) / ((int64_t)Rs * (int64_t)sizeof(V)));
+        a.hub_rows = (int)std::min<int64_t>(g->n, ((int64_t)tuning().spmm_hub_mb << 20) / ((int64_t)Rs * (int64_t)sizeof(V)));
+        a.xpol = tuning().spmm_xpol;
         a.part = w.part.ptr<double>();
         a.hub_part = w.hub_part.ptr<double>();
         a.hub_ts = Vw.n_hub ? w.hub_ts.ptr<double>() : nullptr;

@@ -23,8 +23,11 @@ lib.cheb_cpaa_opts_default(C.byref(o))
 o.eps, o.precision, o.R = 1e-10, prec, 64
 sp = seeds.ctypes.data_as(L.I64P)
 ref = None
-for blk in (64,):
-    lib.cheb_set_tuning(b"batchblock", blk)
+variants = [(64, 0), (64, 1), (96, 1), (48, 1), (96, 0)] if "sweep" in sys.argv else [(64, 0)]
+for hub_mb, xpol in variants:
+    blk = 64
+    lib.cheb_set_tuning(b"spmm_hub_mb", hub_mb)
+    lib.cheb_set_tuning(b"spmm_xpol", xpol)
     ts = []
     for i in range(3):
         cheb.api._check(lib.cheb_cpaa_batch(dg.handle, C.byref(o), sp, None, None, None, None))
@@ -36,5 +39,5 @@ for blk in (64,):
         ref = res.ranks
     err = float(np.max(np.abs(res.ranks - ref)))
     t = min(ts)
-    print(f"{cfg} fp{prec} block {blk:3d}: {t:8.1f} ms/solve {t/39:7.3f} ms/term "
+    print(f"{cfg} fp{prec} hub {hub_mb} MB xpol {xpol}: {t:8.1f} ms/solve {t/39:7.3f} ms/term "
           f"{info['nnz']*64*39/(t*1e-3)/1e9:8.1f} GTEPS(nnz*R)  max|diff vs block 64| {err:.2e}", flush=True)

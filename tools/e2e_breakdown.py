@@ -32,7 +32,7 @@ if fp32:
     o.precision = 32
 tr = (L.cheb_trace_row * 64)()
 rounds, tot = C.c_int(), C.c_double()
-for it in range(4):
+for it in range(int(os.environ.get("ITERS", "4"))):
     t0 = time.perf_counter()
     h = C.c_void_p()
     cheb.api._check(lib.cheb_graph_upload_csr(off.ctypes.data_as(L.I64P), off.size, nb.ctypes.data_as(L.I64P),
