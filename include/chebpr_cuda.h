@@ -153,21 +153,21 @@ cheb_status cheb_validate_csr(const int64_t* offsets, int64_t n_offsets, const i
  * hold by construction): n, m, avg/min/max degree, self loops, builder counts. */
 cheb_status cheb_graph_validate_stats(cheb_graph_t g, cheb_graph_stats* stats);
 
-/* cpaa.cpp:40-68 partition_vertices: degree-prefix cuts (host rule, used for the
- * multi-GPU row partition).  cuts has K+1 entries. */
+/* cpaa.cpp:40-68 partition_vertices: degree-prefix cuts (host rule, the reference's; the
+ * multi-GPU partition is block-cyclic instead, see cheb_partition_block_rows).  cuts has K+1
+ * entries. */
 cheb_status cheb_partition_vertices(const int64_t* degrees, int64_t n, int K, int64_t* cuts);
 
-/* Multi-GPU row partition plan (host only): the view's degree-descending relabel
- * (order[new] = old, ties by id), the reference cut rule (cpaa.cpp:40-68) applied to the
- * relabelled degree sequence -> cuts[G+1] over new ids, and the exchange slot size
- * max_rows = the largest slice.  Padded x position of new id u on rank r:
- * r * max_rows + (u - cuts[r]). */
+/* Row partition plan (host only): the view's degree-descending relabel (order[new] = old,
+ * ties by id) — the order the device partition deals out block-cyclically — and, for
+ * reference, the reference cut rule (cpaa.cpp:40-68) applied to the relabelled degree
+ * sequence -> cuts[G+1] over new ids with max_rows = the largest such slice. */
 cheb_status cheb_partition_plan(const int64_t* degrees, int64_t n, int G, int64_t* order,
                                 int64_t* cuts, int64_t* max_rows);
 
 /* Multi-GPU (one process per GPU): an NCCL communicator shared by G ranks.  Attaching
- * it to a graph handle (every rank holds the same graph) partitions the solver view per
- * cheb_partition_plan: cheb_cpaa then becomes a collective over the G ranks — each rank
+ * it to a graph handle (every rank holds the same graph) partitions the solver view
+ * block-cyclically: cheb_cpaa then becomes a collective over the G ranks — each rank
  * runs the fused term kernel on its rows and all-gathers x_{k+1} (ncclAllGather, equal
  * padded slots) before the next term; trace sums are combined in rank order and every
  * rank receives the full ranks vector.  FAST schedule only. */

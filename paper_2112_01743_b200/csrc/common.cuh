@@ -302,9 +302,9 @@ struct PeerGroup {
     bool lockstep = false;  // all ranks driven by one host thread (cheb_group_*)
     int64_t x_len = 0;
     // this rank's own buffers (cudaMalloc: IPC-exportable)
-    void* X[2] = {nullptr, nullptr};       // padded x_k, x_len * 8 bytes each
+    void* X[2] = {nullptr, nullptr};       // x_k in the global sorted order, x_len * 8 bytes each
     void* trace_all = nullptr;             // [G][2 * kMaxPushTerms] doubles
-    void* rbuf = nullptr;                  // padded ranks, x_len * 8 bytes
+    void* rbuf = nullptr;                  // ranks in the global sorted order, x_len * 8 bytes
     unsigned long long* flags = nullptr;   // [G] barrier epochs written by the peers, [G] timeout flag
     // every rank's buffers as seen from this device ([rank] = own)
     std::vector<void*> pX0, pX1, ptrace, prbuf, pflags;

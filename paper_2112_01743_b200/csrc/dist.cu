@@ -1,4 +1,4 @@
-// Row-partitioned CPAA over G GPUs: the padded-layout solve in phases with
+// Row-partitioned CPAA over G GPUs: the block-cyclic partition's solve in phases with
 // the fused push exchange (x_{k+1} stored by the term kernels into every rank's buffer,
 // flag barrier per term) or the NCCL all-gather baseline; one process per GPU or all ranks
 // in lockstep from one process.
@@ -346,7 +346,7 @@ struct DistSolve {
         launches += 2;
     }
 
-    // phase M+3: padded ranks -> vertex order; read back the trace, check it
+    // phase M+3: global-order ranks -> vertex order; read back the trace, check it
     void finish(std::vector<double>* tr, double* total) {
         cudaStream_t st = g->stream;
         const SolverView& Vw = g->view;

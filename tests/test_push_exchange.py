@@ -1,7 +1,7 @@
 """Fused push exchange of the row partition on one B200.
 
 A PartitionGroup drives G ranks of the same graph from one process: every rank's term kernel
-stores x_{k+1} straight into every rank's padded buffer, and a release/acquire flag barrier
+stores x_{k+1} straight into the buffers of the ranks that read it (halo push), and a release/acquire flag barrier
 separates the terms.  On one GPU the ranks run in lockstep (each rank's wait kernel is
 event-ordered after every rank's signal, so no kernel spins on work not yet enqueued).  The
 kernels, buffers and barrier are the ones a one-process-per-GPU run uses over NVLink.
