@@ -562,6 +562,18 @@ class Solver:
                 px.detach()
             lib.cheb_graph_free(h)
 
+        if dist.world > 1 and self.R_cfg == 1 and comm is None:
+            # push exchange on fresh handles: every rank must map its peers; if any rank
+            # cannot, every rank switches the e2e leg to the NCCL exchange together
+            err = None
+            try:
+                step()
+            except Exception as ex:  # noqa: BLE001
+                err = f"{type(ex).__name__}: {str(ex)[:120]}"
+            if dist.min(0.0 if err else 1.0) < 1.0:
+                log(f"e2e: push exchange unavailable ({err or 'on a peer rank'}); NCCL all-gather")
+                from paper_2112_01743_b200.distributed import Communicator
+                comm = Communicator(dist.rank, dist.world, device)
         for _ in range(max(3, warmup)):  # pool, pinned staging and page-cache warm-up
             step()
         dist.barrier()

@@ -168,8 +168,9 @@ cheb_status cheb_partition_plan(const int64_t* degrees, int64_t n, int G, int64_
 /* Multi-GPU (one process per GPU): an NCCL communicator shared by G ranks.  Attaching
  * it to a graph handle (every rank holds the same graph) partitions the solver view
  * block-cyclically: cheb_cpaa then becomes a collective over the G ranks — each rank
- * runs the fused term kernel on its rows and all-gathers x_{k+1} (ncclAllGather, equal
- * padded slots) before the next term; trace sums are combined in rank order and every
+ * runs the fused term kernel on its rows and all-gathers x_{k+1} (ncclAllGather of equal
+ * slots, then back to the global sorted order) before the next term; trace sums are
+ * combined in rank order and every
  * rank receives the full ranks vector.  FAST schedule only. */
 typedef struct cheb_comm* cheb_comm_t;
 cheb_status cheb_nccl_unique_id(void* out, int out_bytes); /* 128-byte ncclUniqueId */
