@@ -1127,6 +1127,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "batchblock") tuning().batchblock = std::max(1, std::min(value, 128));
         else if (k == "halo") tuning().halo = value;
         else if (k == "prefetch") tuning().prefetch = value;
+        else if (k == "skipwarm") tuning().skipwarm = value;
         else if (k == "spmm_hub_mb") tuning().spmm_hub_mb = value;
         else if (k == "spmm_xpol") tuning().spmm_xpol = value;
         else if (k == "sortrows") tuning().sortrows = value;

@@ -421,6 +421,7 @@ struct Tuning {
     int prefetch = 0;   // term kernel: L2 prefetch distance in tiles (0 off); slower on C2-C4
     int spmm_hub_mb = 64; // batched path: MB of X rows (the hub prefix) gathered under evict-last
     int spmm_xpol = 0;  // batched path x_{k+1} stores: 0 normal, 1 evict-last hub prefix + streaming rest
+    int skipwarm = 0;   // experiment (wrong results): hub-row gathers of ids in [H, skipwarm) dropped
 };
 inline Tuning& tuning() {
     static Tuning t = [] {

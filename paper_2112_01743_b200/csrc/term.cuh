@@ -77,6 +77,7 @@ struct TermArgs {
     int tune_nogather;  // experiments only (cheb_set_tuning): replace x gathers by 1.0
     int prefetch;       // > 0: tile i + prefetch's column ids and row operands are prefetched into L2
     int tune_skip;      // experiments only: 1 skip chunk tiles, 2 skip pack tiles, 16+b only bin b
+    int tune_skipwarm;  // experiments only: chunk tiles drop their gathers of ids in [H, tune_skipwarm)
     int stream_cs;      // per-row operands loaded / stored with the streaming (.cs) policy
     int xout_hint;      // x_{k+1} store policy (tuning().xout_hint)
     int64_t xdiscard_len;  // > 0: drop x_out[0, len) from L2 at kernel start (dead x_{k-1} lines)
@@ -487,6 +488,11 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
 #pragma unroll
             for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
         } else {
+            if (a.tune_skipwarm > 0) {  // experiment: hub-row gathers of ids in [H, skipwarm) dropped
+#pragma unroll
+                for (int q = 0; q < U; ++q)
+                    if (c[q] >= H && c[q] < a.tune_skipwarm) c[q] = -1;
+            }
             gather8(a.x_in, hot_s, H, c, v);
         }
         double sum = 0.0;  // hub-row chunk sums in fp64 (fp32: a lane's U entries in fp32)
@@ -1054,6 +1060,7 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         TermArgs<RP, V> ab = a;
         ab.tune_nogather = tuning().nogather;
         ab.tune_skip = tuning().skip;
+        ab.tune_skipwarm = tuning().skipwarm;
         ab.prefetch = tuning().prefetch;
         ab.stream_cs = tuning().streamcs;
         if (g->view.n_hub > 0) ab.stamp_end = nullptr;  // the hub finalize ends the term

@@ -17,7 +17,7 @@ dg, info = bench.build_device(bench.CONFIGS[cfg], 0)
 opts = L.cheb_cpaa_opts()
 lib.cheb_cpaa_opts_default(C.byref(opts))
 opts.eps = 1e-10
-DEFAULTS = {"hot": -1, "l2win": 1, "pdl": 1, "l2win_mb": -1, "l2win_pct": 100, "streamcs": 0, "xout_hint": -1, "xdiscard": 1, "prefetch": 0, "nogather": 0}
+DEFAULTS = {"hot": -1, "l2win": 1, "pdl": 1, "l2win_mb": -1, "l2win_pct": 100, "streamcs": 0, "xout_hint": -1, "xdiscard": 1, "prefetch": 0, "nogather": 0, "skipwarm": 0}
 print(f"{cfg} n={info['n']} nnz={info['nnz']}", flush=True)
 
 
@@ -36,6 +36,5 @@ def run(label, **kv):
 
 
 run("default")
-run("no discard", xdiscard=0)
-run("x_out plain", xout_hint=0)
-run("default again")
+for w in (50_000, 100_000, 340_000, 1_000_000):
+    run(f"skip hub warm gathers < {w}", skipwarm=w)
