@@ -2,8 +2,9 @@
 #   make            -> paper_2112_01743_b200/lib/libchebpr_b200.so + oracle
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
+EXP       ?= 0
 NVFLAGS   := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC,-ffp-contract=off \
-             --expt-extended-lambda -Iinclude -Xptxas -warn-spills
+             --expt-extended-lambda -Iinclude -Xptxas -warn-spills -DCHEB_TERM_EXPERIMENTS=$(EXP)
 SRC_DIR   := paper_2112_01743_b200/csrc
 LIB_DIR   := paper_2112_01743_b200/lib
 OBJ_DIR   := build/obj

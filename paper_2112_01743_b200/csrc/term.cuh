@@ -50,6 +50,14 @@
 namespace chebgpu {
 namespace {
 
+// Experiment knobs of the term kernel (cheb_set_tuning: nogather, skip, skipwarm, prefetch,
+// streamcs) cost ~5% of its instructions when compiled in (ncu source page, C4): the product
+// build leaves them out; `make EXP=1` builds the experiment variant the tools/ studies use.
+#ifndef CHEB_TERM_EXPERIMENTS
+#define CHEB_TERM_EXPERIMENTS 0
+#endif
+constexpr bool kExp = CHEB_TERM_EXPERIMENTS != 0;
+
 enum Epi : int {
     EPI_CPAA = 0,   // fused CPAA term (cpaa.cpp:126-132 + :116 for the next round)
     EPI_GEN = 1,    // staged generate_stage (cpaa.cpp:178-190): T_next only
@@ -294,7 +302,7 @@ __device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, 
             const V t = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
             const V nacc = add_rn(accv, mul_rn((V)a.ck, t));
             const V xn = mul_rn(t, inv);
-            if (a.stream_cs) {
+            if (kExp && a.stream_cs) {
                 st_cs(a.T + u, t);
                 st_cs(a.acc + u, nacc);
             } else {
@@ -399,7 +407,7 @@ __device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR&
     const int lg = t.meta & 0xf;
     const int g = lane >> lg;
     if ((lane & ((1 << lg) - 1)) == 0 && g < t.rows) {
-        if (a.stream_cs) {
+        if (kExp && a.stream_cs) {
             o.rs = (int)(ld_cs(a.rp + t.r0 + g) - t.z0);
             o.re = (int)(ld_cs(a.rp + t.r0 + g + 1) - t.z0);
             if constexpr (EPI != EPI_PLAIN) o.pv = ld_cs(prev_src<EPI>(a) + t.r0 + g);
@@ -445,7 +453,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
     // L2 prefetch of a tile further ahead (its descriptor lives in the current or the next
     // block of the ring): the per-warp double buffer keeps ~1 tile of column ids in flight,
     // too few bytes to cover DRAM latency on graphs whose streams miss L2 (config 4)
-    if (a.prefetch > 0 && i + a.prefetch < nt && lane < 4) {
+    if (kExp && a.prefetch > 0 && i + a.prefetch < nt && lane < 4) {
         const int j = i + a.prefetch;
         if ((j / kDescBlock) <= (i / kDescBlock) + 1) {
             if ((j / kDescBlock) != (i / kDescBlock)) mbar_wait(&ws.descm[(j / kDescBlock) & 1], ((j / kDescBlock) >> 1) & 1);
@@ -463,7 +471,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
     }
     const int t = w + i * S;  // tile id (slot of a hub-row partial)
     mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
-    if (a.tune_skip &&
+    if (kExp && a.tune_skip &&
         (a.tune_skip >= 16 ? (((d.meta & kTileChunk) ? 6 : (d.meta & 0xf)) != a.tune_skip - 16)
                            : ((a.tune_skip & 1) ? (d.meta & kTileChunk) : !(d.meta & kTileChunk)))) {
         __syncwarp();
@@ -478,17 +486,23 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
     if (d.meta & kTileChunk) {
         // slice of a row with degree > kWarpNnz: partial only; completed by k_hub_finalize
         int c[U];
+        if (d.cnt == kWarpNnz) {  // a full chunk (all but a row's last): only step 7 has empty lanes
 #pragma unroll
-        for (int q = 0; q < U; ++q) {
-            const int pp = lane + 32 * q;
-            c[q] = pp < d.cnt ? cb[pp] : -1;
+            for (int q = 0; q < U - 1; ++q) c[q] = cb[lane + 32 * q];
+            c[U - 1] = lane < kWarpNnz - 32 * (U - 1) ? cb[lane + 32 * (U - 1)] : -1;
+        } else {
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                const int pp = lane + 32 * q;
+                c[q] = pp < d.cnt ? cb[pp] : -1;
+            }
         }
         V v[U];
-        if (a.tune_nogather) {
+        if (kExp && a.tune_nogather) {
 #pragma unroll
             for (int q = 0; q < U; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
         } else {
-            if (a.tune_skipwarm > 0) {  // experiment: hub-row gathers of ids in [H, skipwarm) dropped
+            if (kExp && a.tune_skipwarm > 0) {  // experiment: hub-row gathers of ids in [H, skipwarm) dropped
 #pragma unroll
                 for (int q = 0; q < U; ++q)
                     if (c[q] >= H && c[q] < a.tune_skipwarm) c[q] = -1;
@@ -525,7 +539,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
 #pragma unroll
             for (int q = 0; q < kPackUnroll; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
             V v[kPackUnroll];
-            if (a.tune_nogather) {
+            if (kExp && a.tune_nogather) {
 #pragma unroll
                 for (int q = 0; q < kPackUnroll; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
             } else {

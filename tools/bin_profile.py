@@ -6,7 +6,9 @@ tiles of rows above the warp tile), then summarise:
     python tools/bin_profile.py table [config]   # here: table from the captures + bin sizes
 Skipped tiles still stream their column ids and row operands (the prefetch runs ahead of
 the filter), so per-bin DRAM bytes are not attributable; time, warp efficiency and the
-hit rates of the LSU gathers are."""
+hit rates of the LSU gathers are.
+The nogather / skip / skipwarm / prefetch / streamcs knobs act only in the experiment build
+(`touch paper_2112_01743_b200/csrc/term.cuh && make EXP=1`); the product build compiles them out."""
 import csv
 import io
 import json

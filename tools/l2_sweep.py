@@ -1,6 +1,8 @@
 """L2 policy sweep of the term kernel on one config (per-term time, CUDA events around each
 term of a plain-launch solve): persisting-window size / hit ratio over the head of x, and
-streaming (.cs) loads/stores of the per-row operands.  Usage: python tools/l2_sweep.py [config]"""
+streaming (.cs) loads/stores of the per-row operands.  Usage: python tools/l2_sweep.py [config]
+The nogather / skip / skipwarm / prefetch / streamcs knobs act only in the experiment build
+(`touch paper_2112_01743_b200/csrc/term.cuh && make EXP=1`); the product build compiles them out."""
 import ctypes as C
 import os
 import statistics

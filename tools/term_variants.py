@@ -1,6 +1,8 @@
 """Kernel study: per-term time of the fused CPAA term kernel on a config under tuning
 variants (hot-prefix size, gathers on/off).  Timing via cheb_cpaa_profile (CUDA events
-around every term launch).  Usage: python tools/term_variants.py [config]"""
+around every term launch).  Usage: python tools/term_variants.py [config]
+The nogather / skip / skipwarm / prefetch / streamcs knobs act only in the experiment build
+(`touch paper_2112_01743_b200/csrc/term.cuh && make EXP=1`); the product build compiles them out."""
 import ctypes as C
 import os
 import statistics
