@@ -687,8 +687,12 @@ def timed_steps(sv, flush, steps, dist, clk=None):
 
 
 def secondary_line(name, device, precision, steps, warmup, dist):
-    """A compact measurement of a second workload (C2 next to the C4 headline)."""
+    """A compact measurement of a second workload (C2 next to the C4 headline; "c4:32" = the
+    headline graph in fp32)."""
     import torch
+    if ":" in name:
+        name, p = name.split(":")
+        precision = int(p)
     cfg = CONFIGS[name]
     dg, info = build_device(cfg, device)
     sv = Solver(dg, info, cfg, precision)
@@ -704,7 +708,7 @@ def secondary_line(name, device, precision, steps, warmup, dist):
     ach = B / (term_us * 1e-6) / 1e9
     dg.free()
     return {"config": config_dict(name, n, nnz, sv.M, sv.R), "value": round(nnz * sv.R * sv.M / (ms * 1e-3) / 1e9, 3),
-            "unit": "GTEPS", "ms_per_step": round(ms, 4), "steps": steps,
+            "unit": "GTEPS", "dtype": "f64" if precision == 64 else "f32", "ms_per_step": round(ms, 4), "steps": steps,
             "roofline": {"achieved": round(ach, 1), "peak": peak, "frac": round(ach / peak, 4),
                          "mean_launch_us": round(term_us, 3), "bytes_per_launch": B}}
 
@@ -720,8 +724,8 @@ def main():
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--secondary", default="c2",
-                    help="comma list of extra workloads measured compactly at N=1 ('' for none)")
+    ap.add_argument("--secondary", default="c2,c4:32",
+                    help="comma list of extra workloads measured compactly at N=1, name[:precision] ('' for none)")
     ap.add_argument("--exchange", default="push", choices=["push", "nccl"],
                     help="N>1: x_{k+1} exchange of the row partition (fused push over peer memory, "
                          "or NCCL all-gather); the e2e leg uses the same exchange")
@@ -827,7 +831,8 @@ def main():
         cpu = cpu_baseline_line(sv, args.config, args)
     secondary = []
     if dist.world == 1 and args.secondary:
-        for name in [s for s in args.secondary.split(",") if s and s != args.config]:
+        own = f"{args.config}:{args.precision}"
+        for name in [s for s in args.secondary.split(",") if s and s != args.config and s != own]:
             try:
                 secondary.append(secondary_line(name, device, args.precision, args.steps, args.warmup, dist))
             except Exception as ex:  # noqa: BLE001

@@ -14,6 +14,8 @@ Checked per config (SURVEY.md §8(c)/(d) bars, north_star):
     the same order (ties by vertex id);
   * BITEXACT fp64 ranks: bitwise equal, and the S_k / mass_T trace bitwise equal;
   * fp32: relative L1 <= 1e-6;
+  * Power (C2, C3; 50 rounds) against the reference's run_power: FAST within 1e-12, BITEXACT
+    bitwise, the L1-change trace too; transition_apply (C2, C3) against the reference's;
   * config 5 (batched, 64 one-hot columns): 4 sampled columns against the restated loop
     (oracle/cpaa_oracle.c with T0 = e_seed; the reference has no personalisation), the same
     bars (fp64 1e-12 + top-100, fp32 1e-6), every column a distribution.
@@ -91,25 +93,40 @@ def _threads():
     return bench.host_threads()
 
 
+def _check_power_and_apply(cheb, rg, dg, threads):
+    want = rg.run_power(c=C, rounds=50, parallelism=threads)
+    fast = cheb.run_power(dg, cheb.PowerConfig(c=C, rounds=50))
+    assert float(np.max(np.abs(fast.ranks - want.ranks))) <= 1e-12
+    exact = cheb.run_power(dg, cheb.PowerConfig(c=C, rounds=50, mode=cheb.MODE_BITEXACT))
+    assert np.array_equal(exact.ranks, want.ranks)
+    assert np.array_equal(np.array([r.l1_change for r in exact.trace]), want.trace[:, 4])
+    rng = np.random.default_rng(7)
+    x = rng.random(rg.n)
+    y_ref = rg.transition_apply(x)
+    assert np.array_equal(cheb.transition_apply(dg, x, mode=cheb.MODE_BITEXACT), y_ref)
+    assert float(np.max(np.abs(cheb.transition_apply(dg, x) - y_ref))) <= 1e-12 * float(np.max(np.abs(y_ref)))
+
+
 @pytest.mark.parametrize("name", ["c2", "c3"])
 def test_config_full_size_vs_reference(cheb, reference, name):
     rg = _reference_side(reference, name)
     dg, info = _device_side(name)
     _check_csr(rg, dg, info)
     _check_solves(cheb, rg, dg, _threads())
+    _check_power_and_apply(cheb, rg, dg, _threads())
     dg.free()
 
 
 def test_config4_full_size_vs_reference(cheb, reference):
     """1.05 G CSR entries, int64 row pointers, x larger than L2: CSR bit-exact, FAST within
-    1e-12 with the reference's top-100, BITEXACT bitwise (ranks and trace)."""
+    1e-12 with the reference's top-100, BITEXACT bitwise (ranks and trace), fp32 within 1e-6."""
     rg = _reference_side(reference, "c4")
     dg, info = _device_side("c4")
     assert info["row_ptr_64"] == 1 and info["nnz"] > 1_000_000_000
     _check_csr(rg, dg, info)
     rg._csr = None
     gc.collect()
-    want = _check_solves(cheb, rg, dg, _threads(), fp32=False)
+    want = _check_solves(cheb, rg, dg, _threads(), fp32=True)
     # the mass ledger of the reference's own trace holds for ours too
     t = cheb.coefficients(C, 39)
     n = float(info["n"])
