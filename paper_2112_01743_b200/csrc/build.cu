@@ -588,6 +588,16 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
         }
     }
     HostNarrow hn;
+    struct CopyStream {  // the H2D copy stream, back to the pool once idle
+        cudaStream_t s = nullptr;
+        int device = 0;
+        ~CopyStream() {
+            if (s) {
+                cudaStreamSynchronize(s);
+                release_stream(device, s);
+            }
+        }
+    } copy_stream;
     // Large pinned uploads land in groups of old rows (~nnz / 4 entries each), so that the view
     // permutes and sorts each group while the next one is still being copied.
     ColGroups groups;
@@ -605,23 +615,47 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
     if (pageable) {
         hn.start(neighbors, nnz, n, g->col.ptr<int>(), st, g->device);
     } else if (nnz > 0) {
+        // The copy engine streams the int64 chunks back to back on its own stream into a ring
+        // of staging buffers; each chunk is narrowed on `st` once it has landed, and a slot is
+        // refilled once its narrowing is done.  (On one stream every copy would wait for the
+        // previous chunk's narrowing, which queues behind the view build's kernels.)
         const int64_t chunk = std::min<int64_t>(nnz, int64_t(1) << 25);
-        DevMem stage[2];
-        stage[0].alloc(sizeof(int64_t) * chunk);
-        if (chunk < nnz) stage[1].alloc(sizeof(int64_t) * chunk);
-        int i = 0;
+        const int64_t nchunks = (nnz + chunk - 1) / chunk;
+        const int ring = (int)std::min<int64_t>(nchunks, 4);
+        copy_stream.s = pooled_stream(g->device);
+        copy_stream.device = g->device;
+        cudaStream_t cs = copy_stream.s;
+        CHEB_CUDA_CHECK(cudaStreamWaitEvent(cs, ev_rp, 0));  // after the offsets (and flag reset)
+        std::vector<DevMem> stage((size_t)ring);
+        std::vector<cudaEvent_t> copied((size_t)ring, nullptr), narrowed((size_t)ring, nullptr);
+        for (int r = 0; r < ring; ++r) {
+            stage[(size_t)r].alloc(sizeof(int64_t) * chunk);
+            CHEB_CUDA_CHECK(cudaEventCreateWithFlags(&copied[(size_t)r], cudaEventDisableTiming));
+            CHEB_CUDA_CHECK(cudaEventCreateWithFlags(&narrowed[(size_t)r], cudaEventDisableTiming));
+        }
+        CHEB_CUDA_CHECK(cudaEventRecord(ev_col, st));  // staging allocated (stream-ordered on st)
+        CHEB_CUDA_CHECK(cudaStreamWaitEvent(cs, ev_col, 0));
         size_t next_group = 0;
-        for (int64_t off = 0; off < nnz; off += chunk, i ^= 1) {
-            const int64_t c = std::min(chunk, nnz - off);
-            CHEB_CUDA_CHECK(cudaMemcpyAsync(stage[i].get(), neighbors + off, sizeof(int64_t) * c,
-                                            cudaMemcpyHostToDevice, st));
-            k_narrow_col<<<grid_for(c), kBuildThreads, 0, st>>>(stage[i].ptr<int64_t>(), c, n, off,
+        for (int64_t i = 0; i < nchunks; ++i) {
+            const int64_t off = i * chunk, c = std::min(chunk, nnz - off);
+            const size_t r = (size_t)(i % ring);
+            if (i >= ring) CHEB_CUDA_CHECK(cudaStreamWaitEvent(cs, narrowed[r], 0));
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(stage[r].get(), neighbors + off, sizeof(int64_t) * c,
+                                            cudaMemcpyHostToDevice, cs));
+            CHEB_CUDA_CHECK(cudaEventRecord(copied[r], cs));
+            CHEB_CUDA_CHECK(cudaStreamWaitEvent(st, copied[r], 0));
+            k_narrow_col<<<grid_for(c), kBuildThreads, 0, st>>>(stage[r].ptr<int64_t>(), c, n, off,
                                                                  g->col.ptr<int>() + off, bad);
             CHEB_CUDA_CHECK(cudaGetLastError());
+            CHEB_CUDA_CHECK(cudaEventRecord(narrowed[r], st));
             while (next_group < groups.ready.size() && offsets[groups.row_cut[next_group + 1]] <= off + c)
                 CHEB_CUDA_CHECK(cudaEventRecord(groups.ready[next_group++], st));
         }
         while (next_group < groups.ready.size()) CHEB_CUDA_CHECK(cudaEventRecord(groups.ready[next_group++], st));
+        for (int r = 0; r < ring; ++r) {  // st has waited on every copy: the staging frees on st are safe
+            cudaEventDestroy(copied[(size_t)r]);
+            cudaEventDestroy(narrowed[(size_t)r]);
+        }
     } else {
         for (auto& e : groups.ready) CHEB_CUDA_CHECK(cudaEventRecord(e, st));
     }
