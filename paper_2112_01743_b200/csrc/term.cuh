@@ -469,6 +469,24 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
             }
         }
     }
+    // LSU-path variant (prefetch < 0): tile i + |prefetch|'s column-id lines and row operands
+    // prefetched into L2 with prefetch.global.L2 by lanes 0-11 when its descriptor is in the
+    // current block (no descriptor wait, no TMA-unit traffic)
+    if (kExp && a.prefetch < 0 && lane < 12) {
+        const int j = i - a.prefetch;
+        if (j < nt && j / kDescBlock == i / kDescBlock) {
+            const TileR dp = tile_of(ws.desc[(j / kDescBlock) & 1][j % kDescBlock]);
+            const int64_t a0 = dp.z0 & ~int64_t(31);
+            const int lines = (int)((dp.z0 + dp.cnt - a0 + 31) >> 5);
+            if (lane < 9) {
+                if (lane < lines) asm volatile("prefetch.global.L2 [%0];" :: "l"(a.col + a0 + 32 * lane));
+            } else if (!(dp.meta & kTileChunk)) {
+                const void* p = lane == 9 ? (const void*)(a.rp + dp.r0)
+                                          : lane == 10 ? (const void*)(prev_src<EPI>(a) + dp.r0) : (const void*)(a.acc + dp.r0);
+                asm volatile("prefetch.global.L2 [%0];" :: "l"(p));
+            }
+        }
+    }
     const int t = w + i * S;  // tile id (slot of a hub-row partial)
     mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
     if (kExp && a.tune_skip &&

@@ -38,5 +38,7 @@ def run(label, **kv):
 
 
 run("default")
-for w in (50_000, 100_000, 340_000, 1_000_000):
-    run(f"skip hub warm gathers < {w}", skipwarm=w)
+for P in (-1, -2, -3, -4):
+    run(f"LSU L2 prefetch {-P} ahead", prefetch=P)
+run("nogather", nogather=1)
+run("nogather LSU prefetch 2", nogather=1, prefetch=-2)
