@@ -603,7 +603,7 @@ void upload_csr(cheb_graph* g, const int64_t* offsets, const int64_t* neighbors,
     ColGroups groups;
     const bool view_here = g->part.G == 1 && !g->part.comm && !g->peer && n > 0;
     if (view_here && !pageable && nnz >= (int64_t(1) << 26)) {
-        constexpr int K = 4;
+        const int K = std::max(1, std::min(tuning().upgroups, 64));
         groups.row_cut.assign(K + 1, n);
         groups.row_cut[0] = 0;
         for (int i = 1; i < K; ++i)
@@ -1134,21 +1134,60 @@ PinnedArena& pinned_arena() {
     static PinnedArena* a = new PinnedArena();  // never destroyed: outlives every handle
     return *a;
 }
+// Pinned (mapped) host memory -> device by a kernel reading it over the bus.  During an
+// upload the copy engine is busy with the neighbour DMA (8.4 GB on config 4) and a
+// cudaMemcpyAsync of the view's tiles and programs waited behind all of it (~150 ms); the
+// kernel's reads interleave with the DMA instead.
+__global__ void k_pull_host(const unsigned char* __restrict__ src, size_t bytes, unsigned char* __restrict__ dst) {
+    const size_t n16 = bytes / 16;
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = tid; i < n16; i += nth)
+        reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (size_t i = n16 * 16 + tid; i < bytes; i += nth) dst[i] = src[i];
+}
+void h2d_pinned(void* dst, const void* pinned, size_t bytes, cudaStream_t st) {
+    void* dsrc = nullptr;
+    const bool aligned = ((uintptr_t)dst & 15) == 0 && ((uintptr_t)pinned & 15) == 0;
+    if (bytes > 0 && aligned && tuning().pull && cudaHostGetDevicePointer(&dsrc, const_cast<void*>(pinned), 0) == cudaSuccess) {
+        const int grid = (int)std::min<size_t>((bytes / 16 + kBuildThreads - 1) / kBuildThreads + 1, 148 * 8);
+        k_pull_host<<<grid, kBuildThreads, 0, st>>>(static_cast<const unsigned char*>(dsrc), bytes,
+                                                    static_cast<unsigned char*>(dst));
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        return;
+    }
+    cudaGetLastError();
+    if (bytes > 0) CHEB_CUDA_CHECK(cudaMemcpyAsync(dst, pinned, bytes, cudaMemcpyHostToDevice, st));
+}
 void h2d_staged(void* dst, const void* src, size_t bytes, int slot, cudaStream_t st) {
     void* h = pinned_arena().get(slot, bytes);
     std::memcpy(h, src, bytes);
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(dst, h, bytes, cudaMemcpyHostToDevice, st));
+    h2d_pinned(dst, h, bytes, st);
 }
 
-// Greedy tiling of the degree-sorted rows (runs of equal degree, descending).
-static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
-                                    const std::vector<int64_t>& run_cnt, int64_t n, int64_t nnz,
-                                    int64_t* n_hub, int* n_chunk_tiles, std::vector<int>& hub_first) {
-    std::vector<Tile> tiles;
-    int64_t row = 0, z = 0;
+// Greedy tiling of the degree-sorted rows (runs of equal degree, descending), emitted per
+// run rather than per tile: a run of hub rows (degree > kWarpNnz) is one segment of
+// ceil(d / kWarpNnz) chunk tiles per row; a run of short rows is one segment of its whole
+// tiles (kf = min(32, kWarpNnz / d) rows each) plus single tiles where a tile spans a run
+// boundary.  k_expand_tiles writes the tiles on the device, so an upload does not push the
+// tile list (16 B per tile, 67 MB on config 4) over a bus the neighbour DMA is saturating.
+struct TileSeg {
+    int64_t z0;     // nnz_begin of the segment's first tile
+    int32_t row0;   // row_begin of its first tile
+    int32_t tile0;  // id of its first tile
+    int32_t count;  // tiles
+    int32_t d;      // row degree (single tiles: unused)
+    int32_t k;      // rows per tile (pack) | chunk tiles per row (kTileChunk)
+    int32_t meta;   // pack: log2 lanes per row; chunk: kTileChunk
+};
+
+static std::vector<TileSeg> make_tile_segs(const std::vector<int64_t>& run_deg, const std::vector<int64_t>& run_cnt,
+                                           int64_t n, int64_t nnz, SolverView& V) {
+    std::vector<TileSeg> segs;
+    int64_t row = 0, z = 0, tile = 0;
     int64_t cur_rows = 0, cur_nnz = 0, cur_row0 = 0, cur_z0 = 0, cur_dmax = 0;
-    *n_hub = 0;
-    *n_chunk_tiles = 0;
+    V.n_hub = 0;
+    V.n_chunk_tiles = 0;
+    for (int b = 0; b < 7; ++b) V.bin_tiles[b] = V.bin_rows[b] = V.bin_nnz[b] = 0;
     auto lanes_log2 = [](int64_t dmax, int64_t rows) {
         // lanes per row: as many as 32 lanes allow for the tile's rows, but no more than
         // ~dmax/4 (each lane then walks >= 4 nnz; rows of a tile have similar degree)
@@ -1156,9 +1195,17 @@ static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
         while (lg < 5 && (rows << (lg + 1)) <= 32 && (int64_t(4) << (lg + 1)) <= dmax + 3) ++lg;
         return lg;
     };
+    auto emit = [&](int64_t z0, int64_t r0, int64_t cnt, int64_t d, int64_t k, int meta, int64_t rows, int64_t nz) {
+        segs.push_back(TileSeg{z0, (int32_t)r0, (int32_t)tile, (int32_t)cnt, (int32_t)d, (int32_t)k, meta});
+        const int bin = (meta & kTileChunk) ? 6 : (meta & 0xf);
+        V.bin_tiles[bin] += cnt;
+        V.bin_rows[bin] += rows;
+        V.bin_nnz[bin] += nz;
+        tile += cnt;
+    };
     auto close = [&] {
         if (cur_rows == 0) return;
-        tiles.push_back(Tile{cur_z0, (int32_t)cur_row0, (int32_t)lanes_log2(cur_dmax, cur_rows)});
+        emit(cur_z0, cur_row0, 1, cur_dmax, cur_rows, lanes_log2(cur_dmax, cur_rows), cur_rows, cur_nnz);
         cur_rows = cur_nnz = 0;
     };
     for (size_t r = 0; r < run_deg.size(); ++r) {
@@ -1166,19 +1213,27 @@ static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
         int64_t c = run_cnt[r];
         if (d > kWarpNnz) {
             close();
-            for (int64_t i = 0; i < c; ++i) {
-                const int64_t nch = (d + kWarpNnz - 1) / kWarpNnz;
-                hub_first.push_back((int)tiles.size());
-                for (int64_t j = 0; j < nch; ++j) tiles.push_back(Tile{z + j * kWarpNnz, (int32_t)row, kTileChunk});
-                *n_chunk_tiles += (int)nch;
-                ++row;
-                z += d;
-            }
-            *n_hub += c;
+            const int64_t nch = (d + kWarpNnz - 1) / kWarpNnz;
+            emit(z, row, c * nch, d, nch, kTileChunk, 0, c * d);
+            V.n_chunk_tiles += (int)(c * nch);
+            V.n_hub += c;
+            row += c;
+            z += c * d;
             continue;
         }
         while (c > 0) {
             if (cur_rows == 0) {
+                // whole tiles of kf rows: each closes as soon as it is full (32 rows, or no
+                // room for another row of degree d)
+                const int64_t kf = d > 0 ? std::min<int64_t>(kWarpRows, kWarpNnz / d) : 0;
+                const int64_t m = kf > 0 ? c / kf : 0;
+                if (m > 0) {
+                    emit(z, row, m, d, kf, lanes_log2(d, kf), m * kf, m * kf * d);
+                    row += m * kf;
+                    z += m * kf * d;
+                    c -= m * kf;
+                    continue;
+                }
                 cur_row0 = row;
                 cur_z0 = z;
                 cur_dmax = d;
@@ -1200,8 +1255,218 @@ static std::vector<Tile> make_tiles(const std::vector<int64_t>& run_deg,
     }
     close();
     if (row != n || z != nnz) fail(CHEB_CUDA, "tiling does not cover the graph");
-    tiles.push_back(Tile{nnz, (int32_t)n, 0});  // sentinel
-    return tiles;
+    if (tile >= INT32_MAX) fail(CHEB_CAPACITY, "too many tiles");
+    V.bin_rows[6] = V.n_hub;
+    V.n_tiles = (int)tile;
+    return segs;
+}
+
+// Tiles (+ sentinel {nnz, n}) and hub_first (first chunk tile of each hub row, then
+// n_chunk_tiles) from the run segments: thread per tile, segment by binary search on tile0.
+__global__ void k_expand_tiles(const TileSeg* __restrict__ segs, int nseg, int n_tiles, int64_t nnz, int32_t n,
+                               int n_hub, int n_chunk_tiles, Tile* __restrict__ tiles, int* __restrict__ hub_first) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= n_tiles; t += (int64_t)gridDim.x * blockDim.x) {
+        if (t == n_tiles) {
+            tiles[t] = Tile{nnz, n, 0};
+            hub_first[n_hub] = n_chunk_tiles;
+            continue;
+        }
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {  // last segment with tile0 <= t
+            const int mid = (lo + hi + 1) >> 1;
+            if (segs[mid].tile0 <= t) lo = mid;
+            else hi = mid - 1;
+        }
+        const TileSeg sg = segs[lo];
+        const int64_t i = t - sg.tile0;
+        if (sg.meta & kTileChunk) {
+            const int64_t r = i / sg.k, q = i % sg.k;
+            tiles[t] = Tile{sg.z0 + r * sg.d + q * kWarpNnz, (int32_t)(sg.row0 + r), kTileChunk};
+            if (q == 0) hub_first[sg.row0 + r] = (int)t;
+        } else {
+            tiles[t] = Tile{sg.z0 + i * sg.k * (int64_t)sg.d, (int32_t)(sg.row0 + i * sg.k), sg.meta};
+        }
+    }
+}
+
+// One launch's warp program from the tile list (identity order): tile t is entry t / S of
+// warp t % S.  A chunk tile's WTile.row_begin holds its tile id (its hub_part slot).
+__global__ void k_build_program(const Tile* __restrict__ tiles, int n_tiles, int S, int len, WTile* __restrict__ prog) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tiles; t += (int64_t)gridDim.x * blockDim.x) {
+        const Tile a = tiles[t], b = tiles[t + 1];
+        const bool chunk = (a.meta & kTileChunk) != 0;
+        WTile w;
+        w.nnz_begin = a.nnz_begin;
+        w.row_begin = chunk ? (int32_t)t : a.row_begin;
+        w.cnt = (uint16_t)(b.nnz_begin - a.nnz_begin);
+        w.rows = (uint8_t)(chunk ? 1 : (b.row_begin - a.row_begin));
+        w.meta = (uint8_t)a.meta;
+        prog[(size_t)(t % S) * len + t / S] = w;
+    }
+}
+
+// Tile-bin statistics of the view (host): 0..5 = pack tiles with 2^b lanes per row, 6 = chunk tiles.
+static void tile_stats(SolverView& V, const std::vector<Tile>& tiles) {
+    for (int b = 0; b < 7; ++b) V.bin_tiles[b] = V.bin_rows[b] = V.bin_nnz[b] = 0;
+    for (int t = 0; t < V.n_tiles; ++t) {
+        const Tile& a = tiles[t];
+        const Tile& b = tiles[t + 1];
+        const int bin = (a.meta & kTileChunk) ? 6 : (a.meta & 0xf);
+        ++V.bin_tiles[bin];
+        V.bin_nnz[bin] += b.nnz_begin - a.nnz_begin;
+        V.bin_rows[bin] += (a.meta & kTileChunk) ? 0 : (int64_t)(b.row_begin - a.row_begin);
+    }
+    V.bin_rows[6] = V.n_hub;
+}
+
+// Per-warp tile programs (warp-major, each padded to whole descriptor blocks): entry i of
+// a launch's tile list goes to warp i % S, position i / S.  lists == null: one launch over
+// every tile in tile order; otherwise one launch per list (V.phases, ranges filled by the
+// caller), the programs concatenated.  A chunk tile's WTile.row_begin holds its tile id:
+// the slot of its partial in hub_part, whatever position it runs at.
+static void upload_programs(SolverView& V, const std::vector<Tile>& tiles,
+                            const std::vector<std::vector<int>>* lists, cudaStream_t st) {
+    const int S = V.grid * kWarps;
+    auto len_of = [&](int64_t cnt) {
+        const int64_t per = (cnt + S - 1) / S;
+        return (int)std::max<int64_t>(kDescBlock, (per + kDescBlock - 1) / kDescBlock * kDescBlock);
+    };
+    const int nl = lists ? (int)lists->size() : 1;
+    std::vector<int> lens(nl);
+    size_t np = 0;
+    for (int p = 0; p < nl; ++p) {
+        lens[p] = len_of(lists ? (int64_t)(*lists)[p].size() : (int64_t)V.n_tiles);
+        np += (size_t)S * lens[p];
+    }
+    auto* prog = static_cast<WTile*>(pinned_arena().get(1, sizeof(WTile) * np));  // built in place
+    std::memset(prog, 0, sizeof(WTile) * np);
+    auto wtile = [&](int t) {
+        const Tile& a = tiles[t];
+        const Tile& b = tiles[t + 1];
+        const bool chunk = (a.meta & kTileChunk) != 0;
+        WTile w;
+        w.nnz_begin = a.nnz_begin;
+        w.row_begin = chunk ? t : a.row_begin;
+        w.cnt = (uint16_t)(b.nnz_begin - a.nnz_begin);
+        w.rows = (uint8_t)(chunk ? 1 : (b.row_begin - a.row_begin));
+        w.meta = (uint8_t)a.meta;
+        return w;
+    };
+    size_t off = 0;
+    if (lists) V.phases.resize(nl);
+    else V.phases.clear();
+    for (int p = 0; p < nl; ++p) {
+        WTile* pg = prog + off;
+        const int L = lens[p];
+        const int cnt = lists ? (int)(*lists)[p].size() : V.n_tiles;
+        for (int i = 0; i < cnt; ++i) pg[(size_t)(i % S) * L + i / S] = wtile(lists ? (*lists)[p][i] : i);
+        if (lists) {
+            V.phases[p].prog_off = (int64_t)off;
+            V.phases[p].prog_len = L;
+            V.phases[p].ntiles = cnt;
+        }
+        off += (size_t)S * L;
+    }
+    V.prog_len = lens[0];
+    V.prog.alloc(sizeof(WTile) * np);
+    h2d_pinned(V.prog.get(), prog, sizeof(WTile) * np, st);
+}
+
+// Column-blocked chunk schedule (x larger than L2; rows hold ascending ids).  x ids are cut
+// into K blocks; every hub row's entries are split where its ids cross a block boundary
+// (binary search per (row, boundary): k_hub_splits) and each piece is cut into chunk tiles of
+// <= kWarpNnz entries, so a chunk gathers from one block only.  A term then runs one launch
+// per block, highest first, each under an L2 window over its slice of x: the gathers of a
+// launch hit an L2-resident slice instead of missing across all of x (config 4: 136 MB of
+// fp64 x against a 126 MB L2).  Block 0 (the hot prefix and the hubs) runs last, with the
+// pack tiles.  Chunk partials are still combined in position order by k_hub_finalize
+// (tile ids stay in row order), so the schedule is deterministic.
+template <class RPN>
+__global__ void k_hub_splits(const RPN* __restrict__ rp, const int* __restrict__ col, int64_t n_hub,
+                             const int* __restrict__ bounds, int nb, int* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_hub * nb;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = i / nb;
+        const int key = bounds[i % nb];
+        int64_t lo = rp[h], hi = rp[h + 1];
+        const int64_t b = lo;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (col[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        out[i] = (int)(lo - b);
+    }
+}
+
+template <class RPN>
+static void column_block_schedule(SolverView& V, int K, int64_t x_len, cudaStream_t st) {
+    const int64_t n_hub = V.n_hub;
+    std::vector<Tile> tiles((size_t)V.n_tiles + 1);
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(tiles.data(), V.tiles.get(), sizeof(Tile) * tiles.size(), cudaMemcpyDeviceToHost, st));
+    const int nb = K - 1;
+    std::vector<int> bounds(nb);
+    for (int j = 1; j < K; ++j) {
+        int64_t b = x_len * j / K;
+        if (K == 2 && tuning().colsplit_pct > 0 && tuning().colsplit_pct < 100) b = x_len * tuning().colsplit_pct / 100;
+        bounds[j - 1] = (int)(b & ~int64_t(31));  // whole 256-byte x segments per window
+    }
+    std::vector<int> splits((size_t)n_hub * nb);
+    {
+        DevMem d_b(sizeof(int) * nb), d_s(sizeof(int) * std::max<size_t>(splits.size(), 1));
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(d_b.get(), bounds.data(), sizeof(int) * nb, cudaMemcpyHostToDevice, st));
+        k_hub_splits<RPN><<<grid_for(n_hub * nb), kBuildThreads, 0, st>>>(V.row_ptr.ptr<RPN>(), V.col.ptr<int>(), n_hub,
+                                                                        d_b.ptr<int>(), nb, d_s.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        CHEB_CUDA_CHECK(cudaMemcpyAsync(splits.data(), d_s.get(), sizeof(int) * splits.size(), cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+    const int old_chunks = V.n_chunk_tiles;
+    std::vector<Tile> nt;
+    std::vector<int> blk;  // block of each chunk tile
+    std::vector<int> hub_first;
+    nt.reserve(tiles.size() + (size_t)n_hub * nb);
+    int h = -1;
+    for (int t = 0; t < old_chunks;) {  // the old chunk tiles of row h are consecutive
+        h = tiles[t].row_begin;
+        int t1 = t;
+        while (t1 < old_chunks && tiles[t1].row_begin == h) ++t1;
+        const int64_t z = tiles[t].nnz_begin, d = tiles[t1].nnz_begin - z;
+        hub_first.push_back((int)nt.size());
+        int64_t a = 0;
+        for (int j = 0; j < K; ++j) {
+            const int64_t e = j < nb ? (int64_t)splits[(size_t)h * nb + j] : d;
+            for (int64_t p = a; p < e; p += kWarpNnz) {
+                nt.push_back(Tile{z + p, (int32_t)h, kTileChunk});
+                blk.push_back(j);
+            }
+            a = std::max(a, e);
+        }
+        t = t1;
+    }
+    if ((int64_t)hub_first.size() != n_hub) fail(CHEB_CUDA, "column-block schedule: hub rows do not match");
+    const int new_chunks = (int)nt.size();
+    hub_first.push_back(new_chunks);
+    for (size_t t = (size_t)old_chunks; t < tiles.size(); ++t) nt.push_back(tiles[t]);  // pack tiles + sentinel
+    tiles.swap(nt);
+    V.n_chunk_tiles = new_chunks;
+    V.n_tiles = (int)tiles.size() - 1;
+    tile_stats(V, tiles);
+    std::vector<std::vector<int>> lists(K);
+    for (int t = 0; t < new_chunks; ++t) lists[(size_t)(K - 1 - blk[t])].push_back(t);
+    for (int t = new_chunks; t < V.n_tiles; ++t) lists[(size_t)K - 1].push_back(t);
+    upload_programs(V, tiles, &lists, st);
+    for (int p = 0; p < K; ++p) {
+        const int j = K - 1 - p;
+        V.phases[p].x_lo = j == 0 ? 0 : bounds[j - 1];
+        V.phases[p].x_hi = j == nb ? x_len : bounds[j];
+        V.phases[p].epi = p == K - 1;
+    }
+    V.hub_first.alloc(sizeof(int) * hub_first.size());
+    h2d_staged(V.hub_first.get(), hub_first.data(), sizeof(int) * hub_first.size(), 0, st);
+    V.tiles.alloc(sizeof(Tile) * tiles.size());
+    h2d_staged(V.tiles.get(), tiles.data(), sizeof(Tile) * tiles.size(), 2, st);
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
 // Each of the first `segs` view rows' renamed ids in ascending order (cub segmented sort,
@@ -1315,7 +1580,6 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     // (degree-only: overlaps the neighbour upload when built from upload_csr).
     std::lock_guard<std::mutex> staging_lock(pinned_arena().mu);
     std::vector<int64_t> run_deg, run_cnt;
-    std::vector<int> hub_first;
     if (nl > 0) {
         DevMem uniq(sizeof(int64_t) * nl), cnts(sizeof(int64_t) * nl), nruns(sizeof(int64_t));
         size_t bytes = 0;
@@ -1336,50 +1600,37 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         std::memcpy(run_cnt.data(), hc, sizeof(int64_t) * R);
     }
     dbg_mark("  view: runs read");
-    const std::vector<Tile> tiles = make_tiles(run_deg, run_cnt, nl, nnz_l, &V.n_hub, &V.n_chunk_tiles, hub_first);
-    hub_first.push_back(V.n_chunk_tiles);
-    V.hub_first.alloc(sizeof(int) * hub_first.size());
-    h2d_staged(V.hub_first.get(), hub_first.data(), sizeof(int) * hub_first.size(), 0, st);
-    V.n_tiles = (int)tiles.size() - 1;
-    for (int b = 0; b < 7; ++b) V.bin_tiles[b] = V.bin_rows[b] = V.bin_nnz[b] = 0;
-    for (int t = 0; t < V.n_tiles; ++t) {
-        const Tile& a = tiles[t];
-        const Tile& b = tiles[t + 1];
-        const int bin = (a.meta & kTileChunk) ? 6 : (a.meta & 0xf);
-        ++V.bin_tiles[bin];
-        V.bin_nnz[bin] += b.nnz_begin - a.nnz_begin;
-        V.bin_rows[bin] += (a.meta & kTileChunk) ? 0 : (int64_t)(b.row_begin - a.row_begin);
-    }
-    V.bin_rows[6] = V.n_hub;
     {
+        const std::vector<TileSeg> segs = make_tile_segs(run_deg, run_cnt, nl, nnz_l, V);
         int dev = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         V.grid = std::max(1, std::min(sms, (V.n_tiles + kWarps - 1) / kWarps));
-    }
-    {   // per-warp programs (warp-major), padded to whole descriptor blocks
+        DevMem d_segs(sizeof(TileSeg) * std::max<size_t>(segs.size(), 1));
+        if (!segs.empty()) h2d_staged(d_segs.get(), segs.data(), sizeof(TileSeg) * segs.size(), 0, st);
+        V.tiles.alloc(sizeof(Tile) * ((size_t)V.n_tiles + 1));
+        V.hub_first.alloc(sizeof(int) * ((size_t)V.n_hub + 1));
+        k_expand_tiles<<<grid_for((int64_t)V.n_tiles + 1), kBuildThreads, 0, st>>>(
+            d_segs.ptr<TileSeg>(), (int)segs.size(), V.n_tiles, nnz_l, (int32_t)nl, (int)V.n_hub, V.n_chunk_tiles,
+            V.tiles.ptr<Tile>(), V.hub_first.ptr<int>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
         const int S = V.grid * kWarps;
         const int per = (V.n_tiles + S - 1) / S;
         V.prog_len = std::max(kDescBlock, (per + kDescBlock - 1) / kDescBlock * kDescBlock);
         const size_t np = (size_t)S * V.prog_len;
-        auto* prog = static_cast<WTile*>(pinned_arena().get(1, sizeof(WTile) * np));  // built in place
-        std::memset(prog, 0, sizeof(WTile) * np);
-        for (int t = 0; t < V.n_tiles; ++t) {
-            const Tile& a = tiles[t];
-            const Tile& b = tiles[t + 1];
-            WTile w;
-            w.nnz_begin = a.nnz_begin;
-            w.row_begin = a.row_begin;
-            w.cnt = (uint16_t)(b.nnz_begin - a.nnz_begin);
-            w.rows = (uint8_t)((a.meta & kTileChunk) ? 1 : (b.row_begin - a.row_begin));
-            w.meta = (uint8_t)a.meta;
-            prog[(size_t)(t % S) * V.prog_len + t / S] = w;
-        }
         V.prog.alloc(sizeof(WTile) * np);
-        CHEB_CUDA_CHECK(cudaMemcpyAsync(V.prog.get(), prog, sizeof(WTile) * np, cudaMemcpyHostToDevice, st));
+        CHEB_CUDA_CHECK(cudaMemsetAsync(V.prog.get(), 0, sizeof(WTile) * np, st));
+        if (V.n_tiles > 0)
+            k_build_program<<<grid_for(V.n_tiles), kBuildThreads, 0, st>>>(V.tiles.ptr<Tile>(), V.n_tiles, S,
+                                                                         V.prog_len, V.prog.ptr<WTile>());
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        V.phases.clear();
+        if (dbg_on()) {
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+            dbg_mark(("  view: tiles + programs on the device (" + std::to_string(segs.size()) + " segments, " +
+                      std::to_string(V.n_tiles) + " tiles)").c_str());
+        }
     }
-    V.tiles.alloc(sizeof(Tile) * tiles.size());
-    h2d_staged(V.tiles.get(), tiles.data(), sizeof(Tile) * tiles.size(), 2, st);
     V.col.alloc(sizeof(int) * std::max<int64_t>(nnz_l, 1) + 64);  // TMA reads round up to 16 B
     // When x does not fit L2 (config 4), ascending renamed ids within each row: a row's
     // gathers then walk x in address order (DRAM page / sector locality; C4 4.49 -> 3.95
@@ -1483,6 +1734,11 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
             const int64_t segs = V.n_hub;
             const int64_t items = (int64_t)read_scalar(V.row_ptr.ptr<RPN>() + segs, st);
             sort_view_rows_t<RPN>(V, segs, items, st);
+        }
+        if (sort_grouped && V.n_hub > 0 && tuning().colblocks > 1) {  // opt-in: measured no gain on C4
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+            column_block_schedule<RPN>(V, tuning().colblocks, V.x_len, st);
+            dbg_mark("  view: column-block schedule");
         }
         if (sort_grouped && tuning().chunksched > 1 && V.n_chunk_tiles > 0) {  // the sort undid the chunk order
             k_schedule_chunks_inplace<RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(

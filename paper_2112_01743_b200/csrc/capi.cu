@@ -134,7 +134,7 @@ void chebgpu::retain_pool_memory() {
     }
 }
 
-bool chebgpu::l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* w) {
+bool chebgpu::l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* w, size_t decide_bytes) {
     // Only when the vector does not fit L2 on its own (config 4: x = 136 MB): reserving
     // persisting L2 otherwise shrinks the normal L2 the other streams use (measured: C2 and
     // C5 slower, C4 12% faster).  The device-wide carve-out follows the decision.
@@ -154,7 +154,7 @@ bool chebgpu::l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* 
         }
         init[dev] = true;
     }
-    const bool use = persist_max[dev] > 0 && window_max[dev] > 0 && bytes > l2_size[dev];
+    const bool use = persist_max[dev] > 0 && window_max[dev] > 0 && (decide_bytes ? decide_bytes : bytes) > l2_size[dev];
     const size_t want = use ? persist_max[dev] : 0;
     if (want != current[dev]) {
         cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
@@ -1131,6 +1131,8 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "spmm_hub_mb") tuning().spmm_hub_mb = value;
         else if (k == "spmm_xpol") tuning().spmm_xpol = value;
         else if (k == "sortrows") tuning().sortrows = value;
+        else if (k == "colblocks") tuning().colblocks = value;  // applies to views built afterwards
+        else if (k == "colsplit_pct") tuning().colsplit_pct = value;  // applies to views built afterwards
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }

@@ -60,7 +60,8 @@ void release_stream(int device, cudaStream_t s);
 // L2 persistence for the gathered vector: an access-policy window over the first `bytes` of
 // `base` (the degree-sorted hot prefix of x), sized to the device's persisting-L2 limit.
 // Returns false when the device offers no persisting L2.
-bool l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* w);
+// decide_bytes: the size that decides whether a window is used at all (default: bytes)
+bool l2_window(const void* base, size_t bytes, cudaAccessPolicyWindow* w, size_t decide_bytes = 0);
 
 inline bool alloc_debug() {
     static const bool on = std::getenv("CHEB_DEBUG_ALLOC") != nullptr;
@@ -232,6 +233,17 @@ struct SolverView {
     int64_t n_hub = 0;     // rows [0, n_hub) with degree > kWarpNnz (chunk tiles)
     int n_chunk_tiles = 0;
     DevMem hub_first;      // int32 [n_hub + 1]: first chunk tile of each hub row
+    // Column-blocked schedule (x larger than L2): hub-row chunks never straddle a block of x
+    // ids, and each term runs one launch per block (highest block first) whose program holds
+    // that block's chunks, under an L2 window over that slice of x; the last launch (block 0)
+    // also runs the pack tiles and the row epilogues.  Empty: one launch over `prog`.
+    struct Phase {
+        int64_t prog_off = 0;  // WTile offset of this launch's program inside `prog`
+        int prog_len = 0, ntiles = 0;
+        int64_t x_lo = 0, x_hi = 0;  // x ids this launch's chunks gather (its L2 window)
+        bool epi = false;            // runs pack tiles (row epilogues, trace partials)
+    };
+    std::vector<Phase> phases;
     bool sorted_rows = false;  // rows hold their renamed ids in ascending order
     // Row partition (G > 1): bit r of push_mask[u] = rank r has a row with neighbour u, i.e.
     // needs x[u] (symmetric graph: u has a neighbour owned by r).  The halo-only push stores
@@ -422,6 +434,11 @@ struct Tuning {
     int spmm_hub_mb = 64; // batched path: MB of X rows (the hub prefix) gathered under evict-last
     int spmm_xpol = 0;  // batched path x_{k+1} stores: 0 normal, 1 evict-last hub prefix + streaming rest
     int skipwarm = 0;   // experiment (wrong results): hub-row gathers of ids in [H, skipwarm) dropped
+    int colblocks = 0;  // K > 1: hub-row chunks cut at K column blocks of x, one term launch per block
+                        // under an L2 window over its slice (rows sorted by id only; C4: no gain, off)
+    int upgroups = 16;  // groups of old rows an upload lands in, each permuted + sorted as it lands (C4: 4 -> 16 groups, upload 200 -> 163 ms)
+    int pull = 1;       // view tiles / programs pulled from pinned host memory by a kernel (not the copy engine)
+    int colsplit_pct = -1; // K = 2: first block boundary at this percent of x (-1: equal halves)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -444,6 +461,10 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_PREFETCH")) x.prefetch = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_SPMM_HUB_MB")) x.spmm_hub_mb = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_SPMM_XPOL")) x.spmm_xpol = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_COLBLOCKS")) x.colblocks = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_PULL")) x.pull = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_UPGROUPS")) x.upgroups = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_COLSPLIT_PCT")) x.colsplit_pct = std::atoi(e);
         return x;
     }();
     return t;

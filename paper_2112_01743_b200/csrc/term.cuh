@@ -487,7 +487,6 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
             }
         }
     }
-    const int t = w + i * S;  // tile id (slot of a hub-row partial)
     mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
     if (kExp && a.tune_skip &&
         (a.tune_skip >= 16 ? (((d.meta & kTileChunk) ? 6 : (d.meta & 0xf)) != a.tune_skip - 16)
@@ -538,7 +537,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
             sum = (double)blk;
         }
         sum = warp_sum_v(sum);
-        if (lane == 0) a.hub_part[t] = (double)sum;
+        if (lane == 0) a.hub_part[d.r0] = (double)sum;  // a chunk tile's row_begin is its tile id
     } else {
         // rows of similar degree: L lanes per row, row g owned by lanes [g L, g L + L)
         const int lg = d.meta & 0xf;
@@ -1105,26 +1104,50 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         // x buffers are cudaMalloc'ed (256-B aligned): whole 128-B lines of x_out only
         ab.xdiscard_len = (EPI == EPI_CPAA && tuning().xdiscard && !a.push && g->part.G == 1 && !g->part.comm)
                               ? (g->view.x_len * (int64_t)sizeof(V) / 128) * 128 / (int64_t)sizeof(V) : 0;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(g->view.grid);
-        cfg.blockDim = dim3(kWarps * 32);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[2];
-        cfg.attrs = attr;
-        cfg.numAttrs = 0;
-        // keep the hot (degree-sorted) prefix of x_k resident in L2 across the term
-        if (tuning().l2win &&
-            l2_window(a.x_in, (size_t)std::max<int64_t>(g->view.x_len, 1) * sizeof(V),
-                      &attr[cfg.numAttrs].val.accessPolicyWindow)) {
-            attr[cfg.numAttrs++].id = cudaLaunchAttributeAccessPolicyWindow;
+        const size_t x_bytes = (size_t)std::max<int64_t>(g->view.x_len, 1) * sizeof(V);
+        auto launch = [&](const TermArgs<RP, V>& args, const WTile* prog, int plen, int ntiles, const V* win,
+                          size_t win_bytes) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(g->view.grid);
+            cfg.blockDim = dim3(kWarps * 32);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[2];
+            cfg.attrs = attr;
+            cfg.numAttrs = 0;
+            // keep the hot (degree-sorted) prefix of x_k -- or this launch's block of it --
+            // resident in L2 across the launch (only when x exceeds L2)
+            if (tuning().l2win && l2_window(win, win_bytes, &attr[cfg.numAttrs].val.accessPolicyWindow, x_bytes))
+                attr[cfg.numAttrs++].id = cudaLaunchAttributeAccessPolicyWindow;
+            if (tuning().pdl) {  // overlap this launch + prologue with the previous kernel's tail
+                attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
+            }
+            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V>, args, prog, plen, ntiles, H));
+        };
+        int launched = 0;
+        if (g->view.phases.empty()) {
+            launch(ab, g->view.prog.ptr<WTile>(), g->view.prog_len, g->view.n_tiles, a.x_in, x_bytes);
+            launched = 1;
+        } else {
+            // column-blocked schedule (build.cu column_block_schedule): one launch per block
+            // of x, chunk-only launches first; the last one runs the pack tiles and epilogues
+            for (const SolverView::Phase& ph : g->view.phases) {
+                if (ph.ntiles == 0 && !ph.epi) continue;
+                TermArgs<RP, V> pa = ab;
+                if (launched > 0) {  // once per term: start stamp, dead-line discard
+                    pa.stamp_start = nullptr;
+                    pa.xdiscard_len = 0;
+                }
+                if (!ph.epi) {
+                    pa.part = nullptr;
+                    pa.stamp_end = nullptr;
+                }
+                launch(pa, g->view.prog.ptr<WTile>() + ph.prog_off, ph.prog_len, ph.ntiles, a.x_in + ph.x_lo,
+                       (size_t)(ph.x_hi - ph.x_lo) * sizeof(V));
+                ++launched;
+            }
         }
-        if (tuning().pdl) {  // overlap this launch + prologue with the previous kernel's tail
-            attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
-        }
-        CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V>, ab, (const WTile*)g->view.prog.ptr<WTile>(),
-                                           g->view.prog_len, g->view.n_tiles, H));
         if (g->view.n_hub > 0) {
             CHEB_CUDA_CHECK(cudaGetLastError());
             const int hb = (int)std::min<int64_t>((g->view.n_hub * 32 + 255) / 256, 148 * 16);
@@ -1139,8 +1162,10 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             hc.numAttrs = tuning().pdl ? 1 : 0;
             CHEB_CUDA_CHECK(cudaLaunchKernelEx(&hc, k_hub_finalize<EPI, RP, V>, a,
                                                (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub));
-            return 2;
+            return launched + 1;
         }
+        CHEB_CUDA_CHECK(cudaGetLastError());
+        return launched;
     } else {
         if constexpr (std::is_same<V, double>::value) {
             k_term_exact<EPI, RP><<<grid1d(g->n), kThreads, 0, st>>>(a, g->n);
