@@ -245,6 +245,54 @@ __device__ __forceinline__ void gather8(const V* __restrict__ x, unsigned hot_s,
         if ((unsigned)c[q] < (unsigned)H) v[q] = lds_v(hot_s + (unsigned)c[q] * (unsigned)sizeof(V), V(0));
 }
 
+// Cold gathers through LDGSTS (cp.async.cg, 16 bytes: the aligned piece of x holding x[c])
+// into per-lane staging slots in shared memory, then LDS.  An LDG stages every in-flight load
+// in the L1 data array, and next to the shared hot prefix + warp scratch (164 KB) the L1 left
+// over bounds the random gathers in flight: measured (tools/micro_ldgsts.cu, 32 warps/SM)
+// LDG from a 64 MB table 266 -> 149 G/s and from a 136 MB table 108 -> 81 G/s once 164 KB of
+// shared memory is reserved, while cp.async.cg gathers keep 240 / 108 G/s with up to 220 KB
+// reserved (they land in shared memory and never allocate in L1).  In the term kernel itself
+// the extra instructions (LDGSTS + commit/wait + LDS per cold gather, batches of 1-4 per lane)
+// cost more than the in-flight capacity gains: C2 69.2 -> 75-81 us/term, C3 395 -> 434-464,
+// C4 4051 -> 4001-4212 (profiles/r02_gather_paths.md); off by default, -DCHEB_GATHER_ASYNC=1.
+#ifndef CHEB_GATHER_ASYNC
+#define CHEB_GATHER_ASYNC 0
+#endif
+#ifndef CHEB_STAGE_SLOTS
+#define CHEB_STAGE_SLOTS 2
+#endif
+constexpr bool kGatherAsync = CHEB_GATHER_ASYNC != 0;
+constexpr int kStageSlots = CHEB_STAGE_SLOTS;  // 16-byte slots per lane (gathers in flight per lane)
+
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// gather8 with the cold ids through the lane's staging slots (slot j at stage_s + 512 j), in
+// batches of kStageSlots.
+template <class V, int U>
+__device__ __forceinline__ void gather_staged(const V* __restrict__ x, unsigned hot_s, int H, unsigned stage_s,
+                                              const int (&c)[U], V (&v)[U]) {
+    constexpr int per16 = 16 / (int)sizeof(V);
+#pragma unroll
+    for (int b = 0; b < U; b += kStageSlots) {
+#pragma unroll
+        for (int q = b; q < b + kStageSlots && q < U; ++q)
+            if (c[q] >= H) cp_async16(stage_s + (unsigned)(q - b) * 512u, x + (c[q] & ~(per16 - 1)));
+        cp_async_wait_all();
+#pragma unroll
+        for (int q = b; q < b + kStageSlots && q < U; ++q) {
+            v[q] = V(0);
+            if ((unsigned)c[q] < (unsigned)H) v[q] = lds_v(hot_s + (unsigned)c[q] * (unsigned)sizeof(V), V(0));
+            else if (c[q] >= H)
+                v[q] = lds_v(stage_s + (unsigned)(q - b) * 512u + (unsigned)(c[q] & (per16 - 1)) * (unsigned)sizeof(V), V(0));
+        }
+    }
+}
+
 // Programmatic dependent launch: let the next kernel of the stream launch now (its CTAs
 // take SMs as this grid drains), and wait for the previous kernel's completion + memory
 // flush before reading anything it wrote.  Both are no-ops without the launch attribute.
@@ -354,6 +402,7 @@ struct alignas(16) WarpScratch {
     WTile desc[2][kDescBlock];  // TMA ring of this warp's tile program
     uint64_t colm[2];       // mbarriers of colb
     uint64_t descm[2];      // mbarriers of desc
+    alignas(16) unsigned char stage[kGatherAsync ? kStageSlots : 0][32][16];  // cold-gather slots [slot][lane]
 };
 
 template <class V>
@@ -499,6 +548,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
         return;
     }
     const int* cb = ws.colb[i & 1] + (int)(d.z0 & 7);  // tile-local position p at cb[p]
+    const unsigned stage_s = kGatherAsync ? (unsigned)__cvta_generic_to_shared(&ws.stage[0][lane][0]) : 0u;
 
     if (d.meta & kTileChunk) {
         // slice of a row with degree > kWarpNnz: partial only; completed by k_hub_finalize
@@ -524,7 +574,8 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
                 for (int q = 0; q < U; ++q)
                     if (c[q] >= H && c[q] < a.tune_skipwarm) c[q] = -1;
             }
-            gather8(a.x_in, hot_s, H, c, v);
+            if constexpr (kGatherAsync) gather_staged(a.x_in, hot_s, H, stage_s, c, v);
+            else gather8(a.x_in, hot_s, H, c, v);
         }
         double sum = 0.0;  // hub-row chunk sums in fp64 (fp32: a lane's U entries in fp32)
         if constexpr (sizeof(V) == 8) {
@@ -559,6 +610,8 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
             if (kExp && a.tune_nogather) {
 #pragma unroll
                 for (int q = 0; q < kPackUnroll; ++q) v[q] = c[q] >= 0 ? V(1) : V(0);
+            } else if constexpr (kGatherAsync) {
+                gather_staged(a.x_in, hot_s, H, stage_s, c, v);
             } else {
                 gather8(a.x_in, hot_s, H, c, v);
             }
