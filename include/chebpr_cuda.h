@@ -193,6 +193,13 @@ cheb_status cheb_graph_exchange_info(cheb_graph_t g, int64_t* halo_stores, int64
  * (first entry of every hub-row chunk tile).  Any output may be NULL. */
 cheb_status cheb_graph_view_download(cheb_graph_t g, int64_t* sizes, int64_t* row_ptr, int32_t* col,
                                      int32_t* order, int64_t* chunk_begin);
+/* Warp tiles of the solver view (new; tests and tools): *n_tiles, then per tile its first
+ * entry, first row (a chunk tile: its hub row) and meta (log2 lanes per row, or 0x10 = chunk
+ * of a hub row) for tiles [0, n_tiles] (tile n_tiles: the sentinel {nnz_local, n_local, 0});
+ * *n_launches = term-kernel launches per term (1, or K with the opt-in column-blocked
+ * schedule).  Arrays may be NULL (sizes only). */
+cheb_status cheb_graph_view_tiles(cheb_graph_t g, int64_t* n_tiles, int64_t* nnz_begin, int32_t* row_begin,
+                                  int32_t* meta, int32_t* n_launches);
 
 /* ---- solvers ---- */
 enum { CHEB_MODE_FAST = 0, CHEB_MODE_BITEXACT = 1 };

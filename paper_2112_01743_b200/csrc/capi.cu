@@ -1082,6 +1082,30 @@ cheb_status cheb_graph_view_download(cheb_graph_t g, int64_t* sizes, int64_t* ro
     });
 }
 
+cheb_status cheb_graph_view_tiles(cheb_graph_t g, int64_t* n_tiles, int64_t* nnz_begin, int32_t* row_begin,
+                                  int32_t* meta, int32_t* n_launches) {
+    return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_view_tiles");
+        need_graph(g);
+        GraphScope gs(g);
+        ensure_view(g);
+        const SolverView& V = g->view;
+        if (n_tiles) *n_tiles = V.n_tiles;
+        if (n_launches) *n_launches = V.phases.empty() ? 1 : (int32_t)V.phases.size();
+        if (nnz_begin || row_begin || meta) {
+            std::vector<Tile> t((size_t)V.n_tiles + 1);
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(t.data(), V.tiles.get(), sizeof(Tile) * t.size(), cudaMemcpyDeviceToHost,
+                                            g->stream));
+            CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+            for (size_t i = 0; i < t.size(); ++i) {
+                if (nnz_begin) nnz_begin[i] = t[i].nnz_begin;
+                if (row_begin) row_begin[i] = t[i].row_begin;
+                if (meta) meta[i] = t[i].meta;
+            }
+        }
+    });
+}
+
 cheb_status cheb_graph_partition_info(cheb_graph_t g, int64_t* lo, int64_t* hi, int64_t* nnz_local,
                                       int64_t* max_rows) {
     return guarded([&] {

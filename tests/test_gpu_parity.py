@@ -579,3 +579,134 @@ def test_trace_elapsed_is_per_term_device_time(cheb, mode):
         assert el.sum() <= lm.value * 1.05 + 0.05, (el.sum(), lm.value)
         assert len(set(np.round(el, 9))) > 1  # not one mean repeated
     dg.free()
+
+
+def _greedy_tiles(deg):
+    """The view's greedy tiling restated per row (build.cu make_tile_segs expands the same
+    tiles per run on the device): hub rows (degree > 248) in 248-entry chunks, then pack tiles
+    of <= 32 consecutive rows and <= 248 entries, lanes per row from the first row's degree."""
+    W, RW = 248, 32
+
+    def lanes_log2(dmax, rows):
+        lg = 0
+        while lg < 5 and (rows << (lg + 1)) <= 32 and (4 << (lg + 1)) <= dmax + 3:
+            lg += 1
+        return lg
+
+    tiles = []
+    z = 0
+    cur = None  # [z0, row0, dmax, rows, nnz]
+    for r, d in enumerate(deg.tolist()):
+        if d > W:
+            for j in range(0, d, W):
+                tiles.append((z + j, r, 0x10))
+            z += d
+            continue
+        if cur is not None and (cur[3] == RW or (W - cur[4]) < d):
+            tiles.append((cur[0], cur[1], lanes_log2(cur[2], cur[3])))
+            cur = None
+        if cur is None:
+            cur = [z, r, d, 0, 0]
+        cur[3] += 1
+        cur[4] += d
+        z += d
+        if cur[3] == RW or W - cur[4] < d:
+            tiles.append((cur[0], cur[1], lanes_log2(cur[2], cur[3])))
+            cur = None
+    if cur is not None:
+        tiles.append((cur[0], cur[1], lanes_log2(cur[2], cur[3])))
+    tiles.append((z, deg.size, 0))
+    return tiles
+
+
+def _tiles(lib, dg):
+    import ctypes as C
+    nt = C.c_int64()
+    nl = C.c_int32()
+    assert lib.cheb_graph_view_tiles(dg.handle, C.byref(nt), None, None, None, C.byref(nl)) == 0
+    z = np.zeros(nt.value + 1, dtype=np.int64)
+    r = np.zeros(nt.value + 1, dtype=np.int32)
+    m = np.zeros(nt.value + 1, dtype=np.int32)
+    P32 = C.POINTER(C.c_int32)
+    assert lib.cheb_graph_view_tiles(dg.handle, C.byref(nt), z.ctypes.data_as(C.POINTER(C.c_int64)),
+                                     r.ctypes.data_as(P32), m.ctypes.data_as(P32), C.byref(nl)) == 0
+    return z, r, m, nl.value
+
+
+@pytest.mark.parametrize("graph", ["chung_lu", "rmat", "fixture"])
+def test_device_tiling_matches_the_greedy_rule(cheb, graph):
+    """The tiles written on the device from per-run segments (k_expand_tiles) are exactly the
+    greedy per-row tiling: same first entry, row and lanes per row for every tile."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    if graph == "chung_lu":
+        e = Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 5000.0, 600_000, 5)
+    elif graph == "rmat":
+        e = Gen.rmat_edges(15, 16, 0.57, 0.19, 0.19, 7)
+    else:
+        e = load_golden("config1")["edges"]
+    dg, _ = cheb.build_device_graph(e, cheb.BuildOptions(drop_isolated=graph == "rmat"))
+    try:
+        v = _view(lib, dg)
+        z, r, m, launches = _tiles(lib, dg)
+    finally:
+        dg.free()
+    deg = np.diff(v["rp"])
+    assert np.all(deg[:-1] >= deg[1:])  # degree-descending view rows
+    ref = _greedy_tiles(deg)
+    assert launches == 1
+    assert z.size == len(ref)
+    assert np.array_equal(z, np.array([t[0] for t in ref], dtype=np.int64))
+    assert np.array_equal(r, np.array([t[1] for t in ref], dtype=np.int32))
+    assert np.array_equal(m, np.array([t[2] for t in ref], dtype=np.int32))
+
+
+def test_column_block_schedule_is_a_reassociation(cheb):
+    """Opt-in column-blocked schedule (colblocks = K on a view with ascending-id rows): one
+    term launch per block of x, no hub-row chunk gathers across a block boundary, every hub
+    row's entries still covered once in order, and the ranks stay within the FAST bar of the
+    single-launch schedule with the same top-100."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    e = Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 5000.0, 600_000, 5)
+    K = 3
+    res = {}
+    try:
+        assert lib.cheb_set_tuning(b"sortrows", 1) == 0
+        for cb in (0, K):
+            assert lib.cheb_set_tuning(b"colblocks", cb) == 0
+            dg, _ = cheb.build_device_graph(e)
+            try:
+                v = _view(lib, dg)
+                z, r, m, launches = _tiles(lib, dg)
+                res[cb] = (cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10)).ranks, v, z, r, m, launches)
+            finally:
+                dg.free()
+    finally:
+        lib.cheb_set_tuning(b"colblocks", 0)
+        lib.cheb_set_tuning(b"sortrows", -1)
+    ranks0, v0, *_ = res[0]
+    ranks, v, z, r, m, launches = res[K]
+    assert launches == K
+    assert np.array_equal(v["rp"], v0["rp"]) and np.array_equal(v["col"], v0["col"])
+    n = v["rp"].size - 1
+    bounds = [0] + [(n * j // K) & ~31 for j in range(1, K)] + [n]
+    col = v["col"]
+    chunk = (m & 0x10) != 0
+    assert chunk.any()
+    for t in np.nonzero(chunk)[0]:
+        ids = col[z[t]:z[t + 1]]
+        assert ids.size <= 248
+        blk = np.searchsorted(bounds, ids, side="right") - 1
+        assert np.all(blk == blk[0]), t
+    # chunk tiles of a hub row tile its entries contiguously, in order
+    hub_rows = np.unique(r[chunk])
+    n_hub = int(hub_rows.size)
+    assert np.array_equal(hub_rows, np.arange(n_hub))
+    first = np.nonzero(chunk)[0]
+    assert z[first[0]] == 0 and z[first[-1] + 1] == v["rp"][n_hub]
+    assert np.max(np.abs(ranks - ranks0)) <= TOL64
+    top = lambda x: np.argsort(-x, kind="stable")[:100]  # noqa: E731
+    assert np.array_equal(top(ranks), top(ranks0))
