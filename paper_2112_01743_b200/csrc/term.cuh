@@ -405,9 +405,13 @@ struct alignas(16) WarpScratch {
     alignas(16) unsigned char stage[kGatherAsync ? kStageSlots : 0][32][16];  // cold-gather slots [slot][lane]
 };
 
+#ifndef CHEB_SMEM_PAD_KB
+#define CHEB_SMEM_PAD_KB 0  // experiments: unused shared memory (shrinks the L1 carve-out)
+#endif
 template <class V>
 constexpr size_t warp_smem_bytes() {
-    return (size_t)kHotBytes + (size_t)kWarps * sizeof(WarpScratch<V>) + 2 * 32 * sizeof(double);
+    return (size_t)kHotBytes + (size_t)kWarps * sizeof(WarpScratch<V>) + 2 * 32 * sizeof(double) +
+           (size_t)CHEB_SMEM_PAD_KB * 1024;
 }
 
 // Tile in registers.
