@@ -1186,6 +1186,7 @@ static std::vector<TileSeg> make_tile_segs(const std::vector<int64_t>& run_deg, 
     int64_t row = 0, z = 0, tile = 0;
     int64_t cur_rows = 0, cur_nnz = 0, cur_row0 = 0, cur_z0 = 0, cur_dmax = 0;
     V.n_hub = 0;
+    V.n_hub_wide = 0;
     V.n_chunk_tiles = 0;
     for (int b = 0; b < 7; ++b) V.bin_tiles[b] = V.bin_rows[b] = V.bin_nnz[b] = 0;
     auto lanes_log2 = [](int64_t dmax, int64_t rows) {
@@ -1217,6 +1218,7 @@ static std::vector<TileSeg> make_tile_segs(const std::vector<int64_t>& run_deg, 
             emit(z, row, c * nch, d, nch, kTileChunk, 0, c * d);
             V.n_chunk_tiles += (int)(c * nch);
             V.n_hub += c;
+            if (nch > 32) V.n_hub_wide = V.n_hub;  // degree-descending: a prefix of the hub rows
             row += c;
             z += c * d;
             continue;
@@ -1445,6 +1447,9 @@ static void column_block_schedule(SolverView& V, int K, int64_t x_len, cudaStrea
         t = t1;
     }
     if ((int64_t)hub_first.size() != n_hub) fail(CHEB_CUDA, "column-block schedule: hub rows do not match");
+    V.n_hub_wide = 0;  // rows with more than 32 chunks after the split: warp rows of the hub finalize
+    for (int64_t r = 0; r < n_hub; ++r)
+        if ((r + 1 < n_hub ? hub_first[(size_t)r + 1] : (int)nt.size()) - hub_first[(size_t)r] > 32) V.n_hub_wide = r + 1;
     const int new_chunks = (int)nt.size();
     hub_first.push_back(new_chunks);
     for (size_t t = (size_t)old_chunks; t < tiles.size(); ++t) nt.push_back(tiles[t]);  // pack tiles + sentinel

@@ -231,6 +231,7 @@ struct SolverView {
     int n_tiles = 0;
     int grid = 0;          // CTAs of one term launch (persistent: one per SM)
     int64_t n_hub = 0;     // rows [0, n_hub) with degree > kWarpNnz (chunk tiles)
+    int64_t n_hub_wide = 0;  // rows [0, n_hub_wide): more than 32 chunk tiles (hub finalize: a warp each)
     int n_chunk_tiles = 0;
     DevMem hub_first;      // int32 [n_hub + 1]: first chunk tile of each hub row
     // Column-blocked schedule (x larger than L2): hub-row chunks never straddle a block of x

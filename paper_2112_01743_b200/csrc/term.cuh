@@ -552,7 +552,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
         return;
     }
     const int* cb = ws.colb[i & 1] + (int)(d.z0 & 7);  // tile-local position p at cb[p]
-    const unsigned stage_s = kGatherAsync ? (unsigned)__cvta_generic_to_shared(&ws.stage[0][lane][0]) : 0u;
+    [[maybe_unused]] const unsigned stage_s = kGatherAsync ? (unsigned)__cvta_generic_to_shared(&ws.stage[0][lane][0]) : 0u;
 
     if (d.meta & kTileChunk) {
         // slice of a row with degree > kWarpNnz: partial only; completed by k_hub_finalize
@@ -729,32 +729,63 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
     if (a.stamp_end) stamp_last_cta(a.done, a.stamp_end);
 }
 
-// Hub rows (degree > kWarpNnz, rows [0, n_hub) of the view): one warp per row sums the
-// row's chunk partials in chunk order and runs the fused epilogue.  Chunk tiles of row h
-// are the consecutive tiles [hub_first[h], hub_first[h+1]).
+// Hub rows (degree > kWarpNnz, rows [0, n_hub) of the view, degree-descending): the row's
+// chunk partials summed in the shuffle-tree order of a warp holding partial q in lane
+// q mod 32, then the fused epilogue.  Chunk tiles of row h are the consecutive tiles
+// [hub_first[h], hub_first[h+1]).  Rows [0, n_wide) (> 32 chunks) take a warp each; the
+// rest take a lane each, 32 consecutive rows per warp, and replay the same tree for their
+// <= 32 partials in registers (bitwise the warp result).  A warp per row left every warp
+// walking ~50 rows one dependent load chain at a time (C4: ~1 M hub rows, 0.24 ms per term).
+template <int EPI, class RP, class V>
+__device__ __forceinline__ void hub_epilogue(const TermArgs<RP, V>& a, int64_t h, double tot) {
+    const int64_t deg = a.rp[h + 1] - a.rp[h];
+    double q0 = 0.0, q1 = 0.0;
+    const V hp = EPI != EPI_PLAIN ? prev_src<EPI>(a)[h] : V(0);
+    const V ha = EPI == EPI_CPAA ? a.acc[h] : V(0);
+    epilogue_v<EPI>(a, h, (V)tot, deg, hp, ha, q0, q1);
+    if (a.hub_ts) {
+        a.hub_ts[2 * h] = q0;
+        a.hub_ts[2 * h + 1] = q1;
+    }
+}
+
 template <int EPI, class RP, class V>
 __global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const int* __restrict__ hub_first,
-                                                      int64_t n_hub) {
+                                                      int64_t n_hub, int64_t n_wide) {
     const int lane = threadIdx.x & 31;
     pdl_trigger();
     pdl_wait();  // the term kernel's hub partials
-    for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < n_hub;
-         h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t h = gw; h < n_wide; h += nw) {
         const int f0 = hub_first[h], f1 = hub_first[h + 1];
         double tot = 0.0;
         for (int q = f0 + lane; q < f1; q += 32) tot += a.hub_part[q];
         tot = warp_sum_v(tot);
-        if (lane == 0) {
-            const int64_t deg = a.rp[h + 1] - a.rp[h];
-            double q0 = 0.0, q1 = 0.0;
-            const V hp = EPI != EPI_PLAIN ? prev_src<EPI>(a)[h] : V(0);
-            const V ha = EPI == EPI_CPAA ? a.acc[h] : V(0);
-            epilogue_v<EPI>(a, h, (V)tot, deg, hp, ha, q0, q1);
-            if (a.hub_ts) {
-                a.hub_ts[2 * h] = q0;
-                a.hub_ts[2 * h + 1] = q1;
-            }
+        if (lane == 0) hub_epilogue<EPI>(a, h, tot);
+    }
+    const int64_t groups = (n_hub - n_wide + 31) >> 5;
+    // lane groups continue the rotation where the wide rows stopped (group 0 goes to the warp
+    // that would have taken row n_wide)
+    for (int64_t gi = (gw + nw - n_wide % nw) % nw; gi < groups; gi += nw) {
+        const int64_t h = n_wide + gi * 32 + lane;
+        if (h >= n_hub) continue;
+        const int f0 = hub_first[h], m = hub_first[h + 1] - f0;
+        double tot;
+        if (m <= 32) {
+            double v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = i < m ? __dadd_rn(0.0, a.hub_part[f0 + i]) : 0.0;
+#pragma unroll
+            for (int o = 16; o; o >>= 1)
+#pragma unroll
+                for (int i = 0; i < o; ++i) v[i] = __dadd_rn(v[i], v[i + o]);
+            tot = v[0];
+        } else {  // only after the opt-in column-block split (chunk counts no longer monotone)
+            tot = 0.0;
+            for (int q = 0; q < m; ++q) tot += a.hub_part[f0 + q];
         }
+        hub_epilogue<EPI>(a, h, tot);
     }
     if (a.stamp_end) stamp_last_cta(a.done, a.stamp_end);
 }
@@ -1207,7 +1238,8 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         }
         if (g->view.n_hub > 0) {
             CHEB_CUDA_CHECK(cudaGetLastError());
-            const int hb = (int)std::min<int64_t>((g->view.n_hub * 32 + 255) / 256, 148 * 16);
+            const int64_t hub_warps = g->view.n_hub_wide + (g->view.n_hub - g->view.n_hub_wide + 31) / 32;
+            const int hb = (int)std::max<int64_t>(1, std::min<int64_t>((hub_warps * 32 + 255) / 256, 148 * 16));
             cudaLaunchConfig_t hc = {};
             hc.gridDim = dim3(hb);
             hc.blockDim = dim3(256);
@@ -1218,7 +1250,8 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             hc.attrs = hattr;
             hc.numAttrs = tuning().pdl ? 1 : 0;
             CHEB_CUDA_CHECK(cudaLaunchKernelEx(&hc, k_hub_finalize<EPI, RP, V>, a,
-                                               (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub));
+                                               (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub,
+                                               g->view.n_hub_wide));
             return launched + 1;
         }
         CHEB_CUDA_CHECK(cudaGetLastError());
