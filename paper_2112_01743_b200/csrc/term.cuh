@@ -1238,7 +1238,8 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         }
         if (g->view.n_hub > 0) {
             CHEB_CUDA_CHECK(cudaGetLastError());
-            const int64_t hub_warps = g->view.n_hub_wide + (g->view.n_hub - g->view.n_hub_wide + 31) / 32;
+            const int64_t n_wide = tuning().hubwarp ? g->view.n_hub : g->view.n_hub_wide;
+            const int64_t hub_warps = n_wide + (g->view.n_hub - n_wide + 31) / 32;
             const int hb = (int)std::max<int64_t>(1, std::min<int64_t>((hub_warps * 32 + 255) / 256, 148 * 16));
             cudaLaunchConfig_t hc = {};
             hc.gridDim = dim3(hb);
@@ -1250,8 +1251,7 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             hc.attrs = hattr;
             hc.numAttrs = tuning().pdl ? 1 : 0;
             CHEB_CUDA_CHECK(cudaLaunchKernelEx(&hc, k_hub_finalize<EPI, RP, V>, a,
-                                               (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub,
-                                               g->view.n_hub_wide));
+                                               (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub, n_wide));
             return launched + 1;
         }
         CHEB_CUDA_CHECK(cudaGetLastError());

@@ -710,3 +710,25 @@ def test_column_block_schedule_is_a_reassociation(cheb):
     assert np.max(np.abs(ranks - ranks0)) <= TOL64
     top = lambda x: np.argsort(-x, kind="stable")[:100]  # noqa: E731
     assert np.array_equal(top(ranks), top(ranks0))
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+def test_hub_finalize_lane_rows_bitwise_equal_warp_rows(cheb, precision):
+    """Hub rows with <= 32 chunk partials are finalized by one lane replaying the warp's
+    shuffle-tree sum: ranks and trace bitwise equal to finalizing every hub row with a warp."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    e = Gen.chung_lu_edges(1 << 17, 2.1, 2.0, 20000.0, 2_000_000, 9)
+    dg, info = cheb.build_device_graph(e)
+    out = {}
+    try:
+        for hw in (0, 1):
+            assert lib.cheb_set_tuning(b"hubwarp", hw) == 0
+            out[hw] = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, precision=precision))
+    finally:
+        lib.cheb_set_tuning(b"hubwarp", 0)
+        dg.free()
+    assert info["max_degree"] > 32 * 248  # both finalize paths run
+    assert np.array_equal(out[0].ranks, out[1].ranks)
+    assert [t.S_k for t in out[0].trace] == [t.S_k for t in out[1].trace]
