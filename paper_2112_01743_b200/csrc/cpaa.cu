@@ -67,7 +67,7 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
             CHEB_CUDA_CHECK(cudaGetLastError());
             ++launches;
         } else if (per_term_reduce) {
-            k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
+            k_trace_reduce<<<1, kTraceThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
                                                    (int)g->view.n_hub, k - 1, trace);
             CHEB_CUDA_CHECK(cudaGetLastError());
             ++launches;
@@ -86,7 +86,7 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
         ++launches;
     }
     if (L.fast && !per_term_reduce && M > 0) {
-        k_trace_reduce<<<M, kThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
+        k_trace_reduce<<<M, kTraceThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
                                                (int)g->view.n_hub, 0, trace);
         CHEB_CUDA_CHECK(cudaGetLastError());
         ++launches;

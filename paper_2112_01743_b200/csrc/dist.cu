@@ -80,28 +80,15 @@ __global__ void k_peer_wait(const unsigned long long* flags, int G, unsigned lon
 // Term tail of a one-process-per-GPU push run, one launch instead of three: this rank's
 // trace partials of term k (as k_trace_reduce), then the barrier (signal every rank, wait
 // for every rank).  Launched with PDL; waits for the term kernels before reading anything.
-__global__ void __launch_bounds__(256) k_term_tail(const double* __restrict__ part, int grid,
-                                                   const double* __restrict__ hub_ts, int n_hub, int k,
-                                                   double* __restrict__ trace, unsigned long long* const* flags,
-                                                   const unsigned long long* my_flags, int G, int rank,
-                                                   unsigned long long epoch) {
+__global__ void __launch_bounds__(kTraceThreads) k_term_tail(const double* __restrict__ part, int grid,
+                                                             const double* __restrict__ hub_ts, int n_hub, int k,
+                                                             double* __restrict__ trace, unsigned long long* const* flags,
+                                                             const unsigned long long* my_flags, int G, int rank,
+                                                             unsigned long long epoch) {
     __shared__ double sh[32];
     pdl_wait();
-    const double* pk = part + (size_t)k * grid * 2;
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < grid; i += blockDim.x) {
-        a += pk[2 * i];
-        b += pk[2 * i + 1];
-    }
-    if (hub_ts) {
-        const double* hk = hub_ts + (size_t)k * n_hub * 2;
-        for (int i = threadIdx.x; i < n_hub; i += blockDim.x) {
-            a += hk[2 * i];
-            b += hk[2 * i + 1];
-        }
-    }
-    a = block_sum(a, sh);
-    b = block_sum(b, sh);
+    double a, b;
+    trace_sums(part, grid, hub_ts, n_hub, k, sh, a, b);
     if (threadIdx.x == 0) {
         trace[2 * k] = a;
         trace[2 * k + 1] = b;
@@ -285,7 +272,7 @@ struct DistSolve {
             ++pg->epoch;
             cudaLaunchConfig_t tc = {};
             tc.gridDim = dim3(1);
-            tc.blockDim = dim3(256);
+            tc.blockDim = dim3(kTraceThreads);
             tc.stream = st;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -297,7 +284,7 @@ struct DistSolve {
                                                w.trace.ptr<double>(), flag_table(),
                                                (const unsigned long long*)pg->flags, G, pg->rank, pg->epoch));
         } else {
-            k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), Vw.grid, w.hub_ts.ptr<double>(),
+            k_trace_reduce<<<1, kTraceThreads, 0, st>>>(w.part.ptr<double>(), Vw.grid, w.hub_ts.ptr<double>(),
                                                    (int)Vw.n_hub, k - 1, w.trace.ptr<double>());
         }
         CHEB_CUDA_CHECK(cudaGetLastError());

@@ -96,7 +96,7 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
                 CHEB_CUDA_CHECK(cudaEventRecord(rev[2 * (j - 1) + 1], st));
             }
             if (L.fast) {
-                k_trace_reduce<<<nb, kThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
+                k_trace_reduce<<<nb, kTraceThreads, 0, st>>>(w.part.ptr<double>(), grid, w.hub_ts.ptr<double>(),
                                                         (int)g->view.n_hub, 0, dtr);
                 CHEB_CUDA_CHECK(cudaGetLastError());
             }
@@ -165,7 +165,7 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
         } else {
             launch_pass<EPI_POWER>(g, L, a);
             CHEB_CUDA_CHECK(cudaEventRecord(rev[1], st));
-            k_trace_reduce<<<1, kThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub, 0, dtr);
+            k_trace_reduce<<<1, kTraceThreads, 0, st>>>(w.part.ptr<double>(), grid, a.hub_ts, (int)g->view.n_hub, 0, dtr);
         }
         CHEB_CUDA_CHECK(cudaGetLastError());
         double err2[2] = {0.0, 0.0};

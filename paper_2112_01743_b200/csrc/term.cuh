@@ -971,29 +971,48 @@ __global__ void k_init(const RP* __restrict__ rp, const double* __restrict__ inv
     }
 }
 
-// trace[k] = sum of block partials (+ hub partials) of term k, fixed order.
-__global__ void k_trace_reduce(const double* __restrict__ part, int grid, const double* __restrict__ hub_ts,
-                               int n_hub, int k_first, double* __restrict__ trace) {
+// trace[k] = sum of block partials (+ hub partials) of term k, fixed order: kTraceThreads
+// threads, each with four independent accumulators over 16-byte loads (one CTA per term read
+// C4's ~1 M hub-row pairs at ~10 GB/s with one 256-thread chain of dependent adds each).
+constexpr int kTraceThreads = 1024;
+__device__ __forceinline__ void trace_sums(const double* __restrict__ part, int grid, const double* __restrict__ hub_ts,
+                                           int n_hub, int k, double* sh, double& A, double& B) {
+    const double2* pk = reinterpret_cast<const double2*>(part + (size_t)k * grid * 2);
+    double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+    auto sweep = [&](const double2* p, int cnt) {
+        const int T = blockDim.x;
+        int i = threadIdx.x;
+        for (; i + 3 * T < cnt; i += 4 * T) {
+            double2 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = __ldg(p + i + j * T);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                a[j] += v[j].x;
+                b[j] += v[j].y;
+            }
+        }
+        for (int j = 0; i < cnt; i += T, ++j) {
+            const double2 v = __ldg(p + i);
+            a[j & 3] += v.x;
+            b[j & 3] += v.y;
+        }
+    };
+    sweep(pk, grid);
+    if (hub_ts) sweep(reinterpret_cast<const double2*>(hub_ts + (size_t)k * n_hub * 2), n_hub);
+    A = block_sum((a[0] + a[1]) + (a[2] + a[3]), sh);
+    B = block_sum((b[0] + b[1]) + (b[2] + b[3]), sh);
+}
+__global__ void __launch_bounds__(kTraceThreads) k_trace_reduce(const double* __restrict__ part, int grid,
+                                                                const double* __restrict__ hub_ts, int n_hub,
+                                                                int k_first, double* __restrict__ trace) {
     __shared__ double sh[32];
     const int k = k_first + blockIdx.x;
-    const double* pk = part + (size_t)k * grid * 2;
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < grid; i += blockDim.x) {
-        a += pk[2 * i];
-        b += pk[2 * i + 1];
-    }
-    if (hub_ts) {
-        const double* hk = hub_ts + (size_t)k * n_hub * 2;
-        for (int i = threadIdx.x; i < n_hub; i += blockDim.x) {
-            a += hk[2 * i];
-            b += hk[2 * i + 1];
-        }
-    }
-    a = block_sum(a, sh);
-    b = block_sum(b, sh);
+    double A, B;
+    trace_sums(part, grid, hub_ts, n_hub, k, sh, A, B);
     if (threadIdx.x == 0) {
-        trace[2 * k] = a;
-        trace[2 * k + 1] = b;
+        trace[2 * k] = A;
+        trace[2 * k + 1] = B;
     }
 }
 
