@@ -1785,6 +1785,8 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         V.inv.release();
     }
 
+    if (P.G == 1) V.rank = std::move(rank);  // k_normalize gathers acc[rank[v]] (coalesced writes)
+    else V.rank.release();
     dbg_mark("  view: tiles staged");
     V.ready = true;
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -219,6 +219,7 @@ struct SolverView {
     bool ready = false;
     bool rp64 = false;
     DevMem order;      // int32 [n_local]  local row -> old id
+    DevMem rank;       // int32 [n]  old id -> view row (single-GPU views: the ranks are gathered in vertex order)
     DevMem order_full; // int32 [n]  global sorted row -> old id (partitioned runs only)
     int64_t n_local = 0, nnz_local = 0, x_len = 0;
     int part_G = 1, part_r = 0;  // local row i is sorted row part_global(i, part_r, part_G)
@@ -256,7 +257,7 @@ struct SolverView {
     // tile bins (host statistics): 0..5 = pack tiles with 2^b lanes per row, 6 = chunk tiles
     int64_t bin_tiles[7] = {}, bin_rows[7] = {}, bin_nnz[7] = {};
     void set_stream(cudaStream_t s) {
-        for (DevMem* d : {&order, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first, &push_mask,
+        for (DevMem* d : {&order, &rank, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first, &push_mask,
                           &col_sorted})
             d->set_stream(s);
     }

@@ -109,7 +109,7 @@ int enqueue_solve(cheb_graph* g, const Layout& L, const SolveSpec& s, const std:
         CHEB_CUDA_CHECK(cudaGetLastError());
         d_total = tot;
     }
-    k_normalize<V><<<grid1d(n), kThreads, 0, st>>>(acc, L.order, n, d_total, w.out.ptr<V>());
+    k_normalize<V><<<grid1d(n), kThreads, 0, st>>>(acc, L.order, L.rank, n, d_total, w.out.ptr<V>());
     CHEB_CUDA_CHECK(cudaGetLastError());
     ++launches;
     return launches;
