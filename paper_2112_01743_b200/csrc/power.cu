@@ -194,7 +194,7 @@ void power_t(cheb_graph* g, double c, int budget, bool by_tol, double tol, int m
     // ranks = x (original order); total = Kahan(x) on the host (power.cpp:105-107)
     std::vector<double> xs(n);
     DevMem o(sizeof(double) * n);
-    k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(X, L.order, n, o.ptr<double>());
+    k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(X, L.order, L.rank, n, o.ptr<double>());
     CHEB_CUDA_CHECK(cudaMemcpyAsync(ranks, o.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     *rounds_out = k;
@@ -236,7 +236,7 @@ void transition_t(cheb_graph* g, const double* x, double* y, int mode) {
         a.hub_part = w.hub_part.ptr<double>();
     }
     launch_pass<EPI_PLAIN>(g, L, a);
-    k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(w.T1.ptr<double>(), L.order, n, dx.ptr<double>());
+    k_permute_out<double><<<grid1d(n), kThreads, 0, st>>>(w.T1.ptr<double>(), L.order, L.rank, n, dx.ptr<double>());
     CHEB_CUDA_CHECK(cudaGetLastError());
     CHEB_CUDA_CHECK(cudaMemcpyAsync(y, dx.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, st));
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -347,7 +347,7 @@ void staged_get(cheb_graph* g, double* Tp, double* Tc, double* Tn, double* acc, 
     DevMem tmp(sizeof(double) * std::max<int64_t>(n, 1));
     auto get = [&](double* h, DevMem& d) {
         if (!h) return;
-        k_permute_out<double><<<grid1d(n), kThreads, 0, g->stream>>>(d.ptr<double>(), L.order, n, tmp.ptr<double>());
+        k_permute_out<double><<<grid1d(n), kThreads, 0, g->stream>>>(d.ptr<double>(), L.order, L.rank, n, tmp.ptr<double>());
         CHEB_CUDA_CHECK(cudaMemcpyAsync(h, tmp.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, g->stream));
         CHEB_CUDA_CHECK(cudaStreamSynchronize(g->stream));
     };

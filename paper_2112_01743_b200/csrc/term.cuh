@@ -1063,11 +1063,13 @@ __global__ void k_permute_in(const double* __restrict__ src, const int* __restri
 }
 
 template <class V>
-__global__ void k_permute_out(const V* __restrict__ src, const int* __restrict__ order, int64_t n,
-                              double* __restrict__ dst) {
+__global__ void k_permute_out(const V* __restrict__ src, const int* __restrict__ order, const int* __restrict__ rank,
+                              int64_t n, double* __restrict__ dst) {
     for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-         u += (int64_t)gridDim.x * blockDim.x)
-        dst[order ? order[u] : u] = (double)src[u];
+         u += (int64_t)gridDim.x * blockDim.x) {
+        if (rank) dst[u] = (double)src[rank[u]];  // gather in vertex order (coalesced writes)
+        else dst[order ? order[u] : u] = (double)src[u];
+    }
 }
 
 // x = T D^-1 (staged API / transition_apply pre-scale)
