@@ -283,16 +283,40 @@ struct StreamIO<float, 4> {
 };
 
 // Fused recurrence epilogue for (row u, the lane's columns).
+// The row's T_{k-1} and acc values of the lane (loaded before its gathers, so the two
+// streams overlap the gather latency instead of following it).
+template <class RP, class V, int VPL>
+struct RowPrev {
+    V tp[VPL], ac[VPL];
+};
+template <class RP, class V, int VPL>
+__device__ __forceinline__ void load_prev(const BatchArgs<RP, V>& a, int64_t u, int lane, RowPrev<RP, V, VPL>& o) {
+    const int c0 = lane * VPL;
+    if (c0 + VPL > a.R) return;  // partial lanes load inside the epilogue
+    const int64_t i0 = u * a.Rs + c0;
+    if (!a.first) StreamIO<V, VPL>::ld(a.T + i0, o.tp);
+    StreamIO<V, VPL>::ld(a.acc + i0, o.ac);
+}
+
 template <class RP, class V, int VPL>
 __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_t u, int64_t deg, int lane,
-                                               const double (&s)[VPL], double& p0, double& p1) {
+                                               const double (&s)[VPL], double& p0, double& p1,
+                                               const RowPrev<RP, V, VPL>* pre = nullptr) {
     const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
     const int c0 = lane * VPL;
     const int64_t i0 = u * a.Rs + c0;
     if (c0 + VPL <= a.R) {  // all of the lane's columns live: vector I/O
         V tp[VPL], ac[VPL], t[VPL], na[VPL], xo[VPL];
-        if (!a.first) StreamIO<V, VPL>::ld(a.T + i0, tp);
-        StreamIO<V, VPL>::ld(a.acc + i0, ac);
+        if (pre) {
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+                tp[k] = pre->tp[k];
+                ac[k] = pre->ac[k];
+            }
+        } else {
+            if (!a.first) StreamIO<V, VPL>::ld(a.T + i0, tp);
+            StreamIO<V, VPL>::ld(a.acc + i0, ac);
+        }
 #pragma unroll
         for (int k = 0; k < VPL; ++k) {
             t[k] = a.first ? (V)s[k] : sub_rn(mul_rn(V(2), (V)s[k]), tp[k]);
@@ -327,8 +351,11 @@ __device__ __forceinline__ void batch_epilogue(const BatchArgs<RP, V>& a, int64_
     }
 }
 
+#ifndef CHEB_SPMM_MINB
+#define CHEB_SPMM_MINB 1
+#endif
 template <class RP, class V, int VPL>
-__global__ void __launch_bounds__(256) k_spmm_term(BatchArgs<RP, V> a, const Tile* __restrict__ tiles,
+__global__ void __launch_bounds__(256, CHEB_SPMM_MINB) k_spmm_term(BatchArgs<RP, V> a, const Tile* __restrict__ tiles,
                                                    int ntiles) {
     __shared__ double red[2][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -346,11 +373,15 @@ __global__ void __launch_bounds__(256) k_spmm_term(BatchArgs<RP, V> a, const Til
             for (int k = 0; k < VPL; ++k)
                 if (lane * VPL + k < a.Rs) a.hub_part[(int64_t)t * a.Rs + lane * VPL + k] = s[k];
         } else {
+            int64_t e = tl.row_begin < nx.row_begin ? (int64_t)a.rp[tl.row_begin] : 0;
             for (int64_t u = tl.row_begin; u < nx.row_begin; ++u) {
-                const int64_t b = a.rp[u], e = a.rp[u + 1];
+                const int64_t b = e;
+                e = a.rp[u + 1];
+                RowPrev<RP, V, VPL> pre;
+                if (live) load_prev<RP, V, VPL>(a, u, lane, pre);
                 double s[VPL];
                 row_gather<RP, V, VPL>(a, b, e, lane, live, s);
-                if (live) batch_epilogue<RP, V, VPL>(a, u, e - b, lane, s, p0, p1);
+                if (live) batch_epilogue<RP, V, VPL>(a, u, e - b, lane, s, p0, p1, &pre);
             }
         }
     }
