@@ -150,13 +150,17 @@ struct PolicyIO<float, 4> {
 };
 
 #ifndef CHEB_SPMM_UNROLL
-#define CHEB_SPMM_UNROLL 8
+#define CHEB_SPMM_UNROLL 0  // 0: per storage type (below)
 #endif
 constexpr int kSpmmUnroll = CHEB_SPMM_UNROLL;
-// neighbour R-vectors in flight per lane: 8 for narrow lanes (C5: VPL = 2), 4 when a lane
-// carries 4 values (register budget)
-template <int VPL>
-__host__ __device__ constexpr int spmm_unroll() { return VPL >= 4 && kSpmmUnroll > 4 ? 4 : kSpmmUnroll; }
+// Neighbour R-vectors in flight per lane.  Fewer than 8 keeps the kernel at 64 registers
+// (4 CTAs of 8 warps per SM) once the row's T/acc loads are hoisted ahead of its gathers:
+// C5 fp64 U = 8 / 5 / 4: 301.5 / 272 / 241 ms per solve, fp32 U = 8 / 5 / 4: 205 / 169 / 181
+// (one B200, interleaved runs, tools/batch_time.py).
+template <class V, int VPL>
+__host__ __device__ constexpr int spmm_unroll() {
+    return kSpmmUnroll > 0 ? (VPL >= 4 && kSpmmUnroll > 4 ? 4 : kSpmmUnroll) : (VPL >= 4 ? 4 : sizeof(V) == 8 ? 4 : 5);
+}
 
 // Sum over CSR entries [b, e) of the gathered R-vectors (lane's VPL columns), U entries
 // (U column ids then U row gathers) in flight per lane.  Sums accumulate in fp64 whatever
@@ -167,7 +171,7 @@ __device__ __forceinline__ void row_gather(const BatchArgs<RP, V>& a, int64_t b,
 #pragma unroll
     for (int k = 0; k < VPL; ++k) s[k] = 0.0;
     const int off = lane * VPL;
-    constexpr int U = spmm_unroll<VPL>();
+    constexpr int U = spmm_unroll<V, VPL>();
     const uint64_t p_hub = policy_evict_last(), p_cold = policy_evict_first();
     int64_t j = b;
     for (; j + U - 1 < e; j += U) {
