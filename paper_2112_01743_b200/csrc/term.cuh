@@ -338,14 +338,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, unsigned parity) {
         "}\n" :: "r"(bar), "r"(parity) : "memory");
 }
 
-// Row epilogue with the row's operands already loaded (prev = T_{k-1} / old x).
-template <int EPI, class RP, class V>
+// Row epilogue with the row's operands already loaded (prev = T_{k-1} / old x).  SINGLE:
+// one GPU, canonical inv_degree, no push exchange (the product case): those branches are
+// compiled out of the term kernel.
+template <int EPI, class RP, class V, bool SINGLE = false>
 __device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, V s, int64_t deg,
                                            V prev, V accv, double& p0, double& p1) {
     if constexpr (EPI == EPI_PLAIN) {
         a.out[u] = s;
     } else {
-        const V inv = a.inv ? (V)a.inv[u] : rcp_rn((V)deg);
+        const V inv = (!SINGLE && a.inv) ? (V)a.inv[u] : rcp_rn((V)deg);
         if constexpr (EPI == EPI_CPAA) {
             const V t = a.first ? s : sub_rn(mul_rn(V(2), s), prev);
             const V nacc = add_rn(accv, mul_rn((V)a.ck, t));
@@ -357,8 +359,8 @@ __device__ __forceinline__ void epilogue_v(const TermArgs<RP, V>& a, int64_t u, 
                 a.T[u] = t;
                 a.acc[u] = nacc;
             }
-            const int64_t pos = a.part_G > 1 ? part_global(u, a.part_r, a.part_G) : u;
-            if (a.push) {  // fused exchange: straight into the copies of x_{k+1} that are read
+            const int64_t pos = (!SINGLE && a.part_G > 1) ? part_global(u, a.part_r, a.part_G) : u;
+            if (!SINGLE && a.push) {  // fused exchange: straight into the copies of x_{k+1} that are read
                 const unsigned m = a.push_mask ? __ldg(a.push_mask + u) : ~0u;
                 for (int r = 0; r < a.push_n; ++r)
                     if (m >> r & 1u) a.push[r][pos] = xn;
@@ -489,7 +491,7 @@ constexpr int kPackUnroll = CHEB_PACK_UNROLL;  // gathers in flight per lane in 
 
 // One tile of the warp's program.  cur: this tile's row operands (loaded one tile ago);
 // nxt receives the next tile's.  No register prefetched here is copied at the end.
-template <int EPI, class RP, class V, class WS>
+template <int EPI, bool SINGLE, class RP, class V, class WS>
 __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot_s, int H, WS& ws,
                                           const WTile* my, int w, int S, int nt, int i,
                                           const RowOps<V>& cur, RowOps<V>& nxt, double& p0, double& p1) {
@@ -624,7 +626,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
         }
         for (int o = L >> 1; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         if (li == 0 && g < d.rows)
-            epilogue_v<EPI>(a, (int64_t)d.r0 + g, sum, (int64_t)(rend - rb), cur.pv, cur.av, p0, p1);
+            epilogue_v<EPI, RP, V, SINGLE>(a, (int64_t)d.r0 + g, sum, (int64_t)(rend - rb), cur.pv, cur.av, p0, p1);
     }
     __syncwarp();
     // descriptor block of tile i fully consumed: refill its slot two blocks ahead
@@ -634,7 +636,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
     }
 }
 
-template <int EPI, class RP, class V>
+template <int EPI, class RP, class V, bool SINGLE>
 __global__ void __launch_bounds__(kWarps * 32, 1)
 k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles, int H) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -701,9 +703,9 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
     __syncthreads();
 
     for (int i = 0; i < nt; i += 2) {
-        term_step<EPI>(a, hot_s, H, ws, my, w, S, nt, i, A, B, p0, p1);
+        term_step<EPI, SINGLE>(a, hot_s, H, ws, my, w, S, nt, i, A, B, p0, p1);
         if (i + 1 >= nt) break;
-        term_step<EPI>(a, hot_s, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
+        term_step<EPI, SINGLE>(a, hot_s, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
     }
     if constexpr (EPI == EPI_CPAA || EPI == EPI_POWER) {
         if (a.part) {
@@ -1198,13 +1200,16 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         static std::atomic<uint64_t> attr_set{0};  // per template instance, bit per device
         constexpr size_t smem = warp_smem_bytes<V>();
         if (first_on_device(attr_set, g->device)) {
-            const cudaError_t e = cudaFuncSetAttribute(k_term_warp<EPI, RP, V>,
-                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) {
-                attr_set.fetch_and(~(uint64_t(1) << (g->device & 63)));  // retry next launch
-                CHEB_CUDA_CHECK(e);
+            for (const void* f : {(const void*)k_term_warp<EPI, RP, V, false>, (const void*)k_term_warp<EPI, RP, V, true>}) {
+                const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) {
+                    attr_set.fetch_and(~(uint64_t(1) << (g->device & 63)));  // retry next launch
+                    CHEB_CUDA_CHECK(e);
+                }
             }
         }
+        // single GPU, canonical inv_degree, no push: the specialised kernel
+        const bool single = !a.push && !a.inv && !(g->part.G > 1);
         int H = (int)std::min<int64_t>(g->n, hot_capacity<V>());
         if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);
         TermArgs<RP, V> ab = a;
@@ -1242,7 +1247,8 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
                 attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
                 attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
             }
-            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V>, args, prog, plen, ntiles, H));
+            if (single) CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V, true>, args, prog, plen, ntiles, H));
+            else CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V, false>, args, prog, plen, ntiles, H));
         };
         int launched = 0;
         if (g->view.phases.empty()) {
