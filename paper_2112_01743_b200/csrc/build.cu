@@ -1095,11 +1095,6 @@ __global__ void k_gather_local(const int* __restrict__ order_g, const int64_t* _
     }
 }
 
-__global__ void k_copy_i32(const int* __restrict__ in, int64_t n, int* __restrict__ out) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = in[i];
-}
 
 __global__ void k_gather_inv(const double* __restrict__ inv, const int* __restrict__ order,
                              int64_t n, double* __restrict__ out) {
