@@ -1156,6 +1156,7 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "spmm_xpol") tuning().spmm_xpol = value;
         else if (k == "sortrows") tuning().sortrows = value;
         else if (k == "hubwarp") tuning().hubwarp = value;
+        else if (k == "colbufs") tuning().colbufs = value;
         else if (k == "colblocks") tuning().colblocks = value;  // applies to views built afterwards
         else if (k == "colsplit_pct") tuning().colsplit_pct = value;  // applies to views built afterwards
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);

@@ -439,6 +439,7 @@ struct Tuning {
     int colblocks = 0;  // K > 1: hub-row chunks cut at K column blocks of x, one term launch per block
                         // under an L2 window over its slice (rows sorted by id only; C4: no gain, off)
     int upgroups = 16;  // groups of old rows an upload lands in, each permuted + sorted as it lands (C4: 4 -> 16 groups, upload 200 -> 163 ms)
+    int colbufs = -1;   // term kernel column-id buffers per warp: -1 auto (1 when x exceeds L2), 1 or 2
     int hubwarp = 0;    // 1: every hub row finalized by a warp (the lane-per-row path off; tests)
     int pull = 1;       // view tiles / programs pulled from pinned host memory by a kernel (not the copy engine)
     int colsplit_pct = -1; // K = 2: first block boundary at this percent of x (-1: equal halves)
@@ -467,6 +468,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_COLBLOCKS")) x.colblocks = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_PULL")) x.pull = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_HUBWARP")) x.hubwarp = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_COLBUFS")) x.colbufs = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_UPGROUPS")) x.upgroups = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_COLSPLIT_PCT")) x.colsplit_pct = std::atoi(e);
         return x;

@@ -398,9 +398,14 @@ template <class V>
 constexpr int hot_capacity() { return (kHotBytes / (int)sizeof(V)); }
 
 // Per-warp shared scratch of the term kernel.
-template <class V>
+// Column-id landing buffers per warp (NB): 2 = the next tile's ids are copied while the
+// current tile is read; 1 = one buffer, refilled as soon as the current tile's ids are in
+// registers — 34 KB less shared memory per SM, so the carve-out drops from 164 to 132 KB and
+// the L1 holds more in-flight gathers.  Chosen per graph at launch (launch_pass): 1 for an x
+// larger than 16 MB (config 4: 3737 -> 3558 us/term), 2 below (config 2: 68.1 vs 72.2 with 1).
+template <class V, int NB>
 struct alignas(16) WarpScratch {
-    int colb[2][kColBuf];   // TMA landing buffers: column ids of the current / next tile
+    int colb[NB][kColBuf];  // TMA landing buffers of column ids
     WTile desc[2][kDescBlock];  // TMA ring of this warp's tile program
     uint64_t colm[2];       // mbarriers of colb
     uint64_t descm[2];      // mbarriers of desc
@@ -410,9 +415,9 @@ struct alignas(16) WarpScratch {
 #ifndef CHEB_SMEM_PAD_KB
 #define CHEB_SMEM_PAD_KB 0  // experiments: unused shared memory (shrinks the L1 carve-out)
 #endif
-template <class V>
+template <class V, int NB>
 constexpr size_t warp_smem_bytes() {
-    return (size_t)kHotBytes + (size_t)kWarps * sizeof(WarpScratch<V>) + 2 * 32 * sizeof(double) +
+    return (size_t)kHotBytes + (size_t)kWarps * sizeof(WarpScratch<V, NB>) + 2 * 32 * sizeof(double) +
            (size_t)CHEB_SMEM_PAD_KB * 1024;
 }
 
@@ -477,7 +482,7 @@ __device__ __forceinline__ void load_rows(const TermArgs<RP, V>& a, const TileR&
 }
 
 // Lane 0: bulk-copy descriptor block blk of this warp's program into ring slot blk & 1.
-__device__ __forceinline__ void issue_desc(const WTile* my, int blk, WarpScratch<double>* unused,
+__device__ __forceinline__ void issue_desc(const WTile* my, int blk, void* unused,
                                            WTile* slot, uint64_t* mbar) {
     (void)unused;
     mbar_expect_tx(mbar, kDescBlock * sizeof(WTile));
@@ -491,20 +496,28 @@ constexpr int kPackUnroll = CHEB_PACK_UNROLL;  // gathers in flight per lane in 
 
 // One tile of the warp's program.  cur: this tile's row operands (loaded one tile ago);
 // nxt receives the next tile's.  No register prefetched here is copied at the end.
-template <int EPI, bool SINGLE, class RP, class V, class WS>
+template <int EPI, bool SINGLE, int NB, class RP, class V, class WS>
 __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot_s, int H, WS& ws,
                                           const WTile* my, int w, int S, int nt, int i,
                                           const RowOps<V>& cur, RowOps<V>& nxt, double& p0, double& p1) {
     const int lane = threadIdx.x & 31;
     constexpr int U = 8;
     const TileR d = tile_of(ws.desc[(i / kDescBlock) & 1][i % kDescBlock]);
+    TileR dn{};
     if (i + 1 < nt) {
         const int j = i + 1;
         if (j % kDescBlock == 0) mbar_wait(&ws.descm[(j / kDescBlock) & 1], ((j / kDescBlock) >> 1) & 1);
-        const TileR dn = tile_of(ws.desc[(j / kDescBlock) & 1][j % kDescBlock]);
-        if (lane == 0) issue_cols(a.col, dn, ws.colb[j & 1], &ws.colm[j & 1]);
+        dn = tile_of(ws.desc[(j / kDescBlock) & 1][j % kDescBlock]);
+        if (NB == 2 && lane == 0) issue_cols(a.col, dn, ws.colb[j % NB], &ws.colm[j % NB]);
         load_rows<EPI>(a, dn, nxt);
     }
+    // single buffer: the next tile's ids are copied once this tile's are in registers
+    auto refill = [&] {
+        if constexpr (NB == 1) {
+            __syncwarp();
+            if (lane == 0 && i + 1 < nt) issue_cols(a.col, dn, ws.colb[0], &ws.colm[0]);
+        }
+    };
     // L2 prefetch of a tile further ahead (its descriptor lives in the current or the next
     // block of the ring): the per-warp double buffer keeps ~1 tile of column ids in flight,
     // too few bytes to cover DRAM latency on graphs whose streams miss L2 (config 4)
@@ -542,10 +555,11 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
             }
         }
     }
-    mbar_wait(&ws.colm[i & 1], (i >> 1) & 1);
+    mbar_wait(&ws.colm[i % NB], (i / NB) & 1);
     if (kExp && a.tune_skip &&
         (a.tune_skip >= 16 ? (((d.meta & kTileChunk) ? 6 : (d.meta & 0xf)) != a.tune_skip - 16)
                            : ((a.tune_skip & 1) ? (d.meta & kTileChunk) : !(d.meta & kTileChunk)))) {
+        refill();
         __syncwarp();
         if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
             const int blk = i / kDescBlock + 2;
@@ -553,7 +567,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
         }
         return;
     }
-    const int* cb = ws.colb[i & 1] + (int)(d.z0 & 7);  // tile-local position p at cb[p]
+    const int* cb = ws.colb[i % NB] + (int)(d.z0 & 7);  // tile-local position p at cb[p]
     [[maybe_unused]] const unsigned stage_s = kGatherAsync ? (unsigned)__cvta_generic_to_shared(&ws.stage[0][lane][0]) : 0u;
 
     if (d.meta & kTileChunk) {
@@ -570,6 +584,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
                 c[q] = pp < d.cnt ? cb[pp] : -1;
             }
         }
+        refill();
         V v[U];
         if (kExp && a.tune_nogather) {
 #pragma unroll
@@ -608,7 +623,43 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
         }
         // pack rows: <= 8 entries per lane, summed in V; hub rows (chunk tiles) use fp64
         V sum = V(0);
-        for (int jj = rb + li; jj < rend; jj += kPackUnroll * L) {
+        int jj0 = rb + li;
+        if constexpr (NB == 1) {
+            // the lane's first 2 kPackUnroll entries into registers, then the buffer is free;
+            // the same per-lane order as the loop below
+            int c8[2 * kPackUnroll];
+#pragma unroll
+            for (int q = 0; q < 2 * kPackUnroll; ++q) c8[q] = jj0 + q * L < rend ? cb[jj0 + q * L] : -1;
+            const bool more = __any_sync(0xffffffffu, jj0 + 2 * kPackUnroll * L < rend);
+            if (!more) refill();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (jj0 + h * kPackUnroll * L < rend) {
+                    int c[kPackUnroll];
+#pragma unroll
+                    for (int q = 0; q < kPackUnroll; ++q) c[q] = c8[h * kPackUnroll + q];
+                    V v[kPackUnroll];
+                    gather8(a.x_in, hot_s, H, c, v);
+#pragma unroll
+                    for (int q = 0; q < kPackUnroll; ++q) sum += v[q];
+                }
+            }
+            jj0 += 2 * kPackUnroll * L;
+            if (more) {  // a lane with more than 2 kPackUnroll entries (mixed-degree tile)
+                for (int jj = jj0; jj < rend; jj += kPackUnroll * L) {
+                    int c[kPackUnroll];
+#pragma unroll
+                    for (int q = 0; q < kPackUnroll; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
+                    V v[kPackUnroll];
+                    gather8(a.x_in, hot_s, H, c, v);
+#pragma unroll
+                    for (int q = 0; q < kPackUnroll; ++q) sum += v[q];
+                }
+                refill();
+            }
+            jj0 = rend;  // done
+        }
+        for (int jj = jj0; jj < rend; jj += kPackUnroll * L) {
             int c[kPackUnroll];
 #pragma unroll
             for (int q = 0; q < kPackUnroll; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
@@ -636,7 +687,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
     }
 }
 
-template <int EPI, class RP, class V, bool SINGLE>
+template <int EPI, class RP, class V, bool SINGLE, int NB>
 __global__ void __launch_bounds__(kWarps * 32, 1)
 k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles, int H) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -646,8 +697,8 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
     unsigned hot_s;
     asm volatile("mov.b32 %0, %1;" : "=r"(hot_s) : "r"((unsigned)__cvta_generic_to_shared(smem)));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    WarpScratch<V>& ws = reinterpret_cast<WarpScratch<V>*>(smem + kHotBytes)[warp];
-    double* red = reinterpret_cast<double*>(smem + kHotBytes + kWarps * sizeof(WarpScratch<V>));
+    WarpScratch<V, NB>& ws = reinterpret_cast<WarpScratch<V, NB>*>(smem + kHotBytes)[warp];
+    double* red = reinterpret_cast<double*>(smem + kHotBytes + kWarps * sizeof(WarpScratch<V, NB>));
     __shared__ __align__(8) uint64_t mbar_hot;
 
     const int S = gridDim.x * kWarps;
@@ -660,7 +711,7 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
     if (threadIdx.x == 0) mbar_init(&mbar_hot, 1);
     if (lane == 0) {
         mbar_init(&ws.colm[0], 1);
-        mbar_init(&ws.colm[1], 1);
+        if (NB == 2) mbar_init(&ws.colm[1], 1);
         mbar_init(&ws.descm[0], 1);
         mbar_init(&ws.descm[1], 1);
     }
@@ -703,9 +754,9 @@ k_term_warp(TermArgs<RP, V> a, const WTile* __restrict__ prog, int P, int ntiles
     __syncthreads();
 
     for (int i = 0; i < nt; i += 2) {
-        term_step<EPI, SINGLE>(a, hot_s, H, ws, my, w, S, nt, i, A, B, p0, p1);
+        term_step<EPI, SINGLE, NB>(a, hot_s, H, ws, my, w, S, nt, i, A, B, p0, p1);
         if (i + 1 >= nt) break;
-        term_step<EPI, SINGLE>(a, hot_s, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
+        term_step<EPI, SINGLE, NB>(a, hot_s, H, ws, my, w, S, nt, i + 1, B, A, p0, p1);
     }
     if constexpr (EPI == EPI_CPAA || EPI == EPI_POWER) {
         if (a.part) {
@@ -1198,10 +1249,13 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
     if (L.fast) {
         // the > 48 KB dynamic shared-memory opt-in is a per-device (per-context) attribute
         static std::atomic<uint64_t> attr_set{0};  // per template instance, bit per device
-        constexpr size_t smem = warp_smem_bytes<V>();
+        constexpr size_t smem1 = warp_smem_bytes<V, 1>(), smem2 = warp_smem_bytes<V, 2>();
         if (first_on_device(attr_set, g->device)) {
-            for (const void* f : {(const void*)k_term_warp<EPI, RP, V, false>, (const void*)k_term_warp<EPI, RP, V, true>}) {
-                const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            const std::pair<const void*, size_t> fs[] = {
+                {(const void*)k_term_warp<EPI, RP, V, false, 2>, smem2}, {(const void*)k_term_warp<EPI, RP, V, true, 2>, smem2},
+                {(const void*)k_term_warp<EPI, RP, V, false, 1>, smem1}, {(const void*)k_term_warp<EPI, RP, V, true, 1>, smem1}};
+            for (const auto& f : fs) {
+                const cudaError_t e = cudaFuncSetAttribute(f.first, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.second);
                 if (e != cudaSuccess) {
                     attr_set.fetch_and(~(uint64_t(1) << (g->device & 63)));  // retry next launch
                     CHEB_CUDA_CHECK(e);
@@ -1210,6 +1264,12 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         }
         // single GPU, canonical inv_degree, no push: the specialised kernel
         const bool single = !a.push && !a.inv && !(g->part.G > 1);
+        // one column-id buffer per warp (more L1) once x is larger than 16 MB, two below
+        // (us/term, 1 vs 2 buffers: C2 8 MB 72.2 / 68.1, C3 19 MB 357.5 / 361.0, C4 fp32
+        // 68 MB 2972 / 3017, C4 fp64 136 MB 3561 / 3739)
+        int nbuf = tuning().colbufs;
+        if (nbuf != 1 && nbuf != 2) nbuf = (int64_t)g->view.x_len * (int64_t)sizeof(V) > (int64_t(16) << 20) ? 1 : 2;
+        const size_t smem = nbuf == 1 ? smem1 : smem2;
         int H = (int)std::min<int64_t>(g->n, hot_capacity<V>());
         if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);
         TermArgs<RP, V> ab = a;
@@ -1247,8 +1307,13 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
                 attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
                 attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
             }
-            if (single) CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V, true>, args, prog, plen, ntiles, H));
-            else CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V, false>, args, prog, plen, ntiles, H));
+            if (nbuf == 1) {
+                if (single) CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V, true, 1>, args, prog, plen, ntiles, H));
+                else CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V, false, 1>, args, prog, plen, ntiles, H));
+            } else {
+                if (single) CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V, true, 2>, args, prog, plen, ntiles, H));
+                else CHEB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_term_warp<EPI, RP, V, false, 2>, args, prog, plen, ntiles, H));
+            }
         };
         int launched = 0;
         if (g->view.phases.empty()) {

@@ -732,3 +732,29 @@ def test_hub_finalize_lane_rows_bitwise_equal_warp_rows(cheb, precision):
     assert info["max_degree"] > 32 * 248  # both finalize paths run
     assert np.array_equal(out[0].ranks, out[1].ranks)
     assert [t.S_k for t in out[0].trace] == [t.S_k for t in out[1].trace]
+
+
+@pytest.mark.parametrize("precision", [64, 32])
+@pytest.mark.parametrize("graph", ["chung_lu", "rmat"])
+def test_single_column_buffer_kernel_bitwise_equal(cheb, graph, precision):
+    """The term kernel with one column-id buffer per warp (picked when x exceeds L2) reads each
+    tile's ids into registers before refilling the buffer, lanes with more than 8 entries of a
+    mixed-degree pack tile included: ranks and trace bitwise equal to the two-buffer kernel."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    if graph == "chung_lu":
+        e, kw = Gen.chung_lu_edges(1 << 17, 2.1, 2.0, 20000.0, 2_000_000, 9), {}
+    else:
+        e, kw = Gen.rmat_edges(16, 16, 0.57, 0.19, 0.19, 5), {"drop_isolated": True}
+    dg, _ = cheb.build_device_graph(e, cheb.BuildOptions(**kw))
+    out = {}
+    try:
+        for nb in (2, 1):
+            assert lib.cheb_set_tuning(b"colbufs", nb) == 0
+            out[nb] = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, precision=precision))
+    finally:
+        lib.cheb_set_tuning(b"colbufs", -1)
+        dg.free()
+    assert np.array_equal(out[1].ranks, out[2].ranks)
+    assert [t.S_k for t in out[1].trace] == [t.S_k for t in out[2].trace]
