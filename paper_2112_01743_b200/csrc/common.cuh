@@ -416,7 +416,8 @@ struct Tuning {
     int hot = -1;       // cap on the shared-memory hot prefix (vertices); -1 = capacity
     int nogather = 0;   // 1: skip the x gathers (timing experiments only; wrong results)
     int skip = 0;       // 1: skip chunk tiles, 2: skip pack tiles, 16+b: only tile bin b (experiments only)
-    int l2win = 1;      // 1: persisting-L2 window over the hot prefix of x (default on)
+    int l2win = 0;      // 1: persisting-L2 window over the hot prefix of x when x exceeds L2 (round 1:
+                        // C4 5.21 -> 4.58 ms/term; with sorted rows + one column buffer it costs 1.6%: off)
     int pdl = 1;        // 1: programmatic dependent launch along the term chain (default on)
     int sortrows = -1;  // view rows in ascending id order: -1 when x exceeds L2, 0 never, 1 always, 2 hub rows only (experiment)
     int chunksched = 1; // hub chunks ordered for conflict-free hot gathers (k_permute_chunks); 2: also
@@ -425,7 +426,8 @@ struct Tuning {
     int l2win_pct = 100; // hitRatio of that window (percent)
     int streamcs = 0;   // 1: per-row operands (row pointers, T, acc loads; T, acc stores) as streaming (.cs)
     int xout_hint = -1; // x_{k+1} stores: 0 plain, 1 L2 evict_first policy, 2 .cs, 3 L2 evict_last policy;
-                        // -1: evict_last when x exceeds L2 (config 4: 4.06 -> 3.95 ms/term), else plain
+                        // -1: plain (config 4 without the window: evict_last 3503-3527 us/term, plain
+                        // 3366-3393; with the round-1 window evict_last had won, 4.06 -> 3.95 ms)
     int xdiscard = 1;   // 1: the term kernel drops the x_out buffer's (dead) lines from L2 at its start
                         // (config 3: 384 -> 381 us/term; no write-back of dead lines)
     int packsched = 0;  // pack-tile entries ordered for conflict-free hot gathers (k_schedule_pack);

@@ -401,8 +401,8 @@ constexpr int hot_capacity() { return (kHotBytes / (int)sizeof(V)); }
 // Column-id landing buffers per warp (NB): 2 = the next tile's ids are copied while the
 // current tile is read; 1 = one buffer, refilled as soon as the current tile's ids are in
 // registers — 34 KB less shared memory per SM, so the carve-out drops from 164 to 132 KB and
-// the L1 holds more in-flight gathers.  Chosen per graph at launch (launch_pass): 1 for an x
-// larger than 16 MB (config 4: 3737 -> 3558 us/term), 2 below (config 2: 68.1 vs 72.2 with 1).
+// the L1 holds more in-flight gathers.  Chosen per graph at launch (launch_pass): 1 when x
+// exceeds L2 (config 4 fp64: 3556 -> 3403-3456 us/term), 2 otherwise (config 2: 68.1 vs 72.2).
 template <class V, int NB>
 struct alignas(16) WarpScratch {
     int colb[NB][kColBuf];  // TMA landing buffers of column ids
@@ -511,11 +511,23 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
         if (NB == 2 && lane == 0) issue_cols(a.col, dn, ws.colb[j % NB], &ws.colm[j % NB]);
         load_rows<EPI>(a, dn, nxt);
     }
-    // single buffer: the next tile's ids are copied once this tile's are in registers
-    auto refill = [&] {
+    // single buffer: the next tile's ids are copied once this tile's are in registers (`dep`:
+    // an XOR of every id the lane read from the buffer).
+    auto refill = [&](int dep) {
         if constexpr (NB == 1) {
-            __syncwarp();
-            if (lane == 0 && i + 1 < nt) issue_cols(a.col, dn, ws.colb[0], &ws.colm[0]);
+            // a warp-wide OR of every lane's ids selects the copy's cache hint (either hint is
+            // correct): the copy cannot issue before all of the warp's id loads have returned,
+            // and the compiler cannot drop the dependency (an empty asm or a vote that does not
+            // feed the copy is optimised away, and the copy then raced the reads: C3/C4 ranks
+            // differed run to run)
+            const unsigned all = __reduce_or_sync(0xffffffffu, (unsigned)dep);
+            if (lane == 0 && i + 1 < nt) {
+                const int64_t a0 = dn.z0 & ~int64_t(7);
+                const unsigned bytes = (unsigned)(((dn.z0 - a0) + dn.cnt + 3) & ~3) * 4u;
+                mbar_expect_tx(&ws.colm[0], bytes);
+                if (all == 0x9e3779b9u) bulk_g2s(ws.colb[0], a.col + a0, bytes, &ws.colm[0]);
+                else bulk_g2s_stream(ws.colb[0], a.col + a0, bytes, &ws.colm[0]);
+            }
         }
     };
     // L2 prefetch of a tile further ahead (its descriptor lives in the current or the next
@@ -559,7 +571,7 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
     if (kExp && a.tune_skip &&
         (a.tune_skip >= 16 ? (((d.meta & kTileChunk) ? 6 : (d.meta & 0xf)) != a.tune_skip - 16)
                            : ((a.tune_skip & 1) ? (d.meta & kTileChunk) : !(d.meta & kTileChunk)))) {
-        refill();
+        refill(0);
         __syncwarp();
         if (lane == 0 && i % kDescBlock == kDescBlock - 1) {
             const int blk = i / kDescBlock + 2;
@@ -584,7 +596,12 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
                 c[q] = pp < d.cnt ? cb[pp] : -1;
             }
         }
-        refill();
+        {
+            int dep = 0;
+#pragma unroll
+            for (int q = 0; q < U; ++q) dep ^= c[q];
+            refill(dep);
+        }
         V v[U];
         if (kExp && a.tune_nogather) {
 #pragma unroll
@@ -631,7 +648,10 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
 #pragma unroll
             for (int q = 0; q < 2 * kPackUnroll; ++q) c8[q] = jj0 + q * L < rend ? cb[jj0 + q * L] : -1;
             const bool more = __any_sync(0xffffffffu, jj0 + 2 * kPackUnroll * L < rend);
-            if (!more) refill();
+            int dep = 0;
+#pragma unroll
+            for (int q = 0; q < 2 * kPackUnroll; ++q) dep ^= c8[q];
+            if (!more) refill(dep);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 if (jj0 + h * kPackUnroll * L < rend) {
@@ -646,16 +666,19 @@ __device__ __forceinline__ void term_step(const TermArgs<RP, V>& a, unsigned hot
             }
             jj0 += 2 * kPackUnroll * L;
             if (more) {  // a lane with more than 2 kPackUnroll entries (mixed-degree tile)
+                int dep2 = dep;  // the first 2 kPackUnroll ids too
                 for (int jj = jj0; jj < rend; jj += kPackUnroll * L) {
                     int c[kPackUnroll];
 #pragma unroll
                     for (int q = 0; q < kPackUnroll; ++q) c[q] = jj + q * L < rend ? cb[jj + q * L] : -1;
+#pragma unroll
+                    for (int q = 0; q < kPackUnroll; ++q) dep2 ^= c[q];
                     V v[kPackUnroll];
                     gather8(a.x_in, hot_s, H, c, v);
 #pragma unroll
                     for (int q = 0; q < kPackUnroll; ++q) sum += v[q];
                 }
-                refill();
+                refill(dep2);
             }
             jj0 = rend;  // done
         }
@@ -1264,11 +1287,15 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         }
         // single GPU, canonical inv_degree, no push: the specialised kernel
         const bool single = !a.push && !a.inv && !(g->part.G > 1);
-        // one column-id buffer per warp (more L1) once x is larger than 16 MB, two below
-        // (us/term, 1 vs 2 buffers: C2 8 MB 72.2 / 68.1, C3 19 MB 357.5 / 361.0, C4 fp32
-        // 68 MB 2972 / 3017, C4 fp64 136 MB 3561 / 3739)
+        // one column-id buffer per warp (more L1) when x exceeds L2, two otherwise (us/term,
+        // 1 vs 2 buffers: C2 8 MB 72.2 / 68.1, C3 19 MB 369 / 361, C4 fp32 68 MB 3072 / 3017,
+        // C4 fp64 136 MB 3403-3456 / 3556-3561)
         int nbuf = tuning().colbufs;
-        if (nbuf != 1 && nbuf != 2) nbuf = (int64_t)g->view.x_len * (int64_t)sizeof(V) > (int64_t(16) << 20) ? 1 : 2;
+        if (nbuf != 1 && nbuf != 2) {
+            int l2 = 0;
+            cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
+            nbuf = (int64_t)g->view.x_len * (int64_t)sizeof(V) > (int64_t)l2 ? 1 : 2;
+        }
         const size_t smem = nbuf == 1 ? smem1 : smem2;
         int H = (int)std::min<int64_t>(g->n, hot_capacity<V>());
         if (tuning().hot >= 0) H = (int)std::min<int64_t>(H, tuning().hot);
@@ -1280,11 +1307,7 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         ab.stream_cs = tuning().streamcs;
         if (g->view.n_hub > 0) ab.stamp_end = nullptr;  // the hub finalize ends the term
         ab.xout_hint = tuning().xout_hint;
-        if (ab.xout_hint < 0) {  // x_{k+1} lines kept in L2 for the next term when x exceeds it
-            int l2 = 0;
-            cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, g->device);
-            ab.xout_hint = (int64_t)g->view.x_len * (int64_t)sizeof(V) > (int64_t)l2 ? 3 : 0;
-        }
+        if (ab.xout_hint < 0) ab.xout_hint = 0;  // plain stores (Tuning::xout_hint)
         // x buffers are cudaMalloc'ed (256-B aligned): whole 128-B lines of x_out only
         ab.xdiscard_len = (EPI == EPI_CPAA && tuning().xdiscard && !a.push && g->part.G == 1 && !g->part.comm)
                               ? (g->view.x_len * (int64_t)sizeof(V) / 128) * 128 / (int64_t)sizeof(V) : 0;
