@@ -309,7 +309,14 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, unsig
 // Column ids are read once per term: an L2 evict-first policy on their TMA copies keeps the
 // per-term streams (~130 MB on C2, about the size of L2) from pushing x out of L2
 // (C2 73.2 -> 70.1 us/term; profiles/r01_gather_microbench.md).
+#ifndef CHEB_COL_EVICT_FIRST
+#define CHEB_COL_EVICT_FIRST 1
+#endif
 __device__ __forceinline__ void bulk_g2s_stream(void* smem_dst, const void* gsrc, unsigned bytes, uint64_t* mbar) {
+    if (!CHEB_COL_EVICT_FIRST) {  // experiments: no cache hint
+        bulk_g2s(smem_dst, gsrc, bytes, mbar);
+        return;
+    }
     const unsigned dst = (unsigned)__cvta_generic_to_shared(smem_dst);
     const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
     uint64_t pol;
