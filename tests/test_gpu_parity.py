@@ -758,3 +758,25 @@ def test_single_column_buffer_kernel_bitwise_equal(cheb, graph, precision):
         dg.free()
     assert np.array_equal(out[1].ranks, out[2].ranks)
     assert [t.S_k for t in out[1].trace] == [t.S_k for t in out[2].trace]
+
+
+def test_single_column_buffer_kernel_deterministic_at_scale(cheb):
+    """One column-id buffer per warp on a graph of ~30 M entries (forced; the product picks it
+    when x exceeds L2): repeated solves are bitwise equal to each other and to the two-buffer
+    kernel (a refill racing the id reads shows up here as run-to-run differences)."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    e = Gen.rmat_edges(20, 16, 0.57, 0.19, 0.19, 13)
+    dg, info = cheb.build_device_graph(e, cheb.BuildOptions(drop_isolated=True))
+    assert info["nnz"] > 20_000_000
+    runs = {}
+    try:
+        for nb in (2, 1, 1, 1):
+            assert lib.cheb_set_tuning(b"colbufs", nb) == 0
+            runs.setdefault(nb, []).append(cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10)).ranks)
+    finally:
+        lib.cheb_set_tuning(b"colbufs", -1)
+        dg.free()
+    for r in runs[1]:
+        assert np.array_equal(r, runs[2][0])
