@@ -428,8 +428,9 @@ struct Tuning {
     int xout_hint = -1; // x_{k+1} stores: 0 plain, 1 L2 evict_first policy, 2 .cs, 3 L2 evict_last policy;
                         // -1: plain (config 4 without the window: evict_last 3503-3527 us/term, plain
                         // 3366-3393; with the round-1 window evict_last had won, 4.06 -> 3.95 ms)
-    int xdiscard = 1;   // 1: the term kernel drops the x_out buffer's (dead) lines from L2 at its start
-                        // (config 3: 384 -> 381 us/term; no write-back of dead lines)
+    int xdiscard = 0;   // 1: the term kernel drops the x_out buffer's (dead) lines from L2 at its start.
+                        // Off: neutral on the current kernel (C2/C3/C4 within 0.2%), and a CTA that
+                        // starts late could discard lines other CTAs of the same launch already wrote
     int packsched = 0;  // pack-tile entries ordered for conflict-free hot gathers (k_schedule_pack);
                         // off: no measurable gain (C2 68.8 -> 68.5, C3 381.6 -> 380.2, C4 3953 -> 3950 us/term)
     int batchblock = 128; // right-hand sides per batched pass (column blocks of one call)
