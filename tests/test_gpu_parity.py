@@ -735,7 +735,7 @@ def test_hub_finalize_lane_rows_bitwise_equal_warp_rows(cheb, precision):
 
 
 @pytest.mark.parametrize("precision", [64, 32])
-@pytest.mark.parametrize("graph", ["chung_lu", "rmat"])
+@pytest.mark.parametrize("graph", ["chung_lu", "rmat", "star100"])
 def test_single_column_buffer_kernel_bitwise_equal(cheb, graph, precision):
     """The term kernel with one column-id buffer per warp (picked when x exceeds L2) reads each
     tile's ids into registers before refilling the buffer, lanes with more than 8 entries of a
@@ -745,8 +745,10 @@ def test_single_column_buffer_kernel_bitwise_equal(cheb, graph, precision):
     lib = _lib.load()
     if graph == "chung_lu":
         e, kw = Gen.chung_lu_edges(1 << 17, 2.1, 2.0, 20000.0, 2_000_000, 9), {}
-    else:
+    elif graph == "rmat":
         e, kw = Gen.rmat_edges(16, 16, 0.57, 0.19, 0.19, 5), {"drop_isolated": True}
+    else:  # the hub (degree 99) shares a pack tile with 31 leaves: one lane walks 99 entries
+        e, kw = load_golden("star100")["edges"], {}
     dg, _ = cheb.build_device_graph(e, cheb.BuildOptions(**kw))
     out = {}
     try:
