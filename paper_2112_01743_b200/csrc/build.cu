@@ -1469,6 +1469,423 @@ static void column_block_schedule(SolverView& V, int K, int64_t x_len, cudaStrea
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
+// ---------------------------------------------------------------------------
+// Column windows of the hub rows (SolverView::Windows; rows hold ascending ids)
+// ---------------------------------------------------------------------------
+// S[h][j], j = 0..NW: position inside hub row h of the first id >= H0 + j W.
+template <class RPN>
+__global__ void k_win_splits(const RPN* __restrict__ rp, const int* __restrict__ col, int64_t n_hub, int H0, int W,
+                             int NW, int* __restrict__ S) {
+    const int64_t total = n_hub * (NW + 1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = i / (NW + 1);
+        const int j = (int)(i - h * (NW + 1));
+        const int64_t key64 = (int64_t)H0 + (int64_t)j * W;
+        const int key = key64 > INT32_MAX ? INT32_MAX : (int)key64;
+        int64_t lo = rp[h], hi = rp[h + 1];
+        const int64_t b = lo;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (col[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        S[i] = (int)(lo - b);
+    }
+}
+
+// Piece sizes, window-major: csz[w n_hub + h] = entries of row h inside window w (tail: 0).
+__global__ void k_win_sizes(const int* __restrict__ S, int64_t n_hub, int NW, int64_t* __restrict__ csz) {
+    const int64_t total = n_hub * NW;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q <= total; q += (int64_t)gridDim.x * blockDim.x) {
+        if (q == total) {
+            csz[q] = 0;
+            continue;
+        }
+        const int64_t w = q / n_hub, h = q - w * n_hub;
+        csz[q] = (int64_t)(S[h * (NW + 1) + w + 1] - S[h * (NW + 1) + w]);
+    }
+}
+
+__global__ void k_win_gather_starts(const int64_t* __restrict__ off, int64_t n_hub, int NW, int64_t* __restrict__ out) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w <= NW) out[w] = off[(int64_t)w * n_hub];
+}
+
+// Window-local 16-bit ids into the stream, and each piece's start bit.  A warp per hub row.
+template <class RPN>
+__global__ void k_win_copy(const RPN* __restrict__ rp, const int* __restrict__ col, int64_t n_hub,
+                           const int* __restrict__ S, const int64_t* __restrict__ off,
+                           const int64_t* __restrict__ delta, int H0, int W, int NW,
+                           unsigned short* __restrict__ wcol, unsigned* __restrict__ flags32) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t h = gw; h < n_hub; h += nw) {
+        const int64_t base = rp[h];
+        const int* Sh = S + h * (NW + 1);
+        const int e0 = Sh[0], e1 = Sh[NW];
+        for (int e = e0 + lane; e < e1; e += 32) {
+            const int id = col[base + e] - H0;
+            const int w = id / W;
+            const int64_t pos = off[(int64_t)w * n_hub + h] + delta[w] + (e - Sh[w]);
+            wcol[pos] = (unsigned short)(id - w * W);
+        }
+        for (int w = lane; w < NW; w += 32) {
+            if (Sh[w + 1] > Sh[w]) {
+                const int64_t pos = off[(int64_t)w * n_hub + h] + delta[w];
+                atomicOr(&flags32[pos >> 5], 1u << (pos & 31));
+            }
+        }
+    }
+}
+
+// Pieces starting inside block [blk 256, +256) before in-block position r (the block's
+// first entry always starts one).
+__device__ __forceinline__ int win_starts_before(const unsigned* __restrict__ flags32, int64_t blk, int r) {
+    const unsigned* words = flags32 + blk * (kWinBlock / 32);
+    int cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kWinBlock / 32; ++j) {
+        unsigned wd = words[j];
+        if (j == 0) wd |= 1u;
+        const int lo = j * 32;
+        if (r >= lo + 32) cnt += __popc(wd);
+        else if (r > lo) cnt += __popc(wd & ((1u << (r - lo)) - 1u));
+    }
+    return cnt;
+}
+
+// Padding between a window's last entry and its last block's end: one dummy piece.
+__global__ void k_win_padflags(const int64_t* __restrict__ wend, int NW, unsigned* __restrict__ flags32) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < NW && (wend[w] & (kWinBlock - 1))) atomicOr(&flags32[wend[w] >> 5], 1u << (wend[w] & 31));
+}
+
+// Entries re-ordered inside their pieces (a piece is a sum: any order) so that the 16 lanes
+// of a half-warp read distinct bank pairs of the fp64 window (id mod 16) in each of the 8
+// gather instructions of a block: position p is read by lane p / 8 in instruction p % 8.
+// Greedy, a thread per block: each position takes, among the next entries of its piece, one
+// whose bank pair the instruction's half-warp has not used yet.
+__global__ void k_win_bank_order(unsigned short* __restrict__ wcol, const unsigned* __restrict__ flags32,
+                                 int64_t n_blocks) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n_blocks; b += (int64_t)gridDim.x * blockDim.x) {
+        unsigned short* ids = wcol + b * kWinBlock;
+        const unsigned* fw = flags32 + b * (kWinBlock / 32);
+        unsigned used[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [instruction]: low half-warp bits 0-15, high half-warp 16-31
+        int pe = 0;
+        for (int p = 0; p < kWinBlock; ++p) {
+            if (p >= pe) {  // next piece start after p
+                pe = p + 1;
+                while (pe < kWinBlock && !((fw[pe >> 5] >> (pe & 31)) & 1u)) ++pe;
+            }
+            const int sh = (p >> 7) << 4;
+            const unsigned mask = used[p & 7] >> sh;
+            const int lim = min(pe, p + 24);
+            int pick = p;
+            for (int j = p; j < lim; ++j)
+                if (!((mask >> (ids[j] & 15)) & 1u)) {
+                    pick = j;
+                    break;
+                }
+            const unsigned short v = ids[pick];
+            ids[pick] = ids[p];
+            ids[p] = v;
+            used[p & 7] |= 1u << (sh + (v & 15));
+        }
+    }
+}
+
+// Per lane of every block: its 8 start bits (block start forced) and the number of pieces
+// started in the block's earlier lanes, as one 16-bit word (starts | before << 8).
+__global__ void k_win_lanemeta(const unsigned char* __restrict__ flags8, int64_t n_blocks,
+                               unsigned short* __restrict__ meta) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t b = gw; b < n_blocks; b += nw) {
+        unsigned m = flags8[b * 32 + lane];
+        if (lane == 0) m |= 1u;
+        const int mine = __popc(m);
+        int pre = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += t;
+        }
+        meta[b * 32 + lane] = (unsigned short)(m | ((unsigned)(pre - mine) << 8));
+    }
+}
+
+__global__ void k_win_blockcount(const unsigned* __restrict__ flags32, int64_t n_blocks, int* __restrict__ pc) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= n_blocks; b += (int64_t)gridDim.x * blockDim.x)
+        pc[b] = b < n_blocks ? win_starts_before(flags32, b, kWinBlock) : 0;
+}
+
+// Block ranges of the window pass's CTAs: equal shares of the cost 256 b + pw pieces(b)
+// (blocks of short pieces store more sums and keep more bank conflicts).
+__global__ void k_win_cta_starts(const int* __restrict__ bbase, int64_t n_blocks, int pw, int grid,
+                                 int64_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > grid) return;
+    const double total = 256.0 * (double)n_blocks + (double)pw * (double)bbase[n_blocks];
+    const double target = total * (double)i / (double)grid;
+    int64_t lo = 0, hi = n_blocks;
+    while (lo < hi) {  // first b with cost(b) >= target
+        const int64_t mid = (lo + hi) >> 1;
+        if (256.0 * (double)mid + (double)pw * (double)bbase[mid] < target) lo = mid + 1;
+        else hi = mid;
+    }
+    out[i] = i == grid ? n_blocks : lo;
+}
+
+// Per hub row: its chunk tiles over the entries left in the row (ids < H0, then ids past the
+// last window), its pieces before window w (subx), and its piece count.
+template <class RPN>
+__global__ void k_win_rows(const RPN* __restrict__ rp, int64_t n_hub, const int* __restrict__ S,
+                           const int64_t* __restrict__ off, const int64_t* __restrict__ delta, int NW, int wide_min,
+                           int* __restrict__ mc, int* __restrict__ rowpieces, int* __restrict__ subx,
+                           unsigned long long* __restrict__ wide) {
+    for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h <= n_hub; h += (int64_t)gridDim.x * blockDim.x) {
+        if (h == n_hub) {
+            mc[h] = 0;
+            rowpieces[h] = 0;
+            continue;
+        }
+        const int64_t d = rp[h + 1] - rp[h];
+        const int* Sh = S + h * (NW + 1);
+        const int64_t sA = Sh[0], tail = d - Sh[NW];
+        const int m = (int)((sA + kWarpNnz - 1) / kWarpNnz + (tail + kWarpNnz - 1) / kWarpNnz);
+        int s = 0;
+        for (int w = 0; w < NW; ++w) {
+            subx[h * NW + w] = s;
+            const int64_t c = Sh[w + 1] - Sh[w];
+            if (c > 0) {
+                const int64_t pos = off[(int64_t)w * n_hub + h] + delta[w];
+                s += (int)(((pos + c - 1) >> 8) - (pos >> 8)) + 1;
+            }
+        }
+        mc[h] = m;
+        rowpieces[h] = s;
+        if (m + s > wide_min) atomicMax(wide, (unsigned long long)(h + 1));
+    }
+}
+static_assert(kWinBlock == 256, "k_win_rows / k_win_klist shift by 8");
+
+// Every hub row's pieces (stream indices), row by row in window order: klist[kf[h] ..).
+__global__ void k_win_klist(int64_t n_hub, const int* __restrict__ S, const int64_t* __restrict__ off,
+                            const int64_t* __restrict__ delta, int NW, const unsigned* __restrict__ flags32,
+                            const int* __restrict__ bbase, const int* __restrict__ kf, const int* __restrict__ subx,
+                            int* __restrict__ klist) {
+    const int64_t total = n_hub * NW;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t h = i / NW;
+        const int w = (int)(i - h * NW);
+        const int64_t c = S[h * (NW + 1) + w + 1] - S[h * (NW + 1) + w];
+        if (c <= 0) continue;
+        const int64_t pos = off[(int64_t)w * n_hub + h] + delta[w];
+        const int64_t blk = pos >> 8;
+        const int nsub = (int)(((pos + c - 1) >> 8) - blk) + 1;
+        int* dst = klist + kf[h] + subx[i];
+        dst[0] = bbase[blk] + win_starts_before(flags32, blk, (int)(pos & 255));
+        for (int q = 1; q < nsub; ++q) dst[q] = bbase[blk + q];  // cut at a block start: that block's first piece
+    }
+}
+
+// The term kernel's program with windows: hub row h keeps chunk tiles over [0, S[h][0]) and
+// [S[h][NW], d) (tile tb[h] + j = its partial's slot); pack tiles follow unchanged.
+template <class RPN>
+__global__ void k_win_prog_hub(const RPN* __restrict__ rp, int64_t n_hub, const int* __restrict__ S, int NW,
+                               const int* __restrict__ tb, int Sw, int len, WTile* __restrict__ prog) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t h = gw; h < n_hub; h += nw) {
+        const int64_t base = rp[h], d = rp[h + 1] - base;
+        const int64_t sA = S[h * (NW + 1)], sC = S[h * (NW + 1) + NW];
+        const int nA = (int)((sA + kWarpNnz - 1) / kWarpNnz);
+        const int m = tb[h + 1] - tb[h];
+        for (int j = lane; j < m; j += 32) {
+            int64_t p, end;
+            if (j < nA) {
+                p = (int64_t)j * kWarpNnz;
+                end = sA;
+            } else {
+                p = sC + (int64_t)(j - nA) * kWarpNnz;
+                end = d;
+            }
+            WTile wt;
+            wt.nnz_begin = base + p;
+            wt.row_begin = tb[h] + j;
+            wt.cnt = (uint16_t)(end - p < kWarpNnz ? end - p : kWarpNnz);
+            wt.rows = 1;
+            wt.meta = (uint8_t)kTileChunk;
+            const int64_t t = (int64_t)tb[h] + j;
+            prog[(size_t)(t % Sw) * len + t / Sw] = wt;
+        }
+    }
+}
+
+__global__ void k_win_prog_pack(const Tile* __restrict__ tiles, int old_chunks, int n_tiles_old, int MC, int Sw,
+                                int len, WTile* __restrict__ prog) {
+    for (int64_t t0 = old_chunks + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t0 < n_tiles_old;
+         t0 += (int64_t)gridDim.x * blockDim.x) {
+        const Tile a = tiles[t0], b = tiles[t0 + 1];
+        WTile wt;
+        wt.nnz_begin = a.nnz_begin;
+        wt.row_begin = a.row_begin;
+        wt.cnt = (uint16_t)(b.nnz_begin - a.nnz_begin);
+        wt.rows = (uint8_t)(b.row_begin - a.row_begin);
+        wt.meta = (uint8_t)a.meta;
+        const int64_t t = (int64_t)MC + (t0 - old_chunks);
+        prog[(size_t)(t % Sw) * len + t / Sw] = wt;
+    }
+}
+
+template <class T>
+static void exclusive_scan(const T* in, T* out, int64_t cnt, TempStore& tmp, cudaStream_t st) {
+    size_t bytes = 0;
+    CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, cnt, st));
+    void* t = tmp.get(bytes);
+    CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, bytes, in, out, cnt, st));
+}
+
+// Builds SolverView::Windows on the device (hub rows ascending).  NW windows of W entries
+// from id H0 = the fp64 hot-prefix capacity.
+template <class RPN>
+static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
+    SolverView::Windows& Wn = V.win;
+    Wn.release();
+    const int64_t n_hub = V.n_hub;
+    const int H0 = kHotBytes / 8;
+    W = std::max(256, std::min(W, 65536)) & ~7;
+    if (n_hub <= 0 || V.x_len <= H0) return;
+    const int NW = (int)std::min<int64_t>(NW_req, (V.x_len - H0 + W - 1) / W);
+    if (NW <= 0 || n_hub * (int64_t)(NW + 1) >= (int64_t)INT32_MAX * 4) return;
+    TempStore tmp;
+    const RPN* rp = V.row_ptr.ptr<RPN>();
+    const int* col = V.col.ptr<int>();
+    DevMem S(sizeof(int) * (size_t)n_hub * (NW + 1));
+    k_win_splits<RPN><<<grid_for(n_hub * (NW + 1)), kBuildThreads, 0, st>>>(rp, col, n_hub, H0, W, NW, S.ptr<int>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    const int64_t nq = n_hub * NW;
+    DevMem csz(sizeof(int64_t) * (size_t)(nq + 1)), off(sizeof(int64_t) * (size_t)(nq + 1));
+    k_win_sizes<<<grid_for(nq + 1), kBuildThreads, 0, st>>>(S.ptr<int>(), n_hub, NW, csz.ptr<int64_t>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    exclusive_scan(csz.ptr<int64_t>(), off.ptr<int64_t>(), nq + 1, tmp, st);
+    csz.release();
+    DevMem d_small(sizeof(int64_t) * (size_t)(4 * (NW + 1)));
+    int64_t* d_starts = d_small.ptr<int64_t>();        // [NW + 1] unpadded window starts
+    int64_t* d_delta = d_starts + (NW + 1);             // [NW]
+    int64_t* d_wend = d_delta + (NW + 1);               // [NW]
+    int64_t* d_wblk = d_wend + (NW + 1);                // [NW + 1]
+    k_win_gather_starts<<<(NW + 1 + 127) / 128, 128, 0, st>>>(off.ptr<int64_t>(), n_hub, NW, d_starts);
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    std::vector<int64_t> hs((size_t)4 * (NW + 1), 0);
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(hs.data(), d_starts, sizeof(int64_t) * (NW + 1), cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    int64_t* h_delta = hs.data() + (NW + 1);
+    int64_t* h_wend = h_delta + (NW + 1);
+    int64_t* h_wblk = h_wend + (NW + 1);
+    int64_t cur = 0;
+    for (int w = 0; w < NW; ++w) {
+        const int64_t len = hs[(size_t)w + 1] - hs[(size_t)w];
+        h_delta[w] = cur - hs[(size_t)w];
+        h_wend[w] = cur + len;
+        h_wblk[w] = cur / kWinBlock;
+        cur = (cur + len + kWinBlock - 1) / kWinBlock * kWinBlock;
+    }
+    h_wblk[NW] = cur / kWinBlock;
+    const int64_t entries = hs[(size_t)NW], stream_len = cur, n_blocks = cur / kWinBlock;
+    if (entries == 0 || n_blocks >= INT32_MAX / 2) return;
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(d_delta, h_delta, sizeof(int64_t) * 3 * (NW + 1), cudaMemcpyHostToDevice, st));
+    Wn.wcol.alloc(sizeof(unsigned short) * (size_t)stream_len + 64);
+    Wn.flags.alloc((size_t)stream_len / 8 + 64);
+    CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.wcol.get(), 0, sizeof(unsigned short) * (size_t)stream_len + 64, st));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.flags.get(), 0, (size_t)stream_len / 8 + 64, st));
+    unsigned* flags32 = Wn.flags.ptr<unsigned>();
+    k_win_copy<RPN><<<(int)std::min<int64_t>((n_hub * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+        rp, col, n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, H0, W, NW, Wn.wcol.ptr<unsigned short>(), flags32);
+    k_win_padflags<<<(NW + 127) / 128, 128, 0, st>>>(d_wend, NW, flags32);
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    if (tuning().winbank)
+        k_win_bank_order<<<grid_for(n_blocks, 128), 128, 0, st>>>(Wn.wcol.ptr<unsigned short>(), flags32, n_blocks);
+    Wn.meta.alloc(sizeof(unsigned short) * (size_t)n_blocks * 32 + 64);
+    k_win_lanemeta<<<(int)std::min<int64_t>((n_blocks * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+        Wn.flags.ptr<unsigned char>(), n_blocks, Wn.meta.ptr<unsigned short>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    DevMem pc(sizeof(int) * (size_t)(n_blocks + 1));
+    Wn.bbase.alloc(sizeof(int) * (size_t)(n_blocks + 1));
+    k_win_blockcount<<<grid_for(n_blocks + 1), kBuildThreads, 0, st>>>(flags32, n_blocks, pc.ptr<int>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    exclusive_scan(pc.ptr<int>(), Wn.bbase.ptr<int>(), n_blocks + 1, tmp, st);
+    Wn.grid = (int)std::max<int64_t>(1, std::min<int64_t>(V.grid, n_blocks));
+    Wn.cta.alloc(sizeof(int64_t) * (size_t)(Wn.grid + 1));
+    k_win_cta_starts<<<(Wn.grid + 1 + 127) / 128, 128, 0, st>>>(Wn.bbase.ptr<int>(), n_blocks, tuning().winpw, Wn.grid,
+                                                             Wn.cta.ptr<int64_t>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    DevMem mc(sizeof(int) * (size_t)(n_hub + 1)), rowpieces(sizeof(int) * (size_t)(n_hub + 1)),
+        subx(sizeof(int) * (size_t)nq), wide(sizeof(unsigned long long));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(wide.get(), 0, sizeof(unsigned long long), st));
+    constexpr int kWideMin = 128;  // more partials than this: a warp per row in k_hub_finalize
+    k_win_rows<RPN><<<grid_for(n_hub + 1), kBuildThreads, 0, st>>>(rp, n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, NW,
+                                                                  kWideMin, mc.ptr<int>(), rowpieces.ptr<int>(),
+                                                                  subx.ptr<int>(), wide.ptr<unsigned long long>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    Wn.hub_first.alloc(sizeof(int) * (size_t)(n_hub + 1));  // tb: first main chunk tile (= slot) of each hub row
+    Wn.kf.alloc(sizeof(int) * (size_t)(n_hub + 1));
+    int* tb = Wn.hub_first.ptr<int>();
+    exclusive_scan(mc.ptr<int>(), tb, n_hub + 1, tmp, st);
+    exclusive_scan(rowpieces.ptr<int>(), Wn.kf.ptr<int>(), n_hub + 1, tmp, st);
+    int h_tot[3] = {0, 0, 0};
+    unsigned long long h_wide = 0;
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_tot[0], Wn.bbase.ptr<int>() + n_blocks, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_tot[1], tb + n_hub, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_tot[2], Wn.kf.ptr<int>() + n_hub, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_wide, wide.get(), sizeof h_wide, cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    const int pieces = h_tot[0], MC = h_tot[1], listed = h_tot[2];  // pieces = listed + the padding's
+    if ((int64_t)MC + pieces >= INT32_MAX) fail(CHEB_CAPACITY, "too many hub partials");
+    Wn.klist.alloc(sizeof(int) * (size_t)std::max(listed, 1));
+    k_win_klist<<<grid_for(nq), kBuildThreads, 0, st>>>(n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, NW, flags32,
+                                                     Wn.bbase.ptr<int>(), Wn.kf.ptr<int>(), subx.ptr<int>(),
+                                                     Wn.klist.ptr<int>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    // the term kernel's program: main chunk tiles, then the view's pack tiles
+    const int npack = V.n_tiles - V.n_chunk_tiles;
+    if ((int64_t)MC + npack >= INT32_MAX) fail(CHEB_CAPACITY, "too many tiles");
+    Wn.n_tiles = MC + npack;
+    const int Sw = V.grid * kWarps;
+    const int per = (Wn.n_tiles + Sw - 1) / Sw;
+    Wn.prog_len = std::max(kDescBlock, (per + kDescBlock - 1) / kDescBlock * kDescBlock);
+    const size_t np = (size_t)Sw * Wn.prog_len;
+    Wn.prog.alloc(sizeof(WTile) * np);
+    CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.prog.get(), 0, sizeof(WTile) * np, st));
+    k_win_prog_hub<RPN><<<(int)std::min<int64_t>((n_hub * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+        rp, n_hub, S.ptr<int>(), NW, tb, Sw, Wn.prog_len, Wn.prog.ptr<WTile>());
+    if (npack > 0)
+        k_win_prog_pack<<<grid_for(npack), kBuildThreads, 0, st>>>(V.tiles.ptr<Tile>(), V.n_chunk_tiles, V.n_tiles, MC, Sw,
+                                                                 Wn.prog_len, Wn.prog.ptr<WTile>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
+    Wn.wblk.alloc(sizeof(int64_t) * (size_t)(NW + 1));
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(Wn.wblk.get(), d_wblk, sizeof(int64_t) * (NW + 1), cudaMemcpyDeviceToDevice, st));
+    CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    (void)h_wblk;
+    Wn.NW = NW;
+    Wn.W = W;
+    Wn.H0 = H0;
+    Wn.n_blocks = n_blocks;
+    Wn.n_slots = (int64_t)MC + pieces;
+    Wn.MC = MC;
+    Wn.n_wide = (int64_t)h_wide;
+    Wn.entries = entries;
+    Wn.pieces = pieces;
+    Wn.ready = true;
+    if (dbg_on())
+        dbg_mark(("  view: column windows (" + std::to_string(NW) + " x " + std::to_string(W) + ": " +
+                  std::to_string(entries) + " entries, " + std::to_string(pieces) + " pieces, " +
+                  std::to_string(MC) + " main chunk tiles, wide rows " + std::to_string(h_wide) + ")").c_str());
+}
+
 // Each of the first `segs` view rows' renamed ids in ascending order (cub segmented sort,
 // in place over V.col).
 template <class RPN>
@@ -1643,7 +2060,10 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     }
     const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2) : tuning().sortrows > 0;
-    const bool hubs_only = tuning().sortrows == 2 && V.n_hub > 0;
+    // column windows (single-GPU views) need the hub rows in ascending id order
+    const bool want_windows = tuning().windows > 0 && P.G == 1 && V.n_hub > 0 && tuning().chunksched <= 1 &&
+                              V.x_len > kHotBytes / 8;
+    const bool hubs_only = (tuning().sortrows == 2 || (want_windows && !big_x)) && V.n_hub > 0;
     const bool sort_rows = (big_x || hubs_only) && nnz_l > 0 && nnz_l < INT32_MAX;
     const bool sort_grouped = sort_rows && !hubs_only;  // every row, group by group into V.col
     V.sorted_rows = sort_grouped;
@@ -1739,6 +2159,11 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
             CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
             column_block_schedule<RPN>(V, tuning().colblocks, V.x_len, st);
             dbg_mark("  view: column-block schedule");
+        }
+        V.win.release();
+        if (want_windows && sort_rows) {
+            window_schedule<RPN>(V, tuning().windows, tuning().winsize, st);
+            dbg_mark("  view: column windows");
         }
         if (sort_grouped && tuning().chunksched > 1 && V.n_chunk_tiles > 0) {  // the sort undid the chunk order
             k_schedule_chunks_inplace<RPN><<<std::max(1, std::min((V.n_chunk_tiles + 7) / 8, 148 * 16)), 256, 0, st>>>(

@@ -1159,6 +1159,8 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "colbufs") tuning().colbufs = value;
         else if (k == "colblocks") tuning().colblocks = value;  // applies to views built afterwards
         else if (k == "colsplit_pct") tuning().colsplit_pct = value;  // applies to views built afterwards
+        else if (k == "windows") tuning().windows = value;    // applies to views built afterwards
+        else if (k == "winsize") tuning().winsize = value;    // applies to views built afterwards
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }

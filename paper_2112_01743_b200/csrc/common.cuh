@@ -200,6 +200,7 @@ struct WTile {
     uint8_t meta;
 };
 static_assert(sizeof(WTile) == 16, "WTile is 16 bytes");
+constexpr int kWinBlock = 256;       // entries per block of the window stream (a warp: 8 per lane)
 constexpr int kDescBlock = 8;        // descriptors per TMA refill of a warp's program ring
 constexpr int kThreads = 256;        // CTA size of the auxiliary kernels
 #ifndef CHEB_WARPS
@@ -247,6 +248,44 @@ struct SolverView {
     };
     std::vector<Phase> phases;
     bool sorted_rows = false;  // rows hold their renamed ids in ascending order
+    // Column windows of the hub rows (single-GPU views, build.cu window_schedule): the x ids
+    // [H0, H0 + NW W) are cut into NW windows of W entries.  Every hub row's entries inside a
+    // window (a contiguous piece of the ascending row) are copied, as 16-bit window-local ids,
+    // into one window-major stream cut into blocks of kWinBlock entries; k_window_pass loads a
+    // window of x_k into shared memory and sums each piece from there, so these entries cost
+    // no L2 sector.  A piece (cut again where it crosses a block) writes its sum to
+    // hub_part[MC + k], k its index in stream order (coalesced stores); slots [0, MC) are the
+    // chunk tiles over the entries left in the rows (hot prefix and cold ids).  k_hub_finalize
+    // adds a row's chunk partials hub_part[hub_first[h] ..) and its pieces klist[kf[h] ..).
+    // The term kernel then runs `prog` below instead of the view's own program (which, with
+    // tiles / hub_first above, stays as built for the batched path and the introspection).
+    struct Windows {
+        bool ready = false;
+        int NW = 0, W = 0, H0 = 0;
+        int64_t n_blocks = 0;      // stream blocks (kWinBlock entries each)
+        int64_t n_slots = 0;       // hub_part slots: MC + pieces
+        int MC = 0;                // main chunk tiles (slots [0, MC))
+        int64_t n_wide = 0;        // hub rows [0, n_wide) finalized by a warp each
+        int64_t entries = 0;       // windowed entries (statistics)
+        int64_t pieces = 0;        // their slots
+        DevMem wcol;               // uint16 [n_blocks * kWinBlock] window-local ids
+        DevMem flags;              // uint8 [n_blocks * 32]: bit i of byte j = entry 8 j + i starts a piece
+        DevMem meta;               // uint16 [n_blocks * 32]: per lane, its start bits | pieces in earlier lanes << 8
+        DevMem bbase;              // int32 [n_blocks + 1]: pieces before each block
+        DevMem kf;                 // int32 [n_hub + 1]: first klist entry of each hub row
+        DevMem klist;              // int32: the rows' pieces (stream indices), row by row
+        DevMem wblk;               // int64 [NW + 1]: first block of each window
+        DevMem cta;                // int64 [grid + 1]: block range of each CTA of the window pass
+        int grid = 0;
+        DevMem prog;               // WTile programs of the term kernel (main chunk tiles + pack tiles)
+        int prog_len = 0, n_tiles = 0;
+        DevMem hub_first;          // int32 [n_hub + 1]: first main chunk tile (slot) of each hub row
+        void release() {
+            ready = false;
+            for (DevMem* d : {&wcol, &flags, &meta, &bbase, &cta, &kf, &klist, &wblk, &prog, &hub_first}) d->release();
+        }
+    };
+    Windows win;
     // Row partition (G > 1): bit r of push_mask[u] = rank r has a row with neighbour u, i.e.
     // needs x[u] (symmetric graph: u has a neighbour owned by r).  The halo-only push stores
     // x_{k+1}[u] only there.  push_entries = sum of popcounts over the local rows minus the
@@ -258,7 +297,8 @@ struct SolverView {
     int64_t bin_tiles[7] = {}, bin_rows[7] = {}, bin_nnz[7] = {};
     void set_stream(cudaStream_t s) {
         for (DevMem* d : {&order, &rank, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first, &push_mask,
-                          &col_sorted})
+                          &col_sorted, &win.wcol, &win.flags, &win.meta, &win.bbase, &win.cta, &win.kf, &win.klist, &win.wblk, &win.prog,
+                          &win.hub_first})
             d->set_stream(s);
     }
 };
@@ -446,6 +486,11 @@ struct Tuning {
     int hubwarp = 0;    // 1: every hub row finalized by a warp (the lane-per-row path off; tests)
     int pull = 1;       // view tiles / programs pulled from pinned host memory by a kernel (not the copy engine)
     int colsplit_pct = -1; // K = 2: first block boundary at this percent of x (-1: equal halves)
+    int windows = 0;    // NW > 0: column windows of the hub rows (SolverView::Windows), single-GPU views
+    int winbank = 1;    // window stream entries ordered inside their pieces for conflict-free shared-memory gathers
+    int winpw = 4;      // window pass CTA ranges: cost of a block = 256 + winpw * its pieces
+    int winskip = 0;    // timing experiments (wrong results): 1 no window pass, 2 no term kernel, 3 no hub finalize
+    int winsize = 24576; // entries of x per window (<= 65536: 16-bit local ids; fp64 192 KB of shared memory)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -474,6 +519,11 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_COLBUFS")) x.colbufs = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_UPGROUPS")) x.upgroups = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_COLSPLIT_PCT")) x.colsplit_pct = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_WINDOWS")) x.windows = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_WINSIZE")) x.winsize = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_WINSKIP")) x.winskip = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_WINBANK")) x.winbank = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_WINPW")) x.winpw = std::atoi(e);
         return x;
     }();
     return t;

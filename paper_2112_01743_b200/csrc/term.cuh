@@ -834,7 +834,8 @@ __device__ __forceinline__ void hub_epilogue(const TermArgs<RP, V>& a, int64_t h
 
 template <int EPI, class RP, class V>
 __global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const int* __restrict__ hub_first,
-                                                      int64_t n_hub, int64_t n_wide) {
+                                                      int64_t n_hub, int64_t n_wide, const int* __restrict__ kf,
+                                                      const int* __restrict__ klist, const double* __restrict__ wpart) {
     const int lane = threadIdx.x & 31;
     pdl_trigger();
     pdl_wait();  // the term kernel's hub partials
@@ -844,6 +845,10 @@ __global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const i
         const int f0 = hub_first[h], f1 = hub_first[h + 1];
         double tot = 0.0;
         for (int q = f0 + lane; q < f1; q += 32) tot += a.hub_part[q];
+        if (kf) {  // the row's window pieces (SolverView::Windows)
+            const int g0 = kf[h], g1 = kf[h + 1];
+            for (int q = g0 + lane; q < g1; q += 32) tot += wpart[klist[q]];
+        }
         tot = warp_sum_v(tot);
         if (lane == 0) hub_epilogue<EPI>(a, h, tot);
     }
@@ -868,9 +873,139 @@ __global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const i
             tot = 0.0;
             for (int q = 0; q < m; ++q) tot += a.hub_part[f0 + q];
         }
+        if (kf) {
+            const int g0 = kf[h], g1 = kf[h + 1];
+            int q = g0;
+            for (; q + 4 <= g1; q += 4) {  // four independent loads in flight, summed in list order
+                const double p0 = wpart[klist[q]], p1 = wpart[klist[q + 1]], p2 = wpart[klist[q + 2]],
+                             p3 = wpart[klist[q + 3]];
+                tot += p0;
+                tot += p1;
+                tot += p2;
+                tot += p3;
+            }
+            for (; q < g1; ++q) tot += wpart[klist[q]];
+        }
         hub_epilogue<EPI>(a, h, tot);
     }
     if (a.stamp_end) stamp_last_cta(a.done, a.stamp_end);
+}
+
+// ---------------- column windows of the hub rows (SolverView::Windows) -----------------
+// One CTA per SM over a contiguous range of the window-major stream's blocks.  A CTA loads the
+// window of x_k its blocks belong to into shared memory (reloading when its range crosses into
+// the next window); a warp takes one block of kWinBlock entries at a time, lane l the 8
+// consecutive entries 8 l .. 8 l + 7 (one 16-byte load of 16-bit window-local ids), gathers
+// them from shared memory and sums them piece by piece: runs that start and end inside the
+// lane are stored directly, a run still open at the lane's end takes the following lanes'
+// leading sums up to the next start (segmented suffix scan over the lanes, fixed order).  A
+// block's first entry always starts a piece, so no sum crosses blocks.  Piece sums are in
+// fp64; piece k of the stream goes to wpart[k] (consecutive pieces, coalesced stores), and
+// k_hub_finalize adds a row's pieces (klist) to its chunk partials.  Every entry handled here costs one shared-memory load instead of an L2 sector.
+struct WinBlock {
+    uint4 ids;
+    unsigned m;
+    int kb;
+};
+__device__ __forceinline__ WinBlock win_load(const uint4* __restrict__ wcol, const unsigned short* __restrict__ meta,
+                                             const int* __restrict__ bbase, int64_t blk, int64_t end, int lane) {
+    WinBlock b{};
+    if (blk < end) {
+        b.ids = __ldcs(wcol + blk * 32 + lane);
+        b.m = __ldcs(meta + blk * 32 + lane);  // start bits | pieces started in earlier lanes << 8
+        b.kb = bbase[blk];
+    }
+    return b;
+}
+
+constexpr int kWinAhead = 3;  // blocks of the stream in flight per warp (registers)
+
+template <class V>
+__global__ void __launch_bounds__(1024, 1)
+k_window_pass(const V* __restrict__ x, int64_t x_len, int H0, int W, int NW, const int64_t* __restrict__ wblk,
+              const uint4* __restrict__ wcol, const unsigned short* __restrict__ flags, const int* __restrict__ bbase,
+              double* __restrict__ wpart, const int64_t* __restrict__ cta, unsigned long long* stamp_start) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    V* win = reinterpret_cast<V*>(smem);
+    __shared__ __align__(8) uint64_t mbar;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(&mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_trigger();
+    pdl_wait();  // x_k comes from the previous term's kernels
+    if (stamp_start && blockIdx.x == 0 && threadIdx.x == 0) *stamp_start = global_ns();
+    const int64_t b0 = cta[blockIdx.x], b1 = cta[blockIdx.x + 1];
+    int w = 0;
+    unsigned phase = 0;
+    int64_t b = b0;
+    while (b < b1) {
+        while (wblk[w + 1] <= b) ++w;  // b < n_blocks = wblk[NW]
+        const int64_t e = min(b1, wblk[w + 1]);
+        const int64_t base = (int64_t)H0 + (int64_t)w * W;
+        const int cnt = (int)min((int64_t)W, x_len - base);
+        // this warp's first blocks of the window: issued before the window itself lands
+        WinBlock q[kWinAhead];
+#pragma unroll
+        for (int j = 0; j < kWinAhead; ++j) q[j] = win_load(wcol, flags, bbase, b + warp + 32 * j, e, lane);
+        __syncthreads();  // the previous window's gathers are done
+        const unsigned bytes = (unsigned)(cnt * sizeof(V)) & ~15u;  // base is a multiple of 8 entries: 16-byte aligned
+        if (threadIdx.x == 0) {
+            mbar_expect_tx(&mbar, bytes);
+            constexpr unsigned kPiece = 32768;
+            for (unsigned o = 0; o < bytes; o += kPiece)
+                bulk_g2s(smem + o, reinterpret_cast<const unsigned char*>(x + base) + o, min(kPiece, bytes - o), &mbar);
+        }
+        for (int i = bytes / sizeof(V) + threadIdx.x; i < cnt; i += blockDim.x) win[i] = x[base + i];
+        mbar_wait(&mbar, phase);
+        phase ^= 1u;
+        __syncthreads();
+        for (int64_t blk = b + warp; blk < e; blk += 32 * kWinAhead) {
+#pragma unroll
+            for (int j = 0; j < kWinAhead; ++j) {
+                if (blk + 32 * j >= e) break;
+                const WinBlock cb = q[j];
+                q[j] = win_load(wcol, flags, bbase, blk + 32 * (j + kWinAhead), e, lane);
+                const unsigned idw[4] = {cb.ids.x, cb.ids.y, cb.ids.z, cb.ids.w};
+                double v[8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    v[2 * i] = (double)win[idw[i] & 0xffffu];
+                    v[2 * i + 1] = (double)win[idw[i] >> 16];
+                }
+                int k = cb.kb + (int)(cb.m >> 8) - 1;  // index of the piece the current run belongs to (once started)
+                double head = 0.0, run = 0.0;
+                bool started = false;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if ((cb.m >> i) & 1u) {
+                        if (started) wpart[k] = run;
+                        else head = run;
+                        started = true;
+                        run = 0.0;
+                        ++k;
+                    }
+                    run += v[i];
+                }
+                if (!started) head = run;
+                // G = this lane's leading sum + those of the following lanes up to (and
+                // including) the first lane that starts a piece
+                double G = head;
+                const unsigned ahead = __ballot_sync(0xffffffffu, started) >> lane;  // bit j: lane + j starts a piece
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double nv = __shfl_down_sync(0xffffffffu, G, o);
+                    if (lane + o < 32 && !(ahead & ((1u << o) - 1u))) G += nv;
+                }
+                double Gn = __shfl_down_sync(0xffffffffu, G, 1);
+                if (lane == 31) Gn = 0.0;
+                if (started) wpart[k] = run + Gn;
+            }
+        }
+        b = e;
+    }
 }
 
 // ---------------- BITEXACT: thread per row, storage order ----------------------------
@@ -1319,6 +1454,7 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         ab.xdiscard_len = (EPI == EPI_CPAA && tuning().xdiscard && !a.push && g->part.G == 1 && !g->part.comm)
                               ? (g->view.x_len * (int64_t)sizeof(V) / 128) * 128 / (int64_t)sizeof(V) : 0;
         const size_t x_bytes = (size_t)std::max<int64_t>(g->view.x_len, 1) * sizeof(V);
+        const bool windows_on = g->view.win.ready && g->part.G == 1 && !a.push;
         auto launch = [&](const TermArgs<RP, V>& args, const WTile* prog, int plen, int ntiles, const V* win,
                           size_t win_bytes) {
             cudaLaunchConfig_t cfg = {};
@@ -1333,7 +1469,7 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             // resident in L2 across the launch (only when x exceeds L2)
             if (tuning().l2win && l2_window(win, win_bytes, &attr[cfg.numAttrs].val.accessPolicyWindow, x_bytes))
                 attr[cfg.numAttrs++].id = cudaLaunchAttributeAccessPolicyWindow;
-            if (tuning().pdl) {  // overlap this launch + prologue with the previous kernel's tail
+            if (tuning().pdl && !(windows_on && (tuning().winskip & 8))) {  // overlap this launch + prologue with the previous kernel's tail
                 attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
                 attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
             }
@@ -1346,7 +1482,43 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             }
         };
         int launched = 0;
-        if (g->view.phases.empty()) {
+        const SolverView::Windows& Wn = g->view.win;
+        const bool windows = windows_on;
+        if (windows) {
+            // the hub rows' window pieces first (their sums land in hub_part), then the term
+            // kernel over the remaining entries, then the finalize
+            static std::atomic<uint64_t> wattr_set{0};
+            constexpr int kWinSmemMax = 226 * 1024;  // + the static mbarrier
+            const size_t wsmem = (size_t)Wn.W * sizeof(V);
+            if (wsmem > (size_t)kWinSmemMax) fail(CHEB_INVALID_ARG, "column window larger than shared memory");
+            if (first_on_device(wattr_set, g->device)) {
+                const cudaError_t e = cudaFuncSetAttribute((const void*)k_window_pass<V>,
+                                                           cudaFuncAttributeMaxDynamicSharedMemorySize, kWinSmemMax);
+                if (e != cudaSuccess) {
+                    wattr_set.fetch_and(~(uint64_t(1) << (g->device & 63)));
+                    CHEB_CUDA_CHECK(e);
+                }
+            }
+            cudaLaunchConfig_t wc = {};
+            wc.gridDim = dim3((unsigned)Wn.grid);
+            wc.blockDim = dim3(1024);
+            wc.dynamicSmemBytes = wsmem;
+            wc.stream = st;
+            cudaLaunchAttribute wattr[1];
+            wattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            wattr[0].val.programmaticStreamSerializationAllowed = 1;
+            wc.attrs = wattr;
+            wc.numAttrs = (tuning().pdl && !(tuning().winskip & 4)) ? 1 : 0;
+            if (tuning().winskip != 1)
+            CHEB_CUDA_CHECK(cudaLaunchKernelEx(&wc, k_window_pass<V>, a.x_in, g->view.x_len, Wn.H0, Wn.W, Wn.NW,
+                                               (const int64_t*)Wn.wblk.ptr<int64_t>(), (const uint4*)Wn.wcol.ptr<uint4>(),
+                                               (const unsigned short*)Wn.meta.ptr<unsigned short>(),
+                                               (const int*)Wn.bbase.ptr<int>(), a.hub_part + Wn.MC,
+                                               (const int64_t*)Wn.cta.ptr<int64_t>(), ab.stamp_start));
+            ab.stamp_start = nullptr;
+            if (tuning().winskip != 2) launch(ab, Wn.prog.ptr<WTile>(), Wn.prog_len, Wn.n_tiles, a.x_in, x_bytes);
+            launched = 2;
+        } else if (g->view.phases.empty()) {
             launch(ab, g->view.prog.ptr<WTile>(), g->view.prog_len, g->view.n_tiles, a.x_in, x_bytes);
             launched = 1;
         } else {
@@ -1368,9 +1540,9 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
                 ++launched;
             }
         }
-        if (g->view.n_hub > 0) {
+        if (g->view.n_hub > 0 && tuning().winskip != 3) {
             CHEB_CUDA_CHECK(cudaGetLastError());
-            const int64_t n_wide = tuning().hubwarp ? g->view.n_hub : g->view.n_hub_wide;
+            const int64_t n_wide = tuning().hubwarp ? g->view.n_hub : windows ? Wn.n_wide : g->view.n_hub_wide;
             const int64_t hub_warps = n_wide + (g->view.n_hub - n_wide + 31) / 32;
             const int hb = (int)std::max<int64_t>(1, std::min<int64_t>((hub_warps * 32 + 255) / 256, 148 * 16));
             cudaLaunchConfig_t hc = {};
@@ -1381,9 +1553,13 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             hattr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
             hattr[0].val.programmaticStreamSerializationAllowed = 1;
             hc.attrs = hattr;
-            hc.numAttrs = tuning().pdl ? 1 : 0;
+            hc.numAttrs = (tuning().pdl && !(windows_on && (tuning().winskip & 16))) ? 1 : 0;
             CHEB_CUDA_CHECK(cudaLaunchKernelEx(&hc, k_hub_finalize<EPI, RP, V>, a,
-                                               (const int*)g->view.hub_first.ptr<int>(), g->view.n_hub, n_wide));
+                                               windows ? (const int*)Wn.hub_first.ptr<int>()
+                                                       : (const int*)g->view.hub_first.ptr<int>(),
+                                               g->view.n_hub, n_wide, windows ? (const int*)Wn.kf.ptr<int>() : (const int*)nullptr,
+                                               windows ? (const int*)Wn.klist.ptr<int>() : (const int*)nullptr,
+                                               (const double*)(a.hub_part + (windows ? Wn.MC : 0))));
             return launched + 1;
         }
         CHEB_CUDA_CHECK(cudaGetLastError());
@@ -1417,7 +1593,8 @@ void ensure_workspace(cheb_graph* g, int M, int R) {
     w.out.ensure(vb);
     const int grid = std::max(g->view.ready ? g->view.grid : 1, grid1d(n));
     w.part.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max(grid, 1));
-    w.hub_part.ensure(sizeof(double) * std::max(g->view.n_tiles, 1));
+    w.hub_part.ensure(sizeof(double) * (size_t)std::max<int64_t>(
+                          std::max<int64_t>(g->view.n_tiles, g->view.win.ready ? g->view.win.n_slots : 0), 1));
     w.hub_ts.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1) * std::max<int64_t>(g->view.n_hub, 1));
     w.trace.ensure(sizeof(double) * 2 * (size_t)std::max(M, 1));
     w.total.ensure(sizeof(double) * 4);
