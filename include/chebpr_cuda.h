@@ -193,6 +193,16 @@ cheb_status cheb_graph_exchange_info(cheb_graph_t g, int64_t* halo_stores, int64
  * (first entry of every hub-row chunk tile).  Any output may be NULL. */
 cheb_status cheb_graph_view_download(cheb_graph_t g, int64_t* sizes, int64_t* row_ptr, int32_t* col,
                                      int32_t* order, int64_t* chunk_begin);
+/* Column windows of the hub rows (new; tests and tools): sizes[8] = {windows NW (0: none), entries of
+ * x per window W, first windowed id H0, stream blocks (256 entries each), windowed entries, pieces
+ * (sums the window pass stores, padding included), chunk tiles left to the term kernel over the hub
+ * rows, listed pieces}.  wcol[blocks * 256]: window-local ids, window-major; lane_meta[blocks * 32]:
+ * per lane of a block (8 consecutive entries) its piece-start bits | pieces started in the block's
+ * earlier lanes << 8; block_base[blocks + 1]: pieces before each block; row_first[n_hub + 1] and
+ * piece_list[listed]: the pieces (stream indices) of every hub row.  Window w holds the ids
+ * [H0 + w W, H0 + (w + 1) W) and starts at a block boundary.  Any output may be NULL. */
+cheb_status cheb_graph_view_windows(cheb_graph_t g, int64_t* sizes, uint16_t* wcol, uint16_t* lane_meta,
+                                    int32_t* block_base, int32_t* row_first, int32_t* piece_list);
 /* Warp tiles of the solver view (new; tests and tools): *n_tiles, then per tile its first
  * entry, first row (a chunk tile: its hub row) and meta (log2 lanes per row, or 0x10 = chunk
  * of a hub row) for tiles [0, n_tiles] (tile n_tiles: the sentinel {nnz_local, n_local, 0});

@@ -122,6 +122,8 @@ _SIGS = {
     "cheb_graph_exchange_info": (C.c_int, [C.c_void_p, I64P, I64P]),
     "cheb_partition_block_rows": (C.c_int, []),
     "cheb_graph_view_download": (C.c_int, [C.c_void_p, I64P, I64P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), I64P]),
+    "cheb_graph_view_windows": (C.c_int, [C.c_void_p, I64P, C.POINTER(C.c_uint16), C.POINTER(C.c_uint16),
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "cheb_graph_view_tiles": (C.c_int, [C.c_void_p, I64P, I64P, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                         C.POINTER(C.c_int32)]),
     "cheb_cpaa_batch": (C.c_int, [C.c_void_p, C.POINTER(cheb_cpaa_opts), I64P, F64P, F64P,

@@ -1511,31 +1511,50 @@ __global__ void k_win_gather_starts(const int64_t* __restrict__ off, int64_t n_h
     if (w <= NW) out[w] = off[(int64_t)w * n_hub];
 }
 
-// Window-local 16-bit ids into the stream, and each piece's start bit.  A warp per hub row.
+// Window-local 16-bit ids into the stream, and each piece's start bit: hub row h by `nt`
+// cooperating threads.
 template <class RPN>
+__device__ __forceinline__ void win_copy_row(const RPN* __restrict__ rp, const int* __restrict__ col, int64_t n_hub,
+                                             const int* __restrict__ S, const int64_t* __restrict__ off,
+                                             const int64_t* __restrict__ delta, int H0, int W, int NW,
+                                             unsigned short* __restrict__ wcol, unsigned* __restrict__ flags32,
+                                             int64_t h, int t, int nt) {
+    const int64_t base = rp[h];
+    const int* Sh = S + h * (NW + 1);
+    const int e0 = Sh[0], e1 = Sh[NW];
+    for (int e = e0 + t; e < e1; e += nt) {
+        const int id = col[base + e] - H0;
+        const int w = id / W;
+        const int64_t pos = off[(int64_t)w * n_hub + h] + delta[w] + (e - Sh[w]);
+        wcol[pos] = (unsigned short)(id - w * W);
+    }
+    for (int w = t; w < NW; w += nt) {
+        if (Sh[w + 1] > Sh[w]) {
+            const int64_t pos = off[(int64_t)w * n_hub + h] + delta[w];
+            atomicOr(&flags32[pos >> 5], 1u << (pos & 31));
+        }
+    }
+}
+constexpr int kWinBigRow = 4096;  // windowed entries above which a CTA copies the row (rows [0, kWinBigRows) only)
+constexpr int kWinBigRows = 8192;
+// A warp per hub row (rows a CTA takes are skipped) / a CTA per leading hub row.
+template <class RPN, bool BIG>
 __global__ void k_win_copy(const RPN* __restrict__ rp, const int* __restrict__ col, int64_t n_hub,
                            const int* __restrict__ S, const int64_t* __restrict__ off,
                            const int64_t* __restrict__ delta, int H0, int W, int NW,
                            unsigned short* __restrict__ wcol, unsigned* __restrict__ flags32) {
+    if (BIG) {
+        const int64_t h = blockIdx.x;
+        if (S[h * (NW + 1) + NW] - S[h * (NW + 1)] > kWinBigRow)
+            win_copy_row(rp, col, n_hub, S, off, delta, H0, W, NW, wcol, flags32, h, (int)threadIdx.x, (int)blockDim.x);
+        return;
+    }
     const int lane = threadIdx.x & 31;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t h = gw; h < n_hub; h += nw) {
-        const int64_t base = rp[h];
-        const int* Sh = S + h * (NW + 1);
-        const int e0 = Sh[0], e1 = Sh[NW];
-        for (int e = e0 + lane; e < e1; e += 32) {
-            const int id = col[base + e] - H0;
-            const int w = id / W;
-            const int64_t pos = off[(int64_t)w * n_hub + h] + delta[w] + (e - Sh[w]);
-            wcol[pos] = (unsigned short)(id - w * W);
-        }
-        for (int w = lane; w < NW; w += 32) {
-            if (Sh[w + 1] > Sh[w]) {
-                const int64_t pos = off[(int64_t)w * n_hub + h] + delta[w];
-                atomicOr(&flags32[pos >> 5], 1u << (pos & 31));
-            }
-        }
+        if (h < kWinBigRows && S[h * (NW + 1) + NW] - S[h * (NW + 1)] > kWinBigRow) continue;
+        win_copy_row(rp, col, n_hub, S, off, delta, H0, W, NW, wcol, flags32, h, lane, 32);
     }
 }
 
@@ -1566,31 +1585,66 @@ __global__ void k_win_padflags(const int64_t* __restrict__ wend, int NW, unsigne
 // gather instructions of a block: position p is read by lane p / 8 in instruction p % 8.
 // Greedy, a thread per block: each position takes, among the next entries of its piece, one
 // whose bank pair the instruction's half-warp has not used yet.
-__global__ void k_win_bank_order(unsigned short* __restrict__ wcol, const unsigned* __restrict__ flags32,
-                                 int64_t n_blocks) {
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n_blocks; b += (int64_t)gridDim.x * blockDim.x) {
-        unsigned short* ids = wcol + b * kWinBlock;
-        const unsigned* fw = flags32 + b * (kWinBlock / 32);
-        unsigned used[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [instruction]: low half-warp bits 0-15, high half-warp 16-31
-        int pe = 0;
-        for (int p = 0; p < kWinBlock; ++p) {
-            if (p >= pe) {  // next piece start after p
-                pe = p + 1;
-                while (pe < kWinBlock && !((fw[pe >> 5] >> (pe & 31)) & 1u)) ++pe;
+constexpr int kBankThreads = 64, kBankStride = kWinBlock + 2;  // shorts per thread row (129 words: conflict-free)
+__global__ void __launch_bounds__(kBankThreads)
+k_win_bank_order(unsigned short* __restrict__ wcol, const unsigned* __restrict__ flags32, int64_t n_blocks) {
+    __shared__ unsigned short sh[kBankThreads * kBankStride];
+    for (int64_t b0 = (int64_t)blockIdx.x * kBankThreads; b0 < n_blocks; b0 += (int64_t)gridDim.x * kBankThreads) {
+        const int nb = (int)min((int64_t)kBankThreads, n_blocks - b0);
+        __syncthreads();
+        {  // the CTA's blocks into shared memory, 4 bytes per thread per step
+            const unsigned* src = reinterpret_cast<const unsigned*>(wcol + b0 * kWinBlock);
+            for (int i = threadIdx.x; i < nb * (kWinBlock / 2); i += kBankThreads) {
+                const int r = i / (kWinBlock / 2), c = i % (kWinBlock / 2);
+                *reinterpret_cast<unsigned*>(&sh[r * kBankStride + 2 * c]) = src[i];
             }
-            const int sh = (p >> 7) << 4;
-            const unsigned mask = used[p & 7] >> sh;
-            const int lim = min(pe, p + 24);
-            int pick = p;
-            for (int j = p; j < lim; ++j)
-                if (!((mask >> (ids[j] & 15)) & 1u)) {
-                    pick = j;
-                    break;
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < nb) {
+            unsigned short* ids = sh + threadIdx.x * kBankStride;
+            unsigned fw[kWinBlock / 32];
+#pragma unroll
+            for (int j = 0; j < kWinBlock / 32; ++j) fw[j] = flags32[(b0 + threadIdx.x) * (kWinBlock / 32) + j];
+            unsigned used[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [instruction]: low half-warp bits 0-15, high half-warp 16-31
+            int pe = 0;
+#pragma unroll
+            for (int wq = 0; wq < kWinBlock / 32; ++wq) {
+                const unsigned fword = fw[wq];
+                const unsigned fnext = wq + 1 < kWinBlock / 32 ? fw[wq + 1] : 1u;  // the next block starts a piece
+                for (int p4 = 0; p4 < 4; ++p4) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int p = wq * 32 + p4 * 8 + i;
+                        if (p >= pe) {  // end of the piece holding p: next start bit, at most 24 positions on
+                            const int q = p4 * 8 + i + 1;  // in-word bit of p + 1
+                            const unsigned long long bits = ((unsigned long long)fnext << 32 | fword) >> q;
+                            const int d = bits ? __ffsll((long long)bits) - 1 : 64;
+                            pe = min(p + 1 + d, p + 24);
+                            if (wq + 1 == kWinBlock / 32) pe = min(pe, kWinBlock);
+                        }
+                        const int shf = (p >> 7) << 4;
+                        const unsigned mask = used[i] >> shf;
+                        int pick = p;
+                        for (int j = p; j < pe; ++j)
+                            if (!((mask >> (ids[j] & 15)) & 1u)) {
+                                pick = j;
+                                break;
+                            }
+                        const unsigned short v = ids[pick];
+                        ids[pick] = ids[p];
+                        ids[p] = v;
+                        used[i] |= 1u << (shf + (v & 15));
+                    }
                 }
-            const unsigned short v = ids[pick];
-            ids[pick] = ids[p];
-            ids[p] = v;
-            used[p & 7] |= 1u << (sh + (v & 15));
+            }
+        }
+        __syncthreads();
+        {
+            unsigned* dst = reinterpret_cast<unsigned*>(wcol + b0 * kWinBlock);
+            for (int i = threadIdx.x; i < nb * (kWinBlock / 2); i += kBankThreads) {
+                const int r = i / (kWinBlock / 2), c = i % (kWinBlock / 2);
+                dst[i] = *reinterpret_cast<const unsigned*>(&sh[r * kBankStride + 2 * c]);
+            }
         }
     }
 }
@@ -1803,12 +1857,27 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
     CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.wcol.get(), 0, sizeof(unsigned short) * (size_t)stream_len + 64, st));
     CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.flags.get(), 0, (size_t)stream_len / 8 + 64, st));
     unsigned* flags32 = Wn.flags.ptr<unsigned>();
-    k_win_copy<RPN><<<(int)std::min<int64_t>((n_hub * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
+    if (dbg_on()) {
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        dbg_mark("    windows: splits + layout");
+    }
+    k_win_copy<RPN, true><<<(int)std::min<int64_t>(n_hub, kWinBigRows), 512, 0, st>>>(
+        rp, col, n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, H0, W, NW, Wn.wcol.ptr<unsigned short>(), flags32);
+    k_win_copy<RPN, false><<<(int)std::min<int64_t>((n_hub * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
         rp, col, n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, H0, W, NW, Wn.wcol.ptr<unsigned short>(), flags32);
     k_win_padflags<<<(NW + 127) / 128, 128, 0, st>>>(d_wend, NW, flags32);
     CHEB_CUDA_CHECK(cudaGetLastError());
+    if (dbg_on()) {
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        dbg_mark("    windows: stream copied");
+    }
     if (tuning().winbank)
-        k_win_bank_order<<<grid_for(n_blocks, 128), 128, 0, st>>>(Wn.wcol.ptr<unsigned short>(), flags32, n_blocks);
+        k_win_bank_order<<<(int)std::min<int64_t>((n_blocks + kBankThreads - 1) / kBankThreads, 148 * 32), kBankThreads, 0, st>>>(
+            Wn.wcol.ptr<unsigned short>(), flags32, n_blocks);
+    if (dbg_on()) {
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        dbg_mark("    windows: bank order");
+    }
     Wn.meta.alloc(sizeof(unsigned short) * (size_t)n_blocks * 32 + 64);
     k_win_lanemeta<<<(int)std::min<int64_t>((n_blocks * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
         Wn.flags.ptr<unsigned char>(), n_blocks, Wn.meta.ptr<unsigned short>());
@@ -2061,8 +2130,12 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     }
     const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2) : tuning().sortrows > 0;
     // column windows (single-GPU views) need the hub rows in ascending id order
-    const bool want_windows = tuning().windows > 0 && P.G == 1 && V.n_hub > 0 && tuning().chunksched <= 1 &&
-                              V.x_len > kHotBytes / 8;
+    // (auto: graphs of >= 48 M entries, where the extra launch per term is paid back: config 2,
+    // 19 M entries, runs 65 -> 74 us/term with windows, config 3 362 -> 297, config 4 3447 -> 2554)
+    int n_windows = tuning().windows;
+    if (n_windows < 0) n_windows = nnz_l >= (int64_t(48) << 20) ? (big_x ? 64 : 24) : 0;
+    const bool want_windows = n_windows > 0 && P.G == 1 && V.n_hub > 0 && tuning().chunksched <= 1 &&
+                              V.x_len > kHotBytes / 8 && nnz_l < INT32_MAX;
     const bool hubs_only = (tuning().sortrows == 2 || (want_windows && !big_x)) && V.n_hub > 0;
     const bool sort_rows = (big_x || hubs_only) && nnz_l > 0 && nnz_l < INT32_MAX;
     const bool sort_grouped = sort_rows && !hubs_only;  // every row, group by group into V.col
@@ -2162,7 +2235,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         }
         V.win.release();
         if (want_windows && sort_rows) {
-            window_schedule<RPN>(V, tuning().windows, tuning().winsize, st);
+            window_schedule<RPN>(V, n_windows, tuning().winsize, st);
             dbg_mark("  view: column windows");
         }
         if (sort_grouped && tuning().chunksched > 1 && V.n_chunk_tiles > 0) {  // the sort undid the chunk order

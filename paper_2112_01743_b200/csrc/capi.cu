@@ -1082,6 +1082,50 @@ cheb_status cheb_graph_view_download(cheb_graph_t g, int64_t* sizes, int64_t* ro
     });
 }
 
+cheb_status cheb_graph_view_windows(cheb_graph_t g, int64_t* sizes, uint16_t* wcol, uint16_t* lane_meta,
+                                    int32_t* block_base, int32_t* row_first, int32_t* piece_list) {
+    return guarded([&] {
+        NvtxRange nvtx_("cheb_graph_view_windows");
+        need_graph(g);
+        GraphScope gs(g);
+        ensure_view(g);
+        const SolverView& V = g->view;
+        const SolverView::Windows& W = V.win;
+        cudaStream_t st = g->stream;
+        int listed = 0;
+        if (W.ready)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(&listed, W.kf.ptr<int>() + V.n_hub, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+        if (sizes) {
+            sizes[0] = W.ready ? W.NW : 0;
+            sizes[1] = W.W;
+            sizes[2] = W.H0;
+            sizes[3] = W.n_blocks;
+            sizes[4] = W.entries;
+            sizes[5] = W.pieces;
+            sizes[6] = W.MC;
+            sizes[7] = listed;
+        }
+        if (!W.ready) return;
+        if (wcol)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(wcol, W.wcol.get(), sizeof(uint16_t) * (size_t)W.n_blocks * kWinBlock,
+                                            cudaMemcpyDeviceToHost, st));
+        if (lane_meta)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(lane_meta, W.meta.get(), sizeof(uint16_t) * (size_t)W.n_blocks * 32,
+                                            cudaMemcpyDeviceToHost, st));
+        if (block_base)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(block_base, W.bbase.get(), sizeof(int32_t) * (size_t)(W.n_blocks + 1),
+                                            cudaMemcpyDeviceToHost, st));
+        if (row_first)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(row_first, W.kf.get(), sizeof(int32_t) * (size_t)(V.n_hub + 1),
+                                            cudaMemcpyDeviceToHost, st));
+        if (piece_list && listed > 0)
+            CHEB_CUDA_CHECK(cudaMemcpyAsync(piece_list, W.klist.get(), sizeof(int32_t) * (size_t)listed,
+                                            cudaMemcpyDeviceToHost, st));
+        CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
+    });
+}
+
 cheb_status cheb_graph_view_tiles(cheb_graph_t g, int64_t* n_tiles, int64_t* nnz_begin, int32_t* row_begin,
                                   int32_t* meta, int32_t* n_launches) {
     return guarded([&] {

@@ -486,7 +486,8 @@ struct Tuning {
     int hubwarp = 0;    // 1: every hub row finalized by a warp (the lane-per-row path off; tests)
     int pull = 1;       // view tiles / programs pulled from pinned host memory by a kernel (not the copy engine)
     int colsplit_pct = -1; // K = 2: first block boundary at this percent of x (-1: equal halves)
-    int windows = 0;    // NW > 0: column windows of the hub rows (SolverView::Windows), single-GPU views
+    int windows = -1;   // column windows of the hub rows (SolverView::Windows), single-GPU views: NW > 0 windows,
+                        // 0 off, -1 auto (64 when x exceeds L2, else 24, on graphs of >= 48 M entries)
     int winbank = 1;    // window stream entries ordered inside their pieces for conflict-free shared-memory gathers
     int winpw = 4;      // window pass CTA ranges: cost of a block = 256 + winpw * its pieces
     int winskip = 0;    // timing experiments (wrong results): 1 no window pass, 2 no term kernel, 3 no hub finalize

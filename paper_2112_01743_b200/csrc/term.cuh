@@ -1469,7 +1469,10 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             // resident in L2 across the launch (only when x exceeds L2)
             if (tuning().l2win && l2_window(win, win_bytes, &attr[cfg.numAttrs].val.accessPolicyWindow, x_bytes))
                 attr[cfg.numAttrs++].id = cudaLaunchAttributeAccessPolicyWindow;
-            if (tuning().pdl && !(windows_on && (tuning().winskip & 8))) {  // overlap this launch + prologue with the previous kernel's tail
+            // (not after a window pass: a term CTA that takes over an SM the moment a window CTA
+            // leaves it keeps that kernel's shared-memory carve-out, i.e. a ~28 KB L1, and the
+            // cold gathers lose their in-flight capacity: config 4 3083 -> 3728 us/term)
+            if (tuning().pdl && !(windows_on && !(tuning().winskip & 8))) {  // overlap this launch + prologue with the previous kernel's tail
                 attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
                 attr[cfg.numAttrs++].val.programmaticStreamSerializationAllowed = 1;
             }

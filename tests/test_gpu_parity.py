@@ -782,3 +782,132 @@ def test_single_column_buffer_kernel_deterministic_at_scale(cheb):
         dg.free()
     for r in runs[1]:
         assert np.array_equal(r, runs[2][0])
+
+
+# ---------------- column windows of the hub rows (SolverView::Windows) ----------------
+
+def _window_plan(lib, dg):
+    import ctypes as C
+    P64, P32, P16 = C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_uint16)
+    sizes = np.zeros(8, dtype=np.int64)
+    assert lib.cheb_graph_view_windows(dg.handle, sizes.ctypes.data_as(P64), None, None, None, None, None) == 0
+    NW, W, H0, nb, entries, pieces, MC, listed = (int(v) for v in sizes)
+    v = _view(lib, dg)
+    wcol = np.zeros(nb * 256, dtype=np.uint16)
+    meta = np.zeros(nb * 32, dtype=np.uint16)
+    bbase = np.zeros(nb + 1, dtype=np.int32)
+    kf = np.zeros(v["n_hub"] + 1, dtype=np.int32)
+    klist = np.zeros(max(listed, 1), dtype=np.int32)
+    if NW:
+        assert lib.cheb_graph_view_windows(dg.handle, sizes.ctypes.data_as(P64), wcol.ctypes.data_as(P16),
+                                           meta.ctypes.data_as(P16), bbase.ctypes.data_as(P32),
+                                           kf.ctypes.data_as(P32), klist.ctypes.data_as(P32)) == 0
+    return dict(NW=NW, W=W, H0=H0, blocks=nb, entries=entries, pieces=pieces, MC=MC, listed=listed, wcol=wcol,
+                meta=meta, bbase=bbase, kf=kf, klist=klist[:listed], view=v)
+
+
+def _forced_windows(lib, nw, size):
+    assert lib.cheb_set_tuning(b"windows", nw) == 0
+    assert lib.cheb_set_tuning(b"winsize", size) == 0
+
+
+def _default_windows(lib):
+    lib.cheb_set_tuning(b"windows", -1)
+    lib.cheb_set_tuning(b"winsize", 24576)
+
+
+@pytest.mark.parametrize("graph", ["chung_lu", "rmat"])
+def test_column_windows_hold_every_windowed_entry_once(cheb, graph):
+    """The window stream of a view (forced: 6 windows of 2048 ids on a small graph) holds, piece by
+    piece, exactly the hub rows' entries with ids in [H0, H0 + NW W): every hub row's listed pieces
+    give back the multiset of its windowed ids, pieces never cross a 256-entry block, the per-lane
+    piece counts and block bases agree with the start bits, and the padding belongs to no row."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    e = (Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 20000.0, 900_000, 5) if graph == "chung_lu"
+         else Gen.rmat_edges(16, 16, 0.57, 0.19, 0.19, 3))
+    try:
+        _forced_windows(lib, 6, 2048)
+        dg, info = cheb.build_device_graph(e, cheb.BuildOptions(drop_isolated=True))
+        p = _window_plan(lib, dg)
+        dg.free()
+    finally:
+        _default_windows(lib)
+    v = p["view"]
+    NW, W, H0, n_hub = p["NW"], p["W"], p["H0"], v["n_hub"]
+    assert NW == 6 and W == 2048 and n_hub > 0
+    rp, col = v["rp"], v["col"]
+    hub_end = int(rp[n_hub])
+    row_of = np.repeat(np.arange(n_hub), np.diff(rp[:n_hub + 1]))
+    c = col[:hub_end].astype(np.int64)
+    inw = (c >= H0) & (c < H0 + NW * W)
+    assert p["entries"] == int(inw.sum()) > 0
+    want = np.sort(row_of[inw] * (1 << 32) + c[inw])
+    # stream: start bits -> piece of every position; windows start at block boundaries
+    m = p["meta"]
+    bits = ((m[:, None] & 0xff) >> np.arange(8)[None, :]) & 1
+    starts = bits.reshape(-1).astype(np.int64)
+    assert np.all(starts[::256] == 1)                       # a block's first entry starts a piece
+    piece_of = np.cumsum(starts) - 1
+    assert p["pieces"] == int(starts.sum()) == int(p["bbase"][-1])
+    assert np.array_equal(p["bbase"][:-1], piece_of[::256])
+    before = (m >> 8).astype(np.int64)                      # pieces started in the block's earlier lanes
+    lane_first = np.cumsum(starts.reshape(-1, 8).sum(1).reshape(-1, 32), axis=1)
+    assert np.array_equal(before.reshape(-1, 32)[:, 1:], lane_first[:, :-1]) and np.all(before.reshape(-1, 32)[:, 0] == 0)
+    wlen = np.bincount(((c[inw] - H0) // W).astype(np.int64), minlength=NW)
+    wblocks = (wlen + 255) // 256
+    assert p["blocks"] == int(wblocks.sum())
+    win_of_block = np.repeat(np.arange(NW), wblocks)
+    ids = H0 + np.repeat(win_of_block, 256) * W + p["wcol"].astype(np.int64)
+    piece_row = np.full(p["pieces"], -1, dtype=np.int64)
+    piece_row[p["klist"]] = np.repeat(np.arange(n_hub), np.diff(p["kf"]))
+    assert np.unique(p["klist"]).size == p["listed"]          # a piece belongs to one row
+    r = piece_row[piece_of]
+    got = np.sort(r[r >= 0] * (1 << 32) + ids[r >= 0])
+    assert np.array_equal(got, want)
+    assert int((r < 0).sum()) == int(p["blocks"] * 256 - p["entries"])  # the padding only
+
+
+@pytest.mark.parametrize("graph", ["chung_lu", "rmat"])
+def test_column_windows_against_reference(cheb, oracle, graph):
+    """Solves with the hub rows' column windows (forced on a small graph) against the oracle and
+    against the plain schedule: FAST fp64 <= 1e-12 with the same top-100, fp32 <= 1e-6 relative
+    L1, Power and transition_apply <= 1e-12, repeated solves bitwise equal, int64 row pointers."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    e = (Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 20000.0, 900_000, 5) if graph == "chung_lu"
+         else Gen.rmat_edges(16, 16, 0.57, 0.19, 0.19, 3)).astype(np.int64)
+    ref = oracle.build_graph(e, drop_isolated=True)
+    want = oracle.run_cpaa(ref, 39).ranks
+    x = np.random.default_rng(7).random(ref.n)
+    res = {}
+    try:
+        for nw, rp64 in ((0, False), (6, False), (6, True)):
+            _forced_windows(lib, nw, 2048)
+            dg, info = cheb.build_device_graph(e, cheb.BuildOptions(drop_isolated=True, row_ptr_64=rp64))
+            p = _window_plan(lib, dg)
+            assert p["NW"] == nw
+            a = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+            b = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39))
+            assert np.array_equal(a.ranks, b.ranks)
+            f32 = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39, precision=32))
+            pw = cheb.run_power(dg, cheb.PowerConfig(rounds=60))
+            y = cheb.transition_apply(dg, x)
+            exact = cheb.run_cpaa(dg, cheb.SolverConfig(rounds=39, mode=cheb.MODE_BITEXACT))
+            res[(nw, rp64)] = (a.ranks, f32.ranks, pw.ranks, y)
+            assert np.array_equal(exact.ranks, want)
+            dg.free()
+    finally:
+        _default_windows(lib)
+    plain = res[(0, False)]
+    for key in ((6, False), (6, True)):
+        fast, f32, pw, y = res[key]
+        assert np.max(np.abs(fast - want)) <= TOL64
+        assert np.array_equal(top_k(fast), top_k(want))
+        assert np.sum(np.abs(f32 - want)) / np.sum(want) <= TOL32_L1
+        assert np.max(np.abs(fast - plain[0])) <= TOL64
+        assert np.max(np.abs(pw - plain[2])) <= TOL64
+        assert np.max(np.abs(y - plain[3])) <= 1e-12
+    assert np.array_equal(res[(6, False)][0], res[(6, True)][0])   # same schedule, wider row pointers
