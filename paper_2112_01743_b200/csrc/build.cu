@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <cstring>
@@ -1795,44 +1796,82 @@ __global__ void k_win_prog_pack(const Tile* __restrict__ tiles, int old_chunks, 
     }
 }
 
-template <class T>
-static void exclusive_scan(const T* in, T* out, int64_t cnt, TempStore& tmp, cudaStream_t st) {
-    size_t bytes = 0;
-    CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, cnt, st));
-    void* t = tmp.get(bytes);
-    CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(t, bytes, in, out, cnt, st));
+// Scratch of the window build: one grow-only cudaMalloc'ed block per device, reused by every
+// upload (callers hold pinned_arena().mu), so the temporaries never touch the memory pool.
+static char* window_scratch(size_t bytes) {
+    static std::map<int, DevMem> cache;
+    int dev = 0;
+    CHEB_CUDA_CHECK(cudaGetDevice(&dev));
+    DevMem& d = cache[dev];
+    if (d.bytes() < bytes) {
+        AllocScope plain(nullptr);
+        d.alloc(bytes + bytes / 8);
+    }
+    return d.ptr<char>();
 }
+struct Carver {
+    char* base;
+    size_t off = 0;
+    template <class T>
+    T* take(size_t count) {
+        T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+        off += (count * sizeof(T) + 255) & ~size_t(255);
+        return p;
+    }
+};
 
 // Builds SolverView::Windows on the device (hub rows ascending).  NW windows of W entries
-// from id H0 = the fp64 hot-prefix capacity.
+// from id H0 (0, or the fp64 hot-prefix capacity: tuning().winh0).
 template <class RPN>
 static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
     SolverView::Windows& Wn = V.win;
     Wn.release();
     const int64_t n_hub = V.n_hub;
-    const int H0 = kHotBytes / 8;
+    const int H0 = tuning().winh0 >= 0 ? (tuning().winh0 & ~7) : kHotBytes / 8;
     W = std::max(256, std::min(W, 65536)) & ~7;
     if (n_hub <= 0 || V.x_len <= H0) return;
     const int NW = (int)std::min<int64_t>(NW_req, (V.x_len - H0 + W - 1) / W);
     if (NW <= 0 || n_hub * (int64_t)(NW + 1) >= (int64_t)INT32_MAX * 4) return;
-    TempStore tmp;
     const RPN* rp = V.row_ptr.ptr<RPN>();
     const int* col = V.col.ptr<int>();
-    DevMem S(sizeof(int) * (size_t)n_hub * (NW + 1));
-    k_win_splits<RPN><<<grid_for(n_hub * (NW + 1)), kBuildThreads, 0, st>>>(rp, col, n_hub, H0, W, NW, S.ptr<int>());
-    CHEB_CUDA_CHECK(cudaGetLastError());
     const int64_t nq = n_hub * NW;
-    DevMem csz(sizeof(int64_t) * (size_t)(nq + 1)), off(sizeof(int64_t) * (size_t)(nq + 1));
-    k_win_sizes<<<grid_for(nq + 1), kBuildThreads, 0, st>>>(S.ptr<int>(), n_hub, NW, csz.ptr<int64_t>());
+    const int64_t max_blocks = V.nnz_local / kWinBlock + NW + 1;
+    constexpr size_t kCubTemp = size_t(64) << 20;
+    // scratch layout (sizes first, then the block)
+    Carver sc{nullptr};
+    int* S = nullptr;
+    int64_t *csz = nullptr, *off = nullptr, *d_small = nullptr;
+    int *pc = nullptr, *mc = nullptr, *rowpieces = nullptr, *subx = nullptr;
+    unsigned long long* wide = nullptr;
+    char* cub_tmp = nullptr;
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) sc = Carver{window_scratch(sc.off)};
+        S = sc.take<int>((size_t)n_hub * (NW + 1));
+        csz = sc.take<int64_t>((size_t)nq + 1);
+        off = sc.take<int64_t>((size_t)nq + 1);
+        d_small = sc.take<int64_t>((size_t)4 * (NW + 1));
+        pc = sc.take<int>((size_t)max_blocks + 1);
+        mc = sc.take<int>((size_t)n_hub + 1);
+        rowpieces = sc.take<int>((size_t)n_hub + 1);
+        subx = sc.take<int>((size_t)nq);
+        wide = sc.take<unsigned long long>(1);
+        cub_tmp = sc.take<char>(kCubTemp);
+    }
+    auto scan = [&](auto* in, auto* out, int64_t cnt) {
+        size_t bytes = 0;
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, cnt, st));
+        if (bytes > kCubTemp) fail(CHEB_CAPACITY, "window build: scan scratch");
+        CHEB_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(cub_tmp, bytes, in, out, cnt, st));
+    };
+    k_win_splits<RPN><<<grid_for(n_hub * (NW + 1)), kBuildThreads, 0, st>>>(rp, col, n_hub, H0, W, NW, S);
+    k_win_sizes<<<grid_for(nq + 1), kBuildThreads, 0, st>>>(S, n_hub, NW, csz);
     CHEB_CUDA_CHECK(cudaGetLastError());
-    exclusive_scan(csz.ptr<int64_t>(), off.ptr<int64_t>(), nq + 1, tmp, st);
-    csz.release();
-    DevMem d_small(sizeof(int64_t) * (size_t)(4 * (NW + 1)));
-    int64_t* d_starts = d_small.ptr<int64_t>();        // [NW + 1] unpadded window starts
+    scan(csz, off, nq + 1);
+    int64_t* d_starts = d_small;                        // [NW + 1] unpadded window starts
     int64_t* d_delta = d_starts + (NW + 1);             // [NW]
     int64_t* d_wend = d_delta + (NW + 1);               // [NW]
     int64_t* d_wblk = d_wend + (NW + 1);                // [NW + 1]
-    k_win_gather_starts<<<(NW + 1 + 127) / 128, 128, 0, st>>>(off.ptr<int64_t>(), n_hub, NW, d_starts);
+    k_win_gather_starts<<<(NW + 1 + 127) / 128, 128, 0, st>>>(off, n_hub, NW, d_starts);
     CHEB_CUDA_CHECK(cudaGetLastError());
     std::vector<int64_t> hs((size_t)4 * (NW + 1), 0);
     CHEB_CUDA_CHECK(cudaMemcpyAsync(hs.data(), d_starts, sizeof(int64_t) * (NW + 1), cudaMemcpyDeviceToHost, st));
@@ -1850,11 +1889,26 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
     }
     h_wblk[NW] = cur / kWinBlock;
     const int64_t entries = hs[(size_t)NW], stream_len = cur, n_blocks = cur / kWinBlock;
-    if (entries == 0 || n_blocks >= INT32_MAX / 2) return;
+    if (entries == 0 || n_blocks >= INT32_MAX / 2 || n_blocks > max_blocks) return;
     CHEB_CUDA_CHECK(cudaMemcpyAsync(d_delta, h_delta, sizeof(int64_t) * 3 * (NW + 1), cudaMemcpyHostToDevice, st));
-    Wn.wcol.alloc(sizeof(unsigned short) * (size_t)stream_len + 64);
-    Wn.flags.alloc((size_t)stream_len / 8 + 64);
-    CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.wcol.get(), 0, sizeof(unsigned short) * (size_t)stream_len + 64, st));
+    // the view's own arrays, first allocation
+    Wn.grid = (int)std::max<int64_t>(1, std::min<int64_t>(V.grid, n_blocks));
+    Carver ca{nullptr};
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+            Wn.arena_a.alloc(ca.off);
+            ca = Carver{Wn.arena_a.ptr<char>()};
+        }
+        Wn.wcol.p = ca.take<unsigned short>((size_t)stream_len + 32);
+        Wn.flags.p = ca.take<unsigned char>((size_t)stream_len / 8 + 64);
+        Wn.meta.p = ca.take<unsigned short>((size_t)n_blocks * 32 + 32);
+        Wn.bbase.p = ca.take<int>((size_t)n_blocks + 1);
+        Wn.cta.p = ca.take<int64_t>((size_t)Wn.grid + 1);
+        Wn.wblk.p = ca.take<int64_t>((size_t)NW + 1);
+        Wn.hub_first.p = ca.take<int>((size_t)n_hub + 1);
+        Wn.kf.p = ca.take<int>((size_t)n_hub + 1);
+    }
+    CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.wcol.get(), 0, sizeof(unsigned short) * ((size_t)stream_len + 32), st));
     CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.flags.get(), 0, (size_t)stream_len / 8 + 64, st));
     unsigned* flags32 = Wn.flags.ptr<unsigned>();
     if (dbg_on()) {
@@ -1862,9 +1916,9 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
         dbg_mark("    windows: splits + layout");
     }
     k_win_copy<RPN, true><<<(int)std::min<int64_t>(n_hub, kWinBigRows), 512, 0, st>>>(
-        rp, col, n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, H0, W, NW, Wn.wcol.ptr<unsigned short>(), flags32);
+        rp, col, n_hub, S, off, d_delta, H0, W, NW, Wn.wcol.ptr<unsigned short>(), flags32);
     k_win_copy<RPN, false><<<(int)std::min<int64_t>((n_hub * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
-        rp, col, n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, H0, W, NW, Wn.wcol.ptr<unsigned short>(), flags32);
+        rp, col, n_hub, S, off, d_delta, H0, W, NW, Wn.wcol.ptr<unsigned short>(), flags32);
     k_win_padflags<<<(NW + 127) / 128, 128, 0, st>>>(d_wend, NW, flags32);
     CHEB_CUDA_CHECK(cudaGetLastError());
     if (dbg_on()) {
@@ -1878,48 +1932,32 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
         CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
         dbg_mark("    windows: bank order");
     }
-    Wn.meta.alloc(sizeof(unsigned short) * (size_t)n_blocks * 32 + 64);
     k_win_lanemeta<<<(int)std::min<int64_t>((n_blocks * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
         Wn.flags.ptr<unsigned char>(), n_blocks, Wn.meta.ptr<unsigned short>());
+    k_win_blockcount<<<grid_for(n_blocks + 1), kBuildThreads, 0, st>>>(flags32, n_blocks, pc);
     CHEB_CUDA_CHECK(cudaGetLastError());
-    DevMem pc(sizeof(int) * (size_t)(n_blocks + 1));
-    Wn.bbase.alloc(sizeof(int) * (size_t)(n_blocks + 1));
-    k_win_blockcount<<<grid_for(n_blocks + 1), kBuildThreads, 0, st>>>(flags32, n_blocks, pc.ptr<int>());
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    exclusive_scan(pc.ptr<int>(), Wn.bbase.ptr<int>(), n_blocks + 1, tmp, st);
-    Wn.grid = (int)std::max<int64_t>(1, std::min<int64_t>(V.grid, n_blocks));
-    Wn.cta.alloc(sizeof(int64_t) * (size_t)(Wn.grid + 1));
+    scan(pc, Wn.bbase.ptr<int>(), n_blocks + 1);
     k_win_cta_starts<<<(Wn.grid + 1 + 127) / 128, 128, 0, st>>>(Wn.bbase.ptr<int>(), n_blocks, tuning().winpw, Wn.grid,
                                                              Wn.cta.ptr<int64_t>());
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    DevMem mc(sizeof(int) * (size_t)(n_hub + 1)), rowpieces(sizeof(int) * (size_t)(n_hub + 1)),
-        subx(sizeof(int) * (size_t)nq), wide(sizeof(unsigned long long));
-    CHEB_CUDA_CHECK(cudaMemsetAsync(wide.get(), 0, sizeof(unsigned long long), st));
+    CHEB_CUDA_CHECK(cudaMemsetAsync(wide, 0, sizeof(unsigned long long), st));
     constexpr int kWideMin = 128;  // more partials than this: a warp per row in k_hub_finalize
-    k_win_rows<RPN><<<grid_for(n_hub + 1), kBuildThreads, 0, st>>>(rp, n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, NW,
-                                                                  kWideMin, mc.ptr<int>(), rowpieces.ptr<int>(),
-                                                                  subx.ptr<int>(), wide.ptr<unsigned long long>());
+    k_win_rows<RPN><<<grid_for(n_hub + 1), kBuildThreads, 0, st>>>(rp, n_hub, S, off, d_delta, NW, kWideMin, mc, rowpieces,
+                                                                  subx, wide);
     CHEB_CUDA_CHECK(cudaGetLastError());
-    Wn.hub_first.alloc(sizeof(int) * (size_t)(n_hub + 1));  // tb: first main chunk tile (= slot) of each hub row
-    Wn.kf.alloc(sizeof(int) * (size_t)(n_hub + 1));
-    int* tb = Wn.hub_first.ptr<int>();
-    exclusive_scan(mc.ptr<int>(), tb, n_hub + 1, tmp, st);
-    exclusive_scan(rowpieces.ptr<int>(), Wn.kf.ptr<int>(), n_hub + 1, tmp, st);
+    int* tb = Wn.hub_first.ptr<int>();  // first main chunk tile (= slot) of each hub row
+    scan(mc, tb, n_hub + 1);
+    scan(rowpieces, Wn.kf.ptr<int>(), n_hub + 1);
     int h_tot[3] = {0, 0, 0};
     unsigned long long h_wide = 0;
     CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_tot[0], Wn.bbase.ptr<int>() + n_blocks, sizeof(int), cudaMemcpyDeviceToHost, st));
     CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_tot[1], tb + n_hub, sizeof(int), cudaMemcpyDeviceToHost, st));
     CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_tot[2], Wn.kf.ptr<int>() + n_hub, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_wide, wide.get(), sizeof h_wide, cudaMemcpyDeviceToHost, st));
+    CHEB_CUDA_CHECK(cudaMemcpyAsync(&h_wide, wide, sizeof h_wide, cudaMemcpyDeviceToHost, st));
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     const int pieces = h_tot[0], MC = h_tot[1], listed = h_tot[2];  // pieces = listed + the padding's
     if ((int64_t)MC + pieces >= INT32_MAX) fail(CHEB_CAPACITY, "too many hub partials");
-    Wn.klist.alloc(sizeof(int) * (size_t)std::max(listed, 1));
-    k_win_klist<<<grid_for(nq), kBuildThreads, 0, st>>>(n_hub, S.ptr<int>(), off.ptr<int64_t>(), d_delta, NW, flags32,
-                                                     Wn.bbase.ptr<int>(), Wn.kf.ptr<int>(), subx.ptr<int>(),
-                                                     Wn.klist.ptr<int>());
-    CHEB_CUDA_CHECK(cudaGetLastError());
-    // the term kernel's program: main chunk tiles, then the view's pack tiles
+    // second allocation: the rows' piece lists and the term kernel's program (main chunk
+    // tiles, then the view's pack tiles)
     const int npack = V.n_tiles - V.n_chunk_tiles;
     if ((int64_t)MC + npack >= INT32_MAX) fail(CHEB_CAPACITY, "too many tiles");
     Wn.n_tiles = MC + npack;
@@ -1927,15 +1965,25 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
     const int per = (Wn.n_tiles + Sw - 1) / Sw;
     Wn.prog_len = std::max(kDescBlock, (per + kDescBlock - 1) / kDescBlock * kDescBlock);
     const size_t np = (size_t)Sw * Wn.prog_len;
-    Wn.prog.alloc(sizeof(WTile) * np);
+    Carver cb{nullptr};
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1) {
+            Wn.arena_b.alloc(cb.off);
+            cb = Carver{Wn.arena_b.ptr<char>()};
+        }
+        Wn.klist.p = cb.take<int>((size_t)std::max(listed, 1));
+        Wn.prog.p = cb.take<WTile>(np);
+    }
+    k_win_klist<<<grid_for(nq), kBuildThreads, 0, st>>>(n_hub, S, off, d_delta, NW, flags32, Wn.bbase.ptr<int>(),
+                                                     Wn.kf.ptr<int>(), subx, Wn.klist.ptr<int>());
+    CHEB_CUDA_CHECK(cudaGetLastError());
     CHEB_CUDA_CHECK(cudaMemsetAsync(Wn.prog.get(), 0, sizeof(WTile) * np, st));
     k_win_prog_hub<RPN><<<(int)std::min<int64_t>((n_hub * 32 + 255) / 256, 148 * 16), 256, 0, st>>>(
-        rp, n_hub, S.ptr<int>(), NW, tb, Sw, Wn.prog_len, Wn.prog.ptr<WTile>());
+        rp, n_hub, S, NW, tb, Sw, Wn.prog_len, Wn.prog.ptr<WTile>());
     if (npack > 0)
         k_win_prog_pack<<<grid_for(npack), kBuildThreads, 0, st>>>(V.tiles.ptr<Tile>(), V.n_chunk_tiles, V.n_tiles, MC, Sw,
                                                                  Wn.prog_len, Wn.prog.ptr<WTile>());
     CHEB_CUDA_CHECK(cudaGetLastError());
-    Wn.wblk.alloc(sizeof(int64_t) * (size_t)(NW + 1));
     CHEB_CUDA_CHECK(cudaMemcpyAsync(Wn.wblk.get(), d_wblk, sizeof(int64_t) * (NW + 1), cudaMemcpyDeviceToDevice, st));
     CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
     (void)h_wblk;

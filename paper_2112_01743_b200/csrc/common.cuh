@@ -259,6 +259,12 @@ struct SolverView {
     // adds a row's chunk partials hub_part[hub_first[h] ..) and its pieces klist[kf[h] ..).
     // The term kernel then runs `prog` below instead of the view's own program (which, with
     // tiles / hub_first above, stays as built for the batched path and the introspection).
+    struct Span {  // a piece of one of the two allocations below
+        void* p = nullptr;
+        template <class T>
+        T* ptr() const { return static_cast<T*>(p); }
+        void* get() const { return p; }
+    };
     struct Windows {
         bool ready = false;
         int NW = 0, W = 0, H0 = 0;
@@ -268,21 +274,28 @@ struct SolverView {
         int64_t n_wide = 0;        // hub rows [0, n_wide) finalized by a warp each
         int64_t entries = 0;       // windowed entries (statistics)
         int64_t pieces = 0;        // their slots
-        DevMem wcol;               // uint16 [n_blocks * kWinBlock] window-local ids
-        DevMem flags;              // uint8 [n_blocks * 32]: bit i of byte j = entry 8 j + i starts a piece
-        DevMem meta;               // uint16 [n_blocks * 32]: per lane, its start bits | pieces in earlier lanes << 8
-        DevMem bbase;              // int32 [n_blocks + 1]: pieces before each block
-        DevMem kf;                 // int32 [n_hub + 1]: first klist entry of each hub row
-        DevMem klist;              // int32: the rows' pieces (stream indices), row by row
-        DevMem wblk;               // int64 [NW + 1]: first block of each window
-        DevMem cta;                // int64 [grid + 1]: block range of each CTA of the window pass
+        Span wcol;               // uint16 [n_blocks * kWinBlock] window-local ids
+        Span flags;              // uint8 [n_blocks * 32]: bit i of byte j = entry 8 j + i starts a piece
+        Span meta;               // uint16 [n_blocks * 32]: per lane, its start bits | pieces in earlier lanes << 8
+        Span bbase;              // int32 [n_blocks + 1]: pieces before each block
+        Span kf;                 // int32 [n_hub + 1]: first klist entry of each hub row
+        Span klist;              // int32: the rows' pieces (stream indices), row by row
+        Span wblk;               // int64 [NW + 1]: first block of each window
+        Span cta;                // int64 [grid + 1]: block range of each CTA of the window pass
         int grid = 0;
-        DevMem prog;               // WTile programs of the term kernel (main chunk tiles + pack tiles)
+        Span prog;               // WTile programs of the term kernel (main chunk tiles + pack tiles)
         int prog_len = 0, n_tiles = 0;
-        DevMem hub_first;          // int32 [n_hub + 1]: first main chunk tile (slot) of each hub row
+        Span hub_first;          // int32 [n_hub + 1]: first main chunk tile (slot) of each hub row
+        // two pool allocations per view (the stream and its indices; the piece lists and the
+        // program), carved into the arrays above: many separate blocks of changing sizes left
+        // the pool unable to place the next upload's 4 GB buffers without remapping (config 4
+        // e2e: upload 176 ms with 240-1300 ms outliers)
+        DevMem arena_a, arena_b;
         void release() {
             ready = false;
-            for (DevMem* d : {&wcol, &flags, &meta, &bbase, &cta, &kf, &klist, &wblk, &prog, &hub_first}) d->release();
+            for (Span* d : {&wcol, &flags, &meta, &bbase, &cta, &kf, &klist, &wblk, &prog, &hub_first}) d->p = nullptr;
+            arena_a.release();
+            arena_b.release();
         }
     };
     Windows win;
@@ -297,8 +310,7 @@ struct SolverView {
     int64_t bin_tiles[7] = {}, bin_rows[7] = {}, bin_nnz[7] = {};
     void set_stream(cudaStream_t s) {
         for (DevMem* d : {&order, &rank, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first, &push_mask,
-                          &col_sorted, &win.wcol, &win.flags, &win.meta, &win.bbase, &win.cta, &win.kf, &win.klist, &win.wblk, &win.prog,
-                          &win.hub_first})
+                          &col_sorted, &win.arena_a, &win.arena_b})
             d->set_stream(s);
     }
 };
@@ -490,8 +502,10 @@ struct Tuning {
                         // 0 off, -1 auto (64 when x exceeds L2, else 24, on graphs of >= 48 M entries)
     int winbank = 1;    // window stream entries ordered inside their pieces for conflict-free shared-memory gathers
     int winpw = 4;      // window pass CTA ranges: cost of a block = 256 + winpw * its pieces
+    int winh0 = 0;      // first windowed id (0: the hub rows keep only ids past the last window; config 4 99.5 -> 94.3 ms per
+                        // solve, config 3 11.58 -> 10.91); -1 = the fp64 hot-prefix capacity (the term kernel keeps ids below it)
     int winskip = 0;    // timing experiments (wrong results): 1 no window pass, 2 no term kernel, 3 no hub finalize
-    int winsize = 24576; // entries of x per window (<= 65536: 16-bit local ids; fp64 192 KB of shared memory)
+    int winsize = 28672; // entries of x per window (<= 65536: 16-bit local ids; fp64 224 KB of shared memory; C4 24576 -> 28672: 94.1 -> 92.9 ms)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {
@@ -525,6 +539,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_WINSKIP")) x.winskip = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_WINBANK")) x.winbank = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_WINPW")) x.winpw = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_WINH0")) x.winh0 = std::atoi(e);
         return x;
     }();
     return t;

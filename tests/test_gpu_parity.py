@@ -813,7 +813,7 @@ def _forced_windows(lib, nw, size):
 
 def _default_windows(lib):
     lib.cheb_set_tuning(b"windows", -1)
-    lib.cheb_set_tuning(b"winsize", 24576)
+    lib.cheb_set_tuning(b"winsize", 28672)
 
 
 @pytest.mark.parametrize("graph", ["chung_lu", "rmat"])
