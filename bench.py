@@ -622,6 +622,19 @@ def lsu_roofline(config, precision, world, mean_launch_us, sm_mhz):
             "source": "wavefronts from the committed ncu capture (profiles/traffic.json)"}
 
 
+def window_info(dg):
+    """The resident view's column windows (hub-row entries gathered from shared memory by
+    k_window_pass), or None when the view has none."""
+    from paper_2112_01743_b200 import _lib as L
+    sizes = np.zeros(8, dtype=np.int64)
+    if L.load().cheb_graph_view_windows(dg.handle, sizes.ctypes.data_as(L.I64P), None, None, None, None, None) != 0:
+        return None
+    if sizes[0] <= 0:
+        return None
+    return {"windows": int(sizes[0]), "ids_per_window": int(sizes[1]), "first_id": int(sizes[2]),
+            "entries": int(sizes[4]), "piece_sums": int(sizes[5]), "chunk_tiles_left": int(sizes[6])}
+
+
 def measured_traffic(config, precision, world):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     (profiles/traffic.json), or None when this workload has not been captured."""
@@ -802,6 +815,7 @@ def main():
     B = algorithmic_bytes(n, nnz, rp_bytes, vbytes, R)
     peak, peak_kind = peaks()
     achieved = B / (term_us * 1e-6) / 1e9
+    win = window_info(dg) if R == 1 and dist.world == 1 else None
 
     exchange_info = None
     if dist.world > 1 and R_cfg == 1:
@@ -839,7 +853,8 @@ def main():
                 secondary.append({"config": name, "failed": f"{type(ex).__name__}: {ex}"})
 
     if dist.rank == 0:
-        kernel = "k_spmm_term + k_spmm_hub_finalize" if R > 1 else "k_term_warp<EPI_CPAA> + k_hub_finalize"
+        kernel = ("k_spmm_term + k_spmm_hub_finalize" if R > 1 else
+                  ("k_window_pass + " if win else "") + "k_term_warp<EPI_CPAA> + k_hub_finalize")
         clk_summary = clk.summary()
         line = {
             "metric": "cpaa_gteps_per_term",
@@ -861,11 +876,13 @@ def main():
                         "time_to_1e-10_ms": round(ms_step, 4), "graph_build_s": round(build_s, 3),
                         "gteps_definition": "nnz*R*terms/step_time (every CSR entry one traversal)",
                         "R_per_rank": R,
+                        **({"column_windows": win} if win else {}),
                         **({"exchange_note": exchange_note} if exchange_note else {})},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": measured_traffic(args.config, args.precision, dist.world),
-                         "traffic_unit": "DRAM bytes per launch (ncu --set full, profiles/traffic.json)",
+                         "traffic_unit": "DRAM bytes per term, summed over the term's kernels "
+                                         "(ncu --set full, profiles/traffic.json)",
                          "kernel": kernel, "bytes_per_launch": B,
                          "bytes_formula": "4 nnz + I_r (n+1) + 6 V R n (SURVEY.md 8d)",
                          "mean_launch_us": round(term_us, 3),

@@ -247,6 +247,59 @@ T read_scalar(const T* d, cudaStream_t st) {
 
 }  // namespace
 
+namespace {
+struct WindowArenaCache {
+    std::mutex mu;
+    std::map<int, std::vector<DevMem>> blocks;  // per device, free
+};
+WindowArenaCache& window_arena_cache() {
+    static WindowArenaCache* c = new WindowArenaCache;  // never destroyed (no cudaFree at process exit)
+    return *c;
+}
+constexpr size_t kWindowArenaKeep = 6;  // free blocks kept per device
+}  // namespace
+
+void window_arena_take(DevMem& out, size_t bytes) {
+    int dev = 0;
+    CHEB_CUDA_CHECK(cudaGetDevice(&dev));
+    WindowArenaCache& c = window_arena_cache();
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto& v = c.blocks[dev];
+        int best = -1;
+        for (int i = 0; i < (int)v.size(); ++i)  // smallest block that fits without wasting more than half
+            if (v[i].bytes() >= bytes && v[i].bytes() <= 2 * bytes + (size_t(1) << 20) &&
+                (best < 0 || v[i].bytes() < v[best].bytes()))
+                best = i;
+        if (alloc_debug()) std::fprintf(stderr, "[arena] take %.1f MB: %zu cached, fit %d\n", bytes / 1e6, v.size(), best);
+        if (best >= 0) {
+            out = std::move(v[best]);
+            v.erase(v.begin() + best);
+            return;
+        }
+    }
+    AllocScope plain(nullptr);
+    out.alloc(bytes + bytes / 16);
+}
+
+void window_arena_give(DevMem& blk) {
+    if (!blk.get() || blk.bytes() == 0) return;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaDeviceSynchronize();  // nothing in flight may still read the block
+    WindowArenaCache& c = window_arena_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto& v = c.blocks[dev];
+    if (alloc_debug()) std::fprintf(stderr, "[arena] give %.1f MB (%zu cached)\n", blk.bytes() / 1e6, v.size());
+    v.push_back(std::move(blk));
+    if (v.size() > kWindowArenaKeep) {  // drop the smallest
+        size_t small = 0;
+        for (size_t i = 1; i < v.size(); ++i)
+            if (v[i].bytes() < v[small].bytes()) small = i;
+        v.erase(v.begin() + (long)small);
+    }
+}
+
 void build_from_edges(cheb_graph* g, const void* d_edges, int64_t E, int edge_bits,
                       const cheb_build_opts& o) {
     cudaStream_t st = g->stream;
@@ -1896,7 +1949,7 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
     Carver ca{nullptr};
     for (int pass = 0; pass < 2; ++pass) {
         if (pass == 1) {
-            Wn.arena_a.alloc(ca.off);
+            window_arena_take(Wn.arena_a, ca.off);
             ca = Carver{Wn.arena_a.ptr<char>()};
         }
         Wn.wcol.p = ca.take<unsigned short>((size_t)stream_len + 32);
@@ -1968,7 +2021,7 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
     Carver cb{nullptr};
     for (int pass = 0; pass < 2; ++pass) {
         if (pass == 1) {
-            Wn.arena_b.alloc(cb.off);
+            window_arena_take(Wn.arena_b, cb.off);
             cb = Carver{Wn.arena_b.ptr<char>()};
         }
         Wn.klist.p = cb.take<int>((size_t)std::max(listed, 1));
@@ -2178,11 +2231,13 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
     }
     const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2) : tuning().sortrows > 0;
     // column windows (single-GPU views) need the hub rows in ascending id order
-    // (auto: graphs of >= 48 M entries, where the extra launch per term is paid back: config 2,
+    // (partitioned views too: x keeps the global ids on every rank, and a rank's window pass runs
+    // behind the term barrier like its term kernel; auto: views of >= 48 M entries, where the
+    // extra launch per term is paid back: config 2,
     // 19 M entries, runs 65 -> 74 us/term with windows, config 3 362 -> 297, config 4 3447 -> 2554)
     int n_windows = tuning().windows;
     if (n_windows < 0) n_windows = nnz_l >= (int64_t(48) << 20) ? (big_x ? 64 : 24) : 0;
-    const bool want_windows = n_windows > 0 && P.G == 1 && V.n_hub > 0 && tuning().chunksched <= 1 &&
+    const bool want_windows = n_windows > 0 && V.n_hub > 0 && tuning().chunksched <= 1 &&
                               V.x_len > kHotBytes / 8 && nnz_l < INT32_MAX;
     const bool hubs_only = (tuning().sortrows == 2 || (want_windows && !big_x)) && V.n_hub > 0;
     const bool sort_rows = (big_x || hubs_only) && nnz_l > 0 && nnz_l < INT32_MAX;

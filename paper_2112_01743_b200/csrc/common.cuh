@@ -216,6 +216,12 @@ constexpr int kColBuf = 264;         // ints per TMA column buffer (256 + alignm
 constexpr int kHotBytes = CHEB_HOT_KB * 1024;  // shared hot x prefix; sized so hot + scratch fit the 164 KB carve-out and L1 keeps ~64 KB (tools/variant_run.sh sweep)
 constexpr int kTileChunk = 0x10;
 
+// build.cu: cudaMalloc'ed blocks of the views' window arrays, recycled per device (a block
+// given back may be handed to any later view of the device: give() waits for the device)
+class DevMem;
+void window_arena_take(DevMem& out, size_t bytes);
+void window_arena_give(DevMem& blk);
+
 struct SolverView {
     bool ready = false;
     bool rp64 = false;
@@ -248,7 +254,7 @@ struct SolverView {
     };
     std::vector<Phase> phases;
     bool sorted_rows = false;  // rows hold their renamed ids in ascending order
-    // Column windows of the hub rows (single-GPU views, build.cu window_schedule): the x ids
+    // Column windows of the hub rows (build.cu window_schedule): the x ids
     // [H0, H0 + NW W) are cut into NW windows of W entries.  Every hub row's entries inside a
     // window (a contiguous piece of the ascending row) are copied, as 16-bit window-local ids,
     // into one window-major stream cut into blocks of kWinBlock entries; k_window_pass loads a
@@ -286,17 +292,37 @@ struct SolverView {
         Span prog;               // WTile programs of the term kernel (main chunk tiles + pack tiles)
         int prog_len = 0, n_tiles = 0;
         Span hub_first;          // int32 [n_hub + 1]: first main chunk tile (slot) of each hub row
-        // two pool allocations per view (the stream and its indices; the piece lists and the
-        // program), carved into the arrays above: many separate blocks of changing sizes left
-        // the pool unable to place the next upload's 4 GB buffers without remapping (config 4
-        // e2e: upload 176 ms with 240-1300 ms outliers)
+        // The arrays above are carved from two blocks (the stream and its indices; the piece
+        // lists and the program) of plain cudaMalloc memory recycled through a small per-device
+        // cache (build.cu window_arena_take / _give): steady-state uploads allocate nothing for
+        // the windows.  As ~18 separate pool allocations per upload they left the memory pool
+        // unable to place the next upload's 4 GB buffers without remapping (config 4 e2e: uploads
+        // of 176 ms with 240-1340 ms outliers); as two pool blocks, next to a resident graph's,
+        // the outliers came back inside bench.py (e2e steps of 284-1520 ms).
         DevMem arena_a, arena_b;
         void release() {
             ready = false;
             for (Span* d : {&wcol, &flags, &meta, &bbase, &cta, &kf, &klist, &wblk, &prog, &hub_first}) d->p = nullptr;
-            arena_a.release();
-            arena_b.release();
+            window_arena_give(arena_a);
+            window_arena_give(arena_b);
         }
+        Windows() = default;
+        Windows(Windows&&) = default;
+        Windows& operator=(Windows&& o) noexcept {
+            if (this != &o) {
+                release();  // the blocks go back to the cache, not to cudaFree
+                ready = o.ready; NW = o.NW; W = o.W; H0 = o.H0; n_blocks = o.n_blocks; n_slots = o.n_slots;
+                MC = o.MC; n_wide = o.n_wide; entries = o.entries; pieces = o.pieces; grid = o.grid;
+                prog_len = o.prog_len; n_tiles = o.n_tiles;
+                wcol = o.wcol; flags = o.flags; meta = o.meta; bbase = o.bbase; kf = o.kf; klist = o.klist;
+                wblk = o.wblk; cta = o.cta; prog = o.prog; hub_first = o.hub_first;
+                arena_a = std::move(o.arena_a);
+                arena_b = std::move(o.arena_b);
+                o.ready = false;
+            }
+            return *this;
+        }
+        ~Windows() { release(); }
     };
     Windows win;
     // Row partition (G > 1): bit r of push_mask[u] = rank r has a row with neighbour u, i.e.
@@ -310,7 +336,7 @@ struct SolverView {
     int64_t bin_tiles[7] = {}, bin_rows[7] = {}, bin_nnz[7] = {};
     void set_stream(cudaStream_t s) {
         for (DevMem* d : {&order, &rank, &order_full, &row_ptr, &col, &inv, &tiles, &prog, &hub_first, &push_mask,
-                          &col_sorted, &win.arena_a, &win.arena_b})
+                          &col_sorted})
             d->set_stream(s);
     }
 };
@@ -498,7 +524,7 @@ struct Tuning {
     int hubwarp = 0;    // 1: every hub row finalized by a warp (the lane-per-row path off; tests)
     int pull = 1;       // view tiles / programs pulled from pinned host memory by a kernel (not the copy engine)
     int colsplit_pct = -1; // K = 2: first block boundary at this percent of x (-1: equal halves)
-    int windows = -1;   // column windows of the hub rows (SolverView::Windows), single-GPU views: NW > 0 windows,
+    int windows = -1;   // column windows of the hub rows (SolverView::Windows): NW > 0 windows,
                         // 0 off, -1 auto (64 when x exceeds L2, else 24, on graphs of >= 48 M entries)
     int winbank = 1;    // window stream entries ordered inside their pieces for conflict-free shared-memory gathers
     int winpw = 4;      // window pass CTA ranges: cost of a block = 256 + winpw * its pieces

@@ -1454,7 +1454,7 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
         ab.xdiscard_len = (EPI == EPI_CPAA && tuning().xdiscard && !a.push && g->part.G == 1 && !g->part.comm)
                               ? (g->view.x_len * (int64_t)sizeof(V) / 128) * 128 / (int64_t)sizeof(V) : 0;
         const size_t x_bytes = (size_t)std::max<int64_t>(g->view.x_len, 1) * sizeof(V);
-        const bool windows_on = g->view.win.ready && g->part.G == 1 && !a.push;
+        const bool windows_on = g->view.win.ready;
         auto launch = [&](const TermArgs<RP, V>& args, const WTile* prog, int plen, int ntiles, const V* win,
                           size_t win_bytes) {
             cudaLaunchConfig_t cfg = {};

@@ -67,6 +67,42 @@ def test_push_group_hub_rows_and_eps(cheb):
         grp.close()
 
 
+@pytest.mark.parametrize("halo", [1, 0])
+def test_push_group_with_column_windows(cheb, halo):
+    """Partitioned ranks with the hub rows' column windows forced on (every rank's window pass
+    reads the x its peers pushed, behind the term barrier): equal to the single-GPU solve
+    within 1e-12 with the same top-100, fp64 and fp32, repeated solves bitwise equal."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    import ctypes as C
+    lib = _lib.load()
+    e = Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 20000.0, 900_000, 5)
+    single_dg, info = cheb.build_device_graph(e)
+    single = cheb.run_cpaa(single_dg, cheb.SolverConfig(eps=1e-10))
+    try:
+        assert lib.cheb_set_tuning(b"windows", 6) == 0 and lib.cheb_set_tuning(b"winsize", 2048) == 0
+        assert lib.cheb_set_tuning(b"halo", halo) == 0
+        for G in (2, 4):
+            hs = _handles(cheb, e, G)
+            grp = cheb.PartitionGroup(hs)
+            res = cheb.run_cpaa(grp, cheb.SolverConfig(eps=1e-10))
+            sizes = np.zeros(8, dtype=np.int64)
+            assert lib.cheb_graph_view_windows(hs[0].handle, sizes.ctypes.data_as(C.POINTER(C.c_int64)),
+                                               None, None, None, None, None) == 0
+            assert sizes[0] == 6 and sizes[4] > 0          # the rank's view has windows
+            assert np.max(np.abs(res.ranks - single.ranks)) <= TOL64
+            assert np.array_equal(top_k(res.ranks), top_k(single.ranks))
+            again = cheb.run_cpaa(grp, cheb.SolverConfig(eps=1e-10))
+            assert np.array_equal(again.ranks, res.ranks)
+            f32 = cheb.run_cpaa(grp, cheb.SolverConfig(eps=1e-10, precision=32))
+            assert np.sum(np.abs(f32.ranks - single.ranks)) / np.sum(single.ranks) <= 1e-6
+            grp.close()
+    finally:
+        lib.cheb_set_tuning(b"windows", -1)
+        lib.cheb_set_tuning(b"winsize", 28672)
+        lib.cheb_set_tuning(b"halo", 1)
+
+
 def test_push_group_zero_rounds_and_fp32(cheb):
     z = load_golden("gnp2000")
     grp = cheb.PartitionGroup(_handles(cheb, z["edges"], 2))
