@@ -1751,7 +1751,7 @@ __global__ void k_win_cta_starts(const int* __restrict__ bbase, int64_t n_blocks
 template <class RPN>
 __global__ void k_win_rows(const RPN* __restrict__ rp, int64_t n_hub, const int* __restrict__ S,
                            const int64_t* __restrict__ off, const int64_t* __restrict__ delta, int NW, int wide_min,
-                           int* __restrict__ mc, int* __restrict__ rowpieces, int* __restrict__ subx,
+                           int drop_tail, int* __restrict__ mc, int* __restrict__ rowpieces, int* __restrict__ subx,
                            unsigned long long* __restrict__ wide) {
     for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h <= n_hub; h += (int64_t)gridDim.x * blockDim.x) {
         if (h == n_hub) {
@@ -1762,7 +1762,7 @@ __global__ void k_win_rows(const RPN* __restrict__ rp, int64_t n_hub, const int*
         const int64_t d = rp[h + 1] - rp[h];
         const int* Sh = S + h * (NW + 1);
         const int64_t sA = Sh[0], tail = d - Sh[NW];
-        const int m = (int)((sA + kWarpNnz - 1) / kWarpNnz + (tail + kWarpNnz - 1) / kWarpNnz);
+        const int m = drop_tail ? 0 : (int)((sA + kWarpNnz - 1) / kWarpNnz + (tail + kWarpNnz - 1) / kWarpNnz);
         int s = 0;
         for (int w = 0; w < NW; ++w) {
             subx[h * NW + w] = s;
@@ -1994,7 +1994,9 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
                                                              Wn.cta.ptr<int64_t>());
     CHEB_CUDA_CHECK(cudaMemsetAsync(wide, 0, sizeof(unsigned long long), st));
     constexpr int kWideMin = 128;  // more partials than this: a warp per row in k_hub_finalize
-    k_win_rows<RPN><<<grid_for(n_hub + 1), kBuildThreads, 0, st>>>(rp, n_hub, S, off, d_delta, NW, kWideMin, mc, rowpieces,
+    k_win_rows<RPN><<<grid_for(n_hub + 1), kBuildThreads, 0, st>>>(rp, n_hub, S, off, d_delta, NW, kWideMin,
+                                                                  (tuning().winskip & 32) ? 1 : 0,  // timing experiment: the rows' cold tails dropped (wrong results)
+                                                                  mc, rowpieces,
                                                                   subx, wide);
     CHEB_CUDA_CHECK(cudaGetLastError());
     int* tb = Wn.hub_first.ptr<int>();  // first main chunk tile (= slot) of each hub row
