@@ -51,6 +51,17 @@ def _device_side(name):
     return bench.build_device(bench.CONFIGS[name], 0)
 
 
+def _windows(dg):
+    """(windows, windowed entries) of the resident view: the hub rows' column windows
+    (k_window_pass) are part of the default schedule from 48 M entries up."""
+    import ctypes as C
+    from paper_2112_01743_b200 import _lib
+    sizes = np.zeros(8, dtype=np.int64)
+    assert _lib.load().cheb_graph_view_windows(dg.handle, sizes.ctypes.data_as(C.POINTER(C.c_int64)),
+                                               None, None, None, None, None) == 0
+    return int(sizes[0]), int(sizes[4])
+
+
 def _check_csr(rg, dg, info):
     ref = rg.csr()
     assert info["n"] == rg.n and info["m"] == rg.m and info["nnz"] == rg.nnz
@@ -114,6 +125,11 @@ def test_config_full_size_vs_reference(cheb, reference, name):
     _check_csr(rg, dg, info)
     _check_solves(cheb, rg, dg, _threads())
     _check_power_and_apply(cheb, rg, dg, _threads())
+    nw, entries = _windows(dg)
+    if name == "c3":  # the solves above ran the window schedule (24 windows), config 2 the plain one
+        assert nw == 24 and entries > 0.5 * info["nnz"]
+    else:
+        assert nw == 0
     dg.free()
 
 
@@ -127,6 +143,8 @@ def test_config4_full_size_vs_reference(cheb, reference):
     rg._csr = None
     gc.collect()
     want = _check_solves(cheb, rg, dg, _threads(), fp32=True)
+    nw, entries = _windows(dg)  # ... through the window schedule: 64 windows, two thirds of the entries
+    assert nw == 64 and entries > 0.6 * info["nnz"]
     # the mass ledger of the reference's own trace holds for ours too
     t = cheb.coefficients(C, 39)
     n = float(info["n"])
