@@ -1639,6 +1639,10 @@ __global__ void k_win_padflags(const int64_t* __restrict__ wend, int NW, unsigne
 // gather instructions of a block: position p is read by lane p / 8 in instruction p % 8.
 // Greedy, a thread per block: each position takes, among the next entries of its piece, one
 // whose bank pair the instruction's half-warp has not used yet.
+#ifndef CHEB_WIN_LOOK
+#define CHEB_WIN_LOOK 24
+#endif
+constexpr int kBankLook = CHEB_WIN_LOOK;  // candidates a position may choose from (the next entries of its piece)
 constexpr int kBankThreads = 64, kBankStride = kWinBlock + 2;  // shorts per thread row (129 words: conflict-free)
 __global__ void __launch_bounds__(kBankThreads)
 k_win_bank_order(unsigned short* __restrict__ wcol, const unsigned* __restrict__ flags32, int64_t n_blocks) {
@@ -1669,12 +1673,12 @@ k_win_bank_order(unsigned short* __restrict__ wcol, const unsigned* __restrict__
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int p = wq * 32 + p4 * 8 + i;
-                        if (p >= pe) {  // end of the piece holding p: next start bit, at most 24 positions on
+                        if (p >= pe) {  // end of the piece holding p: next start bit, at most kBankLook positions on
                             const int q = p4 * 8 + i + 1;  // in-word bit of p + 1
                             const unsigned long long bits = ((unsigned long long)fnext << 32 | fword) >> q;
                             const int d = bits ? __ffsll((long long)bits) - 1 : 64;
-                            pe = min(p + 1 + d, p + 24);
-                            if (wq + 1 == kWinBlock / 32) pe = min(pe, kWinBlock);
+                            pe = min(p + 1 + d, p + kBankLook);
+                            pe = min(pe, kWinBlock);  // (start bits are looked up 64 positions ahead at most)
                         }
                         const int shf = (p >> 7) << 4;
                         const unsigned mask = used[i] >> shf;

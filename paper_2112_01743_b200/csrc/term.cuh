@@ -918,7 +918,10 @@ __device__ __forceinline__ WinBlock win_load(const uint4* __restrict__ wcol, con
     return b;
 }
 
-constexpr int kWinAhead = 3;  // blocks of the stream in flight per warp (registers)
+#ifndef CHEB_WIN_AHEAD
+#define CHEB_WIN_AHEAD 3
+#endif
+constexpr int kWinAhead = CHEB_WIN_AHEAD;  // blocks of the stream in flight per warp (registers)
 
 template <class V>
 __global__ void __launch_bounds__(1024, 1)
