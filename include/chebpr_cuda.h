@@ -273,7 +273,10 @@ cheb_status cheb_cpaa_profile(cheb_graph_t g, const cheb_cpaa_opts* opts, double
 
 /* Experiment knobs for kernel studies (not for production use): "hot" caps the shared-memory
  * hot-prefix size in vertices (-1 = full capacity); "nogather" = 1 replaces x gathers by
- * constants (timing of everything but the gather; results are wrong). */
+ * constants (timing of everything but the gather; results are wrong).  "windows" / "winsize" /
+ * "winh0" (views built afterwards): the number of column windows of the hub rows (0 off, -1 the
+ * default policy: graphs of >= 48 M entries), the ids per window and the first windowed id.  The
+ * full list is `Tuning` in csrc/common.cuh; an unknown key returns CHEB_INVALID_ARG. */
 cheb_status cheb_set_tuning(const char* key, int value);
 
 /* run_power (power.hpp:24-25, power.cpp:28-109). */

@@ -1885,7 +1885,7 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
     Wn.release();
     const int64_t n_hub = V.n_hub;
     const int H0 = tuning().winh0 >= 0 ? (tuning().winh0 & ~7) : kHotBytes / 8;
-    W = std::max(256, std::min(W, 65536)) & ~7;
+    W = std::max(256, std::min(W, kWinMaxIds)) & ~7;
     if (n_hub <= 0 || V.x_len <= H0) return;
     const int NW = (int)std::min<int64_t>(NW_req, (V.x_len - H0 + W - 1) / W);
     if (NW <= 0 || n_hub * (int64_t)(NW + 1) >= (int64_t)INT32_MAX * 4) return;

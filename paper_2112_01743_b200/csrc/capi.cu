@@ -1205,6 +1205,10 @@ cheb_status cheb_set_tuning(const char* key, int value) {
         else if (k == "colsplit_pct") tuning().colsplit_pct = value;  // applies to views built afterwards
         else if (k == "windows") tuning().windows = value;    // applies to views built afterwards
         else if (k == "winsize") tuning().winsize = value;    // applies to views built afterwards
+        else if (k == "winh0") tuning().winh0 = value;        // applies to views built afterwards
+        else if (k == "winpw") tuning().winpw = value;        // applies to views built afterwards
+        else if (k == "winbank") tuning().winbank = value;    // applies to views built afterwards
+        else if (k == "winskip") tuning().winskip = value;
         else fail(CHEB_INVALID_ARG, "unknown tuning key " + k);
     });
 }

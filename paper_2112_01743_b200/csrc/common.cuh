@@ -200,6 +200,8 @@ struct WTile {
     uint8_t meta;
 };
 static_assert(sizeof(WTile) == 16, "WTile is 16 bytes");
+constexpr int kWinSmemMax = 226 * 1024;            // dynamic shared memory of k_window_pass (+ its static mbarrier)
+constexpr int kWinMaxIds = (kWinSmemMax / 8) & ~7;  // ids per window: an fp64 window must fit (28,928)
 constexpr int kWinBlock = 256;       // entries per block of the window stream (a warp: 8 per lane)
 constexpr int kDescBlock = 8;        // descriptors per TMA refill of a warp's program ring
 constexpr int kThreads = 256;        // CTA size of the auxiliary kernels
@@ -532,7 +534,7 @@ struct Tuning {
                         // solve, config 3 11.58 -> 10.91); -1 = the fp64 hot-prefix capacity (the term kernel keeps ids below it)
     int winskip = 0;    // timing experiments: 1 no window pass, 2 no term kernel, 3 no hub finalize (wrong results);
                         // bits: 4 window pass launched without PDL, 8 term kernel behind it WITH PDL, 16 hub finalize without
-    int winsize = 28672; // entries of x per window (<= 65536: 16-bit local ids; fp64 224 KB of shared memory; C4 24576 -> 28672: 94.1 -> 92.9 ms)
+    int winsize = 28672; // entries of x per window (clamped to kWinMaxIds; 16-bit local ids; fp64 224 KB of shared memory; C4 24576 -> 28672: 94.1 -> 92.9 ms)
 };
 inline Tuning& tuning() {
     static Tuning t = [] {

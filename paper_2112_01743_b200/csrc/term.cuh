@@ -1494,7 +1494,6 @@ int launch_pass(cheb_graph* g, const Layout& L, const TermArgs<RP, V>& a) {
             // the hub rows' window pieces first (their sums land in hub_part), then the term
             // kernel over the remaining entries, then the finalize
             static std::atomic<uint64_t> wattr_set{0};
-            constexpr int kWinSmemMax = 226 * 1024;  // + the static mbarrier
             const size_t wsmem = (size_t)Wn.W * sizeof(V);
             if (wsmem > (size_t)kWinSmemMax) fail(CHEB_INVALID_ARG, "column window larger than shared memory");
             if (first_on_device(wattr_set, g->device)) {

@@ -816,27 +816,11 @@ def _default_windows(lib):
     lib.cheb_set_tuning(b"winsize", 28672)
 
 
-@pytest.mark.parametrize("graph", ["chung_lu", "rmat"])
-def test_column_windows_hold_every_windowed_entry_once(cheb, graph):
-    """The window stream of a view (forced: 6 windows of 2048 ids on a small graph) holds, piece by
-    piece, exactly the hub rows' entries with ids in [H0, H0 + NW W): every hub row's listed pieces
-    give back the multiset of its windowed ids, pieces never cross a 256-entry block, the per-lane
-    piece counts and block bases agree with the start bits, and the padding belongs to no row."""
-    from paper_2112_01743_b200 import _lib
-    from paper_2112_01743_b200 import generate as Gen
-    lib = _lib.load()
-    e = (Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 20000.0, 900_000, 5) if graph == "chung_lu"
-         else Gen.rmat_edges(16, 16, 0.57, 0.19, 0.19, 3))
-    try:
-        _forced_windows(lib, 6, 2048)
-        dg, info = cheb.build_device_graph(e, cheb.BuildOptions(drop_isolated=True))
-        p = _window_plan(lib, dg)
-        dg.free()
-    finally:
-        _default_windows(lib)
+def _check_window_structure(p):
+    """The stream of a window plan holds, piece by piece, exactly the hub rows' entries with ids
+    in [H0, H0 + NW W): see test_column_windows_hold_every_windowed_entry_once."""
     v = p["view"]
     NW, W, H0, n_hub = p["NW"], p["W"], p["H0"], v["n_hub"]
-    assert NW == 6 and W == 2048 and n_hub > 0
     rp, col = v["rp"], v["col"]
     hub_end = int(rp[n_hub])
     row_of = np.repeat(np.arange(n_hub), np.diff(rp[:n_hub + 1]))
@@ -867,6 +851,69 @@ def test_column_windows_hold_every_windowed_entry_once(cheb, graph):
     got = np.sort(r[r >= 0] * (1 << 32) + ids[r >= 0])
     assert np.array_equal(got, want)
     assert int((r < 0).sum()) == int(p["blocks"] * 256 - p["entries"])  # the padding only
+
+
+@pytest.mark.parametrize("graph", ["chung_lu", "rmat"])
+def test_column_windows_hold_every_windowed_entry_once(cheb, graph):
+    """The window stream of a view (forced: 6 windows of 2048 ids on a small graph) holds, piece by
+    piece, exactly the hub rows' entries with ids in [H0, H0 + NW W): every hub row's listed pieces
+    give back the multiset of its windowed ids, pieces never cross a 256-entry block, the per-lane
+    piece counts and block bases agree with the start bits, and the padding belongs to no row."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    e = (Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 20000.0, 900_000, 5) if graph == "chung_lu"
+         else Gen.rmat_edges(16, 16, 0.57, 0.19, 0.19, 3))
+    try:
+        _forced_windows(lib, 6, 2048)
+        dg, info = cheb.build_device_graph(e, cheb.BuildOptions(drop_isolated=True))
+        p = _window_plan(lib, dg)
+        dg.free()
+    finally:
+        _default_windows(lib)
+    assert p["NW"] == 6 and p["W"] == 2048 and p["view"]["n_hub"] > 0
+    _check_window_structure(p)
+
+
+@pytest.mark.parametrize("nw,size,h0", [(1, 256, 0), (3, 65536, 0), (500, 256, 0), (500, 1024, -1), (2, 28672, -1),
+                                        (64, 8192, 0)])
+def test_column_windows_shapes(cheb, nw, size, h0):
+    """Window shapes at the edges: one 256-id window, a requested size above what an fp64 window
+    may take of shared memory (clamped to 28,928 ids), windows past the end of x (the count is clamped; every hub-row id windowed, no
+    chunk tile left), windows from the hot-prefix capacity instead of id 0.  Structure as above,
+    ranks equal to the plain schedule within 1e-12 with the same top-100, solves repeatable."""
+    from paper_2112_01743_b200 import _lib
+    from paper_2112_01743_b200 import generate as Gen
+    lib = _lib.load()
+    e = Gen.chung_lu_edges(1 << 16, 2.1, 2.0, 20000.0, 900_000, 5)
+    try:
+        _forced_windows(lib, 0, 28672)
+        dg, _ = cheb.build_device_graph(e)
+        plain = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10)).ranks
+        dg.free()
+        _forced_windows(lib, nw, size)
+        assert lib.cheb_set_tuning(b"winh0", h0) == 0
+        dg, info = cheb.build_device_graph(e)
+        p = _window_plan(lib, dg)
+        a = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10)).ranks
+        b = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10)).ranks
+        f32 = cheb.run_cpaa(dg, cheb.SolverConfig(eps=1e-10, precision=32)).ranks
+        dg.free()
+    finally:
+        _default_windows(lib)
+        lib.cheb_set_tuning(b"winh0", 0)
+    H0 = 0 if h0 == 0 else p["view"]["H"]
+    size = min(size, 28928)
+    assert p["H0"] == H0 and p["W"] == size
+    assert p["NW"] == min(nw, -(-(info["n"] - H0) // size))     # clamped to the ids there are
+    _check_window_structure(p)
+    if nw == 500:  # the windows reach the end of x: only ids below H0 are left to the term kernel
+        c = p["view"]["col"][:int(p["view"]["rp"][p["view"]["n_hub"]])]
+        assert p["entries"] == int((c >= H0).sum())
+    assert np.array_equal(a, b)
+    assert np.max(np.abs(a - plain)) <= TOL64
+    assert np.array_equal(top_k(a), top_k(plain))
+    assert np.sum(np.abs(f32 - plain)) / np.sum(plain) <= TOL32_L1
 
 
 @pytest.mark.parametrize("graph", ["chung_lu", "rmat"])
