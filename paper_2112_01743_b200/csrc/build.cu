@@ -1902,7 +1902,13 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
     unsigned long long* wide = nullptr;
     char* cub_tmp = nullptr;
     for (int pass = 0; pass < 2; ++pass) {
-        if (pass == 1) sc = Carver{window_scratch(sc.off)};
+        if (pass == 1) {
+            // the build's scratch + the view's arrays (~the same again) must leave the solver room:
+            // otherwise the view keeps the plain schedule
+            size_t free_b = 0, total_b = 0;
+            if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess || 2 * sc.off > free_b / 2) return;
+            sc = Carver{window_scratch(sc.off)};
+        }
         S = sc.take<int>((size_t)n_hub * (NW + 1));
         csz = sc.take<int64_t>((size_t)nq + 1);
         off = sc.take<int64_t>((size_t)nq + 1);
