@@ -901,7 +901,10 @@ __global__ void __launch_bounds__(256) k_hub_finalize(TermArgs<RP, V> a, const i
 // leading sums up to the next start (segmented suffix scan over the lanes, fixed order).  A
 // block's first entry always starts a piece, so no sum crosses blocks.  Piece sums are in
 // fp64; piece k of the stream goes to wpart[k] (consecutive pieces, coalesced stores), and
-// k_hub_finalize adds a row's pieces (klist) to its chunk partials.  Every entry handled here costs one shared-memory load instead of an L2 sector.
+// k_hub_finalize adds a row's pieces (klist) to its chunk partials.  Every entry handled here
+// costs one shared-memory load instead of an L2 sector.  The CTA block ranges (cta[]) are cut at
+// build time by cost (256 + 4 pieces per block): blocks of short pieces store more sums.
+// Reference loop this replaces for these entries: cpaa.cpp:126-132 (the neighbour sum).
 struct WinBlock {
     uint4 ids;
     unsigned m;
@@ -926,7 +929,7 @@ constexpr int kWinAhead = CHEB_WIN_AHEAD;  // blocks of the stream in flight per
 template <class V>
 __global__ void __launch_bounds__(1024, 1)
 k_window_pass(const V* __restrict__ x, int64_t x_len, int H0, int W, int NW, const int64_t* __restrict__ wblk,
-              const uint4* __restrict__ wcol, const unsigned short* __restrict__ flags, const int* __restrict__ bbase,
+              const uint4* __restrict__ wcol, const unsigned short* __restrict__ meta, const int* __restrict__ bbase,
               double* __restrict__ wpart, const int64_t* __restrict__ cta, unsigned long long* stamp_start) {
     extern __shared__ __align__(16) unsigned char smem[];
     V* win = reinterpret_cast<V*>(smem);
@@ -952,7 +955,7 @@ k_window_pass(const V* __restrict__ x, int64_t x_len, int H0, int W, int NW, con
         // this warp's first blocks of the window: issued before the window itself lands
         WinBlock q[kWinAhead];
 #pragma unroll
-        for (int j = 0; j < kWinAhead; ++j) q[j] = win_load(wcol, flags, bbase, b + warp + 32 * j, e, lane);
+        for (int j = 0; j < kWinAhead; ++j) q[j] = win_load(wcol, meta, bbase, b + warp + 32 * j, e, lane);
         __syncthreads();  // the previous window's gathers are done
         const unsigned bytes = (unsigned)(cnt * sizeof(V)) & ~15u;  // base is a multiple of 8 entries: 16-byte aligned
         if (threadIdx.x == 0) {
@@ -970,7 +973,7 @@ k_window_pass(const V* __restrict__ x, int64_t x_len, int H0, int W, int NW, con
             for (int j = 0; j < kWinAhead; ++j) {
                 if (blk + 32 * j >= e) break;
                 const WinBlock cb = q[j];
-                q[j] = win_load(wcol, flags, bbase, blk + 32 * (j + kWinAhead), e, lane);
+                q[j] = win_load(wcol, meta, bbase, blk + 32 * (j + kWinAhead), e, lane);
                 const unsigned idw[4] = {cb.ids.x, cb.ids.y, cb.ids.z, cb.ids.w};
                 double v[8];
 #pragma unroll
