@@ -2242,7 +2242,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     }
     const bool big_x = tuning().sortrows < 0 ? ((int64_t)V.x_len * 8 > (int64_t)l2) : tuning().sortrows > 0;
-    // column windows (single-GPU views) need the hub rows in ascending id order
+    // column windows need the hub rows in ascending id order
     // (partitioned views too: x keeps the global ids on every rank, and a rank's window pass runs
     // behind the term barrier like its term kernel; auto: views of >= 48 M entries, where the
     // extra launch per term is paid back: config 2,
