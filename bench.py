@@ -574,7 +574,10 @@ class Solver:
                 log(f"e2e: push exchange unavailable ({err or 'on a peer rank'}); NCCL all-gather")
                 from paper_2112_01743_b200.distributed import Communicator
                 comm = Communicator(dist.rank, dist.world, device)
-        for _ in range(max(3, warmup)):  # pool, pinned staging and page-cache warm-up
+        # pool, pinned staging and page-cache warm-up: the memory pool can take a few uploads to
+        # settle on a fresh box (cudaMallocAsync of the 4 GB view buffers: 0.2-0.9 s instead of
+        # microseconds, tools/e2e_breakdown.py with CHEB_DEBUG_ALLOC=1)
+        for _ in range(max(5, warmup)):
             step()
         dist.barrier()
         times = []

@@ -1637,51 +1637,54 @@ __global__ void k_win_padflags(const int64_t* __restrict__ wend, int NW, unsigne
 // Entries re-ordered inside their pieces (a piece is a sum: any order) so that the 16 lanes
 // of a half-warp read distinct bank pairs of the fp64 window (id mod 16) in each of the 8
 // gather instructions of a block: position p is read by lane p / 8 in instruction p % 8.
-// Greedy, a thread per block: each position takes, among the next entries of its piece, one
-// whose bank pair the instruction's half-warp has not used yet.
+// Greedy: each position takes, among the next entries of its piece, one whose bank pair the
+// instruction's half-warp has not used yet.
 #ifndef CHEB_WIN_LOOK
 #define CHEB_WIN_LOOK 24
 #endif
 constexpr int kBankLook = CHEB_WIN_LOOK;  // candidates a position may choose from (the next entries of its piece)
-constexpr int kBankThreads = 64, kBankStride = kWinBlock + 2;  // shorts per thread row (129 words: conflict-free)
+// A thread per half block (the half-warps of a gather instruction are independent: positions
+// 0-127 belong to lanes 0-15), candidates never taken from the other half.
+constexpr int kBankBlocks = 64, kBankThreads = 2 * kBankBlocks, kBankHalf = kWinBlock / 2;
+constexpr int kBankStride = kBankHalf + 2;  // shorts per thread row (65 words: conflict-free)
 __global__ void __launch_bounds__(kBankThreads)
 k_win_bank_order(unsigned short* __restrict__ wcol, const unsigned* __restrict__ flags32, int64_t n_blocks) {
     __shared__ unsigned short sh[kBankThreads * kBankStride];
-    for (int64_t b0 = (int64_t)blockIdx.x * kBankThreads; b0 < n_blocks; b0 += (int64_t)gridDim.x * kBankThreads) {
-        const int nb = (int)min((int64_t)kBankThreads, n_blocks - b0);
+    for (int64_t b0 = (int64_t)blockIdx.x * kBankBlocks; b0 < n_blocks; b0 += (int64_t)gridDim.x * kBankBlocks) {
+        const int nb = (int)min((int64_t)kBankBlocks, n_blocks - b0);
         __syncthreads();
-        {  // the CTA's blocks into shared memory, 4 bytes per thread per step
+        {  // the CTA's blocks into shared memory, 4 bytes per thread per step; row = (block, half)
             const unsigned* src = reinterpret_cast<const unsigned*>(wcol + b0 * kWinBlock);
-            for (int i = threadIdx.x; i < nb * (kWinBlock / 2); i += kBankThreads) {
-                const int r = i / (kWinBlock / 2), c = i % (kWinBlock / 2);
+            for (int i = threadIdx.x; i < nb * kBankHalf; i += kBankThreads) {
+                const int r = i / (kBankHalf / 2), c = i % (kBankHalf / 2);
                 *reinterpret_cast<unsigned*>(&sh[r * kBankStride + 2 * c]) = src[i];
             }
         }
         __syncthreads();
-        if ((int)threadIdx.x < nb) {
+        if ((int)threadIdx.x < 2 * nb) {
             unsigned short* ids = sh + threadIdx.x * kBankStride;
-            unsigned fw[kWinBlock / 32];
+            const int half = threadIdx.x & 1;
+            const unsigned* fwp = flags32 + (b0 + (threadIdx.x >> 1)) * (kWinBlock / 32) + half * (kBankHalf / 32);
+            unsigned fw[kBankHalf / 32 + 1];
 #pragma unroll
-            for (int j = 0; j < kWinBlock / 32; ++j) fw[j] = flags32[(b0 + threadIdx.x) * (kWinBlock / 32) + j];
-            unsigned used[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [instruction]: low half-warp bits 0-15, high half-warp 16-31
+            for (int j = 0; j < kBankHalf / 32; ++j) fw[j] = fwp[j];
+            fw[kBankHalf / 32] = half ? 1u : fwp[kBankHalf / 32];  // the next block starts a piece
+            unsigned used[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // [instruction]: bank pairs taken by this half-warp
             int pe = 0;
 #pragma unroll
-            for (int wq = 0; wq < kWinBlock / 32; ++wq) {
-                const unsigned fword = fw[wq];
-                const unsigned fnext = wq + 1 < kWinBlock / 32 ? fw[wq + 1] : 1u;  // the next block starts a piece
+            for (int wq = 0; wq < kBankHalf / 32; ++wq) {
+                const unsigned fword = fw[wq], fnext = fw[wq + 1];
                 for (int p4 = 0; p4 < 4; ++p4) {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int p = wq * 32 + p4 * 8 + i;
+                        const int p = wq * 32 + p4 * 8 + i;  // position inside the half
                         if (p >= pe) {  // end of the piece holding p: next start bit, at most kBankLook positions on
                             const int q = p4 * 8 + i + 1;  // in-word bit of p + 1
                             const unsigned long long bits = ((unsigned long long)fnext << 32 | fword) >> q;
                             const int d = bits ? __ffsll((long long)bits) - 1 : 64;
-                            pe = min(p + 1 + d, p + kBankLook);
-                            pe = min(pe, kWinBlock);  // (start bits are looked up 64 positions ahead at most)
+                            pe = min(min(p + 1 + d, p + kBankLook), kBankHalf);
                         }
-                        const int shf = (p >> 7) << 4;
-                        const unsigned mask = used[i] >> shf;
+                        const unsigned mask = used[i];
                         int pick = p;
                         for (int j = p; j < pe; ++j)
                             if (!((mask >> (ids[j] & 15)) & 1u)) {
@@ -1691,7 +1694,7 @@ k_win_bank_order(unsigned short* __restrict__ wcol, const unsigned* __restrict__
                         const unsigned short v = ids[pick];
                         ids[pick] = ids[p];
                         ids[p] = v;
-                        used[i] |= 1u << (shf + (v & 15));
+                        used[i] |= 1u << (v & 15);
                     }
                 }
             }
@@ -1699,8 +1702,8 @@ k_win_bank_order(unsigned short* __restrict__ wcol, const unsigned* __restrict__
         __syncthreads();
         {
             unsigned* dst = reinterpret_cast<unsigned*>(wcol + b0 * kWinBlock);
-            for (int i = threadIdx.x; i < nb * (kWinBlock / 2); i += kBankThreads) {
-                const int r = i / (kWinBlock / 2), c = i % (kWinBlock / 2);
+            for (int i = threadIdx.x; i < nb * kBankHalf; i += kBankThreads) {
+                const int r = i / (kBankHalf / 2), c = i % (kBankHalf / 2);
                 dst[i] = *reinterpret_cast<const unsigned*>(&sh[r * kBankStride + 2 * c]);
             }
         }
@@ -1989,7 +1992,7 @@ static void window_schedule(SolverView& V, int NW_req, int W, cudaStream_t st) {
         dbg_mark("    windows: stream copied");
     }
     if (tuning().winbank)
-        k_win_bank_order<<<(int)std::min<int64_t>((n_blocks + kBankThreads - 1) / kBankThreads, 148 * 32), kBankThreads, 0, st>>>(
+        k_win_bank_order<<<(int)std::min<int64_t>((n_blocks + kBankBlocks - 1) / kBankBlocks, 148 * 32), kBankThreads, 0, st>>>(
             Wn.wcol.ptr<unsigned short>(), flags32, n_blocks);
     if (dbg_on()) {
         CHEB_CUDA_CHECK(cudaStreamSynchronize(st));
