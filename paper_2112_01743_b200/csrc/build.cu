@@ -1858,11 +1858,11 @@ __global__ void k_win_prog_pack(const Tile* __restrict__ tiles, int old_chunks, 
 
 // Scratch of the window build: one grow-only cudaMalloc'ed block per device, reused by every
 // upload (callers hold pinned_arena().mu), so the temporaries never touch the memory pool.
-static char* window_scratch(size_t bytes) {
-    static std::map<int, DevMem> cache;
+static char* window_scratch(size_t bytes, int slot = 0) {
+    static std::map<std::pair<int, int>, DevMem> cache;
     int dev = 0;
     CHEB_CUDA_CHECK(cudaGetDevice(&dev));
-    DevMem& d = cache[dev];
+    DevMem& d = cache[{dev, slot}];
     if (d.bytes() < bytes) {
         AllocScope plain(nullptr);
         d.alloc(bytes + bytes / 8);
@@ -2273,9 +2273,17 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
         }
         const int* order_l = V.order.ptr<int>() + lo;
         const RPN* rp_l = V.row_ptr.ptr<RPN>();
-        DevMem perm;  // permute target when the rows are sorted afterwards (sorted into V.col)
-        if (sort_grouped) perm.alloc(sizeof(int) * (size_t)nnz_l + 64);
-        int* dst = sort_grouped ? perm.ptr<int>() : V.col.ptr<int>();
+        // permute target when the rows are sorted afterwards (sorted into V.col), and the
+        // segmented sort's scratch: from the build's grow-only blocks (the staging lock is held
+        // and the build ends synchronised), not two more 4 GB pool allocations per upload
+        int* perm = sort_grouped && tuning().bigscratch
+                        ? reinterpret_cast<int*>(window_scratch(sizeof(int) * (size_t)nnz_l + 64, 1)) : nullptr;
+        DevMem perm_pool;
+        if (sort_grouped && !perm) {
+            perm_pool.alloc(sizeof(int) * (size_t)nnz_l + 64);
+            perm = perm_pool.ptr<int>();
+        }
+        int* dst = sort_grouped ? perm : V.col.ptr<int>();
         const int K = groups ? (int)groups->row_cut.size() - 1 : 1;
         DevMem seg_b, seg_e, seg_n(sizeof(unsigned long long));
         TempStore sort_tmp;
@@ -2313,7 +2321,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
             if (K == 1) {
                 CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, dst, V.col.ptr<int>(), (int)nnz_l,
                                                                    (int)nl, rp_l, rp_l + 1, st));
-                void* t = sort_tmp.get(bytes);
+                void* t = tuning().bigscratch ? (void*)window_scratch(bytes, 2) : sort_tmp.get(bytes);
                 CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, dst, V.col.ptr<int>(), (int)nnz_l,
                                                                    (int)nl, rp_l, rp_l + 1, st));
             } else {
@@ -2326,7 +2334,7 @@ static void build_view_t(cheb_graph* g, cudaStream_t st, const std::function<voi
                 if (nseg == 0) continue;
                 CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, dst, V.col.ptr<int>(), (int)nnz_l,
                                                                    (int)nseg, seg_b.ptr<int64_t>(), seg_e.ptr<int64_t>(), st));
-                void* t = sort_tmp.get(bytes);
+                void* t = tuning().bigscratch ? (void*)window_scratch(bytes, 2) : sort_tmp.get(bytes);
                 CHEB_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(t, bytes, dst, V.col.ptr<int>(), (int)nnz_l,
                                                                    (int)nseg, seg_b.ptr<int64_t>(), seg_e.ptr<int64_t>(), st));
             }

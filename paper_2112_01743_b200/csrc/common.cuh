@@ -532,6 +532,8 @@ struct Tuning {
     int winpw = 4;      // window pass CTA ranges: cost of a block = 256 + winpw * its pieces
     int winh0 = 0;      // first windowed id (0: the hub rows keep only ids past the last window; config 4 99.5 -> 94.3 ms per
                         // solve, config 3 11.58 -> 10.91); -1 = the fp64 hot-prefix capacity (the term kernel keeps ids below it)
+    int bigscratch = 1; // view build: the permute target and the segmented sort's scratch (4 GB each on config 4) from
+                        // per-device grow-only blocks instead of the memory pool
     int winskip = 0;    // timing experiments: 1 no window pass, 2 no term kernel, 3 no hub finalize (wrong results);
                         // bits: 4 window pass launched without PDL, 8 term kernel behind it WITH PDL, 16 hub finalize without
     int winsize = 28672; // entries of x per window (clamped to kWinMaxIds; 16-bit local ids; fp64 224 KB of shared memory; C4 24576 -> 28672: 94.1 -> 92.9 ms)
@@ -569,6 +571,7 @@ inline Tuning& tuning() {
         if (const char* e = std::getenv("CHEB_TUNE_WINBANK")) x.winbank = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_WINPW")) x.winpw = std::atoi(e);
         if (const char* e = std::getenv("CHEB_TUNE_WINH0")) x.winh0 = std::atoi(e);
+        if (const char* e = std::getenv("CHEB_TUNE_BIGSCRATCH")) x.bigscratch = std::atoi(e);
         return x;
     }();
     return t;
